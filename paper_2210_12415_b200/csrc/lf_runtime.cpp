@@ -1,0 +1,949 @@
+// lf_runtime.cpp — device context, whole-graph plans and the C-ABI.
+//
+// A plan is the GPU lowering of one (Graph, SeqMap, schedules) triple: the
+// reference's lower() (proj/src/lower.cpp:545-610) emits one loop nest per
+// node in topological order and interpret() runs it after materializing
+// inputs (interp.cpp:424-470). Here every node becomes one kernel launch on
+// physical-layout device buffers:
+//   Padding / LayoutConvert -> digit_copy (K2/K1) or ix_copy
+//   C2D / GMM               -> tcgen05 kernels (K4/K3) when the layouts are
+//                              tensor-core legal, else gen_contract
+//   DEP                     -> gen_contract
+//   ReLU / BiasAdd / EwAdd  -> fused into the tcgen05 epilogue when the
+//                              schedule asks for it, else gen_eltwise
+// and measure() replaces simulate_cache (cachesim.cpp:152-174) at the
+// tuner's seam (tuner.cpp:178).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "lf_core.hpp"
+#include "lf_generic.hpp"
+#include "lf_kernels.hpp"
+#include "lf_umma.hpp"
+
+using namespace lfg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_OK(expr)                                                               \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      fail(LFGPU_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+std::vector<Dim> dims_of(int rank, const lfgpu_dim* d) {
+  std::vector<Dim> out;
+  for (int i = 0; i < rank; ++i) out.push_back({std::string(d[i].name), d[i].extent});
+  return out;
+}
+
+Seq seq_of(int n, const lfgpu_prim* p) { return Seq(p, p + n); }
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return LFGPU_OK;
+  } catch (const Error& e) {
+    return set_error(e.code, e.what());
+  } catch (const std::exception& e) {
+    return set_error(LFGPU_EINVAL, e.what());
+  }
+}
+
+}  // namespace
+
+namespace lfg {
+int set_error_external(int code, const std::string& msg) { return set_error(code, msg); }
+}  // namespace lfg
+
+// ---------------------------------------------------------------------------
+// context
+
+struct lfgpu_ctx {
+  int device = 0;
+  int* d_err = nullptr;
+  int64_t launches = 0;
+  void* flush = nullptr;  // > L2 buffer for cache flushing between timings
+  size_t flush_bytes = 0;
+};
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  explicit DevBuf(size_t bytes) {
+    if (bytes) CUDA_OK(cudaMalloc(&p, bytes));
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// Upload a POD value / vector into a device buffer kept alive by `keep`.
+template <typename T>
+T* upload(std::vector<std::unique_ptr<DevBuf>>& keep, const T* host, size_t count) {
+  keep.push_back(std::make_unique<DevBuf>(sizeof(T) * std::max<size_t>(count, 1)));
+  CUDA_OK(cudaMemcpy(keep.back()->p, host, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return static_cast<T*>(keep.back()->p);
+}
+
+// One conversion (K1/K2) compiled for launch.
+struct CopyKernel {
+  bool digit = false;
+  DigitMap map;
+  IxProgram* d_progs = nullptr;
+  int64_t n = 0;
+  int src_elem = 0, dst_elem = 0;
+  const char* name = "";
+};
+
+CopyKernel compile_copy(const CopySpec& spec, int se, int de,
+                        std::vector<std::unique_ptr<DevBuf>>& keep, bool* oob) {
+  CopyKernel k;
+  k.src_elem = se;
+  k.dst_elem = de;
+  k.n = numel(derive(spec.lmap.dst_logical, spec.dst_seq));
+  *oob = false;
+  if (compile_digit_map(spec, &k.map, oob)) {
+    k.digit = true;
+    return k;
+  }
+  IxProgram progs[2];
+  compile_ix_programs(spec, &progs[0], &progs[1]);
+  k.d_progs = upload(keep, progs, 2);
+  k.name = "ix_copy";
+  return k;
+}
+
+cudaError_t run_copy(const CopyKernel& k, const void* src, void* dst, int* d_err,
+                     cudaStream_t s) {
+  KernelInfo info;
+  if (k.digit) return launch_digit_copy(k.map, k.src_elem, k.dst_elem, src, dst, s, &info);
+  return launch_ix_copy(k.d_progs, k.n, k.src_elem, k.dst_elem, src, dst, d_err, s, &info);
+}
+
+const char* copy_name(const CopyKernel& k) {
+  if (!k.digit) return "ix_copy";
+  // Mirrors make_params()'s choice in k_copy.cu.
+  int a = k.map.ndig - 1;
+  bool transpose = false;
+  if (k.map.ndig >= 2 && k.map.src_stride[a] != 1)
+    for (int d = 0; d < k.map.ndig - 1; ++d)
+      if (k.map.src_stride[d] == 1) transpose = true;
+  return transpose ? "digit_copy_transpose" : "digit_copy_direct";
+}
+
+LogicalMap identity_map(const std::vector<Dim>& logical) {
+  LogicalMap m;
+  m.dst_logical = logical;
+  m.src_logical = logical;
+  return m;
+}
+
+LogicalMap padding_map(const std::vector<Dim>& in, int64_t pad) {
+  LogicalMap m;
+  m.src_logical = in;
+  m.dst_logical = in;
+  m.dst_logical[2].extent += 2 * pad;
+  m.dst_logical[3].extent += 2 * pad;
+  m.shift = {0, 0, -pad, -pad};
+  m.lo = {0, 0, pad, pad};
+  m.hi = {in[0].extent, in[1].extent, pad + in[2].extent, pad + in[3].extent};
+  m.has_guard = true;
+  return m;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plans
+
+struct PTensor {
+  std::string id;
+  int dtype = LFGPU_DTYPE_F32;
+  int role = LFGPU_ROLE_INTERMEDIATE;
+  std::vector<Dim> logical, phys;
+  Seq seq;
+  int elem = LFGPU_ELEM_F32;  // primary storage
+  void* d = nullptr;
+  void* d_bf16 = nullptr;     // tensor-core operand shadow (same layout)
+  int64_t numel = 0;
+  int producer = -1;
+  std::vector<int> consumers;
+  bool need_f32 = false, need_bf16 = false;
+  bool valid = true;  // false: fused away, never materialized
+};
+
+struct PStep {
+  int node = -1;
+  std::string kernel;
+  std::function<cudaError_t(cudaStream_t)> run;
+};
+
+struct lfgpu_plan {
+  lfgpu_ctx* ctx = nullptr;
+  int flags = 0;
+  std::vector<PTensor> t;
+  std::vector<lfgpu_node> nodes;
+  std::vector<PStep> steps;
+  std::vector<std::string> node_kernel;
+  std::map<int, std::string> summary;
+  std::vector<std::unique_ptr<DevBuf>> keep;
+  cudaStream_t stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t bytes = 0, flops = 0, tc_nodes = 0;
+  std::vector<int> order;
+
+  ~lfgpu_plan() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    keep.clear();
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+std::vector<int> topo(const std::vector<lfgpu_node>& nodes, const std::vector<PTensor>& t) {
+  // Kahn with insertion-order ties (ir.cpp:266-295).
+  int n = static_cast<int>(nodes.size());
+  std::vector<int> indeg(n, 0);
+  std::vector<std::vector<int>> succ(n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < nodes[i].ninputs; ++j) {
+      int p = t[nodes[i].inputs[j]].producer;
+      if (p >= 0 && p != i) {
+        succ[p].push_back(i);
+        ++indeg[i];
+      }
+    }
+  std::set<int> ready;
+  for (int i = 0; i < n; ++i)
+    if (!indeg[i]) ready.insert(i);
+  std::vector<int> order;
+  while (!ready.empty()) {
+    int i = *ready.begin();
+    ready.erase(ready.begin());
+    order.push_back(i);
+    for (int s : succ[i])
+      if (--indeg[s] == 0) ready.insert(s);
+  }
+  if (static_cast<int>(order.size()) != n) fail(LFGPU_EINVAL, "topo_order: graph has a cycle");
+  return order;
+}
+
+int64_t* tables_for(lfgpu_plan* P, const PTensor& t, std::vector<int64_t>* off) {
+  std::vector<int64_t> tab;
+  if (!separable_tables(t.logical, t.seq, &tab, off))
+    fail(LFGPU_EUNSUPPORTED, "layout of '" + t.id + "' is not separable per logical dim: " +
+                                 seq_str(t.seq));
+  return upload(P->keep, tab.data(), tab.size());
+}
+
+IxProgram* out_program(lfgpu_plan* P, const PTensor& t) {
+  CopySpec spec;
+  spec.lmap = identity_map(t.logical);
+  spec.dst_seq = t.seq;
+  spec.mode = FoldMode::Nest;
+  IxProgram progs[2];
+  compile_ix_programs(spec, &progs[0], &progs[1]);
+  return upload(P->keep, &progs[0], 1);
+}
+
+int storage_elem(const PTensor& t) {
+  return t.dtype == LFGPU_DTYPE_I32 ? LFGPU_ELEM_I32 : LFGPU_ELEM_F32;
+}
+
+void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sched* sched) {
+  if (!g || g->ntensors <= 0) fail(LFGPU_EINVAL, "empty graph");
+  P->t.resize(g->ntensors);
+  for (int i = 0; i < g->ntensors; ++i) {
+    const lfgpu_tensor& td = g->tensors[i];
+    PTensor& t = P->t[i];
+    t.id = td.id;
+    t.dtype = td.dtype;
+    t.role = td.role;
+    t.logical = dims_of(td.rank, td.dims);
+    for (const auto& d : t.logical)
+      if (d.extent < 1) fail(LFGPU_EINVAL, "tensor '" + t.id + "' has an extent < 1");
+  }
+  for (int s = 0; s < g->nseqs; ++s) {
+    const lfgpu_seq& sq = g->seqs[s];
+    if (sq.tensor < 0 || sq.tensor >= g->ntensors) fail(LFGPU_EINVAL, "seq names no tensor");
+    P->t[sq.tensor].seq = seq_of(sq.nprims, sq.prims);
+    for (const auto& p : P->t[sq.tensor].seq)
+      if (p.kind == LFGPU_PRIM_STORE_AT || p.kind == LFGPU_PRIM_DECOUPLE_AT)
+        fail(LFGPU_EUNSUPPORTED, "store_at layouts are not supported by the GPU plan yet");
+  }
+  for (auto& t : P->t) {
+    try {
+      t.phys = derive(t.logical, t.seq);
+    } catch (const Error& e) {
+      fail(e.code, "tensor '" + t.id + "': " + e.what());
+    }
+    t.numel = numel(t.phys);
+    t.elem = storage_elem(t);
+  }
+  P->nodes.assign(g->nodes, g->nodes + g->nnodes);
+  for (int i = 0; i < g->nnodes; ++i) {
+    const auto& n = P->nodes[i];
+    if (n.output < 0 || n.output >= g->ntensors) fail(LFGPU_EINVAL, "node output out of range");
+    if (P->t[n.output].producer >= 0) fail(LFGPU_EINVAL, "tensor produced twice");
+    P->t[n.output].producer = i;
+    for (int j = 0; j < n.ninputs; ++j) {
+      if (n.inputs[j] < 0 || n.inputs[j] >= g->ntensors) fail(LFGPU_EINVAL, "input out of range");
+      P->t[n.inputs[j]].consumers.push_back(i);
+    }
+  }
+  P->order = topo(P->nodes, P->t);
+  P->node_kernel.assign(P->nodes.size(), "");
+
+  std::map<int, lfgpu_sched> sched_of;
+  for (int i = 0; i < nsched; ++i) sched_of[sched[i].node] = sched[i];
+  const bool exact = P->flags & LFGPU_PLAN_EXACT;
+
+  // 1. Tensor-core eligibility per contraction and fusion chains.
+  std::map<int, UmmaPlan> umma;
+  std::set<int> fused_away;  // element-wise nodes absorbed into an epilogue
+  for (int ni : P->order) {
+    const auto& n = P->nodes[ni];
+    if (n.kind != LFGPU_OP_C2D && n.kind != LFGPU_OP_GMM) continue;
+    if (exact || P->t[n.output].dtype != LFGPU_DTYPE_F32) continue;
+    UmmaPlan up;
+    std::string why;
+    const PTensor& A = P->t[n.inputs[0]];
+    const PTensor& B = P->t[n.inputs[1]];
+    const PTensor& Cc = P->t[n.output];
+    lfgpu_sched s{};
+    s.node = ni;
+    if (sched_of.count(ni)) s = sched_of[ni];
+    bool ok = n.kind == LFGPU_OP_GMM
+                  ? umma_plan_gemm(A.logical, A.seq, B.logical, B.seq, Cc.logical, Cc.seq, s,
+                                   &up, &why)
+                  : umma_plan_conv(A.logical, A.seq, B.logical, B.seq, Cc.logical, Cc.seq,
+                                   n.stride, s, &up, &why);
+    if (!ok) {
+      if (P->flags & LFGPU_PLAN_REQUIRE_TC)
+        fail(LFGPU_EUNSUPPORTED, "node " + std::to_string(ni) + " not tensor-core legal: " + why);
+      continue;
+    }
+    // Epilogue fusion of the single-consumer element-wise chain (lower.cpp:566-608)
+    // when every member keeps the output's physical layout.
+    if (s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL)) {
+      int cur = n.output;
+      while (true) {
+        const auto& cons = P->t[cur].consumers;
+        if (cons.size() != 1) break;
+        const auto& c = P->nodes[cons[0]];
+        if (c.kind != LFGPU_OP_RELU && c.kind != LFGPU_OP_BIASADD && c.kind != LFGPU_OP_EWADD)
+          break;
+        if (c.inputs[0] != cur) break;
+        if (!seq_equal(P->t[c.output].seq, Cc.seq)) break;
+        if (c.kind == LFGPU_OP_EWADD && !seq_equal(P->t[c.inputs[1]].seq, Cc.seq)) break;
+        if (c.kind == LFGPU_OP_BIASADD && !P->t[c.inputs[1]].seq.empty()) break;
+        if (up.epi_count >= kMaxEpi) break;
+        if (c.kind == LFGPU_OP_RELU && up.epi_count > 0 &&
+            up.epi[up.epi_count - 1].kind == EPI_RELU)
+          break;
+        up.epi[up.epi_count].kind = c.kind == LFGPU_OP_RELU    ? EPI_RELU
+                                    : c.kind == LFGPU_OP_BIASADD ? EPI_BIAS
+                                                                 : EPI_RESIDUAL;
+        up.epi[up.epi_count].tensor = c.kind == LFGPU_OP_RELU ? -1 : c.inputs[1];
+        up.epi[up.epi_count].out_tensor = c.output;
+        ++up.epi_count;
+        fused_away.insert(cons[0]);
+        cur = c.output;
+      }
+    }
+    umma[ni] = up;
+  }
+
+  // 2. Storage decisions: bf16 for tensor-core operands, f32/i32 otherwise.
+  for (auto& t : P->t) {
+    for (int c : t.consumers) {
+      bool tc_operand = umma.count(c) && (P->nodes[c].inputs[0] == &t - &P->t[0] ||
+                                          P->nodes[c].inputs[1] == &t - &P->t[0]);
+      // A tensor read only as an epilogue residual/bias stays fp32.
+      if (tc_operand) t.need_bf16 = true;
+      else t.need_f32 = true;
+    }
+    if (t.producer >= 0 || t.role == LFGPU_ROLE_OUTPUT) t.need_f32 = true;
+    if (t.consumers.empty()) t.need_f32 = true;
+    // A Padding / LayoutConvert output feeding only tensor cores is written in
+    // bf16 directly: the conversion absorbed into the producer.
+    if (t.producer >= 0 && t.need_bf16) {
+      const auto& pn = P->nodes[t.producer];
+      bool all_tc = true;
+      for (int c : t.consumers)
+        if (!umma.count(c)) all_tc = false;
+      if ((pn.kind == LFGPU_OP_PADDING || pn.kind == LFGPU_OP_LAYOUT_CONVERT) && all_tc)
+        t.need_f32 = false;
+    }
+  }
+  for (auto& t : P->t) {
+    size_t es = elem_size(t.elem);
+    if (t.need_f32 || !t.need_bf16) {
+      P->keep.push_back(std::make_unique<DevBuf>(es * t.numel));
+      t.d = P->keep.back()->p;
+    }
+    if (t.need_bf16) {
+      P->keep.push_back(std::make_unique<DevBuf>(2 * t.numel));
+      t.d_bf16 = P->keep.back()->p;
+    }
+    if (!t.d) t.elem = LFGPU_ELEM_BF16;  // bf16-only storage
+  }
+  int* d_err = P->ctx->d_err;
+
+  // 3. One step per node.
+  for (int ni : P->order) {
+    if (fused_away.count(ni)) {
+      P->node_kernel[ni] = "fused";
+      continue;
+    }
+    const auto& n = P->nodes[ni];
+    PTensor& out = P->t[n.output];
+    PStep step;
+    step.node = ni;
+    switch (n.kind) {
+      case LFGPU_OP_PADDING:
+      case LFGPU_OP_LAYOUT_CONVERT: {
+        const PTensor& in = P->t[n.inputs[0]];
+        CopySpec spec;
+        if (n.kind == LFGPU_OP_PADDING) {
+          if (in.logical.size() != 4) fail(LFGPU_EINVAL, "Padding input must be rank 4");
+          spec.lmap = padding_map(in.logical, n.pad);
+        } else {
+          spec.lmap = identity_map(in.logical);
+        }
+        spec.dst_seq = out.seq;
+        spec.src_seq = in.seq;
+        spec.mode = FoldMode::Nest;
+        bool oob = false;
+        int se = in.d ? in.elem : LFGPU_ELEM_BF16;
+        const void* src = in.d ? in.d : in.d_bf16;
+        // Write the primary buffer, and the bf16 shadow in the same pass when
+        // this is the only consumer-facing copy.
+        int de = out.d ? out.elem : LFGPU_ELEM_BF16;
+        void* dst = out.d ? out.d : out.d_bf16;
+        CopyKernel k = compile_copy(spec, se, de, P->keep, &oob);
+        if (oob)
+          fail(LFGPU_ERANGE, std::string("out-of-range access: ") +
+                                 (n.kind == LFGPU_OP_PADDING ? "Padding" : "LayoutConvert") +
+                                 " into '" + out.id + "' reads outside '" + in.id + "'");
+        step.kernel = copy_name(k);
+        step.run = [k, src, dst, d_err](cudaStream_t s) { return run_copy(k, src, dst, d_err, s); };
+        P->bytes += in.numel * elem_size(se) + out.numel * elem_size(de);
+        break;
+      }
+      case LFGPU_OP_RELU:
+      case LFGPU_OP_BIASADD:
+      case LFGPU_OP_EWADD: {
+        GenEltwise G;
+        G.op = n.kind == LFGPU_OP_RELU ? GEN_RELU : n.kind == LFGPU_OP_BIASADD ? GEN_BIASADD : GEN_EWADD;
+        G.rank = static_cast<int32_t>(out.logical.size());
+        G.n = out.numel;
+        const PTensor& x = P->t[n.inputs[0]];
+        if (!x.d) fail(LFGPU_EUNSUPPORTED, "element-wise read of a bf16-only tensor");
+        std::vector<int64_t> off;
+        G.tab0 = tables_for(P, x, &off);
+        for (size_t j = 0; j < off.size(); ++j) G.tab_off[j] = off[j];
+        G.in0 = x.d;
+        if (n.kind != LFGPU_OP_RELU) {
+          const PTensor& y = P->t[n.inputs[1]];
+          std::vector<int64_t> off1;
+          G.tab1 = tables_for(P, y, &off1);
+          G.in1 = y.d;
+          if (n.kind == LFGPU_OP_EWADD)
+            for (size_t j = 0; j < off1.size(); ++j)
+              if (off1[j] != off[j]) fail(LFGPU_EINVAL, "EwAdd operands differ in shape");
+          G.bias_dim = out.logical.size() == 4 ? 1 : static_cast<int32_t>(out.logical.size()) - 1;
+          P->bytes += y.numel * elem_size(y.elem);
+        }
+        IxProgram* prog = out_program(P, out);
+        int elem = out.elem;
+        void* dst = out.d;
+        step.kernel = "gen_eltwise";
+        step.run = [prog, G, elem, dst, d_err](cudaStream_t s) {
+          return launch_gen_eltwise(prog, G, elem, dst, d_err, s);
+        };
+        P->bytes += x.numel * elem_size(x.elem) + out.numel * elem_size(out.elem);
+        break;
+      }
+      case LFGPU_OP_C2D:
+      case LFGPU_OP_GMM:
+      case LFGPU_OP_DEP: {
+        const PTensor& A = P->t[n.inputs[0]];
+        const PTensor& B = P->t[n.inputs[1]];
+        int64_t macs = 0;
+        if (n.kind == LFGPU_OP_GMM) macs = out.logical[0].extent * out.logical[1].extent * A.logical[1].extent;
+        else if (n.kind == LFGPU_OP_C2D)
+          macs = numel(out.logical) * B.logical[1].extent * B.logical[2].extent * B.logical[3].extent;
+        else
+          macs = numel(out.logical) * B.logical[1].extent * B.logical[2].extent;
+        P->flops += 2 * macs;
+        auto it = umma.find(ni);
+        if (it != umma.end()) {
+          UmmaPlan up = it->second;
+          up.a = A.d_bf16;
+          up.b = B.d_bf16;
+          // The chain's final output is the one written; intermediates of a
+          // fused chain are also written when the caller keeps them.
+          int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : n.output;
+          up.out = static_cast<float*>(P->t[final_t].d);
+          for (int e = 0; e < up.epi_count; ++e) {
+            if (up.epi[e].tensor >= 0) {
+              const PTensor& et = P->t[up.epi[e].tensor];
+              if (!et.d) fail(LFGPU_EUNSUPPORTED, "epilogue operand has no fp32 buffer");
+              up.epi[e].ptr = static_cast<const float*>(et.d);
+            }
+          }
+          // Intermediate tensors of a fused chain are never written.
+          for (int e = 0; e + 1 < up.epi_count; ++e) P->t[up.epi[e].out_tensor].valid = false;
+          if (up.epi_count) out.valid = false;
+          UmmaLaunch L = umma_prepare(up);
+          step.kernel = up.kind == UMMA_CONV ? "umma_conv" : "umma_gemm";
+          step.run = [L](cudaStream_t s) { return umma_launch(L, s); };
+          P->tc_nodes += 1;
+          P->bytes += A.numel * 2 + B.numel * 2 + P->t[final_t].numel * 4;
+          P->summary[ni] = up.summary;
+        } else {
+          GenContract G;
+          G.op = n.kind == LFGPU_OP_GMM ? GEN_GMM : n.kind == LFGPU_OP_C2D ? GEN_C2D : GEN_DEP;
+          G.n = out.numel;
+          G.V = n.stride;
+          if (n.kind == LFGPU_OP_GMM) {
+            G.K = A.logical[1].extent;
+          } else if (n.kind == LFGPU_OP_C2D) {
+            G.I = B.logical[1].extent;
+            G.KH = B.logical[2].extent;
+            G.KW = B.logical[3].extent;
+          } else {
+            G.KH = B.logical[1].extent;
+            G.KW = B.logical[2].extent;
+          }
+          if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "CUDA-core contraction on bf16-only operand");
+          std::vector<int64_t> oa, ob;
+          G.ta = tables_for(P, A, &oa);
+          G.tb = tables_for(P, B, &ob);
+          for (size_t j = 0; j < oa.size(); ++j) G.a_off[j] = oa[j];
+          for (size_t j = 0; j < ob.size(); ++j) G.b_off[j] = ob[j];
+          G.a = A.d;
+          G.b = B.d;
+          IxProgram* prog = out_program(P, out);
+          int elem = out.elem;
+          void* dst = out.d;
+          step.kernel = "gen_contract";
+          step.run = [prog, G, elem, exact, dst](cudaStream_t s) {
+            return launch_gen_contract(prog, G, elem, exact, dst, s);
+          };
+          P->bytes += A.numel * elem_size(A.elem) + B.numel * elem_size(B.elem) +
+                      out.numel * elem_size(out.elem);
+        }
+        break;
+      }
+      default:
+        fail(LFGPU_EINVAL, "unknown operator kind " + std::to_string(n.kind));
+    }
+    P->node_kernel[ni] = step.kernel;
+    P->steps.push_back(std::move(step));
+    // Mixed consumers: refresh the bf16 shadow right after the producer.
+    if (out.d && out.d_bf16) {
+      CopySpec spec;
+      spec.lmap = identity_map(out.logical);
+      spec.dst_seq = out.seq;
+      spec.src_seq = out.seq;
+      bool oob;
+      CopyKernel k = compile_copy(spec, out.elem, LFGPU_ELEM_BF16, P->keep, &oob);
+      const void* src = out.d;
+      void* dst = out.d_bf16;
+      PStep sh;
+      sh.node = ni;
+      sh.kernel = "bf16_shadow";
+      sh.run = [k, src, dst, d_err](cudaStream_t s) { return run_copy(k, src, dst, d_err, s); };
+      P->steps.push_back(std::move(sh));
+    }
+  }
+}
+
+void plan_run_steps(lfgpu_plan* P) {
+  if ((P->flags & LFGPU_PLAN_CUDA_GRAPH) && !P->steps.empty()) {
+    if (!P->gexec) {
+      CUDA_OK(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
+      for (auto& s : P->steps) {
+        cudaError_t e = s.run(P->stream);
+        if (e != cudaSuccess) {
+          cudaGraph_t g;
+          cudaStreamEndCapture(P->stream, &g);
+          if (g) cudaGraphDestroy(g);
+          fail(LFGPU_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
+        }
+      }
+      CUDA_OK(cudaStreamEndCapture(P->stream, &P->graph));
+      CUDA_OK(cudaGraphInstantiate(&P->gexec, P->graph, 0));
+    }
+    CUDA_OK(cudaGraphLaunch(P->gexec, P->stream));
+  } else {
+    for (auto& s : P->steps) {
+      cudaError_t e = s.run(P->stream);
+      if (e != cudaSuccess)
+        fail(LFGPU_ECUDA, "kernel " + s.kernel + " (node " + std::to_string(s.node) +
+                              "): " + cudaGetErrorString(e));
+    }
+  }
+  P->ctx->launches += static_cast<int64_t>(P->steps.size());
+}
+
+void check_device_error(lfgpu_plan* P) {
+  int h = 0;
+  CUDA_OK(cudaMemcpyAsync(&h, P->ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
+  CUDA_OK(cudaStreamSynchronize(P->stream));
+  if (h) {
+    CUDA_OK(cudaMemsetAsync(P->ctx->d_err, 0, sizeof(int), P->stream));
+    fail(LFGPU_ERANGE, "out-of-range access during execution");
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+
+extern "C" {
+
+int lfgpu_version(void) { return 1; }
+
+const char* lfgpu_last_error(void) { return g_last_error.c_str(); }
+
+int lfgpu_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) n = 0;
+  *count = n;
+  return LFGPU_OK;
+}
+
+int lfgpu_derive_layout(int32_t rank, const lfgpu_dim* dims, int32_t nprims,
+                        const lfgpu_prim* prims, int32_t* out_rank, lfgpu_dim* out_dims) {
+  return guarded([&] {
+    auto d = derive(dims_of(rank, dims), seq_of(nprims, prims));
+    *out_rank = static_cast<int32_t>(d.size());
+    for (size_t i = 0; i < d.size(); ++i) {
+      std::memset(out_dims[i].name, 0, LFGPU_NAME_LEN);
+      std::strncpy(out_dims[i].name, d[i].name.c_str(), LFGPU_NAME_LEN - 1);
+      out_dims[i].extent = d[i].extent;
+    }
+  });
+}
+
+int lfgpu_convert_kind(int32_t rank, const lfgpu_dim* logical, int32_t nsrc,
+                       const lfgpu_prim* src_seq, int32_t ndst, const lfgpu_prim* dst_seq,
+                       int32_t* kind) {
+  return guarded([&] {
+    CopySpec spec;
+    spec.lmap = identity_map(dims_of(rank, logical));
+    spec.src_seq = seq_of(nsrc, src_seq);
+    spec.dst_seq = seq_of(ndst, dst_seq);
+    DigitMap m;
+    bool oob;
+    *kind = compile_digit_map(spec, &m, &oob) ? 1 : 0;
+  });
+}
+
+int lfgpu_ctx_create(int device, lfgpu_ctx** out) {
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      fail(LFGPU_ECUDA, "no CUDA device available");
+    CUDA_OK(cudaSetDevice(device));
+    auto* c = new lfgpu_ctx;
+    c->device = device;
+    cudaError_t e = cudaMalloc(&c->d_err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, sizeof(int));
+    if (e != cudaSuccess) {
+      delete c;
+      fail(LFGPU_ECUDA, cudaGetErrorString(e));
+    }
+    *out = c;
+  });
+}
+
+int lfgpu_ctx_destroy(lfgpu_ctx* ctx) {
+  if (!ctx) return LFGPU_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->flush) cudaFree(ctx->flush);
+  delete ctx;
+  return LFGPU_OK;
+}
+
+int lfgpu_ctx_launch_count(lfgpu_ctx* ctx, int64_t* count) {
+  *count = ctx ? ctx->launches : 0;
+  return LFGPU_OK;
+}
+
+int lfgpu_layout_convert(lfgpu_ctx* ctx, int32_t rank, const lfgpu_dim* logical, int32_t nsrc,
+                         const lfgpu_prim* src_seq, int32_t ndst, const lfgpu_prim* dst_seq,
+                         int32_t src_elem, int32_t dst_elem, const void* d_src, void* d_dst,
+                         void* stream) {
+  return guarded([&] {
+    if (!ctx) fail(LFGPU_EINVAL, "null context");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    CopySpec spec;
+    spec.lmap = identity_map(dims_of(rank, logical));
+    spec.src_seq = seq_of(nsrc, src_seq);
+    spec.dst_seq = seq_of(ndst, dst_seq);
+    spec.mode = FoldMode::Clamp;
+    std::vector<std::unique_ptr<DevBuf>> keep;
+    bool oob;
+    CopyKernel k = compile_copy(spec, src_elem, dst_elem, keep, &oob);
+    auto s = static_cast<cudaStream_t>(stream);
+    CUDA_OK(run_copy(k, d_src, d_dst, ctx->d_err, s));
+    ctx->launches += 1;
+    if (!keep.empty()) CUDA_OK(cudaStreamSynchronize(s));  // program buffers die here
+  });
+}
+
+int lfgpu_pad_convert(lfgpu_ctx* ctx, const lfgpu_dim* in_logical, int64_t pad, int32_t nsrc,
+                      const lfgpu_prim* src_seq, int32_t ndst, const lfgpu_prim* dst_seq,
+                      int32_t src_elem, int32_t dst_elem, const void* d_src, void* d_dst,
+                      void* stream) {
+  return guarded([&] {
+    if (!ctx) fail(LFGPU_EINVAL, "null context");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    CopySpec spec;
+    spec.lmap = padding_map(dims_of(4, in_logical), pad);
+    spec.src_seq = seq_of(nsrc, src_seq);
+    spec.dst_seq = seq_of(ndst, dst_seq);
+    spec.mode = FoldMode::Nest;
+    std::vector<std::unique_ptr<DevBuf>> keep;
+    bool oob;
+    CopyKernel k = compile_copy(spec, src_elem, dst_elem, keep, &oob);
+    if (oob) fail(LFGPU_ERANGE, "out-of-range access: padding reads outside its input");
+    auto s = static_cast<cudaStream_t>(stream);
+    CUDA_OK(run_copy(k, d_src, d_dst, ctx->d_err, s));
+    ctx->launches += 1;
+    if (!keep.empty()) CUDA_OK(cudaStreamSynchronize(s));
+  });
+}
+
+int lfgpu_plan_build(lfgpu_ctx* ctx, const lfgpu_graph* g, int32_t nsched,
+                     const lfgpu_sched* sched, int32_t flags, lfgpu_plan** out) {
+  *out = nullptr;
+  auto* P = new lfgpu_plan;
+  int rc = guarded([&] {
+    if (!ctx) fail(LFGPU_EINVAL, "null context");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    P->ctx = ctx;
+    P->flags = flags;
+    CUDA_OK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+    build_plan(P, g, nsched, sched);
+  });
+  if (rc != LFGPU_OK) {
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return LFGPU_OK;
+}
+
+int lfgpu_plan_destroy(lfgpu_plan* plan) {
+  if (plan) {
+    cudaSetDevice(plan->ctx->device);
+    cudaStreamSynchronize(plan->stream);
+    delete plan;
+  }
+  return LFGPU_OK;
+}
+
+static void set_input_impl(lfgpu_plan* P, int32_t tensor, const void* d_logical, int32_t elem) {
+  if (tensor < 0 || tensor >= static_cast<int32_t>(P->t.size()))
+    fail(LFGPU_EINVAL, "tensor index out of range");
+  PTensor& t = P->t[tensor];
+  CopySpec spec;
+  spec.lmap = identity_map(t.logical);
+  spec.dst_seq = t.seq;  // materialize_tensor (interp.cpp:280-337)
+  spec.mode = FoldMode::Clamp;
+  bool oob;
+  std::vector<std::unique_ptr<DevBuf>> keep;
+  if (t.d) {
+    CopyKernel k = compile_copy(spec, elem, t.elem, keep, &oob);
+    CUDA_OK(run_copy(k, d_logical, t.d, P->ctx->d_err, P->stream));
+  }
+  if (t.d_bf16) {
+    CopyKernel k = compile_copy(spec, elem, LFGPU_ELEM_BF16, keep, &oob);
+    CUDA_OK(run_copy(k, d_logical, t.d_bf16, P->ctx->d_err, P->stream));
+  }
+  CUDA_OK(cudaStreamSynchronize(P->stream));
+}
+
+int lfgpu_plan_set_input(lfgpu_plan* plan, int32_t tensor, const double* host_logical, int64_t n) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(plan->ctx->device));
+    const PTensor& t = plan->t.at(tensor);
+    if (n != numel(t.logical))
+      fail(LFGPU_EINVAL, "input '" + t.id + "' has " + std::to_string(n) + " values, expected " +
+                             std::to_string(numel(t.logical)));
+    DevBuf tmp(sizeof(double) * std::max<int64_t>(n, 1));
+    CUDA_OK(cudaMemcpyAsync(tmp.p, host_logical, sizeof(double) * n, cudaMemcpyHostToDevice,
+                            plan->stream));
+    set_input_impl(plan, tensor, tmp.p, LFGPU_ELEM_F64);
+  });
+}
+
+int lfgpu_plan_set_input_device(lfgpu_plan* plan, int32_t tensor, const void* d_logical,
+                                int32_t elem) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(plan->ctx->device));
+    set_input_impl(plan, tensor, d_logical, elem);
+  });
+}
+
+int lfgpu_plan_run(lfgpu_plan* plan) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(plan->ctx->device));
+    plan_run_steps(plan);
+  });
+}
+
+int lfgpu_plan_get_output(lfgpu_plan* plan, int32_t tensor, double* host_logical, int64_t n) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(plan->ctx->device));
+    check_device_error(plan);
+    const PTensor& t = plan->t.at(tensor);
+    if (n != numel(t.logical)) fail(LFGPU_EINVAL, "output size mismatch for '" + t.id + "'");
+    if (!t.valid)
+      fail(LFGPU_EUNSUPPORTED, "'" + t.id + "' was fused into an epilogue and not materialized");
+    CopySpec spec;
+    spec.lmap = identity_map(t.logical);
+    spec.src_seq = t.seq;  // forward map back to logical (interp.cpp:441-468)
+    spec.mode = FoldMode::Clamp;
+    std::vector<std::unique_ptr<DevBuf>> keep;
+    bool oob;
+    const void* src = t.d ? t.d : t.d_bf16;
+    int se = t.d ? t.elem : LFGPU_ELEM_BF16;
+    CopyKernel k = compile_copy(spec, se, LFGPU_ELEM_F64, keep, &oob);
+    DevBuf tmp(sizeof(double) * std::max<int64_t>(n, 1));
+    CUDA_OK(run_copy(k, src, tmp.p, plan->ctx->d_err, plan->stream));
+    CUDA_OK(cudaMemcpyAsync(host_logical, tmp.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                            plan->stream));
+    CUDA_OK(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int lfgpu_plan_tensor_buffer(lfgpu_plan* plan, int32_t tensor, void** d_ptr, int32_t* elem,
+                             int64_t* n) {
+  return guarded([&] {
+    const PTensor& t = plan->t.at(tensor);
+    *d_ptr = t.d ? t.d : t.d_bf16;
+    *elem = t.d ? t.elem : LFGPU_ELEM_BF16;
+    *n = t.numel;
+  });
+}
+
+int lfgpu_plan_stream(lfgpu_plan* plan, void** stream) {
+  *stream = plan->stream;
+  return LFGPU_OK;
+}
+
+int lfgpu_plan_info(lfgpu_plan* plan, lfgpu_counters* info) {
+  std::memset(info, 0, sizeof(*info));
+  info->kernels = static_cast<int64_t>(plan->steps.size());
+  info->bytes_moved = plan->bytes;
+  info->flops = plan->flops;
+  info->tc_nodes = plan->tc_nodes;
+  return LFGPU_OK;
+}
+
+int lfgpu_plan_node_kernel(lfgpu_plan* plan, int32_t node, char* buf, int32_t cap) {
+  return guarded([&] {
+    std::string s = plan->node_kernel.at(node);
+    auto it = plan->summary.find(node);
+    if (it != plan->summary.end()) s += " [" + it->second + "]";
+    std::strncpy(buf, s.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  });
+}
+
+int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t flush_l2,
+                       lfgpu_counters* out) {
+  return guarded([&] {
+    lfgpu_ctx* ctx = plan->ctx;
+    CUDA_OK(cudaSetDevice(ctx->device));
+    if (flush_l2 && !ctx->flush) {
+      ctx->flush_bytes = size_t(256) << 20;  // 2x the 126 MB L2
+      CUDA_OK(cudaMalloc(&ctx->flush, ctx->flush_bytes));
+    }
+    for (int i = 0; i < warmup; ++i) plan_run_steps(plan);
+    std::vector<cudaEvent_t> ev(2 * std::max(reps, 1));
+    for (auto& e : ev) CUDA_OK(cudaEventCreate(&e));
+    for (int r = 0; r < reps; ++r) {
+      if (flush_l2)
+        CUDA_OK(cudaMemsetAsync(ctx->flush, r & 0xff, ctx->flush_bytes, plan->stream));
+      CUDA_OK(cudaEventRecord(ev[2 * r], plan->stream));
+      plan_run_steps(plan);
+      CUDA_OK(cudaEventRecord(ev[2 * r + 1], plan->stream));
+    }
+    CUDA_OK(cudaStreamSynchronize(plan->stream));
+    std::vector<double> us;
+    for (int r = 0; r < reps; ++r) {
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
+      us.push_back(ms * 1000.0);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    check_device_error(plan);
+    std::sort(us.begin(), us.end());
+    lfgpu_plan_info(plan, out);
+    out->cost = us.empty() ? 0.0 : us[us.size() / 2];
+    out->min_us = us.empty() ? 0.0 : us.front();
+  });
+}
+
+int lfgpu_interpret(lfgpu_ctx* ctx, const lfgpu_graph* g, int32_t nsched,
+                    const lfgpu_sched* sched, int32_t flags, double* const* host_bufs) {
+  lfgpu_plan* P = nullptr;
+  int rc = lfgpu_plan_build(ctx, g, nsched, sched, flags | LFGPU_PLAN_KEEP_ALL, &P);
+  if (rc != LFGPU_OK) return rc;
+  rc = guarded([&] {
+    for (int i = 0; i < g->ntensors; ++i) {
+      int role = g->tensors[i].role;
+      if (role != LFGPU_ROLE_INPUT && role != LFGPU_ROLE_CONSTANT) continue;
+      if (!host_bufs[i]) fail(LFGPU_EINVAL, std::string("missing input buffer for tensor '") +
+                                                g->tensors[i].id + "'");
+      int r = lfgpu_plan_set_input(P, i, host_bufs[i], numel(P->t[i].logical));
+      if (r) fail(r, g_last_error);
+    }
+    int r = lfgpu_plan_run(P);
+    if (r) fail(r, g_last_error);
+    for (const auto& n : P->nodes) {
+      if (!host_bufs[n.output]) continue;
+      r = lfgpu_plan_get_output(P, n.output, host_bufs[n.output], numel(P->t[n.output].logical));
+      if (r) fail(r, g_last_error);
+    }
+  });
+  lfgpu_plan_destroy(P);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// lf_umma.hpp — planning and launch of the tcgen05 (UMMA) contraction
+// kernel that runs GMM (K3) and C2D (K4) directly on tuned layouts.
+//
+// One generic warp-specialised kernel serves both operators. Everything
+// layout-specific is resolved on the host into tables:
+//   * per CTA tile: TMA box coordinates of the A/B operands (tile part),
+//     the output base offset, valid rows/cols and the logical N base (bias);
+//   * per K stage: TMA coordinate increments (stage part);
+//   * per tile row / column: physical output offsets.
+// A coordinate of any operand dim is tile_part + stage_part because every
+// physical digit of a template layout belongs to exactly one logical dim
+// (space.cpp:174-417), and the unfolded input offset digit is V*h1 + rh.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "lf_core.hpp"
+
+namespace lfg {
+
+enum { UMMA_GEMM = 0, UMMA_CONV = 1 };
+enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_RELU = 2, EPI_RESIDUAL = 3 };
+constexpr int kMaxEpi = 4;
+constexpr int kMaxBoxes = 4;
+
+struct EpiOp {
+  int32_t kind = EPI_NONE;
+  int32_t tensor = -1;      // plan tensor index of the bias / residual operand
+  int32_t out_tensor = -1;  // node output this op produces (chain bookkeeping)
+  const float* ptr = nullptr;
+};
+
+// Host description of one operand's TMA view and UMMA SMEM descriptor.
+struct OperandView {
+  int32_t rank = 0;
+  uint64_t dims[5] = {};
+  uint64_t strides[5] = {};  // bytes, dims 1..rank-1
+  uint32_t box[5] = {};
+  uint32_t estride[5] = {1, 1, 1, 1, 1};
+  int32_t swizzle = 128;  // bytes: 32 / 64 / 128
+  int32_t mn_major = 0;
+  int32_t boxes = 1;      // TMA loads per stage
+  int32_t box_bytes = 0;  // bytes one load writes
+  int32_t slot_bytes = 0; // SMEM bytes reserved per box (>= box_bytes, aligned)
+  uint32_t sbo = 0, lbo = 0;
+  uint32_t k_adv = 0;     // descriptor start-address advance per UMMA K=16 step
+};
+
+struct TileEntry {  // 192 bytes
+  int32_t ca[kMaxBoxes][5];
+  int32_t cb[kMaxBoxes][5];
+  int64_t out_base;
+  int32_t rows, cols;
+  int32_t n_base;
+  int32_t pad[3];
+};
+
+struct StageEntry {  // 40 bytes
+  int32_t sa[5];
+  int32_t sb[5];
+};
+
+struct UmmaPlan {
+  int kind = UMMA_GEMM;
+  int BM = 128, BN = 128;
+  int KC = 64;          // K elements per stage
+  int pipe = 4;         // SMEM pipeline depth
+  int persistent = 0;
+  OperandView A, B;
+  std::vector<TileEntry> tiles;
+  std::vector<StageEntry> stages;
+  std::vector<int64_t> row_off, col_off;
+  EpiOp epi[kMaxEpi];
+  int epi_count = 0;
+  const void* a = nullptr;
+  const void* b = nullptr;
+  float* out = nullptr;
+  std::string summary;
+};
+
+// Per-launch device state (tables uploaded, tensor maps encoded).
+struct UmmaLaunch {
+  CUtensorMap tma_a, tma_b;
+  void* d_tiles = nullptr;
+  void* d_stages = nullptr;
+  void* d_rows = nullptr;
+  void* d_cols = nullptr;
+  int ntiles = 0, nstages = 0, BN = 0, KC = 0, pipe = 0, tmem_cols = 0;
+  int a_boxes = 0, b_boxes = 0, a_slot = 0, b_slot = 0, a_bytes = 0, b_bytes = 0;
+  uint64_t a_desc = 0, b_desc = 0;  // descriptor templates (start address filled on device)
+  uint32_t a_kadv = 0, b_kadv = 0;
+  uint32_t idesc = 0;
+  int epi_kinds[kMaxEpi] = {};
+  const float* epi_ptr[kMaxEpi] = {};
+  int epi_count = 0;
+  float* out = nullptr;
+  size_t smem = 0;
+  int grid = 0;
+  int a_rank_ = 0, b_rank_ = 0;
+  std::shared_ptr<void> owner;  // keeps the device tables alive
+};
+
+bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::vector<Dim>& b_log,
+                    const Seq& b_seq, const std::vector<Dim>& c_log, const Seq& c_seq,
+                    const lfgpu_sched& s, UmmaPlan* out, std::string* why);
+bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::vector<Dim>& k_log,
+                    const Seq& k_seq, const std::vector<Dim>& y_log, const Seq& y_seq,
+                    int64_t stride, const lfgpu_sched& s, UmmaPlan* out, std::string* why);
+// Encodes tensor maps and uploads tables (needs a, b, out set).
+UmmaLaunch umma_prepare(const UmmaPlan& p);
+cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream);
+
+}  // namespace lfg

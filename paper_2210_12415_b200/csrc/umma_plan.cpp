@@ -1,0 +1,687 @@
+// umma_plan.cpp — legality analysis and table construction for the tcgen05
+// contraction kernel (k_umma.cu) on tuned layouts.
+//
+// The GMM template (space.cpp:388-412) stores A as (M/m_t)(K/k_t) m_t k_t
+// bricks, B as (K/k_t)(N/n_t) k_t n_t and C as (M/m_t)(N/n_t) m_t n_t; the
+// C2D template (space.cpp:185-375) stores the input as overlapped tiles
+// N (H/h_t)(W/w_t)(I/i_t) B_h B_w i_t, the weight as (O/o')(I/i') KH KW i' o'
+// and the output as N (H/h_t)(W/w_t)(O/o_t) h_t w_t o_t. Each brick maps to
+// TMA boxes (one per CTA tile and K stage); the innermost brick dim decides
+// whether the operand is K-major or MN-major for UMMA, and its byte width
+// picks the 32/64/128-byte swizzle shared by the tensor map and the SMEM
+// descriptor. SURVEY.md §8(a+) derives the mapping; DESIGN.md §4 states the
+// legality rules enforced here.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+
+#include "lf_umma.hpp"
+
+namespace lfg {
+
+namespace {
+
+enum { DG_PART = 0, DG_TILE = 1, DG_OFF = 2 };
+
+struct PDigit {
+  int lj;        // logical dim
+  int kind;      // DG_*
+  int64_t div;   // DG_PART: logical = ... + (digit * div)
+  int64_t ext;
+  int64_t S;     // DG_TILE / DG_OFF: unfold stride
+  int64_t stride = 0;  // physical stride (elements)
+};
+
+bool analyze(const std::vector<Dim>& logical, const Seq& seq, std::vector<PDigit>* out) {
+  std::vector<PDigit> cur;
+  for (size_t j = 0; j < logical.size(); ++j)
+    cur.push_back({static_cast<int>(j), DG_PART, 1, logical[j].extent, 0});
+  for (const auto& p : seq) {
+    switch (p.kind) {
+      case LFGPU_PRIM_SPLIT: {
+        PDigit d = cur.at(p.dim);
+        if (d.kind != DG_PART) return false;
+        std::vector<PDigit> parts;
+        int64_t suffix = 1;
+        for (int j = 1; j < p.nfactors; ++j) suffix *= p.factors[j];
+        for (int j = 0; j < p.nfactors; ++j) {
+          parts.push_back({d.lj, DG_PART, d.div * suffix, p.factors[j], 0});
+          if (j + 1 < p.nfactors) suffix /= p.factors[j + 1];
+        }
+        cur.erase(cur.begin() + p.dim);
+        cur.insert(cur.begin() + p.dim, parts.begin(), parts.end());
+        break;
+      }
+      case LFGPU_PRIM_REORDER: {
+        std::vector<PDigit> n;
+        for (int j = 0; j < p.nperm; ++j) n.push_back(cur.at(p.perm[j]));
+        cur = n;
+        break;
+      }
+      case LFGPU_PRIM_UNFOLD: {
+        PDigit d = cur.at(p.dim);
+        if (d.kind != DG_PART || d.div != 1 || d.ext != logical[d.lj].extent) return false;
+        int64_t T = unfold_tiles(d.ext, p.tile, p.stride);
+        PDigit t{d.lj, DG_TILE, p.stride, T, p.stride};
+        PDigit o{d.lj, DG_OFF, 1, p.tile, p.stride};
+        cur.erase(cur.begin() + p.dim);
+        cur.insert(cur.begin() + p.dim, {t, o});
+        break;
+      }
+      default:
+        return false;
+    }
+  }
+  std::vector<int64_t> ext;
+  for (const auto& d : cur) ext.push_back(d.ext);
+  auto st = row_strides(ext);
+  for (size_t k = 0; k < cur.size(); ++k) cur[k].stride = st[k];
+  *out = cur;
+  return true;
+}
+
+// Value of logical index `v` on digit d (DG_PART only).
+inline int64_t digit_of(const PDigit& d, int64_t v) { return (v / d.div) % d.ext; }
+
+// A view dimension before merging: one physical digit plus its box and the
+// way its coordinate is formed.
+struct VDim {
+  int64_t ext = 1;
+  int64_t stride = 0;  // elements
+  int64_t box = 1;
+  int64_t estride = 1;
+};
+
+// Merge maximal runs of outer box-1 dims (row-major contiguous) so the view
+// fits TMA's 5 dims. `group[k]` receives the merged dim index of phys dim k
+// and `mult[k]` its coordinate multiplier inside the merged dim.
+bool merge_view(const std::vector<VDim>& phys, OperandView* v, std::vector<int>* group,
+                std::vector<int64_t>* mult, std::string* why) {
+  // phys is outer->inner. Build merged dims inner->outer for TMA.
+  int n = static_cast<int>(phys.size());
+  group->assign(n, -1);
+  mult->assign(n, 1);
+  std::vector<VDim> merged;  // inner -> outer
+  int k = n - 1;
+  while (k >= 0) {
+    if (phys[k].box != 1 || phys[k].estride != 1 || k == n - 1) {
+      (*group)[k] = static_cast<int>(merged.size());
+      merged.push_back(phys[k]);
+      --k;
+      continue;
+    }
+    // run of box-1 dims ending at k (inner end)
+    int lo = k;
+    while (lo - 1 >= 0 && phys[lo - 1].box == 1 && phys[lo - 1].estride == 1) --lo;
+    VDim m;
+    m.stride = phys[k].stride;
+    m.ext = 1;
+    int gi = static_cast<int>(merged.size());
+    for (int q = k; q >= lo; --q) {
+      (*group)[q] = gi;
+      (*mult)[q] = m.ext;
+      m.ext *= phys[q].ext;
+    }
+    merged.push_back(m);
+    k = lo - 1;
+  }
+  if (merged.size() > 5) {
+    *why = "operand view needs " + std::to_string(merged.size()) + " TMA dims";
+    return false;
+  }
+  v->rank = static_cast<int32_t>(merged.size());
+  for (int d = 0; d < v->rank; ++d) {
+    v->dims[d] = static_cast<uint64_t>(merged[d].ext);
+    v->strides[d] = static_cast<uint64_t>(merged[d].stride * 2);
+    v->box[d] = static_cast<uint32_t>(merged[d].box);
+    v->estride[d] = static_cast<uint32_t>(merged[d].estride);
+    if (merged[d].box > 256 || merged[d].box < 1) {
+      *why = "TMA box dim " + std::to_string(merged[d].box) + " out of range";
+      return false;
+    }
+    if (d > 0 && (v->strides[d] % 16) != 0) {
+      *why = "TMA stride not 16-byte aligned";
+      return false;
+    }
+  }
+  return true;
+}
+
+void finish_descriptor(OperandView* v, int rows_alloc) {
+  // Box bytes = product of loaded elements * 2 (bf16).
+  int64_t elems = 1;
+  for (int d = 0; d < v->rank; ++d) elems *= (v->box[d] + v->estride[d] - 1) / v->estride[d];
+  v->box_bytes = static_cast<int32_t>(elems * 2);
+  int align = v->swizzle * 8;  // swizzle atom: 8 rows of `swizzle` bytes
+  if (v->mn_major) {
+    // canonical MN-major: [k rows][swizzle bytes] per box; boxes are the
+    // MN atom-columns (LBO), 8-row K groups at SBO.
+    v->slot_bytes = (v->box_bytes + align - 1) / align * align;
+    v->sbo = static_cast<uint32_t>(8 * v->swizzle);
+    v->lbo = static_cast<uint32_t>(v->slot_bytes);
+    v->k_adv = static_cast<uint32_t>(16 * v->swizzle);
+  } else {
+    // canonical K-major: rows of `swizzle` bytes, 8-row groups at SBO;
+    // UMMA reads rows_alloc rows even if the box fills fewer.
+    int64_t bytes = static_cast<int64_t>(rows_alloc) * v->swizzle;
+    v->slot_bytes = static_cast<int32_t>((std::max<int64_t>(bytes, v->box_bytes) + 1023) / 1024 * 1024);
+    v->sbo = static_cast<uint32_t>(8 * v->swizzle);
+    v->lbo = 16;
+    v->k_adv = 32;  // 16 bf16 along the row
+  }
+}
+
+// Cover `T` consecutive values of a logical dim with its DG_PART digits
+// (ascending div); returns per-digit box sizes. Allows an outermost
+// overhang (TMA zero-fills beyond the tensor).
+bool cover(const std::vector<const PDigit*>& digits_by_div, int64_t T, std::vector<int64_t>* box,
+           std::string* why) {
+  box->assign(digits_by_div.size(), 1);
+  int64_t rem = T;
+  int64_t expect_div = 1;
+  for (size_t i = 0; i < digits_by_div.size(); ++i) {
+    const PDigit& d = *digits_by_div[i];
+    if (d.div != expect_div) {
+      *why = "non-dense digit order";
+      return false;
+    }
+    expect_div *= d.ext;
+    if (rem == 1) continue;
+    if (d.ext >= rem) {
+      if (d.ext % rem) {
+        *why = "tile " + std::to_string(T) + " does not align with brick " + std::to_string(d.ext);
+        return false;
+      }
+      (*box)[i] = rem;
+      rem = 1;
+    } else {
+      if (rem % d.ext) {
+        *why = "brick " + std::to_string(d.ext) + " does not divide tile " + std::to_string(T);
+        return false;
+      }
+      (*box)[i] = d.ext;
+      rem /= d.ext;
+    }
+  }
+  if (rem != 1) {
+    if (digits_by_div.empty()) return false;
+    (*box)[digits_by_div.size() - 1] *= rem;  // overhang past the tensor end
+  }
+  return true;
+}
+
+std::vector<const PDigit*> digits_of(const std::vector<PDigit>& ds, int lj) {
+  std::vector<const PDigit*> v;
+  for (const auto& d : ds)
+    if (d.lj == lj) v.push_back(&d);
+  std::sort(v.begin(), v.end(), [](const PDigit* a, const PDigit* b) { return a->div < b->div; });
+  return v;
+}
+
+// Check that the box>1 dims other than dim0 appear outer->inner with
+// decreasing div (SMEM rows come out in logical order).
+bool rows_ordered(const std::vector<PDigit>& ds, const std::vector<int64_t>& box) {
+  int64_t last = INT64_MAX;
+  for (size_t k = 0; k + 1 < ds.size(); ++k) {
+    if (box[k] <= 1) continue;
+    if (ds[k].div >= last) return false;
+    last = ds[k].div;
+  }
+  return true;
+}
+
+uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
+  uint32_t d = 0;
+  d |= 1u << 4;                          // D format: F32
+  d |= 1u << 7;                          // A format: BF16
+  d |= 1u << 10;                         // B format: BF16
+  d |= (a_mn ? 1u : 0u) << 15;           // A major
+  d |= (b_mn ? 1u : 0u) << 16;           // B major
+  d |= static_cast<uint32_t>(N >> 3) << 17;
+  d |= static_cast<uint32_t>(M >> 4) << 24;
+  return d;
+}
+
+int pick_pipe(const UmmaPlan& p) {
+  int per = p.A.slot_bytes * p.A.boxes + p.B.slot_bytes * p.B.boxes;
+  int budget = 200 * 1024;
+  return std::max(2, std::min(8, budget / std::max(per, 1)));
+}
+
+// Split-only operand view for GEMM: `mn_lj`, `k_lj` name the logical dims.
+bool gemm_operand(const std::vector<Dim>& log, const Seq& seq, int mn_lj, int k_lj, int T_mn,
+                  int KC, OperandView* v, std::vector<PDigit>* ds_out,
+                  std::vector<int64_t>* box_out, std::vector<int>* group,
+                  std::vector<int64_t>* mult, std::string* why) {
+  std::vector<PDigit> ds;
+  if (!analyze(log, seq, &ds)) {
+    *why = "layout is not a split/reorder brick layout";
+    return false;
+  }
+  for (const auto& d : ds)
+    if (d.kind != DG_PART) {
+      *why = "unfold in a GEMM operand";
+      return false;
+    }
+  const PDigit& inner = ds.back();
+  if (inner.div != 1 || inner.ext % 64 != 0) {
+    *why = "innermost brick dim must be a multiple of 64 elements";
+    return false;
+  }
+  v->mn_major = inner.lj == mn_lj ? 1 : 0;
+  v->swizzle = 128;
+  std::vector<int64_t> box(ds.size(), 1);
+  std::vector<int64_t> bmn, bk;
+  auto mnd = digits_of(ds, mn_lj), kd = digits_of(ds, k_lj);
+  if (v->mn_major) {
+    if (T_mn % 64) {
+      *why = "MN-major tile not a multiple of 64";
+      return false;
+    }
+    v->boxes = T_mn / 64;
+    if (v->boxes > kMaxBoxes) {
+      *why = "too many TMA boxes";
+      return false;
+    }
+    if (!cover(kd, KC, &bk, why)) return false;
+    for (size_t i = 0; i < kd.size(); ++i) box[kd[i] - ds.data()] = bk[i];
+    box[ds.size() - 1] = 64;
+  } else {
+    v->boxes = 1;
+    if (!cover(mnd, T_mn, &bmn, why)) return false;
+    for (size_t i = 0; i < mnd.size(); ++i) box[mnd[i] - ds.data()] = bmn[i];
+    box[ds.size() - 1] = KC;
+    if (inner.ext % KC) {
+      *why = "K stage does not divide the K brick";
+      return false;
+    }
+  }
+  if (!rows_ordered(ds, box)) {
+    *why = "brick digits out of order for the SMEM tile";
+    return false;
+  }
+  std::vector<VDim> phys;
+  for (size_t k = 0; k < ds.size(); ++k) phys.push_back({ds[k].ext, ds[k].stride, box[k], 1});
+  if (!merge_view(phys, v, group, mult, why)) return false;
+  *ds_out = ds;
+  *box_out = box;
+  return true;
+}
+
+// Coordinates of one operand box: logical values per logical dim.
+void coords(const std::vector<PDigit>& ds, const std::vector<int>& group,
+            const std::vector<int64_t>& mult, const int64_t* lv, int32_t* out) {
+  for (int d = 0; d < 5; ++d) out[d] = 0;
+  for (size_t k = 0; k < ds.size(); ++k)
+    out[group[k]] += static_cast<int32_t>(digit_of(ds[k], lv[ds[k].lj]) * mult[k]);
+}
+
+int64_t offset_of(const std::vector<PDigit>& ds, const int64_t* lv) {
+  int64_t off = 0;
+  for (const auto& d : ds) off += digit_of(d, lv[d.lj]) * d.stride;
+  return off;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// GEMM: C[M,N] = A[M,K] B[K,N]   (interp.cpp:109-122)
+
+bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::vector<Dim>& b_log,
+                    const Seq& b_seq, const std::vector<Dim>& c_log, const Seq& c_seq,
+                    const lfgpu_sched& s, UmmaPlan* out, std::string* why) {
+  const int64_t M = a_log[0].extent, K = a_log[1].extent, N = b_log[1].extent;
+  if (K % 64) {
+    *why = "K must be a multiple of 64";
+    return false;
+  }
+  std::vector<PDigit> cds;
+  if (!analyze(c_log, c_seq, &cds)) {
+    *why = "output layout is not a brick layout";
+    return false;
+  }
+  UmmaPlan p;
+  p.kind = UMMA_GEMM;
+  p.BM = 128;
+  p.KC = 64;
+  // N tile: the schedule's innermost tile when legal, else the widest tile
+  // that still fills most of the 148 SMs.
+  std::vector<int> cands;
+  if (s.tile_last >= 16 && s.tile_last <= 256 && s.tile_last % 16 == 0) cands.push_back(s.tile_last);
+  const int64_t mtiles = (M + 127) / 128;
+  for (int bn : {256, 128, 64, 32, 16})
+    if (mtiles * ((N + bn - 1) / bn) >= 111 || bn == 16) cands.push_back(bn);
+  std::string last_why;
+  for (int BN : cands) {
+    if (N % BN && N > BN) continue;
+    std::vector<PDigit> ads, bds;
+    std::vector<int64_t> abox, bbox;
+    std::vector<int> ag, bg;
+    std::vector<int64_t> am, bm;
+    UmmaPlan q = p;
+    q.BN = BN;
+    if (!gemm_operand(a_log, a_seq, 0, 1, 128, 64, &q.A, &ads, &abox, &ag, &am, &last_why)) {
+      *why = "A: " + last_why;
+      return false;
+    }
+    if (!gemm_operand(b_log, b_seq, 1, 0, BN, 64, &q.B, &bds, &bbox, &bg, &bm, &last_why)) {
+      last_why = "B: " + last_why;
+      continue;
+    }
+    // Output digits must align with the tile (rows and columns).
+    std::vector<int64_t> tmp;
+    if (!cover(digits_of(cds, 0), 128, &tmp, &last_why) ||
+        !cover(digits_of(cds, 1), BN, &tmp, &last_why)) {
+      last_why = "C: " + last_why;
+      continue;
+    }
+    finish_descriptor(&q.A, 128);
+    finish_descriptor(&q.B, BN);
+    const int64_t ntile_n = (N + BN - 1) / BN;
+    for (int64_t tm = 0; tm < mtiles; ++tm)
+      for (int64_t tn = 0; tn < ntile_n; ++tn) {
+        TileEntry te;
+        std::memset(&te, 0, sizeof(te));
+        for (int b = 0; b < q.A.boxes; ++b) {
+          int64_t lv[2] = {tm * 128 + (q.A.mn_major ? b * 64 : 0), 0};
+          coords(ads, ag, am, lv, te.ca[b]);
+        }
+        for (int b = 0; b < q.B.boxes; ++b) {
+          int64_t lv[2] = {0, tn * BN + (q.B.mn_major ? b * 64 : 0)};
+          coords(bds, bg, bm, lv, te.cb[b]);
+        }
+        int64_t lv[2] = {tm * 128, tn * BN};
+        te.out_base = offset_of(cds, lv);
+        te.rows = static_cast<int32_t>(std::min<int64_t>(128, M - tm * 128));
+        te.cols = static_cast<int32_t>(std::min<int64_t>(BN, N - tn * BN));
+        te.n_base = static_cast<int32_t>(tn * BN);
+        q.tiles.push_back(te);
+      }
+    for (int64_t k0 = 0; k0 < K; k0 += 64) {
+      StageEntry se;
+      std::memset(&se, 0, sizeof(se));
+      int64_t la[2] = {0, k0}, lb[2] = {k0, 0};
+      coords(ads, ag, am, la, se.sa);
+      coords(bds, bg, bm, lb, se.sb);
+      q.stages.push_back(se);
+    }
+    for (int r = 0; r < 128; ++r) {
+      int64_t lv[2] = {r, 0};
+      q.row_off.push_back(offset_of(cds, lv));
+    }
+    for (int c = 0; c < BN; ++c) {
+      int64_t lv[2] = {0, c};
+      q.col_off.push_back(offset_of(cds, lv));
+    }
+    q.pipe = pick_pipe(q);
+    std::ostringstream os;
+    os << "gemm BM=128 BN=" << BN << " KC=64 A=" << (q.A.mn_major ? "MN" : "K") << "-major B="
+       << (q.B.mn_major ? "MN" : "K") << "-major tiles=" << q.tiles.size() << " pipe=" << q.pipe;
+    q.summary = os.str();
+    q.persistent = s.parallel;
+    *out = q;
+    return true;
+  }
+  *why = last_why;
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+// C2D: y[b,o,h,w] = sum_{i,rh,rw} x[b,i,V*h+rh,V*w+rw] * ker[o,i,rh,rw]
+// (interp.cpp:70-89) as an implicit GEMM over the template layouts.
+
+bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::vector<Dim>& k_log,
+                    const Seq& k_seq, const std::vector<Dim>& y_log, const Seq& y_seq,
+                    int64_t V, const lfgpu_sched& s, UmmaPlan* out, std::string* why) {
+  const int64_t N = y_log[0].extent, O = y_log[1].extent, Ho = y_log[2].extent,
+                Wo = y_log[3].extent, I = x_log[1].extent, KH = k_log[2].extent,
+                KW = k_log[3].extent;
+  std::vector<PDigit> xd, kd, yd;
+  if (!analyze(x_log, x_seq, &xd) || !analyze(k_log, k_seq, &kd) || !analyze(y_log, y_seq, &yd)) {
+    *why = "layouts are not template brick layouts";
+    return false;
+  }
+  if (V > 8) {
+    *why = "stride > 8 exceeds TMA traversal stride";
+    return false;
+  }
+  // Output tiling: innermost digits of H, W, O.
+  auto yh = digits_of(yd, 2), yw = digits_of(yd, 3), yo = digits_of(yd, 1);
+  const int64_t h_t = yh[0]->ext, w_t = yw[0]->ext, o_t = yo[0]->ext;
+  if (yh.size() > 2 || yw.size() > 2 || yo.size() > 2 || digits_of(yd, 0).size() != 1) {
+    *why = "output is not a one-level template layout";
+    return false;
+  }
+  for (const auto& d : yd)
+    if (d.kind != DG_PART) {
+      *why = "unfolded output";
+      return false;
+    }
+  if (w_t > 128) {
+    *why = "w_t > 128 rows";
+    return false;
+  }
+  const int64_t h_sub = std::min<int64_t>(h_t, 128 / w_t);
+  if (h_sub * V > 256 || w_t * V > 256) {
+    *why = "TMA box exceeds 256";
+    return false;
+  }
+  // Input: innermost = I inner brick.
+  const PDigit& xi = xd.back();
+  if (xi.lj != 1 || xi.kind != DG_PART || xi.div != 1 || xi.ext % 16) {
+    *why = "input channel brick i_t must be innermost and a multiple of 16";
+    return false;
+  }
+  const int64_t i_t = xi.ext;
+  // Weight: innermost = O inner brick (MN-major B).
+  const PDigit& ko = kd.back();
+  if (ko.lj != 0 || ko.kind != DG_PART || ko.div != 1 || ko.ext % 16) {
+    *why = "weight output-channel brick o' must be innermost and a multiple of 16";
+    return false;
+  }
+  const int64_t o2 = ko.ext;
+  auto ki = digits_of(kd, 1);
+  const int64_t i2 = ki[0]->ext;
+  if (i2 % 16) {
+    *why = "weight input-channel brick i' must be a multiple of 16";
+    return false;
+  }
+  int64_t KC = std::gcd(i_t, i2);
+  KC = std::min<int64_t>(KC, 64);
+  while (KC > 16 && (KC & (KC - 1))) KC /= 2;
+  if (KC != 16 && KC != 32 && KC != 64) {
+    *why = "channel chunk not in {16,32,64}";
+    return false;
+  }
+  // Channel tile of the CTA (UMMA N).
+  int64_t BN = std::min<int64_t>(o_t, 256);
+  if (s.tile_last >= 16 && s.tile_last < BN && o_t % s.tile_last == 0 && s.tile_last % 16 == 0)
+    BN = s.tile_last;
+  if (o_t % BN || BN % 16) {
+    *why = "channel tile not a multiple of 16";
+    return false;
+  }
+  const int64_t bn_sw = std::min<int64_t>(o2 * 2, 128);  // B swizzle bytes
+  const int64_t nbox = bn_sw / 2;                       // n per B box
+  if (BN % nbox) {
+    *why = "channel tile does not align with the weight brick";
+    return false;
+  }
+
+  UmmaPlan p;
+  p.kind = UMMA_CONV;
+  p.BM = 128;
+  p.BN = static_cast<int>(BN);
+  p.KC = static_cast<int>(KC);
+
+  // --- A view (input): boxes and coordinate recipes per phys digit.
+  std::vector<VDim> xv;
+  for (const auto& d : xd) {
+    VDim v{d.ext, d.stride, 1, 1};
+    if (d.lj == 1 && d.div == 1 && &d == &xd.back()) v.box = KC;
+    if ((d.lj == 2 || d.lj == 3) && (d.kind == DG_OFF || d.kind == DG_PART)) {
+      if (d.kind == DG_PART && (d.div != 1 || d.ext != x_log[d.lj].extent)) {
+        *why = "input H/W split without unfold";
+        return false;
+      }
+      int64_t rows = d.lj == 2 ? h_sub : w_t;
+      v.box = rows * V;
+      v.estride = V;
+    }
+    if (d.kind == DG_TILE || d.kind == DG_OFF) {
+      int64_t t = d.lj == 2 ? h_t : w_t;
+      int64_t Bneed = (t - 1) * V + (d.lj == 2 ? KH : KW);
+      if (d.S != t * V || (d.kind == DG_OFF && d.ext < Bneed)) {
+        *why = "input unfold does not match the output tile";
+        return false;
+      }
+    }
+    xv.push_back(v);
+  }
+  // SMEM rows of the A box come out in the physical order of the H and W
+  // row dims: (h, w) when H is outer (the template), (w, h) when an untiled
+  // W dim sits outside the H tile (decode_layout with w_t == W).
+  bool h_outer = true;
+  {
+    int hpos = -1, wpos = -1;
+    for (size_t k = 0; k + 1 < xd.size(); ++k) {
+      if (xv[k].box > 1 && xd[k].lj == 2) hpos = static_cast<int>(k);
+      if (xv[k].box > 1 && xd[k].lj == 3) wpos = static_cast<int>(k);
+    }
+    if (hpos >= 0 && wpos >= 0 && hpos > wpos) h_outer = false;
+    if (!h_outer && h_t % h_sub != 0) {
+      *why = "W-outer input needs whole H chunks";
+      return false;
+    }
+  }
+  std::vector<int> ag;
+  std::vector<int64_t> am;
+  p.A.mn_major = 0;
+  p.A.swizzle = static_cast<int32_t>(KC * 2);
+  p.A.boxes = 1;
+  if (!merge_view(xv, &p.A, &ag, &am, why)) return false;
+  finish_descriptor(&p.A, 128);
+
+  // --- B view (weight): MN-major over o', k rows over i'.
+  std::vector<VDim> kv;
+  for (const auto& d : kd) {
+    VDim v{d.ext, d.stride, 1, 1};
+    if (&d == &kd.back()) v.box = nbox;
+    if (d.lj == 1 && d.div == 1) {
+      if (d.ext % KC) {
+        *why = "weight channel brick";
+        return false;
+      }
+      v.box = KC;
+    }
+    kv.push_back(v);
+  }
+  // the k-row dim must be directly outside the o' dim (rows = channels)
+  std::vector<int> bg;
+  std::vector<int64_t> bm;
+  p.B.mn_major = 1;
+  p.B.swizzle = static_cast<int32_t>(bn_sw);
+  p.B.boxes = static_cast<int32_t>(BN / nbox);
+  if (p.B.boxes > kMaxBoxes) {
+    *why = "too many weight boxes";
+    return false;
+  }
+  {
+    int rows_dims = 0;
+    for (size_t k = 0; k + 1 < kd.size(); ++k)
+      if (kv[k].box > 1) ++rows_dims;
+    if (rows_dims != 1) {
+      *why = "weight brick rows not contiguous";
+      return false;
+    }
+  }
+  if (!merge_view(kv, &p.B, &bg, &bm, why)) return false;
+  finish_descriptor(&p.B, static_cast<int>(BN));
+
+  // --- tiles
+  const int64_t H0 = Ho / h_t, W0 = Wo / w_t, O0 = O / o_t;
+  const int64_t hchunks = (h_t + h_sub - 1) / h_sub, ochunks = o_t / BN;
+  auto coord_x = [&](int64_t n, int64_t h0, int64_t w0, int64_t h1s, int64_t c0, int64_t rh,
+                     int64_t rw, bool tile_part, int32_t* outc) {
+    for (int d = 0; d < 5; ++d) outc[d] = 0;
+    for (size_t k = 0; k < xd.size(); ++k) {
+      const PDigit& d = xd[k];
+      int64_t c = 0;
+      if (d.lj == 0) c = tile_part ? n : 0;
+      else if (d.lj == 1) c = tile_part ? 0 : digit_of(d, c0);
+      else {
+        int64_t t0 = d.lj == 2 ? h0 : w0, s1 = d.lj == 2 ? h1s : 0, r = d.lj == 2 ? rh : rw;
+        int64_t tt = d.lj == 2 ? h_t : w_t;
+        if (d.kind == DG_TILE) c = tile_part ? t0 : 0;
+        else if (d.kind == DG_OFF) c = tile_part ? V * s1 : r;
+        else c = tile_part ? V * (t0 * tt + s1) : r;  // whole dim
+      }
+      outc[ag[k]] += static_cast<int32_t>(c * am[k]);
+    }
+  };
+  auto coord_k = [&](int64_t o, int64_t c0, int64_t rh, int64_t rw, bool tile_part,
+                     int32_t* outc) {
+    for (int d = 0; d < 5; ++d) outc[d] = 0;
+    for (size_t k = 0; k < kd.size(); ++k) {
+      const PDigit& d = kd[k];
+      int64_t c = 0;
+      if (d.lj == 0) c = tile_part ? digit_of(d, o) : 0;
+      else if (d.lj == 1) c = tile_part ? 0 : digit_of(d, c0);
+      else if (d.lj == 2) c = tile_part ? 0 : digit_of(d, rh);
+      else c = tile_part ? 0 : digit_of(d, rw);
+      outc[bg[k]] += static_cast<int32_t>(c * bm[k]);
+    }
+  };
+  auto y_off = [&](int64_t n, int64_t o, int64_t h, int64_t w) {
+    int64_t lv[4] = {n, o, h, w};
+    return offset_of(yd, lv);
+  };
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t h0 = 0; h0 < H0; ++h0)
+      for (int64_t w0 = 0; w0 < W0; ++w0)
+        for (int64_t hc = 0; hc < hchunks; ++hc)
+          for (int64_t o0 = 0; o0 < O0; ++o0)
+            for (int64_t oc = 0; oc < ochunks; ++oc) {
+              TileEntry te;
+              std::memset(&te, 0, sizeof(te));
+              int64_t h1s = hc * h_sub;
+              coord_x(n, h0, w0, h1s, 0, 0, 0, true, te.ca[0]);
+              int64_t obase = o0 * o_t + oc * BN;
+              for (int b = 0; b < p.B.boxes; ++b) coord_k(obase + b * nbox, 0, 0, 0, true, te.cb[b]);
+              te.out_base = y_off(n, obase, h0 * h_t + h1s, w0 * w_t);
+              te.rows = static_cast<int32_t>(std::min<int64_t>(h_sub, h_t - h1s) * w_t);
+              te.cols = static_cast<int32_t>(BN);
+              te.n_base = static_cast<int32_t>(obase);
+              p.tiles.push_back(te);
+            }
+  for (int64_t c0 = 0; c0 < I; c0 += KC)
+    for (int64_t rh = 0; rh < KH; ++rh)
+      for (int64_t rw = 0; rw < KW; ++rw) {
+        StageEntry se;
+        std::memset(&se, 0, sizeof(se));
+        coord_x(0, 0, 0, 0, c0, rh, rw, false, se.sa);
+        coord_k(0, c0, rh, rw, false, se.sb);
+        p.stages.push_back(se);
+      }
+  // Rows: r -> (hh, ww) inside the tile; offsets relative to the tile base.
+  const int64_t base0 = y_off(0, 0, 0, 0);
+  for (int r = 0; r < 128; ++r) {
+    int64_t hh = h_outer ? r / w_t : r % h_sub;
+    int64_t ww = h_outer ? r % w_t : r / h_sub;
+    if (hh >= h_sub || ww >= w_t) hh = 0, ww = 0;
+    p.row_off.push_back(y_off(0, 0, hh, ww) - base0);
+  }
+  for (int c = 0; c < BN; ++c) p.col_off.push_back(y_off(0, c, 0, 0) - base0);
+  p.pipe = pick_pipe(p);
+  p.persistent = s.parallel;
+  std::ostringstream os;
+  os << "conv h_t=" << h_t << " w_t=" << w_t << " o_t=" << o_t << " i_t=" << i_t << " i'=" << i2
+     << " o'=" << o2 << " rows=" << h_sub * w_t << " BN=" << BN << " KC=" << KC
+     << " tiles=" << p.tiles.size() << " stages=" << p.stages.size() << " pipe=" << p.pipe;
+  p.summary = os.str();
+  *out = p;
+  return true;
+}
+
+}  // namespace lfg

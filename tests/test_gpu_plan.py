@@ -1,0 +1,210 @@
+"""Whole-graph execution on the GPU (interpret / plans / measure) against the
+oracle's reference_eval, and the tcgen05 contractions on tuned layouts.
+
+Tolerances (proj/src/cli.cpp:30-49): int32 exact; float
+1e-5 relative with scale max(1,|a|,|b|). Contractions whose operands are the
+reference's k/64 inputs are bit-exact on tensor cores (bf16 products are
+exact, fp32 partial sums stay exact for K <= 4096), so those are checked
+with ==.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2210_12415_b200 import _abi, ir, runtime
+from paper_2210_12415_b200.layout import reorder, split, unfold
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_outputs(g, seed):
+    bufs = O.random_inputs(g, seed)
+    inputs = {t.id: bufs[i].copy() for i, t in enumerate(g.tensors)
+              if t.role in (ir.INPUT, ir.CONSTANT)}
+    O.reference_eval(g, bufs)
+    ref = {n.output: bufs[g.tensor_index(n.output)] for n in g.nodes}
+    return inputs, ref
+
+
+def tol_of(g, tid):
+    return 0.0 if g.tensor(tid).dtype == ir.I32 else 1e-5
+
+
+def check(g, got, ref, exact=False):
+    for tid, want in ref.items():
+        d = O.max_rel_diff(got[tid], want)
+        assert d <= (0.0 if exact else tol_of(g, tid)), (tid, d)
+
+
+def test_interpret_template_layouts_golden(golden):
+    # test_executor.cpp:148-159 via the reference's own interpret output.
+    case = golden["interpret"][0]
+    g = ir.conv_chain(1, 2, 4, 6, 3, 1, 1)
+    from test_oracle import seq_from
+    seqs = {k: seq_from(v) for k, v in case["seqs"].items()}
+    bufs = O.random_inputs(g, case["seed"])
+    inputs = {t.id: bufs[i] for i, t in enumerate(g.tensors) if t.role in (ir.INPUT, ir.CONSTANT)}
+    got = runtime.interpret(g, seqs, [], inputs, flags=_abi.PLAN_EXACT)
+    for tid, st in case["outputs"].items():
+        assert O.fnv1a(got[tid]) == st["fnv"], tid
+
+
+MICRO = [
+    lambda: ir.conv_chain(1, 2, 4, 6, 3, 1, 1),
+    lambda: ir.conv_chain(2, 3, 5, 8, 3, 2, 1),
+    lambda: ir.conv_chain(1, 2, 3, 6, 3, 1, 1, dtype=ir.I32),
+    lambda: ir.dep_chain(1, 4, 6, 3, 1, 1),
+    lambda: ir.gmm_chain(8, 4, 8),
+    lambda: ir.bare_conv(1, 3, 5, 11, 3, 2),
+]
+
+
+@pytest.mark.parametrize("flags", [_abi.PLAN_EXACT, _abi.PLAN_DEFAULT])
+def test_interpret_micrographs_identity(flags):
+    for mk in MICRO:
+        g = mk()
+        inputs, ref = oracle_outputs(g, 17)
+        got = runtime.interpret(g, {}, [], inputs, flags=flags)
+        check(g, got, ref)
+
+
+def test_interpret_fuzz_template_layouts():
+    # test_executor.cpp:413-440: random template layouts through decode_layout.
+    rng = np.random.default_rng(23)
+    for it in range(60):
+        which = it % 3
+        if which == 0:
+            g = ir.conv_chain(1, 1 + int(rng.integers(0, 3)), 2 + int(rng.integers(0, 3)),
+                              4 + 2 * int(rng.integers(0, 3)), 3, 1 + int(rng.integers(0, 2)), 1)
+        elif which == 1:
+            g = ir.dep_chain(1, 2 + int(rng.integers(0, 3)), 6, 3, 1, 1)
+        else:
+            g = ir.gmm_chain(4 + 4 * int(rng.integers(0, 2)), 4, 4 + 4 * int(rng.integers(0, 2)))
+        seqs = {}
+        for node, n in enumerate(g.nodes):
+            if not ir.is_complex_op(n.kind):
+                continue
+            t = runtime.layout_template(g, node)
+            factors = []
+            for _, e in t:
+                divs = [d for d in range(1, e + 1) if e % d == 0]
+                factors.append(int(rng.choice(divs)))
+            seqs.update(runtime.decode_layout(g, node, factors))
+        inputs, ref = oracle_outputs(g, 1000 + it)
+        got = runtime.interpret(g, seqs, [], inputs, flags=_abi.PLAN_EXACT)
+        check(g, got, ref)
+
+
+def gemm_case(M, K, N, factors):
+    g = ir.gemm(M, K, N)
+    seqs = runtime.decode_layout(g, 0, factors) if factors else {}
+    inputs, ref = oracle_outputs(g, 42)
+    return g, seqs, inputs, ref
+
+
+@pytest.mark.parametrize("factors", [(128, 64, 128), (128, 64, 256), (256, 128, 64),
+                                     (128, 512, 64), None, (64, 64, 64)])
+def test_umma_gemm_bitexact(factors):
+    M = K = N = 512
+    g, seqs, inputs, ref = gemm_case(M, K, N, factors)
+    p = runtime.Plan(g, seqs, [], flags=_abi.PLAN_REQUIRE_TC)
+    assert p.node_kernel(0).startswith("umma_gemm"), p.node_kernel(0)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    got = p.get_output("c")
+    assert np.array_equal(got, ref["c"]), np.abs(got - ref["c"]).max()
+
+
+def test_umma_gemm_cfg2_1024():
+    g, seqs, inputs, ref = gemm_case(1024, 1024, 1024, (128, 64, 128))
+    got = runtime.interpret(g, seqs, [runtime.sched(0, tile_last=64)], inputs)
+    assert np.array_equal(got["c"], ref["c"])
+
+
+def test_umma_gemm_mn_major_a_and_k_major_b():
+    # m-only split: A becomes (M/m_t) K m_t (M-contiguous); k-only split on B
+    # gives (K/k_t) N k_t (K-contiguous B).
+    g = ir.gemm(256, 256, 256)
+    seqs = {"a": [split(0, [2, 128]), reorder([0, 2, 1])],
+            "b": [split(0, [4, 64]), reorder([0, 2, 1])]}
+    inputs, ref = oracle_outputs(g, 3)
+    p = runtime.Plan(g, seqs, [], flags=_abi.PLAN_REQUIRE_TC)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    assert np.array_equal(p.get_output("c"), ref["c"])
+
+
+# (h_t, w_t, o_t, i_t, i'_t, o'_t). i_t < I keeps the channel brick innermost
+# (space.cpp:322-337), which the K-major A operand needs.
+CONV_FACTORS = [
+    (4, 28, 16, 32, 32, 16),   # 112 rows, KC=32 (64 B swizzle), o'=16 (32 B)
+    (4, 14, 16, 16, 16, 16),   # SURVEY's example point: 56 rows, KC=16
+    (8, 8, 32, 32, 32, 32),    # 64 rows
+    (2, 56, 64, 32, 32, 64),   # untiled W outside the H tile: (w, h) row order
+    (4, 28, 32, 16, 32, 32),   # i_t != i'_t: KC = gcd = 16
+]
+
+
+@pytest.mark.parametrize("factors", CONV_FACTORS)
+def test_umma_conv_cfg1_bitexact(factors):
+    g = ir.pad_conv(1, 64, 64, 56, 3, 1, 1)
+    seqs = runtime.decode_layout(g, 1, list(factors))
+    inputs, ref = oracle_outputs(g, 42)
+    p = runtime.Plan(g, seqs, [], flags=_abi.PLAN_REQUIRE_TC)
+    assert p.node_kernel(1).startswith("umma_conv"), p.node_kernel(1)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    assert np.array_equal(p.get_output("xp"), ref["xp"])
+    y = p.get_output("y")
+    assert np.array_equal(y, ref["y"]), np.abs(y - ref["y"]).max()
+
+
+def test_umma_conv_stride2_batch():
+    g = ir.pad_conv(2, 64, 64, 28, 3, 2, 1)  # Ho = 14, untiled W
+    seqs = runtime.decode_layout(g, 1, [7, 14, 32, 32, 32, 32])
+    inputs, ref = oracle_outputs(g, 4)
+    p = runtime.Plan(g, seqs, [], flags=_abi.PLAN_REQUIRE_TC)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    assert np.array_equal(p.get_output("y"), ref["y"])
+
+
+def test_fused_epilogue_conv_chain():
+    # Padding -> C2D -> BiasAdd -> ReLU with the C2D schedule's fuse flag:
+    # bias and relu run in the tcgen05 epilogue (lower.cpp:566-608).
+    g = ir.conv_chain(1, 64, 64, 56, 3, 1, 1)
+    seqs = runtime.decode_layout(g, 1, [4, 28, 16, 32, 32, 16])
+    for t in ("biased", "y"):
+        seqs[t] = seqs["conv"]
+    inputs, ref = oracle_outputs(g, 42)
+    p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=1)], flags=_abi.PLAN_REQUIRE_TC)
+    assert p.node_kernel(2) == "fused" and p.node_kernel(3) == "fused"
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    assert np.array_equal(p.get_output("y"), ref["y"])
+    with pytest.raises(runtime.LfError):
+        p.get_output("conv")  # fused away, never materialized
+
+
+def test_require_tc_rejects_illegal_layout():
+    g = ir.pad_conv(1, 3, 8, 10, 3, 1, 1)
+    with pytest.raises(runtime.LfError) as e:
+        runtime.Plan(g, {}, [], flags=_abi.PLAN_REQUIRE_TC)
+    assert e.value.code == _abi.EUNSUPPORTED
+
+
+def test_measure_reports_device_time():
+    g = ir.pad_conv(1, 64, 64, 56, 3, 1, 1)
+    seqs = runtime.decode_layout(g, 1, [4, 28, 16, 32, 32, 16])
+    p = runtime.Plan(g, seqs, [], flags=_abi.PLAN_CUDA_GRAPH)
+    inputs, _ = oracle_outputs(g, 42)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    c = p.measure(warmup=3, reps=20, flush_l2=True)
+    assert c.cost > 0 and c.min_us <= c.cost and c.kernels == 2 and c.tc_nodes == 1
+    assert c.flops == 2 * 64 * 64 * 56 * 56 * 9
