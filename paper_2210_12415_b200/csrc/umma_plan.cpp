@@ -350,8 +350,12 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
   std::vector<int> cands;
   if (s.tile_last >= 16 && s.tile_last <= 256 && s.tile_last % 16 == 0) cands.push_back(s.tile_last);
   const int64_t mtiles = (M + 127) / 128;
+  // Widest tile that still fills ~3/4 of the 148 SMs first, then the rest
+  // from wide to narrow (legality may rule some out).
   for (int bn : {256, 128, 64, 32, 16})
-    if (mtiles * ((N + bn - 1) / bn) >= 111 || bn == 16) cands.push_back(bn);
+    if (mtiles * ((N + bn - 1) / bn) >= 111) cands.push_back(bn);
+  for (int bn : {64, 128, 256, 32, 16})
+    if (mtiles * ((N + bn - 1) / bn) < 111) cands.push_back(bn);
   std::string last_why;
   for (int BN : cands) {
     if (N % BN && N > BN) continue;
@@ -474,13 +478,15 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
     return false;
   }
   const int64_t i_t = xi.ext;
-  // Weight: innermost = O inner brick (MN-major B).
+  // Weight: innermost = O inner brick (MN-major B, the template's o' when
+  // o' < O) or the I inner brick (K-major B, when o' == O leaves O whole).
   const PDigit& ko = kd.back();
-  if (ko.lj != 0 || ko.kind != DG_PART || ko.div != 1 || ko.ext % 16) {
-    *why = "weight output-channel brick o' must be innermost and a multiple of 16";
+  const bool b_kmajor = ko.lj == 1;
+  if ((ko.lj != 0 && ko.lj != 1) || ko.kind != DG_PART || ko.div != 1 || ko.ext % 16) {
+    *why = "weight innermost brick must be o' or i' and a multiple of 16";
     return false;
   }
-  const int64_t o2 = ko.ext;
+  const int64_t o2 = b_kmajor ? 64 : ko.ext;  // K-major: O rows, no swizzle constraint on N
   auto ki = digits_of(kd, 1);
   const int64_t i2 = ki[0]->ext;
   if (i2 % 16) {
@@ -563,11 +569,18 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
   if (!merge_view(xv, &p.A, &ag, &am, why)) return false;
   finish_descriptor(&p.A, 128);
 
-  // --- B view (weight): MN-major over o', k rows over i'.
+  // --- B view (weight). MN-major: o' contiguous, k rows over i'.
+  // K-major: i' contiguous (KC per box row), BN rows over the O digits.
   std::vector<VDim> kv;
-  for (const auto& d : kd) {
+  std::vector<int64_t> obox;
+  if (b_kmajor) {
+    auto od = digits_of(kd, 0);
+    if (!cover(od, BN, &obox, why)) return false;
+  }
+  for (size_t k = 0; k < kd.size(); ++k) {
+    const PDigit& d = kd[k];
     VDim v{d.ext, d.stride, 1, 1};
-    if (&d == &kd.back()) v.box = nbox;
+    if (!b_kmajor && k + 1 == kd.size()) v.box = nbox;
     if (d.lj == 1 && d.div == 1) {
       if (d.ext % KC) {
         *why = "weight channel brick";
@@ -575,23 +588,31 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
       }
       v.box = KC;
     }
+    if (b_kmajor && d.lj == 0) {
+      auto od = digits_of(kd, 0);
+      for (size_t q = 0; q < od.size(); ++q)
+        if (od[q] == &d) v.box = obox[q];
+    }
     kv.push_back(v);
   }
-  // the k-row dim must be directly outside the o' dim (rows = channels)
   std::vector<int> bg;
   std::vector<int64_t> bm;
-  p.B.mn_major = 1;
-  p.B.swizzle = static_cast<int32_t>(bn_sw);
-  p.B.boxes = static_cast<int32_t>(BN / nbox);
+  p.B.mn_major = b_kmajor ? 0 : 1;
+  p.B.swizzle = static_cast<int32_t>(b_kmajor ? KC * 2 : bn_sw);
+  p.B.boxes = b_kmajor ? 1 : static_cast<int32_t>(BN / nbox);
   if (p.B.boxes > kMaxBoxes) {
     *why = "too many weight boxes";
     return false;
   }
   {
+    // MN-major: exactly one row dim (i'); K-major: the O digits, in order.
+    std::vector<int64_t> bx;
     int rows_dims = 0;
-    for (size_t k = 0; k + 1 < kd.size(); ++k)
-      if (kv[k].box > 1) ++rows_dims;
-    if (rows_dims != 1) {
+    for (size_t k = 0; k < kd.size(); ++k) {
+      bx.push_back(kv[k].box);
+      if (k + 1 < kd.size() && kv[k].box > 1) ++rows_dims;
+    }
+    if ((!b_kmajor && rows_dims != 1) || (b_kmajor && !rows_ordered(kd, bx))) {
       *why = "weight brick rows not contiguous";
       return false;
     }
