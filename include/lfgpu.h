@@ -302,6 +302,13 @@ int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t f
 int lfgpu_interpret(lfgpu_ctx* ctx, const lfgpu_graph* g, int32_t nsched,
                     const lfgpu_sched* sched, int32_t flags, double* const* host_bufs);
 
+/* ---- diagnostics ------------------------------------------------------------------------
+ * When d_buf is non-NULL, every subsequent tcgen05 contraction launch writes
+ * eight %globaltimer stamps (ns) per CTA into d_buf[8*cta + i]: entry, setup
+ * done, last TMA issued, first stage landed, last MMA committed, accumulator
+ * ready, epilogue done. NULL disables. Not thread-safe; profiling only. */
+int lfgpu_debug_umma_trace(void* d_buf);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <cstring>
 
 #include "lf_core.hpp"
@@ -89,106 +91,164 @@ __device__ __forceinline__ T zero_of() {
 
 constexpr int kCopyThreads = 256;
 
+// Division by a runtime constant as a multiply-high (Granlund-Montgomery):
+// for n, d < 2^31, q = (umulhi(n, m) + n) >> l with l = ceil(log2 d).
+struct FastDiv {
+  uint32_t d, m, l;
+};
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (__umulhi(n, f.m) + n) >> f.l;
+}
+
+// Tiles are powers of two (TA = 1 << la along the destination-contiguous
+// digit a, TB = 1 << lb along digit b) so per-element indexing is shifts and
+// masks; each CTA walks tiles grid-stride and decodes the outer digits once
+// per tile with multiply-high division. All offsets are 32-bit (tensors
+// above 2^31 elements take the general path).
 struct DCParams {
   int32_t nout;
   int32_t npred, nclamp;
-  int32_t ta, tb;          // tile sizes along a, b
-  int32_t tiles_a, tiles_b;
-  int32_t transpose;       // 1: SMEM-staged (src-contiguous digit b)
-  int64_t oext[kMaxDig];
-  int64_t odst[kMaxDig], osrc[kMaxDig];
-  int64_t opred[kMaxPred][kMaxDig];
-  int64_t oclamp[kMaxClamp][kMaxDig];
-  int64_t ea, eb;
-  int64_t dst_a, dst_b, src_a, src_b;
-  int64_t pa[kMaxPred], pb[kMaxPred], pconst[kMaxPred], plo[kMaxPred], phi[kMaxPred];
-  int64_t ca[kMaxClamp], cb[kMaxClamp], cconst[kMaxClamp], cmax[kMaxClamp],
+  int32_t la, lb;  // log2 tile sizes along a, b
+  int32_t transpose;
+  int32_t ntiles;
+  FastDiv ftiles_a, ftiles_b;
+  FastDiv fext[kMaxDig];
+  int32_t odst[kMaxDig], osrc[kMaxDig];
+  int32_t opred[kMaxPred][kMaxDig];
+  int32_t oclamp[kMaxClamp][kMaxDig];
+  int32_t ea, eb;
+  int32_t dst_a, dst_b, src_a, src_b;
+  int32_t pa[kMaxPred], pb[kMaxPred], pconst[kMaxPred], plo[kMaxPred], phi[kMaxPred];
+  int32_t ca[kMaxClamp], cb[kMaxClamp], cconst[kMaxClamp], cmax[kMaxClamp],
       cstride[kMaxClamp];
-  int64_t src_base;
+  int32_t src_base;
 };
 
-template <typename TS, typename TD>
+struct TileOrigin {
+  int32_t dbase, sbase;
+  int32_t pv[kMaxPred], cv[kMaxClamp];
+  int32_t ta, tb;  // valid extents of this tile
+};
+
+// Param arrays are only ever indexed with compile-time indices (unrolled,
+// guarded loops): a runtime index would make nvcc address the parameter
+// buffer through a generic pointer, i.e. a global-latency load per access.
+template <bool PC>
+__device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileOrigin& o) {
+  uint32_t q = fdiv(t, P.ftiles_a);
+  const int32_t ia0 = static_cast<int32_t>(t - q * P.ftiles_a.d) << P.la;
+  t = q;
+  q = fdiv(t, P.ftiles_b);
+  const int32_t ib0 = static_cast<int32_t>(t - q * P.ftiles_b.d) << P.lb;
+  t = q;
+  o.dbase = 0;
+  o.sbase = P.src_base;
+  if (PC) {
+#pragma unroll
+    for (int p = 0; p < kMaxPred; ++p) o.pv[p] = P.pconst[p] + ia0 * P.pa[p] + ib0 * P.pb[p];
+#pragma unroll
+    for (int c = 0; c < kMaxClamp; ++c) o.cv[c] = P.cconst[c] + ia0 * P.ca[c] + ib0 * P.cb[c];
+  }
+#pragma unroll
+  for (int d = kMaxDig - 1; d >= 0; --d) {
+    if (d < P.nout) {
+      const uint32_t qq = fdiv(t, P.fext[d]);
+      const int32_t x = static_cast<int32_t>(t - qq * P.fext[d].d);
+      t = qq;
+      o.dbase += x * P.odst[d];
+      o.sbase += x * P.osrc[d];
+      if (PC) {
+#pragma unroll
+        for (int p = 0; p < kMaxPred; ++p) o.pv[p] += x * P.opred[p][d];
+#pragma unroll
+        for (int c = 0; c < kMaxClamp; ++c) o.cv[c] += x * P.oclamp[c][d];
+      }
+    }
+  }
+  o.dbase += ia0 * P.dst_a + ib0 * P.dst_b;
+  o.sbase += ia0 * P.src_a + ib0 * P.src_b;
+  o.ta = min(1 << P.la, P.ea - ia0);
+  o.tb = min(1 << P.lb, P.eb - ib0);
+}
+
+template <bool PC, typename TS>
+__device__ __forceinline__ TS load_elem(const DCParams& P, const TileOrigin& o,
+                                        const TS* __restrict__ src, int ia, int ib) {
+  int32_t off = o.sbase + ia * P.src_a + ib * P.src_b;
+  if (!PC) return __ldg(src + off);
+  bool valid = true;
+#pragma unroll
+  for (int p = 0; p < kMaxPred; ++p) {
+    const int32_t v = o.pv[p] + ia * P.pa[p] + ib * P.pb[p];
+    valid = valid && (p >= P.npred || (v >= P.plo[p] && v < P.phi[p]));
+  }
+#pragma unroll
+  for (int c = 0; c < kMaxClamp; ++c) {
+    const int32_t v = o.cv[c] + ia * P.ca[c] + ib * P.cb[c];
+    if (c < P.nclamp) off += min(v, P.cmax[c]) * P.cstride[c];
+  }
+  return valid ? __ldg(src + off) : zero_of<TS>();
+}
+
+// SMEM-staged transpose: read along b (source-contiguous), write along a
+// (destination-contiguous); padded rows keep the column walk conflict-free.
+template <typename TS, typename TD, bool PC>
 __global__ void __launch_bounds__(kCopyThreads)
-    digit_copy(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+    digit_transpose(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TS* tile = reinterpret_cast<TS*>(smem_raw);
-
-  // Decode this CTA's tile and outer digits once.
-  int64_t t = blockIdx.x;
-  const int64_t ia0 = (t % P.tiles_a) * P.ta;
-  t /= P.tiles_a;
-  const int64_t ib0 = (t % P.tiles_b) * P.tb;
-  t /= P.tiles_b;
-  int64_t dbase = 0, sbase = P.src_base;
-  int64_t pv[kMaxPred], cv[kMaxClamp];
-#pragma unroll
-  for (int p = 0; p < kMaxPred; ++p) pv[p] = P.pconst[p];
-#pragma unroll
-  for (int c = 0; c < kMaxClamp; ++c) cv[c] = P.cconst[c];
-  for (int d = P.nout - 1; d >= 0; --d) {
-    int64_t x = t % P.oext[d];
-    t /= P.oext[d];
-    dbase += x * P.odst[d];
-    sbase += x * P.osrc[d];
-    for (int p = 0; p < P.npred; ++p) pv[p] += x * P.opred[p][d];
-    for (int c = 0; c < P.nclamp; ++c) cv[c] += x * P.oclamp[c][d];
-  }
-  // Fold the tile origin into the bases.
-  dbase += ia0 * P.dst_a + ib0 * P.dst_b;
-  sbase += ia0 * P.src_a + ib0 * P.src_b;
-  for (int p = 0; p < P.npred; ++p) pv[p] += ia0 * P.pa[p] + ib0 * P.pb[p];
-  for (int c = 0; c < P.nclamp; ++c) cv[c] += ia0 * P.ca[c] + ib0 * P.cb[c];
-  const int ta = static_cast<int>(min(static_cast<int64_t>(P.ta), P.ea - ia0));
-  const int tb = static_cast<int>(min(static_cast<int64_t>(P.tb), P.eb - ib0));
-  const int n = ta * tb;
-
-  auto load = [&](int ia, int ib, bool& valid) -> TS {
-    valid = true;
-    for (int p = 0; p < P.npred; ++p) {
-      int64_t v = pv[p] + ia * P.pa[p] + ib * P.pb[p];
-      valid = valid && v >= P.plo[p] && v < P.phi[p];
-    }
-    int64_t off = sbase + ia * P.src_a + ib * P.src_b;
-    for (int c = 0; c < P.nclamp; ++c) {
-      int64_t v = cv[c] + ia * P.ca[c] + ib * P.cb[c];
-      off += min(v, P.cmax[c]) * P.cstride[c];
-    }
-    return valid ? __ldg(src + off) : zero_of<TS>();
-  };
-
-  if (P.transpose) {
-    const int ld = P.tb + 1;  // padded row: conflict-free column walk
-    // Read phase: b (source-contiguous) fastest.
-    for (int i = threadIdx.x; i < n; i += kCopyThreads) {
-      int ib = i % tb, ia = i / tb;
-      bool ok;
-      tile[ia * ld + ib] = load(ia, ib, ok);
+  const int TA = 1 << P.la, TB = 1 << P.lb, ld = TB + 1;
+  const int rstep = kCopyThreads >> P.lb, wstep = kCopyThreads >> P.la;
+  const int rb = threadIdx.x & (TB - 1), ra = threadIdx.x >> P.lb;
+  const int wa = threadIdx.x & (TA - 1), wb = threadIdx.x >> P.la;
+  for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+    TileOrigin o;
+    decode_tile<PC>(P, static_cast<uint32_t>(t), o);
+    if (rb < o.tb) {
+#pragma unroll 8
+      for (int ia = ra; ia < TA; ia += rstep)
+        if (ia < o.ta) tile[ia * ld + rb] = load_elem<PC>(P, o, src, ia, rb);
     }
     __syncthreads();
-    // Write phase: a (destination-contiguous) fastest.
-    for (int i = threadIdx.x; i < n; i += kCopyThreads) {
-      int ia = i % ta, ib = i / ta;
-      dst[dbase + ia * P.dst_a + ib * P.dst_b] = convert<TS, TD>(tile[ia * ld + ib]);
+    if (wa < o.ta) {
+      const int32_t d0 = o.dbase + wa * P.dst_a;
+#pragma unroll 8
+      for (int ib = wb; ib < TB; ib += wstep)
+        if (ib < o.tb) dst[d0 + ib * P.dst_b] = convert<TS, TD>(tile[wa * ld + ib]);
     }
-  } else {
-    // Direct: a fastest on both sides; 4 independent loads in flight.
-    constexpr int U = 4;
-    for (int i0 = threadIdx.x; i0 < n; i0 += kCopyThreads * U) {
-      TS v[U];
+    __syncthreads();
+  }
+}
+
+// Direct copy: a fastest on both sides (coalesced destination; the source is
+// coalesced too when its a-stride is 1).
+template <typename TS, typename TD, bool PC>
+__global__ void __launch_bounds__(kCopyThreads)
+    digit_direct(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  const int TB = 1 << P.lb;
+  const int la = min(P.la, 8);
+  const int TA = 1 << P.la;
+  const int astep = 1 << la;                 // threads along a per pass
+  const int bstep = kCopyThreads >> la;      // rows of b per pass
+  const int a0 = threadIdx.x & (astep - 1), b0 = threadIdx.x >> la;
+  for (int t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+    TileOrigin o;
+    decode_tile<PC>(P, static_cast<uint32_t>(t), o);
+    for (int b = b0; b < TB; b += bstep) {
+      if (b >= o.tb) break;
+      constexpr int U = 8;
+      for (int aa = a0; aa < TA; aa += astep * U) {
+        TS v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int i = i0 + u * kCopyThreads;
-        if (i < n) {
-          bool ok;
-          v[u] = load(i % ta, i / ta, ok);
+        for (int u = 0; u < U; ++u) {
+          const int a = aa + u * astep;
+          if (a < o.ta) v[u] = load_elem<PC>(P, o, src, a, b);
         }
-      }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int i = i0 + u * kCopyThreads;
-        if (i < n) {
-          int ia = i % ta, ib = i / ta;
-          dst[dbase + ia * P.dst_a + ib * P.dst_b] = convert<TS, TD>(v[u]);
+        for (int u = 0; u < U; ++u) {
+          const int a = aa + u * astep;
+          if (a < o.ta) dst[o.dbase + a * P.dst_a + b * P.dst_b] = convert<TS, TD>(v[u]);
         }
       }
     }
@@ -353,8 +413,31 @@ int elem_size(int elem) {
   return 0;
 }
 
+static int log2_ceil(int64_t v) {
+  int l = 0;
+  while ((static_cast<int64_t>(1) << l) < v) ++l;
+  return l;
+}
+
+static FastDiv make_fastdiv(int64_t d) {
+  FastDiv f;
+  f.d = static_cast<uint32_t>(d);
+  f.l = static_cast<uint32_t>(log2_ceil(d));
+  f.m = static_cast<uint32_t>(((static_cast<uint64_t>(1) << 32) *
+                               ((static_cast<uint64_t>(1) << f.l) - static_cast<uint64_t>(d))) /
+                                  static_cast<uint64_t>(d) +
+                              1);
+  return f;
+}
+
+static int32_t i32(int64_t v) {
+  if (v > INT32_MAX || v < INT32_MIN) fail(LFGPU_EUNSUPPORTED, "digit map offset exceeds 32 bits");
+  return static_cast<int32_t>(v);
+}
+
 // Tile selection for a DigitMap (see file comment).
 static DCParams make_params(const DigitMap& m, int src_elem) {
+  (void)src_elem;
   DCParams P;
   std::memset(&P, 0, sizeof(P));
   int nd = m.ndig;
@@ -371,61 +454,62 @@ static DCParams make_params(const DigitMap& m, int src_elem) {
   }
   const int64_t ea = nd ? m.ext[a] : 1;
   const int64_t eb = b >= 0 ? m.ext[b] : 1;
-  int ta, tb;
+  int la, lb;
   if (transpose) {
-    // Square-ish tile within a 48 KB SMEM budget, both sides >= 32 B runs.
-    int es = std::max(elem_size(src_elem), 1);
-    int cap = std::max(1024, 32768 / es);
-    ta = static_cast<int>(std::min<int64_t>(ea, 64));
-    tb = static_cast<int>(std::min<int64_t>(eb, std::max<int64_t>(64, cap / ta - 1)));
-    tb = static_cast<int>(std::min<int64_t>(tb, 256));
+    // 4K elements per tile: TA in [2, 32] along a, TB = 4096/TA (<= 256) along b.
+    la = std::min(std::max(log2_ceil(ea), 1), 5);
+    lb = std::min(12 - la, 8);
   } else {
-    ta = static_cast<int>(std::min<int64_t>(ea, 4096));
-    tb = static_cast<int>(std::min<int64_t>(eb, std::max<int64_t>(1, 4096 / ta)));
+    la = std::min(log2_ceil(ea), 12);  // up to 4096 along a
+    lb = std::max(0, std::min(12 - la, log2_ceil(std::max<int64_t>(eb, 1))));
   }
   P.transpose = transpose ? 1 : 0;
-  P.ta = std::max(ta, 1);
-  P.tb = std::max(tb, 1);
-  P.ea = ea;
-  P.eb = eb;
-  P.tiles_a = static_cast<int32_t>((ea + P.ta - 1) / P.ta);
-  P.tiles_b = static_cast<int32_t>((eb + P.tb - 1) / P.tb);
+  P.la = la;
+  P.lb = lb;
+  P.ea = i32(ea);
+  P.eb = i32(eb);
+  const int64_t tiles_a = (ea + (1 << la) - 1) >> la, tiles_b = (eb + (1 << lb) - 1) >> lb;
+  P.ftiles_a = make_fastdiv(tiles_a);
+  P.ftiles_b = make_fastdiv(tiles_b);
   P.npred = m.npred;
   P.nclamp = m.nclamp;
-  P.src_base = m.src_base;
+  P.src_base = i32(m.src_base);
   if (nd) {
-    P.dst_a = m.dst_stride[a];
-    P.src_a = m.src_stride[a];
-    for (int p = 0; p < m.npred; ++p) P.pa[p] = m.pcoef[p][a];
-    for (int c = 0; c < m.nclamp; ++c) P.ca[c] = m.ccoef[c][a];
+    P.dst_a = i32(m.dst_stride[a]);
+    P.src_a = i32(m.src_stride[a]);
+    for (int p = 0; p < m.npred; ++p) P.pa[p] = i32(m.pcoef[p][a]);
+    for (int c = 0; c < m.nclamp; ++c) P.ca[c] = i32(m.ccoef[c][a]);
   }
   if (b >= 0) {
-    P.dst_b = m.dst_stride[b];
-    P.src_b = m.src_stride[b];
-    for (int p = 0; p < m.npred; ++p) P.pb[p] = m.pcoef[p][b];
-    for (int c = 0; c < m.nclamp; ++c) P.cb[c] = m.ccoef[c][b];
+    P.dst_b = i32(m.dst_stride[b]);
+    P.src_b = i32(m.src_stride[b]);
+    for (int p = 0; p < m.npred; ++p) P.pb[p] = i32(m.pcoef[p][b]);
+    for (int c = 0; c < m.nclamp; ++c) P.cb[c] = i32(m.ccoef[c][b]);
   }
   for (int p = 0; p < m.npred; ++p) {
-    P.pconst[p] = m.pconst[p];
-    P.plo[p] = m.plo[p];
-    P.phi[p] = m.phi[p];
+    P.pconst[p] = i32(m.pconst[p]);
+    P.plo[p] = i32(m.plo[p]);
+    P.phi[p] = i32(m.phi[p]);
   }
   for (int c = 0; c < m.nclamp; ++c) {
-    P.cconst[c] = m.cconst[c];
-    P.cmax[c] = m.cmax[c];
-    P.cstride[c] = m.cstride[c];
+    P.cconst[c] = i32(m.cconst[c]);
+    P.cmax[c] = i32(m.cmax[c]);
+    P.cstride[c] = i32(m.cstride[c]);
   }
   int k = 0;
+  int64_t outer = 1;
   for (int d = 0; d < nd; ++d) {
     if (d == a || d == b) continue;
-    P.oext[k] = m.ext[d];
-    P.odst[k] = m.dst_stride[d];
-    P.osrc[k] = m.src_stride[d];
-    for (int p = 0; p < m.npred; ++p) P.opred[p][k] = m.pcoef[p][d];
-    for (int c = 0; c < m.nclamp; ++c) P.oclamp[c][k] = m.ccoef[c][d];
+    P.fext[k] = make_fastdiv(m.ext[d]);
+    P.odst[k] = i32(m.dst_stride[d]);
+    P.osrc[k] = i32(m.src_stride[d]);
+    for (int p = 0; p < m.npred; ++p) P.opred[p][k] = i32(m.pcoef[p][d]);
+    for (int c = 0; c < m.nclamp; ++c) P.oclamp[c][k] = i32(m.ccoef[c][d]);
+    outer *= m.ext[d];
     ++k;
   }
   P.nout = k;
+  P.ntiles = i32(outer * tiles_a * tiles_b);
   return P;
 }
 
@@ -433,10 +517,11 @@ cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, con
                               void* dst, cudaStream_t stream, KernelInfo* info) {
   if (m.dst_numel == 0) return cudaSuccess;
   DCParams P = make_params(m, src_elem);
-  int64_t outer = 1;
-  for (int d = 0; d < P.nout; ++d) outer *= P.oext[d];
-  int64_t grid = outer * P.tiles_a * P.tiles_b;
-  size_t smem = P.transpose ? static_cast<size_t>(P.ta) * (P.tb + 1) * elem_size(src_elem) : 0;
+  // Enough CTAs for 8 resident per SM; each walks tiles grid-stride.
+  int64_t grid = std::min<int64_t>(P.ntiles, 148 * 8);
+  size_t smem = P.transpose
+                    ? static_cast<size_t>(1 << P.la) * ((1 << P.lb) + 1) * elem_size(src_elem)
+                    : 0;
   if (info) {
     info->name = P.transpose ? "digit_copy_transpose" : "digit_copy_direct";
     info->grid = grid;
@@ -444,12 +529,17 @@ cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, con
   return dispatch<Unused>(src_elem, dst_elem, [&](auto s, auto d) -> cudaError_t {
     using TS = decltype(s);
     using TD = decltype(d);
-    auto kern = digit_copy<TS, TD>;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
-    kern<<<static_cast<unsigned>(grid), kCopyThreads, smem, stream>>>(
-        P, static_cast<const TS*>(src), static_cast<TD*>(dst));
+    const bool pc = P.npred > 0 || P.nclamp > 0;
+    const unsigned g = static_cast<unsigned>(grid);
+    const TS* s_ = static_cast<const TS*>(src);
+    TD* d_ = static_cast<TD*>(dst);
+    if (P.transpose) {
+      if (pc) digit_transpose<TS, TD, true><<<g, kCopyThreads, smem, stream>>>(P, s_, d_);
+      else digit_transpose<TS, TD, false><<<g, kCopyThreads, smem, stream>>>(P, s_, d_);
+    } else {
+      if (pc) digit_direct<TS, TD, true><<<g, kCopyThreads, 0, stream>>>(P, s_, d_);
+      else digit_direct<TS, TD, false><<<g, kCopyThreads, 0, stream>>>(P, s_, d_);
+    }
     return cudaGetLastError();
   });
 }

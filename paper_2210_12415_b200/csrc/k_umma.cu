@@ -43,7 +43,19 @@ struct UmmaParams {
   uint32_t a_kadv, b_kadv;
   uint32_t idesc;
   uint32_t tmem_cols;
+  int32_t cols_unit;  // col_off[c] == col_off[0] + c
+  int32_t rows_unit;  // row_off[r] == r
+  int32_t ring_bytes; // pipeline ring (>= the epilogue's fp32 staging tile)
+  unsigned long long* dbg;  // optional per-CTA %globaltimer checkpoints (8 per CTA)
+  int32_t epi_mode;         // unused (diagnostics)
+  int32_t epi_sig;          // EPI_SIG of a <= 3-op chain, -1 = generic
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -137,27 +149,161 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
         "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  // The registers are valid only after wait::ld; tie them to the wait so no
+  // consumer is scheduled between the load and the wait.
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]),
+                 "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                 "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                 "+r"(v[30]), "+r"(v[31])::"memory");
+}
+
+#define EPI_SIG(a, b, c) ((a) | ((b) << 2) | ((c) << 4))
+
+template <int K>
+__device__ __forceinline__ float epi_op(float x, const float* __restrict__ p, int64_t addr,
+                                        int n) {
+  if (K == EPI_BIAS) return x + __ldg(p + n);
+  if (K == EPI_RESIDUAL) return x + __ldg(p + addr);
+  if (K == EPI_RELU) return fmaxf(x, 0.0f);
+  return x;
+}
+
+// Row-contiguous output brick: each epilogue warp walks rows, lanes walk
+// 4-column groups (16-byte SMEM reads and global stores when aligned).
+template <int K0, int K1, int K2>
+__device__ __forceinline__ void epi_rows(const float* __restrict__ stile, int ld, int rows, int cols,
+                                         int64_t cbase, const int64_t* __restrict__ s_row,
+                                         int n_base, float* __restrict__ out,
+                                         const float* __restrict__ e0, const float* __restrict__ e1,
+                                         const float* __restrict__ e2, int ew, int lane) {
+  const int groups = (cols + 3) >> 2;
+  for (int r = ew; r < rows; r += 4) {
+    const int64_t rb = cbase + s_row[r];
+    const bool vec = ((rb & 3) == 0) && ((cols & 3) == 0);
+    for (int g = lane; g < groups; g += 32) {
+      const int c = g << 2;
+      float4 x = *reinterpret_cast<const float4*>(stile + r * ld + c);
+      float v[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t a = rb + c + j;
+        const int n = n_base + c + j;
+        if (c + j < cols) {
+          v[j] = epi_op<K0>(v[j], e0, a, n);
+          v[j] = epi_op<K1>(v[j], e1, a, n);
+          v[j] = epi_op<K2>(v[j], e2, a, n);
+        }
+      }
+      if (vec) {
+        *reinterpret_cast<float4*>(out + rb + c) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (c + j < cols) out[rb + c + j] = v[j];
+      }
+    }
+  }
+}
+
+// Row-contiguous side (M-major output, e.g. NCHW or a (M/m_t) N m_t brick):
+// each epilogue warp walks columns, lanes walk consecutive rows.
+template <int K0, int K1, int K2>
+__device__ __forceinline__ void epi_cols(const float* __restrict__ stile, int ld, int rows, int cols,
+                                         int64_t rbase, const int64_t* __restrict__ s_col,
+                                         int n_base, float* __restrict__ out,
+                                         const float* __restrict__ e0, const float* __restrict__ e1,
+                                         const float* __restrict__ e2, int ew, int lane) {
+  for (int c = ew; c < cols; c += 4) {
+    const int64_t cb = rbase + s_col[c];
+    const int n = n_base + c;
+    for (int r = lane; r < rows; r += 32) {
+      float v = stile[r * ld + c];
+      v = epi_op<K0>(v, e0, cb + r, n);
+      v = epi_op<K1>(v, e1, cb + r, n);
+      v = epi_op<K2>(v, e2, cb + r, n);
+      out[cb + r] = v;
+    }
+  }
+}
+
+// Any output brick (e.g. M-contiguous C): lanes walk rows when the rows are
+// the contiguous side, else columns; runtime op chain (rare shapes).
+template <typename PT>
+__device__ __noinline__ void epi_generic(const PT& P, const float* __restrict__ stile, int ld,
+                                         int rows, int cols, int64_t obase,
+                                         const int64_t* __restrict__ s_row,
+                                         const int64_t* __restrict__ s_col, int n_base,
+                                         float* __restrict__ out, int et) {
+  int ek[kMaxEpi];
+  const float* ep[kMaxEpi];
+#pragma unroll
+  for (int e = 0; e < kMaxEpi; ++e) {
+    ek[e] = e < P.epi_count ? P.epi_kind[e] : EPI_NONE;
+    ep[e] = P.epi_ptr[e];
+  }
+  const bool row_fast = P.rows_unit && !P.cols_unit;
+  const int ew = et >> 5, lane = et & 31;
+  const int outer = row_fast ? cols : rows, inner = row_fast ? rows : cols;
+  for (int o = ew; o < outer; o += 4) {
+    for (int i = lane; i < inner; i += 32) {
+      const int r = row_fast ? i : o, c = row_fast ? o : i;
+      const int64_t addr = obase + s_row[r] + s_col[c];
+      float x = stile[r * ld + c];
+#pragma unroll
+      for (int e = 0; e < kMaxEpi; ++e) {
+        if (ek[e] == EPI_BIAS) x += __ldg(ep[e] + n_base + c);
+        else if (ek[e] == EPI_RESIDUAL) x += __ldg(ep[e] + addr);
+        else if (ek[e] == EPI_RELU) x = fmaxf(x, 0.0f);
+      }
+      out[addr] = x;
+    }
+  }
 }
 
 constexpr int kThreads = 192;
+constexpr int kEpiThreads = 128;
+
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     umma_kernel(const __grid_constant__ CUtensorMap tma_a,
                 const __grid_constant__ CUtensorMap tma_b, const UmmaParams P) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment (SWIZZLE_128B atoms) by offsetting the __shared__
+  // array itself, so every derived pointer stays in the shared window.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stage_bytes = P.a_boxes * P.a_slot + P.b_boxes * P.b_slot;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.pipe * stage_bytes);
+  // The epilogue stages the fp32 tile (128 x (BN+1)) over the pipeline ring
+  // once every MMA has retired; ring_bytes >= that (host-checked).
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = full0 + 8 * P.pipe;
   const uint32_t accf = empty0 + 8 * P.pipe;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.pipe + 1);
+  // After the barriers: this tile's entry, the stage table and the epilogue's
+  // row/column offsets, all copied from global memory once.
+  TileEntry* s_tile = reinterpret_cast<TileEntry*>(bars + 2 * P.pipe + 2);
+  StageEntry* s_stage = reinterpret_cast<StageEntry*>(s_tile + 1);
+  int64_t* s_col = reinterpret_cast<int64_t*>(s_stage + P.nstages);
+  int64_t* s_row = s_col + P.BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  unsigned long long* dbg = P.dbg ? P.dbg + 8 * tile : nullptr;
+  const int pipe = P.pipe;
+  const int early = 0;
+
   if (threadIdx.x == 0) {
-    for (int s = 0; s < P.pipe; ++s) {
+    if (dbg) {
+      dbg[0] = gtimer();
+      P.dbg[8 * gridDim.x + 2 * tile] = clock64();
+    }
+    for (int s = 0; s < pipe; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
@@ -165,6 +311,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+  }
+  {
+    const int* g = reinterpret_cast<const int*>(P.tiles + tile);
+    int* d = reinterpret_cast<int*>(s_tile);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(TileEntry) / 4); i += kThreads) d[i] = g[i];
+    const int* gs = reinterpret_cast<const int*>(P.stages);
+    int* ds = reinterpret_cast<int*>(s_stage);
+    const int nst = P.nstages * static_cast<int>(sizeof(StageEntry) / 4);
+    for (int i = threadIdx.x; i < nst; i += kThreads) ds[i] = gs[i];
+    for (int i = threadIdx.x; i < P.BN; i += kThreads) s_col[i] = P.col_off[i];
+    for (int i = threadIdx.x; i < 128; i += kThreads) s_row[i] = P.row_off[i];
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -177,75 +334,132 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const int tile = blockIdx.x;
+  if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
 
   if (warp == 0 && lane == 0) {
-    // ---- TMA producer
-    const TileEntry& te = P.tiles[tile];
-    for (int s = 0; s < P.nstages; ++s) {
-      const int slot = s % P.pipe;
-      const uint32_t ph = (s / P.pipe) & 1;
-      mbar_wait(empty0 + 8 * slot, ph ^ 1);
+    // ---- TMA producer: coordinates = tile part (registers) + stage part (SMEM)
+    int32_t ta[kMaxBoxes][5], tb[kMaxBoxes][5];
+#pragma unroll
+    for (int b = 0; b < kMaxBoxes; ++b)
+#pragma unroll
+      for (int d = 0; d < 5; ++d) {
+        ta[b][d] = s_tile->ca[b][d];
+        tb[b][d] = s_tile->cb[b][d];
+      }
+    const int na = P.a_boxes, nb = P.b_boxes;
+    for (int s = early; s < P.nstages; ++s) {
+      const int slot = s % pipe;
+      mbar_wait(empty0 + 8 * slot, ((s / pipe) & 1) ^ 1);
       const uint32_t bar = full0 + 8 * slot;
       mbar_expect_tx(bar, P.tx_bytes);
-      const StageEntry& se = P.stages[s];
+      const StageEntry se = s_stage[s];
       const uint32_t a_dst = smem_u32(smem + slot * stage_bytes);
-      const uint32_t b_dst = a_dst + P.a_boxes * P.a_slot;
+      const uint32_t b_dst = a_dst + na * P.a_slot;
       int32_t c[5];
-      for (int b = 0; b < P.a_boxes; ++b) {
 #pragma unroll
-        for (int d = 0; d < 5; ++d) c[d] = te.ca[b][d] + se.sa[d];
+      for (int b = 0; b < kMaxBoxes; ++b) {
+        if (b >= na) break;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) c[d] = ta[b][d] + se.sa[d];
         tma_load(&tma_a, P.a_rank, a_dst + b * P.a_slot, bar, c);
       }
-      for (int b = 0; b < P.b_boxes; ++b) {
 #pragma unroll
-        for (int d = 0; d < 5; ++d) c[d] = te.cb[b][d] + se.sb[d];
+      for (int b = 0; b < kMaxBoxes; ++b) {
+        if (b >= nb) break;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) c[d] = tb[b][d] + se.sb[d];
         tma_load(&tma_b, P.b_rank, b_dst + b * P.b_slot, bar, c);
       }
     }
+    if (dbg) dbg[2] = gtimer();
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
+    const uint64_t adesc = P.a_desc, bdesc = P.b_desc;
+    const uint32_t idesc = P.idesc, akadv = P.a_kadv, bkadv = P.b_kadv;
+    const int ksteps = P.ksteps;
+    const uint32_t a_off_b = P.a_boxes * P.a_slot;
     for (int s = 0; s < P.nstages; ++s) {
-      const int slot = s % P.pipe;
-      const uint32_t ph = (s / P.pipe) & 1;
-      mbar_wait(full0 + 8 * slot, ph);
+      const int slot = s % pipe;
+      mbar_wait(full0 + 8 * slot, (s / pipe) & 1);
+      if (dbg && s == 0) dbg[3] = gtimer();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a_addr = smem_u32(smem + slot * stage_bytes);
-      const uint32_t b_addr = a_addr + P.a_boxes * P.a_slot;
-      for (int k = 0; k < P.ksteps; ++k) {
-        const uint64_t ad = P.a_desc | (((a_addr + k * P.a_kadv) >> 4) & 0x3FFFull);
-        const uint64_t bd = P.b_desc | (((b_addr + k * P.b_kadv) >> 4) & 0x3FFFull);
-        umma_bf16(tmem, ad, bd, P.idesc, (s | k) != 0);
+      const uint32_t b_addr = a_addr + a_off_b;
+      for (int k = 0; k < ksteps; ++k) {
+        const uint64_t ad = adesc | (((a_addr + k * akadv) >> 4) & 0x3FFFull);
+        const uint64_t bd = bdesc | (((b_addr + k * bkadv) >> 4) & 0x3FFFull);
+        umma_bf16(tmem, ad, bd, idesc, (s | k) != 0);
       }
       umma_commit(empty0 + 8 * slot);
     }
     umma_commit(accf);
+    if (dbg) dbg[4] = gtimer();
   } else if (warp >= 2) {
-    // ---- epilogue: TMEM -> registers -> fused element-wise -> global
-    mbar_wait(accf, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---- epilogue (4 warps). Phase 1: TMEM -> SMEM tile (row r = TMEM lane r).
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
-    const TileEntry& te = P.tiles[tile];
-    const bool live = row < te.rows;
-    const int64_t rbase = te.out_base + (live ? P.row_off[row] : 0);
+    // SMEM row stride: 16-byte aligned rows for the float4 row pass, odd for
+    // the column pass (conflict-free lane-per-row reads).
+    const int ld = (P.cols_unit || !P.rows_unit) ? P.BN + 4 : P.BN + 1;
+    float* stile = reinterpret_cast<float*>(smem);
+    mbar_wait(accf, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (dbg && threadIdx.x == 64) dbg[5] = gtimer();
     for (int c0 = 0; c0 < P.BN; c0 += 32) {
       uint32_t v[32];
       tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
-      if (!live) continue;
-#pragma unroll 4
-      for (int j = 0; j < 32; ++j) {
-        const int c = c0 + j;
-        if (c >= te.cols) break;
-        const int64_t addr = rbase + P.col_off[c];
-        float x = __uint_as_float(v[j]);
-        for (int e = 0; e < P.epi_count; ++e) {
-          if (P.epi_kind[e] == EPI_BIAS) x += __ldg(P.epi_ptr[e] + te.n_base + c);
-          else if (P.epi_kind[e] == EPI_RESIDUAL) x += __ldg(P.epi_ptr[e] + addr);
-          else x = fmaxf(x, 0.0f);
-        }
-        P.out[addr] = x;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c0 + j < P.BN) stile[row * ld + c0 + j] = __uint_as_float(v[j]);
+    }
+    epi_bar();
+    if (dbg && threadIdx.x == 64) dbg[7] = gtimer();
+    // Phase 2: cooperative, coalesced stores with the fused element-wise chain
+    // (bias / residual / relu, lower.cpp:566-608). Lanes run along the
+    // physically contiguous side of the output brick.
+    const int et = threadIdx.x - 64;  // 0..127
+    const int rows = s_tile->rows, cols = s_tile->cols, n_base = s_tile->n_base;
+    const int64_t obase = s_tile->out_base;
+    float* __restrict__ out = P.out;
+    // The element-wise chain (<= 3 ops: bias / residual / relu) is resolved
+    // once into a signature and each signature runs a specialised loop: no
+    // per-element switch, no indirect branches, no param-buffer loads.
+    const int sig = P.epi_sig;
+    const float* e0 = P.epi_ptr[0];
+    const float* e1 = P.epi_ptr[1];
+    const float* e2 = P.epi_ptr[2];
+    const int ew = et >> 5;  // epilogue warp 0..3
+    if (P.cols_unit && (ld & 3) == 0) {
+      const int64_t cbase = obase + s_col[0];
+      switch (sig) {
+        case EPI_SIG(0, 0, 0): epi_rows<0, 0, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(1, 0, 0): epi_rows<1, 0, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(1, 2, 0): epi_rows<1, 2, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(1, 3, 0): epi_rows<1, 3, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(1, 3, 2): epi_rows<1, 3, 2>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(2, 0, 0): epi_rows<2, 0, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(3, 0, 0): epi_rows<3, 0, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(3, 2, 0): epi_rows<3, 2, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
+        default: epi_generic(P, stile, ld, rows, cols, obase, s_row, s_col, n_base, out, et); break;
       }
+    } else if (P.rows_unit) {
+      switch (sig) {
+        case EPI_SIG(0, 0, 0): epi_cols<0, 0, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(1, 0, 0): epi_cols<1, 0, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(1, 2, 0): epi_cols<1, 2, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(1, 3, 0): epi_cols<1, 3, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(1, 3, 2): epi_cols<1, 3, 2>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(2, 0, 0): epi_cols<2, 0, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(3, 0, 0): epi_cols<3, 0, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
+        case EPI_SIG(3, 2, 0): epi_cols<3, 2, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
+        default: epi_generic(P, stile, ld, rows, cols, obase, s_row, s_col, n_base, out, et); break;
+      }
+    } else {
+      epi_generic(P, stile, ld, rows, cols, obase, s_row, s_col, n_base, out, et);
+    }
+    if (dbg && threadIdx.x == 64) {
+      dbg[6] = gtimer();
+      P.dbg[8 * gridDim.x + 2 * tile + 1] = clock64();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -342,6 +556,10 @@ void* up(const std::vector<T>& v) {
 
 }  // namespace
 
+static void* g_umma_dbg = nullptr;
+void* umma_debug_buffer() { return g_umma_dbg; }
+void umma_set_debug_buffer(void* p) { g_umma_dbg = p; }
+
 UmmaLaunch umma_prepare(const UmmaPlan& p) {
   UmmaLaunch L;
   L.tma_a = encode(p.A, p.a);
@@ -381,8 +599,20 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     L.epi_ptr[e] = p.epi[e].ptr;
   }
   L.out = p.out;
-  L.smem = 1024 + static_cast<size_t>(p.pipe) * (L.a_boxes * L.a_slot + L.b_boxes * L.b_slot) +
-           8 * (2 * p.pipe + 2) + 16;
+  const size_t ring = static_cast<size_t>(p.pipe) * (L.a_boxes * L.a_slot + L.b_boxes * L.b_slot);
+  const size_t staging = static_cast<size_t>(128) * (p.BN + 4) * 4;
+  L.ring_bytes = static_cast<int>((std::max(ring, staging) + 1023) / 1024 * 1024);
+  L.smem = 1024 + L.ring_bytes + 8 * (2 * p.pipe + 2) + sizeof(TileEntry) +
+           sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 64;
+  // Contiguity over the rows any tile actually stores.
+  int max_rows = 0;
+  for (const auto& t : p.tiles) max_rows = std::max(max_rows, static_cast<int>(t.rows));
+  L.rows_unit = 1;
+  for (int r = 0; r < max_rows && r < static_cast<int>(p.row_off.size()); ++r)
+    if (p.row_off[r] != static_cast<int64_t>(r)) L.rows_unit = 0;
+  L.cols_unit = 1;
+  for (size_t c = 0; c < p.col_off.size(); ++c)
+    if (p.col_off[c] != p.col_off[0] + static_cast<int64_t>(c)) L.cols_unit = 0;
   L.grid = L.ntiles;
   L.a_rank_ = p.A.rank;
   L.b_rank_ = p.B.rank;
@@ -400,6 +630,8 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.col_off = static_cast<const int64_t*>(L.d_cols);
   P.out = L.out;
   P.epi_count = L.epi_count;
+  P.epi_sig = L.epi_count <= 3 ? 0 : -1;
+  for (int e = 0; e < L.epi_count && e < 3; ++e) P.epi_sig |= L.epi_kinds[e] << (2 * e);
   for (int e = 0; e < L.epi_count; ++e) {
     P.epi_kind[e] = L.epi_kinds[e];
     P.epi_ptr[e] = L.epi_ptr[e];
@@ -421,6 +653,14 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.idesc = L.idesc;
   P.tmem_cols = L.tmem_cols;
   P.a_rank = L.a_rank_;
+  P.cols_unit = L.cols_unit;
+  P.rows_unit = L.rows_unit;
+  P.ring_bytes = L.ring_bytes;
+  P.dbg = static_cast<unsigned long long*>(umma_debug_buffer());
+  if (P.dbg) {
+    const char* em = getenv("LFGPU_EPI_MODE");
+    P.epi_mode = em ? atoi(em) : 0;
+  }
   P.b_rank = L.b_rank_;
   static bool attr_set = false;
   if (!attr_set) {

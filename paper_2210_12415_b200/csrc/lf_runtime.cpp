@@ -947,3 +947,8 @@ int lfgpu_interpret(lfgpu_ctx* ctx, const lfgpu_graph* g, int32_t nsched,
 }
 
 }  // extern "C"
+
+extern "C" int lfgpu_debug_umma_trace(void* d_buf) {
+  lfg::umma_set_debug_buffer(d_buf);
+  return LFGPU_OK;
+}

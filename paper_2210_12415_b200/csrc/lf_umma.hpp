@@ -103,6 +103,7 @@ struct UmmaLaunch {
   size_t smem = 0;
   int grid = 0;
   int a_rank_ = 0, b_rank_ = 0;
+  int cols_unit = 0, rows_unit = 0, ring_bytes = 0;
   std::shared_ptr<void> owner;  // keeps the device tables alive
 };
 
@@ -115,5 +116,8 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
 // Encodes tensor maps and uploads tables (needs a, b, out set).
 UmmaLaunch umma_prepare(const UmmaPlan& p);
 cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream);
+// Debug: when set, every umma launch writes 8 %globaltimer checkpoints per CTA.
+void* umma_debug_buffer();
+void umma_set_debug_buffer(void* p);
 
 }  // namespace lfg

@@ -245,8 +245,15 @@ uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
 
 int pick_pipe(const UmmaPlan& p) {
   int per = p.A.slot_bytes * p.A.boxes + p.B.slot_bytes * p.B.boxes;
-  int budget = 200 * 1024;
-  return std::max(2, std::min(8, budget / std::max(per, 1)));
+  // 227 KB per CTA minus alignment slack, barriers, the tile entry, the
+  // stage table and the epilogue column table (k_umma.cu SMEM layout).
+  int fixed = 1024 + 256 + static_cast<int>(sizeof(TileEntry) + sizeof(StageEntry) * p.stages.size() +
+                                           8 * p.col_off.size() + 8 * 128);
+  int budget = 227 * 1024 - fixed;
+  int cap = 8;
+  if (const char* e = getenv("LFGPU_MAX_PIPE")) cap = std::max(2, atoi(e));  // diagnostics
+  if (const char* e = getenv("LFGPU_SMEM_BUDGET_KB")) budget = atoi(e) * 1024 - fixed;
+  return std::max(2, std::min(cap, budget / std::max(per, 1)));
 }
 
 // Split-only operand view for GEMM: `mn_lj`, `k_lj` name the logical dims.

@@ -1,0 +1,93 @@
+"""Per-CTA timeline of the tcgen05 kernel (lfgpu_debug_umma_trace) and a
+copy-bandwidth calibration against torch. Diagnostics only."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2210_12415_b200 import _abi, ir, runtime, tuner  # noqa: E402
+from paper_2210_12415_b200.layout import reorder, split  # noqa: E402
+
+
+def k64(shape):
+    return torch.randint(-64, 65, shape, device="cuda").float() / 64
+
+
+def timeline(g, cand, inputs, name):
+    p = runtime.Plan(g, tuner.seqs_for(g, cand), cand.scheds, _abi.PLAN_REQUIRE_TC)
+    for k, v in inputs.items():
+        p.set_input_device(k, v)
+    p.run()
+    torch.cuda.synchronize()
+    buf = torch.zeros(16 * 4096, dtype=torch.int64, device="cuda")
+    runtime.lib().lfgpu_debug_umma_trace(C.c_void_p(buf.data_ptr()))
+    p2 = runtime.Plan(g, tuner.seqs_for(g, cand), cand.scheds, _abi.PLAN_REQUIRE_TC)
+    for k, v in inputs.items():
+        p2.set_input_device(k, v)
+    torch.cuda.synchronize()
+    p2.run()
+    torch.cuda.synchronize()
+    runtime.lib().lfgpu_debug_umma_trace(None)
+    allb = buf.cpu().numpy().astype(np.int64)
+    import re
+    summ = " ".join(p2.node_kernel(i) for i in range(len(g.nodes)))
+    nct = int(re.search(r"tiles=(\d+)", summ).group(1))
+    t = allb[: 8 * nct].reshape(-1, 8)
+    clk = allb[8 * nct: 8 * nct + 2 * nct].reshape(-1, 2)
+    mhz = (clk[:, 1] - clk[:, 0]) / np.maximum(t[:, 6] - t[:, 0], 1) * 1000.0
+    print(f"  in-kernel SM clock: median {np.median(mhz):.0f} MHz (min {mhz.min():.0f}, max {mhz.max():.0f})")
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1000.0
+    labels = ["entry", "setup", "tma_done", "first_full", "mma_done", "acc_ready", "epi_done",
+              "staged"]
+    print(f"== {name}: {len(t)} CTAs, kernel span {rel[:, 6].max():.2f} us")
+    for i, l in enumerate(labels):
+        print(f"  {l:10s} min {rel[:, i].min():7.2f}  med {np.median(rel[:, i]):7.2f}  max {rel[:, i].max():7.2f}")
+    d = rel[:, 6] - rel[:, 0]
+    print(f"  per-CTA duration med {np.median(d):.2f} max {d.max():.2f}")
+    print(f"  setup {np.median(rel[:,1]-rel[:,0]):.2f}  first_full-setup {np.median(rel[:,3]-rel[:,1]):.2f}"
+          f"  mma {np.median(rel[:,4]-rel[:,3]):.2f}  epi {np.median(rel[:,6]-rel[:,5]):.2f}")
+
+
+def copy_calib():
+    n = 64
+    x = k64((n, 64, 56, 56))
+    y = torch.empty_like(x)
+    dims = [("N", n), ("C", 64), ("H", 56), ("W", 56)]
+
+    def t(fn, reps=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps * 1e3
+    byts = 2 * x.numel() * 4
+    for name, fn in [
+        ("torch clone", lambda: y.copy_(x)),
+        ("torch permute NCHW->NCHWc16", lambda: y.view(n, 4, 56, 56, 16).copy_(x.view(n, 4, 16, 56, 56).permute(0, 1, 3, 4, 2))),
+        ("lfgpu identity", lambda: runtime.layout_convert(x, dims, [], [], y)),
+        ("lfgpu NCHW->NCHWc16", lambda: runtime.layout_convert(x, dims, [], [split(1, [4, 16]), reorder([0, 1, 3, 4, 2])], y)),
+    ]:
+        us = t(fn)
+        print(f"{name:32s} {us:8.2f} us  {byts / us / 1e3:8.1f} GB/s")
+
+
+if __name__ == "__main__":
+    copy_calib()
+    g = ir.gemm(1024, 1024, 1024)
+    A, B = k64((1024, 1024)), k64((1024, 1024))
+    for f, tl in [((128, 64, 1024), 64), ((512, 256, 256), 64), ((128, 64, 128), 128)]:
+        timeline(g, tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tl)]), {"a": A, "b": B},
+                 f"gemm {f} tile {tl}")
+    gc = ir.pad_conv(16, 64, 64, 56, 3, 1, 1)
+    timeline(gc, tuner.Candidate({1: (56, 56, 64, 16, 16, 64)}, [runtime.sched(1)]),
+             {"x": k64((16, 64, 56, 56)), "ker": k64((64, 64, 3, 3))}, "conv b16")
