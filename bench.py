@@ -144,9 +144,11 @@ def time_plan_steps(torch, plan, steps, warmup, flush_buf, world):
     barrier(world)
     torch.cuda.synchronize()
     t_wall = time.perf_counter()
+    half = flush_buf.numel() // 2
     for a, b in evs:
         with torch.cuda.stream(s):
-            flush_buf.add_(1.0)  # > L2 write between timed steps
+            flush_buf[:half].add_(1.0)     # > L2 write between timed steps ...
+            flush_buf[half:].amax()         # ... then a > L2 read: cold, clean L2
             a.record(s)
         plan.run()
         with torch.cuda.stream(s):
@@ -169,7 +171,8 @@ def run_ours(args, rank, world, local):
     pk, pk_kind = peaks()
     gen = torch.Generator(device=dev)
     gen.manual_seed(42 + rank)
-    flush = torch.zeros(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    # 2 x 256 MB (> 126 MB L2): written, then read, between timed steps
+    flush = torch.zeros(128 << 20, dtype=torch.float32, device=dev)
     out = {}
 
     # ---- 1. tune the cfg2 GEMM layout on the GPU (measure backend)
@@ -292,7 +295,8 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     tt = []
     for _ in range(20):
-        flush.add_(1.0)
+        flush[: flush.numel() // 2].add_(1.0)
+        flush[flush.numel() // 2:].amax()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         runtime.layout_convert(xs, dims, [], seq, yd, ctx=ctx)

@@ -122,6 +122,26 @@ __device__ __forceinline__ void tma_load(const CUtensorMap* map, int rank, uint3
   }
 }
 
+__device__ __forceinline__ void tma_load5(const CUtensorMap* map, uint32_t dst, uint32_t bar,
+                                          int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                          int32_t c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void umma_bf16(uint32_t tmem, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -336,8 +356,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer: coordinates = tile part (registers) + stage part (SMEM)
+  if (warp == 0) {
+    // ---- TMA producer (whole warp runs the loop; one elected lane issues).
+    // Coordinates = tile part (registers) + stage part (SMEM); views are
+    // always 5-D (host pads unit dims) so each load is one straight-line
+    // UTMALDG.5D with no rank dispatch.
     int32_t ta[kMaxBoxes][5], tb[kMaxBoxes][5];
 #pragma unroll
     for (int b = 0; b < kMaxBoxes; ++b)
@@ -346,54 +369,72 @@ __global__ void __launch_bounds__(kThreads, 1)
         ta[b][d] = s_tile->ca[b][d];
         tb[b][d] = s_tile->cb[b][d];
       }
-    const int na = P.a_boxes, nb = P.b_boxes;
-    for (int s = early; s < P.nstages; ++s) {
-      const int slot = s % pipe;
-      mbar_wait(empty0 + 8 * slot, ((s / pipe) & 1) ^ 1);
-      const uint32_t bar = full0 + 8 * slot;
-      mbar_expect_tx(bar, P.tx_bytes);
-      const StageEntry se = s_stage[s];
-      const uint32_t a_dst = smem_u32(smem + slot * stage_bytes);
-      const uint32_t b_dst = a_dst + na * P.a_slot;
-      int32_t c[5];
+    const int na = P.a_boxes, nb = P.b_boxes, nst = P.nstages;
+    const uint32_t tx = P.tx_bytes, a_slot = P.a_slot, b_slot = P.b_slot;
+    const uint32_t ring0 = smem_u32(smem);
+    const uint32_t b_off = na * a_slot;
+    const bool leader = elect_one();
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int s = 0; s < nst; ++s) {
+      if (leader) {
+        mbar_wait(empty0 + 8 * slot, phase ^ 1);
+        const uint32_t bar = full0 + 8 * slot;
+        mbar_expect_tx(bar, tx);
+        const StageEntry se = s_stage[s];
+        if (dbg && s < 32) P.dbg[10 * gridDim.x + 64 * tile + s] = gtimer();
+        const uint32_t a_dst = ring0 + slot * stage_bytes;
 #pragma unroll
-      for (int b = 0; b < kMaxBoxes; ++b) {
-        if (b >= na) break;
+        for (int b = 0; b < kMaxBoxes; ++b)
+          if (b < na)
+            tma_load5(&tma_a, a_dst + b * a_slot, bar, ta[b][0] + se.sa[0], ta[b][1] + se.sa[1],
+                      ta[b][2] + se.sa[2], ta[b][3] + se.sa[3], ta[b][4] + se.sa[4]);
 #pragma unroll
-        for (int d = 0; d < 5; ++d) c[d] = ta[b][d] + se.sa[d];
-        tma_load(&tma_a, P.a_rank, a_dst + b * P.a_slot, bar, c);
+        for (int b = 0; b < kMaxBoxes; ++b)
+          if (b < nb)
+            tma_load5(&tma_b, a_dst + b_off + b * b_slot, bar, tb[b][0] + se.sb[0],
+                      tb[b][1] + se.sb[1], tb[b][2] + se.sb[2], tb[b][3] + se.sb[3],
+                      tb[b][4] + se.sb[4]);
       }
-#pragma unroll
-      for (int b = 0; b < kMaxBoxes; ++b) {
-        if (b >= nb) break;
-#pragma unroll
-        for (int d = 0; d < 5; ++d) c[d] = tb[b][d] + se.sb[d];
-        tma_load(&tma_b, P.b_rank, b_dst + b * P.b_slot, bar, c);
+      if (++slot == pipe) {
+        slot = 0;
+        phase ^= 1;
       }
     }
-    if (dbg) dbg[2] = gtimer();
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer
+    if (dbg && leader) dbg[2] = gtimer();
+  } else if (warp == 1) {
+    // ---- MMA issuer (whole warp loops; one elected lane issues tcgen05.mma)
     const uint64_t adesc = P.a_desc, bdesc = P.b_desc;
     const uint32_t idesc = P.idesc, akadv = P.a_kadv, bkadv = P.b_kadv;
-    const int ksteps = P.ksteps;
+    const int ksteps = P.ksteps, nst = P.nstages;
+    const uint32_t ring0 = smem_u32(smem);
     const uint32_t a_off_b = P.a_boxes * P.a_slot;
-    for (int s = 0; s < P.nstages; ++s) {
-      const int slot = s % pipe;
-      mbar_wait(full0 + 8 * slot, (s / pipe) & 1);
-      if (dbg && s == 0) dbg[3] = gtimer();
+    const bool leader = elect_one();
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int s = 0; s < nst; ++s) {
+      mbar_wait(full0 + 8 * slot, phase);
+      if (dbg && leader && s == 0) dbg[3] = gtimer();
+      if (dbg && leader && s < 32) P.dbg[10 * gridDim.x + 64 * tile + 32 + s] = gtimer();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a_addr = smem_u32(smem + slot * stage_bytes);
-      const uint32_t b_addr = a_addr + a_off_b;
-      for (int k = 0; k < ksteps; ++k) {
-        const uint64_t ad = adesc | (((a_addr + k * akadv) >> 4) & 0x3FFFull);
-        const uint64_t bd = bdesc | (((b_addr + k * bkadv) >> 4) & 0x3FFFull);
-        umma_bf16(tmem, ad, bd, idesc, (s | k) != 0);
+      if (leader) {
+        const uint32_t a_addr = ring0 + slot * stage_bytes;
+        const uint32_t b_addr = a_addr + a_off_b;
+        for (int k = 0; k < ksteps; ++k) {
+          const uint64_t ad = adesc | (((a_addr + k * akadv) >> 4) & 0x3FFFull);
+          const uint64_t bd = bdesc | (((b_addr + k * bkadv) >> 4) & 0x3FFFull);
+          umma_bf16(tmem, ad, bd, idesc, (s | k) != 0);
+        }
+        umma_commit(empty0 + 8 * slot);
       }
-      umma_commit(empty0 + 8 * slot);
+      __syncwarp();
+      if (++slot == pipe) {
+        slot = 0;
+        phase ^= 1;
+      }
     }
-    umma_commit(accf);
-    if (dbg) dbg[4] = gtimer();
+    if (leader) umma_commit(accf);
+    if (dbg && leader) dbg[4] = gtimer();
   } else if (warp >= 2) {
     // ---- epilogue (4 warps). Phase 1: TMEM -> SMEM tile (row r = TMEM lane r).
     const int quad = warp & 3;
@@ -498,16 +539,23 @@ CUtensorMap encode(const OperandView& v, const void* base) {
   std::memset(&m, 0, sizeof(m));
   cuuint64_t dims[5], strides[5];
   cuuint32_t box[5], es[5];
-  for (int d = 0; d < v.rank; ++d) {
-    dims[d] = v.dims[d];
-    strides[d] = v.strides[d];
-    box[d] = v.box[d];
-    es[d] = v.estride[d];
+  for (int d = 0; d < 5; ++d) {
+    if (d < v.rank) {
+      dims[d] = v.dims[d];
+      strides[d] = v.strides[d];
+      box[d] = v.box[d];
+      es[d] = v.estride[d];
+    } else {  // unit padding dims: the kernel always issues 5-D loads
+      dims[d] = 1;
+      strides[d] = d == 1 ? ((v.dims[0] * 2 + 15) / 16) * 16 : strides[d - 1] * dims[d - 1];
+      box[d] = 1;
+      es[d] = 1;
+    }
   }
   CUtensorMapSwizzle sw = v.swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                           : v.swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                             : CU_TENSOR_MAP_SWIZZLE_32B;
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, v.rank, const_cast<void*>(base),
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base),
                            dims, strides + 1, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(LFGPU_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));

@@ -19,6 +19,8 @@ int elem_size(int elem);
 // K1/K2 (k_copy.cu)
 cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, const void* src,
                               void* dst, cudaStream_t stream, KernelInfo* info);
+// Stream-read a > L2 buffer (measurement hygiene after the flush write).
+cudaError_t launch_l2_touch(const void* buf, size_t bytes, int* sink, cudaStream_t stream);
 // d_progs: two IxPrograms (dst inverse, src forward) in device memory.
 cudaError_t launch_ix_copy(const IxProgram* d_progs, int64_t n, int src_elem, int dst_elem,
                            const void* src, void* dst, int* d_err, cudaStream_t stream,

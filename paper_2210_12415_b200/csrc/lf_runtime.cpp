@@ -891,15 +891,21 @@ int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t f
     lfgpu_ctx* ctx = plan->ctx;
     CUDA_OK(cudaSetDevice(ctx->device));
     if (flush_l2 && !ctx->flush) {
-      ctx->flush_bytes = size_t(256) << 20;  // 2x the 126 MB L2
+      ctx->flush_bytes = size_t(512) << 20;  // 256 MB write + 256 MB read (L2 is 126 MB)
       CUDA_OK(cudaMalloc(&ctx->flush, ctx->flush_bytes));
     }
     for (int i = 0; i < warmup; ++i) plan_run_steps(plan);
     std::vector<cudaEvent_t> ev(2 * std::max(reps, 1));
     for (auto& e : ev) CUDA_OK(cudaEventCreate(&e));
     for (int r = 0; r < reps; ++r) {
-      if (flush_l2)
-        CUDA_OK(cudaMemsetAsync(ctx->flush, r & 0xff, ctx->flush_bytes, plan->stream));
+      if (flush_l2) {
+        // > L2 write (the flush), then a > L2 read so the measured graph
+        // starts with a cold *and clean* L2 (no dirty-line write-backs).
+        CUDA_OK(cudaMemsetAsync(ctx->flush, r & 0xff, ctx->flush_bytes / 2, plan->stream));
+        CUDA_OK(launch_l2_touch(static_cast<char*>(ctx->flush) + ctx->flush_bytes / 2,
+                                ctx->flush_bytes / 2, static_cast<int*>(ctx->flush),
+                                plan->stream));
+      }
       CUDA_OK(cudaEventRecord(ev[2 * r], plan->stream));
       plan_run_steps(plan);
       CUDA_OK(cudaEventRecord(ev[2 * r + 1], plan->stream));

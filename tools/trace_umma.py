@@ -23,7 +23,7 @@ def timeline(g, cand, inputs, name):
         p.set_input_device(k, v)
     p.run()
     torch.cuda.synchronize()
-    buf = torch.zeros(16 * 4096, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(80 * 4096, dtype=torch.int64, device="cuda")
     runtime.lib().lfgpu_debug_umma_trace(C.c_void_p(buf.data_ptr()))
     p2 = runtime.Plan(g, tuner.seqs_for(g, cand), cand.scheds, _abi.PLAN_REQUIRE_TC)
     for k, v in inputs.items():
@@ -40,6 +40,13 @@ def timeline(g, cand, inputs, name):
     clk = allb[8 * nct: 8 * nct + 2 * nct].reshape(-1, 2)
     mhz = (clk[:, 1] - clk[:, 0]) / np.maximum(t[:, 6] - t[:, 0], 1) * 1000.0
     print(f"  in-kernel SM clock: median {np.median(mhz):.0f} MHz (min {mhz.min():.0f}, max {mhz.max():.0f})")
+    st = allb[10 * nct: 10 * nct + 64 * nct].reshape(-1, 64)
+    c0 = st[0]
+    base = t[0, 0]
+    iss = [(x - base) / 1000.0 for x in c0[:32] if x > 0]
+    ful = [(x - base) / 1000.0 for x in c0[32:] if x > 0]
+    print("  CTA0 TMA issue times (us):", " ".join(f"{v:.2f}" for v in iss[:20]))
+    print("  CTA0 stage landed   (us):", " ".join(f"{v:.2f}" for v in ful[:20]))
     t0 = t[:, 0].min()
     rel = (t - t0) / 1000.0
     labels = ["entry", "setup", "tma_done", "first_full", "mma_done", "acc_ready", "epi_done",
