@@ -247,6 +247,14 @@ int lfgpu_layout_convert(lfgpu_ctx* ctx, int32_t rank, const lfgpu_dim* logical,
                          const lfgpu_prim* dst_seq, int32_t src_elem, int32_t dst_elem,
                          const void* d_src, void* d_dst, void* stream);
 
+/* K1 with host buffers: lf::materialize_tensor for one Input/Constant tensor
+ * (interp.cpp:280-337) — logical doubles in, physical doubles out (stored
+ * on the device as `elem`, LFGPU_ELEM_F32 reproduces float32 tensors
+ * bit-exactly). Synchronous. */
+int lfgpu_materialize_host(lfgpu_ctx* ctx, int32_t rank, const lfgpu_dim* logical,
+                           int32_t nprims, const lfgpu_prim* seq, int32_t elem,
+                           const double* host_logical, double* host_physical);
+
 /* ---- K2: Padding written straight into the consumer's layout ----------------------
  * The Padding nest of lower.cpp:228-238 / 391-403 on a propagated output
  * layout: out-of-interior and unfold-overhang cells get 0. `in_logical` is

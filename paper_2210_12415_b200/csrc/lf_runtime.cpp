@@ -724,6 +724,36 @@ int lfgpu_layout_convert(lfgpu_ctx* ctx, int32_t rank, const lfgpu_dim* logical,
   });
 }
 
+int lfgpu_materialize_host(lfgpu_ctx* ctx, int32_t rank, const lfgpu_dim* logical,
+                           int32_t nprims, const lfgpu_prim* seq, int32_t elem,
+                           const double* host_logical, double* host_physical) {
+  return guarded([&] {
+    if (!ctx) fail(LFGPU_EINVAL, "null context");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    auto dims = dims_of(rank, logical);
+    Seq s = seq_of(nprims, seq);
+    const int64_t nl = numel(dims), np = numel(derive(dims, s));
+    DevBuf in(sizeof(double) * std::max<int64_t>(nl, 1)), mid(elem_size(elem) * std::max<int64_t>(nl, 1)),
+        phys(elem_size(elem) * std::max<int64_t>(np, 1)), out(sizeof(double) * std::max<int64_t>(np, 1));
+    CUDA_OK(cudaMemcpy(in.p, host_logical, sizeof(double) * nl, cudaMemcpyHostToDevice));
+    std::vector<std::unique_ptr<DevBuf>> keep;
+    bool oob;
+    CopySpec id;
+    id.lmap = identity_map(dims);
+    CopySpec mat = id;
+    mat.dst_seq = s;
+    mat.mode = FoldMode::Clamp;
+    // logical f64 -> logical elem (the tensor's storage type) -> physical elem -> f64
+    CUDA_OK(run_copy(compile_copy(id, LFGPU_ELEM_F64, elem, keep, &oob), in.p, mid.p, ctx->d_err, 0));
+    CUDA_OK(run_copy(compile_copy(mat, elem, elem, keep, &oob), mid.p, phys.p, ctx->d_err, 0));
+    CopySpec back;
+    back.lmap = identity_map(derive(dims, s));
+    CUDA_OK(run_copy(compile_copy(back, elem, LFGPU_ELEM_F64, keep, &oob), phys.p, out.p, ctx->d_err, 0));
+    CUDA_OK(cudaMemcpy(host_physical, out.p, sizeof(double) * np, cudaMemcpyDeviceToHost));
+    ctx->launches += 3;
+  });
+}
+
 int lfgpu_pad_convert(lfgpu_ctx* ctx, const lfgpu_dim* in_logical, int64_t pad, int32_t nsrc,
                       const lfgpu_prim* src_seq, int32_t ndst, const lfgpu_prim* dst_seq,
                       int32_t src_elem, int32_t dst_elem, const void* d_src, void* d_dst,

@@ -28,7 +28,7 @@ EXPORTS = [
     "lfgpu_plan_destroy", "lfgpu_plan_set_input", "lfgpu_plan_set_input_device",
     "lfgpu_plan_run", "lfgpu_plan_get_output", "lfgpu_plan_tensor_buffer", "lfgpu_plan_stream",
     "lfgpu_plan_info", "lfgpu_plan_node_kernel", "lfgpu_plan_measure", "lfgpu_interpret",
-    "lfgpu_debug_umma_trace",
+    "lfgpu_debug_umma_trace", "lfgpu_materialize_host",
 ]
 
 
