@@ -79,6 +79,37 @@ def best(results):
     return min(ok, key=lambda r: r.cost_us) if ok else None
 
 
+def sweep_distributed(graph: Graph, cands, inputs=None, measure_fn=None, **kw):
+    """One process per GPU: each rank measures candidates i with
+    i % world == rank (no collective on the data path), then the (index,
+    cost) pairs are all-gathered and committed in candidate-index order, so
+    the winner is the reference's: strictly lowest cost, first index on ties
+    (tuner.cpp:180-189). Returns (results in index order, best index,
+    local seconds, local count)."""
+    import torch.distributed as dist
+    rank, world = (dist.get_rank(), dist.get_world_size()) if dist.is_initialized() else (0, 1)
+    fn = measure_fn or measure
+    t0 = time.perf_counter()
+    local = [(i, fn(graph, c, inputs, **kw)) for i, c in enumerate(cands) if i % world == rank]
+    secs = time.perf_counter() - t0
+    mine = [(i, r.cost_us, r.error) for i, r in local]
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+    else:
+        gathered = [mine]
+    merged = {}
+    for part in gathered:
+        for i, cost, err in part:
+            merged[i] = Result(cands[i], cost, err)
+    results = [merged[i] for i in range(len(cands))]
+    best_i, best_c = -1, float("inf")
+    for i, r in enumerate(results):
+        if r.cost_us is not None and r.cost_us < best_c:
+            best_i, best_c = i, r.cost_us
+    return results, best_i, secs, len(local)
+
+
 # --- candidate streams -------------------------------------------------------
 
 def gemm_candidates(M, K, N, node=0):
