@@ -160,6 +160,32 @@ def time_plan_steps(torch, plan, steps, warmup, flush_buf, world):
     return per, wall
 
 
+def time_plan_rotating(torch, plans, steps, warmup, world):
+    """K back-to-back steps, step i on replica plans[i % R]. The replicas'
+    operand + result buffers together exceed 2x the 126 MB L2, so every step
+    reads operands that are not L2-resident (the 'inputs larger than L2'
+    rule) while no flush kernel sits between timed steps. One event pair on
+    the plans' shared stream brackets the K steps."""
+    s = torch.cuda.Stream()
+    for i in range(max(warmup, len(plans))):
+        plans[i % len(plans)].run(s.cuda_stream)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    with torch.cuda.stream(s):
+        a.record(s)
+    for i in range(steps):
+        plans[(warmup + i) % len(plans)].run(s.cuda_stream)
+    with torch.cuda.stream(s):
+        b.record(s)
+    torch.cuda.synchronize()
+    barrier(world)
+    wall = time.perf_counter() - t_wall
+    return a.elapsed_time(b), wall
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
     import torch
@@ -194,22 +220,37 @@ def run_ours(args, rank, world, local):
                     "candidates_per_s": round(len(res) / tune_s, 1),
                     "best": bestr.candidate.label, "best_us": round(bestr.cost_us, 3)}
 
-    # ---- 2. timed region: K steps of the tuned GEMM
-    plan = runtime.Plan(g, tuner.seqs_for(g, bestr.candidate), bestr.candidate.scheds,
-                        _abi.PLAN_REQUIRE_TC, ctx=ctx)
-    plan.set_input_device("a", A)
-    plan.set_input_device("b", B)
+    # ---- 2. timed region: K steps of the tuned GEMM, rotating over replicas
+    # whose operands + results (2+2+4 MB each) total > 2x L2, so each step
+    # streams cold operands from HBM.
+    seqs_best = tuner.seqs_for(g, bestr.candidate)
+    rep_bytes = 2 * M * K + 2 * K * N + 4 * M * N
+    n_rep = max(2, -(-(256 << 20) // rep_bytes))
+    reps = []
+    for _ in range(n_rep):
+        r = runtime.Plan(g, seqs_best, bestr.candidate.scheds,
+                         _abi.PLAN_REQUIRE_TC | _abi.PLAN_CUDA_GRAPH, ctx=ctx)
+        r.set_input_device("a", A)
+        r.set_input_device("b", B)
+        reps.append(r)
+    plan = reps[0]
     launches0 = ctx.launches
     with ClockSampler(local) as clk:
-        per, wall = time_plan_steps(torch, plan, args.steps, args.warmup, flush, world)
-    launches = ctx.launches - launches0 - args.warmup * plan.info().kernels
-    total_ms = max_over_ranks(sum(per), world)
+        tot_ms, wall = time_plan_rotating(torch, reps, args.steps, args.warmup, world)
+    launches = ctx.launches - launches0 - max(args.warmup, len(reps)) * plan.info().kernels
+    total_ms = max_over_ranks(tot_ms, world)
     flops_step = 2.0 * M * N * K
     value = world * args.steps * flops_step / (total_ms * 1e-3) / 1e12
-    kern_us = statistics.mean(per) * 1e3
+    kern_us = tot_ms / args.steps * 1e3
+    # also the isolated-launch view (flush kernels between steps): one kernel
+    # launched after a > L2 write+read, incl. its launch/drain latency
+    per, _ = time_plan_steps(torch, plan, min(args.steps, 10), 3, flush, world)
     # parity of the benchmarked kernel (k/64 inputs: fp32 accumulation is exact)
-    c = torch.tensor(plan.get_output("c"), device=dev).view(M, N)
-    verified = bool(torch.equal(c.double(), A.double() @ B.double()))
+    ref_c = A.double() @ B.double()
+    verified = True
+    for r in (plan, reps[(args.warmup + args.steps - 1) % n_rep]):
+        c = torch.tensor(r.get_output("c"), device=dev).view(M, N)
+        verified = verified and bool(torch.equal(c.double(), ref_c))
 
     # ---- 3. e2e through the C-ABI with host buffers
     Ah = A.cpu().pin_memory()
@@ -330,7 +371,9 @@ def run_ours(args, rank, world, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic k/64 inputs (the reference's random_inputs distribution)",
         "config": {"workload": "cfg2: GEMM 1024x1024x1024 on the tuned GMM template layout",
-                   "layout": bestr.candidate.label, "l2": "flushed between steps (256 MB write)",
+                   "layout": bestr.candidate.label, "l2": f"inputs larger than L2: {len(reps)} rotating operand replicas "
+                         f"({n_rep * rep_bytes >> 20} MB)",
+                   "isolated_step_us_after_l2_flush": round(statistics.median(per) * 1e3, 3),
                    "parallelism": f"replicas x{world}", "verified_exact": verified},
         "e2e": {"value": round(e2e_val, 4), "unit": "TFLOP/s",
                 "h2d_bytes_per_step": 2 * M * K * 4, "d2h_bytes_per_step": M * N * 8},

@@ -283,6 +283,10 @@ int lfgpu_plan_set_input_device(lfgpu_plan* plan, int32_t tensor, const void* d_
                                 int32_t elem);
 /* Execute every node once on the plan's stream (asynchronous). */
 int lfgpu_plan_run(lfgpu_plan* plan);
+/* Same, enqueued on the caller's stream instead of the plan's own (NULL:
+ * the plan's stream). Stream-ordered like a kernel launch; several plans
+ * may share one stream. */
+int lfgpu_plan_run_on(lfgpu_plan* plan, void* stream);
 /* Convert a node output back to its logical layout and copy it to host
  * doubles (interp.cpp:441-468). Synchronises the plan's stream. */
 int lfgpu_plan_get_output(lfgpu_plan* plan, int32_t tensor, double* host_logical, int64_t n);

@@ -586,7 +586,8 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   }
 }
 
-void plan_run_steps(lfgpu_plan* P) {
+void plan_run_steps(lfgpu_plan* P, cudaStream_t on = nullptr) {
+  cudaStream_t st = on ? on : P->stream;
   if ((P->flags & LFGPU_PLAN_CUDA_GRAPH) && !P->steps.empty()) {
     if (!P->gexec) {
       CUDA_OK(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
@@ -602,10 +603,10 @@ void plan_run_steps(lfgpu_plan* P) {
       CUDA_OK(cudaStreamEndCapture(P->stream, &P->graph));
       CUDA_OK(cudaGraphInstantiate(&P->gexec, P->graph, 0));
     }
-    CUDA_OK(cudaGraphLaunch(P->gexec, P->stream));
+    CUDA_OK(cudaGraphLaunch(P->gexec, st));
   } else {
     for (auto& s : P->steps) {
-      cudaError_t e = s.run(P->stream);
+      cudaError_t e = s.run(st);
       if (e != cudaSuccess)
         fail(LFGPU_ECUDA, "kernel " + s.kernel + " (node " + std::to_string(s.node) +
                               "): " + cudaGetErrorString(e));
@@ -853,6 +854,13 @@ int lfgpu_plan_run(lfgpu_plan* plan) {
   return guarded([&] {
     CUDA_OK(cudaSetDevice(plan->ctx->device));
     plan_run_steps(plan);
+  });
+}
+
+int lfgpu_plan_run_on(lfgpu_plan* plan, void* stream) {
+  return guarded([&] {
+    CUDA_OK(cudaSetDevice(plan->ctx->device));
+    plan_run_steps(plan, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -26,7 +26,7 @@ EXPORTS = [
     "lfgpu_ctx_destroy",
     "lfgpu_ctx_launch_count", "lfgpu_layout_convert", "lfgpu_pad_convert", "lfgpu_plan_build",
     "lfgpu_plan_destroy", "lfgpu_plan_set_input", "lfgpu_plan_set_input_device",
-    "lfgpu_plan_run", "lfgpu_plan_get_output", "lfgpu_plan_tensor_buffer", "lfgpu_plan_stream",
+    "lfgpu_plan_run", "lfgpu_plan_run_on", "lfgpu_plan_get_output", "lfgpu_plan_tensor_buffer", "lfgpu_plan_stream",
     "lfgpu_plan_info", "lfgpu_plan_node_kernel", "lfgpu_plan_measure", "lfgpu_interpret",
     "lfgpu_debug_umma_trace", "lfgpu_materialize_host",
 ]
@@ -74,6 +74,7 @@ def lib():
         L.lfgpu_plan_measure.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                          P(_abi.Counters)]
         L.lfgpu_plan_run.argtypes = [C.c_void_p]
+        L.lfgpu_plan_run_on.argtypes = [C.c_void_p, C.c_void_p]
         L.lfgpu_plan_destroy.argtypes = [C.c_void_p]
         L.lfgpu_ctx_create.argtypes = [C.c_int, P(C.c_void_p)]
         L.lfgpu_ctx_destroy.argtypes = [C.c_void_p]
@@ -263,8 +264,11 @@ class Plan:
         check(lib().lfgpu_plan_set_input_device(self.ptr, self.index(tid),
                                                 C.c_void_p(tensor.data_ptr()), elem_of(tensor)))
 
-    def run(self):
-        check(lib().lfgpu_plan_run(self.ptr))
+    def run(self, stream=None):
+        if stream is None:
+            check(lib().lfgpu_plan_run(self.ptr))
+        else:
+            check(lib().lfgpu_plan_run_on(self.ptr, C.c_void_p(stream)))
 
     def get_output(self, tid):
         n = self.graph.tensor(tid).num_elements()

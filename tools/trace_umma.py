@@ -29,6 +29,11 @@ def timeline(g, cand, inputs, name):
     for k, v in inputs.items():
         p2.set_input_device(k, v)
     torch.cuda.synchronize()
+    if os.environ.get("TRACE_COLD"):
+        fl = torch.zeros(128 << 20, device="cuda")
+        fl[: fl.numel() // 2].add_(1.0)
+        fl[fl.numel() // 2:].amax()
+        torch.cuda.synchronize()
     p2.run()
     torch.cuda.synchronize()
     runtime.lib().lfgpu_debug_umma_trace(None)
