@@ -124,6 +124,7 @@ struct DCParams {
   int32_t ca[kMaxClamp], cb[kMaxClamp], cconst[kMaxClamp], cmax[kMaxClamp],
       cstride[kMaxClamp];
   int32_t src_base;
+  int32_t vec;  // 1: the 16-B vector kernels apply (host-checked)
 };
 
 struct TileOrigin {
@@ -260,6 +261,134 @@ __global__ void __launch_bounds__(kCopyThreads)
         const int a = idx & (TA - 1), b = idx >> la;
         if (idx < n && a < o.ta && b < o.tb)
           dst[o.dbase + a * P.dst_a + b * P.dst_b] = convert<TS, TD>(v[u]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Vectorised variants (no predicates / clamps): every global access is 16 B.
+// V = 16 / min(sizeof(TS), sizeof(TD)) elements per vector, so both sides
+// move whole multiples of 16 B (fp32->bf16: two LDG.128 + one STG.128).
+// The host only picks these when V divides the vector digit's extent and
+// every other stride on that side, and the base pointers are 16-B aligned.
+
+template <typename TS, typename TD>
+struct VecW {
+  static constexpr int V = 16 / (sizeof(TS) < sizeof(TD) ? sizeof(TS) : sizeof(TD));
+};
+
+template <typename T, int V>
+__device__ __forceinline__ void ld_vec(const T* __restrict__ p, T (&v)[V]) {
+  static_assert((V * sizeof(T)) % 16 == 0, "vector must be whole 16-B words");
+  constexpr int W = V * sizeof(T) / 16;
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const uint4 x = __ldg(q + w);
+    memcpy(reinterpret_cast<unsigned char*>(v) + 16 * w, &x, 16);
+  }
+}
+
+template <typename T, int V>
+__device__ __forceinline__ void st_vec(T* __restrict__ p, const T (&v)[V]) {
+  constexpr int W = V * sizeof(T) / 16;
+  uint4* q = reinterpret_cast<uint4*>(p);
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    uint4 x;
+    memcpy(&x, reinterpret_cast<const unsigned char*>(v) + 16 * w, 16);
+    q[w] = x;
+  }
+}
+
+// Transpose: loads are V-vectors along b (source-contiguous), stores are
+// V-vectors along a (destination-contiguous). The SMEM tile is [TA][TB + V]
+// (rows 16-B aligned for vector SMEM stores on the load side; the column
+// reads of the store side are scalar).
+template <typename TS, typename TD>
+__global__ void __launch_bounds__(kCopyThreads)
+    digit_transpose_vec(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  constexpr int V = VecW<TS, TD>::V;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int la = P.la, lb = P.lb, lg = P.lg;
+  const int TA = 1 << la, TB = 1 << lb, ld = TB + V;
+  const int lbv = lb - __ffs(V) + 1, lav = la - __ffs(V) + 1;  // log2(T / V)
+  const int nv = (TA * TB) / V;
+  const int tpt = kCopyThreads >> lg;
+  const int q = threadIdx.x >> (8 - lg), lt = threadIdx.x & (tpt - 1);
+  TS* tile = reinterpret_cast<TS*>(smem_raw) + q * TA * ld;
+  for (int base = blockIdx.x << lg; base < P.ntiles; base += gridDim.x << lg) {
+    const int t = base + q;
+    TileOrigin o;
+    const bool ok = t < P.ntiles;
+    if (ok) {
+      decode_tile<false>(P, static_cast<uint32_t>(t), o);
+      const int tbv = o.tb / V;
+#pragma unroll 2
+      for (int idx = lt; idx < nv; idx += tpt) {
+        const int ia = idx >> lbv, ibv = idx & ((TB / V) - 1);
+        if (ia < o.ta && ibv < tbv) {
+          TS v[V];
+          ld_vec<TS, V>(src + o.sbase + ia * P.src_a + ibv * V, v);
+          st_vec<TS, V>(tile + ia * ld + ibv * V, v);
+        }
+      }
+    }
+    __syncthreads();
+    if (ok) {
+      const int tav = o.ta / V;
+#pragma unroll 2
+      for (int idx = lt; idx < nv; idx += tpt) {
+        const int iav = idx & ((TA / V) - 1), ib = idx >> lav;
+        if (iav < tav && ib < o.tb) {
+          TD v[V];
+#pragma unroll
+          for (int j = 0; j < V; ++j) v[j] = convert<TS, TD>(tile[(iav * V + j) * ld + ib]);
+          st_vec<TD, V>(dst + o.dbase + iav * V + ib * P.dst_b, v);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Direct: a is contiguous on both sides; V-vectors along a.
+template <typename TS, typename TD>
+__global__ void __launch_bounds__(kCopyThreads)
+    digit_direct_vec(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  constexpr int V = VecW<TS, TD>::V;
+  const int la = P.la, lb = P.lb, lg = P.lg;
+  const int lav = la - __ffs(V) + 1;
+  const int nv = (1 << (la + lb)) / V;
+  const int tpt = kCopyThreads >> lg;
+  const int q = threadIdx.x >> (8 - lg), lt = threadIdx.x & (tpt - 1);
+  for (int base = blockIdx.x << lg; base < P.ntiles; base += gridDim.x << lg) {
+    const int t = base + q;
+    if (t >= P.ntiles) continue;
+    TileOrigin o;
+    decode_tile<false>(P, static_cast<uint32_t>(t), o);
+    const int tav = o.ta / V;
+    constexpr int U = 4;
+    for (int i0 = lt; i0 < nv; i0 += tpt * U) {
+      TS v[U][V];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = i0 + u * tpt;
+        const int av = idx & ((1 << lav) - 1), b = idx >> lav;
+        if (idx < nv && av < tav && b < o.tb)
+          ld_vec<TS, V>(src + o.sbase + av * V + b * P.src_b, v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = i0 + u * tpt;
+        const int av = idx & ((1 << lav) - 1), b = idx >> lav;
+        if (idx < nv && av < tav && b < o.tb) {
+          TD w[V];
+#pragma unroll
+          for (int j = 0; j < V; ++j) w[j] = convert<TS, TD>(v[u][j]);
+          st_vec<TD, V>(dst + o.dbase + av * V + b * P.dst_b, w);
+        }
       }
     }
   }
@@ -446,8 +575,7 @@ static int32_t i32(int64_t v) {
 }
 
 // Tile selection for a DigitMap (see file comment).
-static DCParams make_params(const DigitMap& m, int src_elem) {
-  (void)src_elem;
+static DCParams make_params(const DigitMap& m, int src_elem, int dst_elem) {
   DCParams P;
   std::memset(&P, 0, sizeof(P));
   int nd = m.ndig;
@@ -470,6 +598,20 @@ static DCParams make_params(const DigitMap& m, int src_elem) {
   int64_t outer_ext = 1;
   for (int d = 0; d < nd; ++d)
     if (d != a && d != b) outer_ext *= m.ext[d];
+  // 16-B vectors: V elements along a (and along b when transposing) when V
+  // divides the vector digits' extents and every other stride on that side.
+  const int V = 16 / std::min(elem_size(src_elem), elem_size(dst_elem));
+  const int lv = log2_ceil(V);
+  bool vec = nd >= 1 && m.npred == 0 && m.nclamp == 0 && m.dst_stride[a] == 1 && ea % V == 0 &&
+             m.src_base % V == 0;
+  if (vec) {
+    const int sv = transpose ? b : a;  // the source digit read as vectors
+    if (m.src_stride[sv] != 1 || (transpose && eb % V != 0)) vec = false;
+    for (int d = 0; d < nd && vec; ++d) {
+      if (d != a && m.dst_stride[d] % V != 0) vec = false;
+      if (d != sv && m.src_stride[d] % V != 0) vec = false;
+    }
+  }
   int la, lb;
   if (transpose) {
     la = std::min(std::max(log2_ceil(ea), 1), 5);
@@ -478,14 +620,20 @@ static DCParams make_params(const DigitMap& m, int src_elem) {
     la = std::min(log2_ceil(ea), 12);
     lb = std::max(0, std::min(12 - la, log2_ceil(std::max<int64_t>(eb, 1))));
   }
+  if (vec) {
+    la = std::max(la, lv);
+    if (transpose) lb = std::max(lb, lv);
+  }
+  const int min_la = vec ? lv : 1, min_lb = vec && transpose ? lv : (transpose ? 1 : 0);
   auto ntiles_for = [&](int x, int y) {
     return outer_ext * ((ea + (int64_t(1) << x) - 1) >> x) * ((eb + (int64_t(1) << y) - 1) >> y);
   };
   while (la + lb > 8 && ntiles_for(la, lb) < 148 * 8) {
-    if (lb >= la && lb > (transpose ? 1 : 0)) --lb;
-    else if (la > 1) --la;
+    if (lb >= la && lb > min_lb) --lb;
+    else if (la > min_la) --la;
     else break;
   }
+  P.vec = vec ? 1 : 0;
   P.lg = std::max(0, std::min(5, 11 - la - lb));
   P.transpose = transpose ? 1 : 0;
   P.la = la;
@@ -540,14 +688,17 @@ static DCParams make_params(const DigitMap& m, int src_elem) {
 cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, const void* src,
                               void* dst, cudaStream_t stream, KernelInfo* info) {
   if (m.dst_numel == 0) return cudaSuccess;
-  DCParams P = make_params(m, src_elem);
+  DCParams P = make_params(m, src_elem, dst_elem);
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) P.vec = 0;
   // Enough CTAs for 8 resident per SM; each walks tiles grid-stride.
   int64_t grid = std::min<int64_t>((P.ntiles + (1 << P.lg) - 1) >> P.lg, 148 * 8);
+  const int V = 16 / std::min(elem_size(src_elem), elem_size(dst_elem));
   size_t smem = P.transpose ? (static_cast<size_t>(1) << P.lg) * (1 << P.la) *
-                                  ((1 << P.lb) + 1) * elem_size(src_elem)
+                                  ((1 << P.lb) + (P.vec ? V : 1)) * elem_size(src_elem)
                             : 0;
   if (info) {
-    info->name = P.transpose ? "digit_copy_transpose" : "digit_copy_direct";
+    info->name = P.transpose ? (P.vec ? "digit_copy_transpose_v16" : "digit_copy_transpose")
+                             : (P.vec ? "digit_copy_direct_v16" : "digit_copy_direct");
     info->grid = grid;
   }
   return dispatch<Unused>(src_elem, dst_elem, [&](auto s, auto d) -> cudaError_t {
@@ -557,7 +708,10 @@ cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, con
     const unsigned g = static_cast<unsigned>(grid);
     const TS* s_ = static_cast<const TS*>(src);
     TD* d_ = static_cast<TD*>(dst);
-    if (P.transpose) {
+    if (P.vec) {
+      if (P.transpose) digit_transpose_vec<TS, TD><<<g, kCopyThreads, smem, stream>>>(P, s_, d_);
+      else digit_direct_vec<TS, TD><<<g, kCopyThreads, 0, stream>>>(P, s_, d_);
+    } else if (P.transpose) {
       if (pc) digit_transpose<TS, TD, true><<<g, kCopyThreads, smem, stream>>>(P, s_, d_);
       else digit_transpose<TS, TD, false><<<g, kCopyThreads, smem, stream>>>(P, s_, d_);
     } else {
