@@ -124,7 +124,8 @@ struct DCParams {
   int32_t ca[kMaxClamp], cb[kMaxClamp], cconst[kMaxClamp], cmax[kMaxClamp],
       cstride[kMaxClamp];
   int32_t src_base;
-  int32_t vec;  // 1: the 16-B vector kernels apply (host-checked)
+  int32_t vec;     // 1: the 16-B vector kernels apply; 2: vector stores only
+  int32_t rowinv;  // guards and clamps do not depend on digit a
 };
 
 struct TileOrigin {
@@ -136,8 +137,11 @@ struct TileOrigin {
 // Param arrays are only ever indexed with compile-time indices (unrolled,
 // guarded loops): a runtime index would make nvcc address the parameter
 // buffer through a generic pointer, i.e. a global-latency load per access.
-template <bool PC>
+// NP / NC: compile-time bounds on the guard / clamp counts (P.npred <= NP,
+// P.nclamp <= NC); the unrolled per-digit terms cost NP + NC IMADs each.
+template <int NP, int NC>
 __device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileOrigin& o) {
+  constexpr bool PC = NP + NC > 0;
   uint32_t q = fdiv(t, P.ftiles_a);
   const int32_t ia0 = static_cast<int32_t>(t - q * P.ftiles_a.d) << P.la;
   t = q;
@@ -148,9 +152,9 @@ __device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileO
   o.sbase = P.src_base;
   if (PC) {
 #pragma unroll
-    for (int p = 0; p < kMaxPred; ++p) o.pv[p] = P.pconst[p] + ia0 * P.pa[p] + ib0 * P.pb[p];
+    for (int p = 0; p < NP; ++p) o.pv[p] = P.pconst[p] + ia0 * P.pa[p] + ib0 * P.pb[p];
 #pragma unroll
-    for (int c = 0; c < kMaxClamp; ++c) o.cv[c] = P.cconst[c] + ia0 * P.ca[c] + ib0 * P.cb[c];
+    for (int c = 0; c < NC; ++c) o.cv[c] = P.cconst[c] + ia0 * P.ca[c] + ib0 * P.cb[c];
   }
 #pragma unroll
   for (int d = kMaxDig - 1; d >= 0; --d) {
@@ -162,9 +166,9 @@ __device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileO
       o.sbase += x * P.osrc[d];
       if (PC) {
 #pragma unroll
-        for (int p = 0; p < kMaxPred; ++p) o.pv[p] += x * P.opred[p][d];
+        for (int p = 0; p < NP; ++p) o.pv[p] += x * P.opred[p][d];
 #pragma unroll
-        for (int c = 0; c < kMaxClamp; ++c) o.cv[c] += x * P.oclamp[c][d];
+        for (int c = 0; c < NC; ++c) o.cv[c] += x * P.oclamp[c][d];
       }
     }
   }
@@ -174,23 +178,60 @@ __device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileO
   o.tb = min(1 << P.lb, P.eb - ib0);
 }
 
-template <bool PC, typename TS>
+template <int NP, int NC, typename TS>
 __device__ __forceinline__ TS load_elem(const DCParams& P, const TileOrigin& o,
                                         const TS* __restrict__ src, int ia, int ib) {
   int32_t off = o.sbase + ia * P.src_a + ib * P.src_b;
-  if (!PC) return __ldg(src + off);
+  if (NP + NC == 0) return __ldg(src + off);
   bool valid = true;
 #pragma unroll
-  for (int p = 0; p < kMaxPred; ++p) {
+  for (int p = 0; p < NP; ++p) {
     const int32_t v = o.pv[p] + ia * P.pa[p] + ib * P.pb[p];
     valid = valid && (p >= P.npred || (v >= P.plo[p] && v < P.phi[p]));
   }
 #pragma unroll
-  for (int c = 0; c < kMaxClamp; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int32_t v = o.cv[c] + ia * P.ca[c] + ib * P.cb[c];
     if (c < P.nclamp) off += min(v, P.cmax[c]) * P.cstride[c];
   }
   return valid ? __ldg(src + off) : zero_of<TS>();
+}
+
+// Load phase of the SMEM-staged transposes: tile[ia][ib] for the tile's
+// valid extents. When every guard and clamp is independent of digit a
+// (P.rowinv: K2's Padding guards and unfold clamps live on the spatial
+// digits, a is the channel brick) and a thread's column ib is fixed across
+// its iterations (tpt a multiple of TB), the guard/clamp terms are
+// evaluated once per tile and each element costs one guarded load.
+template <int NP, int NC, typename TS>
+__device__ __forceinline__ void load_tile(const DCParams& P, const TileOrigin& o,
+                                          const TS* __restrict__ src, TS* tile, int ld, int lt,
+                                          int tpt) {
+  const int lb = P.lb, TB = 1 << lb, n = (1 << P.la) * TB;
+  if (NP + NC > 0 && P.rowinv && (tpt & (TB - 1)) == 0) {
+    const int ib = lt & (TB - 1);
+    if (ib >= o.tb) return;
+    int32_t off = o.sbase + ib * P.src_b;
+    bool valid = true;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int32_t v = o.pv[p] + ib * P.pb[p];
+      valid = valid && (p >= P.npred || (v >= P.plo[p] && v < P.phi[p]));
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c < P.nclamp) off += min(o.cv[c] + ib * P.cb[c], P.cmax[c]) * P.cstride[c];
+    const int step = tpt >> lb;
+#pragma unroll 4
+    for (int ia = lt >> lb; ia < o.ta; ia += step)
+      tile[ia * ld + ib] = valid ? __ldg(src + off + ia * P.src_a) : zero_of<TS>();
+    return;
+  }
+#pragma unroll 4
+  for (int idx = lt; idx < n; idx += tpt) {
+    const int ia = idx >> lb, ib = idx & (TB - 1);
+    if (ia < o.ta && ib < o.tb) tile[ia * ld + ib] = load_elem<NP, NC>(P, o, src, ia, ib);
+  }
 }
 
 // SMEM-staged transpose: read along b (source-contiguous), write along a
@@ -198,7 +239,7 @@ __device__ __forceinline__ TS load_elem(const DCParams& P, const TileOrigin& o,
 // Tiles are sized to the digit extents; G = 1 << lg small tiles are packed
 // per CTA batch (TPT = 256 >> lg threads each) so short unfolded rows
 // (e.g. B_w = 10) do not leave most threads idle.
-template <typename TS, typename TD, bool PC>
+template <typename TS, typename TD, int NP, int NC>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_transpose(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -212,12 +253,8 @@ __global__ void __launch_bounds__(kCopyThreads)
     TileOrigin o;
     const bool ok = t < P.ntiles;
     if (ok) {
-      decode_tile<PC>(P, static_cast<uint32_t>(t), o);
-#pragma unroll 4
-      for (int idx = lt; idx < n; idx += tpt) {
-        const int ia = idx >> lb, ib = idx & (TB - 1);
-        if (ia < o.ta && ib < o.tb) tile[ia * ld + ib] = load_elem<PC>(P, o, src, ia, ib);
-      }
+      decode_tile<NP, NC>(P, static_cast<uint32_t>(t), o);
+      load_tile<NP, NC>(P, o, src, tile, ld, lt, tpt);
     }
     __syncthreads();
     if (ok) {
@@ -234,7 +271,7 @@ __global__ void __launch_bounds__(kCopyThreads)
 
 // Direct copy: a fastest on both sides (coalesced destination; the source is
 // coalesced too when its a-stride is 1). Same tile packing as above.
-template <typename TS, typename TD, bool PC>
+template <typename TS, typename TD, int NP, int NC>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_direct(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
   const int la = P.la, lb = P.lb, lg = P.lg;
@@ -245,7 +282,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     const int t = base + q;
     if (t >= P.ntiles) continue;
     TileOrigin o;
-    decode_tile<PC>(P, static_cast<uint32_t>(t), o);
+    decode_tile<NP, NC>(P, static_cast<uint32_t>(t), o);
     constexpr int U = 4;
     for (int i0 = lt; i0 < n; i0 += tpt * U) {
       TS v[U];
@@ -253,7 +290,7 @@ __global__ void __launch_bounds__(kCopyThreads)
       for (int u = 0; u < U; ++u) {
         const int idx = i0 + u * tpt;
         const int a = idx & (TA - 1), b = idx >> la;
-        if (idx < n && a < o.ta && b < o.tb) v[u] = load_elem<PC>(P, o, src, a, b);
+        if (idx < n && a < o.ta && b < o.tb) v[u] = load_elem<NP, NC>(P, o, src, a, b);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -323,7 +360,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     TileOrigin o;
     const bool ok = t < P.ntiles;
     if (ok) {
-      decode_tile<false>(P, static_cast<uint32_t>(t), o);
+      decode_tile<0, 0>(P, static_cast<uint32_t>(t), o);
       const int tbv = o.tb / V;
 #pragma unroll 2
       for (int idx = lt; idx < nv; idx += tpt) {
@@ -353,6 +390,45 @@ __global__ void __launch_bounds__(kCopyThreads)
   }
 }
 
+// Transpose with guarded/clamped scalar loads (K2: Padding guards, unfold
+// overhang clamps, unaligned source rows) and 16-B vector stores along a.
+template <typename TS, typename TD, int NP, int NC>
+__global__ void __launch_bounds__(kCopyThreads)
+    digit_transpose_vst(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  constexpr int V = 16 / sizeof(TD);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int la = P.la, lb = P.lb, lg = P.lg;
+  const int TA = 1 << la, TB = 1 << lb, ld = TB + 1, n = TA * TB;
+  const int lav = la - __ffs(V) + 1;
+  const int tpt = kCopyThreads >> lg;
+  const int q = threadIdx.x >> (8 - lg), lt = threadIdx.x & (tpt - 1);
+  TS* tile = reinterpret_cast<TS*>(smem_raw) + q * TA * ld;
+  for (int base = blockIdx.x << lg; base < P.ntiles; base += gridDim.x << lg) {
+    const int t = base + q;
+    TileOrigin o;
+    const bool ok = t < P.ntiles;
+    if (ok) {
+      decode_tile<NP, NC>(P, static_cast<uint32_t>(t), o);
+      load_tile<NP, NC>(P, o, src, tile, ld, lt, tpt);
+    }
+    __syncthreads();
+    if (ok) {
+      const int tav = o.ta / V;
+#pragma unroll 2
+      for (int idx = lt; idx < n / V; idx += tpt) {
+        const int iav = idx & ((TA / V) - 1), ib = idx >> lav;
+        if (iav < tav && ib < o.tb) {
+          TD v[V];
+#pragma unroll
+          for (int j = 0; j < V; ++j) v[j] = convert<TS, TD>(tile[(iav * V + j) * ld + ib]);
+          st_vec<TD, V>(dst + o.dbase + iav * V + ib * P.dst_b, v);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Direct: a is contiguous on both sides; V-vectors along a.
 template <typename TS, typename TD>
 __global__ void __launch_bounds__(kCopyThreads)
@@ -367,7 +443,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     const int t = base + q;
     if (t >= P.ntiles) continue;
     TileOrigin o;
-    decode_tile<false>(P, static_cast<uint32_t>(t), o);
+    decode_tile<0, 0>(P, static_cast<uint32_t>(t), o);
     const int tav = o.ta / V;
     constexpr int U = 4;
     for (int i0 = lt; i0 < nv; i0 += tpt * U) {
@@ -620,11 +696,20 @@ static DCParams make_params(const DigitMap& m, int src_elem, int dst_elem) {
     la = std::min(log2_ceil(ea), 12);
     lb = std::max(0, std::min(12 - la, log2_ceil(std::max<int64_t>(eb, 1))));
   }
+  // Otherwise a transpose can still store 16-B vectors along a (K2 with
+  // guards/clamps or an unaligned source): VS = 16 / sizeof(dst) elements.
+  const int VS = 16 / elem_size(dst_elem);
+  const int lvs = log2_ceil(VS);
+  bool vst = !vec && transpose && m.dst_stride[a] == 1 && ea % VS == 0 && lvs <= 5;
+  for (int d = 0; d < nd && vst; ++d)
+    if (d != a && m.dst_stride[d] % VS != 0) vst = false;
   if (vec) {
     la = std::max(la, lv);
     if (transpose) lb = std::max(lb, lv);
   }
-  const int min_la = vec ? lv : 1, min_lb = vec && transpose ? lv : (transpose ? 1 : 0);
+  if (vst) la = std::max(la, lvs);
+  const int min_la = vec ? lv : (vst ? lvs : 1),
+            min_lb = vec && transpose ? lv : (transpose ? 1 : 0);
   auto ntiles_for = [&](int x, int y) {
     return outer_ext * ((ea + (int64_t(1) << x) - 1) >> x) * ((eb + (int64_t(1) << y) - 1) >> y);
   };
@@ -633,8 +718,10 @@ static DCParams make_params(const DigitMap& m, int src_elem, int dst_elem) {
     else if (la > min_la) --la;
     else break;
   }
-  P.vec = vec ? 1 : 0;
-  P.lg = std::max(0, std::min(5, 11 - la - lb));
+  P.vec = vec ? 1 : (vst ? 2 : 0);
+  // ~16 elements per thread per tile for transposes (one warp per 512-element
+  // tile amortises the per-tile digit decode), ~8 for direct copies.
+  P.lg = std::max(0, std::min(5, (transpose ? 12 : 11) - la - lb));
   P.transpose = transpose ? 1 : 0;
   P.la = la;
   P.lb = lb;
@@ -645,6 +732,11 @@ static DCParams make_params(const DigitMap& m, int src_elem, int dst_elem) {
   P.ftiles_b = make_fastdiv(tiles_b);
   P.npred = m.npred;
   P.nclamp = m.nclamp;
+  P.rowinv = 1;
+  for (int p = 0; p < m.npred && nd; ++p)
+    if (m.pcoef[p][a] != 0) P.rowinv = 0;
+  for (int c = 0; c < m.nclamp && nd; ++c)
+    if (m.ccoef[c][a] != 0) P.rowinv = 0;
   P.src_base = i32(m.src_base);
   if (nd) {
     P.dst_a = i32(m.dst_stride[a]);
@@ -689,35 +781,52 @@ cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, con
                               void* dst, cudaStream_t stream, KernelInfo* info) {
   if (m.dst_numel == 0) return cudaSuccess;
   DCParams P = make_params(m, src_elem, dst_elem);
-  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) P.vec = 0;
-  // Enough CTAs for 8 resident per SM; each walks tiles grid-stride.
-  int64_t grid = std::min<int64_t>((P.ntiles + (1 << P.lg) - 1) >> P.lg, 148 * 8);
+  if (P.vec == 1 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15))
+    P.vec = 0;
+  if (P.vec == 2 && (reinterpret_cast<uintptr_t>(dst) & 15)) P.vec = 0;
   const int V = 16 / std::min(elem_size(src_elem), elem_size(dst_elem));
   size_t smem = P.transpose ? (static_cast<size_t>(1) << P.lg) * (1 << P.la) *
-                                  ((1 << P.lb) + (P.vec ? V : 1)) * elem_size(src_elem)
+                                  ((1 << P.lb) + (P.vec == 1 ? V : 1)) * elem_size(src_elem)
                             : 0;
-  if (info) {
-    info->name = P.transpose ? (P.vec ? "digit_copy_transpose_v16" : "digit_copy_transpose")
+  const int64_t batches = (P.ntiles + (1 << P.lg) - 1) >> P.lg;
+  if (info)
+    info->name = P.transpose ? (P.vec == 1   ? "digit_copy_transpose_v16"
+                                : P.vec == 2 ? "digit_copy_transpose_st16"
+                                             : "digit_copy_transpose")
                              : (P.vec ? "digit_copy_direct_v16" : "digit_copy_direct");
-    info->grid = grid;
-  }
   return dispatch<Unused>(src_elem, dst_elem, [&](auto s, auto d) -> cudaError_t {
     using TS = decltype(s);
     using TD = decltype(d);
-    const bool pc = P.npred > 0 || P.nclamp > 0;
-    const unsigned g = static_cast<unsigned>(grid);
-    const TS* s_ = static_cast<const TS*>(src);
-    TD* d_ = static_cast<TD*>(dst);
-    if (P.vec) {
-      if (P.transpose) digit_transpose_vec<TS, TD><<<g, kCopyThreads, smem, stream>>>(P, s_, d_);
-      else digit_direct_vec<TS, TD><<<g, kCopyThreads, 0, stream>>>(P, s_, d_);
-    } else if (P.transpose) {
-      if (pc) digit_transpose<TS, TD, true><<<g, kCopyThreads, smem, stream>>>(P, s_, d_);
-      else digit_transpose<TS, TD, false><<<g, kCopyThreads, smem, stream>>>(P, s_, d_);
-    } else {
-      if (pc) digit_direct<TS, TD, true><<<g, kCopyThreads, 0, stream>>>(P, s_, d_);
-      else digit_direct<TS, TD, false><<<g, kCopyThreads, 0, stream>>>(P, s_, d_);
-    }
+    using Kern = void (*)(const DCParams, const TS* __restrict__, TD* __restrict__);
+    // guard/clamp mode: none, small (<= 2 + <= 2: 2-D Padding + unfold), general
+    const int mode = P.npred == 0 && P.nclamp == 0 ? 0 : (P.npred <= 2 && P.nclamp <= 2 ? 1 : 2);
+    Kern k;
+    if (P.vec == 2)
+      k = mode == 0   ? digit_transpose_vst<TS, TD, 0, 0>
+          : mode == 1 ? digit_transpose_vst<TS, TD, 2, 2>
+                      : digit_transpose_vst<TS, TD, kMaxPred, kMaxClamp>;
+    else if (P.vec) k = P.transpose ? digit_transpose_vec<TS, TD> : digit_direct_vec<TS, TD>;
+    else if (P.transpose)
+      k = mode == 0   ? digit_transpose<TS, TD, 0, 0>
+          : mode == 1 ? digit_transpose<TS, TD, 2, 2>
+                      : digit_transpose<TS, TD, kMaxPred, kMaxClamp>;
+    else
+      k = mode == 0   ? digit_direct<TS, TD, 0, 0>
+          : mode == 1 ? digit_direct<TS, TD, 2, 2>
+                      : digit_direct<TS, TD, kMaxPred, kMaxClamp>;
+    // One full wave of resident CTAs (occupancy-derived), each walking tile
+    // batches grid-stride: no partial second wave.
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kCopyThreads, smem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(batches, int64_t(nsm) * per_sm));
+    if (info) info->grid = grid;
+    k<<<static_cast<unsigned>(grid), kCopyThreads, smem, stream>>>(
+        P, static_cast<const TS*>(src), static_cast<TD*>(dst));
     return cudaGetLastError();
   });
 }
