@@ -66,7 +66,14 @@ enum {
   LFGPU_OP_RELU = 4,
   LFGPU_OP_BIASADD = 5,
   LFGPU_OP_EWADD = 6,
-  LFGPU_OP_LAYOUT_CONVERT = 7
+  LFGPU_OP_LAYOUT_CONVERT = 7,
+  /* Extensions beyond lf::OpKind (the pools ResNet-18 needs).
+   * Like Padding they are not element-wise and block propagation.
+   * MaxPool: out[b,c,h,w] = max_{rh,rw < window} in[b,c,V*h+rh,V*w+rw] on an
+   *   explicitly padded input (no implicit padding, like C2D).
+   * GlobalAvgPool: out[b,c] = (sum_{h,w} in[b,c,h,w]) / (H*W), rank 4 -> 2. */
+  LFGPU_OP_MAXPOOL = 8,
+  LFGPU_OP_GLOBAL_AVGPOOL = 9
 };
 
 /* lf::DType (ir.hpp:26) and lf::Role (ir.hpp:27) */
@@ -127,8 +134,8 @@ typedef struct lfgpu_node {
   int32_t ninputs;
   int32_t inputs[2];
   int32_t output;
-  int32_t reserved;
-  int64_t stride; /* attrs["stride"], C2D/DEP (default 1) */
+  int32_t window; /* MaxPool window (KH = KW); 0 elsewhere */
+  int64_t stride; /* attrs["stride"], C2D/DEP/MaxPool (default 1) */
   int64_t pad;    /* attrs["pad"], Padding (default 0)    */
 } lfgpu_node;
 

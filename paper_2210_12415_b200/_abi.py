@@ -16,6 +16,7 @@ OK, EINVAL, EUNSUPPORTED, ECUDA, ERANGE = 0, 1, 2, 3, 4
 SPLIT, REORDER, FUSE, UNFOLD, PAD, STORE_AT, FOLD, UNPAD, DECOUPLE_AT = range(9)
 # lf::OpKind (ir.hpp:42)
 C2D, DEP, GMM, PADDING, RELU, BIASADD, EWADD, LAYOUT_CONVERT = range(8)
+MAXPOOL, GLOBAL_AVGPOOL = 8, 9  # extensions beyond lf::OpKind (lfgpu.h)
 # lf::DType / lf::Role
 F32, I32 = 0, 1
 INPUT, CONSTANT, INTERMEDIATE, OUTPUT = range(4)
@@ -67,7 +68,7 @@ class Node(C.Structure):
         ("ninputs", C.c_int32),
         ("inputs", C.c_int32 * 2),
         ("output", C.c_int32),
-        ("reserved", C.c_int32),
+        ("window", C.c_int32),
         ("stride", C.c_int64),
         ("pad", C.c_int64),
     ]

@@ -18,6 +18,7 @@
 #include <climits>
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "lf_core.hpp"
 #include "lf_kernels.hpp"
@@ -125,23 +126,31 @@ struct DCParams {
       cstride[kMaxClamp];
   int32_t src_base;
   int32_t vec;     // 1: the 16-B vector kernels apply; 2: vector stores only
-  int32_t rowinv;  // guards and clamps do not depend on digit a
+  int32_t rowinv;  // guards/clamps independent of digit a; tables depend on a or b only
+  int32_t ntab;
+  int32_t ta[kMaxTab], tb[kMaxTab], tconst[kMaxTab], tmax[kMaxTab], toff[kMaxTab];
+  int32_t otab[kMaxTab][kMaxDig];
+  const int32_t* tab;  // source offset tables (DigitMap::toff), device memory
 };
 
 struct TileOrigin {
   int32_t dbase, sbase;
-  int32_t pv[kMaxPred], cv[kMaxClamp];
+  int32_t pv[kMaxPred], cv[kMaxClamp], tv[kMaxTab];
   int32_t ta, tb;  // valid extents of this tile
 };
+
+__device__ __forceinline__ int32_t tab_at(const DCParams& P, int t, int32_t v) {
+  return __ldg(P.tab + P.toff[t] + min(max(v, 0), P.tmax[t]));
+}
 
 // Param arrays are only ever indexed with compile-time indices (unrolled,
 // guarded loops): a runtime index would make nvcc address the parameter
 // buffer through a generic pointer, i.e. a global-latency load per access.
 // NP / NC: compile-time bounds on the guard / clamp counts (P.npred <= NP,
 // P.nclamp <= NC); the unrolled per-digit terms cost NP + NC IMADs each.
-template <int NP, int NC>
+template <int NP, int NC, int NT = 0>
 __device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileOrigin& o) {
-  constexpr bool PC = NP + NC > 0;
+  constexpr bool PC = NP + NC + NT > 0;
   uint32_t q = fdiv(t, P.ftiles_a);
   const int32_t ia0 = static_cast<int32_t>(t - q * P.ftiles_a.d) << P.la;
   t = q;
@@ -155,6 +164,8 @@ __device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileO
     for (int p = 0; p < NP; ++p) o.pv[p] = P.pconst[p] + ia0 * P.pa[p] + ib0 * P.pb[p];
 #pragma unroll
     for (int c = 0; c < NC; ++c) o.cv[c] = P.cconst[c] + ia0 * P.ca[c] + ib0 * P.cb[c];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) o.tv[k] = P.tconst[k] + ia0 * P.ta[k] + ib0 * P.tb[k];
   }
 #pragma unroll
   for (int d = kMaxDig - 1; d >= 0; --d) {
@@ -169,6 +180,8 @@ __device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileO
         for (int p = 0; p < NP; ++p) o.pv[p] += x * P.opred[p][d];
 #pragma unroll
         for (int c = 0; c < NC; ++c) o.cv[c] += x * P.oclamp[c][d];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) o.tv[k] += x * P.otab[k][d];
       }
     }
   }
@@ -178,11 +191,14 @@ __device__ __forceinline__ void decode_tile(const DCParams& P, uint32_t t, TileO
   o.tb = min(1 << P.lb, P.eb - ib0);
 }
 
-template <int NP, int NC, typename TS>
+template <int NP, int NC, int NT, typename TS>
 __device__ __forceinline__ TS load_elem(const DCParams& P, const TileOrigin& o,
                                         const TS* __restrict__ src, int ia, int ib) {
   int32_t off = o.sbase + ia * P.src_a + ib * P.src_b;
-  if (NP + NC == 0) return __ldg(src + off);
+  if (NP + NC + NT == 0) return __ldg(src + off);
+#pragma unroll
+  for (int k = 0; k < NT; ++k)
+    if (k < P.ntab) off += tab_at(P, k, o.tv[k] + ia * P.ta[k] + ib * P.tb[k]);
   bool valid = true;
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
@@ -203,12 +219,12 @@ __device__ __forceinline__ TS load_elem(const DCParams& P, const TileOrigin& o,
 // digits, a is the channel brick) and a thread's column ib is fixed across
 // its iterations (tpt a multiple of TB), the guard/clamp terms are
 // evaluated once per tile and each element costs one guarded load.
-template <int NP, int NC, typename TS>
+template <int NP, int NC, int NT, typename TS>
 __device__ __forceinline__ void load_tile(const DCParams& P, const TileOrigin& o,
                                           const TS* __restrict__ src, TS* tile, int ld, int lt,
                                           int tpt) {
   const int lb = P.lb, TB = 1 << lb, n = (1 << P.la) * TB;
-  if (NP + NC > 0 && P.rowinv && (tpt & (TB - 1)) == 0) {
+  if (NP + NC + NT > 0 && P.rowinv && (tpt & (TB - 1)) == 0) {
     const int ib = lt & (TB - 1);
     if (ib >= o.tb) return;
     int32_t off = o.sbase + ib * P.src_b;
@@ -221,16 +237,25 @@ __device__ __forceinline__ void load_tile(const DCParams& P, const TileOrigin& o
 #pragma unroll
     for (int c = 0; c < NC; ++c)
       if (c < P.nclamp) off += min(o.cv[c] + ib * P.cb[c], P.cmax[c]) * P.cstride[c];
+    // table terms on the column (b) side here, on the row (a) side per element
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+      if (k < P.ntab && P.ta[k] == 0) off += tab_at(P, k, o.tv[k] + ib * P.tb[k]);
     const int step = tpt >> lb;
 #pragma unroll 4
-    for (int ia = lt >> lb; ia < o.ta; ia += step)
-      tile[ia * ld + ib] = valid ? __ldg(src + off + ia * P.src_a) : zero_of<TS>();
+    for (int ia = lt >> lb; ia < o.ta; ia += step) {
+      int32_t e = off + ia * P.src_a;
+#pragma unroll
+      for (int k = 0; k < NT; ++k)
+        if (k < P.ntab && P.ta[k] != 0) e += tab_at(P, k, o.tv[k] + ia * P.ta[k]);
+      tile[ia * ld + ib] = valid ? __ldg(src + e) : zero_of<TS>();
+    }
     return;
   }
 #pragma unroll 4
   for (int idx = lt; idx < n; idx += tpt) {
     const int ia = idx >> lb, ib = idx & (TB - 1);
-    if (ia < o.ta && ib < o.tb) tile[ia * ld + ib] = load_elem<NP, NC>(P, o, src, ia, ib);
+    if (ia < o.ta && ib < o.tb) tile[ia * ld + ib] = load_elem<NP, NC, NT>(P, o, src, ia, ib);
   }
 }
 
@@ -239,7 +264,7 @@ __device__ __forceinline__ void load_tile(const DCParams& P, const TileOrigin& o
 // Tiles are sized to the digit extents; G = 1 << lg small tiles are packed
 // per CTA batch (TPT = 256 >> lg threads each) so short unfolded rows
 // (e.g. B_w = 10) do not leave most threads idle.
-template <typename TS, typename TD, int NP, int NC>
+template <typename TS, typename TD, int NP, int NC, int NT>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_transpose(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -253,8 +278,8 @@ __global__ void __launch_bounds__(kCopyThreads)
     TileOrigin o;
     const bool ok = t < P.ntiles;
     if (ok) {
-      decode_tile<NP, NC>(P, static_cast<uint32_t>(t), o);
-      load_tile<NP, NC>(P, o, src, tile, ld, lt, tpt);
+      decode_tile<NP, NC, NT>(P, static_cast<uint32_t>(t), o);
+      load_tile<NP, NC, NT>(P, o, src, tile, ld, lt, tpt);
     }
     __syncthreads();
     if (ok) {
@@ -271,7 +296,7 @@ __global__ void __launch_bounds__(kCopyThreads)
 
 // Direct copy: a fastest on both sides (coalesced destination; the source is
 // coalesced too when its a-stride is 1). Same tile packing as above.
-template <typename TS, typename TD, int NP, int NC>
+template <typename TS, typename TD, int NP, int NC, int NT>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_direct(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
   const int la = P.la, lb = P.lb, lg = P.lg;
@@ -282,7 +307,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     const int t = base + q;
     if (t >= P.ntiles) continue;
     TileOrigin o;
-    decode_tile<NP, NC>(P, static_cast<uint32_t>(t), o);
+    decode_tile<NP, NC, NT>(P, static_cast<uint32_t>(t), o);
     constexpr int U = 4;
     for (int i0 = lt; i0 < n; i0 += tpt * U) {
       TS v[U];
@@ -290,7 +315,7 @@ __global__ void __launch_bounds__(kCopyThreads)
       for (int u = 0; u < U; ++u) {
         const int idx = i0 + u * tpt;
         const int a = idx & (TA - 1), b = idx >> la;
-        if (idx < n && a < o.ta && b < o.tb) v[u] = load_elem<NP, NC>(P, o, src, a, b);
+        if (idx < n && a < o.ta && b < o.tb) v[u] = load_elem<NP, NC, NT>(P, o, src, a, b);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -360,7 +385,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     TileOrigin o;
     const bool ok = t < P.ntiles;
     if (ok) {
-      decode_tile<0, 0>(P, static_cast<uint32_t>(t), o);
+      decode_tile<0, 0, 0>(P, static_cast<uint32_t>(t), o);
       const int tbv = o.tb / V;
 #pragma unroll 2
       for (int idx = lt; idx < nv; idx += tpt) {
@@ -392,7 +417,7 @@ __global__ void __launch_bounds__(kCopyThreads)
 
 // Transpose with guarded/clamped scalar loads (K2: Padding guards, unfold
 // overhang clamps, unaligned source rows) and 16-B vector stores along a.
-template <typename TS, typename TD, int NP, int NC>
+template <typename TS, typename TD, int NP, int NC, int NT>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_transpose_vst(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
   constexpr int V = 16 / sizeof(TD);
@@ -408,8 +433,8 @@ __global__ void __launch_bounds__(kCopyThreads)
     TileOrigin o;
     const bool ok = t < P.ntiles;
     if (ok) {
-      decode_tile<NP, NC>(P, static_cast<uint32_t>(t), o);
-      load_tile<NP, NC>(P, o, src, tile, ld, lt, tpt);
+      decode_tile<NP, NC, NT>(P, static_cast<uint32_t>(t), o);
+      load_tile<NP, NC, NT>(P, o, src, tile, ld, lt, tpt);
     }
     __syncthreads();
     if (ok) {
@@ -443,7 +468,7 @@ __global__ void __launch_bounds__(kCopyThreads)
     const int t = base + q;
     if (t >= P.ntiles) continue;
     TileOrigin o;
-    decode_tile<0, 0>(P, static_cast<uint32_t>(t), o);
+    decode_tile<0, 0, 0>(P, static_cast<uint32_t>(t), o);
     const int tav = o.ta / V;
     constexpr int U = 4;
     for (int i0 = lt; i0 < nv; i0 += tpt * U) {
@@ -678,7 +703,8 @@ static DCParams make_params(const DigitMap& m, int src_elem, int dst_elem) {
   // divides the vector digits' extents and every other stride on that side.
   const int V = 16 / std::min(elem_size(src_elem), elem_size(dst_elem));
   const int lv = log2_ceil(V);
-  bool vec = nd >= 1 && m.npred == 0 && m.nclamp == 0 && m.dst_stride[a] == 1 && ea % V == 0 &&
+  bool vec = nd >= 1 && m.npred == 0 && m.nclamp == 0 && m.ntab == 0 && m.dst_stride[a] == 1 &&
+             ea % V == 0 &&
              m.src_base % V == 0;
   if (vec) {
     const int sv = transpose ? b : a;  // the source digit read as vectors
@@ -737,6 +763,16 @@ static DCParams make_params(const DigitMap& m, int src_elem, int dst_elem) {
     if (m.pcoef[p][a] != 0) P.rowinv = 0;
   for (int c = 0; c < m.nclamp && nd; ++c)
     if (m.ccoef[c][a] != 0) P.rowinv = 0;
+  P.ntab = m.ntab;
+  for (int t = 0; t < m.ntab; ++t) {
+    const int64_t ca_ = nd ? m.tcoef[t][a] : 0, cb_ = b >= 0 ? m.tcoef[t][b] : 0;
+    if (ca_ != 0 && cb_ != 0) P.rowinv = 0;
+    P.ta[t] = i32(ca_);
+    P.tb[t] = i32(cb_);
+    P.tconst[t] = i32(m.tconst[t]);
+    P.tmax[t] = i32(m.tmax[t]);
+    P.toff[t] = i32(m.toff[t]);
+  }
   P.src_base = i32(m.src_base);
   if (nd) {
     P.dst_a = i32(m.dst_stride[a]);
@@ -769,6 +805,7 @@ static DCParams make_params(const DigitMap& m, int src_elem, int dst_elem) {
     P.osrc[k] = i32(m.src_stride[d]);
     for (int p = 0; p < m.npred; ++p) P.opred[p][k] = i32(m.pcoef[p][d]);
     for (int c = 0; c < m.nclamp; ++c) P.oclamp[c][k] = i32(m.ccoef[c][d]);
+    for (int t = 0; t < m.ntab; ++t) P.otab[t][k] = i32(m.tcoef[t][d]);
     outer *= m.ext[d];
     ++k;
   }
@@ -778,9 +815,12 @@ static DCParams make_params(const DigitMap& m, int src_elem, int dst_elem) {
 }
 
 cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, const void* src,
-                              void* dst, cudaStream_t stream, KernelInfo* info) {
+                              void* dst, cudaStream_t stream, KernelInfo* info,
+                              const int32_t* d_tab) {
   if (m.dst_numel == 0) return cudaSuccess;
+  if (m.ntab > 0 && (!d_tab || src_elem != LFGPU_ELEM_F32)) return cudaErrorInvalidValue;
   DCParams P = make_params(m, src_elem, dst_elem);
+  P.tab = d_tab;
   if (P.vec == 1 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15))
     P.vec = 0;
   if (P.vec == 2 && (reinterpret_cast<uintptr_t>(dst) & 15)) P.vec = 0;
@@ -798,22 +838,33 @@ cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, con
     using TS = decltype(s);
     using TD = decltype(d);
     using Kern = void (*)(const DCParams, const TS* __restrict__, TD* __restrict__);
-    // guard/clamp mode: none, small (<= 2 + <= 2: 2-D Padding + unfold), general
-    const int mode = P.npred == 0 && P.nclamp == 0 ? 0 : (P.npred <= 2 && P.nclamp <= 2 ? 1 : 2);
-    Kern k;
-    if (P.vec == 2)
-      k = mode == 0   ? digit_transpose_vst<TS, TD, 0, 0>
-          : mode == 1 ? digit_transpose_vst<TS, TD, 2, 2>
-                      : digit_transpose_vst<TS, TD, kMaxPred, kMaxClamp>;
+    // guard/clamp mode: none, small (<= 2 + <= 2: 2-D Padding + unfold),
+    // general, general + source tables (fp32 sources only)
+    const int mode = P.ntab > 0 ? 3
+                     : P.npred == 0 && P.nclamp == 0 ? 0
+                     : (P.npred <= 2 && P.nclamp <= 2 ? 1 : 2);
+    Kern k = nullptr;
+    if (mode == 3) {
+      if constexpr (std::is_same_v<TS, float>) {
+        if (P.vec == 2) k = digit_transpose_vst<TS, TD, kMaxPred, kMaxClamp, kMaxTab>;
+        else if (P.transpose) k = digit_transpose<TS, TD, kMaxPred, kMaxClamp, kMaxTab>;
+        else k = digit_direct<TS, TD, kMaxPred, kMaxClamp, kMaxTab>;
+      } else {
+        return cudaErrorInvalidValue;
+      }
+    } else if (P.vec == 2)
+      k = mode == 0   ? digit_transpose_vst<TS, TD, 0, 0, 0>
+          : mode == 1 ? digit_transpose_vst<TS, TD, 2, 2, 0>
+                      : digit_transpose_vst<TS, TD, kMaxPred, kMaxClamp, 0>;
     else if (P.vec) k = P.transpose ? digit_transpose_vec<TS, TD> : digit_direct_vec<TS, TD>;
     else if (P.transpose)
-      k = mode == 0   ? digit_transpose<TS, TD, 0, 0>
-          : mode == 1 ? digit_transpose<TS, TD, 2, 2>
-                      : digit_transpose<TS, TD, kMaxPred, kMaxClamp>;
+      k = mode == 0   ? digit_transpose<TS, TD, 0, 0, 0>
+          : mode == 1 ? digit_transpose<TS, TD, 2, 2, 0>
+                      : digit_transpose<TS, TD, kMaxPred, kMaxClamp, 0>;
     else
-      k = mode == 0   ? digit_direct<TS, TD, 0, 0>
-          : mode == 1 ? digit_direct<TS, TD, 2, 2>
-                      : digit_direct<TS, TD, kMaxPred, kMaxClamp>;
+      k = mode == 0   ? digit_direct<TS, TD, 0, 0, 0>
+          : mode == 1 ? digit_direct<TS, TD, 2, 2, 0>
+                      : digit_direct<TS, TD, kMaxPred, kMaxClamp, 0>;
     // One full wave of resident CTAs (occupancy-derived), each walking tile
     // batches grid-stride: no partial second wave.
     int per_sm = 0;

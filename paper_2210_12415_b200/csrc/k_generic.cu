@@ -15,6 +15,8 @@
 // (interp.cpp:70-122).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "lf_core.hpp"
 #include "lf_generic.hpp"
 
@@ -168,6 +170,32 @@ __global__ void __launch_bounds__(256)
     decode_phys(sp, f, s);
     ix_exec(sp, s);
     Acc acc = 0;
+    if (P.op == GEN_MAXPOOL) {
+      // max over the window of A(b, c, V*h+rh, V*w+rw) on a padded input
+      const int64_t* ta = P.ta;
+      const int64_t a1 = ta[P.a_off[0] + s.v[0]] + ta[P.a_off[1] + s.v[1]];
+      const int h = s.v[2], w = s.v[3];
+      Acc m = static_cast<Acc>(A[a1 + ta[P.a_off[2] + P.V * h] + ta[P.a_off[3] + P.V * w]]);
+      for (int64_t rh = 0; rh < P.KH; ++rh) {
+        const int64_t a2 = a1 + ta[P.a_off[2] + P.V * h + rh];
+        for (int64_t rw = 0; rw < P.KW; ++rw) {
+          const Acc x = static_cast<Acc>(A[a2 + ta[P.a_off[3] + P.V * w + rw]]);
+          m = x > m ? x : m;
+        }
+      }
+      out[f] = static_cast<T>(m);
+      continue;
+    }
+    if (P.op == GEN_GLOBAL_AVGPOOL) {
+      const int64_t* ta = P.ta;
+      const int64_t a1 = ta[P.a_off[0] + s.v[0]] + ta[P.a_off[1] + s.v[1]];
+      for (int64_t h = 0; h < P.H; ++h) {
+        const int64_t a2 = a1 + ta[P.a_off[2] + h];
+        for (int64_t w = 0; w < P.W; ++w) acc += static_cast<Acc>(A[a2 + ta[P.a_off[3] + w]]);
+      }
+      out[f] = static_cast<T>(acc / static_cast<Acc>(P.H * P.W));
+      continue;
+    }
     if (P.op == GEN_GMM) {
       const int64_t* ta = P.ta;
       const int64_t* tb = P.tb;
@@ -212,6 +240,89 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Few outputs, long reductions (FC at small batch, GlobalAvgPool, a
+// downsample conv on a layout tcgen05 cannot consume): one warp per output
+// element, lanes split the flattened reduction index r and combine with
+// shuffles. Same operand tables as gen_contract.
+template <typename T, typename Acc>
+__global__ void __launch_bounds__(256)
+    gen_contract_warp(const IxProgram* __restrict__ out_prog, GenContract P, T* __restrict__ out) {
+  __shared__ IxProgram sp;
+  {
+    const int* g = reinterpret_cast<const int*>(out_prog);
+    int* s = reinterpret_cast<int*>(&sp);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(IxProgram) / 4); i += blockDim.x)
+      s[i] = g[i];
+  }
+  __syncthreads();
+  const T* A = static_cast<const T*>(P.a);
+  const T* B = static_cast<const T*>(P.b);
+  const int64_t* ta = P.ta;
+  const int64_t* tb = P.tb;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const bool is_max = P.op == GEN_MAXPOOL;
+  int64_t R;
+  switch (P.op) {
+    case GEN_GMM: R = P.K; break;
+    case GEN_C2D: R = P.I * P.KH * P.KW; break;
+    case GEN_GLOBAL_AVGPOOL: R = P.H * P.W; break;
+    default: R = P.KH * P.KW; break;  // DEP, MaxPool
+  }
+  const int64_t khw = P.KH * P.KW;
+  for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); f < P.n;
+       f += warps) {
+    IxState s;
+    decode_phys(sp, f, s);
+    ix_exec(sp, s);
+    Acc acc = 0;
+    bool any = false;
+    for (int64_t r = lane; r < R; r += 32) {
+      Acc x;
+      if (P.op == GEN_GMM) {
+        x = static_cast<Acc>(A[ta[P.a_off[0] + s.v[0]] + ta[P.a_off[1] + r]]) *
+            static_cast<Acc>(B[tb[P.b_off[0] + r] + tb[P.b_off[1] + s.v[1]]]);
+      } else if (P.op == GEN_GLOBAL_AVGPOOL) {
+        const int64_t h = r / P.W, w = r - h * P.W;
+        x = static_cast<Acc>(A[ta[P.a_off[0] + s.v[0]] + ta[P.a_off[1] + s.v[1]] +
+                               ta[P.a_off[2] + h] + ta[P.a_off[3] + w]]);
+      } else if (P.op == GEN_C2D) {
+        const int64_t i = r / khw, rr = r - i * khw, rh = rr / P.KW, rw = rr - rh * P.KW;
+        x = static_cast<Acc>(A[ta[P.a_off[0] + s.v[0]] + ta[P.a_off[1] + i] +
+                               ta[P.a_off[2] + P.V * s.v[2] + rh] +
+                               ta[P.a_off[3] + P.V * s.v[3] + rw]]) *
+            static_cast<Acc>(B[tb[P.b_off[0] + s.v[1]] + tb[P.b_off[1] + i] +
+                               tb[P.b_off[2] + rh] + tb[P.b_off[3] + rw]]);
+      } else {  // DEP / MaxPool window element
+        const int64_t rh = r / P.KW, rw = r - rh * P.KW;
+        const int64_t ao = ta[P.a_off[0] + s.v[0]] + ta[P.a_off[1] + s.v[1]] +
+                           ta[P.a_off[2] + P.V * s.v[2] + rh] + ta[P.a_off[3] + P.V * s.v[3] + rw];
+        x = static_cast<Acc>(A[ao]);
+        if (P.op == GEN_DEP)
+          x *= static_cast<Acc>(B[tb[P.b_off[0] + s.v[1]] + tb[P.b_off[1] + rh] + tb[P.b_off[2] + rw]]);
+      }
+      if (is_max) acc = any ? (x > acc ? x : acc) : x;
+      else acc += x;
+      any = true;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const Acc y = __shfl_xor_sync(0xffffffffu, acc, o);
+      const int ay = __shfl_xor_sync(0xffffffffu, any ? 1 : 0, o);
+      if (is_max) {
+        if (ay && (!any || y > acc)) acc = y;
+        any = any || ay;
+      } else {
+        acc += y;
+      }
+    }
+    if (lane == 0) {
+      if (P.op == GEN_GLOBAL_AVGPOOL) acc = acc / static_cast<Acc>(P.H * P.W);
+      out[f] = static_cast<T>(acc);
+    }
+  }
+}
+
 static int64_t grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   return b < 148 * 32 ? (b < 1 ? 1 : b) : 148 * 32;
@@ -231,6 +342,27 @@ cudaError_t launch_gen_eltwise(const IxProgram* d_prog, const GenEltwise& P, int
 cudaError_t launch_gen_contract(const IxProgram* d_prog, const GenContract& P, int elem,
                                 bool exact, void* out, cudaStream_t stream) {
   if (P.n == 0) return cudaSuccess;
+  int64_t R;
+  switch (P.op) {
+    case GEN_GMM: R = P.K; break;
+    case GEN_C2D: R = P.I * P.KH * P.KW; break;
+    case GEN_GLOBAL_AVGPOOL: R = P.H * P.W; break;
+    default: R = P.KH * P.KW; break;
+  }
+  // Warp per output when the outputs alone cannot fill the GPU with long
+  // serial reductions (148 SMs x 2048 threads).
+  if (R >= 32 && P.n * 8 <= 148 * 2048) {
+    const int64_t warps = std::min<int64_t>(P.n, 148 * 64);
+    const unsigned g = static_cast<unsigned>((warps + 7) / 8);
+    if (elem == LFGPU_ELEM_I32)
+      gen_contract_warp<int32_t, long long>
+          <<<g, 256, 0, stream>>>(d_prog, P, static_cast<int32_t*>(out));
+    else if (exact)
+      gen_contract_warp<float, double><<<g, 256, 0, stream>>>(d_prog, P, static_cast<float*>(out));
+    else
+      gen_contract_warp<float, float><<<g, 256, 0, stream>>>(d_prog, P, static_cast<float*>(out));
+    return cudaGetLastError();
+  }
   unsigned g = static_cast<unsigned>(grid_for(P.n));
   if (elem == LFGPU_ELEM_I32)
     gen_contract<int32_t, long long><<<g, 256, 0, stream>>>(d_prog, P, static_cast<int32_t*>(out));

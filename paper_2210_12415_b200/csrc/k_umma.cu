@@ -49,6 +49,12 @@ struct UmmaParams {
   unsigned long long* dbg;  // optional per-CTA %globaltimer checkpoints (8 per CTA)
   int32_t epi_mode;         // unused (diagnostics)
   int32_t epi_sig;          // EPI_SIG of a <= 3-op chain, -1 = generic
+  // Split-K: CTA (tile, split) accumulates stages [split*n/S, (split+1)*n/S);
+  // partial tiles go to `ws`, the last CTA of a tile (per-tile counter) sums
+  // them in split order and runs the fused epilogue.
+  int32_t splits;
+  float* ws;
+  int* counters;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -313,7 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   int64_t* s_row = s_col + P.BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
+  const int splits = P.splits;
+  const int tile = blockIdx.x / splits, split = blockIdx.x - tile * splits;
+  const int s_lo = split * P.nstages / splits, s_hi = (split + 1) * P.nstages / splits;
+  int* s_flag = reinterpret_cast<int*>(s_row + 128);
   unsigned long long* dbg = P.dbg ? P.dbg + 8 * tile : nullptr;
   const int pipe = P.pipe;
   const int early = 0;
@@ -356,11 +365,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
 
-  if (warp == 0) {
-    // ---- TMA producer (whole warp runs the loop; one elected lane issues).
-    // Coordinates = tile part (registers) + stage part (SMEM); views are
-    // always 5-D (host pads unit dims) so each load is one straight-line
-    // UTMALDG.5D with no rank dispatch.
+  // ---- TMA producers. One thread's serial issue path (barrier wait +
+  // expect_tx + UTMALDGs, ~450 cycles per stage measured) would cap a CTA at
+  // ~one stage per 0.25 us, so warps 0 and 2-4 (the epilogue warps are idle
+  // during the main loop) issue stages round-robin; each computes its own
+  // ring slot / phase. Coordinates = tile part (registers) + stage part
+  // (SMEM); views are always 5-D (host pads unit dims) so each load is one
+  // straight-line UTMALDG.5D with no rank dispatch.
+  constexpr int kProducers = 4;
+  const int prod = warp == 0 ? 0 : (warp >= 2 && warp <= 4 ? warp - 1 : -1);
+  if (prod >= 0) {
     int32_t ta[kMaxBoxes][5], tb[kMaxBoxes][5];
 #pragma unroll
     for (int b = 0; b < kMaxBoxes; ++b)
@@ -369,21 +383,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         ta[b][d] = s_tile->ca[b][d];
         tb[b][d] = s_tile->cb[b][d];
       }
-    const int na = P.a_boxes, nb = P.b_boxes, nst = P.nstages;
+    const int na = P.a_boxes, nb = P.b_boxes;
     const uint32_t tx = P.tx_bytes, a_slot = P.a_slot, b_slot = P.b_slot;
     const uint32_t ring0 = smem_u32(smem);
     const uint32_t b_off = na * a_slot;
     const bool leader = elect_one();
-    int slot = 0;
-    uint32_t phase = 0;
-    for (int s = 0; s < nst; ++s) {
+    for (int s = s_lo + prod; s < s_hi; s += kProducers) {
       if (leader) {
+        const int it = s - s_lo;
+        const int slot = it % pipe;
+        const uint32_t phase = static_cast<uint32_t>(it / pipe) & 1u;
+        const long long c_top = dbg ? clock64() : 0;
         mbar_wait(empty0 + 8 * slot, phase ^ 1);
+        const long long c_wait = dbg ? clock64() : 0;
         const uint32_t bar = full0 + 8 * slot;
         mbar_expect_tx(bar, tx);
         const StageEntry se = s_stage[s];
         if (dbg && s < 32) P.dbg[10 * gridDim.x + 64 * tile + s] = gtimer();
         const uint32_t a_dst = ring0 + slot * stage_bytes;
+        const long long c_issue = dbg ? clock64() : 0;
+        if (dbg && it < 32) {
+          P.dbg[106 * gridDim.x + 64 * tile + 2 * it] = c_wait - c_top;
+          P.dbg[106 * gridDim.x + 64 * tile + 2 * it + 1] = c_issue - c_wait;
+        }
 #pragma unroll
         for (int b = 0; b < kMaxBoxes; ++b)
           if (b < na)
@@ -395,26 +417,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load5(&tma_b, a_dst + b_off + b * b_slot, bar, tb[b][0] + se.sb[0],
                       tb[b][1] + se.sb[1], tb[b][2] + se.sb[2], tb[b][3] + se.sb[3],
                       tb[b][4] + se.sb[4]);
-      }
-      if (++slot == pipe) {
-        slot = 0;
-        phase ^= 1;
+        if (dbg && it < 32) P.dbg[74 * gridDim.x + 32 * tile + it] = clock64() - c_issue;
       }
     }
-    if (dbg && leader) dbg[2] = gtimer();
+    __syncwarp();
+    if (dbg && leader && prod == 0) dbg[2] = gtimer();
+  }
+  if (warp == 0) {
   } else if (warp == 1) {
     // ---- MMA issuer (whole warp loops; one elected lane issues tcgen05.mma)
     const uint64_t adesc = P.a_desc, bdesc = P.b_desc;
     const uint32_t idesc = P.idesc, akadv = P.a_kadv, bkadv = P.b_kadv;
-    const int ksteps = P.ksteps, nst = P.nstages;
+    const int ksteps = P.ksteps;
     const uint32_t ring0 = smem_u32(smem);
     const uint32_t a_off_b = P.a_boxes * P.a_slot;
     const bool leader = elect_one();
     int slot = 0;
     uint32_t phase = 0;
-    for (int s = 0; s < nst; ++s) {
+    for (int s = s_lo; s < s_hi; ++s) {
       mbar_wait(full0 + 8 * slot, phase);
-      if (dbg && leader && s == 0) dbg[3] = gtimer();
+      if (dbg && leader && s == s_lo) dbg[3] = gtimer();
       if (dbg && leader && s < 32) P.dbg[10 * gridDim.x + 64 * tile + 32 + s] = gtimer();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (leader) {
@@ -423,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < ksteps; ++k) {
           const uint64_t ad = adesc | (((a_addr + k * akadv) >> 4) & 0x3FFFull);
           const uint64_t bd = bdesc | (((b_addr + k * bkadv) >> 4) & 0x3FFFull);
-          umma_bf16(tmem, ad, bd, idesc, (s | k) != 0);
+          umma_bf16(tmem, ad, bd, idesc, (s != s_lo) || (k != 0));
         }
         umma_commit(empty0 + 8 * slot);
       }
@@ -446,14 +468,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(accf, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (dbg && threadIdx.x == 64) dbg[5] = gtimer();
-    for (int c0 = 0; c0 < P.BN; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
+    if (splits == 1) {
+      for (int c0 = 0; c0 < P.BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (c0 + j < P.BN) stile[row * ld + c0 + j] = __uint_as_float(v[j]);
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < P.BN) stile[row * ld + c0 + j] = __uint_as_float(v[j]);
+      }
+    } else {
+      // Split-K: publish this split's partial tile, count arrivals; the last
+      // CTA of the tile sums the partials in split order (deterministic).
+      float* wrow = P.ws + ((static_cast<int64_t>(tile) * splits + split) * 128 + row) * P.BN;
+      for (int c0 = 0; c0 < P.BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < P.BN) __stcg(wrow + c0 + j, __uint_as_float(v[j]));
+      }
+      __threadfence();
+      epi_bar();
+      if (threadIdx.x == 64) {
+        const int prev = atomicAdd(P.counters + tile, 1);
+        *s_flag = prev == splits - 1;
+        if (prev == splits - 1) P.counters[tile] = 0;  // re-armed for the next launch
+      }
+      epi_bar();
+      if (*s_flag) {
+        __threadfence();
+        const float* w0 = P.ws + (static_cast<int64_t>(tile) * splits * 128 + row) * P.BN;
+        for (int c = 0; c < P.BN; ++c) {
+          float acc = 0.f;
+          for (int q = 0; q < splits; ++q) acc += __ldcg(w0 + static_cast<int64_t>(q) * 128 * P.BN + c);
+          stile[row * ld + c] = acc;
+        }
+      }
     }
     epi_bar();
+    if (splits == 1 || *s_flag) {
     if (dbg && threadIdx.x == 64) dbg[7] = gtimer();
     // Phase 2: cooperative, coalesced stores with the fused element-wise chain
     // (bias / residual / relu, lower.cpp:566-608). Lanes run along the
@@ -501,6 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (dbg && threadIdx.x == 64) {
       dbg[6] = gtimer();
       P.dbg[8 * gridDim.x + 2 * tile + 1] = clock64();
+    }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -585,7 +639,7 @@ uint32_t idesc_of(int M, int N, bool a_mn, bool b_mn) {
 }
 
 struct Tables {
-  void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   ~Tables() {
     for (auto* q : p)
       if (q) cudaFree(q);
@@ -661,7 +715,24 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   L.cols_unit = 1;
   for (size_t c = 0; c < p.col_off.size(); ++c)
     if (p.col_off[c] != p.col_off[0] + static_cast<int64_t>(c)) L.cols_unit = 0;
-  L.grid = L.ntiles;
+  // Split-K when the tiles alone leave most of the 148 SMs idle and the
+  // K loop is long: up to 8 splits of >= 4 stages each.
+  L.splits = 1;
+  if (L.ntiles * 2 <= 148 && L.nstages >= 8) {
+    L.splits = std::min({148 / L.ntiles, L.nstages / 4, 8});
+    if (L.splits < 2) L.splits = 1;
+  }
+  if (const char* e = getenv("LFGPU_SPLITK")) L.splits = std::max(1, std::min(atoi(e), L.nstages));
+  if (L.splits > 1) {
+    const size_t ws = sizeof(float) * static_cast<size_t>(L.ntiles) * L.splits * 128 * L.BN;
+    if (cudaMalloc(&t->p[4], ws) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc split-K workspace");
+    if (cudaMalloc(&t->p[5], sizeof(int) * L.ntiles) != cudaSuccess ||
+        cudaMemset(t->p[5], 0, sizeof(int) * L.ntiles) != cudaSuccess)
+      fail(LFGPU_ECUDA, "cudaMalloc split-K counters");
+    L.ws = static_cast<float*>(t->p[4]);
+    L.counters = static_cast<int*>(t->p[5]);
+  }
+  L.grid = L.ntiles * L.splits;
   L.a_rank_ = p.A.rank;
   L.b_rank_ = p.B.rank;
   static_assert(sizeof(TileEntry) == 192, "TileEntry layout");
@@ -704,6 +775,9 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.cols_unit = L.cols_unit;
   P.rows_unit = L.rows_unit;
   P.ring_bytes = L.ring_bytes;
+  P.splits = L.splits;
+  P.ws = L.ws;
+  P.counters = L.counters;
   P.dbg = static_cast<unsigned long long*>(umma_debug_buffer());
   if (P.dbg) {
     const char* em = getenv("LFGPU_EPI_MODE");

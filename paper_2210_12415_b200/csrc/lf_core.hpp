@@ -28,6 +28,7 @@ constexpr int kMaxRank = LFGPU_MAX_RANK;
 constexpr int kMaxDig = 16;    // digits of a DigitMap
 constexpr int kMaxPred = 6;    // zero predicates of a DigitMap
 constexpr int kMaxClamp = 4;   // unfold clamps of a DigitMap
+constexpr int kMaxTab = 4;     // source offset-table terms of a DigitMap
 constexpr int kMaxOps = 40;    // steps of an IxProgram
 
 struct Error : std::runtime_error {
@@ -103,11 +104,15 @@ struct IxProgram {
 //       ? src[ src_base + sum_d src_stride[d]*x_d
 //              + sum_c cstride_c * min(ccoef[c].x + cconst_c, cmax_c) ]
 //       : 0
+// When the source sequence is not affine in the digits (a split of a
+// shifted / unfolded coordinate), each source logical coordinate l_t is kept
+// as an affine (clamped) digit form and looked up in a per-dimension offset
+// table: src offset += tab[toff_t + clamp(tcoef[t].x + tconst_t, 0, tmax_t)].
 struct DigitMap {
   int32_t ndig = 0;
   int32_t npred = 0;
   int32_t nclamp = 0;
-  int32_t reserved = 0;
+  int32_t ntab = 0;
   int64_t ext[kMaxDig] = {};
   int64_t dst_stride[kMaxDig] = {};
   int64_t src_stride[kMaxDig] = {};
@@ -120,6 +125,10 @@ struct DigitMap {
   int64_t cconst[kMaxClamp] = {};
   int64_t cmax[kMaxClamp] = {};
   int64_t cstride[kMaxClamp] = {};
+  int64_t tcoef[kMaxTab][kMaxDig] = {};
+  int64_t tconst[kMaxTab] = {};
+  int64_t tmax[kMaxTab] = {};
+  int64_t toff[kMaxTab] = {};
   int64_t dst_numel = 0;
 };
 
@@ -149,7 +158,10 @@ struct CopySpec {
 // the general program (the out-param is then unspecified). `oob` is set
 // when some destination cell would read outside the source's logical range
 // without a guard (the reference throws out-of-range there).
-bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob);
+// With `tables` non-null, a non-affine source side falls back to offset
+// tables (their int32 data is appended to *tables; the caller uploads it).
+bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob,
+                       std::vector<int32_t>* tables = nullptr);
 // Compile to the general program pair: dst physical -> dst logical (+guard,
 // +shift) -> src physical. Always succeeds for valid sequences.
 void compile_ix_programs(const CopySpec& spec, IxProgram* dst_inv, IxProgram* src_fwd);

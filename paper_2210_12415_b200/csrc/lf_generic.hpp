@@ -16,7 +16,9 @@ enum GenOp : int32_t {
   GEN_EWADD = 3,
   GEN_C2D = 4,
   GEN_DEP = 5,
-  GEN_GMM = 6
+  GEN_GMM = 6,
+  GEN_MAXPOOL = 7,         // window max (KH = KW = window, stride V); b unused
+  GEN_GLOBAL_AVGPOOL = 8   // [N,C,H,W] -> [N,C]: sum over (h, w) / (H*W); b unused
 };
 
 // Element-wise node: out physical element f -> logical l (out_prog), then
@@ -39,6 +41,7 @@ struct GenContract {
   int32_t reserved = 0;
   int64_t n = 0;  // output physical elements
   int64_t I = 0, KH = 0, KW = 0, V = 1, K = 0;
+  int64_t H = 0, W = 0;  // GEN_GLOBAL_AVGPOOL input extents
   const void* a = nullptr;
   const void* b = nullptr;
   const int64_t* ta = nullptr;

@@ -17,8 +17,10 @@ struct KernelInfo {
 int elem_size(int elem);
 
 // K1/K2 (k_copy.cu)
+// d_tab: the DigitMap's source offset tables in device memory (ntab > 0).
 cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, const void* src,
-                              void* dst, cudaStream_t stream, KernelInfo* info);
+                              void* dst, cudaStream_t stream, KernelInfo* info,
+                              const int32_t* d_tab = nullptr);
 // Stream-read a > L2 buffer (measurement hygiene after the flush write).
 cudaError_t launch_l2_touch(const void* buf, size_t bytes, int* sink, cudaStream_t stream);
 // d_progs: two IxPrograms (dst inverse, src forward) in device memory.

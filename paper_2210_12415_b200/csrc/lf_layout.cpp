@@ -470,7 +470,8 @@ class DigitEngine {
 
 }  // namespace
 
-bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob) {
+bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob,
+                       std::vector<int32_t>* tables) {
   *oob = false;
   std::vector<Dim> dst_phys = derive(spec.lmap.dst_logical, spec.dst_seq);
   std::vector<Dim> src_phys = derive(spec.lmap.src_logical, spec.src_seq);
@@ -560,39 +561,52 @@ bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob) {
     }
   for (size_t j = 0; j < en.V.size(); ++j) en.E[j] = L.src_logical[j].extent;
 
-  // 3. source logical -> source physical (forward sequence).
-  std::vector<Dim> cur = L.src_logical;
-  for (const auto& p : spec.src_seq) {
-    std::vector<Dim> nxt = apply_shape(cur, p);
-    switch (p.kind) {
-      case LFGPU_PRIM_SPLIT: {
-        std::vector<int64_t> f(p.factors, p.factors + p.nfactors);
-        if (!en.split_entry(p.dim, f)) return false;
-        break;
+  // 3. source logical -> source physical (forward sequence); on failure
+  // (and when allowed) keep the logical forms and use offset tables.
+  const DigitEngine logical_state = en;
+  auto forward_src = [&]() -> bool {
+    std::vector<Dim> cur = L.src_logical;
+    for (const auto& p : spec.src_seq) {
+      std::vector<Dim> nxt = apply_shape(cur, p);
+      switch (p.kind) {
+        case LFGPU_PRIM_SPLIT: {
+          std::vector<int64_t> f(p.factors, p.factors + p.nfactors);
+          if (!en.split_entry(p.dim, f)) return false;
+          break;
+        }
+        case LFGPU_PRIM_REORDER:
+          en.permute(p.perm, p.nperm, /*inverse=*/false);
+          break;
+        case LFGPU_PRIM_FUSE:
+          en.fuse_entries(p.dim, p.span);
+          if (!en.ok) return false;
+          break;
+        case LFGPU_PRIM_UNFOLD: {
+          int64_t D = cur[p.dim].extent;
+          int64_t T = unfold_tiles(D, p.tile, p.stride);
+          if (D % p.stride != 0 || D / p.stride > T) return false;
+          if (!en.split_entry(p.dim, {D / p.stride, p.stride})) return false;
+          en.E[p.dim] = T;
+          en.E[p.dim + 1] = p.tile;
+          break;
+        }
+        case LFGPU_PRIM_PAD:
+          en.E[p.dim] += p.pad;
+          break;
+        default:
+          return false;
       }
-      case LFGPU_PRIM_REORDER:
-        en.permute(p.perm, p.nperm, /*inverse=*/false);
-        break;
-      case LFGPU_PRIM_FUSE:
-        en.fuse_entries(p.dim, p.span);
-        if (!en.ok) return false;
-        break;
-      case LFGPU_PRIM_UNFOLD: {
-        int64_t D = cur[p.dim].extent;
-        int64_t T = unfold_tiles(D, p.tile, p.stride);
-        if (D % p.stride != 0 || D / p.stride > T) return false;
-        if (!en.split_entry(p.dim, {D / p.stride, p.stride})) return false;
-        en.E[p.dim] = T;
-        en.E[p.dim + 1] = p.tile;
-        break;
-      }
-      case LFGPU_PRIM_PAD:
-        en.E[p.dim] += p.pad;
-        break;
-      default:
-        return false;
+      cur = nxt;
     }
-    cur = nxt;
+    return true;
+  };
+  bool use_tables = false;
+  std::vector<int64_t> ltab, ltab_off;
+  if (!forward_src()) {
+    if (!tables || spec.src_seq.empty()) return false;
+    en = logical_state;
+    if (!separable_tables(L.src_logical, spec.src_seq, &ltab, &ltab_off)) return false;
+    use_tables = true;
   }
 
   // 4. emit.
@@ -601,16 +615,40 @@ bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob) {
   std::vector<int64_t> src_coef(en.ext.size(), 0);
   std::vector<Combo> clamps;
   std::vector<int64_t> clamp_stride;
+  std::vector<Combo> tabs;
+  std::vector<int64_t> tab_max, tab_off;
   int64_t base = 0;
   for (size_t k = 0; k < en.V.size(); ++k) {
     const Combo& c = en.V[k];
+    int64_t stride = use_tables ? 0 : sstr[k];
+    if (use_tables) {
+      // Logical coordinate k: affine table -> a stride, else a table term.
+      const int64_t D = L.src_logical[k].extent;
+      const int64_t* T = ltab.data() + ltab_off[k];
+      stride = D > 1 ? T[1] - T[0] : 0;
+      bool affine = true;
+      for (int64_t l = 0; l < D && affine; ++l) affine = T[l] == T[0] + l * stride;
+      base += T[0];
+      if (!affine) {
+        if (static_cast<int>(tabs.size()) >= kMaxTab) return false;
+        tabs.push_back(c);
+        tab_max.push_back(c.clamped ? std::min(c.cmax, D - 1) : D - 1);
+        tab_off.push_back(static_cast<int64_t>(tables->size()));
+        for (int64_t l = 0; l < D; ++l) {
+          const int64_t v = T[l] - T[0];
+          if (v > INT32_MAX || v < INT32_MIN) return false;
+          tables->push_back(static_cast<int32_t>(v));
+        }
+        continue;
+      }
+    }
     if (c.clamped) {
       clamps.push_back(c);
-      clamp_stride.push_back(sstr[k]);
+      clamp_stride.push_back(stride);
       continue;
     }
-    base += c.c0 * sstr[k];
-    for (const auto& [d, v] : c.t) src_coef[d] += v * sstr[k];
+    base += c.c0 * stride;
+    for (const auto& [d, v] : c.t) src_coef[d] += v * stride;
   }
   // Digits in destination order (descending dst stride); drop extent-1 digits.
   std::vector<int> order;
@@ -628,10 +666,15 @@ bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob) {
       return it == en.preds[pi].first.t.end() ? 0 : it->second;
     }
     int ci = pi - static_cast<int>(en.preds.size());
-    auto it = clamps[ci].t.find(d);
-    return it == clamps[ci].t.end() ? 0 : it->second;
+    if (ci < static_cast<int>(clamps.size())) {
+      auto it = clamps[ci].t.find(d);
+      return it == clamps[ci].t.end() ? 0 : it->second;
+    }
+    int ti = ci - static_cast<int>(clamps.size());
+    auto it = tabs[ti].t.find(d);
+    return it == tabs[ti].t.end() ? 0 : it->second;
   };
-  int nforms = 2 + static_cast<int>(en.preds.size() + clamps.size());
+  int nforms = 2 + static_cast<int>(en.preds.size() + clamps.size() + tabs.size());
   // Groups of consecutive digits merged when every form is contiguous.
   struct G {
     int64_t ext;
@@ -660,6 +703,7 @@ bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob) {
   m.ndig = static_cast<int32_t>(groups.size());
   m.npred = static_cast<int32_t>(en.preds.size());
   m.nclamp = static_cast<int32_t>(clamps.size());
+  m.ntab = static_cast<int32_t>(tabs.size());
   m.src_base = base;
   for (size_t g = 0; g < groups.size(); ++g) {
     m.ext[g] = groups[g].ext;
@@ -667,6 +711,12 @@ bool compile_digit_map(const CopySpec& spec, DigitMap* out, bool* oob) {
     m.src_stride[g] = groups[g].coef[1];
     for (int p = 0; p < m.npred; ++p) m.pcoef[p][g] = groups[g].coef[2 + p];
     for (int c = 0; c < m.nclamp; ++c) m.ccoef[c][g] = groups[g].coef[2 + m.npred + c];
+    for (int t = 0; t < m.ntab; ++t) m.tcoef[t][g] = groups[g].coef[2 + m.npred + m.nclamp + t];
+  }
+  for (int t = 0; t < m.ntab; ++t) {
+    m.tconst[t] = tabs[t].c0;
+    m.tmax[t] = tab_max[t];
+    m.toff[t] = tab_off[t];
   }
   for (int p = 0; p < m.npred; ++p) {
     m.pconst[p] = en.preds[p].first.c0;

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "lf_core.hpp"
+#include "lf_direct.hpp"
 #include "lf_generic.hpp"
 #include "lf_kernels.hpp"
 #include "lf_umma.hpp"
@@ -111,6 +112,7 @@ T* upload(std::vector<std::unique_ptr<DevBuf>>& keep, const T* host, size_t coun
 struct CopyKernel {
   bool digit = false;
   DigitMap map;
+  const int32_t* d_tab = nullptr;  // DigitMap source offset tables (ntab > 0)
   IxProgram* d_progs = nullptr;
   int64_t n = 0;
   int src_elem = 0, dst_elem = 0;
@@ -124,8 +126,11 @@ CopyKernel compile_copy(const CopySpec& spec, int se, int de,
   k.dst_elem = de;
   k.n = numel(derive(spec.lmap.dst_logical, spec.dst_seq));
   *oob = false;
-  if (compile_digit_map(spec, &k.map, oob)) {
+  // fp32 sources may use offset tables for a non-affine source side.
+  std::vector<int32_t> tabs;
+  if (compile_digit_map(spec, &k.map, oob, se == LFGPU_ELEM_F32 ? &tabs : nullptr)) {
     k.digit = true;
+    if (k.map.ntab > 0) k.d_tab = upload(keep, tabs.data(), tabs.size());
     return k;
   }
   IxProgram progs[2];
@@ -138,7 +143,7 @@ CopyKernel compile_copy(const CopySpec& spec, int se, int de,
 cudaError_t run_copy(const CopyKernel& k, const void* src, void* dst, int* d_err,
                      cudaStream_t s) {
   KernelInfo info;
-  if (k.digit) return launch_digit_copy(k.map, k.src_elem, k.dst_elem, src, dst, s, &info);
+  if (k.digit) return launch_digit_copy(k.map, k.src_elem, k.dst_elem, src, dst, s, &info, k.d_tab);
   return launch_ix_copy(k.d_progs, k.n, k.src_elem, k.dst_elem, src, dst, d_err, s, &info);
 }
 
@@ -150,6 +155,7 @@ const char* copy_name(const CopyKernel& k) {
   if (k.map.ndig >= 2 && k.map.src_stride[a] != 1)
     for (int d = 0; d < k.map.ndig - 1; ++d)
       if (k.map.src_stride[d] == 1) transpose = true;
+  if (k.map.ntab > 0) return transpose ? "digit_copy_transpose_tab" : "digit_copy_direct_tab";
   return transpose ? "digit_copy_transpose" : "digit_copy_direct";
 }
 
@@ -325,7 +331,42 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
 
   // 1. Tensor-core eligibility per contraction and fusion chains.
   std::map<int, UmmaPlan> umma;
+  std::map<int, std::vector<EpiOp>> direct;  // CUDA-core direct convs (k_direct.cu)
   std::set<int> fused_away;  // element-wise nodes absorbed into an epilogue
+  std::vector<int> pos(P->nodes.size(), 0);
+  for (size_t k = 0; k < P->order.size(); ++k) pos[P->order[k]] = static_cast<int>(k);
+  // Epilogue fusion of the single-consumer element-wise chain after node ni
+  // (lower.cpp:566-608) while every member keeps the output's physical layout.
+  auto fuse_chain = [&](int ni, const PTensor& Cc) {
+    std::vector<EpiOp> epi;
+    int cur = P->nodes[ni].output;
+    while (true) {
+      const auto& cons = P->t[cur].consumers;
+      if (cons.size() != 1) break;
+      const auto& c = P->nodes[cons[0]];
+      if (c.kind != LFGPU_OP_RELU && c.kind != LFGPU_OP_BIASADD && c.kind != LFGPU_OP_EWADD) break;
+      if (c.inputs[0] != cur) break;
+      if (!seq_equal(P->t[c.output].seq, Cc.seq)) break;
+      if (c.kind == LFGPU_OP_EWADD && !seq_equal(P->t[c.inputs[1]].seq, Cc.seq)) break;
+      if (c.kind == LFGPU_OP_BIASADD && !P->t[c.inputs[1]].seq.empty()) break;
+      if (static_cast<int>(epi.size()) >= kMaxEpi) break;
+      if (c.kind == LFGPU_OP_RELU && !epi.empty() && epi.back().kind == EPI_RELU) break;
+      // The epilogue reads a residual / bias when the contraction runs: its
+      // producer must already have run (e.g. a ResNet downsample branch).
+      if (c.kind != LFGPU_OP_RELU) {
+        const int pr = P->t[c.inputs[1]].producer;
+        if (pr >= 0 && pos[pr] > pos[ni]) break;
+      }
+      EpiOp e;
+      e.kind = c.kind == LFGPU_OP_RELU ? EPI_RELU : c.kind == LFGPU_OP_BIASADD ? EPI_BIAS : EPI_RESIDUAL;
+      e.tensor = c.kind == LFGPU_OP_RELU ? -1 : c.inputs[1];
+      e.out_tensor = c.output;
+      epi.push_back(e);
+      fused_away.insert(cons[0]);
+      cur = c.output;
+    }
+    return epi;
+  };
   for (int ni : P->order) {
     const auto& n = P->nodes[ni];
     if (n.kind != LFGPU_OP_C2D && n.kind != LFGPU_OP_GMM) continue;
@@ -344,37 +385,22 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
                   : umma_plan_conv(A.logical, A.seq, B.logical, B.seq, Cc.logical, Cc.seq,
                                    n.stride, s, &up, &why);
     if (!ok) {
+      // Small-I convolutions on logical operands: the CUDA-core direct kernel.
+      const bool dc = n.kind == LFGPU_OP_C2D && A.seq.empty() && B.seq.empty() &&
+                      direct_conv_applies(B.logical[1].extent, B.logical[2].extent,
+                                          B.logical[3].extent, B.logical[0].extent);
+      if (dc) {
+        direct[ni] = s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL) ? fuse_chain(ni, Cc)
+                                                                 : std::vector<EpiOp>{};
+        continue;
+      }
       if (P->flags & LFGPU_PLAN_REQUIRE_TC)
         fail(LFGPU_EUNSUPPORTED, "node " + std::to_string(ni) + " not tensor-core legal: " + why);
       continue;
     }
-    // Epilogue fusion of the single-consumer element-wise chain (lower.cpp:566-608)
-    // when every member keeps the output's physical layout.
     if (s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL)) {
-      int cur = n.output;
-      while (true) {
-        const auto& cons = P->t[cur].consumers;
-        if (cons.size() != 1) break;
-        const auto& c = P->nodes[cons[0]];
-        if (c.kind != LFGPU_OP_RELU && c.kind != LFGPU_OP_BIASADD && c.kind != LFGPU_OP_EWADD)
-          break;
-        if (c.inputs[0] != cur) break;
-        if (!seq_equal(P->t[c.output].seq, Cc.seq)) break;
-        if (c.kind == LFGPU_OP_EWADD && !seq_equal(P->t[c.inputs[1]].seq, Cc.seq)) break;
-        if (c.kind == LFGPU_OP_BIASADD && !P->t[c.inputs[1]].seq.empty()) break;
-        if (up.epi_count >= kMaxEpi) break;
-        if (c.kind == LFGPU_OP_RELU && up.epi_count > 0 &&
-            up.epi[up.epi_count - 1].kind == EPI_RELU)
-          break;
-        up.epi[up.epi_count].kind = c.kind == LFGPU_OP_RELU    ? EPI_RELU
-                                    : c.kind == LFGPU_OP_BIASADD ? EPI_BIAS
-                                                                 : EPI_RESIDUAL;
-        up.epi[up.epi_count].tensor = c.kind == LFGPU_OP_RELU ? -1 : c.inputs[1];
-        up.epi[up.epi_count].out_tensor = c.output;
-        ++up.epi_count;
-        fused_away.insert(cons[0]);
-        cur = c.output;
-      }
+      std::vector<EpiOp> epi = fuse_chain(ni, Cc);
+      for (const auto& e : epi) up.epi[up.epi_count++] = e;
     }
     umma[ni] = up;
   }
@@ -503,7 +529,46 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           macs = numel(out.logical) * B.logical[1].extent * B.logical[2].extent;
         P->flops += 2 * macs;
         auto it = umma.find(ni);
-        if (it != umma.end()) {
+        auto dt = direct.find(ni);
+        if (dt != direct.end()) {
+          DirectConv D;
+          D.N = static_cast<int32_t>(A.logical[0].extent);
+          D.I = static_cast<int32_t>(A.logical[1].extent);
+          D.H = static_cast<int32_t>(A.logical[2].extent);
+          D.W = static_cast<int32_t>(A.logical[3].extent);
+          D.O = static_cast<int32_t>(B.logical[0].extent);
+          D.KH = static_cast<int32_t>(B.logical[2].extent);
+          D.KW = static_cast<int32_t>(B.logical[3].extent);
+          D.V = static_cast<int32_t>(n.stride);
+          D.Ho = static_cast<int32_t>(out.logical[2].extent);
+          D.Wo = static_cast<int32_t>(out.logical[3].extent);
+          if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "direct conv on a bf16-only operand");
+          D.x = static_cast<const float*>(A.d);
+          D.w = static_cast<const float*>(B.d);
+          const auto& epi = dt->second;
+          int final_t = epi.empty() ? n.output : epi.back().out_tensor;
+          PTensor& fo = P->t[final_t];
+          std::vector<int64_t> oo;
+          D.tab = tables_for(P, fo, &oo);
+          for (size_t j = 0; j < oo.size(); ++j) D.tab_off[j] = oo[j];
+          D.out = static_cast<float*>(fo.d);
+          D.nepi = static_cast<int32_t>(epi.size());
+          for (size_t e = 0; e < epi.size(); ++e) {
+            D.epi_kind[e] = epi[e].kind == EPI_BIAS ? DIRECT_EPI_BIAS
+                            : epi[e].kind == EPI_RELU ? DIRECT_EPI_RELU
+                                                      : DIRECT_EPI_RESIDUAL;
+            if (epi[e].tensor >= 0) {
+              const PTensor& et = P->t[epi[e].tensor];
+              if (!et.d) fail(LFGPU_EUNSUPPORTED, "epilogue operand has no fp32 buffer");
+              D.epi_ptr[e] = static_cast<const float*>(et.d);
+            }
+          }
+          for (size_t e = 0; e + 1 < epi.size(); ++e) P->t[epi[e].out_tensor].valid = false;
+          if (!epi.empty()) out.valid = false;
+          step.kernel = "c2d_direct";
+          step.run = [D](cudaStream_t st) { return launch_c2d_direct(D, st); };
+          P->bytes += A.numel * 4 + B.numel * 4 + fo.numel * 4;
+        } else if (it != umma.end()) {
           UmmaPlan up = it->second;
           up.a = A.d_bf16;
           up.b = B.d_bf16;
@@ -560,6 +625,51 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           P->bytes += A.numel * elem_size(A.elem) + B.numel * elem_size(B.elem) +
                       out.numel * elem_size(out.elem);
         }
+        break;
+      }
+      case LFGPU_OP_MAXPOOL:
+      case LFGPU_OP_GLOBAL_AVGPOOL: {
+        // Op-set extension (lfgpu.h): CUDA-core window reductions through the
+        // operand's separable offset tables, output walked in physical order.
+        const PTensor& A = P->t[n.inputs[0]];
+        if (A.logical.size() != 4) fail(LFGPU_EINVAL, "pool input must be rank 4");
+        GenContract G;
+        G.n = out.numel;
+        if (n.kind == LFGPU_OP_MAXPOOL) {
+          const int64_t k = n.window, v = n.stride;
+          if (k < 1 || v < 1) fail(LFGPU_EINVAL, "MaxPool needs window >= 1 and stride >= 1");
+          if (out.logical.size() != 4 || out.logical[0].extent != A.logical[0].extent ||
+              out.logical[1].extent != A.logical[1].extent ||
+              out.logical[2].extent != (A.logical[2].extent - k) / v + 1 ||
+              out.logical[3].extent != (A.logical[3].extent - k) / v + 1 ||
+              A.logical[2].extent < k || A.logical[3].extent < k)
+            fail(LFGPU_EINVAL, "MaxPool output shape mismatch for '" + out.id + "'");
+          G.op = GEN_MAXPOOL;
+          G.KH = G.KW = k;
+          G.V = v;
+        } else {
+          if (out.logical.size() != 2 || out.logical[0].extent != A.logical[0].extent ||
+              out.logical[1].extent != A.logical[1].extent)
+            fail(LFGPU_EINVAL, "GlobalAvgPool output must be [N, C] for '" + out.id + "'");
+          if (out.dtype != LFGPU_DTYPE_F32)
+            fail(LFGPU_EUNSUPPORTED, "GlobalAvgPool is defined for f32 tensors only");
+          G.op = GEN_GLOBAL_AVGPOOL;
+          G.H = A.logical[2].extent;
+          G.W = A.logical[3].extent;
+        }
+        if (!A.d) fail(LFGPU_EUNSUPPORTED, "pool read of a bf16-only tensor");
+        std::vector<int64_t> oa;
+        G.ta = tables_for(P, A, &oa);
+        for (size_t j = 0; j < oa.size(); ++j) G.a_off[j] = oa[j];
+        G.a = A.d;
+        IxProgram* prog = out_program(P, out);
+        int elem = out.elem;
+        void* dst = out.d;
+        step.kernel = n.kind == LFGPU_OP_MAXPOOL ? "gen_maxpool" : "gen_global_avgpool";
+        step.run = [prog, G, elem, exact, dst](cudaStream_t s) {
+          return launch_gen_contract(prog, G, elem, exact, dst, s);
+        };
+        P->bytes += A.numel * elem_size(A.elem) + out.numel * elem_size(out.elem);
         break;
       }
       default:

@@ -104,6 +104,9 @@ struct UmmaLaunch {
   int grid = 0;
   int a_rank_ = 0, b_rank_ = 0;
   int cols_unit = 0, rows_unit = 0, ring_bytes = 0;
+  int splits = 1;               // split-K factor (k_umma.cu)
+  float* ws = nullptr;          // split-K partial tiles
+  int* counters = nullptr;      // split-K per-tile arrival counters
   std::shared_ptr<void> owner;  // keeps the device tables alive
 };
 

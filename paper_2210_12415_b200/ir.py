@@ -17,9 +17,12 @@ INPUT, CONSTANT, INTERMEDIATE, OUTPUT = _abi.INPUT, _abi.CONSTANT, _abi.INTERMED
 C2D, DEP, GMM, PADDING, RELU, BIASADD, EWADD, LAYOUT_CONVERT = (
     _abi.C2D, _abi.DEP, _abi.GMM, _abi.PADDING, _abi.RELU, _abi.BIASADD, _abi.EWADD,
     _abi.LAYOUT_CONVERT)
+# Op-set extension: the pools ResNet-18 needs.
+MAXPOOL, GLOBAL_AVGPOOL = _abi.MAXPOOL, _abi.GLOBAL_AVGPOOL
 
 OP_NAMES = {C2D: "C2D", DEP: "DEP", GMM: "GMM", PADDING: "Padding", RELU: "ReLU",
-            BIASADD: "BiasAdd", EWADD: "EwAdd", LAYOUT_CONVERT: "LayoutConvert"}
+            BIASADD: "BiasAdd", EWADD: "EwAdd", LAYOUT_CONVERT: "LayoutConvert",
+            MAXPOOL: "MaxPool", GLOBAL_AVGPOOL: "GlobalAvgPool"}
 
 
 def is_complex_op(k):  # ir.cpp:26-28
@@ -96,8 +99,10 @@ class Graph:
         for i in range(desc.nnodes):
             nd = desc.nodes[i]
             attrs = {}
-            if nd.kind in (C2D, DEP):
+            if nd.kind in (C2D, DEP, MAXPOOL):
                 attrs["stride"] = nd.stride
+            if nd.kind == MAXPOOL:
+                attrs["window"] = nd.window
             if nd.kind == PADDING:
                 attrs["pad"] = nd.pad
             g.nodes.append(OperatorNode(nd.kind,
@@ -138,6 +143,7 @@ class CGraph:
             d.output = g.tensor_index(n.output)
             d.stride = int(n.attr("stride", 1))
             d.pad = int(n.attr("pad", 0))
+            d.window = int(n.attr("window", 0))
         items = [(k, v) for k, v in seqs.items() if v]
         self.prim_arrays = []
         self.seqs = (_abi.Seq * max(1, len(items)))()

@@ -56,3 +56,193 @@ BERT_GEMMS = [
     ("ffn1", 768, 3072, "bias+relu"),
     ("ffn2", 3072, 768, "bias+residual"),
 ]
+
+
+# ---------------------------------------------------------------------------
+# cfg4: ResNet-18 inference graph (BatchNorm folded into the conv bias).
+
+class Builder:
+    """Small helper to declare tensors and nodes in order."""
+
+    def __init__(self):
+        self.g = ir.Graph()
+
+    def t(self, tid, dims, role=ir.INTERMEDIATE):
+        self.g.tensors.append(ir.TensorDecl(tid, list(dims), role))
+        return tid
+
+    def op(self, kind, inputs, out, **attrs):
+        self.g.nodes.append(ir.OperatorNode(kind, list(inputs), out, dict(attrs)))
+        return out
+
+
+RESNET18_STAGES = [(64, 1), (128, 2), (256, 2), (512, 2)]
+
+
+def resnet18(n, classes=1000, h=224):
+    """ResNet-18 v1 inference as one graph. Returns (graph, info) where info
+    lists the C2D nodes with their role:
+      stem   7x7 s2 3->64 (+ bias + ReLU), then Padding(1) + MaxPool 3 s2
+      per basic block: Padding -> C2D 3x3 (stride s) -> BiasAdd -> ReLU ->
+        Padding -> C2D 3x3 -> BiasAdd -> EwAdd(residual) -> ReLU; the first
+        block of stages 2-4 has a LayoutConvert -> C2D 1x1 s2 -> BiasAdd
+        downsample branch as the residual
+      GlobalAvgPool -> GMM 512x1000 -> BiasAdd -> logits
+    The downsample nodes are declared before the block's main path so the
+    residual exists when the fused epilogue of the second conv reads it."""
+    b = Builder()
+    I, C, O = ir.INPUT, ir.CONSTANT, ir.OUTPUT
+
+    def nchw(tid, c, hh, role=ir.INTERMEDIATE):
+        return b.t(tid, [("N", n), ("C", c), ("H", hh), ("W", hh)], role)
+
+    convs = []
+
+    def conv(name, x, cin, cout, hin, k, stride, pad, role):
+        """Padding (if pad) -> C2D -> BiasAdd; returns (biased tensor, hout)."""
+        xin = x
+        hp = hin + 2 * pad
+        if pad:
+            xin = nchw(f"{name}_xp", cin, hp)
+            b.op(ir.PADDING, [x], xin, pad=pad)
+        else:
+            xin = nchw(f"{name}_xcv", cin, hin)
+            b.op(ir.LAYOUT_CONVERT, [x], xin)
+        ho = (hp - k) // stride + 1
+        w = b.t(f"{name}_w", [("O", cout), ("I", cin), ("KH", k), ("KW", k)], C)
+        bias = b.t(f"{name}_b", [("O", cout)], C)
+        y = nchw(f"{name}_y", cout, ho)
+        b.op(ir.C2D, [xin, w], y, stride=stride)
+        convs.append({"name": name, "node": len(b.g.nodes) - 1, "cin": cin, "cout": cout,
+                      "h": hin, "k": k, "stride": stride, "pad": pad, "role": role})
+        yb = nchw(f"{name}_yb", cout, ho)
+        b.op(ir.BIASADD, [y, bias], yb)
+        return yb, ho
+
+    x = nchw("x", 3, h, I)
+    s, hh = conv("stem", x, 3, 64, h, 7, 2, 3, "stem")
+    r = nchw("stem_r", 64, hh)
+    b.op(ir.RELU, [s], r)
+    mp_in = nchw("pool_xp", 64, hh + 2)
+    b.op(ir.PADDING, [r], mp_in, pad=1)
+    hh = (hh + 2 - 3) // 2 + 1
+    cur = nchw("pool_y", 64, hh)
+    b.op(ir.MAXPOOL, [mp_in], cur, window=3, stride=2)
+    cin = 64
+    for si, (cout, stride) in enumerate(RESNET18_STAGES):
+        for bi in range(2):
+            st = stride if bi == 0 else 1
+            name = f"s{si + 1}b{bi + 1}"
+            res = cur
+            if st != 1 or cin != cout:
+                res, _ = conv(f"{name}_ds", cur, cin, cout, hh, 1, st, 0, f"s{si + 1}_ds")
+            a, ho = conv(f"{name}_a", cur, cin, cout, hh, 3, st, 1, f"s{si + 1}_a")
+            ar = nchw(f"{name}_ar", cout, ho)
+            b.op(ir.RELU, [a], ar)
+            bb, _ = conv(f"{name}_b", ar, cout, cout, ho, 3, 1, 1, f"s{si + 1}_b")
+            sm = nchw(f"{name}_sum", cout, ho)
+            b.op(ir.EWADD, [bb, res], sm)
+            cur = nchw(f"{name}_out", cout, ho)
+            b.op(ir.RELU, [sm], cur)
+            cin, hh = cout, ho
+    gp = b.t("gap", [("N", n), ("C", cin)])
+    b.op(ir.GLOBAL_AVGPOOL, [cur], gp)
+    fw = b.t("fc_w", [("K", cin), ("M", classes)], C)
+    fb = b.t("fc_b", [("M", classes)], C)
+    lg = b.t("fc_y", [("N", n), ("M", classes)])
+    b.op(ir.GMM, [gp, fw], lg)
+    b.op(ir.BIASADD, [lg, fb], b.t("logits", [("N", n), ("M", classes)], O))
+    return b.g, convs
+
+
+def propagate_elementwise(g, seqs):
+    """Element-wise outputs inherit their first input's layout (the
+    reference's forward propagation through element-wise chains,
+    propagation.cpp); returns a new SeqMap."""
+    out = dict(seqs)
+    for nd in g.nodes:
+        if ir.is_elementwise_op(nd.kind) and nd.output not in out and nd.inputs[0] in out:
+            out[nd.output] = out[nd.inputs[0]]
+    return out
+
+
+def resnet18_seqs(g, convs, factors_of):
+    """SeqMap for the ResNet-18 graph from per-conv C2D template factors
+    (name -> (h_t, w_t, o_t, i_t, i'_t, o'_t); missing -> logical layouts).
+    The MaxPool writes stage 1's residual layout; element-wise outputs
+    inherit their producer's layout."""
+    from . import runtime
+    seqs = {}
+    for c in convs:
+        f = factors_of.get(c["name"])
+        if f:
+            seqs.update(runtime.decode_layout(g, c["node"], list(f)))
+    if "s1b1_b_y" in seqs:
+        seqs["pool_y"] = seqs["s1b1_b_y"]
+    return propagate_elementwise(g, seqs)
+
+
+def tune_resnet18(n, inputs_for, ctx=None, log=None):
+    """Per-conv GPU-measured layout choice under the residual constraint:
+    within a stage, the two second convs of the blocks (3x3, stride 1) and
+    the downsample conv must share one output brick (h_t, w_t, o_t) so the
+    residual EwAdd fuses into the tcgen05 epilogue. The brick minimises
+    2*t(second conv) + t(downsample) over bricks legal for both; the other
+    convs are tuned freely. `inputs_for(graph)` returns device inputs for a
+    sub-graph. Returns name -> factors (absent: logical layouts)."""
+    from . import tuner
+    g, convs = resnet18(n)
+    chosen, memo = {}, {}
+
+    def shape_key(c):
+        return (c["cin"], c["cout"], c["h"], c["k"], c["stride"], c["pad"])
+
+    def sweep(c):
+        """{factors: cost_us} over the template candidates of conv c's shape."""
+        key = shape_key(c)
+        if key not in memo:
+            sub, node = conv_graph(n, *key)
+            res, _ = tuner.sweep(sub, tuner.conv_candidates(sub, node), inputs_for(sub),
+                                 warmup=1, reps=3, ctx=ctx)
+            memo[key] = {tuple(r.candidate.factors[node]): r.cost_us
+                         for r in res if r.cost_us is not None}
+        return memo[key]
+
+    def best_of(costs, brick=None):
+        ok = {f: t for f, t in costs.items() if brick is None or f[:3] == brick}
+        return min(ok, key=ok.get) if ok else None
+
+    for si in range(len(RESNET18_STAGES)):
+        tag = f"s{si + 1}"
+        seconds = [c for c in convs if c["role"] == tag + "_b"]
+        ds = [c for c in convs if c["role"] == tag + "_ds"]
+        cb = sweep(seconds[0])
+        brick = None
+        if ds:
+            cd = sweep(ds[0])
+            tb = {}
+            for f, t in cb.items():
+                tb[f[:3]] = min(t, tb.get(f[:3], float("inf")))
+            td = {}
+            for f, t in cd.items():
+                td[f[:3]] = min(t, td.get(f[:3], float("inf")))
+            both = [k for k in tb if k in td]
+            if both:
+                brick = min(both, key=lambda k: 2 * tb[k] + td[k])
+            fd = best_of(cd, brick)
+            if fd:
+                chosen[ds[0]["name"]] = fd
+        fb = best_of(cb, brick)
+        for c in seconds:
+            if fb:
+                chosen[c["name"]] = fb
+    for c in convs:
+        if c["name"] in chosen or c["role"] == "stem" or c["role"].endswith(("_b", "_ds")):
+            continue
+        f = best_of(sweep(c))
+        if f:
+            chosen[c["name"]] = f
+    if log:
+        for c in convs:
+            log(f"{c['name']}: {chosen.get(c['name'])}")
+    return chosen

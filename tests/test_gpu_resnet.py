@@ -1,0 +1,181 @@
+"""cfg4 pieces on the GPU: conversions between two different C2D templates
+(source-table digit maps), the pool ops, the direct small-I conv, and
+ResNet-18 end to end.
+
+Tolerances: conversions, pools and single k/64 contractions are bit-exact
+against the oracle. The ResNet-18 logits go through 20 chained convs whose
+activations are stored / fed to tcgen05 in bf16 (SURVEY.md §8c "chained
+fp32 graphs"): they are checked (a) against a float64 reference that applies
+the same bf16 rounding to tensor-core operands, max_rel_diff <= 1e-4, and
+(b) against the exact float64 forward, max_rel_diff <= 2e-3 (the stated
+bf16-activation tolerance of this path).
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import oracle_lib as O
+from paper_2210_12415_b200 import _abi, ir, runtime, workloads
+from paper_2210_12415_b200.layout import reorder, split
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                "tools"))
+import resnet18_run as R  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+# (in extents, y template factors of the producer, xp template factors of the consumer)
+TEMPLATE_PAIRS = [
+    ((1, 64, 56, 56), (8, 7, 32, 32, 32, 32), (7, 7, 32, 32, 32, 32)),
+    ((2, 64, 28, 28), (2, 28, 32, 64, 64, 16), (14, 4, 64, 16, 16, 64)),
+    ((1, 128, 14, 14), (7, 7, 16, 64, 64, 16), (7, 14, 32, 32, 32, 32)),
+]
+
+
+def test_padding_between_templates_is_exact():
+    rng = np.random.default_rng(3)
+    for ext, fy, fx in TEMPLATE_PAIRS:
+        n, c, h, _ = ext
+        g = ir.pad_conv(n, c, c, h, 3, 1, 1)
+        y_seq = runtime.decode_layout(g, 1, list(fy))["y"]
+        xp_seq = runtime.decode_layout(g, 1, list(fx))["xp"]
+        x = rng.integers(-64, 65, int(np.prod(ext))) / 64.0
+        xs = O.materialize(list(ext), y_seq, x)   # source in the producer's output layout
+        rc, want = O.padding_nest(list(ext), 1, y_seq, xp_seq, xs)
+        assert rc == 0
+        for dt in (torch.float32, torch.bfloat16):
+            src = torch.tensor(xs, dtype=torch.float32, device="cuda")
+            dst = torch.full((want.size,), float("nan"), dtype=dt, device="cuda")
+            runtime.pad_convert(src, [("N", n), ("C", c), ("H", h), ("W", h)], 1, y_seq, xp_seq,
+                                dst)
+            torch.cuda.synchronize()
+            assert np.array_equal(dst.double().cpu().numpy(), want), (ext, fy, fx, dt)
+
+
+def pool_graph(n, c, h):
+    g = ir.Graph()
+    g.tensors = [
+        ir.TensorDecl("x", [("N", n), ("C", c), ("H", h), ("W", h)], ir.INPUT),
+        ir.TensorDecl("xp", [("N", n), ("C", c), ("H", h + 2), ("W", h + 2)]),
+        ir.TensorDecl("mp", [("N", n), ("C", c), ("H", h // 2), ("W", h // 2)]),
+        ir.TensorDecl("y", [("N", n), ("C", c)], ir.OUTPUT),
+    ]
+    g.nodes = [
+        ir.OperatorNode(ir.PADDING, ["x"], "xp", {"pad": 1}),
+        ir.OperatorNode(ir.MAXPOOL, ["xp"], "mp", {"window": 3, "stride": 2}),
+        ir.OperatorNode(ir.GLOBAL_AVGPOOL, ["mp"], "y"),
+    ]
+    return g
+
+
+@pytest.mark.parametrize("layouts", [
+    {},
+    {"x": [split(1, [4, 16]), reorder([0, 1, 3, 4, 2])],
+     "mp": [split(1, [4, 16]), split(3, [2, 7]), reorder([0, 1, 3, 4, 5, 2])]},
+])
+def test_pools_match_oracle(layouts):
+    g = pool_graph(2, 64, 28)
+    bufs = O.random_inputs(g, 42)
+    ins = {"x": bufs[0].copy()}
+    O.reference_eval(g, bufs)
+    out = runtime.interpret(g, layouts, [], ins)
+    assert np.array_equal(out["mp"], bufs[g.tensor_index("mp")])       # max: exact
+    assert O.max_rel_diff(out["y"], bufs[g.tensor_index("y")]) <= 1e-6
+
+
+def test_direct_stem_conv_fused_exact():
+    # 3-channel 7x7 stride-2 conv (the ResNet stem) + BiasAdd + ReLU: k/64
+    # inputs make fp32 accumulation exact, so the direct kernel must match.
+    g = ir.conv_chain(2, 3, 64, 64, 7, 2, 3)
+    bufs = O.random_inputs(g, 42)
+    ins = {t.id: bufs[i].copy() for i, t in enumerate(g.tensors) if t.role in (ir.INPUT, ir.CONSTANT)}
+    O.reference_eval(g, bufs)
+    p = runtime.Plan(g, {}, [runtime.sched(1, fuse=1)])
+    assert p.node_kernel(1) == "c2d_direct"
+    assert p.node_kernel(2) == "fused" and p.node_kernel(3) == "fused"
+    for k, v in ins.items():
+        p.set_input(k, v)
+    p.run()
+    assert np.array_equal(p.get_output("y"), bufs[g.tensor_index("y")])
+
+
+@pytest.mark.parametrize("shape,factors,force", [
+    ((1, 512, 512, 7, 3, 1, 1), (7, 7, 16, 64, 64, 16), None),     # auto split-K (deep K, 32 tiles)
+    ((1, 64, 64, 56, 3, 1, 1), (4, 28, 16, 32, 32, 16), "3"),      # forced, uneven stage ranges
+    ((2, 256, 256, 14, 3, 1, 1), (14, 14, 32, 64, 64, 32), "5"),
+])
+def test_splitk_conv_exact(shape, factors, force, monkeypatch):
+    if force:
+        monkeypatch.setenv("LFGPU_SPLITK", force)
+    n, ci, co, h, k, s, p = shape
+    g = ir.pad_conv(n, ci, co, h, k, s, p)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    x = R.k64((n, ci, h, h), gen)
+    w = R.k64((co, ci, k, k), gen)
+    plan = runtime.Plan(g, runtime.decode_layout(g, 1, list(factors)), [runtime.sched(1)],
+                        _abi.PLAN_REQUIRE_TC)
+    plan.set_input_device("x", x)
+    plan.set_input_device("ker", w)
+    for _ in range(3):  # re-launches exercise the re-armed arrival counters
+        plan.run()
+    y = torch.tensor(plan.get_output("y"), device="cuda")
+    ref = torch.nn.functional.conv2d(x.double(), w.double(), stride=s, padding=p).flatten()
+    assert torch.equal(y, ref)
+
+
+def test_splitk_fused_epilogue():
+    # bias + ReLU applied once, by the last CTA of each tile
+    g = ir.conv_chain(1, 256, 256, 14, 3, 1, 1)
+    bufs = O.random_inputs(g, 42)
+    ins = {t.id: bufs[i].copy() for i, t in enumerate(g.tensors) if t.role in (ir.INPUT, ir.CONSTANT)}
+    O.reference_eval(g, bufs)
+    seqs = runtime.decode_layout(g, 1, [7, 7, 16, 64, 64, 16])
+    seqs = workloads.propagate_elementwise(g, seqs)
+    p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=1)], _abi.PLAN_REQUIRE_TC)
+    assert "umma" in p.node_kernel(1) and p.node_kernel(3) == "fused"
+    for k, v in ins.items():
+        p.set_input(k, v)
+    p.run()
+    p.run()
+    assert np.array_equal(p.get_output("y"), bufs[g.tensor_index("y")])
+
+
+FIXED_FACTORS_B1 = {
+    # a residual-consistent assignment (stage output bricks shared by the
+    # second convs and the downsample conv), used so the test needs no tuning
+    "s1b1_a": (8, 7, 32, 32, 32, 32), "s1b1_b": (8, 7, 32, 32, 32, 32),
+    "s1b2_a": (8, 7, 32, 32, 32, 32), "s1b2_b": (8, 7, 32, 32, 32, 32),
+    "s2b1_ds": (28, 28, 32, 64, 64, 32), "s2b1_a": (28, 2, 16, 32, 32, 16),
+    "s2b1_b": (28, 28, 32, 64, 64, 32), "s2b2_a": (28, 28, 32, 64, 64, 32),
+    "s2b2_b": (28, 28, 32, 64, 64, 32),
+    "s3b1_ds": (14, 14, 16, 64, 64, 16), "s3b1_a": (7, 7, 32, 64, 64, 32),
+    "s3b1_b": (14, 14, 16, 64, 64, 16), "s3b2_a": (14, 14, 16, 64, 64, 16),
+    "s3b2_b": (14, 14, 16, 64, 64, 16),
+    "s4b1_ds": (7, 7, 16, 64, 64, 16), "s4b1_a": (7, 7, 16, 64, 64, 16),
+    "s4b1_b": (7, 7, 16, 64, 64, 16), "s4b2_a": (7, 7, 16, 64, 64, 16),
+    "s4b2_b": (7, 7, 16, 64, 64, 16),
+}
+
+
+def test_resnet18_b1_logits():
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(42)
+    g, convs, plan = R.build(1, FIXED_FACTORS_B1)
+    kinds = [plan.node_kernel(i) for i in range(len(g.nodes))]
+    tc = frozenset(i for i, k in enumerate(kinds) if k.startswith("umma"))
+    assert len(tc) >= 17, kinds                # every conv but the stem on tcgen05
+    assert kinds[convs[0]["node"]] == "c2d_direct"
+    assert "ix_copy" not in kinds                # template-to-template Paddings are digit maps
+    ins = R.make_inputs(g, gen)
+    for k, x in ins.items():
+        plan.set_input_device(k, x)
+    plan.run()
+    out = torch.tensor(plan.get_output("logits"), device="cuda").view(1, -1)
+    emu = R.reference(g, ins, tc, emulate=True)["logits"]
+    ex = R.reference(g, ins)["logits"]
+    assert R.max_rel(out, emu) <= 1e-4
+    assert R.max_rel(out, ex) <= 2e-3

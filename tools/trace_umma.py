@@ -52,6 +52,22 @@ def timeline(g, cand, inputs, name):
     ful = [(x - base) / 1000.0 for x in c0[32:] if x > 0]
     print("  CTA0 TMA issue times (us):", " ".join(f"{v:.2f}" for v in iss[:20]))
     print("  CTA0 stage landed   (us):", " ".join(f"{v:.2f}" for v in ful[:20]))
+    cyc = allb[74 * nct: 74 * nct + 32]
+    print("  CTA0 TMA issue-block cycles:", " ".join(str(int(x)) for x in cyc[:20]))
+    ph = allb[106 * nct: 106 * nct + 64].reshape(32, 2)
+    print("  CTA0 empty-wait cycles:", " ".join(str(int(x)) for x in ph[:20, 0]))
+    print("  CTA0 expect+stamp cycles:", " ".join(str(int(x)) for x in ph[:20, 1]))
+    # untraced kernel time (events, back-to-back launches of the same plan)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for _ in range(3):
+        p2.run()
+    torch.cuda.synchronize()
+    ev[0].record(torch.cuda.ExternalStream(p2.stream))
+    for _ in range(20):
+        p2.run()
+    ev[1].record(torch.cuda.ExternalStream(p2.stream))
+    torch.cuda.synchronize()
+    print(f"  untraced back-to-back: {ev[0].elapsed_time(ev[1]) / 20 * 1e3:.2f} us per launch")
     t0 = t[:, 0].min()
     rel = (t - t0) / 1000.0
     labels = ["entry", "setup", "tma_done", "first_full", "mma_done", "acc_ready", "epi_done",
@@ -93,7 +109,31 @@ def copy_calib():
         print(f"{name:32s} {us:8.2f} us  {byts / us / 1e3:8.1f} GB/s")
 
 
+def resnet_b1():
+    """The b1 ResNet-18 3x3 convs of stages 2-4 at the tuned bricks."""
+    for (c, h, f) in [(128, 28, (28, 28, 16, 64, 64, 16)), (256, 14, (14, 14, 16, 64, 64, 16)),
+                      (512, 7, (7, 7, 16, 64, 64, 16))]:
+        gc = ir.pad_conv(1, c, c, h, 3, 1, 1)
+        timeline(gc, tuner.Candidate({1: f}, [runtime.sched(1)]),
+                 {"x": k64((1, c, h, h)), "ker": k64((c, c, 3, 3))}, f"conv b1 {c}@{h} {f}")
+
+
+def single_cta():
+    """One CTA, long K: per-stage TMA issue/landing cost with an idle chip."""
+    for (M, K, N, f, tl) in [(128, 4096, 64, (128, 64, 64), 64), (128, 4096, 16, (128, 64, 16), 16),
+                             (128, 4096, 256, (128, 64, 256), 256)]:
+        g = ir.gemm(M, K, N)
+        timeline(g, tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tl)]),
+                 {"a": k64((M, K)), "b": k64((K, N))}, f"gemm 1-CTA {M}x{K}x{N} {f}")
+
+
 if __name__ == "__main__":
+    if os.environ.get("TRACE_SINGLE"):
+        single_cta()
+        sys.exit(0)
+    if os.environ.get("TRACE_RESNET"):
+        resnet_b1()
+        sys.exit(0)
     copy_calib()
     g = ir.gemm(1024, 1024, 1024)
     A, B = k64((1024, 1024)), k64((1024, 1024))
