@@ -70,7 +70,9 @@ def build(jobs=8, force=False, verbose=False):
         for src, log in failed:
             sys.stderr.write(f"--- {src}\n{log}\n")
         raise RuntimeError(f"nvcc failed on {len(failed)} file(s)")
-    if todo or not os.path.exists(LIB):
+    stale_lib = not os.path.exists(LIB) or any(
+        os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs)
+    if todo or stale_lib:
         cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -36,20 +36,18 @@ struct UmmaParams {
   const float* epi_ptr[kMaxEpi];
   int32_t epi_kind[kMaxEpi];
   int32_t epi_count;
-  int32_t nstages, BN, ksteps, pipe;
+  int32_t ntiles, nstages, BN, ksteps, pipe, nprod;
   int32_t a_boxes, b_boxes, a_slot, b_slot, tx_bytes;
-  int32_t a_rank, b_rank;
   uint64_t a_desc, b_desc;  // LBO/SBO/version/layout bits; start address added on device
   uint32_t a_kadv, b_kadv;
   uint32_t idesc;
-  uint32_t tmem_cols;
-  int32_t cols_unit;  // col_off[c] == col_off[0] + c
-  int32_t rows_unit;  // row_off[r] == r
-  int32_t ring_bytes; // pipeline ring (>= the epilogue's fp32 staging tile)
+  uint32_t tmem_cols;       // >= 2*BN: two accumulators
+  int32_t ring_bytes;       // SMEM pipeline ring
+  int32_t table_ints;       // [stages | col_off | row_off] as one contiguous int array
+  int32_t store_mode;       // 1: row-contiguous, 16-byte aligned output rows; 0: generic
+  int64_t col0;             // col_off[0] folded into the tile base in store mode 1
   unsigned long long* dbg;  // optional per-CTA %globaltimer checkpoints (8 per CTA)
-  int32_t epi_mode;         // unused (diagnostics)
-  int32_t epi_sig;          // EPI_SIG of a <= 3-op chain, -1 = generic
-  // Split-K: CTA (tile, split) accumulates stages [split*n/S, (split+1)*n/S);
+  // Split-K: unit (tile, split) accumulates stages [split*n/S, (split+1)*n/S);
   // partial tiles go to `ws`, the last CTA of a tile (per-tile counter) sums
   // them in split order and runs the fused epilogue.
   int32_t splits;
@@ -84,48 +82,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "@!p bra WAIT_LOOP;\n\t}" ::"r"(bar),
       "r"(parity)
       : "memory");
-}
-
-__device__ __forceinline__ void tma_load(const CUtensorMap* map, int rank, uint32_t dst,
-                                         uint32_t bar, const int32_t* c) {
-  const uint64_t m = reinterpret_cast<uint64_t>(map);
-  switch (rank) {
-    case 1:
-      asm volatile(
-          "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%3}], [%2];" ::"r"(dst),
-          "l"(m), "r"(bar), "r"(c[0])
-          : "memory");
-      break;
-    case 2:
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-          "l"(m), "r"(bar), "r"(c[0]), "r"(c[1])
-          : "memory");
-      break;
-    case 3:
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-          "l"(m), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2])
-          : "memory");
-      break;
-    case 4:
-      asm volatile(
-          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
-          "l"(m), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3])
-          : "memory");
-      break;
-    default:
-      asm volatile(
-          "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
-          "l"(m), "r"(bar), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
-          : "memory");
-      break;
-  }
 }
 
 __device__ __forceinline__ void tma_load5(const CUtensorMap* map, uint32_t dst, uint32_t bar,
@@ -186,171 +142,280 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
                  "+r"(v[30]), "+r"(v[31])::"memory");
 }
 
-#define EPI_SIG(a, b, c) ((a) | ((b) << 2) | ((c) << 4))
+// ---- kernel -----------------------------------------------------------------
+//
+// Persistent, warp-specialised (256 threads, one CTA per SM):
+//   warps 0, 2, 3   TMA producers: the CTA's stage sequence (over all its work
+//                   units) is dealt round-robin to them; one elected lane per
+//                   warp waits the ring slot, arms expect_tx and issues the
+//                   UTMALDG.5D boxes (tile part from the tile table + stage part
+//                   from the SMEM stage table);
+//   warp 1          MMA issuer: tcgen05.mma.cta_group::1.kind::f16 into one of
+//                   two TMEM accumulators (columns [0,BN) / [BN,2BN)), commit
+//                   frees the ring slot; the last stage of a unit commits the
+//                   accumulator to the epilogue;
+//   warps 4-7       epilogue: tcgen05.ld.32x32b (thread = tile row), the fused
+//                   element-wise chain, stores; releases the accumulator so the
+//                   MMA of the unit after next can reuse it. The epilogue of
+//                   unit i overlaps the main loop of unit i+1.
+// A work unit is (tile, K split). Split-K partials go to a workspace laid out
+// [unit][col/4][row][4] (coalesced float4 per warp); the last CTA to finish a
+// tile (per-tile counter) sums the partials in split order (deterministic) and
+// runs the epilogue.
 
-template <int K>
-__device__ __forceinline__ float epi_op(float x, const float* __restrict__ p, int64_t addr,
-                                        int n) {
-  if (K == EPI_BIAS) return x + __ldg(p + n);
-  if (K == EPI_RESIDUAL) return x + __ldg(p + addr);
-  if (K == EPI_RELU) return fmaxf(x, 0.0f);
-  return x;
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+constexpr int kEpiLd = 36;  // per-warp transpose buffer row stride (floats)
+static_assert(kEpiSmemBytes == 4 * 32 * kEpiLd * 4, "epilogue SMEM size");
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// Row-contiguous output brick: each epilogue warp walks rows, lanes walk
-// 4-column groups (16-byte SMEM reads and global stores when aligned).
-template <int K0, int K1, int K2>
-__device__ __forceinline__ void epi_rows(const float* __restrict__ stile, int ld, int rows, int cols,
-                                         int64_t cbase, const int64_t* __restrict__ s_row,
-                                         int n_base, float* __restrict__ out,
-                                         const float* __restrict__ e0, const float* __restrict__ e1,
-                                         const float* __restrict__ e2, int ew, int lane) {
-  const int groups = (cols + 3) >> 2;
-  for (int r = ew; r < rows; r += 4) {
-    const int64_t rb = cbase + s_row[r];
-    const bool vec = ((rb & 3) == 0) && ((cols & 3) == 0);
-    for (int g = lane; g < groups; g += 32) {
-      const int c = g << 2;
-      float4 x = *reinterpret_cast<const float4*>(stile + r * ld + c);
-      float v[4] = {x.x, x.y, x.z, x.w};
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32"
+      " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])::"memory");
+}
+
+template <int W>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float* f) {
+  uint32_t* v = reinterpret_cast<uint32_t*>(f);
+  if (W == 32) tmem_ld32(taddr, v);
+  else tmem_ld16(taddr, v);
+}
+
+// The fused element-wise chain (BiasAdd / EwAdd / ReLU, interp.cpp:137-165;
+// fusion groups lower.cpp:566-608). Kinds are kernel parameters, so every
+// branch is warp-uniform.
+//
+// Code size matters more than instruction count here: each SM runs the
+// epilogue only a few times per launch, so straight-line (unrolled) code is
+// fetched cold from L2 instruction by instruction (ncu: stall_no_inst
+// dominated an unrolled version, ~12 us per tile). The loops below are kept
+// rolled so one small body is fetched once and reused.
+// One W-column chunk of one unit's accumulator for the calling thread's row.
+// mode 3 publishes a split-K partial; otherwise (after the split-K sum when
+// splits > 1) the chunk goes through the per-warp SMEM buffer and is stored
+// with mode 1 (row-contiguous output: float4 row segments, 8 lanes per
+// 128 bytes) or mode 0 (generic: thread = row, coalesced when rows are the
+// contiguous side).
+template <int W>
+__device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, int c0, int row,
+                                       int lane, int q, float* wbuf, int rows, int cols,
+                                       int n_base, int64_t obase, const int64_t* s_row,
+                                       const int64_t* s_col, int mode, int split, int splits,
+                                       int64_t ws_tile, bool release, uint32_t tempty) {
+  float v[W];
+  tmem_ld<W>(taddr + c0, v);
+  if (release) {
+    // Every TMEM read of this accumulator is complete: hand it back to the MMA.
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty);
+  }
+  const int64_t wstride = static_cast<int64_t>(P.BN / 4) * 128;
+  if (mode == 3) {  // publish this split's partial tile ([unit][col/4][row] float4)
+    float4* w = reinterpret_cast<float4*>(P.ws) + (ws_tile + split) * wstride + (c0 / 4) * 128 + row;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t a = rb + c + j;
-        const int n = n_base + c + j;
-        if (c + j < cols) {
-          v[j] = epi_op<K0>(v[j], e0, a, n);
-          v[j] = epi_op<K1>(v[j], e1, a, n);
-          v[j] = epi_op<K2>(v[j], e2, a, n);
+    for (int j = 0; j < W / 4; ++j)
+      __stcg(w + j * 128, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+    return;
+  }
+  if (splits > 1) {  // last CTA of the tile: sum the partials in split order
+    float acc[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc[j] = 0.0f;
+    const float4* w0 = reinterpret_cast<const float4*>(P.ws) + ws_tile * wstride + (c0 / 4) * 128 + row;
+#pragma unroll 1
+    for (int s = 0; s < splits; ++s) {
+      if (s == split) {
+#pragma unroll
+        for (int j = 0; j < W; ++j) acc[j] += v[j];
+      } else {
+        const float4* w = w0 + s * wstride;
+#pragma unroll
+        for (int j = 0; j < W / 4; ++j) {
+          const float4 x = __ldcg(w + j * 128);
+          acc[4 * j] += x.x;
+          acc[4 * j + 1] += x.y;
+          acc[4 * j + 2] += x.z;
+          acc[4 * j + 3] += x.w;
         }
       }
-      if (vec) {
-        *reinterpret_cast<float4*>(out + rb + c) = make_float4(v[0], v[1], v[2], v[3]);
-      } else {
+    }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (c + j < cols) out[rb + c + j] = v[j];
+    for (int j = 0; j < W; ++j) v[j] = acc[j];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < W / 4; ++j)
+    *reinterpret_cast<float4*>(wbuf + lane * kEpiLd + 4 * j) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  __syncwarp();
+  if (mode == 1) {
+    // All SMEM reads and addresses first, then the op chain, then the
+    // stores: independent instructions the SM can overlap (the previous
+    // one-row-per-iteration loop was latency bound).
+    constexpr int LPR = W / 4;     // lanes per row
+    constexpr int RPI = 32 / LPR;  // rows per instruction
+    constexpr int IT = 32 / RPI;
+    const int cl = (lane % LPR) * 4;
+    const int c = c0 + cl;
+    float4 x[IT];
+    int64_t addr[IT];
+    bool ok[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int rr = it * RPI + lane / LPR;
+      const int r = q * 32 + rr;
+      ok[it] = r < rows && c < cols;
+      x[it] = *reinterpret_cast<const float4*>(wbuf + rr * kEpiLd + cl);
+      addr[it] = obase + s_row[r] + c;
+    }
+#pragma unroll 1
+    for (int e = 0; e < P.epi_count; ++e) {
+      const int k = P.epi_kind[e];
+      const float* ep = P.epi_ptr[e];
+      if (k == EPI_RELU) {
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          x[it].x = fmaxf(x[it].x, 0.0f);
+          x[it].y = fmaxf(x[it].y, 0.0f);
+          x[it].z = fmaxf(x[it].z, 0.0f);
+          x[it].w = fmaxf(x[it].w, 0.0f);
+        }
+      } else if (k == EPI_BIAS) {
+        const float* bp = ep + n_base + c;
+        const float4 bb = c < cols ? make_float4(__ldg(bp), __ldg(bp + 1), __ldg(bp + 2), __ldg(bp + 3))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          x[it].x += bb.x;
+          x[it].y += bb.y;
+          x[it].z += bb.z;
+          x[it].w += bb.w;
+        }
+      } else {  // EPI_RESIDUAL
+        float4 rv[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it)
+          rv[it] = ok[it] ? __ldg(reinterpret_cast<const float4*>(ep + addr[it]))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          x[it].x += rv[it].x;
+          x[it].y += rv[it].y;
+          x[it].z += rv[it].z;
+          x[it].w += rv[it].w;
+        }
       }
     }
-  }
-}
-
-// Row-contiguous side (M-major output, e.g. NCHW or a (M/m_t) N m_t brick):
-// each epilogue warp walks columns, lanes walk consecutive rows.
-template <int K0, int K1, int K2>
-__device__ __forceinline__ void epi_cols(const float* __restrict__ stile, int ld, int rows, int cols,
-                                         int64_t rbase, const int64_t* __restrict__ s_col,
-                                         int n_base, float* __restrict__ out,
-                                         const float* __restrict__ e0, const float* __restrict__ e1,
-                                         const float* __restrict__ e2, int ew, int lane) {
-  for (int c = ew; c < cols; c += 4) {
-    const int64_t cb = rbase + s_col[c];
-    const int n = n_base + c;
-    for (int r = lane; r < rows; r += 32) {
-      float v = stile[r * ld + c];
-      v = epi_op<K0>(v, e0, cb + r, n);
-      v = epi_op<K1>(v, e1, cb + r, n);
-      v = epi_op<K2>(v, e2, cb + r, n);
-      out[cb + r] = v;
-    }
-  }
-}
-
-// Any output brick (e.g. M-contiguous C): lanes walk rows when the rows are
-// the contiguous side, else columns; runtime op chain (rare shapes).
-template <typename PT>
-__device__ __noinline__ void epi_generic(const PT& P, const float* __restrict__ stile, int ld,
-                                         int rows, int cols, int64_t obase,
-                                         const int64_t* __restrict__ s_row,
-                                         const int64_t* __restrict__ s_col, int n_base,
-                                         float* __restrict__ out, int et) {
-  int ek[kMaxEpi];
-  const float* ep[kMaxEpi];
 #pragma unroll
-  for (int e = 0; e < kMaxEpi; ++e) {
-    ek[e] = e < P.epi_count ? P.epi_kind[e] : EPI_NONE;
-    ep[e] = P.epi_ptr[e];
+    for (int it = 0; it < IT; ++it)
+      if (ok[it]) *reinterpret_cast<float4*>(P.out + addr[it]) = x[it];
+    return;
   }
-  const bool row_fast = P.rows_unit && !P.cols_unit;
-  const int ew = et >> 5, lane = et & 31;
-  const int outer = row_fast ? cols : rows, inner = row_fast ? rows : cols;
-  for (int o = ew; o < outer; o += 4) {
-    for (int i = lane; i < inner; i += 32) {
-      const int r = row_fast ? i : o, c = row_fast ? o : i;
-      const int64_t addr = obase + s_row[r] + s_col[c];
-      float x = stile[r * ld + c];
+  // Generic: thread = row, 8 columns per step (loads, ops, stores batched).
+  if (row < rows) {
+    const int64_t rb = obase + s_row[row];
+    const float* mine = wbuf + lane * kEpiLd;
+#pragma unroll 1
+    for (int j0 = 0; j0 < W; j0 += 8) {
+      float y[8];
+      int64_t a[8];
 #pragma unroll
-      for (int e = 0; e < kMaxEpi; ++e) {
-        if (ek[e] == EPI_BIAS) x += __ldg(ep[e] + n_base + c);
-        else if (ek[e] == EPI_RESIDUAL) x += __ldg(ep[e] + addr);
-        else if (ek[e] == EPI_RELU) x = fmaxf(x, 0.0f);
+      for (int j = 0; j < 8; ++j) {
+        y[j] = mine[j0 + j];
+        a[j] = rb + s_col[c0 + j0 + j];
       }
-      out[addr] = x;
+#pragma unroll 1
+      for (int e = 0; e < P.epi_count; ++e) {
+        const int k = P.epi_kind[e];
+        const float* ep = P.epi_ptr[e];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (k == EPI_RELU) y[j] = fmaxf(y[j], 0.0f);
+          else if (c0 + j0 + j < cols)
+            y[j] += __ldg(ep + (k == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j0 + j) : a[j]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (c0 + j0 + j < cols) P.out[a[j]] = y[j];
     }
   }
-}
-
-constexpr int kThreads = 192;
-constexpr int kEpiThreads = 128;
-
-__device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     umma_kernel(const __grid_constant__ CUtensorMap tma_a,
-                const __grid_constant__ CUtensorMap tma_b, const UmmaParams P) {
+                const __grid_constant__ CUtensorMap tma_b, const __grid_constant__ UmmaParams P) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B atoms) by offsetting the __shared__
   // array itself, so every derived pointer stays in the shared window.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stage_bytes = P.a_boxes * P.a_slot + P.b_boxes * P.b_slot;
-  // The epilogue stages the fp32 tile (128 x (BN+1)) over the pipeline ring
-  // once every MMA has retired; ring_bytes >= that (host-checked).
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes);
+  float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + kEpiSmemBytes);
+  const int pipe = P.pipe;
   const uint32_t full0 = smem_u32(bars);
-  const uint32_t empty0 = full0 + 8 * P.pipe;
-  const uint32_t accf = empty0 + 8 * P.pipe;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P.pipe + 1);
-  // After the barriers: this tile's entry, the stage table and the epilogue's
-  // row/column offsets, all copied from global memory once.
-  TileEntry* s_tile = reinterpret_cast<TileEntry*>(bars + 2 * P.pipe + 2);
-  StageEntry* s_stage = reinterpret_cast<StageEntry*>(s_tile + 1);
+  const uint32_t empty0 = full0 + 8 * pipe;
+  const uint32_t tfull0 = empty0 + 8 * pipe;   // 2 accumulator-full barriers
+  const uint32_t tempty0 = tfull0 + 16;        // 2 accumulator-empty barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * pipe + 4);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  StageEntry* s_stage = reinterpret_cast<StageEntry*>(bars + 2 * pipe + 5);
   int64_t* s_col = reinterpret_cast<int64_t*>(s_stage + P.nstages);
   int64_t* s_row = s_col + P.BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int splits = P.splits;
-  const int tile = blockIdx.x / splits, split = blockIdx.x - tile * splits;
-  const int s_lo = split * P.nstages / splits, s_hi = (split + 1) * P.nstages / splits;
-  int* s_flag = reinterpret_cast<int*>(s_row + 128);
-  unsigned long long* dbg = P.dbg ? P.dbg + 8 * tile : nullptr;
-  const int pipe = P.pipe;
-  const int early = 0;
+  const int nunits = P.ntiles * splits;
+  const int nst = P.nstages;
+  unsigned long long* dbg = P.dbg ? P.dbg + 8 * blockIdx.x : nullptr;
+  if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
 
   if (threadIdx.x == 0) {
-    if (dbg) {
-      dbg[0] = gtimer();
-      P.dbg[8 * gridDim.x + 2 * tile] = clock64();
-    }
     for (int s = 0; s < pipe; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
-  {
-    const int* g = reinterpret_cast<const int*>(P.tiles + tile);
-    int* d = reinterpret_cast<int*>(s_tile);
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(TileEntry) / 4); i += kThreads) d[i] = g[i];
-    const int* gs = reinterpret_cast<const int*>(P.stages);
-    int* ds = reinterpret_cast<int*>(s_stage);
-    const int nst = P.nstages * static_cast<int>(sizeof(StageEntry) / 4);
-    for (int i = threadIdx.x; i < nst; i += kThreads) ds[i] = gs[i];
-    for (int i = threadIdx.x; i < P.BN; i += kThreads) s_col[i] = P.col_off[i];
-    for (int i = threadIdx.x; i < 128; i += kThreads) s_row[i] = P.row_off[i];
+  {  // plan tables (written once by the host, never by kernels: safe before
+     // the PDL wait). One flat int array [stages | col_off | row_off]; all
+     // loads of a thread are issued before any SMEM store (one DRAM latency).
+    const int* src = reinterpret_cast<const int*>(P.stages);
+    int* dst = reinterpret_cast<int*>(s_stage);
+    const int n = P.table_ints;
+    int v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = threadIdx.x + k * kThreads;
+      v[k] = i < n ? __ldg(src + i) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = threadIdx.x + k * kThreads;
+      if (i < n) dst[i] = v[k];
+    }
+    for (int i = threadIdx.x + 8 * kThreads; i < n; i += kThreads) dst[i] = __ldg(src + i);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -363,49 +428,46 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch: everything above overlapped the previous
+  // kernel's tail; operands / outputs are touched only after this wait.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
 
-  // ---- TMA producers. One thread's serial issue path (barrier wait +
-  // expect_tx + UTMALDGs, ~450 cycles per stage measured) would cap a CTA at
-  // ~one stage per 0.25 us, so warps 0 and 2-4 (the epilogue warps are idle
-  // during the main loop) issue stages round-robin; each computes its own
-  // ring slot / phase. Coordinates = tile part (registers) + stage part
-  // (SMEM); views are always 5-D (host pads unit dims) so each load is one
-  // straight-line UTMALDG.5D with no rank dispatch.
-  constexpr int kProducers = 4;
-  const int prod = warp == 0 ? 0 : (warp >= 2 && warp <= 4 ? warp - 1 : -1);
-  if (prod >= 0) {
-    int32_t ta[kMaxBoxes][5], tb[kMaxBoxes][5];
-#pragma unroll
-    for (int b = 0; b < kMaxBoxes; ++b)
-#pragma unroll
-      for (int d = 0; d < 5; ++d) {
-        ta[b][d] = s_tile->ca[b][d];
-        tb[b][d] = s_tile->cb[b][d];
-      }
-    const int na = P.a_boxes, nb = P.b_boxes;
+  const int prod = warp == 0 ? 0 : (warp == 2 || warp == 3 ? warp - 1 : -1);
+  if (prod >= 0 && prod < P.nprod) {
+    // ---- TMA producers
+    const int np = P.nprod;
     const uint32_t tx = P.tx_bytes, a_slot = P.a_slot, b_slot = P.b_slot;
     const uint32_t ring0 = smem_u32(smem);
-    const uint32_t b_off = na * a_slot;
+    const uint32_t b_off = P.a_boxes * a_slot;
+    const int na = P.a_boxes, nb = P.b_boxes;
     const bool leader = elect_one();
-    for (int s = s_lo + prod; s < s_hi; s += kProducers) {
-      if (leader) {
-        const int it = s - s_lo;
+    int g = 0;  // CTA-wide stage counter (ring slot / phase)
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int tile = u / splits, split = u - tile * splits;
+      const int s_lo = split * nst / splits, s_hi = (split + 1) * nst / splits;
+      int s = s_lo + ((prod - g) % np + np) % np;
+      g += s_hi - s_lo;
+      if (s >= s_hi || !leader) continue;
+      int32_t ta[kMaxBoxes][5], tb[kMaxBoxes][5];
+      const TileEntry* te = P.tiles + tile;
+#pragma unroll
+      for (int b = 0; b < kMaxBoxes; ++b)
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          ta[b][d] = b < na ? __ldg(&te->ca[b][d]) : 0;
+          tb[b][d] = b < nb ? __ldg(&te->cb[b][d]) : 0;
+        }
+      for (; s < s_hi; s += np) {
+        const int it = g - (s_hi - s);  // CTA-wide index of stage s
         const int slot = it % pipe;
         const uint32_t phase = static_cast<uint32_t>(it / pipe) & 1u;
-        const long long c_top = dbg ? clock64() : 0;
         mbar_wait(empty0 + 8 * slot, phase ^ 1);
-        const long long c_wait = dbg ? clock64() : 0;
         const uint32_t bar = full0 + 8 * slot;
         mbar_expect_tx(bar, tx);
         const StageEntry se = s_stage[s];
-        if (dbg && s < 32) P.dbg[10 * gridDim.x + 64 * tile + s] = gtimer();
         const uint32_t a_dst = ring0 + slot * stage_bytes;
-        const long long c_issue = dbg ? clock64() : 0;
-        if (dbg && it < 32) {
-          P.dbg[106 * gridDim.x + 64 * tile + 2 * it] = c_wait - c_top;
-          P.dbg[106 * gridDim.x + 64 * tile + 2 * it + 1] = c_issue - c_wait;
-        }
 #pragma unroll
         for (int b = 0; b < kMaxBoxes; ++b)
           if (b < na)
@@ -417,15 +479,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load5(&tma_b, a_dst + b_off + b * b_slot, bar, tb[b][0] + se.sb[0],
                       tb[b][1] + se.sb[1], tb[b][2] + se.sb[2], tb[b][3] + se.sb[3],
                       tb[b][4] + se.sb[4]);
-        if (dbg && it < 32) P.dbg[74 * gridDim.x + 32 * tile + it] = clock64() - c_issue;
       }
     }
     __syncwarp();
-    if (dbg && leader && prod == 0) dbg[2] = gtimer();
-  }
-  if (warp == 0) {
+    if (dbg && prod == 0 && lane == 0) dbg[2] = gtimer();
   } else if (warp == 1) {
-    // ---- MMA issuer (whole warp loops; one elected lane issues tcgen05.mma)
+    // ---- MMA issuer (whole warp loops; one elected lane issues)
     const uint64_t adesc = P.a_desc, bdesc = P.b_desc;
     const uint32_t idesc = P.idesc, akadv = P.a_kadv, bkadv = P.b_kadv;
     const int ksteps = P.ksteps;
@@ -434,128 +493,94 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = elect_one();
     int slot = 0;
     uint32_t phase = 0;
-    for (int s = s_lo; s < s_hi; ++s) {
-      mbar_wait(full0 + 8 * slot, phase);
-      if (dbg && leader && s == s_lo) dbg[3] = gtimer();
-      if (dbg && leader && s < 32) P.dbg[10 * gridDim.x + 64 * tile + 32 + s] = gtimer();
+    int i = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+      const int split = u % splits;
+      const int s_lo = split * nst / splits, s_hi = (split + 1) * nst / splits;
+      const int b = i & 1;
+      mbar_wait(tempty0 + 8 * b, (static_cast<uint32_t>(i >> 1) & 1u) ^ 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (leader) {
-        const uint32_t a_addr = ring0 + slot * stage_bytes;
-        const uint32_t b_addr = a_addr + a_off_b;
-        for (int k = 0; k < ksteps; ++k) {
-          const uint64_t ad = adesc | (((a_addr + k * akadv) >> 4) & 0x3FFFull);
-          const uint64_t bd = bdesc | (((b_addr + k * bkadv) >> 4) & 0x3FFFull);
-          umma_bf16(tmem, ad, bd, idesc, (s != s_lo) || (k != 0));
+      const uint32_t dtm = tmem + static_cast<uint32_t>(b * P.BN);
+      for (int s = s_lo; s < s_hi; ++s) {
+        mbar_wait(full0 + 8 * slot, phase);
+        if (dbg && leader && i == 0 && s == s_lo) dbg[3] = gtimer();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (leader) {
+          const uint32_t a_addr = ring0 + slot * stage_bytes;
+          const uint32_t b_addr = a_addr + a_off_b;
+          for (int k = 0; k < ksteps; ++k) {
+            const uint64_t ad = adesc | (((a_addr + k * akadv) >> 4) & 0x3FFFull);
+            const uint64_t bd = bdesc | (((b_addr + k * bkadv) >> 4) & 0x3FFFull);
+            umma_bf16(dtm, ad, bd, idesc, (s != s_lo) || (k != 0));
+          }
+          umma_commit(empty0 + 8 * slot);
         }
-        umma_commit(empty0 + 8 * slot);
+        __syncwarp();
+        if (++slot == pipe) {
+          slot = 0;
+          phase ^= 1;
+        }
       }
+      if (leader) umma_commit(tfull0 + 8 * b);
       __syncwarp();
-      if (++slot == pipe) {
-        slot = 0;
-        phase ^= 1;
-      }
     }
-    if (leader) umma_commit(accf);
     if (dbg && leader) dbg[4] = gtimer();
-  } else if (warp >= 2) {
-    // ---- epilogue (4 warps). Phase 1: TMEM -> SMEM tile (row r = TMEM lane r).
-    const int quad = warp & 3;
-    const int row = quad * 32 + lane;
-    // SMEM row stride: 16-byte aligned rows for the float4 row pass, odd for
-    // the column pass (conflict-free lane-per-row reads).
-    const int ld = (P.cols_unit || !P.rows_unit) ? P.BN + 4 : P.BN + 1;
-    float* stile = reinterpret_cast<float*>(smem);
-    mbar_wait(accf, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (dbg && threadIdx.x == 64) dbg[5] = gtimer();
-    if (splits == 1) {
-      for (int c0 = 0; c0 < P.BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (c0 + j < P.BN) stile[row * ld + c0 + j] = __uint_as_float(v[j]);
-      }
-    } else {
-      // Split-K: publish this split's partial tile, count arrivals; the last
-      // CTA of the tile sums the partials in split order (deterministic).
-      float* wrow = P.ws + ((static_cast<int64_t>(tile) * splits + split) * 128 + row) * P.BN;
-      for (int c0 = 0; c0 < P.BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (c0 + j < P.BN) __stcg(wrow + c0 + j, __uint_as_float(v[j]));
-      }
-      __threadfence();
-      epi_bar();
-      if (threadIdx.x == 64) {
-        const int prev = atomicAdd(P.counters + tile, 1);
-        *s_flag = prev == splits - 1;
-        if (prev == splits - 1) P.counters[tile] = 0;  // re-armed for the next launch
-      }
-      epi_bar();
-      if (*s_flag) {
+  } else if (warp >= kEpiWarp0) {
+    // ---- epilogue (4 warps; warp w reads TMEM lanes 32*(w%4)..+31)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    float* wbuf = s_epi + q * 32 * kEpiLd;
+    const int BN = P.BN;
+    int i = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+      const int tile = u / splits, split = u - tile * splits;
+      const int b = i & 1;
+      const uint32_t tempty = tempty0 + 8 * b;
+      // The tile entry does not depend on the accumulator: load it before
+      // waiting so its (possibly DRAM) latency hides under the main loop.
+      const TileEntry* te = P.tiles + tile;
+      const int rows = __ldg(&te->rows), cols = __ldg(&te->cols), n_base = __ldg(&te->n_base);
+      const int64_t obase = __ldg(&te->out_base) + P.col0;
+      mbar_wait(tfull0 + 8 * b, static_cast<uint32_t>(i >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[5] = gtimer();
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * BN);
+      const int64_t ws_tile = static_cast<int64_t>(tile) * splits;
+      if (splits > 1) {
+        int c0 = 0;
+        for (; c0 + 32 <= BN; c0 += 32)
+          epi_chunk<32>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, 3,
+                        split, splits, ws_tile, false, tempty);
+        if (c0 < BN)
+          epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, 3,
+                        split, splits, ws_tile, false, tempty);
         __threadfence();
-        const float* w0 = P.ws + (static_cast<int64_t>(tile) * splits * 128 + row) * P.BN;
-        for (int c = 0; c < P.BN; ++c) {
-          float acc = 0.f;
-          for (int q = 0; q < splits; ++q) acc += __ldcg(w0 + static_cast<int64_t>(q) * 128 * P.BN + c);
-          stile[row * ld + c] = acc;
+        epi_bar();
+        if (threadIdx.x == kEpiWarp0 * 32) {
+          const int prev = atomicAdd(P.counters + tile, 1);
+          *s_flag = prev == splits - 1;
+          if (prev == splits - 1) P.counters[tile] = 0;  // re-armed for the next launch
         }
+        epi_bar();
+        if (!*s_flag) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+          continue;
+        }
+        __threadfence();
       }
+      const int mode = P.store_mode;
+      int c0 = 0;
+      const int full_end = BN & ~31;
+      for (; c0 < full_end; c0 += 32)
+        epi_chunk<32>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, mode,
+                      split, splits, ws_tile, c0 + 32 >= BN, tempty);
+      if (c0 < BN)
+        epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, mode,
+                      split, splits, ws_tile, true, tempty);
     }
-    epi_bar();
-    if (splits == 1 || *s_flag) {
-    if (dbg && threadIdx.x == 64) dbg[7] = gtimer();
-    // Phase 2: cooperative, coalesced stores with the fused element-wise chain
-    // (bias / residual / relu, lower.cpp:566-608). Lanes run along the
-    // physically contiguous side of the output brick.
-    const int et = threadIdx.x - 64;  // 0..127
-    const int rows = s_tile->rows, cols = s_tile->cols, n_base = s_tile->n_base;
-    const int64_t obase = s_tile->out_base;
-    float* __restrict__ out = P.out;
-    // The element-wise chain (<= 3 ops: bias / residual / relu) is resolved
-    // once into a signature and each signature runs a specialised loop: no
-    // per-element switch, no indirect branches, no param-buffer loads.
-    const int sig = P.epi_sig;
-    const float* e0 = P.epi_ptr[0];
-    const float* e1 = P.epi_ptr[1];
-    const float* e2 = P.epi_ptr[2];
-    const int ew = et >> 5;  // epilogue warp 0..3
-    if (P.cols_unit && (ld & 3) == 0) {
-      const int64_t cbase = obase + s_col[0];
-      switch (sig) {
-        case EPI_SIG(0, 0, 0): epi_rows<0, 0, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(1, 0, 0): epi_rows<1, 0, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(1, 2, 0): epi_rows<1, 2, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(1, 3, 0): epi_rows<1, 3, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(1, 3, 2): epi_rows<1, 3, 2>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(2, 0, 0): epi_rows<2, 0, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(3, 0, 0): epi_rows<3, 0, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(3, 2, 0): epi_rows<3, 2, 0>(stile, ld, rows, cols, cbase, s_row, n_base, out, e0, e1, e2, ew, lane); break;
-        default: epi_generic(P, stile, ld, rows, cols, obase, s_row, s_col, n_base, out, et); break;
-      }
-    } else if (P.rows_unit) {
-      switch (sig) {
-        case EPI_SIG(0, 0, 0): epi_cols<0, 0, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(1, 0, 0): epi_cols<1, 0, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(1, 2, 0): epi_cols<1, 2, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(1, 3, 0): epi_cols<1, 3, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(1, 3, 2): epi_cols<1, 3, 2>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(2, 0, 0): epi_cols<2, 0, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(3, 0, 0): epi_cols<3, 0, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
-        case EPI_SIG(3, 2, 0): epi_cols<3, 2, 0>(stile, ld, rows, cols, obase, s_col, n_base, out, e0, e1, e2, ew, lane); break;
-        default: epi_generic(P, stile, ld, rows, cols, obase, s_row, s_col, n_base, out, et); break;
-      }
-    } else {
-      epi_generic(P, stile, ld, rows, cols, obase, s_row, s_col, n_base, out, et);
-    }
-    if (dbg && threadIdx.x == 64) {
-      dbg[6] = gtimer();
-      P.dbg[8 * gridDim.x + 2 * tile + 1] = clock64();
-    }
-    }
+    if (dbg && threadIdx.x == kEpiWarp0 * 32) dbg[6] = gtimer();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -662,13 +687,36 @@ static void* g_umma_dbg = nullptr;
 void* umma_debug_buffer() { return g_umma_dbg; }
 void umma_set_debug_buffer(void* p) { g_umma_dbg = p; }
 
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
 UmmaLaunch umma_prepare(const UmmaPlan& p) {
   UmmaLaunch L;
   L.tma_a = encode(p.A, p.a);
   L.tma_b = encode(p.B, p.b);
   auto t = std::make_shared<Tables>();
   t->p[0] = up(p.tiles);
-  t->p[1] = up(p.stages);
+  {  // [stages | col_off | row_off] contiguous: the kernel copies it to SMEM in one pass
+    std::vector<int32_t> tab(p.stages.size() * sizeof(StageEntry) / 4 + 2 * (p.col_off.size() + 128));
+    size_t o = 0;
+    std::memcpy(tab.data(), p.stages.data(), p.stages.size() * sizeof(StageEntry));
+    o += p.stages.size() * sizeof(StageEntry) / 4;
+    std::memcpy(tab.data() + o, p.col_off.data(), p.col_off.size() * 8);
+    o += p.col_off.size() * 2;
+    std::vector<int64_t> rows(128, 0);
+    for (size_t r = 0; r < 128 && r < p.row_off.size(); ++r) rows[r] = p.row_off[r];
+    std::memcpy(tab.data() + o, rows.data(), 128 * 8);
+    L.table_ints = static_cast<int>(tab.size());
+    t->p[1] = up(tab);
+  }
   t->p[2] = up(p.row_off);
   t->p[3] = up(p.col_off);
   L.d_tiles = t->p[0];
@@ -682,7 +730,8 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   L.KC = p.KC;
   L.pipe = p.pipe;
   int cols = 32;
-  while (cols < p.BN) cols *= 2;
+  while (cols < 2 * p.BN) cols *= 2;  // two accumulators (epilogue/main-loop overlap)
+  if (cols > 512) fail(LFGPU_EUNSUPPORTED, "accumulators exceed 512 TMEM columns");
   L.tmem_cols = cols;
   L.a_boxes = p.A.boxes;
   L.b_boxes = p.B.boxes;
@@ -702,26 +751,40 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   }
   L.out = p.out;
   const size_t ring = static_cast<size_t>(p.pipe) * (L.a_boxes * L.a_slot + L.b_boxes * L.b_slot);
-  const size_t staging = static_cast<size_t>(128) * (p.BN + 4) * 4;
-  L.ring_bytes = static_cast<int>((std::max(ring, staging) + 1023) / 1024 * 1024);
-  L.smem = 1024 + L.ring_bytes + 8 * (2 * p.pipe + 2) + sizeof(TileEntry) +
+  L.ring_bytes = static_cast<int>((ring + 1023) / 1024 * 1024);
+  L.smem = 1024 + L.ring_bytes + kEpiSmemBytes + 8 * (2 * p.pipe + 4) + 8 +
            sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 64;
-  // Contiguity over the rows any tile actually stores.
+  if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "tcgen05 kernel SMEM exceeds 227 KB");
+  L.nprod = std::max(1, std::min(3, p.pipe - 1));
+  // Store mode 1 (transposed, float4 row stores): output columns contiguous
+  // and every stored row 16-byte aligned.
   int max_rows = 0;
-  for (const auto& t : p.tiles) max_rows = std::max(max_rows, static_cast<int>(t.rows));
-  L.rows_unit = 1;
-  for (int r = 0; r < max_rows && r < static_cast<int>(p.row_off.size()); ++r)
-    if (p.row_off[r] != static_cast<int64_t>(r)) L.rows_unit = 0;
-  L.cols_unit = 1;
+  for (const auto& te : p.tiles) max_rows = std::max(max_rows, static_cast<int>(te.rows));
+  bool cols_unit = !p.col_off.empty();
   for (size_t c = 0; c < p.col_off.size(); ++c)
-    if (p.col_off[c] != p.col_off[0] + static_cast<int64_t>(c)) L.cols_unit = 0;
-  // Split-K when the tiles alone leave most of the 148 SMs idle and the
-  // K loop is long: up to 8 splits of >= 4 stages each.
+    if (p.col_off[c] != p.col_off[0] + static_cast<int64_t>(c)) cols_unit = false;
+  bool aligned = cols_unit && (p.col_off[0] % 4 == 0);
+  for (int r = 0; aligned && r < max_rows && r < static_cast<int>(p.row_off.size()); ++r)
+    if (p.row_off[r] % 4) aligned = false;
+  for (const auto& te : p.tiles)
+    if (te.out_base % 4 || te.cols % 4) aligned = false;
+  L.store_mode = aligned ? 1 : 0;
+  L.col0 = aligned ? p.col_off[0] : 0;
+  if (const char* e = getenv("LFGPU_STORE_MODE")) {  // diagnostics: force the generic path
+    if (atoi(e) == 0) {
+      L.store_mode = 0;
+      L.col0 = 0;
+    }
+  }
+  // Split-K (schedule `order`: 0 = heuristic, 1 = never, 2 = at least 2):
+  // when the tiles alone leave most of the SMs idle and the K loop is long.
+  const int sms = num_sms();
   L.splits = 1;
-  if (L.ntiles * 2 <= 148 && L.nstages >= 8) {
-    L.splits = std::min({148 / L.ntiles, L.nstages / 4, 8});
+  if (p.split_pref != 1 && L.ntiles * 2 <= sms && L.nstages >= 8) {
+    L.splits = std::min({sms / L.ntiles, L.nstages / 4, 8});
     if (L.splits < 2) L.splits = 1;
   }
+  if (p.split_pref == 2) L.splits = std::max(L.splits, std::min(2, L.nstages));
   if (const char* e = getenv("LFGPU_SPLITK")) L.splits = std::max(1, std::min(atoi(e), L.nstages));
   if (L.splits > 1) {
     const size_t ws = sizeof(float) * static_cast<size_t>(L.ntiles) * L.splits * 128 * L.BN;
@@ -732,9 +795,8 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     L.ws = static_cast<float*>(t->p[4]);
     L.counters = static_cast<int*>(t->p[5]);
   }
-  L.grid = L.ntiles * L.splits;
-  L.a_rank_ = p.A.rank;
-  L.b_rank_ = p.B.rank;
+  // Persistent grid: one CTA per SM at most, units dealt round-robin.
+  L.grid = std::min(L.ntiles * L.splits, sms);
   static_assert(sizeof(TileEntry) == 192, "TileEntry layout");
   return L;
 }
@@ -749,48 +811,59 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.col_off = static_cast<const int64_t*>(L.d_cols);
   P.out = L.out;
   P.epi_count = L.epi_count;
-  P.epi_sig = L.epi_count <= 3 ? 0 : -1;
-  for (int e = 0; e < L.epi_count && e < 3; ++e) P.epi_sig |= L.epi_kinds[e] << (2 * e);
   for (int e = 0; e < L.epi_count; ++e) {
     P.epi_kind[e] = L.epi_kinds[e];
     P.epi_ptr[e] = L.epi_ptr[e];
   }
+  P.ntiles = L.ntiles;
   P.nstages = L.nstages;
   P.BN = L.BN;
   P.ksteps = L.KC / 16;
   P.pipe = L.pipe;
+  P.nprod = L.nprod;
   P.a_boxes = L.a_boxes;
   P.b_boxes = L.b_boxes;
   P.a_slot = L.a_slot;
   P.b_slot = L.b_slot;
   P.tx_bytes = L.a_boxes * L.a_bytes + L.b_boxes * L.b_bytes;
-  // rank is encoded in the tensor map; keep our own copy for the PTX form
   P.a_desc = L.a_desc;
   P.b_desc = L.b_desc;
   P.a_kadv = L.a_kadv;
   P.b_kadv = L.b_kadv;
   P.idesc = L.idesc;
   P.tmem_cols = L.tmem_cols;
-  P.a_rank = L.a_rank_;
-  P.cols_unit = L.cols_unit;
-  P.rows_unit = L.rows_unit;
   P.ring_bytes = L.ring_bytes;
+  P.table_ints = L.table_ints;
+  P.store_mode = L.store_mode;
+  P.col0 = L.col0;
   P.splits = L.splits;
   P.ws = L.ws;
   P.counters = L.counters;
   P.dbg = static_cast<unsigned long long*>(umma_debug_buffer());
-  if (P.dbg) {
-    const char* em = getenv("LFGPU_EPI_MODE");
-    P.epi_mode = em ? atoi(em) : 0;
-  }
-  P.b_rank = L.b_rank_;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  umma_kernel<<<L.grid, kThreads, L.smem, stream>>>(L.tma_a, L.tma_b, P);
-  return cudaGetLastError();
+  // Programmatic dependent launch: the prologue (barriers, TMEM, tables)
+  // overlaps the previous kernel; the kernel waits (griddepcontrol.wait)
+  // before touching operands or outputs.
+  static const bool pdl = [] {
+    const char* e = getenv("LFGPU_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(L.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, umma_kernel, L.tma_a, L.tma_b, P);
 }
 
 }  // namespace lfg

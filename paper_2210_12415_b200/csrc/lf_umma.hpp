@@ -28,6 +28,8 @@ enum { UMMA_GEMM = 0, UMMA_CONV = 1 };
 enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_RELU = 2, EPI_RESIDUAL = 3 };
 constexpr int kMaxEpi = 4;
 constexpr int kMaxBoxes = 4;
+// Epilogue transpose buffers: 4 warps x 32 rows x 36 floats (k_umma.cu).
+constexpr int kEpiSmemBytes = 4 * 32 * 36 * 4;
 
 struct EpiOp {
   int32_t kind = EPI_NONE;
@@ -72,6 +74,7 @@ struct UmmaPlan {
   int KC = 64;          // K elements per stage
   int pipe = 4;         // SMEM pipeline depth
   int persistent = 0;
+  int split_pref = 0;   // schedule `order`: 0 heuristic split-K, 1 never, 2 at least 2
   OperandView A, B;
   std::vector<TileEntry> tiles;
   std::vector<StageEntry> stages;
@@ -91,7 +94,7 @@ struct UmmaLaunch {
   void* d_stages = nullptr;
   void* d_rows = nullptr;
   void* d_cols = nullptr;
-  int ntiles = 0, nstages = 0, BN = 0, KC = 0, pipe = 0, tmem_cols = 0;
+  int ntiles = 0, nstages = 0, BN = 0, KC = 0, pipe = 0, tmem_cols = 0, nprod = 1;
   int a_boxes = 0, b_boxes = 0, a_slot = 0, b_slot = 0, a_bytes = 0, b_bytes = 0;
   uint64_t a_desc = 0, b_desc = 0;  // descriptor templates (start address filled on device)
   uint32_t a_kadv = 0, b_kadv = 0;
@@ -102,8 +105,10 @@ struct UmmaLaunch {
   float* out = nullptr;
   size_t smem = 0;
   int grid = 0;
-  int a_rank_ = 0, b_rank_ = 0;
-  int cols_unit = 0, rows_unit = 0, ring_bytes = 0;
+  int ring_bytes = 0;
+  int table_ints = 0;            // [stages | col_off | row_off] int32 count
+  int store_mode = 0;           // 1: transposed float4 row stores; 0: generic
+  int64_t col0 = 0;
   int splits = 1;               // split-K factor (k_umma.cu)
   float* ws = nullptr;          // split-K partial tiles
   int* counters = nullptr;      // split-K per-tile arrival counters

@@ -245,10 +245,10 @@ uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
 
 int pick_pipe(const UmmaPlan& p) {
   int per = p.A.slot_bytes * p.A.boxes + p.B.slot_bytes * p.B.boxes;
-  // 227 KB per CTA minus alignment slack, barriers, the tile entry, the
-  // stage table and the epilogue column table (k_umma.cu SMEM layout).
-  int fixed = 1024 + 256 + static_cast<int>(sizeof(TileEntry) + sizeof(StageEntry) * p.stages.size() +
-                                           8 * p.col_off.size() + 8 * 128);
+  // 227 KB per CTA minus alignment slack, the epilogue transpose buffers,
+  // barriers, the stage table and the row/column tables (k_umma.cu SMEM layout).
+  int fixed = 1024 + 256 + kEpiSmemBytes +
+              static_cast<int>(sizeof(StageEntry) * p.stages.size() + 8 * p.col_off.size() + 8 * 128);
   int budget = 227 * 1024 - fixed;
   int cap = 8;
   if (const char* e = getenv("LFGPU_MAX_PIPE")) cap = std::max(2, atoi(e));  // diagnostics
@@ -431,6 +431,7 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
        << (q.B.mn_major ? "MN" : "K") << "-major tiles=" << q.tiles.size() << " pipe=" << q.pipe;
     q.summary = os.str();
     q.persistent = s.parallel;
+    q.split_pref = s.order;
     *out = q;
     return true;
   }
@@ -703,6 +704,7 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
   for (int c = 0; c < BN; ++c) p.col_off.push_back(y_off(0, c, 0, 0) - base0);
   p.pipe = pick_pipe(p);
   p.persistent = s.parallel;
+  p.split_pref = s.order;
   std::ostringstream os;
   os << "conv h_t=" << h_t << " w_t=" << w_t << " o_t=" << o_t << " i_t=" << i_t << " i'=" << i2
      << " o'=" << o2 << " rows=" << h_sub * w_t << " BN=" << BN << " KC=" << KC
