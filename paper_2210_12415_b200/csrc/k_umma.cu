@@ -44,6 +44,13 @@ struct UmmaParams {
   uint32_t tmem_cols;       // >= 2*BN: two accumulators
   int32_t ring_bytes;       // SMEM pipeline ring
   int32_t table_ints;       // [stages | col_off | row_off] as one contiguous int array
+  int32_t ntaps, b_tap;     // halo C2D: tap t reads A at +a_tap[t], B at +t*b_tap
+  // Weights resident (halo C2D with one output-channel tile): every chunk's
+  // B slab is loaded once per CTA into SMEM at w_off (w_chunk bytes apart,
+  // barrier wfull[c]); the ring then carries A only.
+  int32_t wres, w_off, w_chunk, w_tx;
+  int32_t red_bytes;        // split-K: SMEM for the siblings' column slices
+  int32_t a_tap[kMaxTaps];
   int32_t store_mode;       // 1: row-contiguous, 16-byte aligned output rows; 0: generic
   int64_t col0;             // col_off[0] folded into the tile base in store mode 1
   unsigned long long* dbg;  // optional per-CTA %globaltimer checkpoints (8 per CTA)
@@ -166,6 +173,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
 constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiLd = 36;  // per-warp transpose buffer row stride (floats)
+constexpr int kMaxSplits = 4;
 static_assert(kEpiSmemBytes == 4 * 32 * kEpiLd * 4, "epilogue SMEM size");
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -215,7 +223,8 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
                                        int lane, int q, float* wbuf, int rows, int cols,
                                        int n_base, int64_t obase, const int64_t* s_row,
                                        const int64_t* s_col, int mode, int split, int splits,
-                                       int64_t ws_tile, bool release, uint32_t tempty) {
+                                       int64_t ws_tile, const float4* red, int red_lo,
+                                       bool release, uint32_t tempty) {
   float v[W];
   tmem_ld<W>(taddr + c0, v);
   if (release) {
@@ -232,30 +241,52 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
       __stcg(w + j * 128, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
     return;
   }
-  if (splits > 1) {  // last CTA of the tile: sum the partials in split order
-    float acc[W];
+  if (splits > 1) {
+    // Sum this chunk over the splits' partials in split order (this split's
+    // own from TMEM; the siblings' slices were bulk-copied into SMEM `red`,
+    // laid out [other split][col/4][row] float4).
+    const int slice4 = P.BN / splits / 4;
+    const float4* r0 = red + ((c0 - red_lo) / 4) * 128 + row;
+    float4 part[kMaxSplits - 1][W / 4];
 #pragma unroll
-    for (int j = 0; j < W; ++j) acc[j] = 0.0f;
-    const float4* w0 = reinterpret_cast<const float4*>(P.ws) + ws_tile * wstride + (c0 / 4) * 128 + row;
-#pragma unroll 1
-    for (int s = 0; s < splits; ++s) {
-      if (s == split) {
+    for (int o = 0; o < kMaxSplits - 1; ++o) {
+      if (o < splits - 1) {
 #pragma unroll
-        for (int j = 0; j < W; ++j) acc[j] += v[j];
-      } else {
-        const float4* w = w0 + s * wstride;
-#pragma unroll
-        for (int j = 0; j < W / 4; ++j) {
-          const float4 x = __ldcg(w + j * 128);
-          acc[4 * j] += x.x;
-          acc[4 * j + 1] += x.y;
-          acc[4 * j + 2] += x.z;
-          acc[4 * j + 3] += x.w;
-        }
+        for (int j = 0; j < W / 4; ++j) part[o][j] = r0[(o * slice4 + j) * 128];
       }
     }
 #pragma unroll
-    for (int j = 0; j < W; ++j) v[j] = acc[j];
+    for (int j = 0; j < W / 4; ++j) {
+      // Terms in split order: the other splits' partials in order, with
+      // this split's own values inserted at position `split`.
+      const float4 mine = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int o = 0; o < kMaxSplits - 1; ++o) {
+        if (o == split && split < splits - 1) {
+          acc.x += mine.x;
+          acc.y += mine.y;
+          acc.z += mine.z;
+          acc.w += mine.w;
+        }
+        if (o < splits - 1) {
+          acc.x += part[o][j].x;
+          acc.y += part[o][j].y;
+          acc.z += part[o][j].z;
+          acc.w += part[o][j].w;
+        }
+      }
+      if (split == splits - 1) {
+        acc.x += mine.x;
+        acc.y += mine.y;
+        acc.z += mine.z;
+        acc.w += mine.w;
+      }
+      v[4 * j] = acc.x;
+      v[4 * j + 1] = acc.y;
+      v[4 * j + 2] = acc.z;
+      v[4 * j + 3] = acc.w;
+    }
   }
   __syncwarp();
 #pragma unroll
@@ -279,7 +310,7 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
     for (int it = 0; it < IT; ++it) {
       const int rr = it * RPI + lane / LPR;
       const int r = q * 32 + rr;
-      ok[it] = r < rows && c < cols;
+      ok[it] = r < rows && c < cols && s_row[r] >= 0;
       x[it] = *reinterpret_cast<const float4*>(wbuf + rr * kEpiLd + cl);
       addr[it] = obase + s_row[r] + c;
     }
@@ -327,7 +358,7 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
     return;
   }
   // Generic: thread = row, 8 columns per step (loads, ops, stores batched).
-  if (row < rows) {
+  if (row < rows && s_row[row] >= 0) {
     const int64_t rb = obase + s_row[row];
     const float* mine = wbuf + lane * kEpiLd;
 #pragma unroll 1
@@ -364,17 +395,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-byte alignment (SWIZZLE_128B atoms) by offsetting the __shared__
   // array itself, so every derived pointer stays in the shared window.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int stage_bytes = P.a_boxes * P.a_slot + P.b_boxes * P.b_slot;
-  float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + kEpiSmemBytes);
+  const int stage_bytes = P.a_boxes * P.a_slot + (P.wres ? 0 : P.b_boxes * P.b_slot);
+  const int wbytes = P.wres ? P.nstages * P.w_chunk : 0;
+  float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes + wbytes);
+  const float4* s_red = reinterpret_cast<const float4*>(smem + P.ring_bytes + wbytes + kEpiSmemBytes);
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem + P.ring_bytes + wbytes + kEpiSmemBytes + P.red_bytes);
+  const int nw = P.wres ? P.nstages : 0;
   const int pipe = P.pipe;
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = full0 + 8 * pipe;
   const uint32_t tfull0 = empty0 + 8 * pipe;   // 2 accumulator-full barriers
   const uint32_t tempty0 = tfull0 + 16;        // 2 accumulator-empty barriers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * pipe + 4);
+  const uint32_t wfull0 = tempty0 + 16;        // nw resident-weight barriers
+  const uint32_t redbar = wfull0 + 8 * nw;     // split-K sibling slices landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * pipe + 5 + nw);
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
-  StageEntry* s_stage = reinterpret_cast<StageEntry*>(bars + 2 * pipe + 5);
+  StageEntry* s_stage = reinterpret_cast<StageEntry*>(bars + 2 * pipe + 6 + nw);
   int64_t* s_col = reinterpret_cast<int64_t*>(s_stage + P.nstages);
   int64_t* s_row = s_col + P.BN;
 
@@ -382,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int splits = P.splits;
   const int nunits = P.ntiles * splits;
   const int nst = P.nstages;
-  unsigned long long* dbg = P.dbg ? P.dbg + 8 * blockIdx.x : nullptr;
+  unsigned long long* dbg = P.dbg ? P.dbg + 24 * blockIdx.x : nullptr;
   if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
 
   if (threadIdx.x == 0) {
@@ -394,6 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tfull0 + 8 * b, 1);
       mbar_init(tempty0 + 8 * b, 4);  // one arrive per epilogue warp
     }
+    for (int c = 0; c < nw; ++c) mbar_init(wfull0 + 8 * c, 1);
+    mbar_init(redbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
@@ -443,6 +482,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t b_off = P.a_boxes * a_slot;
     const int na = P.a_boxes, nb = P.b_boxes;
     const bool leader = elect_one();
+    if (nw && prod == 0 && leader && blockIdx.x < nunits) {
+      // Resident weights: every chunk's slab once, on its own barrier.
+      const TileEntry* te = P.tiles + blockIdx.x / splits;
+      for (int c = 0; c < nw; ++c) {
+        const StageEntry se = s_stage[c];
+        const uint32_t bar = wfull0 + 8 * c;
+        mbar_expect_tx(bar, P.w_tx);
+        for (int b = 0; b < nb; ++b)
+          tma_load5(&tma_b, ring0 + P.w_off + c * P.w_chunk + b * b_slot, bar,
+                    __ldg(&te->cb[b][0]) + se.sb[0], __ldg(&te->cb[b][1]) + se.sb[1],
+                    __ldg(&te->cb[b][2]) + se.sb[2], __ldg(&te->cb[b][3]) + se.sb[3],
+                    __ldg(&te->cb[b][4]) + se.sb[4]);
+      }
+    }
+    const int nbs = nw ? 0 : nb;  // B boxes streamed per stage
     int g = 0;  // CTA-wide stage counter (ring slot / phase)
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       const int tile = u / splits, split = u - tile * splits;
@@ -475,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       ta[b][2] + se.sa[2], ta[b][3] + se.sa[3], ta[b][4] + se.sa[4]);
 #pragma unroll
         for (int b = 0; b < kMaxBoxes; ++b)
-          if (b < nb)
+          if (b < nbs)
             tma_load5(&tma_b, a_dst + b_off + b * b_slot, bar, tb[b][0] + se.sb[0],
                       tb[b][1] + se.sb[1], tb[b][2] + se.sb[2], tb[b][3] + se.sb[3],
                       tb[b][4] + se.sb[4]);
@@ -486,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---- MMA issuer (whole warp loops; one elected lane issues)
     const uint64_t adesc = P.a_desc, bdesc = P.b_desc;
-    const uint32_t idesc = P.idesc, akadv = P.a_kadv, bkadv = P.b_kadv;
+    const uint32_t idesc = P.idesc, akadv16 = P.a_kadv >> 4, bkadv16 = P.b_kadv >> 4;
     const int ksteps = P.ksteps;
     const uint32_t ring0 = smem_u32(smem);
     const uint32_t a_off_b = P.a_boxes * P.a_slot;
@@ -505,13 +559,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(full0 + 8 * slot, phase);
         if (dbg && leader && i == 0 && s == s_lo) dbg[3] = gtimer();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (nw) {
+          mbar_wait(wfull0 + 8 * s, 0);  // completes once; later waits return at once
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
         if (leader) {
           const uint32_t a_addr = ring0 + slot * stage_bytes;
-          const uint32_t b_addr = a_addr + a_off_b;
-          for (int k = 0; k < ksteps; ++k) {
-            const uint64_t ad = adesc | (((a_addr + k * akadv) >> 4) & 0x3FFFull);
-            const uint64_t bd = bdesc | (((b_addr + k * bkadv) >> 4) & 0x3FFFull);
-            umma_bf16(dtm, ad, bd, idesc, (s != s_lo) || (k != 0));
+          const uint32_t b_addr = nw ? ring0 + P.w_off + s * P.w_chunk : a_addr + a_off_b;
+          // Descriptors are (address >> 4) in their low 14 bits: advance
+          // them by 16-byte units directly (SMEM addresses < 256 KB never
+          // carry out of the field).
+          const uint64_t ad0 = adesc | (a_addr >> 4), bd0 = bdesc | (b_addr >> 4);
+          for (int t = 0; t < P.ntaps; ++t) {
+            const uint64_t adt = ad0 + (P.a_tap[t] >> 4), bdt = bd0 + ((t * P.b_tap) >> 4);
+            for (int k = 0; k < ksteps; ++k)
+              umma_bf16(dtm, adt + k * akadv16, bdt + k * bkadv16, idesc, (s != s_lo) | t | k);
           }
           umma_commit(empty0 + 8 * slot);
         }
@@ -531,6 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     float* wbuf = s_epi + q * 32 * kEpiLd;
     const int BN = P.BN;
+    uint32_t red_phase = 0;
     int i = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       const int tile = u / splits, split = u - tile * splits;
@@ -544,41 +607,73 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(tfull0 + 8 * b, static_cast<uint32_t>(i >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[5] = gtimer();
+      if (dbg && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[8 + i] = gtimer();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * BN);
       const int64_t ws_tile = static_cast<int64_t>(tile) * splits;
+      const int red_lo = split * (BN / splits);
+      const int mode = P.store_mode;
+      // Columns [a, b) in 32-wide chunks (16-wide tail); `rel` hands the
+      // accumulator back after the last TMEM read.
+      // One loop, one (inlined) chunk body: each SM runs the epilogue only a
+      // few times per launch, so code size is paid in cold instruction
+      // fetches. Items are 16-column chunks: first (split-K only) the
+      // columns the sibling splits reduce, published to the workspace; then
+      // this unit's own columns [lo, hi), summed over the splits in split
+      // order (own partial from TMEM) and stored with the fused chain.
+      //   Split-K: split s reduces columns [s*BN/S, (s+1)*BN/S). The
+      // siblings meet at a per-tile counter (they are co-resident: the grid
+      // is a multiple of S and units are dealt in rounds), then bulk-copy
+      // the siblings' slices of the reduced columns into SMEM.
+      const int sl = BN / splits, lo = split * sl, hi = lo + sl;
+      const int npub = (BN - sl) / 16, nitems = npub + sl / 16;
+      for (int it = 0; it < nitems; ++it) {
+        if (it == npub && splits > 1) {
+          if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[16] = gtimer();
+          __threadfence();
+          epi_bar();
+          if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[17] = gtimer();
+          if (threadIdx.x == kEpiWarp0 * 32) {
+            atomicAdd(P.counters + tile, 1);
+            int seen;
+            do {
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(P.counters + tile) : "memory");
+              if (seen < splits) __nanosleep(64);
+            } while (seen < splits);
+            // generic-proxy writes of the siblings -> async-proxy bulk copies
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const uint32_t slice_bytes = static_cast<uint32_t>(sl) * 128 * 4;
+            mbar_expect_tx(redbar, slice_bytes * (splits - 1));
+            for (int o = 0; o < splits - 1; ++o) {
+              const int sib = o < split ? o : o + 1;
+              const float* src = P.ws + ((ws_tile + sib) * (BN / 4) + lo / 4) * 128 * 4;
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      smem_u32(s_red) + o * slice_bytes),
+                  "l"(src), "r"(slice_bytes), "r"(redbar)
+                  : "memory");
+            }
+          }
+          if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[18] = gtimer();
+          mbar_wait(redbar, red_phase);
+          red_phase ^= 1;
+          if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[19] = gtimer();
+        }
+        const bool pub = it < npub;
+        const int c0 = pub ? (it * 16 < lo ? it * 16 : it * 16 + sl) : lo + (it - npub) * 16;
+        epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col,
+                      pub ? 3 : mode, split, splits, ws_tile, s_red, red_lo, it == nitems - 1, tempty);
+      }
       if (splits > 1) {
-        int c0 = 0;
-        for (; c0 + 32 <= BN; c0 += 32)
-          epi_chunk<32>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, 3,
-                        split, splits, ws_tile, false, tempty);
-        if (c0 < BN)
-          epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, 3,
-                        split, splits, ws_tile, false, tempty);
-        __threadfence();
         epi_bar();
         if (threadIdx.x == kEpiWarp0 * 32) {
-          const int prev = atomicAdd(P.counters + tile, 1);
-          *s_flag = prev == splits - 1;
-          if (prev == splits - 1) P.counters[tile] = 0;  // re-armed for the next launch
+          // Last one out re-arms both counters for the next launch.
+          if (atomicAdd(P.counters + P.ntiles + tile, 1) == splits - 1) {
+            P.counters[tile] = 0;
+            P.counters[P.ntiles + tile] = 0;
+          }
         }
-        epi_bar();
-        if (!*s_flag) {
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty);
-          continue;
-        }
-        __threadfence();
       }
-      const int mode = P.store_mode;
-      int c0 = 0;
-      const int full_end = BN & ~31;
-      for (; c0 < full_end; c0 += 32)
-        epi_chunk<32>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, mode,
-                      split, splits, ws_tile, c0 + 32 >= BN, tempty);
-      if (c0 < BN)
-        epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, mode,
-                      split, splits, ws_tile, true, tempty);
+      if (dbg && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[12 + i] = gtimer();
     }
     if (dbg && threadIdx.x == kEpiWarp0 * 32) dbg[6] = gtimer();
   }
@@ -633,7 +728,8 @@ CUtensorMap encode(const OperandView& v, const void* base) {
   }
   CUtensorMapSwizzle sw = v.swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                           : v.swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                            : CU_TENSOR_MAP_SWIZZLE_32B;
+                          : v.swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base),
                            dims, strides + 1, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -642,7 +738,7 @@ CUtensorMap encode(const OperandView& v, const void* base) {
 }
 
 uint64_t desc_bits(const OperandView& v) {
-  uint64_t layout = v.swizzle == 128 ? 2 : v.swizzle == 64 ? 4 : 6;
+  uint64_t layout = v.swizzle == 128 ? 2 : v.swizzle == 64 ? 4 : v.swizzle == 32 ? 6 : 0;
   uint64_t d = 0;
   d |= static_cast<uint64_t>((v.lbo >> 4) & 0x3FFF) << 16;
   d |= static_cast<uint64_t>((v.sbo >> 4) & 0x3FFF) << 32;
@@ -750,32 +846,6 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     L.epi_ptr[e] = p.epi[e].ptr;
   }
   L.out = p.out;
-  const size_t ring = static_cast<size_t>(p.pipe) * (L.a_boxes * L.a_slot + L.b_boxes * L.b_slot);
-  L.ring_bytes = static_cast<int>((ring + 1023) / 1024 * 1024);
-  L.smem = 1024 + L.ring_bytes + kEpiSmemBytes + 8 * (2 * p.pipe + 4) + 8 +
-           sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 64;
-  if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "tcgen05 kernel SMEM exceeds 227 KB");
-  L.nprod = std::max(1, std::min(3, p.pipe - 1));
-  // Store mode 1 (transposed, float4 row stores): output columns contiguous
-  // and every stored row 16-byte aligned.
-  int max_rows = 0;
-  for (const auto& te : p.tiles) max_rows = std::max(max_rows, static_cast<int>(te.rows));
-  bool cols_unit = !p.col_off.empty();
-  for (size_t c = 0; c < p.col_off.size(); ++c)
-    if (p.col_off[c] != p.col_off[0] + static_cast<int64_t>(c)) cols_unit = false;
-  bool aligned = cols_unit && (p.col_off[0] % 4 == 0);
-  for (int r = 0; aligned && r < max_rows && r < static_cast<int>(p.row_off.size()); ++r)
-    if (p.row_off[r] % 4) aligned = false;
-  for (const auto& te : p.tiles)
-    if (te.out_base % 4 || te.cols % 4) aligned = false;
-  L.store_mode = aligned ? 1 : 0;
-  L.col0 = aligned ? p.col_off[0] : 0;
-  if (const char* e = getenv("LFGPU_STORE_MODE")) {  // diagnostics: force the generic path
-    if (atoi(e) == 0) {
-      L.store_mode = 0;
-      L.col0 = 0;
-    }
-  }
   // Split-K (schedule `order`: 0 = heuristic, 1 = never, 2 = at least 2):
   // when the tiles alone leave most of the SMs idle and the K loop is long.
   const int sms = num_sms();
@@ -786,17 +856,66 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   }
   if (p.split_pref == 2) L.splits = std::max(L.splits, std::min(2, L.nstages));
   if (const char* e = getenv("LFGPU_SPLITK")) L.splits = std::max(1, std::min(atoi(e), L.nstages));
+  // Each split reduces a column slice: BN/S must be a multiple of 16, and
+  // all S splits of a tile must fit in one round of the persistent grid.
+  L.splits = std::min(L.splits, 4);  // kMaxSplits (k_umma.cu)
+  while (L.splits > 1 && ((L.BN % L.splits) || (L.BN / L.splits) % 16 || L.splits > sms))
+    --L.splits;
+  L.red_bytes = L.splits > 1 ? (L.splits - 1) * 128 * (p.BN / L.splits) * 4 : 0;
+  L.wres = p.wres;
+  L.w_chunk = L.b_boxes * L.b_slot;
+  L.w_tx = L.b_boxes * L.b_bytes;
+  const size_t wbytes = p.wres ? static_cast<size_t>(p.stages.size()) * L.w_chunk : 0;
+  // SMEM: ring | resident weights | epilogue buffers | split-K slices |
+  // barriers | tables. The ring gives up stages if the rest needs room.
+  for (;;) {
+    const size_t ring = static_cast<size_t>(L.pipe) *
+                        (L.a_boxes * L.a_slot + (p.wres ? 0 : L.b_boxes * L.b_slot));
+    L.ring_bytes = static_cast<int>((ring + 1023) / 1024 * 1024);
+    L.smem = 1024 + L.ring_bytes + wbytes + kEpiSmemBytes + L.red_bytes +
+             8 * (2 * L.pipe + 5 + (p.wres ? p.stages.size() : 0)) + 8 +
+             sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 64;
+    if (L.smem <= 227 * 1024 || L.pipe <= 2) break;
+    --L.pipe;
+  }
+  if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "tcgen05 kernel SMEM exceeds 227 KB");
+  L.nprod = std::max(1, std::min(3, L.pipe - 1));
+  L.ntaps = p.ntaps;
+  L.b_tap = p.b_tap;
+  if (p.ntaps > kMaxTaps || static_cast<int>(p.a_tap.size()) < p.ntaps)
+    fail(LFGPU_EINVAL, "umma: tap table");
+  for (int t = 0; t < p.ntaps; ++t) L.a_tap[t] = p.a_tap[t];
+  // Store mode 1 (transposed, float4 row stores): output columns contiguous
+  // and every stored row 16-byte aligned.
+  int max_rows = 0;
+  for (const auto& te : p.tiles) max_rows = std::max(max_rows, static_cast<int>(te.rows));
+  bool cols_unit = !p.col_off.empty();
+  for (size_t c = 0; c < p.col_off.size(); ++c)
+    if (p.col_off[c] != p.col_off[0] + static_cast<int64_t>(c)) cols_unit = false;
+  bool aligned = cols_unit && (p.col_off[0] % 4 == 0);
+  for (int r = 0; aligned && r < max_rows && r < static_cast<int>(p.row_off.size()); ++r)
+    if (p.row_off[r] >= 0 && p.row_off[r] % 4) aligned = false;
+  for (const auto& te : p.tiles)
+    if (te.out_base % 4 || te.cols % 4) aligned = false;
+  L.store_mode = aligned ? 1 : 0;
+  L.col0 = aligned ? p.col_off[0] : 0;
+  if (const char* e = getenv("LFGPU_STORE_MODE")) {  // diagnostics: force the generic path
+    if (atoi(e) == 0) {
+      L.store_mode = 0;
+      L.col0 = 0;
+    }
+  }
   if (L.splits > 1) {
     const size_t ws = sizeof(float) * static_cast<size_t>(L.ntiles) * L.splits * 128 * L.BN;
     if (cudaMalloc(&t->p[4], ws) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc split-K workspace");
-    if (cudaMalloc(&t->p[5], sizeof(int) * L.ntiles) != cudaSuccess ||
-        cudaMemset(t->p[5], 0, sizeof(int) * L.ntiles) != cudaSuccess)
+    if (cudaMalloc(&t->p[5], 2 * sizeof(int) * L.ntiles) != cudaSuccess ||
+        cudaMemset(t->p[5], 0, 2 * sizeof(int) * L.ntiles) != cudaSuccess)
       fail(LFGPU_ECUDA, "cudaMalloc split-K counters");
     L.ws = static_cast<float*>(t->p[4]);
     L.counters = static_cast<int*>(t->p[5]);
   }
   // Persistent grid: one CTA per SM at most, units dealt round-robin.
-  L.grid = std::min(L.ntiles * L.splits, sms);
+  L.grid = std::min(L.ntiles * L.splits, sms / L.splits * L.splits);
   static_assert(sizeof(TileEntry) == 192, "TileEntry layout");
   return L;
 }
@@ -825,7 +944,12 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.b_boxes = L.b_boxes;
   P.a_slot = L.a_slot;
   P.b_slot = L.b_slot;
-  P.tx_bytes = L.a_boxes * L.a_bytes + L.b_boxes * L.b_bytes;
+  P.tx_bytes = L.a_boxes * L.a_bytes + (L.wres ? 0 : L.b_boxes * L.b_bytes);
+  P.wres = L.wres;
+  P.w_off = L.ring_bytes;
+  P.w_chunk = L.w_chunk;
+  P.w_tx = L.w_tx;
+  P.red_bytes = L.red_bytes;
   P.a_desc = L.a_desc;
   P.b_desc = L.b_desc;
   P.a_kadv = L.a_kadv;
@@ -834,6 +958,9 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.tmem_cols = L.tmem_cols;
   P.ring_bytes = L.ring_bytes;
   P.table_ints = L.table_ints;
+  P.ntaps = L.ntaps;
+  P.b_tap = L.b_tap;
+  for (int t = 0; t < kMaxTaps; ++t) P.a_tap[t] = L.a_tap[t];
   P.store_mode = L.store_mode;
   P.col0 = L.col0;
   P.splits = L.splits;

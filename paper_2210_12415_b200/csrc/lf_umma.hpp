@@ -28,6 +28,7 @@ enum { UMMA_GEMM = 0, UMMA_CONV = 1 };
 enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_RELU = 2, EPI_RESIDUAL = 3 };
 constexpr int kMaxEpi = 4;
 constexpr int kMaxBoxes = 4;
+constexpr int kMaxTaps = 32;  // taps of the halo C2D path (KH*KW)
 // Epilogue transpose buffers: 4 warps x 32 rows x 36 floats (k_umma.cu).
 constexpr int kEpiSmemBytes = 4 * 32 * 36 * 4;
 
@@ -75,6 +76,12 @@ struct UmmaPlan {
   int pipe = 4;         // SMEM pipeline depth
   int persistent = 0;
   int split_pref = 0;   // schedule `order`: 0 heuristic split-K, 1 never, 2 at least 2
+  // Halo C2D: per K stage, `ntaps` UMMA groups; tap t reads A at +a_tap[t]
+  // bytes and B at +t*b_tap bytes inside the stage (ntaps = 1: plain GEMM).
+  int ntaps = 1;
+  std::vector<int32_t> a_tap{0};
+  int b_tap = 0;
+  int wres = 0;          // halo C2D: weights resident in SMEM (one output-channel tile)
   OperandView A, B;
   std::vector<TileEntry> tiles;
   std::vector<StageEntry> stages;
@@ -107,6 +114,10 @@ struct UmmaLaunch {
   int grid = 0;
   int ring_bytes = 0;
   int table_ints = 0;            // [stages | col_off | row_off] int32 count
+  int ntaps = 1, b_tap = 0;
+  int wres = 0, w_chunk = 0, w_tx = 0;
+  int red_bytes = 0;
+  int32_t a_tap[kMaxTaps] = {};
   int store_mode = 0;           // 1: transposed float4 row stores; 0: generic
   int64_t col0 = 0;
   int splits = 1;               // split-K factor (k_umma.cu)

@@ -443,6 +443,334 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
 // C2D: y[b,o,h,w] = sum_{i,rh,rw} x[b,i,V*h+rh,V*w+rw] * ker[o,i,rh,rw]
 // (interp.cpp:70-89) as an implicit GEMM over the template layouts.
 
+// C2D with the overlapped input tile reused across taps ("halo" path).
+//
+// The template input brick xp[n][h0][w0][i0][B_h][B_w][i_t] already holds
+// every pixel one output tile reads (B = (t-1)V + K, space.cpp:279-280). It
+// is loaded ONCE per channel chunk (one TMA box, SWIZZLE_NONE, channel groups
+// of 8 outermost: SMEM [group][pixel][8 ch]), and each tap (rh, rw) is a UMMA
+// A operand starting rh*B_w + rw pixels into it: UMMA rows are pixels
+// y*B_w + x of the tile computed on the B_w-wide grid (columns x >= w_t are
+// discarded by the epilogue). The weights of the chunk for all KH*KW taps are
+// one TMA box ([KH][KW][i'][o'] is contiguous in the template weight brick).
+// Compared with one shifted input box per tap this cuts the input's L2->SMEM
+// traffic by ~KH*KW.
+static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDigit>& xd,
+                           const std::vector<Dim>& k_log, const std::vector<PDigit>& kd,
+                           const std::vector<Dim>& y_log, const std::vector<PDigit>& yd,
+                           int64_t V, const lfgpu_sched& s, UmmaPlan* out, std::string* why) {
+  const int64_t N = y_log[0].extent, O = y_log[1].extent, Ho = y_log[2].extent,
+                Wo = y_log[3].extent, I = x_log[1].extent, KH = k_log[2].extent,
+                KW = k_log[3].extent;
+  if (V != 1 || KH * KW < 2 || KH * KW > kMaxTaps) {
+    *why = "halo path: stride 1, 2..32 taps";
+    return false;
+  }
+  auto yh = digits_of(yd, 2), yw = digits_of(yd, 3), yo = digits_of(yd, 1);
+  if (yh.size() > 2 || yw.size() > 2 || yo.size() > 2 || digits_of(yd, 0).size() != 1) {
+    *why = "halo path: output is not a one-level template layout";
+    return false;
+  }
+  const int64_t h_t = yh[0]->ext, w_t = yw[0]->ext, o_t = yo[0]->ext;
+  // Input: N, H0, W0, I0, Hoff, Woff, i_t (H/W either unfolded with S = t,
+  // B = t + K - 1, or whole with extent = out + K - 1).
+  struct Ax {
+    int tile = -1, off = -1;
+  } ah, aw;
+  int an = -1, ai0 = -1, ai1 = -1;
+  for (size_t k = 0; k < xd.size(); ++k) {
+    const PDigit& d = xd[k];
+    if (d.lj == 0) an = static_cast<int>(k);
+    else if (d.lj == 1) (d.div == 1 ? ai1 : ai0) = static_cast<int>(k);
+    else {
+      Ax& a = d.lj == 2 ? ah : aw;
+      if (d.kind == DG_TILE) a.tile = static_cast<int>(k);
+      else a.off = static_cast<int>(k);  // DG_OFF, or the whole dim (DG_PART)
+    }
+  }
+  const int nk = static_cast<int>(xd.size());
+  if (ai1 != nk - 1 || ah.off < 0 || aw.off < 0 || xd[ai1].ext % 16 ||
+      !(ah.off < aw.off && aw.off == nk - 2 && ah.off == nk - 3)) {
+    *why = "halo path: input brick must end [H off][W off][i_t]";
+    return false;
+  }
+  const int64_t i_t = xd[ai1].ext;
+  const int64_t B_h = xd[ah.off].ext, B_w = xd[aw.off].ext;
+  auto fits = [&](const Ax& a, int64_t t, int64_t out_ext, int64_t K, int64_t Bx) {
+    const PDigit& o = xd[a.off];
+    if (a.tile >= 0) return xd[a.tile].kind == DG_TILE && o.kind == DG_OFF && o.S == t && Bx == t + K - 1;
+    return o.kind == DG_PART && o.div == 1 && t == out_ext && Bx == out_ext + K - 1;
+  };
+  if (!fits(ah, h_t, Ho, KH, B_h) || !fits(aw, w_t, Wo, KW, B_w)) {
+    *why = "halo path: input tiles do not match the output tile";
+    return false;
+  }
+  for (int k : {ah.tile, aw.tile, an, ai0})
+    if (k >= 0 && k >= ah.off) {
+      *why = "halo path: tile digits must be outside the brick";
+      return false;
+    }
+  if (B_w > 128) {
+    *why = "halo path: B_w > 128";
+    return false;
+  }
+  const int64_t h_sub = std::min<int64_t>(h_t, 128 / B_w);
+  const int64_t rows_h = h_sub + KH - 1;
+  // Weight: [..][KH][KW][i'][o'] (o' innermost: MN-major B) or, when the
+  // template leaves O whole (o' == O), [O][I0][KH][KW][i'] (K-major B).
+  if (kd.size() < 3) return false;
+  const bool b_kmajor = kd.back().lj == 1;
+  const size_t kbase = b_kmajor ? kd.size() - 3 : kd.size() - 4;  // index of the KH digit
+  if (kd.size() < (b_kmajor ? 3u : 4u)) return false;
+  const PDigit& kh_ = kd[kbase];
+  const PDigit& kw_ = kd[kbase + 1];
+  const PDigit& ki = kd[kbase + 2];
+  if (kh_.lj != 2 || kw_.lj != 3 || kh_.ext != KH || kw_.ext != KW || ki.lj != 1 || ki.div != 1 ||
+      ki.ext % 16) {
+    *why = "halo path: weight brick must end [KH][KW][i'] or [KH][KW][i'][o']";
+    return false;
+  }
+  int ko_outer = -1, ki_outer = -1;  // K-major: the whole-O digit and the I0 digit
+  for (size_t k = 0; k < kbase; ++k) {
+    if (kd[k].lj == 0) {
+      if (ko_outer >= 0) return false;
+      ko_outer = static_cast<int>(k);
+    } else if (kd[k].lj == 1) {
+      if (ki_outer >= 0) return false;
+      ki_outer = static_cast<int>(k);
+    } else {
+      return false;
+    }
+  }
+  if (!b_kmajor) {
+    const PDigit& ko = kd.back();
+    if (ko.lj != 0 || ko.div != 1 || ko.ext % 16) {
+      *why = "halo path: weight o' brick";
+      return false;
+    }
+  } else if (ko_outer < 0 || kd[ko_outer].div != 1 || kd[ko_outer].ext != O) {
+    *why = "halo path: K-major weight needs O whole";
+    return false;
+  }
+  const int64_t o2 = b_kmajor ? O : kd.back().ext, i2 = ki.ext;
+  int64_t KC = std::gcd(i_t, i2);
+  KC = std::min<int64_t>(KC, 64);
+  while (KC > 16 && (KC & (KC - 1))) KC /= 2;
+  if (KC % 16) {
+    *why = "halo path: channel chunk";
+    return false;
+  }
+  int64_t BN = std::min<int64_t>({o_t, o2, 256});
+  if (s.tile_last >= 16 && s.tile_last < BN && BN % s.tile_last == 0 && s.tile_last % 16 == 0)
+    BN = s.tile_last;
+  if (o_t % BN || o2 % BN || BN % 16 || (!b_kmajor && BN > 64 && BN % 64)) {
+    *why = "halo path: channel tile";
+    return false;
+  }
+  const int64_t nbw = b_kmajor ? BN : std::min<int64_t>(BN, 64);  // o per weight box
+  const int64_t taps = KH * KW;
+
+  UmmaPlan p;
+  p.kind = UMMA_CONV;
+  p.BM = 128;
+  p.BN = static_cast<int>(BN);
+  p.KC = static_cast<int>(KC);
+  // --- A: {i_t, B_w, B_h, bricks} box {KC, B_w, rows_h, 1}: SMEM rows are
+  // pixels of KC*2 bytes in the K-major swizzled canonical layout (swizzle =
+  // row bytes), so a tap is a start-address shift of (rh*B_w + rw) rows.
+  const int64_t brick = B_h * B_w * i_t;
+  int64_t nbricks = 1;
+  for (int k = 0; k < ah.off; ++k) nbricks *= xd[k].ext;
+  p.A.rank = 4;
+  p.A.dims[0] = i_t;
+  p.A.dims[1] = B_w;
+  p.A.dims[2] = B_h;
+  p.A.dims[3] = nbricks;
+  p.A.strides[0] = 2;
+  p.A.strides[1] = i_t * 2;
+  p.A.strides[2] = B_w * i_t * 2;
+  p.A.strides[3] = brick * 2;
+  p.A.box[0] = static_cast<uint32_t>(KC);
+  p.A.box[1] = static_cast<uint32_t>(B_w);
+  p.A.box[2] = static_cast<uint32_t>(rows_h);
+  p.A.box[3] = 1;
+  if (rows_h > 256 || B_w > 256) {
+    *why = "halo path: box too large";
+    return false;
+  }
+  p.A.swizzle = static_cast<int32_t>(KC * 2);
+  p.A.mn_major = 0;
+  p.A.boxes = 1;
+  const int64_t npix = rows_h * B_w;
+  const int64_t tapmax = (KH - 1) * B_w + (KW - 1);
+  p.A.box_bytes = static_cast<int32_t>(npix * KC * 2);
+  const int64_t a_need = std::max(npix, tapmax + 128) * KC * 2;
+  p.A.slot_bytes = static_cast<int32_t>((a_need + 1023) / 1024 * 1024);
+  p.A.sbo = static_cast<uint32_t>(8 * p.A.swizzle);
+  p.A.lbo = 16;
+  p.A.k_adv = 32;
+  // --- B
+  int64_t wbr = 1;
+  for (size_t k = 0; k < kbase; ++k) wbr *= kd[k].ext;
+  p.B.rank = 5;
+  if (!b_kmajor) {
+    // {o', i', KW, KH, outer bricks} box {nbw, KC, KW, KH, 1}: per tap a
+    // [KC][nbw] MN-major tile.
+    p.B.dims[0] = o2;
+    p.B.dims[1] = i2;
+    p.B.dims[2] = KW;
+    p.B.dims[3] = KH;
+    p.B.dims[4] = wbr;
+    p.B.strides[1] = o2 * 2;
+    p.B.strides[2] = i2 * o2 * 2;
+    p.B.strides[3] = KW * i2 * o2 * 2;
+    p.B.strides[4] = KH * KW * i2 * o2 * 2;
+    p.B.box[0] = static_cast<uint32_t>(nbw);
+    p.B.box[1] = static_cast<uint32_t>(KC);
+    p.B.swizzle = static_cast<int32_t>(nbw * 2);
+    p.B.mn_major = 1;
+  } else {
+    // {i', O, KW, KH, I0} box {KC, BN, KW, KH, 1}: per tap a [BN][KC] K-major
+    // tile (the view permutes the O digit inside the taps).
+    const int64_t ostride = kd[ko_outer].stride, istride = ki_outer >= 0 ? kd[ki_outer].stride : 0;
+    p.B.dims[0] = i2;
+    p.B.dims[1] = O;
+    p.B.dims[2] = KW;
+    p.B.dims[3] = KH;
+    p.B.dims[4] = ki_outer >= 0 ? kd[ki_outer].ext : 1;
+    p.B.strides[1] = ostride * 2;
+    p.B.strides[2] = kw_.stride * 2;
+    p.B.strides[3] = kh_.stride * 2;
+    p.B.strides[4] = (ki_outer >= 0 ? istride : KH * KW * i2) * 2;
+    p.B.box[0] = static_cast<uint32_t>(KC);
+    p.B.box[1] = static_cast<uint32_t>(BN);
+    p.B.swizzle = static_cast<int32_t>(KC * 2);
+    p.B.mn_major = 0;
+  }
+  p.B.strides[0] = 2;
+  p.B.box[2] = static_cast<uint32_t>(KW);
+  p.B.box[3] = static_cast<uint32_t>(KH);
+  p.B.box[4] = 1;
+  for (int d = 1; d < 5; ++d)
+    if (p.B.strides[d] % 16) {
+      *why = "halo path: weight stride not 16-byte aligned";
+      return false;
+    }
+  p.B.boxes = static_cast<int32_t>(BN / nbw);
+  if (p.B.boxes > kMaxBoxes) {
+    *why = "halo path: too many weight boxes";
+    return false;
+  }
+  p.B.box_bytes = static_cast<int32_t>(nbw * KC * taps * 2);
+  p.B.slot_bytes = (p.B.box_bytes + 1023) / 1024 * 1024;
+  p.B.sbo = static_cast<uint32_t>(8 * p.B.swizzle);
+  p.B.lbo = b_kmajor ? 16u : static_cast<uint32_t>(p.B.slot_bytes);
+  p.B.k_adv = b_kmajor ? 32u : static_cast<uint32_t>(16 * p.B.swizzle);
+  p.ntaps = static_cast<int>(taps);
+  p.b_tap = static_cast<int>(KC * nbw * 2);
+  p.a_tap.clear();
+  for (int64_t rh = 0; rh < KH; ++rh)
+    for (int64_t rw = 0; rw < KW; ++rw) p.a_tap.push_back(static_cast<int32_t>((rh * B_w + rw) * KC * 2));
+  // brick index of (n, h0, w0, i0): row-major over the digits outside the brick
+  auto brick_of = [&](int64_t n, int64_t h0, int64_t w0, int64_t i0) {
+    int64_t b = 0;
+    for (int k = 0; k < ah.off; ++k) {
+      const PDigit& d = xd[k];
+      int64_t v = 0;
+      if (k == an) v = n;
+      else if (k == ai0) v = i0;
+      else if (k == ah.tile) v = h0;
+      else if (k == aw.tile) v = w0;
+      b = b * d.ext + v;
+    }
+    return b;
+  };
+  auto wbrick_of = [&](int64_t o, int64_t i) {  // o, i logical; digits outside [KH][KW][i'][o']
+    int64_t b = 0;
+    for (size_t k = 0; k < kbase; ++k) b = b * kd[k].ext + digit_of(kd[k], kd[k].lj == 0 ? o : i);
+    return b;
+  };
+  auto y_off = [&](int64_t n, int64_t o, int64_t h, int64_t w) {
+    int64_t lv[4] = {n, o, h, w};
+    return offset_of(yd, lv);
+  };
+  const int64_t H0 = Ho / h_t, W0 = Wo / w_t, O0 = O / o_t;
+  const int64_t hchunks = (h_t + h_sub - 1) / h_sub, ochunks = o_t / BN;
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t h0 = 0; h0 < H0; ++h0)
+      for (int64_t w0 = 0; w0 < W0; ++w0)
+        for (int64_t hc = 0; hc < hchunks; ++hc)
+          for (int64_t o0 = 0; o0 < O0; ++o0)
+            for (int64_t oc = 0; oc < ochunks; ++oc) {
+              TileEntry te;
+              std::memset(&te, 0, sizeof(te));
+              const int64_t h1s = hc * h_sub;
+              te.ca[0][2] = static_cast<int32_t>(h1s);
+              te.ca[0][3] = static_cast<int32_t>(brick_of(n, h0, w0, 0));
+              const int64_t obase = o0 * o_t + oc * BN;
+              for (int b = 0; b < p.B.boxes; ++b) {
+                const int64_t o = obase + b * nbw;
+                if (b_kmajor) {
+                  te.cb[b][1] = static_cast<int32_t>(o);
+                } else {
+                  te.cb[b][0] = static_cast<int32_t>(o % o2);
+                  te.cb[b][4] = static_cast<int32_t>(wbrick_of(o, 0));
+                }
+              }
+              te.out_base = y_off(n, obase, h0 * h_t + h1s, w0 * w_t);
+              te.rows = static_cast<int32_t>(std::min<int64_t>(h_sub, h_t - h1s) * B_w);
+              te.cols = static_cast<int32_t>(BN);
+              te.n_base = static_cast<int32_t>(obase);
+              p.tiles.push_back(te);
+            }
+  for (int64_t c0 = 0; c0 < I; c0 += KC) {
+    StageEntry se;
+    std::memset(&se, 0, sizeof(se));
+    se.sa[0] = static_cast<int32_t>(c0 % i_t);
+    se.sa[3] = static_cast<int32_t>(brick_of(0, 0, 0, c0 / i_t) - brick_of(0, 0, 0, 0));
+    if (b_kmajor) {
+      se.sb[0] = static_cast<int32_t>(c0 % i2);
+      se.sb[4] = static_cast<int32_t>(c0 / i2);
+    } else {
+      se.sb[1] = static_cast<int32_t>(c0 % i2);
+      se.sb[4] = static_cast<int32_t>(wbrick_of(0, c0) - wbrick_of(0, 0));
+    }
+    p.stages.push_back(se);
+  }
+  // Rows: UMMA row r = pixel (r / B_w, r % B_w) of the B_w-wide grid; columns
+  // x >= w_t are not outputs (-1).
+  const int64_t base0 = y_off(0, 0, 0, 0);
+  for (int r = 0; r < 128; ++r) {
+    const int64_t hh = r / B_w, ww = r % B_w;
+    p.row_off.push_back(hh < h_sub && ww < w_t ? y_off(0, 0, hh, ww) - base0 : -1);
+  }
+  for (int c = 0; c < BN; ++c) p.col_off.push_back(y_off(0, c, 0, 0) - base0);
+  p.pipe = pick_pipe(p);
+  {
+    // Weights resident when the layer has one output-channel tile and all
+    // its chunks' slabs fit beside a >= 3-deep input ring.
+    const int64_t wbytes = static_cast<int64_t>(p.stages.size()) * p.B.boxes * p.B.slot_bytes;
+    const int64_t fixed = 1024 + 512 + kEpiSmemBytes + 8 * static_cast<int64_t>(p.stages.size()) * 6 +
+                          static_cast<int64_t>(sizeof(StageEntry) * p.stages.size() + 8 * p.col_off.size() + 8 * 128);
+    const int64_t budget = 227 * 1024 - fixed - wbytes;
+    const char* e = getenv("LFGPU_NO_WRES");
+    if (O0 * ochunks == 1 && !(e && atoi(e)) && budget >= 3 * p.A.slot_bytes) {
+      p.wres = 1;
+      p.pipe = static_cast<int>(std::min<int64_t>(8, budget / p.A.slot_bytes));
+    }
+  }
+  p.persistent = s.parallel;
+  p.split_pref = s.order;
+  std::ostringstream os;
+  os << (p.wres ? "conv-halo-wres" : "conv-halo") << " h_t=" << h_t << " w_t=" << w_t << " o_t=" << o_t << " i_t=" << i_t << " i'=" << i2
+     << " o'=" << o2 << " rows=" << h_sub << "x" << B_w << " BN=" << BN << " KC=" << KC
+     << " taps=" << taps << " tiles=" << p.tiles.size() << " stages=" << p.stages.size()
+     << " pipe=" << p.pipe;
+  p.summary = os.str();
+  *out = p;
+  return true;
+}
+
 bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::vector<Dim>& k_log,
                     const Seq& k_seq, const std::vector<Dim>& y_log, const Seq& y_seq,
                     int64_t V, const lfgpu_sched& s, UmmaPlan* out, std::string* why) {
@@ -453,6 +781,15 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
   if (!analyze(x_log, x_seq, &xd) || !analyze(k_log, k_seq, &kd) || !analyze(y_log, y_seq, &yd)) {
     *why = "layouts are not template brick layouts";
     return false;
+  }
+  std::string halo_why;
+  {
+    const char* e = getenv("LFGPU_NO_HALO");
+    std::string hwhy;
+    if (!(e && atoi(e)) && s.unroll == 0 &&
+        plan_conv_halo(x_log, xd, k_log, kd, y_log, yd, V, s, out, &hwhy))
+      return true;
+    halo_why = hwhy.empty() ? "off" : hwhy;
   }
   if (V > 8) {
     *why = "stride > 8 exceeds TMA traversal stride";
@@ -708,7 +1045,8 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
   std::ostringstream os;
   os << "conv h_t=" << h_t << " w_t=" << w_t << " o_t=" << o_t << " i_t=" << i_t << " i'=" << i2
      << " o'=" << o2 << " rows=" << h_sub * w_t << " BN=" << BN << " KC=" << KC
-     << " tiles=" << p.tiles.size() << " stages=" << p.stages.size() << " pipe=" << p.pipe;
+     << " tiles=" << p.tiles.size() << " stages=" << p.stages.size() << " pipe=" << p.pipe
+     << " (halo: " << halo_why << ")";
   p.summary = os.str();
   *out = p;
   return true;

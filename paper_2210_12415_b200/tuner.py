@@ -122,9 +122,11 @@ def gemm_candidates(M, K, N, node=0):
                 for tl in (64, 128, 256):
                     if tl > nt and nt != N:
                         continue
-                    out.append(Candidate({node: (mt, kt, nt)},
-                                         [runtime.sched(node, tile_last=tl)],
-                                         f"m_t={mt} k_t={kt} n_t={nt} tile={tl}"))
+                    # order: 0 = split-K by heuristic, 1 = no split (lfgpu_sched docs)
+                    for order in (0, 1):
+                        out.append(Candidate({node: (mt, kt, nt)},
+                                             [runtime.sched(node, tile_last=tl, order=order)],
+                                             f"m_t={mt} k_t={kt} n_t={nt} tile={tl} order={order}"))
     return out
 
 

@@ -18,9 +18,9 @@ def k64(shape):
     return torch.randint(-64, 65, shape, device="cuda").float() / 64
 
 
-def gemm(reps=3, factors=(128, 64, 1024), tile=64):
+def gemm(reps=3, factors=(128, 64, 1024), tile=64, order=0):
     g = ir.gemm(1024, 1024, 1024)
-    c = tuner.Candidate({0: factors}, [runtime.sched(0, tile_last=tile)])
+    c = tuner.Candidate({0: factors}, [runtime.sched(0, tile_last=tile, order=order)])
     p = runtime.Plan(g, tuner.seqs_for(g, c), c.scheds, _abi.PLAN_REQUIRE_TC)
     p.set_input_device("a", k64((1024, 1024)))
     p.set_input_device("b", k64((1024, 1024)))
@@ -51,7 +51,16 @@ def transform(reps=3, n=64):
     torch.cuda.synchronize()
 
 
+def gemm_split(reps=3):
+    gemm(reps, (128, 64, 256), 128, 0)
+
+
+def conv_halo(reps=3, nb=16, factors=(7, 14, 32, 32, 32, 32)):
+    conv(reps, nb, factors)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["gemm", "conv", "transform"]
     for w in which:
         globals()[w]()
+

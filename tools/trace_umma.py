@@ -23,7 +23,7 @@ def timeline(g, cand, inputs, name):
         p.set_input_device(k, v)
     p.run()
     torch.cuda.synchronize()
-    buf = torch.zeros(80 * 4096, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(24 * 4096, dtype=torch.int64, device="cuda")
     runtime.lib().lfgpu_debug_umma_trace(C.c_void_p(buf.data_ptr()))
     p2 = runtime.Plan(g, tuner.seqs_for(g, cand), cand.scheds, _abi.PLAN_REQUIRE_TC)
     for k, v in inputs.items():
@@ -38,8 +38,17 @@ def timeline(g, cand, inputs, name):
     torch.cuda.synchronize()
     runtime.lib().lfgpu_debug_umma_trace(None)
     allb = buf.cpu().numpy().astype(np.int64)
-    nct = int((allb.reshape(-1, 8)[:, 0] != 0).sum())
-    t = allb[: 8 * nct].reshape(-1, 8)
+    nct = int((allb.reshape(-1, 24)[:, 0] != 0).sum())
+    t16 = allb[: 24 * nct].reshape(-1, 24)
+    if (t16[:, 16] > 0).all():
+        sp = (t16[:, 16:20] - t16[:, :1]) / 1000.0
+        print("  split-K: published %.2f fenced %.2f spin-done %.2f slices-landed %.2f us" %
+              tuple(np.median(sp, axis=0)))
+    t = t16[:, :8]
+    ep = (t16[:, 8:16] - t16[:, :1]) / 1000.0
+    for k in range(4):
+        if (t16[:, 8 + k] > 0).all():
+            print(f"  unit {k}: epi start med {np.median(ep[:, k]):.2f} end {np.median(ep[:, 4 + k]):.2f} us")
     # untraced kernel time (events, back-to-back launches of the same plan)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for _ in range(3):
@@ -54,6 +63,7 @@ def timeline(g, cand, inputs, name):
     t0 = t[:, 0].min()
     rel = (t - t0) / 1000.0
     labels = ["entry", "setup", "tma_done", "first_full", "mma_done", "acc_ready", "epi_done"]
+    print(p2.node_kernel(len(g.nodes) - 1))
     print(f"== {name}: {len(t)} CTAs, kernel span {rel[:, 6].max():.2f} us")
     for i, l in enumerate(labels):
         print(f"  {l:10s} min {rel[:, i].min():7.2f}  med {np.median(rel[:, i]):7.2f}  max {rel[:, i].max():7.2f}")
@@ -118,9 +128,12 @@ if __name__ == "__main__":
         sys.exit(0)
     g = ir.gemm(1024, 1024, 1024)
     A, B = k64((1024, 1024)), k64((1024, 1024))
-    for f, tl in [((256, 1024, 256), 64), ((128, 64, 1024), 64), ((128, 64, 128), 128)]:
-        timeline(g, tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tl)]), {"a": A, "b": B},
-                 f"gemm {f} tile {tl}")
+    for f, tl, o in [((256, 1024, 256), 64, 1), ((128, 64, 256), 128, 0), ((128, 64, 256), 256, 0)]:
+        timeline(g, tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tl, order=o)]), {"a": A, "b": B},
+                 f"gemm {f} tile {tl} order {o}")
+    if os.environ.get("TRACE_GEMM_ONLY"):
+        sys.exit(0)
     gc = ir.pad_conv(16, 64, 64, 56, 3, 1, 1)
-    timeline(gc, tuner.Candidate({1: (56, 56, 64, 16, 16, 64)}, [runtime.sched(1)]),
-             {"x": k64((16, 64, 56, 56)), "ker": k64((64, 64, 3, 3))}, "conv b16")
+    for f in [(8, 14, 64, 32, 32, 64), (7, 14, 32, 32, 32, 32)]:
+        timeline(gc, tuner.Candidate({1: f}, [runtime.sched(1)]),
+                 {"x": k64((16, 64, 56, 56)), "ker": k64((64, 64, 3, 3))}, f"conv b16 {f}")

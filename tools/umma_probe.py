@@ -47,8 +47,9 @@ if __name__ == "__main__":
         us, cold, summ = probe(g, c, {"a": A, "b": B})
         print(f"gemm {f} tile={tl} order={order}: b2b {us:7.2f} us  cold {cold:7.2f} us  "
               f"{2 * 1024**3 / us / 1e6:7.1f} TFLOP/s  [{summ}]")
-    for nb, f in [(1, (7, 14, 16, 32, 32, 16)), (16, (7, 14, 32, 32, 32, 32)),
-                  (16, (8, 8, 64, 32, 32, 64)), (16, (4, 28, 64, 32, 32, 64))]:
+    for nb, f in [(1, (7, 14, 16, 32, 32, 16)), (1, (4, 14, 64, 32, 32, 64)), (1, (8, 14, 64, 32, 32, 64)),
+                  (16, (7, 14, 32, 32, 32, 32)), (16, (8, 14, 64, 32, 32, 64)), (16, (8, 28, 64, 32, 32, 64)),
+                  (16, (4, 28, 64, 32, 32, 64))]:
         gc = ir.pad_conv(nb, 64, 64, 56, 3, 1, 1)
         c = tuner.Candidate({1: f}, [runtime.sched(1)])
         fl = 2.0 * nb * 64 * 64 * 56 * 56 * 9
