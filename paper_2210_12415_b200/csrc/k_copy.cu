@@ -22,6 +22,7 @@
 
 #include "lf_core.hpp"
 #include "lf_kernels.hpp"
+#include "lf_pdl.hpp"
 
 namespace lfg {
 
@@ -267,6 +268,7 @@ __device__ __forceinline__ void load_tile(const DCParams& P, const TileOrigin& o
 template <typename TS, typename TD, int NP, int NC, int NT>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_transpose(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  LFG_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int la = P.la, lb = P.lb, lg = P.lg;
   const int TA = 1 << la, TB = 1 << lb, ld = TB + 1, n = TA * TB;
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(kCopyThreads)
 template <typename TS, typename TD, int NP, int NC, int NT>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_direct(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  LFG_PDL_ENTRY();
   const int la = P.la, lb = P.lb, lg = P.lg;
   const int TA = 1 << la, n = TA << lb;
   const int tpt = kCopyThreads >> lg;
@@ -371,6 +374,7 @@ __device__ __forceinline__ void st_vec(T* __restrict__ p, const T (&v)[V]) {
 template <typename TS, typename TD>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_transpose_vec(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  LFG_PDL_ENTRY();
   constexpr int V = VecW<TS, TD>::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int la = P.la, lb = P.lb, lg = P.lg;
@@ -420,6 +424,7 @@ __global__ void __launch_bounds__(kCopyThreads)
 template <typename TS, typename TD, int NP, int NC, int NT>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_transpose_vst(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  LFG_PDL_ENTRY();
   constexpr int V = 16 / sizeof(TD);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int la = P.la, lb = P.lb, lg = P.lg;
@@ -458,6 +463,7 @@ __global__ void __launch_bounds__(kCopyThreads)
 template <typename TS, typename TD>
 __global__ void __launch_bounds__(kCopyThreads)
     digit_direct_vec(const DCParams P, const TS* __restrict__ src, TD* __restrict__ dst) {
+  LFG_PDL_ENTRY();
   constexpr int V = VecW<TS, TD>::V;
   const int la = P.la, lb = P.lb, lg = P.lg;
   const int lav = la - __ffs(V) + 1;
@@ -575,6 +581,7 @@ template <typename TS, typename TD>
 __global__ void __launch_bounds__(kCopyThreads)
     ix_copy(const IxProgram* __restrict__ progs, int64_t n, const TS* __restrict__ src,
             TD* __restrict__ dst, int* err) {
+  LFG_PDL_ENTRY();
   __shared__ IxProgram sp[2];
   {
     const int* g = reinterpret_cast<const int*>(progs);
@@ -876,8 +883,9 @@ cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, con
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(batches, int64_t(nsm) * per_sm));
     if (info) info->grid = grid;
-    k<<<static_cast<unsigned>(grid), kCopyThreads, smem, stream>>>(
-        P, static_cast<const TS*>(src), static_cast<TD*>(dst));
+    cudaError_t le = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(kCopyThreads), smem, stream,
+                                P, static_cast<const TS*>(src), static_cast<TD*>(dst));
+    if (le != cudaSuccess) return le;
     return cudaGetLastError();
   });
 }
@@ -911,7 +919,7 @@ cudaError_t launch_ix_copy(const IxProgram* d_progs, int64_t n, int src_elem, in
   return dispatch<Unused>(src_elem, dst_elem, [&](auto s, auto d) -> cudaError_t {
     using TS = decltype(s);
     using TD = decltype(d);
-    ix_copy<TS, TD><<<static_cast<unsigned>(blocks), kCopyThreads, 0, stream>>>(
+    launch_pdl(ix_copy<TS, TD>, dim3(static_cast<unsigned>(blocks)), dim3(kCopyThreads), 0, stream,
         d_progs, n, static_cast<const TS*>(src), static_cast<TD*>(dst), d_err);
     return cudaGetLastError();
   });

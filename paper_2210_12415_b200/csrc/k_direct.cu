@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "lf_direct.hpp"
+#include "lf_pdl.hpp"
 
 namespace lfg {
 
@@ -22,6 +23,7 @@ constexpr int kDTW = 16, kDTH = 8, kDThreads = kDTW * kDTH, kDOC = 16;
 
 __global__ void __launch_bounds__(kDThreads)
     c2d_direct(const DirectConv P) {
+  LFG_PDL_ENTRY();
   extern __shared__ __align__(16) float sm[];
   const int R = P.I * P.KH * P.KW;
   const int PH = (kDTH - 1) * P.V + P.KH, PW = (kDTW - 1) * P.V + P.KW;
@@ -103,7 +105,7 @@ cudaError_t launch_c2d_direct(const DirectConv& P, cudaStream_t stream) {
   dim3 grid(static_cast<unsigned>((P.Wo + kDTW - 1) / kDTW),
             static_cast<unsigned>((P.Ho + kDTH - 1) / kDTH),
             static_cast<unsigned>(P.N * (P.O / kDOC)));
-  c2d_direct<<<grid, kDThreads, smem, stream>>>(P);
+  launch_pdl(c2d_direct, grid, dim3(kDThreads), smem, stream, P);
   return cudaGetLastError();
 }
 

@@ -19,6 +19,7 @@
 
 #include "lf_core.hpp"
 #include "lf_generic.hpp"
+#include "lf_pdl.hpp"
 
 namespace lfg {
 
@@ -111,6 +112,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     gen_eltwise(const IxProgram* __restrict__ out_prog, GenEltwise P, T* __restrict__ out,
                 int* err) {
+  LFG_PDL_ENTRY();
   __shared__ IxProgram sp;
   {
     const int* g = reinterpret_cast<const int*>(out_prog);
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(256)
 template <typename T, typename Acc>
 __global__ void __launch_bounds__(256)
     gen_contract(const IxProgram* __restrict__ out_prog, GenContract P, T* __restrict__ out) {
+  LFG_PDL_ENTRY();
   __shared__ IxProgram sp;
   {
     const int* g = reinterpret_cast<const int*>(out_prog);
@@ -247,6 +250,7 @@ __global__ void __launch_bounds__(256)
 template <typename T, typename Acc>
 __global__ void __launch_bounds__(256)
     gen_contract_warp(const IxProgram* __restrict__ out_prog, GenContract P, T* __restrict__ out) {
+  LFG_PDL_ENTRY();
   __shared__ IxProgram sp;
   {
     const int* g = reinterpret_cast<const int*>(out_prog);
@@ -333,9 +337,9 @@ cudaError_t launch_gen_eltwise(const IxProgram* d_prog, const GenEltwise& P, int
   if (P.n == 0) return cudaSuccess;
   unsigned g = static_cast<unsigned>(grid_for(P.n));
   if (elem == LFGPU_ELEM_I32)
-    gen_eltwise<int32_t><<<g, 256, 0, stream>>>(d_prog, P, static_cast<int32_t*>(out), d_err);
+    launch_pdl(gen_eltwise<int32_t>, dim3(g), dim3(256), 0, stream, d_prog, P, static_cast<int32_t*>(out), d_err);
   else
-    gen_eltwise<float><<<g, 256, 0, stream>>>(d_prog, P, static_cast<float*>(out), d_err);
+    launch_pdl(gen_eltwise<float>, dim3(g), dim3(256), 0, stream, d_prog, P, static_cast<float*>(out), d_err);
   return cudaGetLastError();
 }
 
@@ -355,21 +359,20 @@ cudaError_t launch_gen_contract(const IxProgram* d_prog, const GenContract& P, i
     const int64_t warps = std::min<int64_t>(P.n, 148 * 64);
     const unsigned g = static_cast<unsigned>((warps + 7) / 8);
     if (elem == LFGPU_ELEM_I32)
-      gen_contract_warp<int32_t, long long>
-          <<<g, 256, 0, stream>>>(d_prog, P, static_cast<int32_t*>(out));
+      launch_pdl(gen_contract_warp<int32_t, long long>, dim3(g), dim3(256), 0, stream, d_prog, P, static_cast<int32_t*>(out));
     else if (exact)
-      gen_contract_warp<float, double><<<g, 256, 0, stream>>>(d_prog, P, static_cast<float*>(out));
+      launch_pdl(gen_contract_warp<float, double>, dim3(g), dim3(256), 0, stream, d_prog, P, static_cast<float*>(out));
     else
-      gen_contract_warp<float, float><<<g, 256, 0, stream>>>(d_prog, P, static_cast<float*>(out));
+      launch_pdl(gen_contract_warp<float, float>, dim3(g), dim3(256), 0, stream, d_prog, P, static_cast<float*>(out));
     return cudaGetLastError();
   }
   unsigned g = static_cast<unsigned>(grid_for(P.n));
   if (elem == LFGPU_ELEM_I32)
-    gen_contract<int32_t, long long><<<g, 256, 0, stream>>>(d_prog, P, static_cast<int32_t*>(out));
+    launch_pdl(gen_contract<int32_t, long long>, dim3(g), dim3(256), 0, stream, d_prog, P, static_cast<int32_t*>(out));
   else if (exact)
-    gen_contract<float, double><<<g, 256, 0, stream>>>(d_prog, P, static_cast<float*>(out));
+    launch_pdl(gen_contract<float, double>, dim3(g), dim3(256), 0, stream, d_prog, P, static_cast<float*>(out));
   else
-    gen_contract<float, float><<<g, 256, 0, stream>>>(d_prog, P, static_cast<float*>(out));
+    launch_pdl(gen_contract<float, float>, dim3(g), dim3(256), 0, stream, d_prog, P, static_cast<float*>(out));
   return cudaGetLastError();
 }
 

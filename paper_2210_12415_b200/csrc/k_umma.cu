@@ -33,6 +33,7 @@ struct UmmaParams {
   const int64_t* row_off;
   const int64_t* col_off;
   float* out;
+  __nv_bfloat16* out_bf16;  // optional bf16 copy of the output (same layout)
   const float* epi_ptr[kMaxEpi];
   int32_t epi_kind[kMaxEpi];
   int32_t epi_count;
@@ -50,6 +51,11 @@ struct UmmaParams {
   // barrier wfull[c]); the ring then carries A only.
   int32_t wres, w_off, w_chunk, w_tx;
   int32_t red_bytes;        // split-K: SMEM for the siblings' column slices
+  // Store mode 2 (TMA store): staging buffers (2 x stg_f32 fp32 + 2 x stg_bf
+  // bf16 bytes) at stg_off; per-tile box origins; row positions in the box
+  // follow row_off in the SMEM table.
+  int32_t stg_off, stg_f32, stg_bf;
+  const int32_t* tile_coords;
   int32_t a_tap[kMaxTaps];
   int32_t store_mode;       // 1: row-contiguous, 16-byte aligned output rows; 0: generic
   int64_t col0;             // col_off[0] folded into the tile base in store mode 1
@@ -98,6 +104,16 @@ __device__ __forceinline__ void tma_load5(const CUtensorMap* map, uint32_t dst, 
       "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
+// TMA store of one SMEM box (bulk-group completion).
+__device__ __forceinline__ void tma_store5(const CUtensorMap* map, uint32_t src, int32_t c0, int32_t c1,
+                                           int32_t c2, int32_t c3, int32_t c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
 
@@ -212,39 +228,12 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float* f) {
 // fetched cold from L2 instruction by instruction (ncu: stall_no_inst
 // dominated an unrolled version, ~12 us per tile). The loops below are kept
 // rolled so one small body is fetched once and reused.
-// One W-column chunk of one unit's accumulator for the calling thread's row.
-// mode 3 publishes a split-K partial; otherwise (after the split-K sum when
-// splits > 1) the chunk goes through the per-warp SMEM buffer and is stored
-// with mode 1 (row-contiguous output: float4 row segments, 8 lanes per
-// 128 bytes) or mode 0 (generic: thread = row, coalesced when rows are the
-// contiguous side).
+// Sum one W-column chunk over the split-K partials in split order (this
+// split's own values `v` from TMEM; the siblings' slices were bulk-copied
+// into SMEM `red`, laid out [other split][col/4][row] float4).
 template <int W>
-__device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, int c0, int row,
-                                       int lane, int q, float* wbuf, int rows, int cols,
-                                       int n_base, int64_t obase, const int64_t* s_row,
-                                       const int64_t* s_col, int mode, int split, int splits,
-                                       int64_t ws_tile, const float4* red, int red_lo,
-                                       bool release, uint32_t tempty) {
-  float v[W];
-  tmem_ld<W>(taddr + c0, v);
-  if (release) {
-    // Every TMEM read of this accumulator is complete: hand it back to the MMA.
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive(tempty);
-  }
-  const int64_t wstride = static_cast<int64_t>(P.BN / 4) * 128;
-  if (mode == 3) {  // publish this split's partial tile ([unit][col/4][row] float4)
-    float4* w = reinterpret_cast<float4*>(P.ws) + (ws_tile + split) * wstride + (c0 / 4) * 128 + row;
-#pragma unroll
-    for (int j = 0; j < W / 4; ++j)
-      __stcg(w + j * 128, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-    return;
-  }
-  if (splits > 1) {
-    // Sum this chunk over the splits' partials in split order (this split's
-    // own from TMEM; the siblings' slices were bulk-copied into SMEM `red`,
-    // laid out [other split][col/4][row] float4).
+__device__ __forceinline__ void split_sum(const UmmaParams& P, float* v, const float4* red, int c0,
+                                          int red_lo, int row, int split, int splits) {
     const int slice4 = P.BN / splits / 4;
     const float4* r0 = red + ((c0 - red_lo) / 4) * 128 + row;
     float4 part[kMaxSplits - 1][W / 4];
@@ -287,13 +276,46 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
       v[4 * j + 2] = acc.z;
       v[4 * j + 3] = acc.w;
     }
+}
+
+// One W-column chunk of one unit's accumulator for the calling thread's row.
+// mode 3 publishes a split-K partial; otherwise (after the split-K sum when
+// splits > 1) the chunk goes through the per-warp SMEM buffer and is stored
+// with mode 1 (row-contiguous output: float4 row segments, 8 lanes per
+// 128 bytes) or mode 0 (generic: thread = row, coalesced when rows are the
+// contiguous side).
+template <int W>
+__device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, int c0, int row,
+                                       int lane, int q, float* wbuf, int rows, int cols,
+                                       int n_base, int64_t obase, const int64_t* s_row,
+                                       const int64_t* s_col, int mode, int split, int splits,
+                                       int64_t ws_tile, const float4* red, int red_lo,
+                                       bool release, uint32_t tempty) {
+  float v[W];
+  tmem_ld<W>(taddr + c0, v);
+
+  if (release) {
+    // Every TMEM read of this accumulator is complete: hand it back to the MMA.
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty);
   }
+  const int64_t wstride = static_cast<int64_t>(P.BN / 4) * 128;
+  if (mode == 3) {  // publish this split's partial tile ([unit][col/4][row] float4)
+    float4* w = reinterpret_cast<float4*>(P.ws) + (ws_tile + split) * wstride + (c0 / 4) * 128 + row;
+#pragma unroll
+    for (int j = 0; j < W / 4; ++j)
+      __stcg(w + j * 128, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+    return;
+  }
+  if (splits > 1) split_sum<W>(P, v, red, c0, red_lo, row, split, splits);
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < W / 4; ++j)
     *reinterpret_cast<float4*>(wbuf + lane * kEpiLd + 4 * j) =
         make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
   __syncwarp();
+
   if (mode == 1) {
     // All SMEM reads and addresses first, then the op chain, then the
     // stores: independent instructions the SM can overlap (the previous
@@ -355,6 +377,18 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
 #pragma unroll
     for (int it = 0; it < IT; ++it)
       if (ok[it]) *reinterpret_cast<float4*>(P.out + addr[it]) = x[it];
+    if (P.out_bf16) {  // the tensor-core consumers' bf16 copy, same layout
+#pragma unroll
+      for (int it = 0; it < IT; ++it)
+        if (ok[it]) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(x[it].x, x[it].y);
+          __nv_bfloat162 hi = __floats2bfloat162_rn(x[it].z, x[it].w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(P.out_bf16 + addr[it]) = pk;
+        }
+    }
     return;
   }
   // Generic: thread = row, 8 columns per step (loads, ops, stores batched).
@@ -383,14 +417,18 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (c0 + j0 + j < cols) P.out[a[j]] = y[j];
+        if (c0 + j0 + j < cols) {
+          P.out[a[j]] = y[j];
+          if (P.out_bf16) P.out_bf16[a[j]] = __float2bfloat16_rn(y[j]);
+        }
     }
   }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     umma_kernel(const __grid_constant__ CUtensorMap tma_a,
-                const __grid_constant__ CUtensorMap tma_b, const __grid_constant__ UmmaParams P) {
+                const __grid_constant__ CUtensorMap tma_b, const __grid_constant__ UmmaParams P,
+                const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ CUtensorMap tma_ob) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B atoms) by offsetting the __shared__
   // array itself, so every derived pointer stays in the shared window.
@@ -398,9 +436,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int stage_bytes = P.a_boxes * P.a_slot + (P.wres ? 0 : P.b_boxes * P.b_slot);
   const int wbytes = P.wres ? P.nstages * P.w_chunk : 0;
   float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes + wbytes);
-  const float4* s_red = reinterpret_cast<const float4*>(smem + P.ring_bytes + wbytes + kEpiSmemBytes);
-  uint64_t* bars =
-      reinterpret_cast<uint64_t*>(smem + P.ring_bytes + wbytes + kEpiSmemBytes + P.red_bytes);
+  const int stg_bytes = 2 * (P.stg_f32 + P.stg_bf);
+  const float4* s_red =
+      reinterpret_cast<const float4*>(smem + P.ring_bytes + wbytes + kEpiSmemBytes + stg_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + wbytes + kEpiSmemBytes +
+                                               stg_bytes + P.red_bytes);
   const int nw = P.wres ? P.nstages : 0;
   const int pipe = P.pipe;
   const uint32_t full0 = smem_u32(bars);
@@ -414,12 +454,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   StageEntry* s_stage = reinterpret_cast<StageEntry*>(bars + 2 * pipe + 6 + nw);
   int64_t* s_col = reinterpret_cast<int64_t*>(s_stage + P.nstages);
   int64_t* s_row = s_col + P.BN;
+  const int32_t* s_rowpos = reinterpret_cast<const int32_t*>(s_row + 128);  // store mode 2
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int splits = P.splits;
   const int nunits = P.ntiles * splits;
   const int nst = P.nstages;
-  unsigned long long* dbg = P.dbg ? P.dbg + 24 * blockIdx.x : nullptr;
+  unsigned long long* dbg = P.dbg ? P.dbg + 32 * blockIdx.x : nullptr;
   if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
 
   if (threadIdx.x == 0) {
@@ -594,6 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* wbuf = s_epi + q * 32 * kEpiLd;
     const int BN = P.BN;
     uint32_t red_phase = 0;
+    int stg_count = 0;  // TMA-store chunks issued (staging double buffer)
     int i = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       const int tile = u / splits, split = u - tile * splits;
@@ -660,8 +702,76 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const bool pub = it < npub;
         const int c0 = pub ? (it * 16 < lo ? it * 16 : it * 16 + sl) : lo + (it - npub) * 16;
-        epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col,
-                      pub ? 3 : mode, split, splits, ws_tile, s_red, red_lo, it == nitems - 1, tempty);
+        if (!pub && mode == 2) {
+          // TMA-store epilogue: registers -> swizzled SMEM box -> one
+          // cp.async.bulk.tensor per 16-column chunk (double-buffered).
+          const int kb = stg_count & 1;
+          if (threadIdx.x == kEpiWarp0 * 32)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer kb drained
+          epi_bar();
+          float v[16];
+          tmem_ld<16>(tbase + c0, v);
+
+          if (it == nitems - 1) {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+          }
+          if (splits > 1) split_sum<16>(P, v, s_red, c0, red_lo, row, split, splits);
+          const int rp = row < rows ? s_rowpos[row] : -1;
+          if (rp >= 0) {
+            const int64_t addr = obase + s_row[row] + c0;
+#pragma unroll 1
+            for (int e = 0; e < P.epi_count; ++e) {
+              const int k = P.epi_kind[e];
+              const float* ep = P.epi_ptr[e];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (k == EPI_RELU) v[j] = fmaxf(v[j], 0.0f);
+                else v[j] += __ldg(ep + (k == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j) : addr + j));
+              }
+            }
+            // SWIZZLE_64B rows of 16 fp32: 16-byte chunk j at j ^ ((rp >> 1) & 3)
+            uint8_t* sf = smem + P.stg_off + kb * P.stg_f32 + rp * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<float4*>(sf + ((j ^ ((rp >> 1) & 3)) << 4)) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            if (P.stg_bf) {  // SWIZZLE_32B rows of 16 bf16: chunk j at j ^ ((rp >> 2) & 1)
+              uint8_t* sb = smem + P.stg_off + 2 * P.stg_f32 + kb * P.stg_bf + rp * 32;
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                uint4 pk;
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+                __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+                __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+                pk.x = *reinterpret_cast<uint32_t*>(&h0);
+                pk.y = *reinterpret_cast<uint32_t*>(&h1);
+                pk.z = *reinterpret_cast<uint32_t*>(&h2);
+                pk.w = *reinterpret_cast<uint32_t*>(&h3);
+                *reinterpret_cast<uint4*>(sb + ((j ^ ((rp >> 2) & 1)) << 4)) = pk;
+              }
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          epi_bar();
+          if (threadIdx.x == kEpiWarp0 * 32) {
+            const int32_t* tc = P.tile_coords + tile * 5;
+            const int32_t x0 = __ldg(tc) + c0, x1 = __ldg(tc + 1), x2 = __ldg(tc + 2),
+                          x3 = __ldg(tc + 3), x4 = __ldg(tc + 4);
+            tma_store5(&tma_o, smem_u32(smem + P.stg_off + kb * P.stg_f32), x0, x1, x2, x3, x4);
+            if (P.stg_bf)
+              tma_store5(&tma_ob, smem_u32(smem + P.stg_off + 2 * P.stg_f32 + kb * P.stg_bf), x0, x1,
+                         x2, x3, x4);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          ++stg_count;
+        } else {
+          epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col,
+                        pub ? 3 : mode, split, splits, ws_tile, s_red, red_lo, it == nitems - 1, tempty);
+        }
+        if (dbg && i == 0 && it < 8 && threadIdx.x == kEpiWarp0 * 32) dbg[20 + it] = gtimer();
       }
       if (splits > 1) {
         epi_bar();
@@ -675,6 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (dbg && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[12 + i] = gtimer();
     }
+    if (threadIdx.x == kEpiWarp0 * 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (dbg && threadIdx.x == kEpiWarp0 * 32) dbg[6] = gtimer();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -721,7 +832,7 @@ CUtensorMap encode(const OperandView& v, const void* base) {
       es[d] = v.estride[d];
     } else {  // unit padding dims: the kernel always issues 5-D loads
       dims[d] = 1;
-      strides[d] = d == 1 ? ((v.dims[0] * 2 + 15) / 16) * 16 : strides[d - 1] * dims[d - 1];
+      strides[d] = d == 1 ? ((v.dims[0] * v.elem_bytes + 15) / 16) * 16 : strides[d - 1] * dims[d - 1];
       box[d] = 1;
       es[d] = 1;
     }
@@ -730,10 +841,15 @@ CUtensorMap encode(const OperandView& v, const void* base) {
                           : v.swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                           : v.swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                             : CU_TENSOR_MAP_SWIZZLE_NONE;
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base),
+  const CUtensorMapDataType dt =
+      v.elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = encode_fn()(&m, dt, 5, const_cast<void*>(base),
                            dims, strides + 1, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fail(LFGPU_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  // A view TMA cannot express is an illegal candidate, not a device fault.
+  if (r != CUDA_SUCCESS)
+    fail(LFGPU_EUNSUPPORTED, "TMA cannot express operand view (cuTensorMapEncodeTiled " +
+                                 std::to_string(r) + ")");
   return m;
 }
 
@@ -760,7 +876,7 @@ uint32_t idesc_of(int M, int N, bool a_mn, bool b_mn) {
 }
 
 struct Tables {
-  void* p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  void* p[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   ~Tables() {
     for (auto* q : p)
       if (q) cudaFree(q);
@@ -779,6 +895,16 @@ void* up(const std::vector<T>& v) {
 
 }  // namespace
 
+bool umma_view_encodable(const OperandView& v, std::string* why) {
+  try {
+    encode(v, reinterpret_cast<void*>(static_cast<uintptr_t>(1) << 20));
+    return true;
+  } catch (const Error& e) {
+    *why = e.what();
+    return false;
+  }
+}
+
 static void* g_umma_dbg = nullptr;
 void* umma_debug_buffer() { return g_umma_dbg; }
 void umma_set_debug_buffer(void* p) { g_umma_dbg = p; }
@@ -796,12 +922,14 @@ static int num_sms() {
 
 UmmaLaunch umma_prepare(const UmmaPlan& p) {
   UmmaLaunch L;
+  std::memset(&L.tma_o, 0, sizeof(L.tma_o));
+  std::memset(&L.tma_ob, 0, sizeof(L.tma_ob));
   L.tma_a = encode(p.A, p.a);
   L.tma_b = encode(p.B, p.b);
   auto t = std::make_shared<Tables>();
   t->p[0] = up(p.tiles);
   {  // [stages | col_off | row_off] contiguous: the kernel copies it to SMEM in one pass
-    std::vector<int32_t> tab(p.stages.size() * sizeof(StageEntry) / 4 + 2 * (p.col_off.size() + 128));
+    std::vector<int32_t> tab(p.stages.size() * sizeof(StageEntry) / 4 + 2 * (p.col_off.size() + 128) + 128);
     size_t o = 0;
     std::memcpy(tab.data(), p.stages.data(), p.stages.size() * sizeof(StageEntry));
     o += p.stages.size() * sizeof(StageEntry) / 4;
@@ -810,6 +938,8 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     std::vector<int64_t> rows(128, 0);
     for (size_t r = 0; r < 128 && r < p.row_off.size(); ++r) rows[r] = p.row_off[r];
     std::memcpy(tab.data() + o, rows.data(), 128 * 8);
+    o += 256;
+    for (int r = 0; r < 128; ++r) tab[o + r] = p.ost.ok ? p.ost.row_pos[r] : -1;
     L.table_ints = static_cast<int>(tab.size());
     t->p[1] = up(tab);
   }
@@ -846,6 +976,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     L.epi_ptr[e] = p.epi[e].ptr;
   }
   L.out = p.out;
+  L.out_bf16 = p.out_bf16;
   // Split-K (schedule `order`: 0 = heuristic, 1 = never, 2 = at least 2):
   // when the tiles alone leave most of the SMs idle and the K loop is long.
   const int sms = num_sms();
@@ -866,25 +997,6 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   L.w_chunk = L.b_boxes * L.b_slot;
   L.w_tx = L.b_boxes * L.b_bytes;
   const size_t wbytes = p.wres ? static_cast<size_t>(p.stages.size()) * L.w_chunk : 0;
-  // SMEM: ring | resident weights | epilogue buffers | split-K slices |
-  // barriers | tables. The ring gives up stages if the rest needs room.
-  for (;;) {
-    const size_t ring = static_cast<size_t>(L.pipe) *
-                        (L.a_boxes * L.a_slot + (p.wres ? 0 : L.b_boxes * L.b_slot));
-    L.ring_bytes = static_cast<int>((ring + 1023) / 1024 * 1024);
-    L.smem = 1024 + L.ring_bytes + wbytes + kEpiSmemBytes + L.red_bytes +
-             8 * (2 * L.pipe + 5 + (p.wres ? p.stages.size() : 0)) + 8 +
-             sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 64;
-    if (L.smem <= 227 * 1024 || L.pipe <= 2) break;
-    --L.pipe;
-  }
-  if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "tcgen05 kernel SMEM exceeds 227 KB");
-  L.nprod = std::max(1, std::min(3, L.pipe - 1));
-  L.ntaps = p.ntaps;
-  L.b_tap = p.b_tap;
-  if (p.ntaps > kMaxTaps || static_cast<int>(p.a_tap.size()) < p.ntaps)
-    fail(LFGPU_EINVAL, "umma: tap table");
-  for (int t = 0; t < p.ntaps; ++t) L.a_tap[t] = p.a_tap[t];
   // Store mode 1 (transposed, float4 row stores): output columns contiguous
   // and every stored row 16-byte aligned.
   int max_rows = 0;
@@ -899,12 +1011,51 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     if (te.out_base % 4 || te.cols % 4) aligned = false;
   L.store_mode = aligned ? 1 : 0;
   L.col0 = aligned ? p.col_off[0] : 0;
-  if (const char* e = getenv("LFGPU_STORE_MODE")) {  // diagnostics: force the generic path
-    if (atoi(e) == 0) {
-      L.store_mode = 0;
-      L.col0 = 0;
+  // Store mode 2 (TMA store) when the output tile is a TMA box.
+  bool full_cols = true;
+  for (const auto& te : p.tiles)
+    if (te.cols != p.BN) full_cols = false;
+  const char* sm_env = getenv("LFGPU_STORE_MODE");
+  const bool want_tma = (p.tma_store && !(sm_env && atoi(sm_env) < 2)) || (sm_env && atoi(sm_env) == 2);
+  if (p.ost.ok && cols_unit && full_cols && want_tma) {
+    L.store_mode = 2;
+    L.col0 = p.col_off[0];
+    L.tma_o = encode(p.ost.O, p.out);
+    L.stg_f32 = (p.ost.box_rows * 64 + 1023) / 1024 * 1024;
+    if (p.out_bf16) {
+      OperandView ob = p.ost.O;
+      ob.elem_bytes = 2;
+      ob.swizzle = 32;
+      for (int d = 1; d < ob.rank; ++d) ob.strides[d] /= 2;
+      L.tma_ob = encode(ob, p.out_bf16);
+      L.stg_bf = (p.ost.box_rows * 32 + 1023) / 1024 * 1024;
     }
+    t->p[6] = up(p.ost.tile_coords);
+    L.d_tcoords = t->p[6];
   }
+  if (sm_env && atoi(sm_env) == 0) {  // diagnostics: force the generic path
+    L.store_mode = 0;
+    L.col0 = 0;
+  }
+  // SMEM: ring | resident weights | epilogue buffers | split-K slices |
+  // barriers | tables. The ring gives up stages if the rest needs room.
+  for (;;) {
+    const size_t ring = static_cast<size_t>(L.pipe) *
+                        (L.a_boxes * L.a_slot + (p.wres ? 0 : L.b_boxes * L.b_slot));
+    L.ring_bytes = static_cast<int>((ring + 1023) / 1024 * 1024);
+    L.smem = 1024 + L.ring_bytes + wbytes + kEpiSmemBytes + 2 * (L.stg_f32 + L.stg_bf) + L.red_bytes +
+             8 * (2 * L.pipe + 5 + (p.wres ? p.stages.size() : 0)) + 8 +
+             sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 4 * 128 + 64;
+    if (L.smem <= 227 * 1024 || L.pipe <= 2) break;
+    --L.pipe;
+  }
+  if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "tcgen05 kernel SMEM exceeds 227 KB");
+  L.nprod = std::max(1, std::min(3, L.pipe - 1));
+  L.ntaps = p.ntaps;
+  L.b_tap = p.b_tap;
+  if (p.ntaps > kMaxTaps || static_cast<int>(p.a_tap.size()) < p.ntaps)
+    fail(LFGPU_EINVAL, "umma: tap table");
+  for (int t = 0; t < p.ntaps; ++t) L.a_tap[t] = p.a_tap[t];
   if (L.splits > 1) {
     const size_t ws = sizeof(float) * static_cast<size_t>(L.ntiles) * L.splits * 128 * L.BN;
     if (cudaMalloc(&t->p[4], ws) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc split-K workspace");
@@ -929,6 +1080,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.row_off = static_cast<const int64_t*>(L.d_rows);
   P.col_off = static_cast<const int64_t*>(L.d_cols);
   P.out = L.out;
+  P.out_bf16 = static_cast<__nv_bfloat16*>(L.out_bf16);
   P.epi_count = L.epi_count;
   for (int e = 0; e < L.epi_count; ++e) {
     P.epi_kind[e] = L.epi_kinds[e];
@@ -950,6 +1102,11 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.w_chunk = L.w_chunk;
   P.w_tx = L.w_tx;
   P.red_bytes = L.red_bytes;
+  P.stg_f32 = L.stg_f32;
+  P.stg_off = L.ring_bytes + (L.wres ? L.nstages * L.w_chunk : 0) + kEpiSmemBytes;
+  P.stg_bf = L.stg_bf;
+  P.tile_coords = static_cast<const int32_t*>(L.d_tcoords);
+
   P.a_desc = L.a_desc;
   P.b_desc = L.b_desc;
   P.a_kadv = L.a_kadv;
@@ -990,7 +1147,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, umma_kernel, L.tma_a, L.tma_b, P);
+  return cudaLaunchKernelEx(&cfg, umma_kernel, L.tma_a, L.tma_b, P, L.tma_o, L.tma_ob);
 }
 
 }  // namespace lfg

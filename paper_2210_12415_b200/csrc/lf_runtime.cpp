@@ -198,6 +198,7 @@ struct PTensor {
   std::vector<int> consumers;
   bool need_f32 = false, need_bf16 = false;
   bool valid = true;  // false: fused away, never materialized
+  bool shadow_by_producer = false;  // the producer's epilogue writes d_bf16 too
 };
 
 struct PStep {
@@ -441,10 +442,32 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   }
   int* d_err = P->ctx->d_err;
 
+  // Mixed consumers: refresh a tensor's bf16 shadow right after it is
+  // written (by its own node, or by the fused epilogue of the chain it ends).
+  auto refresh_shadow = [&](int ni, PTensor& out) {
+    if (!(out.d && out.d_bf16) || out.shadow_by_producer) return;
+    CopySpec spec;
+    spec.lmap = identity_map(out.logical);
+    spec.dst_seq = out.seq;
+    spec.src_seq = out.seq;
+    bool oob;
+    CopyKernel k = compile_copy(spec, out.elem, LFGPU_ELEM_BF16, P->keep, &oob);
+    const void* src = out.d;
+    void* dst = out.d_bf16;
+    PStep sh;
+    sh.node = ni;
+    sh.kernel = "bf16_shadow";
+    sh.run = [k, src, dst, d_err](cudaStream_t s) { return run_copy(k, src, dst, d_err, s); };
+    P->steps.push_back(std::move(sh));
+  };
+
   // 3. One step per node.
   for (int ni : P->order) {
     if (fused_away.count(ni)) {
       P->node_kernel[ni] = "fused";
+      // The chain's final tensor was written by the producer's epilogue.
+      PTensor& fo = P->t[P->nodes[ni].output];
+      if (fo.valid) refresh_shadow(ni, fo);
       continue;
     }
     const auto& n = P->nodes[ni];
@@ -576,6 +599,11 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           // fused chain are also written when the caller keeps them.
           int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : n.output;
           up.out = static_cast<float*>(P->t[final_t].d);
+          if (P->t[final_t].d && P->t[final_t].d_bf16 &&
+              P->t[final_t].elem == LFGPU_ELEM_F32) {  // dual store: no shadow pass
+            up.out_bf16 = P->t[final_t].d_bf16;
+            P->t[final_t].shadow_by_producer = true;
+          }
           for (int e = 0; e < up.epi_count; ++e) {
             if (up.epi[e].tensor >= 0) {
               const PTensor& et = P->t[up.epi[e].tensor];
@@ -678,22 +706,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
     }
     P->node_kernel[ni] = step.kernel;
     P->steps.push_back(std::move(step));
-    // Mixed consumers: refresh the bf16 shadow right after the producer.
-    if (out.d && out.d_bf16) {
-      CopySpec spec;
-      spec.lmap = identity_map(out.logical);
-      spec.dst_seq = out.seq;
-      spec.src_seq = out.seq;
-      bool oob;
-      CopyKernel k = compile_copy(spec, out.elem, LFGPU_ELEM_BF16, P->keep, &oob);
-      const void* src = out.d;
-      void* dst = out.d_bf16;
-      PStep sh;
-      sh.node = ni;
-      sh.kernel = "bf16_shadow";
-      sh.run = [k, src, dst, d_err](cudaStream_t s) { return run_copy(k, src, dst, d_err, s); };
-      P->steps.push_back(std::move(sh));
-    }
+    if (out.valid) refresh_shadow(ni, out);
   }
 }
 

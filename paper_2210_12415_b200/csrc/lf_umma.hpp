@@ -42,6 +42,7 @@ struct EpiOp {
 // Host description of one operand's TMA view and UMMA SMEM descriptor.
 struct OperandView {
   int32_t rank = 0;
+  int32_t elem_bytes = 2;  // 2: bf16, 4: fp32 (output views)
   uint64_t dims[5] = {};
   uint64_t strides[5] = {};  // bytes, dims 1..rank-1
   uint32_t box[5] = {};
@@ -69,6 +70,20 @@ struct StageEntry {  // 40 bytes
   int32_t sb[5];
 };
 
+// TMA-store epilogue (store mode 2): the fp32 output tile is staged in SMEM
+// (16 columns = 64 bytes per row, SWIZZLE_64B) and written by
+// cp.async.bulk.tensor; `row_pos[r]` is accumulator row r's row in the box
+// (-1: not an output row), `tile_coords` the box origin of every tile.
+struct OutStore {
+  bool ok = false;
+  OperandView O;                     // fp32 view of the output (box: 16 cols x tile rows)
+  int col_dim = 0;                   // view dim of the columns (0)
+  std::vector<int32_t> tile_coords;  // ntiles x 5
+  std::vector<int32_t> row_pos;      // 128
+  int box_rows = 0;                  // rows of one staged chunk
+  std::string why;
+};
+
 struct UmmaPlan {
   int kind = UMMA_GEMM;
   int BM = 128, BN = 128;
@@ -82,6 +97,8 @@ struct UmmaPlan {
   std::vector<int32_t> a_tap{0};
   int b_tap = 0;
   int wres = 0;          // halo C2D: weights resident in SMEM (one output-channel tile)
+  OutStore ost;          // TMA-store epilogue, when the output tile is a TMA box
+  int tma_store = 0;     // schedule `vectorize`: use the TMA-store epilogue when legal
   OperandView A, B;
   std::vector<TileEntry> tiles;
   std::vector<StageEntry> stages;
@@ -91,6 +108,7 @@ struct UmmaPlan {
   const void* a = nullptr;
   const void* b = nullptr;
   float* out = nullptr;
+  void* out_bf16 = nullptr;  // optional bf16 copy written by the epilogue
   std::string summary;
 };
 
@@ -110,12 +128,16 @@ struct UmmaLaunch {
   const float* epi_ptr[kMaxEpi] = {};
   int epi_count = 0;
   float* out = nullptr;
+  void* out_bf16 = nullptr;
   size_t smem = 0;
   int grid = 0;
   int ring_bytes = 0;
   int table_ints = 0;            // [stages | col_off | row_off] int32 count
   int ntaps = 1, b_tap = 0;
   int wres = 0, w_chunk = 0, w_tx = 0;
+  CUtensorMap tma_o, tma_ob;     // store mode 2: fp32 output and its bf16 copy
+  int stg_off = 0, stg_f32 = 0, stg_bf = 0;
+  void* d_tcoords = nullptr;
   int red_bytes = 0;
   int32_t a_tap[kMaxTaps] = {};
   int store_mode = 0;           // 1: transposed float4 row stores; 0: generic
@@ -132,6 +154,8 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
 bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::vector<Dim>& k_log,
                     const Seq& k_seq, const std::vector<Dim>& y_log, const Seq& y_seq,
                     int64_t stride, const lfgpu_sched& s, UmmaPlan* out, std::string* why);
+// True when TMA can encode the view (checked with a dummy base address).
+bool umma_view_encodable(const OperandView& v, std::string* why);
 // Encodes tensor maps and uploads tables (needs a, b, out set).
 UmmaLaunch umma_prepare(const UmmaPlan& p);
 cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream);

@@ -12,6 +12,8 @@
 // descriptor. SURVEY.md §8(a+) derives the mapping; DESIGN.md §4 states the
 // legality rules enforced here.
 #include <algorithm>
+#include <array>
+#include <climits>
 #include <cstring>
 #include <numeric>
 #include <sstream>
@@ -332,6 +334,112 @@ int64_t offset_of(const std::vector<PDigit>& ds, const int64_t* lv) {
 
 }  // namespace
 
+// Output TMA-store view (OutStore): box = 16 columns (64-byte fp32 rows,
+// SWIZZLE_64B) x the tile's rows. `yd` are the output's physical digits,
+// `col_lj` its column (N / O) logical dim; `tile_lv[t]` the logical origin
+// of tile t, `row_rel[r]` the logical offset of accumulator row r from the
+// origin (`row_ok[r]` false: not an output row). The tile's rows must fill
+// the box exactly (else no TMA store).
+static void plan_out_store(const std::vector<PDigit>& yd, int nlog, int col_lj, int BN,
+                           const std::vector<std::array<int64_t, 4>>& tile_lv,
+                           const std::vector<std::array<int64_t, 4>>& row_rel,
+                           const std::vector<bool>& row_ok, OutStore* o) {
+  o->ok = false;
+  if (BN % 16 || tile_lv.empty()) {
+    o->why = "BN not a multiple of 16";
+    return;
+  }
+  if (yd.back().lj != col_lj || yd.back().div != 1 || yd.back().ext % 16) {
+    o->why = "columns not innermost";
+    return;
+  }
+  const int nk = static_cast<int>(yd.size());
+  auto dval = [&](const std::array<int64_t, 4>& lv, int k) { return digit_of(yd[k], lv[yd[k].lj]); };
+  // Row digit ranges over the valid rows of tile 0.
+  std::vector<int64_t> lo(nk, INT64_MAX), hi(nk, INT64_MIN);
+  int nvalid = 0;
+  for (int r = 0; r < 128; ++r) {
+    if (!row_ok[r]) continue;
+    ++nvalid;
+    std::array<int64_t, 4> lv = tile_lv[0];
+    for (int j = 0; j < nlog; ++j) lv[j] += row_rel[r][j];
+    for (int k = 0; k < nk; ++k) {
+      lo[k] = std::min(lo[k], dval(lv, k));
+      hi[k] = std::max(hi[k], dval(lv, k));
+    }
+  }
+  std::vector<VDim> v;
+  int64_t cells = 1;
+  for (int k = 0; k < nk; ++k) {
+    VDim d{yd[k].ext, yd[k].stride, 1, 1};
+    if (k == nk - 1) d.box = 16;
+    else if (yd[k].lj != col_lj) {
+      if (dval(tile_lv[0], k) != lo[k]) {
+        o->why = "tile origin is not the box corner";
+        return;
+      }
+      d.box = hi[k] - lo[k] + 1;
+      cells *= d.box;
+    } else if (lo[k] != hi[k]) {
+      o->why = "column tile spans an outer column digit";
+      return;
+    }
+    v.push_back(d);
+  }
+  if (cells != nvalid) {
+    o->why = "tile rows do not fill a box";
+    return;
+  }
+  std::vector<int> grp;
+  std::vector<int64_t> mult;
+  std::string why;
+  OperandView O;
+  if (!merge_view(v, &O, &grp, &mult, &why)) {
+    o->why = why;
+    return;
+  }
+  for (int d = 0; d < O.rank; ++d) O.strides[d] = O.strides[d] / 2 * 4;  // merge_view assumes bf16
+  O.elem_bytes = 4;
+  O.swizzle = 64;  // 16 fp32 = 64-byte box rows
+  O.mn_major = 0;
+  if (!umma_view_encodable(O, &why)) {
+    o->why = why;
+    return;
+  }
+  auto coord = [&](const std::array<int64_t, 4>& lv, int32_t* c) {
+    for (int d = 0; d < 5; ++d) c[d] = 0;
+    for (int k = 0; k < nk; ++k) c[grp[k]] += static_cast<int32_t>(dval(lv, k) * mult[k]);
+  };
+  // Row position inside the box (view dims >= 1, innermost first).
+  int32_t c0[5];
+  coord(tile_lv[0], c0);
+  o->row_pos.assign(128, -1);
+  for (int r = 0; r < 128; ++r) {
+    if (!row_ok[r]) continue;
+    std::array<int64_t, 4> lv = tile_lv[0];
+    for (int j = 0; j < nlog; ++j) lv[j] += row_rel[r][j];
+    int32_t c[5];
+    coord(lv, c);
+    int64_t pos = 0, scale = 1;
+    for (int d = 1; d < O.rank; ++d) {
+      const int64_t rel = c[d] - c0[d];
+      if (rel < 0 || rel >= O.box[d]) {
+        o->why = "row outside the box";
+        return;
+      }
+      pos += rel * scale;
+      scale *= O.box[d];
+    }
+    o->row_pos[r] = static_cast<int32_t>(pos);
+  }
+  o->box_rows = static_cast<int>(cells);
+  o->tile_coords.assign(tile_lv.size() * 5, 0);
+  for (size_t t = 0; t < tile_lv.size(); ++t) coord(tile_lv[t], &o->tile_coords[t * 5]);
+  o->O = O;
+  o->col_dim = 0;
+  o->ok = true;
+}
+
 // ---------------------------------------------------------------------------
 // GEMM: C[M,N] = A[M,K] B[K,N]   (interp.cpp:109-122)
 
@@ -425,6 +533,18 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
       int64_t lv[2] = {0, c};
       q.col_off.push_back(offset_of(cds, lv));
     }
+    {
+      std::vector<std::array<int64_t, 4>> tl, rr(128);
+      std::vector<bool> ok(128);
+      for (int64_t tm = 0; tm < mtiles; ++tm)
+        for (int64_t tn = 0; tn < ntile_n; ++tn) tl.push_back({tm * 128, tn * BN, 0, 0});
+      for (int r = 0; r < 128; ++r) {
+        rr[r] = {r, 0, 0, 0};
+        ok[r] = r < M;
+      }
+      bool full = M % 128 == 0 && N % BN == 0;
+      if (full) plan_out_store(cds, 2, 1, BN, tl, rr, ok, &q.ost);
+    }
     q.pipe = pick_pipe(q);
     std::ostringstream os;
     os << "gemm BM=128 BN=" << BN << " KC=64 A=" << (q.A.mn_major ? "MN" : "K") << "-major B="
@@ -432,6 +552,7 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     q.summary = os.str();
     q.persistent = s.parallel;
     q.split_pref = s.order;
+    q.tma_store = s.vectorize;
     *out = q;
     return true;
   }
@@ -489,9 +610,8 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
     }
   }
   const int nk = static_cast<int>(xd.size());
-  if (ai1 != nk - 1 || ah.off < 0 || aw.off < 0 || xd[ai1].ext % 16 ||
-      !(ah.off < aw.off && aw.off == nk - 2 && ah.off == nk - 3)) {
-    *why = "halo path: input brick must end [H off][W off][i_t]";
+  if (ai1 != nk - 1 || ah.off < 0 || aw.off < 0 || xd[ai1].ext % 16 || !(ah.off < aw.off)) {
+    *why = "halo path: input needs H outside W outside an innermost i_t brick";
     return false;
   }
   const int64_t i_t = xd[ai1].ext;
@@ -505,11 +625,6 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
     *why = "halo path: input tiles do not match the output tile";
     return false;
   }
-  for (int k : {ah.tile, aw.tile, an, ai0})
-    if (k >= 0 && k >= ah.off) {
-      *why = "halo path: tile digits must be outside the brick";
-      return false;
-    }
   if (B_w > 128) {
     *why = "halo path: B_w > 128";
     return false;
@@ -575,29 +690,45 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   p.BM = 128;
   p.BN = static_cast<int>(BN);
   p.KC = static_cast<int>(KC);
-  // --- A: {i_t, B_w, B_h, bricks} box {KC, B_w, rows_h, 1}: SMEM rows are
-  // pixels of KC*2 bytes in the K-major swizzled canonical layout (swizzle =
-  // row bytes), so a tap is a start-address shift of (rh*B_w + rw) rows.
-  const int64_t brick = B_h * B_w * i_t;
-  int64_t nbricks = 1;
-  for (int k = 0; k < ah.off; ++k) nbricks *= xd[k].ext;
-  p.A.rank = 4;
-  p.A.dims[0] = i_t;
-  p.A.dims[1] = B_w;
-  p.A.dims[2] = B_h;
-  p.A.dims[3] = nbricks;
-  p.A.strides[0] = 2;
-  p.A.strides[1] = i_t * 2;
-  p.A.strides[2] = B_w * i_t * 2;
-  p.A.strides[3] = brick * 2;
-  p.A.box[0] = static_cast<uint32_t>(KC);
-  p.A.box[1] = static_cast<uint32_t>(B_w);
-  p.A.box[2] = static_cast<uint32_t>(rows_h);
-  p.A.box[3] = 1;
+  // --- A: box {KC of i_t, B_w (W offsets), rows_h (H offsets)} over the
+  // physical digits (other digits box 1, merged into <= 5 TMA dims). SMEM
+  // rows are pixels (h, w) of KC*2 bytes in the K-major swizzled canonical
+  // layout (swizzle = row bytes), so a tap is a start-address shift of
+  // (rh*B_w + rw) rows.
   if (rows_h > 256 || B_w > 256) {
     *why = "halo path: box too large";
     return false;
   }
+  std::vector<VDim> xv;
+  for (int k = 0; k < nk; ++k) {
+    VDim v{xd[k].ext, xd[k].stride, 1, 1};
+    if (k == ai1) v.box = KC;
+    else if (k == aw.off) v.box = B_w;
+    else if (k == ah.off) v.box = rows_h;
+    xv.push_back(v);
+  }
+  std::vector<int> ag;
+  std::vector<int64_t> am;
+  if (!merge_view(xv, &p.A, &ag, &am, why)) {
+    *why = "halo path: " + *why;
+    return false;
+  }
+  // Coordinates of the A box: tile part (n, h0, w0, first H row) and stage
+  // part (channel chunk c0: the i0 brick and the offset inside i_t).
+  auto coord_a = [&](int64_t n, int64_t h0, int64_t w0, int64_t h1s, int64_t c0, bool tile_part,
+                     int32_t* outc) {
+    for (int d = 0; d < 5; ++d) outc[d] = 0;
+    for (int k = 0; k < nk; ++k) {
+      int64_t c = 0;
+      if (k == an) c = tile_part ? n : 0;
+      else if (k == ah.tile) c = tile_part ? h0 : 0;
+      else if (k == aw.tile) c = tile_part ? w0 : 0;
+      else if (k == ah.off) c = tile_part ? h1s : 0;
+      else if (k == ai0) c = tile_part ? 0 : c0 / i_t;
+      else if (k == ai1) c = tile_part ? 0 : c0 % i_t;
+      outc[ag[k]] += static_cast<int32_t>(c * am[k]);
+    }
+  };
   p.A.swizzle = static_cast<int32_t>(KC * 2);
   p.A.mn_major = 0;
   p.A.boxes = 1;
@@ -671,20 +802,6 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   p.a_tap.clear();
   for (int64_t rh = 0; rh < KH; ++rh)
     for (int64_t rw = 0; rw < KW; ++rw) p.a_tap.push_back(static_cast<int32_t>((rh * B_w + rw) * KC * 2));
-  // brick index of (n, h0, w0, i0): row-major over the digits outside the brick
-  auto brick_of = [&](int64_t n, int64_t h0, int64_t w0, int64_t i0) {
-    int64_t b = 0;
-    for (int k = 0; k < ah.off; ++k) {
-      const PDigit& d = xd[k];
-      int64_t v = 0;
-      if (k == an) v = n;
-      else if (k == ai0) v = i0;
-      else if (k == ah.tile) v = h0;
-      else if (k == aw.tile) v = w0;
-      b = b * d.ext + v;
-    }
-    return b;
-  };
   auto wbrick_of = [&](int64_t o, int64_t i) {  // o, i logical; digits outside [KH][KW][i'][o']
     int64_t b = 0;
     for (size_t k = 0; k < kbase; ++k) b = b * kd[k].ext + digit_of(kd[k], kd[k].lj == 0 ? o : i);
@@ -696,6 +813,7 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   };
   const int64_t H0 = Ho / h_t, W0 = Wo / w_t, O0 = O / o_t;
   const int64_t hchunks = (h_t + h_sub - 1) / h_sub, ochunks = o_t / BN;
+  std::vector<std::array<int64_t, 4>> tile_lv;
   for (int64_t n = 0; n < N; ++n)
     for (int64_t h0 = 0; h0 < H0; ++h0)
       for (int64_t w0 = 0; w0 < W0; ++w0)
@@ -705,8 +823,7 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
               TileEntry te;
               std::memset(&te, 0, sizeof(te));
               const int64_t h1s = hc * h_sub;
-              te.ca[0][2] = static_cast<int32_t>(h1s);
-              te.ca[0][3] = static_cast<int32_t>(brick_of(n, h0, w0, 0));
+              coord_a(n, h0, w0, h1s, 0, true, te.ca[0]);
               const int64_t obase = o0 * o_t + oc * BN;
               for (int b = 0; b < p.B.boxes; ++b) {
                 const int64_t o = obase + b * nbw;
@@ -718,6 +835,7 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
                 }
               }
               te.out_base = y_off(n, obase, h0 * h_t + h1s, w0 * w_t);
+              tile_lv.push_back({n, obase, h0 * h_t + h1s, w0 * w_t});
               te.rows = static_cast<int32_t>(std::min<int64_t>(h_sub, h_t - h1s) * B_w);
               te.cols = static_cast<int32_t>(BN);
               te.n_base = static_cast<int32_t>(obase);
@@ -726,8 +844,7 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   for (int64_t c0 = 0; c0 < I; c0 += KC) {
     StageEntry se;
     std::memset(&se, 0, sizeof(se));
-    se.sa[0] = static_cast<int32_t>(c0 % i_t);
-    se.sa[3] = static_cast<int32_t>(brick_of(0, 0, 0, c0 / i_t) - brick_of(0, 0, 0, 0));
+    coord_a(0, 0, 0, 0, c0, false, se.sa);
     if (b_kmajor) {
       se.sb[0] = static_cast<int32_t>(c0 % i2);
       se.sb[4] = static_cast<int32_t>(c0 / i2);
@@ -745,7 +862,28 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
     p.row_off.push_back(hh < h_sub && ww < w_t ? y_off(0, 0, hh, ww) - base0 : -1);
   }
   for (int c = 0; c < BN; ++c) p.col_off.push_back(y_off(0, c, 0, 0) - base0);
+  if (h_t % h_sub == 0) {
+    std::vector<std::array<int64_t, 4>> rr(128);
+    std::vector<bool> ok(128);
+    for (int r = 0; r < 128; ++r) {
+      rr[r] = {0, 0, r / B_w, r % B_w};
+      ok[r] = p.row_off[r] >= 0;
+    }
+    plan_out_store(yd, 4, 1, static_cast<int>(BN), tile_lv, rr, ok, &p.ost);
+  }
+  if (!umma_view_encodable(p.A, why) || !umma_view_encodable(p.B, why)) {
+    *why = "halo path: " + *why;
+    return false;
+  }
   p.pipe = pick_pipe(p);
+  {
+    const int64_t need = 2LL * (p.A.slot_bytes + p.B.boxes * p.B.slot_bytes) + 1024 + 512 +
+                         kEpiSmemBytes + sizeof(StageEntry) * p.stages.size() + 8 * BN + 8 * 128;
+    if (need > 227 * 1024) {
+      *why = "halo path: two stages exceed SMEM";
+      return false;
+    }
+  }
   {
     // Weights resident when the layer has one output-channel tile and all
     // its chunks' slabs fit beside a >= 3-deep input ring.
@@ -761,6 +899,7 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   }
   p.persistent = s.parallel;
   p.split_pref = s.order;
+  p.tma_store = s.vectorize;
   std::ostringstream os;
   os << (p.wres ? "conv-halo-wres" : "conv-halo") << " h_t=" << h_t << " w_t=" << w_t << " o_t=" << o_t << " i_t=" << i_t << " i'=" << i2
      << " o'=" << o2 << " rows=" << h_sub << "x" << B_w << " BN=" << BN << " KC=" << KC
@@ -1003,6 +1142,7 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
     int64_t lv[4] = {n, o, h, w};
     return offset_of(yd, lv);
   };
+  std::vector<std::array<int64_t, 4>> tile_lv;
   for (int64_t n = 0; n < N; ++n)
     for (int64_t h0 = 0; h0 < H0; ++h0)
       for (int64_t w0 = 0; w0 < W0; ++w0)
@@ -1016,6 +1156,7 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
               int64_t obase = o0 * o_t + oc * BN;
               for (int b = 0; b < p.B.boxes; ++b) coord_k(obase + b * nbox, 0, 0, 0, true, te.cb[b]);
               te.out_base = y_off(n, obase, h0 * h_t + h1s, w0 * w_t);
+              tile_lv.push_back({n, obase, h0 * h_t + h1s, w0 * w_t});
               te.rows = static_cast<int32_t>(std::min<int64_t>(h_sub, h_t - h1s) * w_t);
               te.cols = static_cast<int32_t>(BN);
               te.n_base = static_cast<int32_t>(obase);
@@ -1039,9 +1180,20 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
     p.row_off.push_back(y_off(0, 0, hh, ww) - base0);
   }
   for (int c = 0; c < BN; ++c) p.col_off.push_back(y_off(0, c, 0, 0) - base0);
+  if (h_t % h_sub == 0) {
+    std::vector<std::array<int64_t, 4>> rr(128);
+    std::vector<bool> ok(128);
+    for (int r = 0; r < 128; ++r) {
+      const int64_t hh = h_outer ? r / w_t : r % h_sub, ww = h_outer ? r % w_t : r / h_sub;
+      rr[r] = {0, 0, hh, ww};
+      ok[r] = r < h_sub * w_t;
+    }
+    plan_out_store(yd, 4, 1, static_cast<int>(BN), tile_lv, rr, ok, &p.ost);
+  }
   p.pipe = pick_pipe(p);
   p.persistent = s.parallel;
   p.split_pref = s.order;
+  p.tma_store = s.vectorize;
   std::ostringstream os;
   os << "conv h_t=" << h_t << " w_t=" << w_t << " o_t=" << o_t << " i_t=" << i_t << " i'=" << i2
      << " o'=" << o2 << " rows=" << h_sub * w_t << " BN=" << BN << " KC=" << KC

@@ -58,6 +58,54 @@ BERT_GEMMS = [
 ]
 
 
+def bert_chain(layers=12, seq=128, hidden=768, ffn=3072, qkv=2304):
+    """cfg5: the BERT-base encoder GEMM chain at seq 128 as one graph.
+
+    Per layer, on h[seq, hidden]:
+      qkv   = GMM(h, Wqkv) + b          (graph output: the attention core -
+                                          softmax / batched matmul - is not in
+                                          the reference op set, ir.hpp:42)
+      a     = GMM(h, Wo) + bo + h        (attention-output projection with its
+                                          residual; h stands in for the
+                                          attention context)
+      f     = ReLU(GMM(a, W1) + b1)      (GELU -> ReLU: no GELU in the op set)
+      h'    = GMM(f, W2) + b2 + a
+    1.812 GFLOP per layer. Returns (graph, gmm node
+    indices)."""
+    b = Builder()
+    I, C, O = ir.INPUT, ir.CONSTANT, ir.OUTPUT
+    gmms = []
+
+    def mat(tid, m, n, role=ir.INTERMEDIATE):
+        return b.t(tid, [("M", m), ("N", n)], role)
+
+    def linear(name, x, k, n, role_out=ir.INTERMEDIATE):
+        w = b.t(f"{name}_w", [("K", k), ("N", n)], C)
+        bias = b.t(f"{name}_b", [("N", n)], C)
+        y = mat(f"{name}_y", seq, n)
+        b.op(ir.GMM, [x, w], y)
+        gmms.append(len(b.g.nodes) - 1)
+        yb = mat(f"{name}_yb", seq, n, role_out)
+        b.op(ir.BIASADD, [y, bias], yb)
+        return yb
+
+    h = mat("h0", seq, hidden, I)
+    for l in range(layers):
+        last = l == layers - 1
+        linear(f"l{l}_qkv", h, hidden, qkv, O)
+        ao = linear(f"l{l}_ao", h, hidden, hidden)
+        a = b.op(ir.EWADD, [ao, h], mat(f"l{l}_a", seq, hidden))
+        f1 = linear(f"l{l}_f1", a, hidden, ffn)
+        f = b.op(ir.RELU, [f1], mat(f"l{l}_f", seq, ffn))
+        f2 = linear(f"l{l}_f2", f, ffn, hidden)
+        h = b.op(ir.EWADD, [f2, a], mat(f"l{l + 1}_h" if not last else "out", seq, hidden,
+                                       O if last else ir.INTERMEDIATE))
+    return b.g, gmms
+
+
+BERT_FLOPS_PER_LAYER = 2.0 * 128 * (768 * 2304 + 768 * 768 + 768 * 3072 + 3072 * 768)
+
+
 # ---------------------------------------------------------------------------
 # cfg4: ResNet-18 inference graph (BatchNorm folded into the conv bias).
 

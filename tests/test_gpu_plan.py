@@ -208,3 +208,46 @@ def test_measure_reports_device_time():
     c = p.measure(warmup=3, reps=20, flush_l2=True)
     assert c.cost > 0 and c.min_us <= c.cost and c.kernels == 2 and c.tc_nodes == 1
     assert c.flops == 2 * 64 * 64 * 56 * 56 * 9
+
+
+# Epilogue variants of the tcgen05 kernel: the TMA-store epilogue (schedule
+# `vectorize`=1), split-K with the distributed column-slice reduction
+# (`order`), fused bias/ReLU chains, on GEMM and on the halo C2D path.
+@pytest.mark.parametrize("factors,tile,order,vec", [
+    ((128, 64, 256), 64, 1, 1), ((128, 64, 256), 128, 0, 1), ((128, 64, 256), 256, 0, 1),
+    ((256, 128, 128), 128, 2, 0), ((128, 64, 128), 64, 0, 1)])
+def test_umma_gemm_epilogue_variants(factors, tile, order, vec):
+    M = K = N = 512
+    g = ir.gmm_chain(M, K, N)
+    seqs = runtime.decode_layout(g, 0, list(factors))
+    seqs["biased"] = seqs["c"]
+    seqs["y"] = seqs["c"]
+    inputs, ref = oracle_outputs(g, 11)
+    p = runtime.Plan(g, seqs, [runtime.sched(0, tile_last=tile, order=order, vectorize=vec, fuse=1)],
+                     flags=_abi.PLAN_REQUIRE_TC)
+    k = p.node_kernel(0)
+    assert k.startswith("umma_gemm"), k
+    if vec:
+        assert "store=2" in k, k
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    got = p.get_output("y")
+    assert np.array_equal(got, ref["y"]), np.abs(got - ref["y"]).max()
+
+
+@pytest.mark.parametrize("f,vec", [((8, 14, 64, 32, 32, 64), 1), ((7, 14, 32, 32, 32, 32), 1),
+                                   ((14, 14, 64, 64, 64, 64), 0)])
+def test_halo_conv_tma_store(f, vec):
+    n, c, h = (1, 64, 56) if f[0] != 14 else (1, 256, 14)
+    g = ir.pad_conv(n, c, 64 if c == 64 else c, h, 3, 1, 1)
+    seqs = runtime.decode_layout(g, 1, list(f))
+    inputs, ref = oracle_outputs(g, 5)
+    p = runtime.Plan(g, seqs, [runtime.sched(1, vectorize=vec)], flags=_abi.PLAN_REQUIRE_TC)
+    k = p.node_kernel(1)
+    assert "conv-halo" in k, k
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    got = p.get_output("y")
+    assert np.array_equal(got, ref["y"]), np.abs(got - ref["y"]).max()

@@ -6,7 +6,9 @@ from paper_2210_12415_b200 import _abi, ir, runtime, tuner
 for (nb, ci, co, h, f) in [(1, 64, 64, 56, (7, 14, 32, 32, 32, 32)), (1, 64, 64, 56, (8, 14, 64, 32, 32, 64)),
                           (1, 64, 64, 56, (4, 14, 64, 32, 32, 64)), (2, 128, 128, 28, (4, 14, 64, 64, 64, 64)),
                           (1, 64, 128, 28, (14, 14, 128, 32, 32, 128)), (2, 64, 64, 56, (8, 28, 64, 32, 32, 64)),
-                          (1, 32, 64, 14, (14, 14, 64, 16, 16, 32))]:
+                          (1, 32, 64, 14, (14, 14, 64, 16, 16, 32)), (1, 256, 256, 14, (14, 14, 64, 64, 64, 64)),
+                          (2, 256, 256, 14, (14, 7, 128, 64, 64, 128)), (1, 512, 512, 7, (7, 7, 64, 64, 64, 64)),
+                          (1, 128, 128, 28, (28, 28, 32, 64, 64, 32))]:
     g = ir.pad_conv(nb, ci, co, h, 3, 1, 1)
     seqs = runtime.decode_layout(g, 1, list(f))
     bufs = O.random_inputs(g, 42)

@@ -23,7 +23,7 @@ def timeline(g, cand, inputs, name):
         p.set_input_device(k, v)
     p.run()
     torch.cuda.synchronize()
-    buf = torch.zeros(24 * 4096, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(32 * 4096, dtype=torch.int64, device="cuda")
     runtime.lib().lfgpu_debug_umma_trace(C.c_void_p(buf.data_ptr()))
     p2 = runtime.Plan(g, tuner.seqs_for(g, cand), cand.scheds, _abi.PLAN_REQUIRE_TC)
     for k, v in inputs.items():
@@ -38,8 +38,10 @@ def timeline(g, cand, inputs, name):
     torch.cuda.synchronize()
     runtime.lib().lfgpu_debug_umma_trace(None)
     allb = buf.cpu().numpy().astype(np.int64)
-    nct = int((allb.reshape(-1, 24)[:, 0] != 0).sum())
-    t16 = allb[: 24 * nct].reshape(-1, 24)
+    nct = int((allb.reshape(-1, 32)[:, 0] != 0).sum())
+    t16 = allb[: 32 * nct].reshape(-1, 32)
+    ck = [(np.median(t16[:, 20 + k] - t16[:, 0]) / 1000.0) for k in range(8) if (t16[:, 20 + k] > 0).all()]
+    print("  unit-0 chunk ends (us):", " ".join(f"{v:.2f}" for v in ck))
     if (t16[:, 16] > 0).all():
         sp = (t16[:, 16:20] - t16[:, :1]) / 1000.0
         print("  split-K: published %.2f fenced %.2f spin-done %.2f slices-landed %.2f us" %
@@ -128,7 +130,7 @@ if __name__ == "__main__":
         sys.exit(0)
     g = ir.gemm(1024, 1024, 1024)
     A, B = k64((1024, 1024)), k64((1024, 1024))
-    for f, tl, o in [((256, 1024, 256), 64, 1), ((128, 64, 256), 128, 0), ((128, 64, 256), 256, 0)]:
+    for f, tl, o in [((256, 1024, 256), 64, 1), ((128, 64, 256), 128, 0)]:
         timeline(g, tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tl, order=o)]), {"a": A, "b": B},
                  f"gemm {f} tile {tl} order {o}")
     if os.environ.get("TRACE_GEMM_ONLY"):
