@@ -353,6 +353,47 @@ def run_ours(args, rank, world, local):
         "bytes": byts, "us": round(statistics.median(tt) * 1e3, 2), "GB_per_s": round(gbs, 1),
         "frac_of_hbm": round(gbs / pk["hbm_gbs"], 4)}
 
+    # ---- 4b. end-to-end graphs: cfg4 ResNet-18 b1 (tuned per-conv layouts,
+    # fused epilogues, whole-graph CUDA graph) and cfg5 BERT-base GEMM chain
+    # (seq 128, 12 layers); device time per inference step, L2 flushed.
+    if not args.no_e2e_graphs:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bert_run
+        import resnet18_run
+        from paper_2210_12415_b200 import workloads
+        try:
+            t0 = time.perf_counter()
+            fac = workloads.tune_resnet18(1, lambda sub: resnet18_run.make_inputs(sub, gen), ctx=ctx)
+            tune_s = time.perf_counter() - t0
+            g18, _, p18 = resnet18_run.build(1, fac, ctx=ctx)
+            for k, x in resnet18_run.make_inputs(g18, gen).items():
+                p18.set_input_device(k, x)
+            m18 = p18.measure(warmup=5, reps=30, flush_l2=True)
+            kinds = [p18.node_kernel(i) for i in range(len(g18.nodes))]
+            sec["resnet18_b1_inference"] = {
+                "latency_us": round(m18.cost, 2), "launches": int(m18.kernels),
+                "tflops": round(3.628e9 / (m18.cost * 1e-6) / 1e12, 3),
+                "tc_convs": sum(k.startswith("umma") for k in kinds), "tuning_s": round(tune_s, 1)}
+            p18.close()
+        except Exception as e:  # reported, not hidden
+            sec["resnet18_b1_inference"] = {"error": str(e)[:200]}
+        try:
+            best = None
+            for t in (64, 128):
+                gb, _, pb = bert_run.build(12, t, 0, ctx=ctx)
+                for k, x in bert_run.make_inputs(gb, gen).items():
+                    pb.set_input_device(k, x)
+                mb = pb.measure(warmup=5, reps=30, flush_l2=True)
+                if best is None or mb.cost < best[0]:
+                    best = (mb.cost, t, int(mb.kernels))
+                pb.close()
+            fl = workloads.BERT_FLOPS_PER_LAYER * 12
+            sec["bert_base_gemm_chain_seq128_12l"] = {
+                "latency_us": round(best[0], 2), "brick_t": best[1], "launches": best[2],
+                "tflops": round(fl / (best[0] * 1e-6) / 1e12, 2)}
+        except Exception as e:
+            sec["bert_base_gemm_chain_seq128_12l"] = {"error": str(e)[:200]}
+
     # ---- 5. cpu baseline (rank 0, N=1): the reference's GEMM on a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -471,6 +512,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e-graphs", action="store_true", help="skip ResNet-18 / BERT secondaries")
     ap.add_argument("--cpu-rows", type=int, default=192)
     ap.add_argument("--ref-rows", type=int, default=16)
     args = ap.parse_args()
