@@ -1050,6 +1050,10 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     --L.pipe;
   }
   if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "tcgen05 kernel SMEM exceeds 227 KB");
+  // One CTA per SM: the kernel's register budget (launch bounds 1, ~230
+  // registers) leaves no room for a second; measured 2-per-SM variants
+  // (launch bounds 2, <= 128 registers, <= 113 KB SMEM) were not faster.
+  L.per_sm = 1;
   L.nprod = std::max(1, std::min(3, L.pipe - 1));
   L.ntaps = p.ntaps;
   L.b_tap = p.b_tap;
@@ -1066,7 +1070,14 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     L.counters = static_cast<int*>(t->p[5]);
   }
   // Persistent grid: one CTA per SM at most, units dealt round-robin.
-  L.grid = std::min(L.ntiles * L.splits, sms / L.splits * L.splits);
+  {
+    // Fill both resident slots only when there is more than one wave of
+    // units (then one CTA's epilogue overlaps the other's main loop).
+    const char* e = getenv("LFGPU_GRID_PER_SM");  // diagnostics override
+    int per = L.ntiles * L.splits > sms ? L.per_sm : 1;
+    if (e) per = std::max(1, std::min(atoi(e), L.per_sm));
+    L.grid = std::min(L.ntiles * L.splits, per * sms / L.splits * L.splits);
+  }
   static_assert(sizeof(TileEntry) == 192, "TileEntry layout");
   return L;
 }

@@ -131,6 +131,7 @@ struct UmmaLaunch {
   void* out_bf16 = nullptr;
   size_t smem = 0;
   int grid = 0;
+  int per_sm = 1;  // CTAs that fit on one SM (SMEM / TMEM)
   int ring_bytes = 0;
   int table_ints = 0;            // [stages | col_off | row_off] int32 count
   int ntaps = 1, b_tap = 0;
