@@ -56,6 +56,7 @@ struct UmmaParams {
   // follow row_off in the SMEM table.
   int32_t stg_off, stg_f32, stg_bf;
   const int32_t* tile_coords;
+  ScatterDesc sc;           // Padding absorbed into this epilogue (sc.enabled)
   int32_t a_tap[kMaxTaps];
   int32_t store_mode;       // 1: row-contiguous, 16-byte aligned output rows; 0: generic
   int64_t col0;             // col_off[0] folded into the tile base in store mode 1
@@ -278,6 +279,28 @@ __device__ __forceinline__ void split_sum(const UmmaParams& P, float* v, const f
     }
 }
 
+// The absorbed Padding: 4 consecutive channels of output pixel (n, h, w)
+// into every copy of (h+pad, w+pad) in the consumer's (unfolded) bf16 layout.
+__device__ __forceinline__ void scatter4(const ScatterDesc& sc, int n, int c, int h, int w,
+                                         float4 x) {
+  const int hp = h + sc.pad, wp = w + sc.pad;
+  const int64_t base = n * sc.sN + (c / sc.ic) * sc.sC0 + (c % sc.ic);
+  __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(x.z, x.w);
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<uint32_t*>(&hi);
+  const int th0 = max(0, (hp - sc.Bh + sc.Sh) / sc.Sh), th1 = min(sc.Th - 1, hp / sc.Sh);
+  const int tw0 = max(0, (wp - sc.Bw + sc.Sw) / sc.Sw), tw1 = min(sc.Tw - 1, wp / sc.Sw);
+  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(sc.dst);
+  for (int th = th0; th <= th1; ++th)
+    for (int tw = tw0; tw <= tw1; ++tw) {
+      const int64_t off = base + th * sc.sHt + static_cast<int64_t>(hp - th * sc.Sh) * sc.sHo +
+                          tw * sc.sWt + static_cast<int64_t>(wp - tw * sc.Sw) * sc.sWo;
+      *reinterpret_cast<uint2*>(dst + off) = pk;
+    }
+}
+
 // One W-column chunk of one unit's accumulator for the calling thread's row.
 // mode 3 publishes a split-K partial; otherwise (after the split-K sum when
 // splits > 1) the chunk goes through the per-warp SMEM buffer and is stored
@@ -290,7 +313,8 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
                                        int n_base, int64_t obase, const int64_t* s_row,
                                        const int64_t* s_col, int mode, int split, int splits,
                                        int64_t ws_tile, const float4* red, int red_lo,
-                                       bool release, uint32_t tempty) {
+                                       bool release, uint32_t tempty, int3 org,
+                                       const int32_t* s_rowrel) {
   float v[W];
   tmem_ld<W>(taddr + c0, v);
 
@@ -377,6 +401,14 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
 #pragma unroll
     for (int it = 0; it < IT; ++it)
       if (ok[it]) *reinterpret_cast<float4*>(P.out + addr[it]) = x[it];
+    if (P.sc.enabled) {
+#pragma unroll 1
+      for (int it = 0; it < IT; ++it)
+        if (ok[it]) {
+          const int rel = s_rowrel[q * 32 + it * RPI + lane / LPR];
+          scatter4(P.sc, org.x, n_base + c, org.y + (rel >> 16), org.z + (rel & 0xFFFF), x[it]);
+        }
+    }
     if (P.out_bf16) {  // the tensor-core consumers' bf16 copy, same layout
 #pragma unroll
       for (int it = 0; it < IT; ++it)
@@ -421,6 +453,12 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
           P.out[a[j]] = y[j];
           if (P.out_bf16) P.out_bf16[a[j]] = __float2bfloat16_rn(y[j]);
         }
+      if (P.sc.enabled && c0 + j0 + 8 <= cols) {
+        const int rel = s_rowrel[row];
+        const int hh = org.y + (rel >> 16), ww = org.z + (rel & 0xFFFF);
+        scatter4(P.sc, org.x, n_base + c0 + j0, hh, ww, make_float4(y[0], y[1], y[2], y[3]));
+        scatter4(P.sc, org.x, n_base + c0 + j0 + 4, hh, ww, make_float4(y[4], y[5], y[6], y[7]));
+      }
     }
   }
 }
@@ -455,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int64_t* s_col = reinterpret_cast<int64_t*>(s_stage + P.nstages);
   int64_t* s_row = s_col + P.BN;
   const int32_t* s_rowpos = reinterpret_cast<const int32_t*>(s_row + 128);  // store mode 2
+  const int32_t* s_rowrel = s_rowpos + 128;                                   // C2D: (dh << 16) | dw
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int splits = P.splits;
@@ -645,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // waiting so its (possibly DRAM) latency hides under the main loop.
       const TileEntry* te = P.tiles + tile;
       const int rows = __ldg(&te->rows), cols = __ldg(&te->cols), n_base = __ldg(&te->n_base);
+      const int3 org = make_int3(__ldg(&te->org[0]), __ldg(&te->org[1]), __ldg(&te->org[2]));
       const int64_t obase = __ldg(&te->out_base) + P.col0;
       mbar_wait(tfull0 + 8 * b, static_cast<uint32_t>(i >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -769,7 +809,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++stg_count;
         } else {
           epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col,
-                        pub ? 3 : mode, split, splits, ws_tile, s_red, red_lo, it == nitems - 1, tempty);
+                        pub ? 3 : mode, split, splits, ws_tile, s_red, red_lo, it == nitems - 1, tempty,
+                        org, s_rowrel);
         }
         if (dbg && i == 0 && it < 8 && threadIdx.x == kEpiWarp0 * 32) dbg[20 + it] = gtimer();
       }
@@ -929,7 +970,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   auto t = std::make_shared<Tables>();
   t->p[0] = up(p.tiles);
   {  // [stages | col_off | row_off] contiguous: the kernel copies it to SMEM in one pass
-    std::vector<int32_t> tab(p.stages.size() * sizeof(StageEntry) / 4 + 2 * (p.col_off.size() + 128) + 128);
+    std::vector<int32_t> tab(p.stages.size() * sizeof(StageEntry) / 4 + 2 * (p.col_off.size() + 128) + 256);
     size_t o = 0;
     std::memcpy(tab.data(), p.stages.data(), p.stages.size() * sizeof(StageEntry));
     o += p.stages.size() * sizeof(StageEntry) / 4;
@@ -940,6 +981,8 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     std::memcpy(tab.data() + o, rows.data(), 128 * 8);
     o += 256;
     for (int r = 0; r < 128; ++r) tab[o + r] = p.ost.ok ? p.ost.row_pos[r] : -1;
+    o += 128;
+    for (int r = 0; r < 128; ++r) tab[o + r] = r < static_cast<int>(p.row_rel.size()) ? p.row_rel[r] : 0;
     L.table_ints = static_cast<int>(tab.size());
     t->p[1] = up(tab);
   }
@@ -1017,7 +1060,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     if (te.cols != p.BN) full_cols = false;
   const char* sm_env = getenv("LFGPU_STORE_MODE");
   const bool want_tma = (p.tma_store && !(sm_env && atoi(sm_env) < 2)) || (sm_env && atoi(sm_env) == 2);
-  if (p.ost.ok && cols_unit && full_cols && want_tma) {
+  if (p.ost.ok && cols_unit && full_cols && want_tma && !p.scatter.enabled) {
     L.store_mode = 2;
     L.col0 = p.col_off[0];
     L.tma_o = encode(p.ost.O, p.out);
@@ -1045,7 +1088,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     L.ring_bytes = static_cast<int>((ring + 1023) / 1024 * 1024);
     L.smem = 1024 + L.ring_bytes + wbytes + kEpiSmemBytes + 2 * (L.stg_f32 + L.stg_bf) + L.red_bytes +
              8 * (2 * L.pipe + 5 + (p.wres ? p.stages.size() : 0)) + 8 +
-             sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 4 * 128 + 64;
+             sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 8 * 128 + 64;
     if (L.smem <= 227 * 1024 || L.pipe <= 2) break;
     --L.pipe;
   }
@@ -1056,6 +1099,9 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   L.per_sm = 1;
   L.nprod = std::max(1, std::min(3, L.pipe - 1));
   L.ntaps = p.ntaps;
+  L.scatter = p.scatter;
+  if (L.scatter.enabled && (L.scatter.ic % 4 || p.BN % 8))
+    fail(LFGPU_EINVAL, "umma: absorbed Padding needs 4-aligned channel bricks");
   L.b_tap = p.b_tap;
   if (p.ntaps > kMaxTaps || static_cast<int>(p.a_tap.size()) < p.ntaps)
     fail(LFGPU_EINVAL, "umma: tap table");
@@ -1117,6 +1163,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.stg_off = L.ring_bytes + (L.wres ? L.nstages * L.w_chunk : 0) + kEpiSmemBytes;
   P.stg_bf = L.stg_bf;
   P.tile_coords = static_cast<const int32_t*>(L.d_tcoords);
+  P.sc = L.scatter;
 
   P.a_desc = L.a_desc;
   P.b_desc = L.b_desc;

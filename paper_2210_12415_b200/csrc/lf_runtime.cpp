@@ -406,6 +406,41 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
     umma[ni] = up;
   }
 
+  // 1b. Padding absorbed into the producing C2D's epilogue: when a Padding's
+  // input is the final tensor of a tcgen05 C2D (after its fused chain) and
+  // the padded tensor feeds only tensor-core contractions, the producer
+  // writes the padded (possibly unfolded) bf16 layout itself and the
+  // Padding step disappears (the paper's "producer yields the consumer's
+  // layout"; lower.cpp:228-238).
+  std::map<int, int> absorbed_pad;  // umma node -> Padding node it absorbs
+  if (!(P->flags & (LFGPU_PLAN_KEEP_ALL | LFGPU_PLAN_EXACT)) && !getenv("LFGPU_NO_PAD_ABSORB")) {
+    for (int pn : P->order) {
+      const auto& pnode = P->nodes[pn];
+      if (pnode.kind != LFGPU_OP_PADDING) continue;
+      const int tin = pnode.inputs[0];
+      int u = P->t[tin].producer;
+      while (u >= 0 && fused_away.count(u)) u = P->t[P->nodes[u].inputs[0]].producer;
+      if (u < 0 || !umma.count(u) || P->nodes[u].kind != LFGPU_OP_C2D || absorbed_pad.count(u))
+        continue;
+      const UmmaPlan& up = umma[u];
+      const int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : P->nodes[u].output;
+      if (final_t != tin) continue;
+      const PTensor& xp = P->t[pnode.output];
+      bool all_tc = !xp.consumers.empty() && xp.role != LFGPU_ROLE_OUTPUT;
+      for (int c : xp.consumers)
+        if (!umma.count(c)) all_tc = false;
+      if (!all_tc) continue;
+      ScatterDesc sd;
+      std::string why;
+      if (!umma_scatter_desc(xp.logical, xp.seq, pnode.pad, &sd, &why) || sd.sC1 != 1 || sd.ic % 4 ||
+          up.BN % 8)
+        continue;
+      umma[u].scatter = sd;
+      absorbed_pad[u] = pn;
+      fused_away.insert(pn);
+    }
+  }
+
   // 2. Storage decisions: bf16 for tensor-core operands, f32/i32 otherwise.
   for (auto& t : P->t) {
     for (int c : t.consumers) {
@@ -439,6 +474,12 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
       t.d_bf16 = P->keep.back()->p;
     }
     if (!t.d) t.elem = LFGPU_ELEM_BF16;  // bf16-only storage
+  }
+  for (auto& kv : absorbed_pad) {
+    PTensor& xp = P->t[P->nodes[kv.second].output];
+    if (!xp.d_bf16 || xp.d) fail(LFGPU_EINVAL, "absorbed Padding output must be bf16-only");
+    CUDA_OK(cudaMemset(xp.d_bf16, 0, 2 * xp.numel));  // the pad ring, never written
+    umma[kv.first].scatter.dst = xp.d_bf16;
   }
   int* d_err = P->ctx->d_err;
 

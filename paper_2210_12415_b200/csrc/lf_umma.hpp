@@ -56,13 +56,35 @@ struct OperandView {
   uint32_t k_adv = 0;     // descriptor start-address advance per UMMA K=16 step
 };
 
+// A Padding absorbed into the producing C2D's epilogue (the producer writes
+// the consumer's padded, possibly unfolded layout directly; PAPER.md:379-381,
+// lower.cpp:228-238). Output element (n, c, h, w) lands at every physical
+// position of the bf16 destination whose logical coordinate is
+// (n, c, h+pad, w+pad): per unfolded dim the tiles t with
+// t*S <= x < t*S + B (exact tilings only), offset
+// n*sN + (c/ic)*sC0 + (c%ic)*sC1 + t_h*sHt + (x_h - t_h*S_h)*sHo + (same for W).
+// The pad ring is zeroed once at plan build and never written.
+struct ScatterDesc {
+  int32_t enabled = 0;
+  int32_t pad = 0;
+  int32_t ic = 1;           // channel brick (c % ic inner)
+  int32_t Th = 1, Bh = 1, Sh = 1 << 30, Tw = 1, Bw = 1, Sw = 1 << 30;
+  int64_t sN = 0, sC0 = 0, sC1 = 0, sHt = 0, sHo = 0, sWt = 0, sWo = 0;
+  void* dst = nullptr;      // bf16 buffer of the padded tensor
+};
+
+// Descriptor of a Padding(pad) output layout for the epilogue scatter; false
+// when the layout is not a separable (N, C, H, W) brick form.
+bool umma_scatter_desc(const std::vector<Dim>& xp_log, const Seq& xp_seq, int64_t pad,
+                       ScatterDesc* sd, std::string* why);
+
 struct TileEntry {  // 192 bytes
   int32_t ca[kMaxBoxes][5];
   int32_t cb[kMaxBoxes][5];
   int64_t out_base;
   int32_t rows, cols;
   int32_t n_base;
-  int32_t pad[3];
+  int32_t org[3];  // C2D: logical (n, h, w) of the tile origin (epilogue scatter)
 };
 
 struct StageEntry {  // 40 bytes
@@ -99,6 +121,8 @@ struct UmmaPlan {
   int wres = 0;          // halo C2D: weights resident in SMEM (one output-channel tile)
   OutStore ost;          // TMA-store epilogue, when the output tile is a TMA box
   int tma_store = 0;     // schedule `vectorize`: use the TMA-store epilogue when legal
+  std::vector<int32_t> row_rel;  // C2D: (dh << 16) | dw of accumulator row r from the tile origin
+  ScatterDesc scatter;   // Padding absorbed into this epilogue (runtime fills it)
   OperandView A, B;
   std::vector<TileEntry> tiles;
   std::vector<StageEntry> stages;
@@ -139,6 +163,7 @@ struct UmmaLaunch {
   CUtensorMap tma_o, tma_ob;     // store mode 2: fp32 output and its bf16 copy
   int stg_off = 0, stg_f32 = 0, stg_bf = 0;
   void* d_tcoords = nullptr;
+  ScatterDesc scatter;
   int red_bytes = 0;
   int32_t a_tap[kMaxTaps] = {};
   int store_mode = 0;           // 1: transposed float4 row stores; 0: generic

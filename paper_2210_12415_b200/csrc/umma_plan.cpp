@@ -836,6 +836,9 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
               }
               te.out_base = y_off(n, obase, h0 * h_t + h1s, w0 * w_t);
               tile_lv.push_back({n, obase, h0 * h_t + h1s, w0 * w_t});
+              te.org[0] = static_cast<int32_t>(n);
+              te.org[1] = static_cast<int32_t>(h0 * h_t + h1s);
+              te.org[2] = static_cast<int32_t>(w0 * w_t);
               te.rows = static_cast<int32_t>(std::min<int64_t>(h_sub, h_t - h1s) * B_w);
               te.cols = static_cast<int32_t>(BN);
               te.n_base = static_cast<int32_t>(obase);
@@ -860,6 +863,7 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   for (int r = 0; r < 128; ++r) {
     const int64_t hh = r / B_w, ww = r % B_w;
     p.row_off.push_back(hh < h_sub && ww < w_t ? y_off(0, 0, hh, ww) - base0 : -1);
+    p.row_rel.push_back(static_cast<int32_t>((hh << 16) | ww));
   }
   for (int c = 0; c < BN; ++c) p.col_off.push_back(y_off(0, c, 0, 0) - base0);
   if (h_t % h_sub == 0) {
@@ -1157,6 +1161,9 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
               for (int b = 0; b < p.B.boxes; ++b) coord_k(obase + b * nbox, 0, 0, 0, true, te.cb[b]);
               te.out_base = y_off(n, obase, h0 * h_t + h1s, w0 * w_t);
               tile_lv.push_back({n, obase, h0 * h_t + h1s, w0 * w_t});
+              te.org[0] = static_cast<int32_t>(n);
+              te.org[1] = static_cast<int32_t>(h0 * h_t + h1s);
+              te.org[2] = static_cast<int32_t>(w0 * w_t);
               te.rows = static_cast<int32_t>(std::min<int64_t>(h_sub, h_t - h1s) * w_t);
               te.cols = static_cast<int32_t>(BN);
               te.n_base = static_cast<int32_t>(obase);
@@ -1178,6 +1185,7 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
     int64_t ww = h_outer ? r % w_t : r / h_sub;
     if (hh >= h_sub || ww >= w_t) hh = 0, ww = 0;
     p.row_off.push_back(y_off(0, 0, hh, ww) - base0);
+    p.row_rel.push_back(static_cast<int32_t>((hh << 16) | ww));
   }
   for (int c = 0; c < BN; ++c) p.col_off.push_back(y_off(0, c, 0, 0) - base0);
   if (h_t % h_sub == 0) {
@@ -1201,6 +1209,67 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
      << " (halo: " << halo_why << ")";
   p.summary = os.str();
   *out = p;
+  return true;
+}
+
+bool umma_scatter_desc(const std::vector<Dim>& xp_log, const Seq& xp_seq, int64_t pad,
+                       ScatterDesc* sd, std::string* why) {
+  std::vector<PDigit> ds;
+  if (xp_log.size() != 4 || !analyze(xp_log, xp_seq, &ds)) {
+    *why = "padded layout is not a brick layout";
+    return false;
+  }
+  ScatterDesc d;
+  d.pad = static_cast<int32_t>(pad);
+  int nN = 0, nC = 0;
+  for (const auto& g : ds) {
+    switch (g.lj) {
+      case 0:
+        if (g.kind != DG_PART || g.div != 1) return *why = "N split", false;
+        d.sN = g.stride;
+        ++nN;
+        break;
+      case 1:
+        if (g.kind != DG_PART) return *why = "C unfolded", false;
+        if (g.div == 1) {
+          d.sC1 = g.stride;
+          d.ic = static_cast<int32_t>(g.ext);
+        } else {
+          d.sC0 = g.stride;
+        }
+        ++nC;
+        break;
+      default: {
+        const bool h = g.lj == 2;
+        const int64_t D = xp_log[g.lj].extent;
+        if (g.kind == DG_PART) {
+          if (g.div != 1 || g.ext != D) return *why = "H/W split without unfold", false;
+          (h ? d.sHo : d.sWo) = g.stride;
+        } else if (g.kind == DG_TILE) {
+          (h ? d.sHt : d.sWt) = g.stride;
+          (h ? d.Th : d.Tw) = static_cast<int32_t>(g.ext);
+          (h ? d.Sh : d.Sw) = static_cast<int32_t>(g.S);
+        } else {
+          (h ? d.sHo : d.sWo) = g.stride;
+          (h ? d.Bh : d.Bw) = static_cast<int32_t>(g.ext);
+        }
+      }
+    }
+  }
+  if (nN != 1 || nC < 1 || nC > 2) return *why = "N/C digits", false;
+  if (nC == 1 && d.sC1 == 0) return *why = "C digit", false;
+  // Exact unfold tilings only (no clamped overhang duplicates).
+  for (int k = 0; k < 2; ++k) {
+    const int64_t D = xp_log[2 + k].extent;
+    const int64_t T = k ? d.Tw : d.Th, B = k ? d.Bw : d.Bh, S = k ? d.Sw : d.Sh;
+    if (T > 1 && (T - 1) * S + B != D) return *why = "unfold with overhang", false;
+    if (T == 1 && B == 1) {  // whole dim: one 'tile' covering it
+      if (k) d.Bw = static_cast<int32_t>(D);
+      else d.Bh = static_cast<int32_t>(D);
+    }
+  }
+  d.enabled = 1;
+  *sd = d;
   return true;
 }
 

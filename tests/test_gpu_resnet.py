@@ -179,3 +179,64 @@ def test_resnet18_b1_logits():
     ex = R.reference(g, ins)["logits"]
     assert R.max_rel(out, emu) <= 1e-4
     assert R.max_rel(out, ex) <= 2e-3
+
+
+def _two_conv_graph(n=1, c=64, h=56):
+    """conv -> BiasAdd -> ReLU -> Padding -> conv: the edge a ResNet basic
+    block has between its two 3x3 convs."""
+    b = workloads.Builder()
+    nchw = lambda tid, cc, hh, role=ir.INTERMEDIATE: b.t(tid, [("N", n), ("C", cc), ("H", hh), ("W", hh)], role)
+    x = nchw("x", c, h, ir.INPUT)
+    xp = nchw("xp", c, h + 2)
+    b.op(ir.PADDING, [x], xp, pad=1)
+    w1 = b.t("w1", [("O", c), ("I", c), ("KH", 3), ("KW", 3)], ir.CONSTANT)
+    b1 = b.t("b1", [("O", c)], ir.CONSTANT)
+    y1 = nchw("y1", c, h)
+    b.op(ir.C2D, [xp, w1], y1, stride=1)
+    yb = nchw("yb", c, h)
+    b.op(ir.BIASADD, [y1, b1], yb)
+    yr = nchw("yr", c, h)
+    b.op(ir.RELU, [yb], yr)
+    yp = nchw("yp", c, h + 2)
+    b.op(ir.PADDING, [yr], yp, pad=1)
+    w2 = b.t("w2", [("O", c), ("I", c), ("KH", 3), ("KW", 3)], ir.CONSTANT)
+    y2 = nchw("y2", c, h, ir.OUTPUT)
+    b.op(ir.C2D, [yp, w2], y2, stride=1)
+    return b.g
+
+
+@pytest.mark.parametrize("f1,f2", [((8, 14, 64, 32, 32, 64), (8, 14, 64, 32, 32, 64)),
+                                   ((7, 14, 32, 32, 32, 32), (4, 28, 64, 32, 32, 64)),
+                                   ((14, 14, 64, 16, 16, 64), (8, 8, 32, 32, 32, 32))])
+def test_padding_absorbed_into_producer_epilogue(f1, f2, monkeypatch):
+    """The Padding between two tensor-core convs is written by the first
+    conv's epilogue straight into the second conv's padded, unfolded bf16
+    layout (no conversion kernel), bit-identical to the separate K2 step."""
+    g = _two_conv_graph()
+    seqs = {}
+    seqs.update(runtime.decode_layout(g, 1, list(f1)))
+    seqs.update(runtime.decode_layout(g, 5, list(f2)))
+    seqs = workloads.propagate_elementwise(g, seqs)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    ins = {"x": R.k64((1, 64, 56, 56), gen), "w1": R.k64((64, 64, 3, 3), gen, 1 / 8),
+           "b1": R.k64((64,), gen, 1 / 8), "w2": R.k64((64, 64, 3, 3), gen, 1 / 8)}
+    outs = []
+    for absorb in (True, False):
+        if absorb:
+            monkeypatch.delenv("LFGPU_NO_PAD_ABSORB", raising=False)
+        else:
+            monkeypatch.setenv("LFGPU_NO_PAD_ABSORB", "1")
+        p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=1), runtime.sched(5)], _abi.PLAN_REQUIRE_TC)
+        kinds = [p.node_kernel(i) for i in range(len(g.nodes))]
+        assert (kinds[4] == "fused") == absorb, kinds
+        for k, v in ins.items():
+            p.set_input_device(k, v)
+        p.run()
+        outs.append(p.get_output("y2"))
+    assert np.array_equal(outs[0], outs[1])
+    ref = torch.nn.functional.conv2d(
+        torch.relu(torch.nn.functional.conv2d(ins["x"].double(), ins["w1"].double(), padding=1)
+                   + ins["b1"].double().view(1, -1, 1, 1)).bfloat16().double(),
+        ins["w2"].double(), padding=1).flatten().cpu().numpy()
+    assert np.max(np.abs(outs[0] - ref) / np.maximum(1, np.abs(ref))) < 1e-4
