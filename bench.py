@@ -377,6 +377,30 @@ def run_ours(args, rank, world, local):
             p18.close()
         except Exception as e:  # reported, not hidden
             sec["resnet18_b1_inference"] = {"error": str(e)[:200]}
+        # cfg4 b64 batch-sharded over the ranks (shard.py): each rank runs
+        # its contiguous shard through its own plan; throughput from the
+        # max-over-ranks step time (the logits gather is outside the step).
+        try:
+            from paper_2210_12415_b200 import shard
+            gb = 64
+            _, nloc = shard.batch_shard(gb, rank, world)
+            t0 = time.perf_counter()
+            facb = workloads.tune_resnet18(nloc, lambda sub: resnet18_run.make_inputs(sub, gen), ctx=ctx)
+            tune_b = time.perf_counter() - t0
+            gbb, _, pbb = resnet18_run.build(nloc, facb, ctx=ctx)
+            for k, x in resnet18_run.make_inputs(gbb, gen).items():
+                pbb.set_input_device(k, x)
+            mbb = pbb.measure(warmup=3, reps=20, flush_l2=True)
+            step_us = max_over_ranks(mbb.cost, world)
+            sec["resnet18_b64_batch_sharded"] = {
+                "global_batch": gb, "ranks": world, "per_rank_batch": nloc,
+                "step_us_max_over_ranks": round(step_us, 2),
+                "images_per_s": round(gb / (step_us * 1e-6), 1),
+                "tflops": round(3.628e9 * gb / (step_us * 1e-6) / 1e12, 2),
+                "launches": int(mbb.kernels), "tuning_s": round(tune_b, 1)}
+            pbb.close()
+        except Exception as e:
+            sec["resnet18_b64_batch_sharded"] = {"error": str(e)[:200]}
         try:
             best = None
             for t in (64, 128):
