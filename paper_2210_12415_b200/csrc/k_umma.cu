@@ -1024,8 +1024,11 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   // when the tiles alone leave most of the SMs idle and the K loop is long.
   const int sms = num_sms();
   L.splits = 1;
-  if (p.split_pref != 1 && L.ntiles * 2 <= sms && L.nstages >= 8) {
-    L.splits = std::min({sms / L.ntiles, L.nstages / 4, 8});
+  // A halo C2D stage is KH*KW UMMA groups (heavy), so a split may be a
+  // single stage there; a GEMM / per-tap stage is one K step (>= 4 each).
+  const int min_stages = p.ntaps > 1 ? 1 : 4;
+  if (p.split_pref != 1 && L.ntiles * 2 <= sms && L.nstages >= 2 * min_stages) {
+    L.splits = std::min({sms / L.ntiles, L.nstages / min_stages, 8});
     if (L.splits < 2) L.splits = 1;
   }
   if (p.split_pref == 2) L.splits = std::max(L.splits, std::min(2, L.nstages));
@@ -1089,8 +1092,16 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     L.smem = 1024 + L.ring_bytes + wbytes + kEpiSmemBytes + 2 * (L.stg_f32 + L.stg_bf) + L.red_bytes +
              8 * (2 * L.pipe + 5 + (p.wres ? p.stages.size() : 0)) + 8 +
              sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 8 * 128 + 64;
-    if (L.smem <= 227 * 1024 || L.pipe <= 2) break;
-    --L.pipe;
+    if (L.smem <= 227 * 1024) break;
+    if (L.pipe > 2) {
+      --L.pipe;
+    } else if (L.splits > 1) {  // then give up split-K slices
+      --L.splits;
+      while (L.splits > 1 && ((L.BN % L.splits) || (L.BN / L.splits) % 16)) --L.splits;
+      L.red_bytes = L.splits > 1 ? (L.splits - 1) * 128 * (p.BN / L.splits) * 4 : 0;
+    } else {
+      break;
+    }
   }
   if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "tcgen05 kernel SMEM exceeds 227 KB");
   // One CTA per SM: the kernel's register budget (launch bounds 1, ~230
