@@ -187,13 +187,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
 // tile (per-tile counter) sums the partials in split order (deterministic) and
 // runs the epilogue.
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant, alternating 16-column chunks
 constexpr int kEpiLd = 36;  // per-warp transpose buffer row stride (floats)
 constexpr int kMaxSplits = 4;
-static_assert(kEpiSmemBytes == 4 * 32 * kEpiLd * 4, "epilogue SMEM size");
+static_assert(kEpiSmemBytes == kEpiWarps * 32 * kEpiLd * 4, "epilogue SMEM size");
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// One half of the epilogue (4 warps = the 128 TMEM lanes).
+__device__ __forceinline__ void half_bar(int h) {
+  asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory");
+}
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull0 + 8 * b, 1);
-      mbar_init(tempty0 + 8 * b, 4);  // one arrive per epilogue warp
+      mbar_init(tempty0 + 8 * b, kEpiWarps);  // one arrive per epilogue warp
     }
     for (int c = 0; c < nw; ++c) mbar_init(wfull0 + 8 * c, 1);
     mbar_init(redbar, 1);
@@ -668,13 +673,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (dbg && leader) dbg[4] = gtimer();
   } else if (warp >= kEpiWarp0) {
-    // ---- epilogue (4 warps; warp w reads TMEM lanes 32*(w%4)..+31)
-    const int q = warp & 3;
+    // ---- epilogue (8 warps; warp w reads TMEM lanes 32*(w%4)..+31; the
+    // two halves take alternate 16-column chunks)
+    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
     const int row = q * 32 + lane;
-    float* wbuf = s_epi + q * 32 * kEpiLd;
+    float* wbuf = s_epi + (warp - kEpiWarp0) * 32 * kEpiLd;
+    const bool half_leader = lane == 0 && q == 0;  // TMA-store issuer of this half
     const int BN = P.BN;
     uint32_t red_phase = 0;
-    int stg_count = 0;  // TMA-store chunks issued (staging double buffer)
     int i = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       const int tile = u / splits, split = u - tile * splits;
@@ -694,65 +700,71 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t ws_tile = static_cast<int64_t>(tile) * splits;
       const int red_lo = split * (BN / splits);
       const int mode = P.store_mode;
-      // Columns [a, b) in 32-wide chunks (16-wide tail); `rel` hands the
-      // accumulator back after the last TMEM read.
-      // One loop, one (inlined) chunk body: each SM runs the epilogue only a
-      // few times per launch, so code size is paid in cold instruction
-      // fetches. Items are 16-column chunks: first (split-K only) the
-      // columns the sibling splits reduce, published to the workspace; then
-      // this unit's own columns [lo, hi), summed over the splits in split
-      // order (own partial from TMEM) and stored with the fused chain.
+      // Items are 16-column chunks (one small inlined body: each SM runs the
+      // epilogue only a few times per launch, so code size is paid in cold
+      // instruction fetches): first (split-K only) the columns the sibling
+      // splits reduce, published to the workspace; then this unit's own
+      // columns [lo, hi), summed over the splits in split order (own partial
+      // from TMEM) and stored with the fused chain.
       //   Split-K: split s reduces columns [s*BN/S, (s+1)*BN/S). The
       // siblings meet at a per-tile counter (they are co-resident: the grid
       // is a multiple of S and units are dealt in rounds), then bulk-copy
       // the siblings' slices of the reduced columns into SMEM.
-      const int sl = BN / splits, lo = split * sl, hi = lo + sl;
-      const int npub = (BN - sl) / 16, nitems = npub + sl / 16;
-      for (int it = 0; it < nitems; ++it) {
-        if (it == npub && splits > 1) {
-          if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[16] = gtimer();
-          __threadfence();
-          epi_bar();
-          if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[17] = gtimer();
-          if (threadIdx.x == kEpiWarp0 * 32) {
-            atomicAdd(P.counters + tile, 1);
-            int seen;
-            do {
-              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(P.counters + tile) : "memory");
-              if (seen < splits) __nanosleep(64);
-            } while (seen < splits);
-            // generic-proxy writes of the siblings -> async-proxy bulk copies
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            const uint32_t slice_bytes = static_cast<uint32_t>(sl) * 128 * 4;
-            mbar_expect_tx(redbar, slice_bytes * (splits - 1));
-            for (int o = 0; o < splits - 1; ++o) {
-              const int sib = o < split ? o : o + 1;
-              const float* src = P.ws + ((ws_tile + sib) * (BN / 4) + lo / 4) * 128 * 4;
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                      smem_u32(s_red) + o * slice_bytes),
-                  "l"(src), "r"(slice_bytes), "r"(redbar)
-                  : "memory");
-            }
+      const int sl = BN / splits, lo = split * sl;
+      const int npub = (BN - sl) / 16, nown = sl / 16;
+      for (int it = half; it < npub; it += 2) {
+        const int c0 = it * 16 < lo ? it * 16 : it * 16 + sl;
+        epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, 3,
+                      split, splits, ws_tile, s_red, red_lo, false, tempty, org, s_rowrel);
+      }
+      if (splits > 1) {
+        if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[16] = gtimer();
+        __threadfence();
+        epi_bar();
+        if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[17] = gtimer();
+        if (threadIdx.x == kEpiWarp0 * 32) {
+          atomicAdd(P.counters + tile, 1);
+          int seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(P.counters + tile) : "memory");
+            if (seen < splits) __nanosleep(64);
+          } while (seen < splits);
+          // generic-proxy writes of the siblings -> async-proxy bulk copies
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const uint32_t slice_bytes = static_cast<uint32_t>(sl) * 128 * 4;
+          mbar_expect_tx(redbar, slice_bytes * (splits - 1));
+          for (int o = 0; o < splits - 1; ++o) {
+            const int sib = o < split ? o : o + 1;
+            const float* src = P.ws + ((ws_tile + sib) * (BN / 4) + lo / 4) * 128 * 4;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(s_red) + o * slice_bytes),
+                "l"(src), "r"(slice_bytes), "r"(redbar)
+                : "memory");
           }
-          if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[18] = gtimer();
-          mbar_wait(redbar, red_phase);
-          red_phase ^= 1;
-          if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[19] = gtimer();
         }
-        const bool pub = it < npub;
-        const int c0 = pub ? (it * 16 < lo ? it * 16 : it * 16 + sl) : lo + (it - npub) * 16;
-        if (!pub && mode == 2) {
+        if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[18] = gtimer();
+        mbar_wait(redbar, red_phase);
+        red_phase ^= 1;
+        if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[19] = gtimer();
+      }
+      if (half >= nown) {  // nothing for this half: hand the accumulator back now
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+      }
+      for (int k = half; k < nown; k += 2) {
+        const int c0 = lo + k * 16;
+        const bool last = k + 2 >= nown;  // this warp's last TMEM read of the unit
+        if (mode == 2) {
           // TMA-store epilogue: registers -> swizzled SMEM box -> one
-          // cp.async.bulk.tensor per 16-column chunk (double-buffered).
-          const int kb = stg_count & 1;
-          if (threadIdx.x == kEpiWarp0 * 32)
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // buffer kb drained
-          epi_bar();
+          // cp.async.bulk.tensor per 16-column chunk; each half owns one
+          // staging buffer and its own bulk group.
+          if (half_leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          half_bar(half);
           float v[16];
           tmem_ld<16>(tbase + c0, v);
-
-          if (it == nitems - 1) {
+          if (last) {
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty);
@@ -763,22 +775,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t addr = obase + s_row[row] + c0;
 #pragma unroll 1
             for (int e = 0; e < P.epi_count; ++e) {
-              const int k = P.epi_kind[e];
+              const int kk = P.epi_kind[e];
               const float* ep = P.epi_ptr[e];
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-                if (k == EPI_RELU) v[j] = fmaxf(v[j], 0.0f);
-                else v[j] += __ldg(ep + (k == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j) : addr + j));
+                if (kk == EPI_RELU) v[j] = fmaxf(v[j], 0.0f);
+                else v[j] += __ldg(ep + (kk == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j) : addr + j));
               }
             }
             // SWIZZLE_64B rows of 16 fp32: 16-byte chunk j at j ^ ((rp >> 1) & 3)
-            uint8_t* sf = smem + P.stg_off + kb * P.stg_f32 + rp * 64;
+            uint8_t* sf = smem + P.stg_off + half * P.stg_f32 + rp * 64;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               *reinterpret_cast<float4*>(sf + ((j ^ ((rp >> 1) & 3)) << 4)) =
                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             if (P.stg_bf) {  // SWIZZLE_32B rows of 16 bf16: chunk j at j ^ ((rp >> 2) & 1)
-              uint8_t* sb = smem + P.stg_off + 2 * P.stg_f32 + kb * P.stg_bf + rp * 32;
+              uint8_t* sb = smem + P.stg_off + 2 * P.stg_f32 + half * P.stg_bf + rp * 32;
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
                 uint4 pk;
@@ -795,27 +807,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          epi_bar();
-          if (threadIdx.x == kEpiWarp0 * 32) {
+          half_bar(half);
+          if (half_leader) {
             const int32_t* tc = P.tile_coords + tile * 5;
             const int32_t x0 = __ldg(tc) + c0, x1 = __ldg(tc + 1), x2 = __ldg(tc + 2),
                           x3 = __ldg(tc + 3), x4 = __ldg(tc + 4);
-            tma_store5(&tma_o, smem_u32(smem + P.stg_off + kb * P.stg_f32), x0, x1, x2, x3, x4);
+            tma_store5(&tma_o, smem_u32(smem + P.stg_off + half * P.stg_f32), x0, x1, x2, x3, x4);
             if (P.stg_bf)
-              tma_store5(&tma_ob, smem_u32(smem + P.stg_off + 2 * P.stg_f32 + kb * P.stg_bf), x0, x1,
-                         x2, x3, x4);
+              tma_store5(&tma_ob, smem_u32(smem + P.stg_off + 2 * P.stg_f32 + half * P.stg_bf), x0,
+                         x1, x2, x3, x4);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          ++stg_count;
         } else {
           epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col,
-                        pub ? 3 : mode, split, splits, ws_tile, s_red, red_lo, it == nitems - 1, tempty,
-                        org, s_rowrel);
+                        mode, split, splits, ws_tile, s_red, red_lo, last, tempty, org, s_rowrel);
         }
-        if (dbg && i == 0 && it < 8 && threadIdx.x == kEpiWarp0 * 32) dbg[20 + it] = gtimer();
+        if (dbg && i == 0 && k < 8 && threadIdx.x == kEpiWarp0 * 32) dbg[20 + k] = gtimer();
       }
       if (splits > 1) {
-        epi_bar();
+        epi_bar();  // every warp is done with the SMEM slices of this unit
         if (threadIdx.x == kEpiWarp0 * 32) {
           // Last one out re-arms both counters for the next launch.
           if (atomicAdd(P.counters + P.ntiles + tile, 1) == splits - 1) {
@@ -826,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (dbg && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[12 + i] = gtimer();
     }
-    if (threadIdx.x == kEpiWarp0 * 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (half_leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (dbg && threadIdx.x == kEpiWarp0 * 32) dbg[6] = gtimer();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -29,8 +29,8 @@ enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_RELU = 2, EPI_RESIDUAL = 3 };
 constexpr int kMaxEpi = 4;
 constexpr int kMaxBoxes = 4;
 constexpr int kMaxTaps = 32;  // taps of the halo C2D path (KH*KW)
-// Epilogue transpose buffers: 4 warps x 32 rows x 36 floats (k_umma.cu).
-constexpr int kEpiSmemBytes = 4 * 32 * 36 * 4;
+// Epilogue transpose buffers: 8 warps x 32 rows x 36 floats (k_umma.cu).
+constexpr int kEpiSmemBytes = 8 * 32 * 36 * 4;
 
 struct EpiOp {
   int32_t kind = EPI_NONE;
