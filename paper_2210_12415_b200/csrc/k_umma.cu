@@ -45,7 +45,8 @@ struct UmmaParams {
   uint32_t tmem_cols;       // >= 2*BN: two accumulators
   int32_t ring_bytes;       // SMEM pipeline ring
   int32_t table_ints;       // [stages | col_off | row_off] as one contiguous int array
-  int32_t ntaps, b_tap;     // halo C2D: tap t reads A at +a_tap[t], B at +t*b_tap
+  int32_t ntaps;            // halo C2D: tap t reads A at +a_tap[t], B at +b_tap[t] bytes
+  int32_t bias_rows;        // BiasAdd indexed by accumulator row (channels-as-rows C2D)
   // Weights resident (halo C2D with one output-channel tile): every chunk's
   // B slab is loaded once per CTA into SMEM at w_off (w_chunk bytes apart,
   // barrier wfull[c]); the ring then carries A only.
@@ -58,6 +59,7 @@ struct UmmaParams {
   const int32_t* tile_coords;
   ScatterDesc sc;           // Padding absorbed into this epilogue (sc.enabled)
   int32_t a_tap[kMaxTaps];
+  int32_t b_tap[kMaxTaps];
   int32_t store_mode;       // 1: row-contiguous, 16-byte aligned output rows; 0: generic
   int64_t col0;             // col_off[0] folded into the tile base in store mode 1
   unsigned long long* dbg;  // optional per-CTA %globaltimer checkpoints (8 per CTA)
@@ -436,10 +438,12 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
     for (int j0 = 0; j0 < W; j0 += 8) {
       float y[8];
       int64_t a[8];
+      bool cv[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         y[j] = mine[j0 + j];
-        a[j] = rb + s_col[c0 + j0 + j];
+        cv[j] = c0 + j0 + j < cols && s_col[c0 + j0 + j] >= 0;
+        a[j] = rb + (cv[j] ? s_col[c0 + j0 + j] : 0);
       }
 #pragma unroll 1
       for (int e = 0; e < P.epi_count; ++e) {
@@ -448,13 +452,14 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (k == EPI_RELU) y[j] = fmaxf(y[j], 0.0f);
-          else if (c0 + j0 + j < cols)
-            y[j] += __ldg(ep + (k == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j0 + j) : a[j]));
+          else if (cv[j])
+            y[j] += __ldg(ep + (k == EPI_BIAS ? static_cast<int64_t>(n_base + (P.bias_rows ? row : c0 + j0 + j))
+                                              : a[j]));
         }
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (c0 + j0 + j < cols) {
+        if (cv[j]) {
           P.out[a[j]] = y[j];
           if (P.out_bf16) P.out_bf16[a[j]] = __float2bfloat16_rn(y[j]);
         }
@@ -656,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // carry out of the field).
           const uint64_t ad0 = adesc | (a_addr >> 4), bd0 = bdesc | (b_addr >> 4);
           for (int t = 0; t < P.ntaps; ++t) {
-            const uint64_t adt = ad0 + (P.a_tap[t] >> 4), bdt = bd0 + ((t * P.b_tap) >> 4);
+            const uint64_t adt = ad0 + (P.a_tap[t] >> 4), bdt = bd0 + (P.b_tap[t] >> 4);
             for (int k = 0; k < ksteps; ++k)
               umma_bf16(dtm, adt + k * akadv16, bdt + k * bkadv16, idesc, (s != s_lo) | t | k);
           }
@@ -1123,7 +1128,9 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   L.scatter = p.scatter;
   if (L.scatter.enabled && (L.scatter.ic % 4 || p.BN % 8))
     fail(LFGPU_EINVAL, "umma: absorbed Padding needs 4-aligned channel bricks");
-  L.b_tap = p.b_tap;
+  for (int t = 0; t < p.ntaps; ++t)
+    L.b_tapv[t] = t < static_cast<int>(p.b_tapv.size()) ? p.b_tapv[t] : t * p.b_tap;
+  L.bias_rows = p.trans;
   if (p.ntaps > kMaxTaps || static_cast<int>(p.a_tap.size()) < p.ntaps)
     fail(LFGPU_EINVAL, "umma: tap table");
   for (int t = 0; t < p.ntaps; ++t) L.a_tap[t] = p.a_tap[t];
@@ -1195,7 +1202,8 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.ring_bytes = L.ring_bytes;
   P.table_ints = L.table_ints;
   P.ntaps = L.ntaps;
-  P.b_tap = L.b_tap;
+  for (int t = 0; t < kMaxTaps; ++t) P.b_tap[t] = L.b_tapv[t];
+  P.bias_rows = L.bias_rows;
   for (int t = 0; t < kMaxTaps; ++t) P.a_tap[t] = L.a_tap[t];
   P.store_mode = L.store_mode;
   P.col0 = L.col0;

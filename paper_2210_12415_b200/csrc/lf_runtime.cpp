@@ -423,6 +423,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
       if (u < 0 || !umma.count(u) || P->nodes[u].kind != LFGPU_OP_C2D || absorbed_pad.count(u))
         continue;
       const UmmaPlan& up = umma[u];
+      if (up.trans) continue;  // accumulator columns are pixels there, not channels
       const int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : P->nodes[u].output;
       if (final_t != tin) continue;
       const PTensor& xp = P->t[pnode.output];

@@ -118,6 +118,8 @@ struct UmmaPlan {
   int ntaps = 1;
   std::vector<int32_t> a_tap{0};
   int b_tap = 0;
+  std::vector<int32_t> b_tapv;  // per-tap B offsets (empty: t * b_tap)
+  int trans = 0;                // C2D with output channels as UMMA rows (pixels as N)
   int wres = 0;          // halo C2D: weights resident in SMEM (one output-channel tile)
   OutStore ost;          // TMA-store epilogue, when the output tile is a TMA box
   int tma_store = 0;     // schedule `vectorize`: use the TMA-store epilogue when legal
@@ -158,7 +160,8 @@ struct UmmaLaunch {
   int per_sm = 1;  // CTAs that fit on one SM (SMEM / TMEM)
   int ring_bytes = 0;
   int table_ints = 0;            // [stages | col_off | row_off] int32 count
-  int ntaps = 1, b_tap = 0;
+  int ntaps = 1, b_tap = 0, bias_rows = 0;
+  int32_t b_tapv[kMaxTaps] = {};
   int wres = 0, w_chunk = 0, w_tx = 0;
   CUtensorMap tma_o, tma_ob;     // store mode 2: fp32 output and its bf16 copy
   int stg_off = 0, stg_f32 = 0, stg_bf = 0;

@@ -564,6 +564,26 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
 // C2D: y[b,o,h,w] = sum_{i,rh,rw} x[b,i,V*h+rh,V*w+rw] * ker[o,i,rh,rw]
 // (interp.cpp:70-89) as an implicit GEMM over the template layouts.
 
+static bool plan_conv_halo_kc(const std::vector<Dim>& x_log, const std::vector<PDigit>& xd,
+                              const std::vector<Dim>& k_log, const std::vector<PDigit>& kd,
+                              const std::vector<Dim>& y_log, const std::vector<PDigit>& yd,
+                              int64_t V, const lfgpu_sched& s, int64_t kc_cap, UmmaPlan* out,
+                              std::string* why);
+
+// The halo plan with the widest channel chunk whose stages fit SMEM (a
+// chunk carries the weights of all KH*KW taps, so wide output tiles need
+// narrower chunks).
+static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDigit>& xd,
+                           const std::vector<Dim>& k_log, const std::vector<PDigit>& kd,
+                           const std::vector<Dim>& y_log, const std::vector<PDigit>& yd,
+                           int64_t V, const lfgpu_sched& s, UmmaPlan* out, std::string* why) {
+  for (int64_t cap : {64, 32, 16}) {
+    if (plan_conv_halo_kc(x_log, xd, k_log, kd, y_log, yd, V, s, cap, out, why)) return true;
+    if (why->find("exceed SMEM") == std::string::npos) return false;
+  }
+  return false;
+}
+
 // C2D with the overlapped input tile reused across taps ("halo" path).
 //
 // The template input brick xp[n][h0][w0][i0][B_h][B_w][i_t] already holds
@@ -576,10 +596,11 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
 // one TMA box ([KH][KW][i'][o'] is contiguous in the template weight brick).
 // Compared with one shifted input box per tap this cuts the input's L2->SMEM
 // traffic by ~KH*KW.
-static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDigit>& xd,
-                           const std::vector<Dim>& k_log, const std::vector<PDigit>& kd,
-                           const std::vector<Dim>& y_log, const std::vector<PDigit>& yd,
-                           int64_t V, const lfgpu_sched& s, UmmaPlan* out, std::string* why) {
+static bool plan_conv_halo_kc(const std::vector<Dim>& x_log, const std::vector<PDigit>& xd,
+                              const std::vector<Dim>& k_log, const std::vector<PDigit>& kd,
+                              const std::vector<Dim>& y_log, const std::vector<PDigit>& yd,
+                              int64_t V, const lfgpu_sched& s, int64_t kc_cap, UmmaPlan* out,
+                              std::string* why) {
   const int64_t N = y_log[0].extent, O = y_log[1].extent, Ho = y_log[2].extent,
                 Wo = y_log[3].extent, I = x_log[1].extent, KH = k_log[2].extent,
                 KW = k_log[3].extent;
@@ -669,7 +690,7 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   }
   const int64_t o2 = b_kmajor ? O : kd.back().ext, i2 = ki.ext;
   int64_t KC = std::gcd(i_t, i2);
-  KC = std::min<int64_t>(KC, 64);
+  KC = std::min<int64_t>(KC, kc_cap);
   while (KC > 16 && (KC & (KC - 1))) KC /= 2;
   if (KC % 16) {
     *why = "halo path: channel chunk";
@@ -678,7 +699,11 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   int64_t BN = std::min<int64_t>({o_t, o2, 256});
   if (s.tile_last >= 16 && s.tile_last < BN && BN % s.tile_last == 0 && s.tile_last % 16 == 0)
     BN = s.tile_last;
-  if (o_t % BN || o2 % BN || BN % 16 || (!b_kmajor && BN > 64 && BN % 64)) {
+  // MN-major weight boxes are 64 channels wide (128B swizzle), each inside
+  // one o' brick; a K-major slab takes all BN rows in one box.
+  const int64_t wbox = b_kmajor ? BN : std::min<int64_t>(BN, 64);
+  if (o_t % BN || o2 % wbox || (!b_kmajor && BN > 64 && (BN % 64 || o2 % 64)) || BN % 16 ||
+      o2 % BN) {
     *why = "halo path: channel tile";
     return false;
   }
@@ -881,7 +906,7 @@ static bool plan_conv_halo(const std::vector<Dim>& x_log, const std::vector<PDig
   }
   p.pipe = pick_pipe(p);
   {
-    const int64_t need = 2LL * (p.A.slot_bytes + p.B.boxes * p.B.slot_bytes) + 1024 + 512 +
+    const int64_t need = 2LL * (p.A.boxes * p.A.slot_bytes + p.B.boxes * p.B.slot_bytes) + 1024 + 512 +
                          kEpiSmemBytes + sizeof(StageEntry) * p.stages.size() + 8 * BN + 8 * 128;
     if (need > 227 * 1024) {
       *why = "halo path: two stages exceed SMEM";
