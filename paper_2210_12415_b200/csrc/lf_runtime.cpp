@@ -635,8 +635,8 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           P->bytes += A.numel * 4 + B.numel * 4 + fo.numel * 4;
         } else if (it != umma.end()) {
           UmmaPlan up = it->second;
-          up.a = A.d_bf16;
-          up.b = B.d_bf16;
+          up.a = up.swap_ab ? B.d_bf16 : A.d_bf16;
+          up.b = up.swap_ab ? A.d_bf16 : B.d_bf16;
           // The chain's final output is the one written; intermediates of a
           // fused chain are also written when the caller keeps them.
           int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : n.output;

@@ -120,6 +120,7 @@ struct UmmaPlan {
   int b_tap = 0;
   std::vector<int32_t> b_tapv;  // per-tap B offsets (empty: t * b_tap)
   int trans = 0;                // C2D with output channels as UMMA rows (pixels as N)
+  int swap_ab = 0;              // A views the node's second operand (weights), B the first
   int wres = 0;          // halo C2D: weights resident in SMEM (one output-channel tile)
   OutStore ost;          // TMA-store epilogue, when the output tile is a TMA box
   int tma_store = 0;     // schedule `vectorize`: use the TMA-store epilogue when legal

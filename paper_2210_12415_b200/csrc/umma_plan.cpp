@@ -650,7 +650,13 @@ static bool plan_conv_halo_kc(const std::vector<Dim>& x_log, const std::vector<P
     *why = "halo path: B_w > 128";
     return false;
   }
-  const int64_t h_sub = std::min<int64_t>(h_t, 128 / B_w);
+  // trans (schedule unroll = 2): output channels are the 128 UMMA rows and
+  // the tile's pixels the N columns (up to 256) - for small spatial tiles
+  // (deep layers, small batches) this puts 4-8x more work in every UMMA.
+  const bool trans = s.unroll == 2;
+  int64_t h_sub = std::min<int64_t>(h_t, (trans ? 256 : 128) / B_w);
+  if (trans)  // whole pixel chunks per tile: every tile has the same columns
+    while (h_sub > 1 && h_t % h_sub) --h_sub;
   const int64_t rows_h = h_sub + KH - 1;
   // Weight: [..][KH][KW][i'][o'] (o' innermost: MN-major B) or, when the
   // template leaves O whole (o' == O), [O][I0][KH][KW][i'] (K-major B).
@@ -701,9 +707,10 @@ static bool plan_conv_halo_kc(const std::vector<Dim>& x_log, const std::vector<P
     BN = s.tile_last;
   // MN-major weight boxes are 64 channels wide (128B swizzle), each inside
   // one o' brick; a K-major slab takes all BN rows in one box.
+  if (trans) BN = 128;  // weight rows per tile
   const int64_t wbox = b_kmajor ? BN : std::min<int64_t>(BN, 64);
   if (o_t % BN || o2 % wbox || (!b_kmajor && BN > 64 && (BN % 64 || o2 % 64)) || BN % 16 ||
-      o2 % BN) {
+      (!trans && o2 % BN)) {
     *why = "halo path: channel tile";
     return false;
   }
@@ -900,6 +907,48 @@ static bool plan_conv_halo_kc(const std::vector<Dim>& x_log, const std::vector<P
     }
     plan_out_store(yd, 4, 1, static_cast<int>(BN), tile_lv, rr, ok, &p.ost);
   }
+  if (trans) {
+    // Swap roles: A = the weight slabs (128 channel rows per tile), B = the
+    // overlapped input tile (pixel rows, shifted per tap); the runtime binds
+    // the operand buffers accordingly (swap_ab). The accumulator is
+    // [channel][pixel]: rows = channels, columns = pixels of the B_w-wide
+    // grid (x >= w_t and padding columns are not outputs).
+    const int64_t npad = (h_sub * B_w + 15) / 16 * 16;
+    const int64_t slab = p.b_tap;  // bytes of one tap's weight slab (per box)
+    std::swap(p.A, p.B);
+    p.swap_ab = 1;
+    p.B.slot_bytes = static_cast<int32_t>(
+        (std::max(npix, tapmax + npad) * KC * 2 + 1023) / 1024 * 1024);
+    p.b_tapv = p.a_tap;
+    p.a_tap.clear();
+    for (int64_t t = 0; t < taps; ++t) p.a_tap.push_back(static_cast<int32_t>(t * slab));
+    p.b_tap = 0;
+    for (auto& te : p.tiles) {
+      int32_t tmp[kMaxBoxes][5];
+      std::memcpy(tmp, te.ca, sizeof(tmp));
+      std::memcpy(te.ca, te.cb, sizeof(tmp));
+      std::memcpy(te.cb, tmp, sizeof(tmp));
+      te.rows = 128;
+      te.cols = static_cast<int32_t>(npad);
+    }
+    for (auto& se : p.stages) {
+      int32_t tmp[5];
+      std::memcpy(tmp, se.sa, sizeof(tmp));
+      std::memcpy(se.sa, se.sb, sizeof(tmp));
+      std::memcpy(se.sb, tmp, sizeof(tmp));
+    }
+    p.row_off.clear();
+    p.col_off.clear();
+    p.row_rel.assign(128, 0);
+    for (int r = 0; r < 128; ++r) p.row_off.push_back(y_off(0, r, 0, 0) - base0);
+    for (int64_t c = 0; c < npad; ++c) {
+      const int64_t hh = c / B_w, ww = c % B_w;
+      p.col_off.push_back(hh < h_sub && ww < w_t ? y_off(0, 0, hh, ww) - base0 : -1);
+    }
+    p.BN = static_cast<int>(npad);
+    p.trans = 1;
+    p.ost = OutStore();
+  }
   if (!umma_view_encodable(p.A, why) || !umma_view_encodable(p.B, why)) {
     *why = "halo path: " + *why;
     return false;
@@ -921,7 +970,7 @@ static bool plan_conv_halo_kc(const std::vector<Dim>& x_log, const std::vector<P
                           static_cast<int64_t>(sizeof(StageEntry) * p.stages.size() + 8 * p.col_off.size() + 8 * 128);
     const int64_t budget = 227 * 1024 - fixed - wbytes;
     const char* e = getenv("LFGPU_NO_WRES");
-    if (O0 * ochunks == 1 && !(e && atoi(e)) && budget >= 3 * p.A.slot_bytes) {
+    if (!trans && O0 * ochunks == 1 && !(e && atoi(e)) && budget >= 3 * p.A.slot_bytes) {
       p.wres = 1;
       p.pipe = static_cast<int>(std::min<int64_t>(8, budget / p.A.slot_bytes));
     }
@@ -930,7 +979,7 @@ static bool plan_conv_halo_kc(const std::vector<Dim>& x_log, const std::vector<P
   p.split_pref = s.order;
   p.tma_store = s.vectorize;
   std::ostringstream os;
-  os << (p.wres ? "conv-halo-wres" : "conv-halo") << " h_t=" << h_t << " w_t=" << w_t << " o_t=" << o_t << " i_t=" << i_t << " i'=" << i2
+  os << (p.wres ? "conv-halo-wres" : trans ? "conv-halo-trans" : "conv-halo") << " h_t=" << h_t << " w_t=" << w_t << " o_t=" << o_t << " i_t=" << i_t << " i'=" << i2
      << " o'=" << o2 << " rows=" << h_sub << "x" << B_w << " BN=" << BN << " KC=" << KC
      << " taps=" << taps << " tiles=" << p.tiles.size() << " stages=" << p.stages.size()
      << " pipe=" << p.pipe;
@@ -954,7 +1003,7 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
   {
     const char* e = getenv("LFGPU_NO_HALO");
     std::string hwhy;
-    if (!(e && atoi(e)) && s.unroll == 0 &&
+    if (!(e && atoi(e)) && s.unroll != 1 &&
         plan_conv_halo(x_log, xd, k_log, kd, y_log, yd, V, s, out, &hwhy))
       return true;
     halo_why = hwhy.empty() ? "off" : hwhy;

@@ -155,4 +155,10 @@ def conv_candidates(graph: Graph, node, fuse=0):
                         out.append(Candidate({node: (ht, wt, ot, it, it, o2)},
                                              [runtime.sched(node, fuse=fuse)],
                                              f"h_t={ht} w_t={wt} o_t={ot} i_t={it} o'={o2}"))
+                        # channels-as-rows orientation (schedule unroll=2) for
+                        # wide channel tiles on small spatial tiles
+                        if ot % 128 == 0 and o2 % 64 == 0 and ht * wt <= 256:
+                            out.append(Candidate({node: (ht, wt, ot, it, it, o2)},
+                                                 [runtime.sched(node, fuse=fuse, unroll=2)],
+                                                 f"h_t={ht} w_t={wt} o_t={ot} i_t={it} o'={o2} trans"))
     return out

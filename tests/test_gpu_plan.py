@@ -251,3 +251,22 @@ def test_halo_conv_tma_store(f, vec):
     p.run()
     got = p.get_output("y")
     assert np.array_equal(got, ref["y"]), np.abs(got - ref["y"]).max()
+
+
+@pytest.mark.parametrize("shape,f", [((1, 512, 512, 7), (7, 7, 128, 64, 64, 128)),
+                                     ((1, 64, 128, 7), (7, 7, 128, 32, 32, 128)),
+                                     ((1, 128, 128, 14), (14, 14, 128, 64, 64, 128))])
+def test_halo_conv_channels_as_rows(shape, f):
+    """Schedule unroll=2: output channels are the 128 UMMA rows and the
+    tile's pixels the N columns (weights = A, shifted input tile = B)."""
+    n, c, o, h = shape
+    g = ir.pad_conv(n, c, o, h, 3, 1, 1)
+    seqs = runtime.decode_layout(g, 1, list(f))
+    inputs, ref = oracle_outputs(g, 9)
+    p = runtime.Plan(g, seqs, [runtime.sched(1, unroll=2)], flags=_abi.PLAN_REQUIRE_TC)
+    assert "conv-halo-trans" in p.node_kernel(1), p.node_kernel(1)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    got = p.get_output("y")
+    assert np.array_equal(got, ref["y"]), np.abs(got - ref["y"]).max()
