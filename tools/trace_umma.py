@@ -135,6 +135,11 @@ if __name__ == "__main__":
                  f"gemm {f} tile {tl} order {o}")
     if os.environ.get("TRACE_GEMM_ONLY"):
         sys.exit(0)
+    if os.environ.get("TRACE_TINY"):  # fixed per-kernel cost: one 128x64 tile, one K stage
+        gt = ir.gemm(128, 64, 64)
+        timeline(gt, tuner.Candidate({0: (128, 64, 64)}, [runtime.sched(0, tile_last=64, order=1)]),
+                 {"a": k64((128, 64)), "b": k64((64, 64))}, "gemm 128x64x64 (1 tile, 1 stage)")
+        sys.exit(0)
     gc = ir.pad_conv(16, 64, 64, 56, 3, 1, 1)
     for f in [(8, 14, 64, 32, 32, 64), (7, 14, 32, 32, 32, 32)]:
         timeline(gc, tuner.Candidate({1: f}, [runtime.sched(1)]),
