@@ -175,6 +175,10 @@ def time_plan_rotating(torch, plans, steps, warmup, world):
     torch.cuda.synchronize()
     t_wall = time.perf_counter()
     with torch.cuda.stream(s):
+        # A ~1 ms device-side sleep ahead of the start event lets the host
+        # enqueue all K steps before the GPU reaches them, so the timed
+        # region holds back-to-back device work, not host launch gaps.
+        torch.cuda._sleep(2_000_000)
         a.record(s)
     for i in range(steps):
         plans[(warmup + i) % len(plans)].run(s.cuda_stream)
