@@ -55,6 +55,18 @@ def gemm_split(reps=3):
     gemm(reps, (128, 64, 256), 128, 0)
 
 
+def conv_trans(reps=3):
+    g = ir.pad_conv(1, 512, 512, 7, 3, 1, 1)
+    c = tuner.Candidate({1: (7, 7, 128, 64, 64, 128)}, [runtime.sched(1, unroll=2)])
+    p = runtime.Plan(g, tuner.seqs_for(g, c), c.scheds, _abi.PLAN_REQUIRE_TC)
+    p.set_input_device("x", k64((1, 512, 7, 7)))
+    p.set_input_device("ker", k64((512, 512, 3, 3)))
+    print(p.node_kernel(1))
+    for _ in range(reps):
+        p.run()
+    torch.cuda.synchronize()
+
+
 def conv_halo(reps=3, nb=16, factors=(7, 14, 32, 32, 32, 32)):
     conv(reps, nb, factors)
 
