@@ -282,6 +282,74 @@ int storage_elem(const PTensor& t) {
   return t.dtype == LFGPU_DTYPE_I32 ? LFGPU_ELEM_I32 : LFGPU_ELEM_F32;
 }
 
+// store_at is folded offline (lower.cpp:32-82): the attachment only
+// co-locates a constant with its target's storage, one extra slot along
+// `dim`, so values are unaffected. The plan applies the reference's
+// validation (source constant, attachment last, target known and not itself
+// attached, shape compatible, the grown target still derivable), then
+// keeps the source in its own buffer in the absorb-prefix layout and the
+// target in its own layout: every consumer reads the same values the fused
+// storage would hold.
+void fold_store_at(lfgpu_plan* P, int ntensors) {
+  std::vector<int> target(ntensors, -1), dim(ntensors, 0);
+  for (int i = 0; i < ntensors; ++i) {
+    PTensor& t = P->t[i];
+    for (size_t j = 0; j < t.seq.size(); ++j) {
+      const lfgpu_prim& p = t.seq[j];
+      if (p.kind == LFGPU_PRIM_DECOUPLE_AT)
+        fail(LFGPU_EINVAL, "decouple_at cannot appear in a compilation sequence");
+      if (p.kind != LFGPU_PRIM_STORE_AT) continue;
+      if (t.role != LFGPU_ROLE_CONSTANT)
+        fail(LFGPU_EINVAL, "store_at on non-constant tensor '" + t.id +
+                               "': layout fusion is offline only");
+      if (j + 1 != t.seq.size())
+        fail(LFGPU_EINVAL, "store_at must be the final primitive of '" + t.id + "'");
+      if (p.target < 0 || p.target >= ntensors)
+        fail(LFGPU_EINVAL, "store_at target of '" + t.id + "' unknown");
+      target[i] = p.target;
+      dim[i] = p.dim;
+    }
+  }
+  std::map<int, std::vector<Dim>> grown;  // target -> dims with its slots
+  for (int i = 0; i < ntensors; ++i) {
+    if (target[i] < 0) continue;
+    PTensor& src = P->t[i];
+    PTensor& dst = P->t[target[i]];
+    if (target[target[i]] >= 0)
+      fail(LFGPU_EINVAL, "store_at target '" + dst.id + "' is itself attached elsewhere");
+    src.seq.pop_back();  // the absorb prefix (lower.cpp:59)
+    std::vector<Dim> sd;
+    try {
+      sd = derive(src.logical, src.seq);
+    } catch (const Error& e) {
+      fail(e.code, "tensor '" + src.id + "': " + e.what());
+    }
+    // apply_store_at (layout.cpp:450-467)
+    // Each attachment sees the target as grown by the earlier ones.
+    auto it = grown.emplace(target[i], dst.logical).first;
+    std::vector<Dim>& td = it->second;
+    const int d = dim[i], rank = static_cast<int>(td.size());
+    if (d < 0 || d >= rank) fail(LFGPU_EINVAL, "store_at: dim out of range");
+    if (static_cast<int>(sd.size()) + 1 != rank)
+      fail(LFGPU_EINVAL, "store_at: source must match target with one dim removed");
+    for (int k = 0, j = 0; k < rank; ++k) {
+      if (k == d) continue;
+      if (sd[j].extent != td[k].extent)
+        fail(LFGPU_EINVAL, "store_at: shape incompatibility at target dim " + std::to_string(k));
+      ++j;
+    }
+    td[d].extent += 1;
+  }
+  // The target's sequence must still derive on the grown dims (lower.cpp:84-95).
+  for (const auto& [ti, td] : grown) {
+    try {
+      (void)derive(td, P->t[ti].seq);
+    } catch (const Error& e) {
+      fail(e.code, "tensor '" + P->t[ti].id + "': " + e.what());
+    }
+  }
+}
+
 void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sched* sched) {
   if (!g || g->ntensors <= 0) fail(LFGPU_EINVAL, "empty graph");
   P->t.resize(g->ntensors);
@@ -299,10 +367,8 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
     const lfgpu_seq& sq = g->seqs[s];
     if (sq.tensor < 0 || sq.tensor >= g->ntensors) fail(LFGPU_EINVAL, "seq names no tensor");
     P->t[sq.tensor].seq = seq_of(sq.nprims, sq.prims);
-    for (const auto& p : P->t[sq.tensor].seq)
-      if (p.kind == LFGPU_PRIM_STORE_AT || p.kind == LFGPU_PRIM_DECOUPLE_AT)
-        fail(LFGPU_EUNSUPPORTED, "store_at layouts are not supported by the GPU plan yet");
   }
+  fold_store_at(P, g->ntensors);
   for (auto& t : P->t) {
     try {
       t.phys = derive(t.logical, t.seq);

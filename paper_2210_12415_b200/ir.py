@@ -73,6 +73,13 @@ class Graph:
                 return i
         raise KeyError(f"unknown tensor '{tid}'")
 
+    def _target_index(self, tid):
+        """store_at target index, -1 when unknown (the plan reports it, lower.cpp:54)."""
+        for i, t in enumerate(self.tensors):
+            if t.id == tid:
+                return i
+        return -1
+
     def tensor(self, tid):
         return self.tensors[self.tensor_index(tid)]
 
@@ -150,7 +157,7 @@ class CGraph:
         for i, (tid, seq) in enumerate(items):
             arr = (_abi.Prim * len(seq))()
             for k, p in enumerate(seq):
-                p.fill(arr[k], g.tensor_index)
+                p.fill(arr[k], g._target_index)
             self.prim_arrays.append(arr)
             self.seqs[i].tensor = g.tensor_index(tid)
             self.seqs[i].nprims = len(seq)

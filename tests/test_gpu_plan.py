@@ -12,7 +12,7 @@ import pytest
 
 import oracle_lib as O
 from paper_2210_12415_b200 import _abi, ir, runtime
-from paper_2210_12415_b200.layout import reorder, split, unfold
+from paper_2210_12415_b200.layout import reorder, split, store_at, unfold
 
 pytestmark = pytest.mark.gpu
 
@@ -270,3 +270,47 @@ def test_halo_conv_channels_as_rows(shape, f):
     p.run()
     got = p.get_output("y")
     assert np.array_equal(got, ref["y"]), np.abs(got - ref["y"]).max()
+
+
+def _store_at_cases(g):
+    t = runtime.decode_layout(g, 0, [128, 64, 128])
+    return {
+        "plain": {"bias": [store_at("b", 0)]},
+        "b_split_n": {"a": t["a"], "c": t["c"], "b": [split(1, [2, 128]), reorder([1, 0, 2])],
+                      "bias": [store_at("b", 0)]},
+    }
+
+
+@pytest.mark.parametrize("case", ["plain", "b_split_n"])
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_store_at_gmm_bias(case, fuse):
+    """test_executor.cpp:196-201 at tensor-core size: bias store_at-attached
+    to the weights runs like the unfused graph (lower.cpp:32-82 folds it
+    offline; the attachment co-locates storage, values are unchanged)."""
+    g = ir.gmm_chain(256, 128, 256)
+    seqs = _store_at_cases(g)[case]
+    inputs, ref = oracle_outputs(g, 8)
+    p = runtime.Plan(g, seqs, [runtime.sched(0, fuse=fuse)], flags=_abi.PLAN_REQUIRE_TC)
+    assert p.node_kernel(0).startswith("umma_gemm"), p.node_kernel(0)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    assert np.array_equal(p.get_output("y"), ref["y"])
+
+
+@pytest.mark.parametrize("seqs,msg", [
+    # messages are the reference's own (checked against oracle/_ref in
+    # test_oracle.py::test_reference_store_at_rules)
+    ({"a": [store_at("b", 0)]}, "store_at on non-constant tensor 'a'"),
+    ({"bias": [store_at("b", 0), split(0, [2, 128])]}, "store_at must be the final primitive"),
+    ({"bias": [split(0, [4, 64]), store_at("b", 0)]},
+     "store_at: source must match target with one dim removed"),
+    ({"bias": [store_at("nope", 0)]}, "store_at target"),
+    ({"bias": [store_at("b", 2)]}, "store_at: dim out of range"),
+    ({"bias": [store_at("b", 0)], "b": [split(0, [2, 64])]}, "dim K has extent 129"),
+])
+def test_store_at_rules(seqs, msg):
+    g = ir.gmm_chain(256, 128, 256)
+    with pytest.raises(runtime.LfError) as e:
+        runtime.Plan(g, seqs, [])
+    assert e.value.code == _abi.EINVAL and msg in str(e.value), str(e.value)

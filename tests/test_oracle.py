@@ -10,7 +10,7 @@ import pytest
 
 import oracle_lib as O
 from paper_2210_12415_b200 import ir
-from paper_2210_12415_b200.layout import LayoutPrimitive, fuse, padding, reorder, split, unfold
+from paper_2210_12415_b200.layout import LayoutPrimitive, fuse, padding, reorder, split, store_at, unfold
 
 GRAPHS = {
     "cfg1_pad_conv": lambda: ir.pad_conv(1, 64, 64, 56, 3, 1, 1),
@@ -116,6 +116,32 @@ class TestAgainstReference:
                 b = O.random_inputs(g, seed, lib="ref")
                 for i in range(len(a)):
                     assert np.array_equal(a[i], b[i])
+
+    def test_reference_store_at_rules(self):
+        """Pins the store_at semantics the GPU plan mirrors (lower.cpp:32-82):
+        an accepted attachment leaves values unchanged (test_executor.cpp:
+        196-201); rejected ones carry the messages test_gpu_plan.py expects."""
+        g = ir.gmm_chain(256, 128, 256)
+        ok = [{"bias": [store_at("b", 0)]},
+              {"b": [split(1, [2, 128]), reorder([1, 0, 2])], "bias": [store_at("b", 0)]}]
+        bad = [({"a": [store_at("b", 0)]}, "store_at on non-constant tensor 'a'"),
+               ({"bias": [store_at("b", 0), split(0, [2, 128])]},
+                "store_at must be the final primitive"),
+               ({"bias": [split(0, [4, 64]), store_at("b", 0)]},
+                "store_at: source must match target with one dim removed"),
+               ({"bias": [store_at("nope", 0)]}, "store_at target"),
+               ({"bias": [store_at("b", 2)]}, "store_at: dim out of range"),
+               ({"bias": [store_at("b", 0)], "b": [split(0, [2, 64])]}, "dim K has extent 129")]
+        want = O.random_inputs(g, 8)
+        O.reference_eval(g, want)
+        for seqs in ok:
+            bufs = O.random_inputs(g, 8)
+            assert O.ref_interpret(g, seqs, [], bufs) == 0, O.ref().ref_last_error()
+            y = g.tensor_index("y")
+            assert np.array_equal(bufs[y], want[y])
+        for seqs, msg in bad:
+            assert O.ref_interpret(g, seqs, [], O.random_inputs(g, 8)) != 0
+            assert msg in O.ref().ref_last_error().decode(), O.ref().ref_last_error()
 
     def test_materialize_fuzz(self):
         rng = np.random.default_rng(11)
