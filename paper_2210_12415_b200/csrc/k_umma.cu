@@ -56,11 +56,14 @@ struct UmmaParams {
   // bf16 bytes) at stg_off; per-tile box origins; row positions in the box
   // follow row_off in the SMEM table.
   int32_t stg_off, stg_f32, stg_bf;
+  int32_t stg_cstride, stg_cdim;  // >0: transposed box, column j at plane j * stg_cstride
   const int32_t* tile_coords;
   ScatterDesc sc;           // Padding absorbed into this epilogue (sc.enabled)
   int32_t a_tap[kMaxTaps];
   int32_t b_tap[kMaxTaps];
   int32_t store_mode;       // 1: row-contiguous, 16-byte aligned output rows; 0: generic
+  int32_t diag;             // diagnostics (LFGPU_UMMA_DIAG, timing only): bit0 skips the
+                            // epilogue's stores, 2 traces, 4 unshifted taps, 8 one tap
   int64_t col0;             // col_off[0] folded into the tile base in store mode 1
   unsigned long long* dbg;  // optional per-CTA %globaltimer checkpoints (8 per CTA)
   // Split-K: unit (tile, split) accumulates stages [split*n/S, (split+1)*n/S);
@@ -324,6 +327,9 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
                                        const int32_t* s_rowrel) {
   float v[W];
   tmem_ld<W>(taddr + c0, v);
+  if (P.dbg && (P.diag & 2) && threadIdx.x == kEpiWarp0 * 32 && c0 == 0 &&
+      P.dbg[32 * blockIdx.x + 28] == 0)
+    P.dbg[32 * blockIdx.x + 28] = gtimer();
 
   if (release) {
     // Every TMEM read of this accumulator is complete: hand it back to the MMA.
@@ -431,6 +437,7 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
     return;
   }
   // Generic: thread = row, 8 columns per step (loads, ops, stores batched).
+  if (P.diag & 1) return;
   if (row < rows && s_row[row] >= 0) {
     const int64_t rb = obase + s_row[row];
     const float* mine = wbuf + lane * kEpiLd;
@@ -660,8 +667,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           // them by 16-byte units directly (SMEM addresses < 256 KB never
           // carry out of the field).
           const uint64_t ad0 = adesc | (a_addr >> 4), bd0 = bdesc | (b_addr >> 4);
-          for (int t = 0; t < P.ntaps; ++t) {
-            const uint64_t adt = ad0 + (P.a_tap[t] >> 4), bdt = bd0 + (P.b_tap[t] >> 4);
+          const int ntaps = (P.diag & 8) ? 1 : P.ntaps;
+          for (int t = 0; t < ntaps; ++t) {
+            const uint64_t adt = ad0 + ((P.diag & 4) ? 0 : (P.a_tap[t] >> 4)), bdt = bd0 + (P.b_tap[t] >> 4);
             for (int k = 0; k < ksteps; ++k)
               umma_bf16(dtm, adt + k * akadv16, bdt + k * bkadv16, idesc, (s != s_lo) | t | k);
           }
@@ -777,7 +785,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (splits > 1) split_sum<16>(P, v, s_red, c0, red_lo, row, split, splits);
           const int rp = row < rows ? s_rowpos[row] : -1;
           if (rp >= 0) {
-            const int64_t addr = obase + s_row[row] + c0;
+            const int64_t addr = obase + s_row[row];
+            const int cs = P.stg_cstride;
 #pragma unroll 1
             for (int e = 0; e < P.epi_count; ++e) {
               const int kk = P.epi_kind[e];
@@ -785,9 +794,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 if (kk == EPI_RELU) v[j] = fmaxf(v[j], 0.0f);
-                else v[j] += __ldg(ep + (kk == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j) : addr + j));
+                else
+                  v[j] += __ldg(ep + (kk == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j)
+                                                     : addr + (cs ? s_col[c0 + j] : c0 + j)));
               }
             }
+            if (cs) {
+              // Transposed box: column j is the plane at j * cs; consecutive
+              // rows of a warp are consecutive words (conflict-free).
+              float* sf = reinterpret_cast<float*>(smem + P.stg_off + half * P.stg_f32) + rp;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) sf[j * cs] = v[j];
+              if (P.stg_bf) {
+                __nv_bfloat16* sb =
+                    reinterpret_cast<__nv_bfloat16*>(smem + P.stg_off + 2 * P.stg_f32 + half * P.stg_bf) + rp;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sb[j * cs] = __float2bfloat16_rn(v[j]);
+              }
+            } else {
             // SWIZZLE_64B rows of 16 fp32: 16-byte chunk j at j ^ ((rp >> 1) & 3)
             uint8_t* sf = smem + P.stg_off + half * P.stg_f32 + rp * 64;
 #pragma unroll
@@ -810,13 +834,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 *reinterpret_cast<uint4*>(sb + ((j ^ ((rp >> 2) & 1)) << 4)) = pk;
               }
             }
+            }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           half_bar(half);
           if (half_leader) {
             const int32_t* tc = P.tile_coords + tile * 5;
-            const int32_t x0 = __ldg(tc) + c0, x1 = __ldg(tc + 1), x2 = __ldg(tc + 2),
-                          x3 = __ldg(tc + 3), x4 = __ldg(tc + 4);
+            const int cd = P.stg_cdim;
+            const int32_t x0 = __ldg(tc) + (cd == 0 ? c0 : 0), x1 = __ldg(tc + 1) + (cd == 1 ? c0 : 0),
+                          x2 = __ldg(tc + 2) + (cd == 2 ? c0 : 0), x3 = __ldg(tc + 3) + (cd == 3 ? c0 : 0),
+                          x4 = __ldg(tc + 4) + (cd == 4 ? c0 : 0);
             tma_store5(&tma_o, smem_u32(smem + P.stg_off + half * P.stg_f32), x0, x1, x2, x3, x4);
             if (P.stg_bf)
               tma_store5(&tma_ob, smem_u32(smem + P.stg_off + 2 * P.stg_f32 + half * P.stg_bf), x0,
@@ -1077,17 +1104,33 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   for (const auto& te : p.tiles)
     if (te.cols != p.BN) full_cols = false;
   const char* sm_env = getenv("LFGPU_STORE_MODE");
-  const bool want_tma = (p.tma_store && !(sm_env && atoi(sm_env) < 2)) || (sm_env && atoi(sm_env) == 2);
-  if (p.ost.ok && cols_unit && full_cols && want_tma && !p.scatter.enabled) {
+  // TMA store when the schedule asks (vectorize), and by default for
+  // transposed boxes whose alternative is the generic scalar path (one
+  // 4-byte store per element, ~3x slower epilogue on the cfg1 b16 conv).
+  const bool auto_tma = p.ost.ok && p.ost.col_stride > 0 && !aligned;
+  const bool want_tma = ((p.tma_store || auto_tma) && !(sm_env && atoi(sm_env) < 2)) ||
+                        (sm_env && atoi(sm_env) == 2);
+  // Transposed boxes (columns not innermost) stage each column as a plane
+  // of the box, unswizzled; their bf16 twin must be encodable too.
+  const bool tbox = p.ost.ok && p.ost.col_stride > 0;
+  OperandView ob;
+  bool ob_ok = true;
+  if (p.ost.ok && p.out_bf16) {
+    ob = p.ost.O;
+    ob.elem_bytes = 2;
+    ob.swizzle = tbox ? 0 : 32;
+    for (int d = 1; d < ob.rank; ++d) ob.strides[d] /= 2;
+    std::string why;
+    ob_ok = umma_view_encodable(ob, &why);
+  }
+  if (p.ost.ok && (cols_unit || tbox) && ob_ok && full_cols && want_tma && !p.scatter.enabled) {
     L.store_mode = 2;
-    L.col0 = p.col_off[0];
+    L.col0 = tbox ? 0 : p.col_off[0];
+    L.stg_cstride = tbox ? p.ost.col_stride : 0;
+    L.stg_cdim = p.ost.col_dim;
     L.tma_o = encode(p.ost.O, p.out);
     L.stg_f32 = (p.ost.box_rows * 64 + 1023) / 1024 * 1024;
     if (p.out_bf16) {
-      OperandView ob = p.ost.O;
-      ob.elem_bytes = 2;
-      ob.swizzle = 32;
-      for (int d = 1; d < ob.rank; ++d) ob.strides[d] /= 2;
       L.tma_ob = encode(ob, p.out_bf16);
       L.stg_bf = (p.ost.box_rows * 32 + 1023) / 1024 * 1024;
     }
@@ -1206,7 +1249,10 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.bias_rows = L.bias_rows;
   for (int t = 0; t < kMaxTaps; ++t) P.a_tap[t] = L.a_tap[t];
   P.store_mode = L.store_mode;
+  P.diag = getenv("LFGPU_UMMA_DIAG") ? atoi(getenv("LFGPU_UMMA_DIAG")) : 0;
   P.col0 = L.col0;
+  P.stg_cstride = L.stg_cstride;
+  P.stg_cdim = L.stg_cdim;
   P.splits = L.splits;
   P.ws = L.ws;
   P.counters = L.counters;

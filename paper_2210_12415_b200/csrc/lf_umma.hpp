@@ -99,7 +99,8 @@ struct StageEntry {  // 40 bytes
 struct OutStore {
   bool ok = false;
   OperandView O;                     // fp32 view of the output (box: 16 cols x tile rows)
-  int col_dim = 0;                   // view dim of the columns (0)
+  int col_dim = 0;                   // view dim of the columns (0 unless transposed)
+  int col_stride = 0;                // transposed box: element stride of one column plane
   std::vector<int32_t> tile_coords;  // ntiles x 5
   std::vector<int32_t> row_pos;      // 128
   int box_rows = 0;                  // rows of one staged chunk
@@ -166,6 +167,7 @@ struct UmmaLaunch {
   int wres = 0, w_chunk = 0, w_tx = 0;
   CUtensorMap tma_o, tma_ob;     // store mode 2: fp32 output and its bf16 copy
   int stg_off = 0, stg_f32 = 0, stg_bf = 0;
+  int stg_cstride = 0, stg_cdim = 0;  // transposed TMA-store box (OutStore::col_stride / col_dim)
   void* d_tcoords = nullptr;
   ScatterDesc scatter;
   int red_bytes = 0;

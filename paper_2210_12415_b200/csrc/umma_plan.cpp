@@ -349,11 +349,18 @@ static void plan_out_store(const std::vector<PDigit>& yd, int nlog, int col_lj, 
     o->why = "BN not a multiple of 16";
     return;
   }
-  if (yd.back().lj != col_lj || yd.back().div != 1 || yd.back().ext % 16) {
-    o->why = "columns not innermost";
+  // The column digit: the innermost digit of the column index. When it is
+  // not the innermost physical digit the box is "transposed": its inner
+  // dims are row digits and each staged column is a plane of the box.
+  const int nk = static_cast<int>(yd.size());
+  int kc = -1;
+  for (int k = 0; k < nk; ++k)
+    if (yd[k].lj == col_lj && yd[k].div == 1) kc = k;
+  if (kc < 0 || yd[kc].ext % 16) {
+    o->why = "column digit not a multiple of 16";
     return;
   }
-  const int nk = static_cast<int>(yd.size());
+  const bool transposed = kc != nk - 1;
   auto dval = [&](const std::array<int64_t, 4>& lv, int k) { return digit_of(yd[k], lv[yd[k].lj]); };
   // Row digit ranges over the valid rows of tile 0.
   std::vector<int64_t> lo(nk, INT64_MAX), hi(nk, INT64_MIN);
@@ -370,9 +377,16 @@ static void plan_out_store(const std::vector<PDigit>& yd, int nlog, int col_lj, 
   }
   std::vector<VDim> v;
   int64_t cells = 1;
+  for (const auto& lv : tile_lv)
+    if (dval(lv, kc) + BN > yd[kc].ext) {
+      o->why = "column tile crosses its digit";
+      return;
+    }
   for (int k = 0; k < nk; ++k) {
-    VDim d{yd[k].ext, yd[k].stride, 1, 1};
-    if (k == nk - 1) d.box = 16;
+    // fp32 strides: merge_view counts bf16 elements, so doubled strides
+    // give it fp32 bytes (and its 16-byte stride check applies to those).
+    VDim d{yd[k].ext, yd[k].stride * 2, 1, 1};
+    if (k == kc) d.box = 16;
     else if (yd[k].lj != col_lj) {
       if (dval(tile_lv[0], k) != lo[k]) {
         o->why = "tile origin is not the box corner";
@@ -398,9 +412,8 @@ static void plan_out_store(const std::vector<PDigit>& yd, int nlog, int col_lj, 
     o->why = why;
     return;
   }
-  for (int d = 0; d < O.rank; ++d) O.strides[d] = O.strides[d] / 2 * 4;  // merge_view assumes bf16
   O.elem_bytes = 4;
-  O.swizzle = 64;  // 16 fp32 = 64-byte box rows
+  O.swizzle = transposed ? 0 : 64;  // columns innermost: 16 fp32 = 64-byte box rows
   O.mn_major = 0;
   if (!umma_view_encodable(O, &why)) {
     o->why = why;
@@ -413,6 +426,15 @@ static void plan_out_store(const std::vector<PDigit>& yd, int nlog, int col_lj, 
   // Row position inside the box (view dims >= 1, innermost first).
   int32_t c0[5];
   coord(tile_lv[0], c0);
+  // Box element position of (row, column j): row_pos[row] + j * col_stride.
+  const int cdim = grp[kc];
+  int64_t col_stride = 1;
+  for (int d = 0; d < cdim; ++d) col_stride *= O.box[d];
+  col_stride *= mult[kc];
+  if (transposed && (cdim == 0 || mult[kc] != 1)) {
+    o->why = "column dim merged into a row dim";
+    return;
+  }
   o->row_pos.assign(128, -1);
   for (int r = 0; r < 128; ++r) {
     if (!row_ok[r]) continue;
@@ -421,7 +443,15 @@ static void plan_out_store(const std::vector<PDigit>& yd, int nlog, int col_lj, 
     int32_t c[5];
     coord(lv, c);
     int64_t pos = 0, scale = 1;
-    for (int d = 1; d < O.rank; ++d) {
+    for (int d = 0; d < O.rank; ++d) {
+      if (d == cdim) {
+        if (c[d] != c0[d]) {
+          o->why = "rows vary the column coordinate";
+          return;
+        }
+        if (transposed) scale *= O.box[d];  // else row_pos counts 16-column rows
+        continue;
+      }
       const int64_t rel = c[d] - c0[d];
       if (rel < 0 || rel >= O.box[d]) {
         o->why = "row outside the box";
@@ -436,7 +466,8 @@ static void plan_out_store(const std::vector<PDigit>& yd, int nlog, int col_lj, 
   o->tile_coords.assign(tile_lv.size() * 5, 0);
   for (size_t t = 0; t < tile_lv.size(); ++t) coord(tile_lv[t], &o->tile_coords[t * 5]);
   o->O = O;
-  o->col_dim = 0;
+  o->col_dim = cdim;
+  o->col_stride = static_cast<int32_t>(transposed ? col_stride : 0);
   o->ok = true;
 }
 

@@ -237,7 +237,8 @@ def test_umma_gemm_epilogue_variants(factors, tile, order, vec):
 
 
 @pytest.mark.parametrize("f,vec", [((8, 14, 64, 32, 32, 64), 1), ((7, 14, 32, 32, 32, 32), 1),
-                                   ((14, 14, 64, 64, 64, 64), 0)])
+                                   ((14, 14, 64, 64, 64, 64), 0), ((28, 28, 64, 32, 32, 64), 1),
+                                   ((28, 28, 32, 32, 32, 32), 1)])
 def test_halo_conv_tma_store(f, vec):
     n, c, h = (1, 64, 56) if f[0] != 14 else (1, 256, 14)
     g = ir.pad_conv(n, c, 64 if c == 64 else c, h, 3, 1, 1)
@@ -246,11 +247,29 @@ def test_halo_conv_tma_store(f, vec):
     p = runtime.Plan(g, seqs, [runtime.sched(1, vectorize=vec)], flags=_abi.PLAN_REQUIRE_TC)
     k = p.node_kernel(1)
     assert "conv-halo" in k, k
+    if f[1] == 28 and vec:  # w-innermost output: transposed TMA-store box (112-byte rows)
+        assert "store=2" in k, k
     for tid, v in inputs.items():
         p.set_input(tid, v)
     p.run()
     got = p.get_output("y")
     assert np.array_equal(got, ref["y"]), np.abs(got - ref["y"]).max()
+
+
+def test_transposed_tma_store_fused_chain():
+    """Padding -> C2D -> BiasAdd -> ReLU with a w-innermost output: the
+    fused chain runs before the transposed TMA-store staging."""
+    g = ir.conv_chain(2, 64, 64, 56, 3, 1, 1)
+    seqs = runtime.decode_layout(g, 1, [28, 28, 64, 32, 32, 64])
+    for t in ("biased", "y"):
+        seqs[t] = seqs["conv"]
+    inputs, ref = oracle_outputs(g, 21)
+    p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=1, vectorize=1)], flags=_abi.PLAN_REQUIRE_TC)
+    assert "store=2" in p.node_kernel(1), p.node_kernel(1)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    assert np.array_equal(p.get_output("y"), ref["y"])
 
 
 @pytest.mark.parametrize("shape,f", [((1, 512, 512, 7), (7, 7, 128, 64, 64, 128)),

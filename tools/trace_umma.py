@@ -46,6 +46,8 @@ def timeline(g, cand, inputs, name):
         sp = (t16[:, 16:20] - t16[:, :1]) / 1000.0
         print("  split-K: published %.2f fenced %.2f spin-done %.2f slices-landed %.2f us" %
               tuple(np.median(sp, axis=0)))
+    if (t16[:, 28] > 0).all():
+        print("  unit-0 first tmem_ld done %.2f us after epi start" % np.median((t16[:, 28] - t16[:, 8]) / 1000.0))
     t = t16[:, :8]
     ep = (t16[:, 8:16] - t16[:, :1]) / 1000.0
     for k in range(4):
@@ -128,6 +130,27 @@ if __name__ == "__main__":
     if os.environ.get("TRACE_RESNET"):
         resnet_b1()
         sys.exit(0)
+    if os.environ.get("TRACE_CONV_VARIANTS"):
+        gc = ir.pad_conv(16, 64, 64, 56, 3, 1, 1)
+        ins = {"x": k64((16, 64, 56, 56)), "ker": k64((64, 64, 3, 3))}
+        for f, sc in [((28, 28, 64, 64, 64, 64), runtime.sched(1, vectorize=1)),
+                      ((28, 28, 64, 32, 32, 64), runtime.sched(1, vectorize=1, unroll=1)),
+                      ((14, 28, 64, 32, 32, 64), runtime.sched(1, vectorize=1))]:
+            try:
+                timeline(gc, tuner.Candidate({1: f}, [sc]), ins, f"conv b16 {f} unroll={sc.unroll}")
+            except Exception as e:
+                print("FAILED", f, e)
+        gg = ir.gemm(50176, 576, 64)
+        for f, tl in [((128, 64, 64), 64), ((128, 32, 64), 64)]:
+            timeline(gg, tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tl, order=1)]),
+                     {"a": k64((50176, 576)), "b": k64((576, 64))}, f"gemm 50176x576x64 {f}")
+        sys.exit(0)
+    if os.environ.get("TRACE_CONV_ONLY"):
+        gc = ir.pad_conv(16, 64, 64, 56, 3, 1, 1)
+        f = (28, 28, 64, 32, 32, 64)
+        timeline(gc, tuner.Candidate({1: f}, [runtime.sched(1)]),
+                 {"x": k64((16, 64, 56, 56)), "ker": k64((64, 64, 3, 3))}, f"conv b16 {f}")
+        sys.exit(0)
     g = ir.gemm(1024, 1024, 1024)
     A, B = k64((1024, 1024)), k64((1024, 1024))
     for f, tl, o in [((256, 1024, 256), 64, 1), ((128, 64, 256), 128, 0)]:
@@ -141,6 +164,6 @@ if __name__ == "__main__":
                  {"a": k64((128, 64)), "b": k64((64, 64))}, "gemm 128x64x64 (1 tile, 1 stage)")
         sys.exit(0)
     gc = ir.pad_conv(16, 64, 64, 56, 3, 1, 1)
-    for f in [(8, 14, 64, 32, 32, 64), (7, 14, 32, 32, 32, 32)]:
+    for f in [(28, 28, 64, 32, 32, 64), (8, 14, 64, 32, 32, 64), (7, 14, 32, 32, 32, 32)]:
         timeline(gc, tuner.Candidate({1: f}, [runtime.sched(1)]),
                  {"x": k64((16, 64, 56, 56)), "ker": k64((64, 64, 3, 3))}, f"conv b16 {f}")
