@@ -38,6 +38,7 @@ struct UmmaParams {
   int32_t epi_kind[kMaxEpi];
   int32_t epi_count;
   int32_t ntiles, nstages, BN, ksteps, pipe, nprod;
+  int32_t dual;  // two MMA issuers: warp 1 takes even units, warp 3 odd ones
   int32_t a_boxes, b_boxes, a_slot, b_slot, tx_bytes;
   uint64_t a_desc, b_desc;  // LBO/SBO/version/layout bits; start address added on device
   uint32_t a_kadv, b_kadv;
@@ -56,6 +57,8 @@ struct UmmaParams {
   // bf16 bytes) at stg_off; per-tile box origins; row positions in the box
   // follow row_off in the SMEM table.
   int32_t stg_off, stg_f32, stg_bf;
+  int32_t stg_nbuf;    // staging buffers per half (ring of bulk groups)
+  int32_t epi_region;  // bytes of the epilogue region (wbuf, or the mode-2 staging it aliases)
   int32_t stg_cstride, stg_cdim;  // >0: transposed box, column j at plane j * stg_cstride
   const int32_t* tile_coords;
   ScatterDesc sc;           // Padding absorbed into this epilogue (sc.enabled)
@@ -491,11 +494,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int stage_bytes = P.a_boxes * P.a_slot + (P.wres ? 0 : P.b_boxes * P.b_slot);
   const int wbytes = P.wres ? P.nstages * P.w_chunk : 0;
   float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes + wbytes);
-  const int stg_bytes = 2 * (P.stg_f32 + P.stg_bf);
-  const float4* s_red =
-      reinterpret_cast<const float4*>(smem + P.ring_bytes + wbytes + kEpiSmemBytes + stg_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + wbytes + kEpiSmemBytes +
-                                               stg_bytes + P.red_bytes);
+  const float4* s_red = reinterpret_cast<const float4*>(smem + P.ring_bytes + wbytes + P.epi_region);
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem + P.ring_bytes + wbytes + P.epi_region + P.red_bytes);
   const int nw = P.wres ? P.nstages : 0;
   const int pipe = P.pipe;
   const uint32_t full0 = smem_u32(bars);
@@ -634,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
     if (dbg && prod == 0 && lane == 0) dbg[2] = gtimer();
-  } else if (warp == 1) {
+  } else if (warp == 1 || (P.dual && warp == 3)) {
     // ---- MMA issuer (whole warp loops; one elected lane issues)
     const uint64_t adesc = P.a_desc, bdesc = P.b_desc;
     const uint32_t idesc = P.idesc, akadv16 = P.a_kadv >> 4, bkadv16 = P.b_kadv >> 4;
@@ -645,9 +646,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     int slot = 0;
     uint32_t phase = 0;
     int i = 0;
+    const int role = warp == 3 ? 1 : 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
       const int split = u % splits;
       const int s_lo = split * nst / splits, s_hi = (split + 1) * nst / splits;
+      if (P.dual && (i & 1) != role) {  // the other issuer's unit: step over its stages
+        for (int s = s_lo; s < s_hi; ++s)
+          if (++slot == pipe) {
+            slot = 0;
+            phase ^= 1;
+          }
+        continue;
+      }
       const int b = i & 1;
       mbar_wait(tempty0 + 8 * b, (static_cast<uint32_t>(i >> 1) & 1u) ^ 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -684,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (leader) umma_commit(tfull0 + 8 * b);
       __syncwarp();
     }
-    if (dbg && leader) dbg[4] = gtimer();
+    if (dbg && leader) atomicMax(dbg + 4, gtimer());
   } else if (warp >= kEpiWarp0) {
     // ---- epilogue (8 warps; warp w reads TMEM lanes 32*(w%4)..+31; the
     // two halves take alternate 16-column chunks)
@@ -705,6 +715,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rows = __ldg(&te->rows), cols = __ldg(&te->cols), n_base = __ldg(&te->n_base);
       const int3 org = make_int3(__ldg(&te->org[0]), __ldg(&te->org[1]), __ldg(&te->org[2]));
       const int64_t obase = __ldg(&te->out_base) + P.col0;
+      int32_t tco[5] = {0, 0, 0, 0, 0};  // TMA-store box origin (mode 2 issuers)
+      if (P.store_mode == 2 && half_leader) {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) tco[d] = __ldg(P.tile_coords + tile * 5 + d);
+      }
       mbar_wait(tfull0 + 8 * b, static_cast<uint32_t>(i >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[5] = gtimer();
@@ -773,10 +788,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           // TMA-store epilogue: registers -> swizzled SMEM box -> one
           // cp.async.bulk.tensor per 16-column chunk; each half owns one
           // staging buffer and its own bulk group.
-          if (half_leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          const bool tr = dbg && (P.diag & 2) && i == ((P.diag & 16) ? 1 : 0) && threadIdx.x == kEpiWarp0 * 32;
+          // Buffer ring per half: chunk n uses buffer n % nbuf, free once at
+          // most nbuf-1 younger bulk groups are still reading.
+          const int nbuf = P.stg_nbuf, bi = ((k - half) >> 1) % nbuf;
+          if (half_leader) {
+            if (nbuf == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          }
           half_bar(half);
+          uint8_t* stf = smem + P.stg_off + (half * nbuf + bi) * P.stg_f32;
+          uint8_t* stb = smem + P.stg_off + 2 * nbuf * P.stg_f32 + (half * nbuf + bi) * P.stg_bf;
+          if (tr) dbg[k == half ? 24 : 29] = gtimer();
           float v[16];
           tmem_ld<16>(tbase + c0, v);
+          if (tr && k == half) dbg[25] = gtimer();
           if (last) {
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -802,24 +828,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (cs) {
               // Transposed box: column j is the plane at j * cs; consecutive
               // rows of a warp are consecutive words (conflict-free).
-              float* sf = reinterpret_cast<float*>(smem + P.stg_off + half * P.stg_f32) + rp;
+              float* sf = reinterpret_cast<float*>(stf) + rp;
 #pragma unroll
               for (int j = 0; j < 16; ++j) sf[j * cs] = v[j];
               if (P.stg_bf) {
-                __nv_bfloat16* sb =
-                    reinterpret_cast<__nv_bfloat16*>(smem + P.stg_off + 2 * P.stg_f32 + half * P.stg_bf) + rp;
+                __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(stb) + rp;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) sb[j * cs] = __float2bfloat16_rn(v[j]);
               }
             } else {
             // SWIZZLE_64B rows of 16 fp32: 16-byte chunk j at j ^ ((rp >> 1) & 3)
-            uint8_t* sf = smem + P.stg_off + half * P.stg_f32 + rp * 64;
+            uint8_t* sf = stf + rp * 64;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               *reinterpret_cast<float4*>(sf + ((j ^ ((rp >> 1) & 3)) << 4)) =
                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             if (P.stg_bf) {  // SWIZZLE_32B rows of 16 bf16: chunk j at j ^ ((rp >> 2) & 1)
-              uint8_t* sb = smem + P.stg_off + 2 * P.stg_f32 + half * P.stg_bf + rp * 32;
+              uint8_t* sb = stb + rp * 32;
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
                 uint4 pk;
@@ -836,18 +861,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             }
           }
+          if (tr && k == half) dbg[26] = gtimer();
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           half_bar(half);
+          if (tr && k == half) dbg[27] = gtimer();
           if (half_leader) {
-            const int32_t* tc = P.tile_coords + tile * 5;
             const int cd = P.stg_cdim;
-            const int32_t x0 = __ldg(tc) + (cd == 0 ? c0 : 0), x1 = __ldg(tc + 1) + (cd == 1 ? c0 : 0),
-                          x2 = __ldg(tc + 2) + (cd == 2 ? c0 : 0), x3 = __ldg(tc + 3) + (cd == 3 ? c0 : 0),
-                          x4 = __ldg(tc + 4) + (cd == 4 ? c0 : 0);
-            tma_store5(&tma_o, smem_u32(smem + P.stg_off + half * P.stg_f32), x0, x1, x2, x3, x4);
+            const int32_t x0 = tco[0] + (cd == 0 ? c0 : 0), x1 = tco[1] + (cd == 1 ? c0 : 0),
+                          x2 = tco[2] + (cd == 2 ? c0 : 0), x3 = tco[3] + (cd == 3 ? c0 : 0),
+                          x4 = tco[4] + (cd == 4 ? c0 : 0);
+            tma_store5(&tma_o, smem_u32(stf), x0, x1, x2, x3, x4);
             if (P.stg_bf)
-              tma_store5(&tma_ob, smem_u32(smem + P.stg_off + 2 * P.stg_f32 + half * P.stg_bf), x0,
-                         x1, x2, x3, x4);
+              tma_store5(&tma_ob, smem_u32(stb), x0, x1, x2, x3, x4);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         } else {
@@ -1136,6 +1161,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     }
     t->p[6] = up(p.ost.tile_coords);
     L.d_tcoords = t->p[6];
+    L.stg_nbuf = (L.BN / L.splits / 16 + 1) / 2 >= 2 ? 2 : 1;
   }
   if (sm_env && atoi(sm_env) == 0) {  // diagnostics: force the generic path
     L.store_mode = 0;
@@ -1147,11 +1173,16 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     const size_t ring = static_cast<size_t>(L.pipe) *
                         (L.a_boxes * L.a_slot + (p.wres ? 0 : L.b_boxes * L.b_slot));
     L.ring_bytes = static_cast<int>((ring + 1023) / 1024 * 1024);
-    L.smem = 1024 + L.ring_bytes + wbytes + kEpiSmemBytes + 2 * (L.stg_f32 + L.stg_bf) + L.red_bytes +
+    // Mode 2 stages in the epilogue region (its transpose buffers are
+    // unused then): two buffers per half when a half stores >= 2 chunks.
+    L.epi_region = std::max(kEpiSmemBytes, 2 * L.stg_nbuf * (L.stg_f32 + L.stg_bf));
+    L.smem = 1024 + L.ring_bytes + wbytes + L.epi_region + L.red_bytes +
              8 * (2 * L.pipe + 5 + (p.wres ? p.stages.size() : 0)) + 8 +
              sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 8 * 128 + 64;
     if (L.smem <= 227 * 1024) break;
-    if (L.pipe > 2) {
+    if (L.stg_nbuf > 1 && L.pipe <= 4) {
+      L.stg_nbuf = 1;
+    } else if (L.pipe > 2) {
       --L.pipe;
     } else if (L.splits > 1) {  // then give up split-K slices
       --L.splits;
@@ -1195,6 +1226,21 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     if (e) per = std::max(1, std::min(atoi(e), L.per_sm));
     L.grid = std::min(L.ntiles * L.splits, per * sms / L.splits * L.splits);
   }
+  // Two MMA issuers. One thread issues a tcgen05.mma only every ~80 cycles
+  // (tools/micro/mma_rate.cu: M=128 N<=128 tops out at 84 cycles per MMA
+  // from one thread, while two issuing warps on different SM sub-partitions
+  // reach 48 (N=64) and the dense peak (N=128)), so N <= 128 tiles are
+  // issue-bound. Warp 3 becomes a second issuer taking every other unit
+  // (own TMEM accumulator, the ring's stages in order), leaving two TMA
+  // producers. Worth it when a CTA gets >= 2 units and two units' stages
+  // fit in the ring together.
+  {
+    const int units = L.ntiles * L.splits;
+    const int spu = (L.nstages + L.splits - 1) / L.splits;
+    L.dual = p.BN <= 128 && units >= 2 * L.grid && 2 * spu <= L.pipe;
+    if (const char* e = getenv("LFGPU_DUAL_MMA")) L.dual = atoi(e) != 0;
+    if (L.dual) L.nprod = std::min(L.nprod, 2);
+  }
   static_assert(sizeof(TileEntry) == 192, "TileEntry layout");
   return L;
 }
@@ -1220,6 +1266,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.ksteps = L.KC / 16;
   P.pipe = L.pipe;
   P.nprod = L.nprod;
+  P.dual = L.dual;
   P.a_boxes = L.a_boxes;
   P.b_boxes = L.b_boxes;
   P.a_slot = L.a_slot;
@@ -1231,7 +1278,9 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.w_tx = L.w_tx;
   P.red_bytes = L.red_bytes;
   P.stg_f32 = L.stg_f32;
-  P.stg_off = L.ring_bytes + (L.wres ? L.nstages * L.w_chunk : 0) + kEpiSmemBytes;
+  P.stg_off = L.ring_bytes + (L.wres ? L.nstages * L.w_chunk : 0);
+  P.stg_nbuf = L.stg_nbuf;
+  P.epi_region = L.epi_region;
   P.stg_bf = L.stg_bf;
   P.tile_coords = static_cast<const int32_t*>(L.d_tcoords);
   P.sc = L.scatter;

@@ -728,7 +728,8 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           P->tc_nodes += 1;
           P->bytes += A.numel * 2 + B.numel * 2 + P->t[final_t].numel * 4;
           P->summary[ni] = up.summary + " store=" + std::to_string(L.store_mode) +
-                           " splits=" + std::to_string(L.splits) + " grid=" + std::to_string(L.grid);
+                           " splits=" + std::to_string(L.splits) + " grid=" + std::to_string(L.grid) +
+                           (L.dual ? " dual" : "");
         } else {
           GenContract G;
           G.op = n.kind == LFGPU_OP_GMM ? GEN_GMM : n.kind == LFGPU_OP_C2D ? GEN_C2D : GEN_DEP;

@@ -167,6 +167,7 @@ struct UmmaLaunch {
   int wres = 0, w_chunk = 0, w_tx = 0;
   CUtensorMap tma_o, tma_ob;     // store mode 2: fp32 output and its bf16 copy
   int stg_off = 0, stg_f32 = 0, stg_bf = 0;
+  int stg_nbuf = 1, epi_region = kEpiSmemBytes;
   int stg_cstride = 0, stg_cdim = 0;  // transposed TMA-store box (OutStore::col_stride / col_dim)
   void* d_tcoords = nullptr;
   ScatterDesc scatter;
@@ -175,6 +176,7 @@ struct UmmaLaunch {
   int store_mode = 0;           // 1: transposed float4 row stores; 0: generic
   int64_t col0 = 0;
   int splits = 1;               // split-K factor (k_umma.cu)
+  int dual = 0;                 // two MMA issuers (warps 1 and 3) on alternate units
   float* ws = nullptr;          // split-K partial tiles
   int* counters = nullptr;      // split-K per-tile arrival counters
   std::shared_ptr<void> owner;  // keeps the device tables alive

@@ -48,6 +48,11 @@ def timeline(g, cand, inputs, name):
               tuple(np.median(sp, axis=0)))
     if (t16[:, 28] > 0).all():
         print("  unit-0 first tmem_ld done %.2f us after epi start" % np.median((t16[:, 28] - t16[:, 8]) / 1000.0))
+    if (t16[:, 24] > 0).all():
+        e0 = 9 if int(os.environ.get("LFGPU_UMMA_DIAG", "0")) & 16 else 8
+        r = lambda k: np.median((t16[:, k] - t16[:, e0]) / 1000.0)
+        print("  mode-2 chunk0 (us after epi start): waited %.2f ld %.2f staged %.2f barred %.2f | chunk1 waited %.2f"
+              % (r(24), r(25), r(26), r(27), r(29)))
     t = t16[:, :8]
     ep = (t16[:, 8:16] - t16[:, :1]) / 1000.0
     for k in range(4):
