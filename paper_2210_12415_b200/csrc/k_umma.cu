@@ -483,6 +483,12 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
   }
 }
 
+// Instantiated per store mode and split-K (MODE, SPLITK): each instance
+// carries only its epilogue path. The epilogue runs a few times per SM per
+// launch, so its code is fetched cold; a smaller instance misses the
+// instruction caches less (ncu: ~2300 L1i misses per SM on the
+// all-paths kernel).
+template <int MODE, bool SPLITK>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_kernel(const __grid_constant__ CUtensorMap tma_a,
                 const __grid_constant__ CUtensorMap tma_b, const __grid_constant__ UmmaParams P,
@@ -514,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int32_t* s_rowrel = s_rowpos + 128;                                   // C2D: (dh << 16) | dw
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int splits = P.splits;
+  const int splits = SPLITK ? P.splits : 1;
   const int nunits = P.ntiles * splits;
   const int nst = P.nstages;
   unsigned long long* dbg = P.dbg ? P.dbg + 32 * blockIdx.x : nullptr;
@@ -534,6 +540,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+    if (MODE == 2) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_o)) : "memory");
+      if (P.stg_bf)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_ob)) : "memory");
+    }
   }
   {  // plan tables (written once by the host, never by kernels: safe before
      // the PDL wait). One flat int array [stages | col_off | row_off]; all
@@ -716,18 +727,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int3 org = make_int3(__ldg(&te->org[0]), __ldg(&te->org[1]), __ldg(&te->org[2]));
       const int64_t obase = __ldg(&te->out_base) + P.col0;
       int32_t tco[5] = {0, 0, 0, 0, 0};  // TMA-store box origin (mode 2 issuers)
-      if (P.store_mode == 2 && half_leader) {
+      if (MODE == 2 && half_leader) {
 #pragma unroll
         for (int d = 0; d < 5; ++d) tco[d] = __ldg(P.tile_coords + tile * 5 + d);
       }
       mbar_wait(tfull0 + 8 * b, static_cast<uint32_t>(i >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[5] = gtimer();
+      if (dbg && (P.diag & 32) && i == 0 && lane == 0) dbg[24 + warp - kEpiWarp0] = gtimer();
       if (dbg && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[8 + i] = gtimer();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * BN);
       const int64_t ws_tile = static_cast<int64_t>(tile) * splits;
       const int red_lo = split * (BN / splits);
-      const int mode = P.store_mode;
+      constexpr int mode = MODE;
       // Items are 16-column chunks (one small inlined body: each SM runs the
       // epilogue only a few times per launch, so code size is paid in cold
       // instruction fetches): first (split-K only) the columns the sibling
@@ -1306,11 +1318,18 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.ws = L.ws;
   P.counters = L.counters;
   P.dbg = static_cast<unsigned long long*>(umma_debug_buffer());
+  using KernelFn = void (*)(CUtensorMap, CUtensorMap, UmmaParams, CUtensorMap, CUtensorMap);
+  static const KernelFn fns[3][2] = {{umma_kernel<0, false>, umma_kernel<0, true>},
+                                     {umma_kernel<1, false>, umma_kernel<1, true>},
+                                     {umma_kernel<2, false>, umma_kernel<2, true>}};
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    for (auto& row : fns)
+      for (auto f : row)
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
+  const KernelFn fn = fns[std::min(std::max(L.store_mode, 0), 2)][L.splits > 1 ? 1 : 0];
   // Programmatic dependent launch: the prologue (barriers, TMEM, tables)
   // overlaps the previous kernel; the kernel waits (griddepcontrol.wait)
   // before touching operands or outputs.
@@ -1329,7 +1348,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, umma_kernel, L.tma_a, L.tma_b, P, L.tma_o, L.tma_ob);
+  return cudaLaunchKernelEx(&cfg, fn, L.tma_a, L.tma_b, P, L.tma_o, L.tma_ob);
 }
 
 }  // namespace lfg

@@ -71,6 +71,10 @@ def conv_halo(reps=3, nb=16, factors=(7, 14, 32, 32, 32, 32)):
     conv(reps, nb, factors)
 
 
+def conv_b16best(reps=3):
+    conv(reps, 16, (8, 28, 64, 32, 32, 64))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["gemm", "conv", "transform"]
     for w in which:

@@ -48,7 +48,11 @@ def timeline(g, cand, inputs, name):
               tuple(np.median(sp, axis=0)))
     if (t16[:, 28] > 0).all():
         print("  unit-0 first tmem_ld done %.2f us after epi start" % np.median((t16[:, 28] - t16[:, 8]) / 1000.0))
-    if (t16[:, 24] > 0).all():
+    if int(os.environ.get("LFGPU_UMMA_DIAG", "0")) & 32:
+        w = (t16[:, 24:32] - t16[:, 8:9]) / 1000.0
+        print("  epilogue warps 4..11 wake after warp 4 (us, median):", " ".join(f"{np.median(w[:, j]):.2f}" for j in range(8)))
+        print("  tmem alloc/tfull ready (acc_ready) vs wake of last warp (us, median): %.2f" % np.median(w.max(axis=1)))
+    elif (t16[:, 24] > 0).all():
         e0 = 9 if int(os.environ.get("LFGPU_UMMA_DIAG", "0")) & 16 else 8
         r = lambda k: np.median((t16[:, k] - t16[:, e0]) / 1000.0)
         print("  mode-2 chunk0 (us after epi start): waited %.2f ld %.2f staged %.2f barred %.2f | chunk1 waited %.2f"
