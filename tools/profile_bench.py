@@ -17,7 +17,7 @@ def k64(shape):
     return torch.randint(-64, 65, shape, device="cuda").float() / 64
 
 
-def gemm(reps=3, f=(128, 128, 128), tile=64, order=0):
+def gemm(reps=3, f=(128, 1024, 64), tile=64, order=0):
     g = ir.gemm(1024, 1024, 1024)
     c = tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tile, order=order)])
     p = runtime.Plan(g, tuner.seqs_for(g, c), c.scheds, _abi.PLAN_REQUIRE_TC)
@@ -29,7 +29,7 @@ def gemm(reps=3, f=(128, 128, 128), tile=64, order=0):
     torch.cuda.synchronize()
 
 
-def conv16(reps=3, f=(8, 14, 64, 32, 32, 64)):
+def conv16(reps=3, f=(28, 28, 64, 32, 32, 64)):
     g = ir.bare_conv(16, 64, 64, 58, 3, 1)
     gp = ir.pad_conv(16, 64, 64, 56, 3, 1, 1)
     s = runtime.decode_layout(gp, 1, list(f))
