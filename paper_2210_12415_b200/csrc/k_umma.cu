@@ -327,14 +327,17 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
                                        const int64_t* s_col, int mode, int split, int splits,
                                        int64_t ws_tile, const float4* red, int red_lo,
                                        bool release, uint32_t tempty, int3 org,
-                                       const int32_t* s_rowrel) {
+                                       const int32_t* s_rowrel, bool dry) {
+  if (P.dbg && !dry && (P.diag & 2) && threadIdx.x == kEpiWarp0 * 32 && c0 == 0 &&
+      P.dbg[32 * blockIdx.x + 30] == 0)
+    P.dbg[32 * blockIdx.x + 30] = gtimer();
   float v[W];
   tmem_ld<W>(taddr + c0, v);
-  if (P.dbg && (P.diag & 2) && threadIdx.x == kEpiWarp0 * 32 && c0 == 0 &&
+  if (P.dbg && !dry && (P.diag & 2) && threadIdx.x == kEpiWarp0 * 32 && c0 == 0 &&
       P.dbg[32 * blockIdx.x + 28] == 0)
     P.dbg[32 * blockIdx.x + 28] = gtimer();
 
-  if (release) {
+  if (release && !dry) {
     // Every TMEM read of this accumulator is complete: hand it back to the MMA.
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncwarp();
@@ -414,11 +417,15 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
         }
       }
     }
+    if (dry || (P.diag & 1)) return;  // warm-up pass / timing knob: no side effects
 #pragma unroll
     for (int it = 0; it < IT; ++it)
       if (ok[it]) *reinterpret_cast<float4*>(P.out + addr[it]) = x[it];
     if (P.sc.enabled) {
-#pragma unroll 1
+      // Unrolled: a rolled loop indexes x[] / ok[] dynamically and moves
+      // them to local memory for the whole epilogue (ncu: STL.128 on the
+      // store path of every mode-1 launch).
+#pragma unroll
       for (int it = 0; it < IT; ++it)
         if (ok[it]) {
           const int rel = s_rowrel[q * 32 + it * RPI + lane / LPR];
@@ -440,7 +447,7 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
     return;
   }
   // Generic: thread = row, 8 columns per step (loads, ops, stores batched).
-  if (P.diag & 1) return;
+  if (dry || (P.diag & 1)) return;
   if (row < rows && s_row[row] >= 0) {
     const int64_t rb = obase + s_row[row];
     const float* mine = wbuf + lane * kEpiLd;
@@ -716,7 +723,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int BN = P.BN;
     uint32_t red_phase = 0;
     int i = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+    // Warm-up pass: the epilogue code is fetched cold (a few runs per SM per
+    // launch), so the idle epilogue warps first run their path once over
+    // the first unit with every side effect off (no accumulator wait, no
+    // stores, no barrier arrivals) while the main loop fills TMEM; the real
+    // pass then executes from a warm instruction cache.
+    bool dry = !SPLITK && !(P.diag & 64);
+    for (int u = blockIdx.x; u < nunits;) {
       const int tile = u / splits, split = u - tile * splits;
       const int b = i & 1;
       const uint32_t tempty = tempty0 + 8 * b;
@@ -731,11 +744,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int d = 0; d < 5; ++d) tco[d] = __ldg(P.tile_coords + tile * 5 + d);
       }
-      mbar_wait(tfull0 + 8 * b, static_cast<uint32_t>(i >> 1) & 1u);
+      if (!dry) mbar_wait(tfull0 + 8 * b, static_cast<uint32_t>(i >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[5] = gtimer();
-      if (dbg && (P.diag & 32) && i == 0 && lane == 0) dbg[24 + warp - kEpiWarp0] = gtimer();
-      if (dbg && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[8 + i] = gtimer();
+      if (dbg && !dry && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[5] = gtimer();
+      if (dbg && !dry && (P.diag & 32) && i == 0 && lane == 0) dbg[24 + warp - kEpiWarp0] = gtimer();
+      if (dbg && !dry && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[8 + i] = gtimer();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * BN);
       const int64_t ws_tile = static_cast<int64_t>(tile) * splits;
       const int red_lo = split * (BN / splits);
@@ -755,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int it = half; it < npub; it += 2) {
         const int c0 = it * 16 < lo ? it * 16 : it * 16 + sl;
         epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, 3,
-                      split, splits, ws_tile, s_red, red_lo, false, tempty, org, s_rowrel);
+                      split, splits, ws_tile, s_red, red_lo, false, tempty, org, s_rowrel, false);
       }
       if (splits > 1) {
         if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[16] = gtimer();
@@ -788,7 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         red_phase ^= 1;
         if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[19] = gtimer();
       }
-      if (half >= nown) {  // nothing for this half: hand the accumulator back now
+      if (half >= nown && !dry) {  // nothing for this half: hand the accumulator back now
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty);
@@ -800,7 +813,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           // TMA-store epilogue: registers -> swizzled SMEM box -> one
           // cp.async.bulk.tensor per 16-column chunk; each half owns one
           // staging buffer and its own bulk group.
-          const bool tr = dbg && (P.diag & 2) && i == ((P.diag & 16) ? 1 : 0) && threadIdx.x == kEpiWarp0 * 32;
+          const bool tr = dbg && !dry && (P.diag & 2) && i == ((P.diag & 16) ? 1 : 0) &&
+                          threadIdx.x == kEpiWarp0 * 32;
           // Buffer ring per half: chunk n uses buffer n % nbuf, free once at
           // most nbuf-1 younger bulk groups are still reading.
           const int nbuf = P.stg_nbuf, bi = ((k - half) >> 1) % nbuf;
@@ -815,7 +829,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v[16];
           tmem_ld<16>(tbase + c0, v);
           if (tr && k == half) dbg[25] = gtimer();
-          if (last) {
+          if (last && !dry) {
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty);
@@ -877,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           half_bar(half);
           if (tr && k == half) dbg[27] = gtimer();
-          if (half_leader) {
+          if (half_leader && !dry) {
             const int cd = P.stg_cdim;
             const int32_t x0 = tco[0] + (cd == 0 ? c0 : 0), x1 = tco[1] + (cd == 1 ? c0 : 0),
                           x2 = tco[2] + (cd == 2 ? c0 : 0), x3 = tco[3] + (cd == 3 ? c0 : 0),
@@ -889,9 +903,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col,
-                        mode, split, splits, ws_tile, s_red, red_lo, last, tempty, org, s_rowrel);
+                        mode, split, splits, ws_tile, s_red, red_lo, last, tempty, org, s_rowrel, dry);
         }
-        if (dbg && i == 0 && k < 8 && threadIdx.x == kEpiWarp0 * 32) dbg[20 + k] = gtimer();
+        if (dbg && !dry && i == 0 && k < 8 && threadIdx.x == kEpiWarp0 * 32) dbg[20 + k] = gtimer();
       }
       if (splits > 1) {
         epi_bar();  // every warp is done with the SMEM slices of this unit
@@ -903,7 +917,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (dbg && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[12 + i] = gtimer();
+      if (dbg && !dry && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[12 + i] = gtimer();
+      if (dry) {  // same unit again, for real
+        dry = false;
+        continue;
+      }
+      u += gridDim.x;
+      ++i;
     }
     if (half_leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (dbg && threadIdx.x == kEpiWarp0 * 32) dbg[6] = gtimer();

@@ -47,7 +47,8 @@ def timeline(g, cand, inputs, name):
         print("  split-K: published %.2f fenced %.2f spin-done %.2f slices-landed %.2f us" %
               tuple(np.median(sp, axis=0)))
     if (t16[:, 28] > 0).all():
-        print("  unit-0 first tmem_ld done %.2f us after epi start" % np.median((t16[:, 28] - t16[:, 8]) / 1000.0))
+        print("  unit-0 first tmem_ld: issued %.2f done %.2f us after epi start" %
+              (np.median((t16[:, 30] - t16[:, 8]) / 1000.0), np.median((t16[:, 28] - t16[:, 8]) / 1000.0)))
     if int(os.environ.get("LFGPU_UMMA_DIAG", "0")) & 32:
         w = (t16[:, 24:32] - t16[:, 8:9]) / 1000.0
         print("  epilogue warps 4..11 wake after warp 4 (us, median):", " ".join(f"{np.median(w[:, j]):.2f}" for j in range(8)))
@@ -162,7 +163,7 @@ if __name__ == "__main__":
         sys.exit(0)
     g = ir.gemm(1024, 1024, 1024)
     A, B = k64((1024, 1024)), k64((1024, 1024))
-    for f, tl, o in [((256, 1024, 256), 64, 1), ((128, 64, 256), 128, 0)]:
+    for f, tl, o in [((128, 1024, 64), 64, 0), ((128, 64, 256), 128, 0)]:
         timeline(g, tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tl, order=o)]), {"a": A, "b": B},
                  f"gemm {f} tile {tl} order {o}")
     if os.environ.get("TRACE_GEMM_ONLY"):
