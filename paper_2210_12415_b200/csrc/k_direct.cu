@@ -83,6 +83,186 @@ __global__ void __launch_bounds__(kDThreads)
   }
 }
 
+// ---- K6: depthwise (DEP) -----------------------------------------------
+// K > 0: square KxK window unrolled with its offsets in registers; K == 0:
+// any window through the tables.
+template <int K>
+__global__ void __launch_bounds__(256) dep_direct(const DirectDep P) {
+  LFG_PDL_ENTRY();
+  const int64_t total = static_cast<int64_t>(P.N) * P.C * P.Ho * P.Wo;
+  const int64_t* xt = P.xt;
+  const int64_t* wt = P.wt;
+  const int64_t* ot = P.ot;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r = e;
+    int n, c, h, w;
+    if (P.fast == 1) {  // (c, w, h, n) from fastest to slowest
+      c = static_cast<int>(r % P.C), r /= P.C;
+      w = static_cast<int>(r % P.Wo), r /= P.Wo;
+      h = static_cast<int>(r % P.Ho), n = static_cast<int>(r / P.Ho);
+    } else {  // (w, h, c, n)
+      w = static_cast<int>(r % P.Wo), r /= P.Wo;
+      h = static_cast<int>(r % P.Ho), r /= P.Ho;
+      c = static_cast<int>(r % P.C), n = static_cast<int>(r / P.C);
+    }
+    const int64_t xb = __ldg(xt + P.x_off[0] + n) + __ldg(xt + P.x_off[1] + c);
+    const int64_t wb = __ldg(wt + P.w_off[0] + c);
+    const int64_t* xh = xt + P.x_off[2] + static_cast<int64_t>(P.V) * h;
+    const int64_t* xw = xt + P.x_off[3] + static_cast<int64_t>(P.V) * w;
+    float acc = 0.f;
+    if constexpr (K > 0) {
+      int64_t ow[K], kw[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) ow[j] = __ldg(xw + j), kw[j] = __ldg(wt + P.w_off[2] + j);
+#pragma unroll
+      for (int rh = 0; rh < K; ++rh) {
+        const int64_t oh = xb + __ldg(xh + rh), kh = wb + __ldg(wt + P.w_off[1] + rh);
+#pragma unroll
+        for (int rw = 0; rw < K; ++rw) acc = fmaf(__ldg(P.x + oh + ow[rw]), __ldg(P.w + kh + kw[rw]), acc);
+      }
+    } else {
+      for (int rh = 0; rh < P.KH; ++rh) {
+        const int64_t oh = xb + __ldg(xh + rh), kh = wb + __ldg(wt + P.w_off[1] + rh);
+        for (int rw = 0; rw < P.KW; ++rw)
+          acc = fmaf(__ldg(P.x + oh + __ldg(xw + rw)), __ldg(P.w + kh + __ldg(wt + P.w_off[2] + rw)), acc);
+      }
+    }
+    const int64_t off = __ldg(ot + P.o_off[0] + n) + __ldg(ot + P.o_off[1] + c) +
+                        __ldg(ot + P.o_off[2] + h) + __ldg(ot + P.o_off[3] + w);
+    for (int k = 0; k < P.nepi; ++k) {
+      if (P.epi_kind[k] == DIRECT_EPI_BIAS) acc += __ldg(P.epi_ptr[k] + c);
+      else if (P.epi_kind[k] == DIRECT_EPI_RESIDUAL) acc += __ldg(P.epi_ptr[k] + off);
+      else acc = acc > 0.f ? acc : 0.f;
+    }
+    P.out[off] = acc;
+  }
+}
+
+// Channel-vectorised K6: four consecutive channels per thread as float4
+// (channel-brick layouts: C is unit-stride in 4-aligned groups in the input,
+// the weights and the output, every other table entry a multiple of 4), and
+// a strip of WS outputs along W per thread so each input column and each
+// table entry is loaded once per strip instead of once per tap.
+template <int K, int V, int WS>
+__global__ void __launch_bounds__(256, (K == 3 ? 3 : 2)) dep_direct4(const DirectDep P) {
+  LFG_PDL_ENTRY();
+  constexpr int NC = (WS - 1) * V + K;  // input columns a strip touches
+  const int C4 = P.C >> 2, WSN = (P.Wo + WS - 1) / WS;
+  const int64_t total = static_cast<int64_t>(P.N) * C4 * P.Ho * WSN;
+  const int64_t* xt = P.xt;
+  const int64_t* wt = P.wt;
+  const int64_t* ot = P.ot;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r = e;
+    const int c = static_cast<int>(r % C4) * 4;
+    r /= C4;
+    const int w0 = static_cast<int>(r % WSN) * WS;
+    r /= WSN;
+    const int h = static_cast<int>(r % P.Ho), n = static_cast<int>(r / P.Ho);
+    const int64_t xb = __ldg(xt + P.x_off[0] + n) + __ldg(xt + P.x_off[1] + c);
+    const int64_t wb = __ldg(wt + P.w_off[0] + c);
+    const int64_t* xh = xt + P.x_off[2] + static_cast<int64_t>(V) * h;
+    // Columns past the padded input (a ragged last strip) read column 0:
+    // their outputs are not stored.
+    const int Wi = (P.Wo - 1) * V + K;
+    int64_t oc[NC], kw[K];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int col = w0 * V + j;
+      oc[j] = __ldg(xt + P.x_off[3] + (col < Wi ? col : 0));
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) kw[j] = __ldg(wt + P.w_off[2] + j);
+    float4 acc[WS];
+#pragma unroll
+    for (int o = 0; o < WS; ++o) acc[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int rh = 0; rh < K; ++rh) {
+      const int64_t oh = xb + __ldg(xh + rh), kh = wb + __ldg(wt + P.w_off[1] + rh);
+      float4 wv[K];
+#pragma unroll
+      for (int rw = 0; rw < K; ++rw) wv[rw] = __ldg(reinterpret_cast<const float4*>(P.w + kh + kw[rw]));
+      float4 xv[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) xv[j] = __ldg(reinterpret_cast<const float4*>(P.x + oh + oc[j]));
+      // (rh, rw) order per output, as interp.cpp:90-108 accumulates.
+#pragma unroll
+      for (int o = 0; o < WS; ++o)
+#pragma unroll
+        for (int rw = 0; rw < K; ++rw) {
+          const float4 a = xv[o * V + rw], b = wv[rw];
+          acc[o].x = fmaf(a.x, b.x, acc[o].x);
+          acc[o].y = fmaf(a.y, b.y, acc[o].y);
+          acc[o].z = fmaf(a.z, b.z, acc[o].z);
+          acc[o].w = fmaf(a.w, b.w, acc[o].w);
+        }
+    }
+    const int64_t ob = __ldg(ot + P.o_off[0] + n) + __ldg(ot + P.o_off[1] + c) + __ldg(ot + P.o_off[2] + h);
+#pragma unroll
+    for (int o = 0; o < WS; ++o) {
+      const bool live = w0 + o < P.Wo;
+      const int64_t off = ob + __ldg(ot + P.o_off[3] + (live ? w0 + o : 0));
+      float4 v = acc[o];
+      for (int k = 0; k < P.nepi; ++k) {
+        if (P.epi_kind[k] == DIRECT_EPI_RELU) {
+          v.x = fmaxf(v.x, 0.f), v.y = fmaxf(v.y, 0.f), v.z = fmaxf(v.z, 0.f), v.w = fmaxf(v.w, 0.f);
+        } else {
+          const float* ep = P.epi_ptr[k];
+          const float4 b = P.epi_kind[k] == DIRECT_EPI_BIAS
+                               ? make_float4(__ldg(ep + c), __ldg(ep + c + 1), __ldg(ep + c + 2), __ldg(ep + c + 3))
+                               : __ldg(reinterpret_cast<const float4*>(ep + off));
+          v.x += b.x, v.y += b.y, v.z += b.z, v.w += b.w;
+        }
+      }
+      if (live) *reinterpret_cast<float4*>(P.out + off) = v;
+    }
+  }
+}
+
+template <int K, int V>
+static void launch_dep4(const DirectDep& P, unsigned grid, cudaStream_t stream) {
+  launch_pdl(dep_direct4<K, V, 2>, dim3(grid), dim3(256), 0, stream, P);
+}
+
+cudaError_t launch_dep_direct(const DirectDep& P, cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(P.N) * P.C * P.Ho * P.Wo;
+  if (total == 0) return cudaSuccess;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  }
+  // Grid: enough 256-thread blocks for one output each, capped at 8 waves
+  // of 148 SMs x 8 resident blocks (grid-stride beyond).
+  const int64_t want = (total + 255) / 256;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(sms) * 8 * 8));
+  const bool sq = P.KH == P.KW;
+  if (P.vec4 && sq && (P.KH == 3 || P.KH == 5 || P.KH == 7) && (P.V == 1 || P.V == 2)) {
+    const int ws = 2;
+    const int64_t strips = static_cast<int64_t>(P.N) * (P.C / 4) * P.Ho * ((P.Wo + ws - 1) / ws);
+    const unsigned g4 = static_cast<unsigned>(std::min<int64_t>((strips + 255) / 256,
+                                                                static_cast<int64_t>(sms) * 64));
+    if (P.V == 1) {
+      if (P.KH == 3) launch_dep4<3, 1>(P, g4, stream);
+      else if (P.KH == 5) launch_dep4<5, 1>(P, g4, stream);
+      else launch_dep4<7, 1>(P, g4, stream);
+    } else {
+      if (P.KH == 3) launch_dep4<3, 2>(P, g4, stream);
+      else if (P.KH == 5) launch_dep4<5, 2>(P, g4, stream);
+      else launch_dep4<7, 2>(P, g4, stream);
+    }
+    return cudaGetLastError();
+  }
+  if (sq && P.KH == 3) launch_pdl(dep_direct<3>, dim3(grid), dim3(256), 0, stream, P);
+  else if (sq && P.KH == 5) launch_pdl(dep_direct<5>, dim3(grid), dim3(256), 0, stream, P);
+  else if (sq && P.KH == 7) launch_pdl(dep_direct<7>, dim3(grid), dim3(256), 0, stream, P);
+  else launch_pdl(dep_direct<0>, dim3(grid), dim3(256), 0, stream, P);
+  return cudaGetLastError();
+}
+
 bool direct_conv_applies(int64_t I, int64_t KH, int64_t KW, int64_t O) {
   return I * KH * KW <= 512 && I < 16 && O % kDOC == 0;
 }

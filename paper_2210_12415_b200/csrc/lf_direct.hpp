@@ -25,6 +25,34 @@ struct DirectConv {
   const float* epi_ptr[4] = {};        // bias: logical [O]; residual: output layout
 };
 
+// K6: depthwise C2D (DEP, interp.cpp:90-108) on tuned layouts. Every
+// operand is addressed through per-logical-dim offset tables (the layout
+// must be separable: split / reorder / fuse / unfold / pad), one thread
+// per output element, threads ordered so that `fast` — the output's
+// unit-stride logical dim (C for channel bricks, W for NCHW) — varies
+// fastest: loads and stores coalesce. Accumulates in fp32 in the
+// reference's (rh, rw) order; the fused element-wise chain runs before
+// the store.
+struct DirectDep {
+  int32_t N = 0, C = 0, Ho = 0, Wo = 0, KH = 0, KW = 0, V = 1;
+  int32_t fast = 1;                    // 1: C fastest, 3: W fastest
+  int32_t vec4 = 0;                    // float4 over 4 channels (dep_direct4)
+  const float* x = nullptr;            // padded input, its own layout
+  const int64_t* xt = nullptr;         // input tables (n, c, h, w)
+  int64_t x_off[4] = {};
+  const float* w = nullptr;            // weights [C][KH][KW], their own layout
+  const int64_t* wt = nullptr;
+  int64_t w_off[3] = {};
+  float* out = nullptr;
+  const int64_t* ot = nullptr;         // output tables (n, c, h, w)
+  int64_t o_off[4] = {};
+  int32_t nepi = 0;
+  int32_t epi_kind[4] = {};
+  const float* epi_ptr[4] = {};        // bias: logical [C]; residual: output layout
+};
+
+cudaError_t launch_dep_direct(const DirectDep& P, cudaStream_t stream);
+
 bool direct_conv_applies(int64_t I, int64_t KH, int64_t KW, int64_t O);
 size_t direct_conv_smem(const DirectConv& P);
 cudaError_t launch_c2d_direct(const DirectConv& P, cudaStream_t stream);

@@ -399,6 +399,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   // 1. Tensor-core eligibility per contraction and fusion chains.
   std::map<int, UmmaPlan> umma;
   std::map<int, std::vector<EpiOp>> direct;  // CUDA-core direct convs (k_direct.cu)
+  std::map<int, std::vector<EpiOp>> depd;    // K6 depthwise (k_direct.cu)
   std::set<int> fused_away;  // element-wise nodes absorbed into an epilogue
   std::vector<int> pos(P->nodes.size(), 0);
   for (size_t k = 0; k < P->order.size(); ++k) pos[P->order[k]] = static_cast<int>(k);
@@ -436,6 +437,21 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   };
   for (int ni : P->order) {
     const auto& n = P->nodes[ni];
+    if (n.kind == LFGPU_OP_DEP && !exact && P->t[n.output].dtype == LFGPU_DTYPE_F32) {
+      // K6 when every operand's layout is separable per logical dim.
+      std::vector<int64_t> tb, of;
+      bool ok = true;
+      for (int t : {n.inputs[0], n.inputs[1], n.output})
+        ok = ok && separable_tables(P->t[t].logical, P->t[t].seq, &tb, &of);
+      if (ok) {
+        lfgpu_sched s{};
+        s.node = ni;
+        if (sched_of.count(ni)) s = sched_of[ni];
+        depd[ni] = s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL) ? fuse_chain(ni, P->t[n.output])
+                                                               : std::vector<EpiOp>{};
+      }
+      continue;
+    }
     if (n.kind != LFGPU_OP_C2D && n.kind != LFGPU_OP_GMM) continue;
     if (exact || P->t[n.output].dtype != LFGPU_DTYPE_F32) continue;
     UmmaPlan up;
@@ -661,7 +677,80 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
         P->flops += 2 * macs;
         auto it = umma.find(ni);
         auto dt = direct.find(ni);
-        if (dt != direct.end()) {
+        auto dp = depd.find(ni);
+        if (dp != depd.end()) {
+          DirectDep D;
+          D.N = static_cast<int32_t>(out.logical[0].extent);
+          D.C = static_cast<int32_t>(out.logical[1].extent);
+          D.Ho = static_cast<int32_t>(out.logical[2].extent);
+          D.Wo = static_cast<int32_t>(out.logical[3].extent);
+          D.KH = static_cast<int32_t>(B.logical[1].extent);
+          D.KW = static_cast<int32_t>(B.logical[2].extent);
+          D.V = static_cast<int32_t>(n.stride);
+          if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "depthwise conv on a bf16-only operand");
+          std::vector<int64_t> xo, wo, oo;
+          D.x = static_cast<const float*>(A.d);
+          D.xt = tables_for(P, A, &xo);
+          for (size_t j = 0; j < xo.size(); ++j) D.x_off[j] = xo[j];
+          D.w = static_cast<const float*>(B.d);
+          D.wt = tables_for(P, B, &wo);
+          for (size_t j = 0; j < wo.size(); ++j) D.w_off[j] = wo[j];
+          const auto& epi = dp->second;
+          const int final_t = epi.empty() ? n.output : epi.back().out_tensor;
+          PTensor& fo = P->t[final_t];
+          D.ot = tables_for(P, fo, &oo);
+          for (size_t j = 0; j < oo.size(); ++j) D.o_off[j] = oo[j];
+          D.out = static_cast<float*>(fo.d);
+          // Thread order follows the output's unit-stride logical dim.
+          {
+            std::vector<int64_t> tb, of;
+            separable_tables(fo.logical, fo.seq, &tb, &of);
+            auto stride_of = [&](int d) {
+              return fo.logical[d].extent > 1 ? tb[of[d] + 1] - tb[of[d]] : INT64_MAX;
+            };
+            D.fast = stride_of(1) <= stride_of(3) ? 1 : 3;
+          }
+          // float4 over channels when C is unit-stride in aligned groups of
+          // 4 in input, weights and output and all other offsets are
+          // multiples of 4 (16-byte aligned float4 accesses).
+          {
+            auto quad_ok = [&](const PTensor& t, int cdim) {
+              std::vector<int64_t> tb, of;
+              if (!separable_tables(t.logical, t.seq, &tb, &of)) return false;
+              if (t.logical[cdim].extent % 4) return false;
+              for (size_t d = 0; d < t.logical.size(); ++d)
+                for (int64_t i = 0; i < t.logical[d].extent; ++i) {
+                  const int64_t v = tb[of[d] + i];
+                  if (static_cast<int>(d) == cdim) {
+                    if (i % 4 == 0 ? v % 4 != 0 : v != tb[of[d] + i - 1] + 1) return false;
+                  } else if (v % 4) {
+                    return false;
+                  }
+                }
+              return true;
+            };
+            bool q = D.fast == 1 && quad_ok(A, 1) && quad_ok(B, 0) && quad_ok(fo, 1);
+            for (size_t e = 0; q && e < epi.size(); ++e)
+              if (epi[e].kind == EPI_RESIDUAL && !quad_ok(P->t[epi[e].tensor], 1)) q = false;
+            D.vec4 = q ? 1 : 0;
+          }
+          D.nepi = static_cast<int32_t>(epi.size());
+          for (size_t e = 0; e < epi.size(); ++e) {
+            D.epi_kind[e] = epi[e].kind == EPI_BIAS ? DIRECT_EPI_BIAS
+                            : epi[e].kind == EPI_RELU ? DIRECT_EPI_RELU
+                                                      : DIRECT_EPI_RESIDUAL;
+            if (epi[e].tensor >= 0) {
+              const PTensor& et = P->t[epi[e].tensor];
+              if (!et.d) fail(LFGPU_EUNSUPPORTED, "epilogue operand has no fp32 buffer");
+              D.epi_ptr[e] = static_cast<const float*>(et.d);
+            }
+          }
+          for (size_t e = 0; e + 1 < epi.size(); ++e) P->t[epi[e].out_tensor].valid = false;
+          if (!epi.empty()) out.valid = false;
+          step.kernel = D.vec4 ? "dep_direct4" : "dep_direct";
+          step.run = [D](cudaStream_t st) { return launch_dep_direct(D, st); };
+          P->bytes += A.numel * 4 + B.numel * 4 + fo.numel * 4;
+        } else if (dt != direct.end()) {
           DirectConv D;
           D.N = static_cast<int32_t>(A.logical[0].extent);
           D.I = static_cast<int32_t>(A.logical[1].extent);

@@ -333,3 +333,36 @@ def test_store_at_rules(seqs, msg):
     with pytest.raises(runtime.LfError) as e:
         runtime.Plan(g, seqs, [])
     assert e.value.code == _abi.EINVAL and msg in str(e.value), str(e.value)
+
+
+@pytest.mark.parametrize("shape,f,fuse", [
+    ((2, 64, 28, 3, 1), None, 0),                    # logical NCHW: W is the fast dim
+    ((2, 64, 28, 3, 1), (7, 14, 32, 32, 32), 1),     # channel bricks, ReLU fused
+    ((1, 96, 27, 5, 2), (13, 13, 32, 32, 32), 1),    # 5x5 stride 2, ragged bricks
+    ((1, 32, 14, 7, 1), (14, 14, 16, 16, 16), 0),    # 7x7
+    ((1, 48, 10, 4, 1), None, 1),                    # even window: the generic-K path
+])
+def test_dep_direct(shape, f, fuse):
+    """K6: DEP (interp.cpp:90-108) on its template layouts (space.cpp:76-90)
+    through the per-dim offset tables, against reference_eval."""
+    n, c, h, k, s = shape
+    g = ir.dep_chain(n, c, h, k, s, k // 2)
+    seqs = {}
+    if f is not None:
+        try:
+            seqs = runtime.decode_layout(g, 1, list(f))
+        except runtime.LfError:
+            pytest.skip("template point not legal for this shape")
+        seqs["y"] = seqs["conv"]
+    inputs, ref = oracle_outputs(g, 13)
+    p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=fuse)])
+    assert p.node_kernel(1).startswith("dep_direct"), p.node_kernel(1)
+    if f is not None and c % 4 == 0 and f[4] % 4 == 0:
+        assert p.node_kernel(1) == "dep_direct4", p.node_kernel(1)
+    if fuse:
+        assert p.node_kernel(2) == "fused"
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    got = p.get_output("y")
+    assert np.array_equal(got, ref["y"]), O.max_rel_diff(got, ref["y"])

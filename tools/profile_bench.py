@@ -52,6 +52,20 @@ def transform(reps=3, n=64):
     torch.cuda.synchronize()
 
 
+def dep16(reps=3, f=(56, 28, 32, 32, 32)):
+    """K6: depthwise 3x3 over 16x256x56x56 on channel-brick layouts."""
+    g = ir.dep_chain(16, 256, 56, 3, 1, 1)
+    seqs = runtime.decode_layout(g, 1, list(f))
+    seqs["y"] = seqs["conv"]
+    p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=1)])
+    p.set_input_device("x", k64((16, 256, 56, 56)))
+    p.set_input_device("ker", k64((256, 3, 3)))
+    print([p.node_kernel(i) for i in range(len(g.nodes))])
+    for _ in range(reps):
+        p.run()
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["all"]
     if which == ["all"]:

@@ -155,6 +155,12 @@ if __name__ == "__main__":
             timeline(gg, tuner.Candidate({0: f}, [runtime.sched(0, tile_last=tl, order=1)]),
                      {"a": k64((50176, 576)), "b": k64((576, 64))}, f"gemm 50176x576x64 {f}")
         sys.exit(0)
+    if os.environ.get("TRACE_INGEST"):  # main-loop time per tile vs number of CTAs pulling
+        for M in (256, 512, 1024):
+            g = ir.gemm(M, 1024, 1024)
+            timeline(g, tuner.Candidate({0: (128, 1024, 64)}, [runtime.sched(0, tile_last=64, order=1)]),
+                     {"a": k64((M, 1024)), "b": k64((1024, 1024))}, f"gemm {M}x1024x1024 BN=64")
+        sys.exit(0)
     if os.environ.get("TRACE_CONV_ONLY"):
         gc = ir.pad_conv(16, 64, 64, 56, 3, 1, 1)
         f = (28, 28, 64, 32, 32, 64)
