@@ -10,6 +10,7 @@
 // (BiasAdd / EwAdd / ReLU, lower.cpp:566-608) is applied before the store,
 // which goes through the output's separable offset tables, so the output may
 // carry any propagated layout.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -260,6 +261,66 @@ cudaError_t launch_dep_direct(const DirectDep& P, cudaStream_t stream) {
   else if (sq && P.KH == 5) launch_pdl(dep_direct<5>, dim3(grid), dim3(256), 0, stream, P);
   else if (sq && P.KH == 7) launch_pdl(dep_direct<7>, dim3(grid), dim3(256), 0, stream, P);
   else launch_pdl(dep_direct<0>, dim3(grid), dim3(256), 0, stream, P);
+  return cudaGetLastError();
+}
+
+// ---- im2col for the tensor-core stem ----------------------------------------
+// One thread per (pixel m, 64-wide k block): lanes take consecutive pixels,
+// so each x read of a warp is one strided run of a row (coalesced), and the
+// thread writes its pixel's whole 128-byte brick row as eight 16-byte
+// stores. (k -> (i, rh, rw) is stepped incrementally, no divisions.)
+__global__ void __launch_bounds__(256) im2col_stem(const Im2col Q) {
+  LFG_PDL_ENTRY();
+  const int kb_n = Q.Kp / 64, hw = Q.Ho * Q.Wo;
+  const int64_t M = static_cast<int64_t>(Q.N) * hw;
+  const int64_t na = M * kb_n, nb = static_cast<int64_t>(Q.O) * (Q.Kp / 8);
+  __nv_bfloat16* A = static_cast<__nv_bfloat16*>(Q.a);
+  __nv_bfloat16* B = static_cast<__nv_bfloat16*>(Q.b);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < na + nb;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    __align__(16) __nv_bfloat16 v[8];
+    if (e < na) {
+      const int kb = static_cast<int>(e / M);
+      const int64_t m = e - static_cast<int64_t>(kb) * M;
+      const int n = static_cast<int>(m / hw), rem = static_cast<int>(m - static_cast<int64_t>(n) * hw);
+      const int ho = rem / Q.Wo, wo = rem - ho * Q.Wo;
+      const float* xb = Q.x + (static_cast<int64_t>(n) * Q.I * Q.H + ho * Q.V) * Q.W + wo * Q.V;
+      int k = kb * 64;
+      int i = k / (Q.KH * Q.KW), r = k - i * Q.KH * Q.KW, rh = r / Q.KW, rw = r - rh * Q.KW;
+      const int64_t mt = m / Q.RT;
+      __nv_bfloat16* dst = A + (mt * kb_n + kb) * (static_cast<int64_t>(Q.RT) * 64) + (m - mt * Q.RT) * 64;
+#pragma unroll 1
+      for (int g = 0; g < 8; ++g) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j, ++k) {
+          float x = 0.f;
+          if (k < Q.K) x = __ldg(xb + (static_cast<int64_t>(i) * Q.H + rh) * Q.W + rw);
+          v[j] = __float2bfloat16_rn(x);
+          if (++rw == Q.KW) {
+            rw = 0;
+            if (++rh == Q.KH) rh = 0, ++i;
+          }
+        }
+        reinterpret_cast<uint4*>(dst)[g] = *reinterpret_cast<const uint4*>(v);
+      }
+    } else {  // B[o][k0..k0+8) as [K0][O][64]
+      const int64_t f = e - na;
+      const int o = static_cast<int>(f / (Q.Kp / 8)), k0 = static_cast<int>(f - static_cast<int64_t>(o) * (Q.Kp / 8)) * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0 + j;
+        v[j] = __float2bfloat16_rn(k < Q.K ? __ldg(Q.w + static_cast<int64_t>(o) * Q.K + k) : 0.f);
+      }
+      *reinterpret_cast<uint4*>(B + (static_cast<int64_t>(k0 >> 6) * Q.O + o) * 64 + (k0 & 63)) =
+          *reinterpret_cast<const uint4*>(v);
+    }
+  }
+}
+
+cudaError_t launch_im2col(const Im2col& Q, cudaStream_t stream) {
+  const int64_t total = static_cast<int64_t>(Q.N) * Q.Ho * Q.Wo * (Q.Kp / 64) + static_cast<int64_t>(Q.O) * (Q.Kp / 8);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 64));
+  launch_pdl(im2col_stem, dim3(grid), dim3(256), 0, stream, Q);
   return cudaGetLastError();
 }
 

@@ -53,6 +53,22 @@ struct DirectDep {
 
 cudaError_t launch_dep_direct(const DirectDep& P, cudaStream_t stream);
 
+// Small-I C2D on tensor cores (the ResNet stem): im2col into K-major
+// [M/RT][Kp/64][RT][64] bf16 bricks (RT = whole output rows per tile) (M = N*Ho*Wo pixels, K = I*KH*KW
+// zero-padded to Kp) plus the weights as [1][Kp/64][O][64] bf16, then the
+// tcgen05 GEMM writes the conv output layout directly. One launch prepares
+// both operands.
+struct Im2col {
+  const float* x = nullptr;  // logical (padded) NCHW input
+  const float* w = nullptr;  // logical OIHW weights
+  void* a = nullptr;         // bf16 A bricks
+  void* b = nullptr;         // bf16 B bricks
+  int32_t N = 0, I = 0, H = 0, W = 0, KH = 0, KW = 0, V = 1, Ho = 0, Wo = 0, O = 0, K = 0, Kp = 0;
+  int32_t RT = 128;          // rows (pixels) per A brick = per GEMM tile
+};
+
+cudaError_t launch_im2col(const Im2col& Q, cudaStream_t stream);
+
 bool direct_conv_applies(int64_t I, int64_t KH, int64_t KW, int64_t O);
 size_t direct_conv_smem(const DirectConv& P);
 cudaError_t launch_c2d_direct(const DirectConv& P, cudaStream_t stream);

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -203,6 +204,7 @@ struct PTensor {
 
 struct PStep {
   int node = -1;
+  int launches = 1;  // kernels this step launches
   std::string kernel;
   std::function<cudaError_t(cudaStream_t)> run;
 };
@@ -400,6 +402,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   std::map<int, UmmaPlan> umma;
   std::map<int, std::vector<EpiOp>> direct;  // CUDA-core direct convs (k_direct.cu)
   std::map<int, std::vector<EpiOp>> depd;    // K6 depthwise (k_direct.cu)
+  std::map<int, UmmaPlan> im2col;            // small-I C2D: im2col + tcgen05 GEMM
   std::set<int> fused_away;  // element-wise nodes absorbed into an epilogue
   std::vector<int> pos(P->nodes.size(), 0);
   for (size_t k = 0; k < P->order.size(); ++k) pos[P->order[k]] = static_cast<int>(k);
@@ -473,6 +476,48 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
                       direct_conv_applies(B.logical[1].extent, B.logical[2].extent,
                                           B.logical[3].extent, B.logical[0].extent);
       if (dc) {
+        // Tensor cores through an im2col operand when the pixel count tiles
+        // by 128 and O fits one UMMA N; else the CUDA-core direct kernel.
+        const int64_t Nb = A.logical[0].extent, Ho = Cc.logical[2].extent, Wo = Cc.logical[3].extent;
+        const int64_t O = B.logical[0].extent;
+        const int64_t K = B.logical[1].extent * B.logical[2].extent * B.logical[3].extent;
+        const int64_t M = Nb * Ho * Wo, Kp = (K + 63) / 64 * 64;
+        UmmaPlan ug;
+        std::string w2;
+        // Rows per tile: whole output rows (the C layout splits Ho and Wo).
+        int64_t RT = 0;
+        if (Wo <= 128) {
+          for (int64_t r = 128 / Wo; r >= 1 && !RT; --r)
+            if (Ho % r == 0) RT = r * Wo;
+        } else {
+          for (int64_t d = 128; d >= 16 && !RT; --d)
+            if (Wo % d == 0) RT = d;
+        }
+        bool ic = !getenv("LFGPU_NO_IM2COL") && RT >= 16 && M % RT == 0 && O % 16 == 0 && O <= 256;
+        if (ic) {
+          const std::vector<Dim> a_log{{"M", M}, {"K", Kp}}, b_log{{"K", Kp}, {"N", O}},
+              c_log{{"M", M}, {"N", O}};
+          const Seq a_seq{make_split(0, {M / RT, RT}), make_split(2, {Kp / 64, 64}),
+                          make_reorder({0, 2, 1, 3})};
+          const Seq b_seq{make_split(0, {Kp / 64, 64}), make_split(2, {1, O}), make_reorder({2, 0, 3, 1})};
+          // C rows are pixels (n, ho, wo): reshape to the conv output's
+          // logical NCHW, then its own sequence: the GEMM writes it in place.
+          Seq c_seq{make_split(0, {Nb, Ho, Wo}), make_reorder({0, 3, 1, 2})};
+          c_seq.insert(c_seq.end(), Cc.seq.begin(), Cc.seq.end());
+          lfgpu_sched s2 = s;
+          s2.tile_last = static_cast<int32_t>(O);
+          s2.order = 1;
+          ic = umma_plan_gemm(a_log, a_seq, b_log, b_seq, c_log, c_seq, s2, &ug, &w2, static_cast<int>(RT));
+          if (!ic && getenv("LFGPU_DEBUG_IM2COL")) fprintf(stderr, "im2col gemm rejected: %s\n", w2.c_str());
+        }
+        if (ic) {
+          if (s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL)) {
+            std::vector<EpiOp> epi = fuse_chain(ni, Cc);
+            for (const auto& e : epi) ug.epi[ug.epi_count++] = e;
+          }
+          im2col[ni] = ug;
+          continue;
+        }
         direct[ni] = s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL) ? fuse_chain(ni, Cc)
                                                                  : std::vector<EpiOp>{};
         continue;
@@ -678,7 +723,60 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
         auto it = umma.find(ni);
         auto dt = direct.find(ni);
         auto dp = depd.find(ni);
-        if (dp != depd.end()) {
+        auto ic = im2col.find(ni);
+        if (ic != im2col.end()) {
+          UmmaPlan up = ic->second;
+          Im2col Q;
+          Q.N = static_cast<int32_t>(A.logical[0].extent);
+          Q.I = static_cast<int32_t>(A.logical[1].extent);
+          Q.H = static_cast<int32_t>(A.logical[2].extent);
+          Q.W = static_cast<int32_t>(A.logical[3].extent);
+          Q.O = static_cast<int32_t>(B.logical[0].extent);
+          Q.KH = static_cast<int32_t>(B.logical[2].extent);
+          Q.KW = static_cast<int32_t>(B.logical[3].extent);
+          Q.V = static_cast<int32_t>(n.stride);
+          Q.Ho = static_cast<int32_t>(out.logical[2].extent);
+          Q.Wo = static_cast<int32_t>(out.logical[3].extent);
+          Q.K = Q.I * Q.KH * Q.KW;
+          Q.Kp = (Q.K + 63) / 64 * 64;
+          Q.RT = up.tiles.empty() ? 128 : up.tiles[0].rows;  // rows per A brick = rows per tile
+          if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "im2col conv on a bf16-only operand");
+          Q.x = static_cast<const float*>(A.d);
+          Q.w = static_cast<const float*>(B.d);
+          const int64_t M = static_cast<int64_t>(Q.N) * Q.Ho * Q.Wo;
+          P->keep.push_back(std::make_unique<DevBuf>(2 * static_cast<size_t>(M) * Q.Kp));
+          Q.a = P->keep.back()->p;
+          P->keep.push_back(std::make_unique<DevBuf>(2 * static_cast<size_t>(Q.O) * Q.Kp));
+          Q.b = P->keep.back()->p;
+          up.a = Q.a;
+          up.b = Q.b;
+          int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : n.output;
+          up.out = static_cast<float*>(P->t[final_t].d);
+          if (P->t[final_t].d && P->t[final_t].d_bf16 && P->t[final_t].elem == LFGPU_ELEM_F32) {
+            up.out_bf16 = P->t[final_t].d_bf16;
+            P->t[final_t].shadow_by_producer = true;
+          }
+          for (int e = 0; e < up.epi_count; ++e) {
+            if (up.epi[e].tensor >= 0) {
+              const PTensor& et = P->t[up.epi[e].tensor];
+              if (!et.d) fail(LFGPU_EUNSUPPORTED, "epilogue operand has no fp32 buffer");
+              up.epi[e].ptr = static_cast<const float*>(et.d);
+            }
+          }
+          for (int e = 0; e + 1 < up.epi_count; ++e) P->t[up.epi[e].out_tensor].valid = false;
+          if (up.epi_count) out.valid = false;
+          UmmaLaunch L = umma_prepare(up);
+          step.kernel = "im2col_umma";
+          step.launches = 2;
+          step.run = [Q, L](cudaStream_t st) {
+            cudaError_t e = launch_im2col(Q, st);
+            return e != cudaSuccess ? e : umma_launch(L, st);
+          };
+          P->tc_nodes += 1;
+          P->bytes += A.numel * 4 + B.numel * 4 + 4 * M * Q.Kp + P->t[final_t].numel * 4;
+          P->summary[ni] = "im2col(Kp=" + std::to_string(Q.Kp) + ") + " + up.summary +
+                           " store=" + std::to_string(L.store_mode) + " grid=" + std::to_string(L.grid);
+        } else if (dp != depd.end()) {
           DirectDep D;
           D.N = static_cast<int32_t>(out.logical[0].extent);
           D.C = static_cast<int32_t>(out.logical[1].extent);
@@ -1228,7 +1326,8 @@ int lfgpu_plan_stream(lfgpu_plan* plan, void** stream) {
 
 int lfgpu_plan_info(lfgpu_plan* plan, lfgpu_counters* info) {
   std::memset(info, 0, sizeof(*info));
-  info->kernels = static_cast<int64_t>(plan->steps.size());
+  info->kernels = 0;
+  for (const auto& st : plan->steps) info->kernels += st.launches;
   info->bytes_moved = plan->bytes;
   info->flops = plan->flops;
   info->tc_nodes = plan->tc_nodes;

@@ -184,7 +184,7 @@ struct UmmaLaunch {
 
 bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::vector<Dim>& b_log,
                     const Seq& b_seq, const std::vector<Dim>& c_log, const Seq& c_seq,
-                    const lfgpu_sched& s, UmmaPlan* out, std::string* why);
+                    const lfgpu_sched& s, UmmaPlan* out, std::string* why, int rows_per_tile = 128);
 bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::vector<Dim>& k_log,
                     const Seq& k_seq, const std::vector<Dim>& y_log, const Seq& y_seq,
                     int64_t stride, const lfgpu_sched& s, UmmaPlan* out, std::string* why);

@@ -476,7 +476,14 @@ static void plan_out_store(const std::vector<PDigit>& yd, int nlog, int col_lj, 
 
 bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::vector<Dim>& b_log,
                     const Seq& b_seq, const std::vector<Dim>& c_log, const Seq& c_seq,
-                    const lfgpu_sched& s, UmmaPlan* out, std::string* why) {
+                    const lfgpu_sched& s, UmmaPlan* out, std::string* why, int RT) {
+  // RT: logical rows per tile (<= 128). Below 128 the UMMA still computes
+  // 128 rows; rows >= RT read stale SMEM and are never stored (the im2col
+  // stem tiles one 112-pixel output row per tile).
+  if (RT < 16 || RT > 128) {
+    *why = "rows per tile out of range";
+    return false;
+  }
   const int64_t M = a_log[0].extent, K = a_log[1].extent, N = b_log[1].extent;
   if (K % 64) {
     *why = "K must be a multiple of 64";
@@ -495,7 +502,7 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
   // that still fills most of the 148 SMs.
   std::vector<int> cands;
   if (s.tile_last >= 16 && s.tile_last <= 256 && s.tile_last % 16 == 0) cands.push_back(s.tile_last);
-  const int64_t mtiles = (M + 127) / 128;
+  const int64_t mtiles = (M + RT - 1) / RT;
   // Widest tile that still fills ~3/4 of the 148 SMs first, then the rest
   // from wide to narrow (legality may rule some out).
   for (int bn : {256, 128, 64, 32, 16})
@@ -511,8 +518,12 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     std::vector<int64_t> am, bm;
     UmmaPlan q = p;
     q.BN = BN;
-    if (!gemm_operand(a_log, a_seq, 0, 1, 128, 64, &q.A, &ads, &abox, &ag, &am, &last_why)) {
+    if (!gemm_operand(a_log, a_seq, 0, 1, RT, 64, &q.A, &ads, &abox, &ag, &am, &last_why)) {
       *why = "A: " + last_why;
+      return false;
+    }
+    if (RT != 128 && q.A.mn_major) {
+      *why = "A: partial row tiles need a K-major A";
       return false;
     }
     if (!gemm_operand(b_log, b_seq, 1, 0, BN, 64, &q.B, &bds, &bbox, &bg, &bm, &last_why)) {
@@ -521,7 +532,7 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     }
     // Output digits must align with the tile (rows and columns).
     std::vector<int64_t> tmp;
-    if (!cover(digits_of(cds, 0), 128, &tmp, &last_why) ||
+    if (!cover(digits_of(cds, 0), RT, &tmp, &last_why) ||
         !cover(digits_of(cds, 1), BN, &tmp, &last_why)) {
       last_why = "C: " + last_why;
       continue;
@@ -534,16 +545,16 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
         TileEntry te;
         std::memset(&te, 0, sizeof(te));
         for (int b = 0; b < q.A.boxes; ++b) {
-          int64_t lv[2] = {tm * 128 + (q.A.mn_major ? b * 64 : 0), 0};
+          int64_t lv[2] = {tm * RT + (q.A.mn_major ? b * 64 : 0), 0};
           coords(ads, ag, am, lv, te.ca[b]);
         }
         for (int b = 0; b < q.B.boxes; ++b) {
           int64_t lv[2] = {0, tn * BN + (q.B.mn_major ? b * 64 : 0)};
           coords(bds, bg, bm, lv, te.cb[b]);
         }
-        int64_t lv[2] = {tm * 128, tn * BN};
+        int64_t lv[2] = {tm * RT, tn * BN};
         te.out_base = offset_of(cds, lv);
-        te.rows = static_cast<int32_t>(std::min<int64_t>(128, M - tm * 128));
+        te.rows = static_cast<int32_t>(std::min<int64_t>(RT, M - tm * RT));
         te.cols = static_cast<int32_t>(std::min<int64_t>(BN, N - tn * BN));
         te.n_base = static_cast<int32_t>(tn * BN);
         q.tiles.push_back(te);
@@ -558,7 +569,7 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     }
     for (int r = 0; r < 128; ++r) {
       int64_t lv[2] = {r, 0};
-      q.row_off.push_back(offset_of(cds, lv));
+      q.row_off.push_back(r < RT ? offset_of(cds, lv) : -1);
     }
     for (int c = 0; c < BN; ++c) {
       int64_t lv[2] = {0, c};
@@ -568,17 +579,17 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
       std::vector<std::array<int64_t, 4>> tl, rr(128);
       std::vector<bool> ok(128);
       for (int64_t tm = 0; tm < mtiles; ++tm)
-        for (int64_t tn = 0; tn < ntile_n; ++tn) tl.push_back({tm * 128, tn * BN, 0, 0});
+        for (int64_t tn = 0; tn < ntile_n; ++tn) tl.push_back({tm * RT, tn * BN, 0, 0});
       for (int r = 0; r < 128; ++r) {
         rr[r] = {r, 0, 0, 0};
-        ok[r] = r < M;
+        ok[r] = r < M && r < RT;
       }
-      bool full = M % 128 == 0 && N % BN == 0;
+      bool full = M % RT == 0 && N % BN == 0;
       if (full) plan_out_store(cds, 2, 1, BN, tl, rr, ok, &q.ost);
     }
     q.pipe = pick_pipe(q);
     std::ostringstream os;
-    os << "gemm BM=128 BN=" << BN << " KC=64 A=" << (q.A.mn_major ? "MN" : "K") << "-major B="
+    os << "gemm BM=128" << (RT != 128 ? "(rows " + std::to_string(RT) + ")" : std::string()) << " BN=" << BN << " KC=64 A=" << (q.A.mn_major ? "MN" : "K") << "-major B="
        << (q.B.mn_major ? "MN" : "K") << "-major tiles=" << q.tiles.size() << " pipe=" << q.pipe;
     q.summary = os.str();
     q.persistent = s.parallel;

@@ -86,15 +86,20 @@ def test_pools_match_oracle(layouts):
     assert O.max_rel_diff(out["y"], bufs[g.tensor_index("y")]) <= 1e-6
 
 
-def test_direct_stem_conv_fused_exact():
+@pytest.mark.parametrize("path,hw", [("im2col_umma", 64), ("c2d_direct", 64), ("im2col_umma", 224)])
+def test_direct_stem_conv_fused_exact(path, hw, monkeypatch):
     # 3-channel 7x7 stride-2 conv (the ResNet stem) + BiasAdd + ReLU: k/64
-    # inputs make fp32 accumulation exact, so the direct kernel must match.
-    g = ir.conv_chain(2, 3, 64, 64, 7, 2, 3)
+    # inputs make fp32 (and bf16-operand) accumulation exact, so both the
+    # im2col + tcgen05 path and the CUDA-core direct kernel must match.
+    if path == "c2d_direct":
+        monkeypatch.setenv("LFGPU_NO_IM2COL", "1")
+    # hw=224: 112-pixel output rows, one per GEMM tile (rows-per-tile < 128)
+    g = ir.conv_chain(2 if hw == 64 else 1, 3, 64, hw, 7, 2, 3)
     bufs = O.random_inputs(g, 42)
     ins = {t.id: bufs[i].copy() for i, t in enumerate(g.tensors) if t.role in (ir.INPUT, ir.CONSTANT)}
     O.reference_eval(g, bufs)
     p = runtime.Plan(g, {}, [runtime.sched(1, fuse=1)])
-    assert p.node_kernel(1) == "c2d_direct"
+    assert p.node_kernel(1).startswith(path), p.node_kernel(1)
     assert p.node_kernel(2) == "fused" and p.node_kernel(3) == "fused"
     for k, v in ins.items():
         p.set_input(k, v)
@@ -168,7 +173,7 @@ def test_resnet18_b1_logits():
     kinds = [plan.node_kernel(i) for i in range(len(g.nodes))]
     tc = frozenset(i for i, k in enumerate(kinds) if k.startswith("umma"))
     assert len(tc) >= 17, kinds                # every conv but the stem on tcgen05
-    assert kinds[convs[0]["node"]] == "c2d_direct"
+    assert kinds[convs[0]["node"]].startswith("im2col_umma")  # the stem: im2col operand + tcgen05
     assert "ix_copy" not in kinds                # template-to-template Paddings are digit maps
     ins = R.make_inputs(g, gen)
     for k, x in ins.items():
