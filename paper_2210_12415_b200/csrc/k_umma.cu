@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- MMA issuer (whole warp loops; one elected lane issues)
     const uint64_t adesc = P.a_desc, bdesc = P.b_desc;
     const uint32_t idesc = P.idesc, akadv16 = P.a_kadv >> 4, bkadv16 = P.b_kadv >> 4;
-    const int ksteps = P.ksteps;
+    const int ksteps = (P.diag & 128) ? 1 : P.ksteps;  // timing knob: one k-step per stage
     const uint32_t ring0 = smem_u32(smem);
     const uint32_t a_off_b = P.a_boxes * P.a_slot;
     const bool leader = elect_one();
