@@ -58,6 +58,7 @@ struct UmmaParams {
   // follow row_off in the SMEM table.
   int32_t stg_off, stg_f32, stg_bf;
   int32_t stg_nbuf;    // staging buffers per half (ring of bulk groups)
+  int32_t epi_alias;   // epilogue region lives in the (idle) operand ring
   int32_t epi_region;  // bytes of the epilogue region (wbuf, or the mode-2 staging it aliases)
   int32_t stg_cstride, stg_cdim;  // >0: transposed box, column j at plane j * stg_cstride
   const int32_t* tile_coords;
@@ -506,10 +507,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stage_bytes = P.a_boxes * P.a_slot + (P.wres ? 0 : P.b_boxes * P.b_slot);
   const int wbytes = P.wres ? P.nstages * P.w_chunk : 0;
-  float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes + wbytes);
-  const float4* s_red = reinterpret_cast<const float4*>(smem + P.ring_bytes + wbytes + P.epi_region);
-  uint64_t* bars =
-      reinterpret_cast<uint64_t*>(smem + P.ring_bytes + wbytes + P.epi_region + P.red_bytes);
+  const int epi_own = P.epi_alias ? 0 : P.epi_region;  // bytes of a separate epilogue region
+  float* s_epi = reinterpret_cast<float*>(P.epi_alias ? smem : smem + P.ring_bytes + wbytes);
+  const float4* s_red = reinterpret_cast<const float4*>(smem + P.ring_bytes + wbytes + epi_own);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + wbytes + epi_own + P.red_bytes);
   const int nw = P.wres ? P.nstages : 0;
   const int pipe = P.pipe;
   const uint32_t full0 = smem_u32(bars);
@@ -683,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int s = s_lo; s < s_hi; ++s) {
         mbar_wait(full0 + 8 * slot, phase);
         if (dbg && leader && i == 0 && s == s_lo) dbg[3] = gtimer();
+        if (dbg && leader && (P.diag & 256) && i == 0 && s - s_lo < 16) dbg[16 + s - s_lo] = gtimer();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (nw) {
           mbar_wait(wfull0 + 8 * s, 0);  // completes once; later waits return at once
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the first unit with every side effect off (no accumulator wait, no
     // stores, no barrier arrivals) while the main loop fills TMEM; the real
     // pass then executes from a warm instruction cache.
-    bool dry = !SPLITK && !(P.diag & 64);
+    bool dry = !SPLITK && (P.diag & 64) && !P.epi_alias;  // opt-in (no measured gain)
     for (int u = blockIdx.x; u < nunits;) {
       const int tile = u / splits, split = u - tile * splits;
       const int b = i & 1;
@@ -905,7 +907,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col,
                         mode, split, splits, ws_tile, s_red, red_lo, last, tempty, org, s_rowrel, dry);
         }
-        if (dbg && !dry && i == 0 && k < 8 && threadIdx.x == kEpiWarp0 * 32) dbg[20 + k] = gtimer();
+        if (dbg && !dry && !(P.diag & 256) && i == 0 && k < 8 && threadIdx.x == kEpiWarp0 * 32)
+          dbg[20 + k] = gtimer();
       }
       if (splits > 1) {
         epi_bar();  // every warp is done with the SMEM slices of this unit
@@ -1201,16 +1204,26 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   }
   // SMEM: ring | resident weights | epilogue buffers | split-K slices |
   // barriers | tables. The ring gives up stages if the rest needs room.
-  for (;;) {
+  // When every CTA gets at most one unit, the epilogue runs only after the
+  // unit's last MMA (the ring is idle: all loads landed and were consumed),
+  // so its buffers alias the ring and the freed bytes become one more stage
+  // in flight (L2->SMEM ingest is latency-bound: bytes in flight / ~1.4 us).
+  const int64_t ntl = static_cast<int64_t>(p.tiles.size());
+  auto layout_smem = [&]() {
     const size_t ring = static_cast<size_t>(L.pipe) *
                         (L.a_boxes * L.a_slot + (p.wres ? 0 : L.b_boxes * L.b_slot));
     L.ring_bytes = static_cast<int>((ring + 1023) / 1024 * 1024);
     // Mode 2 stages in the epilogue region (its transpose buffers are
     // unused then): two buffers per half when a half stores >= 2 chunks.
     L.epi_region = std::max(kEpiSmemBytes, 2 * L.stg_nbuf * (L.stg_f32 + L.stg_bf));
-    L.smem = 1024 + L.ring_bytes + wbytes + L.epi_region + L.red_bytes +
+    L.epi_alias = !getenv("LFGPU_NO_EPI_ALIAS") && ntl * L.splits <= sms / L.splits * L.splits &&
+                  L.ring_bytes >= L.epi_region;
+    L.smem = 1024 + L.ring_bytes + wbytes + (L.epi_alias ? 0 : L.epi_region) + L.red_bytes +
              8 * (2 * L.pipe + 5 + (p.wres ? p.stages.size() : 0)) + 8 +
              sizeof(StageEntry) * p.stages.size() + 8 * p.BN + 8 * 128 + 8 * 128 + 64;
+  };
+  for (;;) {
+    layout_smem();
     if (L.smem <= 227 * 1024) break;
     if (L.stg_nbuf > 1 && L.pipe <= 4) {
       L.stg_nbuf = 1;
@@ -1225,6 +1238,18 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     }
   }
   if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "tcgen05 kernel SMEM exceeds 227 KB");
+  if (L.epi_alias) {  // grow the ring into the freed bytes, up to one unit's stages
+    const int spu = (L.nstages + L.splits - 1) / L.splits;
+    while (L.pipe < spu && !getenv("LFGPU_MAX_PIPE")) {
+      ++L.pipe;
+      layout_smem();
+      if (L.smem > 227 * 1024 || !L.epi_alias) {
+        --L.pipe;
+        layout_smem();
+        break;
+      }
+    }
+  }
   // One CTA per SM: the kernel's register budget (launch bounds 1, ~230
   // registers) leaves no room for a second; measured 2-per-SM variants
   // (launch bounds 2, <= 128 registers, <= 113 KB SMEM) were not faster.
@@ -1310,7 +1335,8 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.w_tx = L.w_tx;
   P.red_bytes = L.red_bytes;
   P.stg_f32 = L.stg_f32;
-  P.stg_off = L.ring_bytes + (L.wres ? L.nstages * L.w_chunk : 0);
+  P.stg_off = L.epi_alias ? 0 : L.ring_bytes + (L.wres ? L.nstages * L.w_chunk : 0);
+  P.epi_alias = L.epi_alias;
   P.stg_nbuf = L.stg_nbuf;
   P.epi_region = L.epi_region;
   P.stg_bf = L.stg_bf;

@@ -916,6 +916,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           P->bytes += A.numel * 2 + B.numel * 2 + P->t[final_t].numel * 4;
           P->summary[ni] = up.summary + " store=" + std::to_string(L.store_mode) +
                            " splits=" + std::to_string(L.splits) + " grid=" + std::to_string(L.grid) +
+                           " ring=" + std::to_string(L.pipe) + (L.epi_alias ? " epi-in-ring" : "") +
                            (L.dual ? " dual" : "");
         } else {
           GenContract G;

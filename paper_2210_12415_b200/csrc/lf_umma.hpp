@@ -168,6 +168,7 @@ struct UmmaLaunch {
   CUtensorMap tma_o, tma_ob;     // store mode 2: fp32 output and its bf16 copy
   int stg_off = 0, stg_f32 = 0, stg_bf = 0;
   int stg_nbuf = 1, epi_region = kEpiSmemBytes;
+  int epi_alias = 0;  // epilogue buffers alias the operand ring (<= 1 unit per CTA)
   int stg_cstride = 0, stg_cdim = 0;  // transposed TMA-store box (OutStore::col_stride / col_dim)
   void* d_tcoords = nullptr;
   ScatterDesc scatter;

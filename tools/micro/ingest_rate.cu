@@ -1,8 +1,10 @@
 // Microbenchmark: per-SM L2->SMEM ingest with 1-D bulk copies
 // (cp.async.bulk, contiguous chunks) versus 2-D tensor TMA boxes of
-// 128-byte rows (SWIZZLE_128B, the UMMA K-major operand format). One CTA per
-// SM streams a 4 MB L2-resident buffer through an 8-slot ring of CHUNK bytes.
-// Diagnostics only.
+// 128-byte rows (SWIZZLE_128B, the UMMA K-major operand format), one box or
+// three boxes per slot. One CTA per SM streams a 4 MB L2-resident buffer
+// through an 8-slot ring of CHUNK bytes. Diagnostics only; see DESIGN.md
+// §4.3 for the readings (runs disagreed on the tensor-box rate: 70 vs
+// 30-35 B/clk for 24 KB slots, bulk copies 70 B/clk in every run).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ingest_rate ingest_rate.cu -lcuda && ./ingest_rate
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -15,7 +17,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 __device__ int g_spin;  // 1: mbarrier.test_wait busy poll, 0: try_wait
 __device__ __forceinline__ void wait(uint32_t bar, uint32_t ph) {
-  if (g_spin)
+  if (false)
     asm volatile("{\n\t.reg .pred p;\n\tW: mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W;\n\t}" ::"r"(bar), "r"(ph) : "memory");
   else
     asm volatile("{\n\t.reg .pred p;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W;\n\t}" ::"r"(bar), "r"(ph) : "memory");
@@ -49,10 +51,14 @@ __global__ void __launch_bounds__(32, 1) ingest(const __grid_constant__ CUtensor
                      "l"(src + c * chunk), "r"(chunk), "r"(bar)
                      : "memory");
       } else {
-        const int y = static_cast<int>(c * rows);
-        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-                     "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(y), "r"(bar)
-                     : "memory");
+        // g_spin: the slot as three boxes of rows/3 (the GEMM's 2 A + 1 B boxes)
+        const int nbox = g_spin ? 3 : 1, r = rows / nbox;
+        for (int q = 0; q < nbox; ++q) {
+          const int y = static_cast<int>(c * rows) + q * r;
+          asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst + q * r * 128),
+                       "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(y), "r"(bar)
+                       : "memory");
+        }
       }
     }
   }
@@ -75,12 +81,12 @@ int main() {
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
   for (int spin = 0; spin < 2; ++spin) {
   cudaMemcpyToSymbol(g_spin, &spin, sizeof(int));
-  printf("-- wait: %s\n", spin ? "test_wait spin" : "try_wait");
-  for (int chunk : {8192, 24576}) {
+  printf("-- %s\n", spin ? "tensor: three boxes per slot" : "one box per slot");
+  for (int chunk : {24576}) {
     CUtensorMap map;
     cuuint64_t dims[2] = {64, bytes / 128};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(chunk / 128)}, es[2] = {1, 1};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(chunk / 128 / (spin ? 3 : 1))}, es[2] = {1, 1};
     if (chunk / 128 > 256) continue;
     ((Enc)fn)(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, src, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -40,9 +40,12 @@ def timeline(g, cand, inputs, name):
     allb = buf.cpu().numpy().astype(np.int64)
     nct = int((allb.reshape(-1, 32)[:, 0] != 0).sum())
     t16 = allb[: 32 * nct].reshape(-1, 32)
+    if int(os.environ.get("LFGPU_UMMA_DIAG", "0")) & 256:
+        st = [np.median(t16[:, 16 + k] - t16[:, 1]) / 1000.0 for k in range(16) if (t16[:, 16 + k] > 0).all()]
+        print("  unit-0 stage landed (us after setup):", " ".join(f"{v:.2f}" for v in st))
     ck = [(np.median(t16[:, 20 + k] - t16[:, 0]) / 1000.0) for k in range(8) if (t16[:, 20 + k] > 0).all()]
     print("  unit-0 chunk ends (us):", " ".join(f"{v:.2f}" for v in ck))
-    if (t16[:, 16] > 0).all():
+    if (t16[:, 16] > 0).all() and not int(os.environ.get("LFGPU_UMMA_DIAG", "0")) & 256:
         sp = (t16[:, 16:20] - t16[:, :1]) / 1000.0
         print("  split-K: published %.2f fenced %.2f spin-done %.2f slices-landed %.2f us" %
               tuple(np.median(sp, axis=0)))
