@@ -3,8 +3,7 @@
 // 128-byte rows (SWIZZLE_128B, the UMMA K-major operand format), one box or
 // three boxes per slot. One CTA per SM streams a 4 MB L2-resident buffer
 // through an 8-slot ring of CHUNK bytes. Diagnostics only; see DESIGN.md
-// §4.3 for the readings (runs disagreed on the tensor-box rate: 70 vs
-// 30-35 B/clk for 24 KB slots, bulk copies 70 B/clk in every run).
+// §4.3 for the readings.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ingest_rate ingest_rate.cu -lcuda && ./ingest_rate
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -36,6 +35,7 @@ __global__ void __launch_bounds__(32, 1) ingest(const __grid_constant__ CUtensor
   __syncwarp();
   if (threadIdx.x != 0) return;
   const int rows = chunk / 128;
+  const int nbox = g_spin ? 3 : 1;  // read once: a per-iteration global load would serialise issue
   const size_t nchunks = src_bytes / chunk;
   long long t0 = clock64();
   for (int it = 0; it < iters + slots; ++it) {
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(32, 1) ingest(const __grid_constant__ CUtensor
                      : "memory");
       } else {
         // g_spin: the slot as three boxes of rows/3 (the GEMM's 2 A + 1 B boxes)
-        const int nbox = g_spin ? 3 : 1, r = rows / nbox;
+        const int r = rows / nbox;
         for (int q = 0; q < nbox; ++q) {
           const int y = static_cast<int>(c * rows) + q * r;
           asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst + q * r * 128),
