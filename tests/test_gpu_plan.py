@@ -366,3 +366,48 @@ def test_dep_direct(shape, f, fuse):
     p.run()
     got = p.get_output("y")
     assert np.array_equal(got, ref["y"]), O.max_rel_diff(got, ref["y"])
+
+
+def _dep_residual_graph(n, c, h):
+    """Padding -> DEP 3x3 -> BiasAdd -> EwAdd(skip) -> ReLU: every epilogue
+    kind the K6 kernel fuses (bias per channel, residual in the output
+    layout, ReLU)."""
+    g = ir.Graph()
+    d4 = [("N", n), ("C", c), ("H", h), ("W", h)]
+    g.tensors = [
+        ir.TensorDecl("x", d4, ir.INPUT),
+        ir.TensorDecl("ker", [("C", c), ("KH", 3), ("KW", 3)], ir.CONSTANT),
+        ir.TensorDecl("bias", [("C", c)], ir.CONSTANT),
+        ir.TensorDecl("skip", d4, ir.INPUT),
+        ir.TensorDecl("xp", [("N", n), ("C", c), ("H", h + 2), ("W", h + 2)], ir.INTERMEDIATE),
+        ir.TensorDecl("conv", d4, ir.INTERMEDIATE),
+        ir.TensorDecl("biased", d4, ir.INTERMEDIATE),
+        ir.TensorDecl("summed", d4, ir.INTERMEDIATE),
+        ir.TensorDecl("y", d4, ir.OUTPUT),
+    ]
+    g.nodes = [
+        ir.OperatorNode(ir.PADDING, ["x"], "xp", {"pad": 1}),
+        ir.OperatorNode(ir.DEP, ["xp", "ker"], "conv", {"stride": 1}),
+        ir.OperatorNode(ir.BIASADD, ["conv", "bias"], "biased"),
+        ir.OperatorNode(ir.EWADD, ["biased", "skip"], "summed"),
+        ir.OperatorNode(ir.RELU, ["summed"], "y"),
+    ]
+    return g
+
+
+@pytest.mark.parametrize("brick", [None, 16])
+def test_dep_direct_fused_bias_residual(brick):
+    g = _dep_residual_graph(2, 64, 28)
+    seqs = {}
+    if brick:
+        seqs = runtime.decode_layout(g, 1, [14, 14, brick, brick, brick])
+        for t in ("biased", "summed", "y", "skip"):
+            seqs[t] = seqs["conv"]
+    inputs, ref = oracle_outputs(g, 29)
+    p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=1)])
+    assert p.node_kernel(1).startswith("dep_direct"), p.node_kernel(1)
+    assert all(p.node_kernel(i) == "fused" for i in (2, 3, 4)), [p.node_kernel(i) for i in range(5)]
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    assert np.array_equal(p.get_output("y"), ref["y"])
