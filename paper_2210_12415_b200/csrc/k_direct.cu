@@ -284,7 +284,10 @@ __global__ void __launch_bounds__(256) im2col_stem(const Im2col Q) {
       const int64_t m = e - static_cast<int64_t>(kb) * M;
       const int n = static_cast<int>(m / hw), rem = static_cast<int>(m - static_cast<int64_t>(n) * hw);
       const int ho = rem / Q.Wo, wo = rem - ho * Q.Wo;
-      const float* xb = Q.x + (static_cast<int64_t>(n) * Q.I * Q.H + ho * Q.V) * Q.W + wo * Q.V;
+      // Window origin in x; with an absorbed Padding (Q.pad > 0) taps
+      // outside x read as zero (interp.cpp:123-136).
+      const int y0 = ho * Q.V - Q.pad, x0 = wo * Q.V - Q.pad;
+      const float* xb = Q.x + static_cast<int64_t>(n) * Q.I * Q.H * Q.W;
       int k = kb * 64;
       int i = k / (Q.KH * Q.KW), r = k - i * Q.KH * Q.KW, rh = r / Q.KW, rw = r - rh * Q.KW;
       const int64_t mt = m / Q.RT;
@@ -294,7 +297,9 @@ __global__ void __launch_bounds__(256) im2col_stem(const Im2col Q) {
 #pragma unroll
         for (int j = 0; j < 8; ++j, ++k) {
           float x = 0.f;
-          if (k < Q.K) x = __ldg(xb + (static_cast<int64_t>(i) * Q.H + rh) * Q.W + rw);
+          const int yy = y0 + rh, xx = x0 + rw;
+          if (k < Q.K && yy >= 0 && yy < Q.H && xx >= 0 && xx < Q.W)
+            x = __ldg(xb + (static_cast<int64_t>(i) * Q.H + yy) * Q.W + xx);
           v[j] = __float2bfloat16_rn(x);
           if (++rw == Q.KW) {
             rw = 0;

@@ -65,6 +65,7 @@ struct Im2col {
   void* b = nullptr;         // bf16 B bricks
   int32_t N = 0, I = 0, H = 0, W = 0, KH = 0, KW = 0, V = 1, Ho = 0, Wo = 0, O = 0, K = 0, Kp = 0;
   int32_t RT = 128;          // rows (pixels) per A brick = per GEMM tile
+  int32_t pad = 0;           // absorbed Padding: x is the unpadded input
 };
 
 cudaError_t launch_im2col(const Im2col& Q, cudaStream_t stream);

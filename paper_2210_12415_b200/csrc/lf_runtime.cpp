@@ -403,6 +403,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   std::map<int, std::vector<EpiOp>> direct;  // CUDA-core direct convs (k_direct.cu)
   std::map<int, std::vector<EpiOp>> depd;    // K6 depthwise (k_direct.cu)
   std::map<int, UmmaPlan> im2col;            // small-I C2D: im2col + tcgen05 GEMM
+  std::map<int, int> im2col_pad;             // im2col node -> Padding node it reads through
   std::set<int> fused_away;  // element-wise nodes absorbed into an epilogue
   std::vector<int> pos(P->nodes.size(), 0);
   for (size_t k = 0; k < P->order.size(); ++k) pos[P->order[k]] = static_cast<int>(k);
@@ -516,6 +517,15 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
             for (const auto& e : epi) ug.epi[ug.epi_count++] = e;
           }
           im2col[ni] = ug;
+          // The Padding feeding only this conv is folded into the im2col
+          // reads (zero outside x): its step and its buffer's writes vanish.
+          const int pn = A.producer;
+          if (pn >= 0 && P->nodes[pn].kind == LFGPU_OP_PADDING && A.consumers.size() == 1 &&
+              P->t[P->nodes[pn].inputs[0]].seq.empty() && A.role == LFGPU_ROLE_INTERMEDIATE &&
+              !(P->flags & LFGPU_PLAN_KEEP_ALL) && !getenv("LFGPU_NO_PAD_ABSORB")) {
+            im2col_pad[ni] = pn;
+            fused_away.insert(pn);
+          }
           continue;
         }
         direct[ni] = s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL) ? fuse_chain(ni, Cc)
@@ -742,6 +752,17 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           Q.RT = up.tiles.empty() ? 128 : up.tiles[0].rows;  // rows per A brick = rows per tile
           if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "im2col conv on a bf16-only operand");
           Q.x = static_cast<const float*>(A.d);
+          auto ipd = im2col_pad.find(ni);
+          if (ipd != im2col_pad.end()) {  // read the unpadded input
+            const auto& pnode = P->nodes[ipd->second];
+            PTensor& xin = P->t[pnode.inputs[0]];
+            if (!xin.d) fail(LFGPU_EUNSUPPORTED, "im2col: padded input has no fp32 buffer");
+            Q.x = static_cast<const float*>(xin.d);
+            Q.H = static_cast<int32_t>(xin.logical[2].extent);
+            Q.W = static_cast<int32_t>(xin.logical[3].extent);
+            Q.pad = static_cast<int32_t>(pnode.pad);
+            const_cast<PTensor&>(A).valid = false;  // the padded tensor is never materialized
+          }
           Q.w = static_cast<const float*>(B.d);
           const int64_t M = static_cast<int64_t>(Q.N) * Q.Ho * Q.Wo;
           P->keep.push_back(std::make_unique<DevBuf>(2 * static_cast<size_t>(M) * Q.Kp));

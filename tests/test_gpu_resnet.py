@@ -100,6 +100,10 @@ def test_direct_stem_conv_fused_exact(path, hw, monkeypatch):
     O.reference_eval(g, bufs)
     p = runtime.Plan(g, {}, [runtime.sched(1, fuse=1)])
     assert p.node_kernel(1).startswith(path), p.node_kernel(1)
+    if path == "im2col_umma":  # the Padding is read through by im2col (zero outside x)
+        assert p.node_kernel(0) == "fused"
+        with pytest.raises(runtime.LfError):
+            p.get_output("xp")
     assert p.node_kernel(2) == "fused" and p.node_kernel(3) == "fused"
     for k, v in ins.items():
         p.set_input(k, v)
