@@ -285,9 +285,15 @@ int lfgpu_plan_destroy(lfgpu_plan* plan);
  * it into the plan's physical layout on the device (K1). */
 int lfgpu_plan_set_input(lfgpu_plan* plan, int32_t tensor, const double* host_logical,
                          int64_t n);
-/* Same, from a device buffer of `elem` type already in the logical layout. */
+/* Same, from a device buffer of `elem` type already in the logical layout.
+ * Returns once the conversion has consumed `d_logical`. */
 int lfgpu_plan_set_input_device(lfgpu_plan* plan, int32_t tensor, const void* d_logical,
                                 int32_t elem);
+/* Same, stream-ordered: the conversion is enqueued on the plan's stream and
+ * the call returns at once; `d_logical` must stay valid and unchanged until
+ * the plan's stream passes this point (the serving / pipelined path). */
+int lfgpu_plan_set_input_device_async(lfgpu_plan* plan, int32_t tensor, const void* d_logical,
+                                      int32_t elem);
 /* Execute every node once on the plan's stream (asynchronous). */
 int lfgpu_plan_run(lfgpu_plan* plan);
 /* Same, enqueued on the caller's stream instead of the plan's own (NULL:

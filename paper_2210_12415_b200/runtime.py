@@ -26,6 +26,7 @@ EXPORTS = [
     "lfgpu_ctx_destroy",
     "lfgpu_ctx_launch_count", "lfgpu_layout_convert", "lfgpu_pad_convert", "lfgpu_plan_build",
     "lfgpu_plan_destroy", "lfgpu_plan_set_input", "lfgpu_plan_set_input_device",
+    "lfgpu_plan_set_input_device_async",
     "lfgpu_plan_run", "lfgpu_plan_run_on", "lfgpu_plan_get_output", "lfgpu_plan_tensor_buffer", "lfgpu_plan_stream",
     "lfgpu_plan_info", "lfgpu_plan_node_kernel", "lfgpu_plan_measure", "lfgpu_interpret",
     "lfgpu_debug_umma_trace", "lfgpu_materialize_host",
@@ -65,6 +66,7 @@ def lib():
                                        C.c_int32, P(C.c_void_p)]
         L.lfgpu_plan_set_input.argtypes = [C.c_void_p, C.c_int32, P(C.c_double), C.c_int64]
         L.lfgpu_plan_set_input_device.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]
+        L.lfgpu_plan_set_input_device_async.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]
         L.lfgpu_plan_get_output.argtypes = [C.c_void_p, C.c_int32, P(C.c_double), C.c_int64]
         L.lfgpu_plan_tensor_buffer.argtypes = [C.c_void_p, C.c_int32, P(C.c_void_p),
                                                P(C.c_int32), P(C.c_int64)]
@@ -259,10 +261,12 @@ class Plan:
         check(lib().lfgpu_plan_set_input(self.ptr, self.index(tid),
                                          v.ctypes.data_as(C.POINTER(C.c_double)), v.size))
 
-    def set_input_device(self, tid, tensor):
-        """From a torch CUDA tensor in the logical layout (float32/bfloat16/...)."""
-        check(lib().lfgpu_plan_set_input_device(self.ptr, self.index(tid),
-                                                C.c_void_p(tensor.data_ptr()), elem_of(tensor)))
+    def set_input_device(self, tid, tensor, wait=True):
+        """From a torch CUDA tensor in the logical layout (float32/bfloat16/...).
+        wait=False enqueues the conversion on the plan's stream and returns at
+        once; the caller keeps `tensor` alive and unchanged until then."""
+        fn = lib().lfgpu_plan_set_input_device if wait else lib().lfgpu_plan_set_input_device_async
+        check(fn(self.ptr, self.index(tid), C.c_void_p(tensor.data_ptr()), elem_of(tensor)))
 
     def run(self, stream=None):
         if stream is None:
