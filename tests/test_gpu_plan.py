@@ -338,7 +338,7 @@ def test_store_at_rules(seqs, msg):
 @pytest.mark.parametrize("shape,f,fuse", [
     ((2, 64, 28, 3, 1), None, 0),                    # logical NCHW: W is the fast dim
     ((2, 64, 28, 3, 1), (7, 14, 32, 32, 32), 1),     # channel bricks, ReLU fused
-    ((1, 96, 27, 5, 2), (13, 13, 32, 32, 32), 1),    # 5x5 stride 2, ragged bricks
+    ((1, 96, 27, 5, 2), (7, 7, 32, 32, 32), 1),      # 5x5 stride 2 (14x14 output)
     ((1, 32, 14, 7, 1), (14, 14, 16, 16, 16), 0),    # 7x7
     ((1, 48, 10, 4, 1), None, 1),                    # even window: the generic-K path
 ])
