@@ -1,0 +1,573 @@
+// k_pair.cu — K3 (second generation): the CTA-pair tcgen05 GEMM for sm_100a.
+//
+// Replaces the GMM loop nest of the reference (lower.cpp:221-227, evaluated
+// by interp.cpp:381-411; oracle interp.cpp:109-122) on the GMM template
+// bricks (space.cpp:388-412) when M is a multiple of 256.
+//
+// One cluster = S CTA pairs working on the same 256 x BN output tile; pair p
+// accumulates K stages [p*KS/S, (p+1)*KS/S). Per CTA (256 threads):
+//   warp 0      TMA producer (one lane): A rows [128*r, +128) and B columns
+//               [BN/2*r, +BN/2) of the pair tile for each K stage into a
+//               `pipe`-deep ring; completion bytes land on the pair leader's
+//               barrier (cp.async.bulk.tensor .cta_group::2);
+//   warp 1      (pair leader only) MMA issuer: tcgen05.mma.cta_group::2
+//               M=256 N=BN K=16, bf16 x bf16 -> fp32 into one of two TMEM
+//               accumulators of BN columns; tcgen05.commit multicasts the
+//               ring-slot release and the accumulator-ready signal to both
+//               CTAs of the pair;
+//   warp 2      TMEM allocation (cta_group::2, both CTAs);
+//   warps 4-7   epilogue: tcgen05.ld (thread = accumulator row), fused
+//               BiasAdd / EwAdd / ReLU chain (lower.cpp:566-608 fusion
+//               groups), 128-byte row-segment stores through a per-warp
+//               SMEM transpose; the accumulator is released to the leader's
+//               MMA (remote mbarrier arrive) as soon as it has been read, so
+//               the next tile's main loop overlaps this epilogue.
+// With S > 1 every CTA publishes its fp32 partial rows to an L2 workspace,
+// arrives (release, cluster scope) on the reduction barrier of the S CTAs
+// holding the same rows, waits for theirs, and reduces the column slice
+// [p*BN/S, (p+1)*BN/S) summing partials in split order: the result does not
+// depend on arrival order, and no CTA spins on global memory (the cluster
+// guarantees the S pairs are co-resident).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+
+#include "lf_pair.hpp"
+#include "lf_ptx.hpp"
+
+namespace lfg {
+
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+constexpr int kLd = 36;  // transpose buffer row stride (floats)
+constexpr int kEpiBytes = 4 * 32 * kLd * 4;
+
+struct PairParams {
+  const int32_t* a_crd;
+  const int32_t* b_crd;
+  const int32_t* s_crd;
+  const int64_t* out_r;
+  const int64_t* out_c;
+  const int64_t* row_off;
+  const int64_t* col_off;
+  float* out;
+  __nv_bfloat16* out_bf16;
+  float* ws;
+  const float* epi_ptr[kMaxEpi];
+  int32_t epi_kind[kMaxEpi];
+  int32_t epi_count;
+  int32_t MT2, NT, KS, S, ntiles, group;
+  int32_t a_boxes, b_boxes, a_slot, b_slot, stage_bytes, tx_bytes, pipe, BN;
+  uint64_t a_desc, b_desc;
+  uint32_t a_kadv, b_kadv, idesc, tmem_cols;
+  int32_t ring_bytes;
+  int32_t col_unit;
+  // Diagnostics (lfgpu_debug_umma_trace): 256 %globaltimer stamps per CTA:
+  // [0,64) producer slot acquired per stage, [64,128) leader full-wait done
+  // per stage, [128,192) epilogue accumulator ready per tile, [192,256)
+  // epilogue done per tile (first 64 of each).
+  unsigned long long* dbg;
+  int32_t dbg_split;  // diagnostics: >= 0 keeps only that split's partial in the reduction
+};
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Grouped rasterisation: `group` row tiles sweep the column tiles together
+// so concurrently running clusters share A row blocks and B column blocks in L2.
+__device__ __forceinline__ void tile_coords(const PairParams& P, int t, int* Mi, int* Nj) {
+  const int per = P.group * P.NT;
+  const int g = t / per, first = g * P.group;
+  const int gs = min(P.MT2 - first, P.group);
+  const int r = t - g * per;
+  *Mi = first + r % gs;
+  *Nj = r / gs;
+}
+
+// Fused element-wise chain on 4 consecutive columns of one row.
+__device__ __forceinline__ float4 epi4(const PairParams& P, float4 x, int n, int64_t addr) {
+#pragma unroll 1
+  for (int e = 0; e < P.epi_count; ++e) {
+    const int k = P.epi_kind[e];
+    const float* ep = P.epi_ptr[e];
+    if (k == EPI_RELU) {
+      x.x = fmaxf(x.x, 0.f);
+      x.y = fmaxf(x.y, 0.f);
+      x.z = fmaxf(x.z, 0.f);
+      x.w = fmaxf(x.w, 0.f);
+    } else {
+      const float4 b = k == EPI_BIAS ? make_float4(__ldg(ep + n), __ldg(ep + n + 1), __ldg(ep + n + 2),
+                                                   __ldg(ep + n + 3))
+                                     : __ldg(reinterpret_cast<const float4*>(ep + addr));
+      x.x += b.x;
+      x.y += b.y;
+      x.z += b.z;
+      x.w += b.w;
+    }
+  }
+  return x;
+}
+
+// Store 32 accumulator columns [c0, c0+32) of the calling thread's row
+// (v[j] = column c0 + j) through the per-warp transpose buffer.
+__device__ __forceinline__ void store_chunk(const PairParams& P, const float* v, float* wbuf, int q,
+                                            int lane, int c0, int n0, int64_t obase,
+                                            const int64_t* row_off, const int64_t* col_off) {
+  if (P.col_unit) {
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(wbuf + lane * kLd + 4 * j) =
+          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    __syncwarp();
+    const int cl = (lane & 7) * 4;
+    const int64_t cb = obase + __ldg(col_off + c0) + cl;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int rr = it * 4 + (lane >> 3);
+      float4 x = *reinterpret_cast<const float4*>(wbuf + rr * kLd + cl);
+      const int64_t addr = cb + __ldg(row_off + q * 32 + rr);
+      x = epi4(P, x, n0 + c0 + cl, addr);
+      *reinterpret_cast<float4*>(P.out + addr) = x;
+      if (P.out_bf16) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(x.z, x.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(P.out_bf16 + addr) = pk;
+      }
+    }
+    return;
+  }
+  // Generic layouts: thread = row, one element at a time.
+  const int64_t rb = obase + __ldg(row_off + q * 32 + lane);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int64_t addr = rb + __ldg(col_off + c0 + j);
+    float y = v[j];
+#pragma unroll 1
+    for (int e = 0; e < P.epi_count; ++e) {
+      const int k = P.epi_kind[e];
+      if (k == EPI_RELU) y = fmaxf(y, 0.f);
+      else y += __ldg(P.epi_ptr[e] + (k == EPI_BIAS ? static_cast<int64_t>(n0 + c0 + j) : addr));
+    }
+    P.out[addr] = y;
+    if (P.out_bf16) P.out_bf16[addr] = __float2bfloat16_rn(y);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                const __grid_constant__ PairParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + kEpiBytes);
+  const int pipe = P.pipe;
+  const uint32_t full0 = smem_u32(bars);
+  const uint32_t empty0 = full0 + 8 * pipe;
+  const uint32_t tfull0 = empty0 + 8 * pipe;  // 2 accumulator-ready barriers
+  const uint32_t tempty0 = tfull0 + 16;       // 2 accumulator-free barriers (leader)
+  const uint32_t red0 = tempty0 + 16;         // 2 split-reduction barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * pipe + 6);
+  int32_t* s_stage = reinterpret_cast<int32_t*>(bars + 2 * pipe + 8);  // KS x 10 stage coordinates
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const int pr = static_cast<int>(crank & 1u);     // rank inside the pair
+  const int split = static_cast<int>(crank >> 1);  // pair index = K split
+  const uint32_t lead = crank & ~1u;
+  const uint16_t pair_mask = static_cast<uint16_t>(3u << lead);
+  const int S = P.S;
+  const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < pipe; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tempty0 + 8 * b, 2 * 4);  // both CTAs' epilogue warps
+      mbar_init(red0 + 8 * b, S * 4);     // epilogue warps of the S CTAs holding these rows
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+  }
+  for (int i = threadIdx.x; i < 10 * P.KS; i += kThreads) s_stage[i] = __ldg(P.s_crd + i);
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  const int s_lo = split * P.KS / S, s_hi = (split + 1) * P.KS / S;
+  const uint32_t ring0 = smem_u32(smem);
+
+  if (warp == 0) {
+    // ---- TMA producer (both CTAs of the pair). Coordinates never come from
+    // global memory inside the stage loop: the tile part is loaded into
+    // registers once per tile, the stage part lives in SMEM (an L2 round
+    // trip per stage would pace the whole pipeline).
+    if (elect_one()) {
+      const uint32_t lead_full0 = mapa(full0, lead);
+      const uint32_t b_off = P.a_boxes * P.a_slot;
+      int g = 0;
+      for (int t = cid; t < P.ntiles; t += ncl) {
+        int Mi, Nj;
+        tile_coords(P, t, &Mi, &Nj);
+        int32_t ta[kMaxBoxes][5], tb[kMaxBoxes][5];
+        const int32_t* ca = P.a_crd + (2 * Mi + pr) * P.a_boxes * 5;
+        const int32_t* cb = P.b_crd + (2 * Nj + pr) * P.b_boxes * 5;
+#pragma unroll
+        for (int b = 0; b < kMaxBoxes; ++b)
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            ta[b][d] = b < P.a_boxes ? __ldg(ca + b * 5 + d) : 0;
+            tb[b][d] = b < P.b_boxes ? __ldg(cb + b * 5 + d) : 0;
+          }
+        for (int s = s_lo; s < s_hi; ++s, ++g) {
+          const int slot = g % pipe;
+          const uint32_t ph = static_cast<uint32_t>(g / pipe) & 1u;
+          const int32_t* sc = s_stage + s * 10;
+          int32_t c[5];
+          mbar_wait(empty0 + 8 * slot, ph ^ 1u);
+          if (P.dbg && g < 64) P.dbg[256 * blockIdx.x + g] = gtime();
+          if (pr == 0) mbar_expect_tx(full0 + 8 * slot, 2 * P.tx_bytes);
+          const uint32_t bar = lead_full0 + 8 * slot;
+          const uint32_t dst = ring0 + slot * P.stage_bytes;
+#pragma unroll
+          for (int b = 0; b < kMaxBoxes; ++b)
+            if (b < P.a_boxes) {
+#pragma unroll
+              for (int d = 0; d < 5; ++d) c[d] = ta[b][d] + sc[d];
+              tma_load5_pair(&tma_a, dst + b * P.a_slot, bar, c);
+            }
+#pragma unroll
+          for (int b = 0; b < kMaxBoxes; ++b)
+            if (b < P.b_boxes) {
+#pragma unroll
+              for (int d = 0; d < 5; ++d) c[d] = tb[b][d] + sc[5 + d];
+              tma_load5_pair(&tma_b, dst + b_off + b * P.b_slot, bar, c);
+            }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1 && pr == 0) {
+    // ---- MMA issuer (pair leader)
+    const uint32_t akadv = P.a_kadv >> 4, bkadv = P.b_kadv >> 4;
+    const uint32_t b_off = P.a_boxes * P.a_slot;
+    const bool issuer = elect_one();
+    int g = 0, i = 0;
+    for (int t = cid; t < P.ntiles; t += ncl, ++i) {
+      const int acc = i & 1;
+      mbar_wait_cluster(tempty0 + 8 * acc, (static_cast<uint32_t>(i >> 1) & 1u) ^ 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d = tmem + static_cast<uint32_t>(acc * P.BN);
+      for (int s = s_lo; s < s_hi; ++s, ++g) {
+        const int slot = g % pipe;
+        mbar_wait(full0 + 8 * slot, static_cast<uint32_t>(g / pipe) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (P.dbg && issuer && g < 64) P.dbg[256 * blockIdx.x + 64 + g] = gtime();
+        if (issuer) {
+          const uint32_t a_addr = ring0 + slot * P.stage_bytes;
+          const uint64_t ad = P.a_desc | (a_addr >> 4), bd = P.b_desc | ((a_addr + b_off) >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma2_bf16(d, ad + k * akadv, bd + k * bkadv, P.idesc, (s != s_lo) | k);
+          umma2_commit_mc(empty0 + 8 * slot, pair_mask);
+        }
+        __syncwarp();
+      }
+      if (issuer) umma2_commit_mc(tfull0 + 8 * acc, pair_mask);
+      __syncwarp();
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ---- epilogue (both CTAs): warp w reads TMEM lanes 32*(w%4)..+31
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    float* wbuf = s_epi + q * 32 * kLd;
+    const uint32_t lead_tempty0 = mapa(tempty0, lead);
+    int i = 0;
+    for (int t = cid; t < P.ntiles; t += ncl, ++i) {
+      int Mi, Nj;
+      tile_coords(P, t, &Mi, &Nj);
+      const int acc = i & 1;
+      const int mi = 2 * Mi + pr;
+      const int64_t obase = __ldg(P.out_r + mi) + __ldg(P.out_c + Nj);
+      const int n0 = Nj * P.BN;
+      mbar_wait(tfull0 + 8 * acc, static_cast<uint32_t>(i >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (P.dbg && row == 0 && i < 64) P.dbg[256 * blockIdx.x + 128 + i] = gtime();
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.BN);
+      float v[32];
+      if (S == 1) {
+        for (int c0 = 0; c0 < P.BN; c0 += 32) {
+          tmem_ld32(taddr + c0, v);
+          if (c0 + 32 == P.BN) {  // accumulator fully read: hand it back
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(lead_tempty0 + 8 * acc);
+          }
+          store_chunk(P, v, wbuf, q, lane, c0, n0, obase, P.row_off, P.col_off);
+        }
+        if (P.dbg && row == 0 && i < 64) P.dbg[256 * blockIdx.x + 192 + i] = gtime();
+        continue;
+      }
+      // Split K: publish this split's partial rows ([col/4][row] float4).
+      const size_t tile_floats = static_cast<size_t>(128) * P.BN;
+      float4* mine = reinterpret_cast<float4*>(P.ws + ((static_cast<size_t>(t) * S + split) * 2 + pr) * tile_floats);
+      for (int c0 = 0; c0 < P.BN; c0 += 32) {
+        tmem_ld32(taddr + c0, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          __stcg(mine + (c0 / 4 + j) * 128 + row, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_cluster(lead_tempty0 + 8 * acc);
+        for (int p = 0; p < S; ++p) mbar_arrive_cluster(mapa(red0 + 8 * acc, 2 * p + pr));
+      }
+      mbar_wait_cluster(red0 + 8 * acc, static_cast<uint32_t>(i >> 1) & 1u);
+      const int W = P.BN / S;
+      for (int c0 = split * W; c0 < (split + 1) * W; c0 += 32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        for (int p = 0; p < S; ++p) {
+          if (P.dbg_split >= 0 && p != P.dbg_split) continue;
+          const float4* src =
+              reinterpret_cast<const float4*>(P.ws + ((static_cast<size_t>(t) * S + p) * 2 + pr) * tile_floats);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 x = __ldcg(src + (c0 / 4 + j) * 128 + row);
+            v[4 * j] += x.x;
+            v[4 * j + 1] += x.y;
+            v[4 * j + 2] += x.z;
+            v[4 * j + 3] += x.w;
+          }
+        }
+        store_chunk(P, v, wbuf, q, lane, c0, n0, obase, P.row_off, P.col_off);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols)
+                 : "memory");
+  }
+}
+
+struct PairTables {
+  void* p[8] = {};
+  ~PairTables() {
+    for (auto* q : p)
+      if (q) cudaFree(q);
+  }
+};
+
+template <typename T>
+void* upload(const std::vector<T>& v) {
+  void* d = nullptr;
+  const size_t bytes = sizeof(T) * std::max<size_t>(v.size(), 1);
+  if (cudaMalloc(&d, bytes) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc pair tables");
+  if (!v.empty() && cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    fail(LFGPU_ECUDA, "cudaMemcpy pair tables");
+  return d;
+}
+
+}  // namespace
+
+PairLaunch pair_prepare(const PairPlan& p) {
+  PairLaunch L;
+  L.tma_a = umma_encode(p.A, p.a);
+  L.tma_b = umma_encode(p.B, p.b);
+  auto t = std::make_shared<PairTables>();
+  t->p[0] = upload(p.a_crd);
+  t->p[1] = upload(p.b_crd);
+  t->p[2] = upload(p.s_crd);
+  t->p[3] = upload(p.out_r);
+  t->p[4] = upload(p.out_c);
+  t->p[5] = upload(p.row_off);
+  t->p[6] = upload(p.col_off);
+  L.a_crd = static_cast<const int32_t*>(t->p[0]);
+  L.b_crd = static_cast<const int32_t*>(t->p[1]);
+  L.s_crd = static_cast<const int32_t*>(t->p[2]);
+  L.out_r = static_cast<const int64_t*>(t->p[3]);
+  L.out_c = static_cast<const int64_t*>(t->p[4]);
+  L.row_off = static_cast<const int64_t*>(t->p[5]);
+  L.col_off = static_cast<const int64_t*>(t->p[6]);
+  L.BN = p.BN;
+  L.S = p.S;
+  L.MT = p.MT;
+  L.NT = p.NT;
+  L.KS = p.KS;
+  L.pipe = p.pipe;
+  L.a_boxes = p.A.boxes;
+  L.b_boxes = p.B.boxes;
+  L.a_slot = p.A.slot_bytes;
+  L.b_slot = p.B.slot_bytes;
+  L.stage_bytes = L.a_boxes * L.a_slot + L.b_boxes * L.b_slot;
+  L.tx_bytes = L.a_boxes * p.A.box_bytes + L.b_boxes * p.B.box_bytes;
+  L.a_desc = umma_desc_bits(p.A);
+  L.b_desc = umma_desc_bits(p.B);
+  L.a_kadv = p.A.k_adv;
+  L.b_kadv = p.B.k_adv;
+  L.idesc = umma_idesc(256, p.BN, p.A.mn_major, p.B.mn_major);
+  int cols = 32;
+  while (cols < 2 * p.BN) cols *= 2;
+  L.tmem_cols = cols;
+  L.ring_bytes = L.pipe * L.stage_bytes;
+  L.smem = 1024 + L.ring_bytes + kEpiBytes + 8 * (2 * L.pipe + 8) + 40 * static_cast<size_t>(p.KS);
+  if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "pair kernel SMEM exceeds 227 KB");
+  // Row-segment stores need contiguous output columns and 16-byte aligned rows.
+  bool unit = true;
+  for (size_t c = 0; c < p.col_off.size(); c += 32)
+    for (size_t j = 1; j < 32 && c + j < p.col_off.size(); ++j)
+      if (p.col_off[c + j] != p.col_off[c] + static_cast<int64_t>(j)) unit = false;
+  for (size_t c = 0; c < p.col_off.size(); c += 32)
+    if (p.col_off[c] % 4) unit = false;
+  for (auto v : p.row_off)
+    if (v % 4) unit = false;
+  for (auto v : p.out_r)
+    if (v % 4) unit = false;
+  for (auto v : p.out_c)
+    if (v % 4) unit = false;
+  for (int e = 0; e < p.epi_count; ++e)
+    if (reinterpret_cast<uintptr_t>(p.epi[e].ptr) % 16) unit = false;
+  L.col_unit = unit ? 1 : 0;
+  L.epi_count = p.epi_count;
+  for (int e = 0; e < p.epi_count; ++e) {
+    L.epi_kinds[e] = p.epi[e].kind;
+    L.epi_ptr[e] = p.epi[e].ptr;
+  }
+  L.out = p.out;
+  L.out_bf16 = p.out_bf16;
+  const int ntiles = p.MT / 2 * p.NT;
+  if (L.S > 1) {
+    const size_t ws = sizeof(float) * static_cast<size_t>(ntiles) * L.S * 256 * L.BN;
+    if (cudaMalloc(&t->p[7], ws) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc pair split-K workspace");
+    L.ws = static_cast<float*>(t->p[7]);
+  }
+  L.owner = t;
+  if (const char* e = getenv("LFGPU_PAIR_GROUP")) L.group = std::max(1, atoi(e));
+  // Persistent grid: as many clusters as can be co-resident, at most one per tile.
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  const int csize = 2 * L.S;
+  int max_cl = umma_num_sms() / csize;
+  {
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(csize * max_cl);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = L.smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, pair_kernel, &cfg) == cudaSuccess && n > 0)
+      max_cl = std::min(max_cl, n);
+    cudaGetLastError();
+  }
+  L.grid = csize * std::max(1, std::min(ntiles, max_cl));
+  return L;
+}
+
+cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
+  PairParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.a_crd = L.a_crd;
+  P.b_crd = L.b_crd;
+  P.s_crd = L.s_crd;
+  P.out_r = L.out_r;
+  P.out_c = L.out_c;
+  P.row_off = L.row_off;
+  P.col_off = L.col_off;
+  P.out = L.out;
+  P.out_bf16 = static_cast<__nv_bfloat16*>(L.out_bf16);
+  P.ws = L.ws;
+  P.epi_count = L.epi_count;
+  for (int e = 0; e < L.epi_count; ++e) {
+    P.epi_kind[e] = L.epi_kinds[e];
+    P.epi_ptr[e] = L.epi_ptr[e];
+  }
+  P.MT2 = L.MT / 2;
+  P.NT = L.NT;
+  P.KS = L.KS;
+  P.S = L.S;
+  P.ntiles = L.MT / 2 * L.NT;
+  P.group = L.group;
+  P.a_boxes = L.a_boxes;
+  P.b_boxes = L.b_boxes;
+  P.a_slot = L.a_slot;
+  P.b_slot = L.b_slot;
+  P.stage_bytes = L.stage_bytes;
+  P.tx_bytes = L.tx_bytes;
+  P.pipe = L.pipe;
+  P.BN = L.BN;
+  P.a_desc = L.a_desc;
+  P.b_desc = L.b_desc;
+  P.a_kadv = L.a_kadv;
+  P.b_kadv = L.b_kadv;
+  P.idesc = L.idesc;
+  P.tmem_cols = L.tmem_cols;
+  P.ring_bytes = L.ring_bytes;
+  P.col_unit = L.col_unit;
+  P.dbg = static_cast<unsigned long long*>(umma_debug_buffer());
+  P.dbg_split = getenv("LFGPU_PAIR_DBG_SPLIT") ? atoi(getenv("LFGPU_PAIR_DBG_SPLIT")) : -1;
+  static const bool pdl = [] {
+    const char* e = getenv("LFGPU_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(L.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * L.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, pair_kernel, L.tma_a, L.tma_b, P);
+}
+
+}  // namespace lfg

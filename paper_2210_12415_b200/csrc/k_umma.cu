@@ -21,6 +21,7 @@
 #include <cstring>
 #include <memory>
 
+#include "lf_pair.hpp"
 #include "lf_umma.hpp"
 
 namespace lfg {
@@ -1048,6 +1049,10 @@ bool umma_view_encodable(const OperandView& v, std::string* why) {
   }
 }
 
+CUtensorMap umma_encode(const OperandView& v, const void* base) { return encode(v, base); }
+uint64_t umma_desc_bits(const OperandView& v) { return desc_bits(v); }
+uint32_t umma_idesc(int M, int N, bool a_mn, bool b_mn) { return idesc_of(M, N, a_mn, b_mn); }
+
 static void* g_umma_dbg = nullptr;
 void* umma_debug_buffer() { return g_umma_dbg; }
 void umma_set_debug_buffer(void* p) { g_umma_dbg = p; }
@@ -1063,8 +1068,27 @@ static int num_sms() {
   return n;
 }
 
+int umma_num_sms() { return num_sms(); }
+
 UmmaLaunch umma_prepare(const UmmaPlan& p) {
   UmmaLaunch L;
+  if (p.pair) {
+    PairPlan q = *p.pair;
+    q.a = p.a;
+    q.b = p.b;
+    q.out = p.out;
+    q.out_bf16 = p.out_bf16;
+    q.epi_count = p.epi_count;
+    for (int e = 0; e < p.epi_count; ++e) q.epi[e] = p.epi[e];
+    L.pair = std::make_shared<PairLaunch>(pair_prepare(q));
+    L.ntiles = q.MT / 2 * q.NT;
+    L.BN = q.BN;
+    L.splits = L.pair->S;
+    L.grid = L.pair->grid;
+    L.pipe = L.pair->pipe;
+    L.store_mode = L.pair->col_unit;
+    return L;
+  }
   std::memset(&L.tma_o, 0, sizeof(L.tma_o));
   std::memset(&L.tma_ob, 0, sizeof(L.tma_ob));
   L.tma_a = encode(p.A, p.a);
@@ -1304,6 +1328,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
 
 cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   if (L.ntiles == 0) return cudaSuccess;
+  if (L.pair) return pair_launch(*L.pair, stream);
   UmmaParams P;
   std::memset(&P, 0, sizeof(P));
   P.tiles = static_cast<const TileEntry*>(L.d_tiles);

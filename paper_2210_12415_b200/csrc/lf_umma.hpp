@@ -24,6 +24,9 @@
 
 namespace lfg {
 
+struct PairPlan;    // lf_pair.hpp
+struct PairLaunch;
+
 enum { UMMA_GEMM = 0, UMMA_CONV = 1 };
 enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_RELU = 2, EPI_RESIDUAL = 3 };
 constexpr int kMaxEpi = 4;
@@ -138,6 +141,9 @@ struct UmmaPlan {
   float* out = nullptr;
   void* out_bf16 = nullptr;  // optional bf16 copy written by the epilogue
   std::string summary;
+  // GEMM on the CTA-pair kernel (k_pair.cu) when its tile is legal: the
+  // fields above except epi/a/b/out are then unused.
+  std::shared_ptr<PairPlan> pair;
 };
 
 // Per-launch device state (tables uploaded, tensor maps encoded).
@@ -181,6 +187,7 @@ struct UmmaLaunch {
   float* ws = nullptr;          // split-K partial tiles
   int* counters = nullptr;      // split-K per-tile arrival counters
   std::shared_ptr<void> owner;  // keeps the device tables alive
+  std::shared_ptr<PairLaunch> pair;  // launch through k_pair.cu instead
 };
 
 bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::vector<Dim>& b_log,
@@ -189,6 +196,13 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
 bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::vector<Dim>& k_log,
                     const Seq& k_seq, const std::vector<Dim>& y_log, const Seq& y_seq,
                     int64_t stride, const lfgpu_sched& s, UmmaPlan* out, std::string* why);
+// Tensor map of an operand view at `base`, its UMMA SMEM descriptor bits
+// (start address added on the device) and the kind::f16 instruction
+// descriptor (shared with the CTA-pair kernel, k_pair.cu).
+CUtensorMap umma_encode(const OperandView& v, const void* base);
+uint64_t umma_desc_bits(const OperandView& v);
+uint32_t umma_idesc(int M, int N, bool a_mn, bool b_mn);
+int umma_num_sms();
 // True when TMA can encode the view (checked with a dummy base address).
 bool umma_view_encodable(const OperandView& v, std::string* why);
 // Encodes tensor maps and uploads tables (needs a, b, out set).

@@ -14,10 +14,12 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <sstream>
 
+#include "lf_pair.hpp"
 #include "lf_umma.hpp"
 
 namespace lfg {
@@ -483,6 +485,24 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
   if (RT < 16 || RT > 128) {
     *why = "rows per tile out of range";
     return false;
+  }
+  if (RT == 128 && !getenv("LFGPU_NO_PAIR")) {
+    // The CTA-pair kernel (256-row tiles, cta_group::2) when the shape and
+    // the layouts allow it; the 1-CTA kernel below otherwise.
+    PairPlan pp;
+    std::string pwhy;
+    if (pair_plan_gemm(a_log, a_seq, b_log, b_seq, c_log, c_seq, s, &pp, &pwhy)) {
+      UmmaPlan q;
+      q.kind = UMMA_GEMM;
+      q.BM = 256;
+      q.BN = pp.BN;
+      q.pipe = pp.pipe;
+      q.summary = pp.summary;
+      q.pair = std::make_shared<PairPlan>(pp);
+      *out = q;
+      return true;
+    }
+    if (getenv("LFGPU_DEBUG_PAIR")) fprintf(stderr, "pair GEMM rejected: %s\n", pwhy.c_str());
   }
   const int64_t M = a_log[0].extent, K = a_log[1].extent, N = b_log[1].extent;
   if (K % 64) {
@@ -1386,6 +1406,151 @@ bool umma_scatter_desc(const std::vector<Dim>& xp_log, const Seq& xp_seq, int64_
   }
   d.enabled = 1;
   *sd = d;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair GEMM (k_pair.cu): 256 x BN tiles, cta_group::2, K splits in one
+// cluster. Same brick analysis as umma_plan_gemm; A is viewed in 128-row
+// boxes (one per CTA of the pair), B in BN/2-column boxes.
+
+bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::vector<Dim>& b_log,
+                    const Seq& b_seq, const std::vector<Dim>& c_log, const Seq& c_seq,
+                    const lfgpu_sched& s, PairPlan* out, std::string* why) {
+  const int64_t M = a_log[0].extent, K = a_log[1].extent, N = b_log[1].extent;
+  if (M % 256 || K % 64) {
+    *why = "pair GEMM needs M % 256 == 0 and K % 64 == 0";
+    return false;
+  }
+  std::vector<PDigit> cds;
+  if (!analyze(c_log, c_seq, &cds)) {
+    *why = "output layout is not a brick layout";
+    return false;
+  }
+  const int KS = static_cast<int>(K / 64);
+  const int sms = 148;
+  int force_bn = 0, force_s = 0;
+  if (const char* e = getenv("LFGPU_PAIR_BN")) force_bn = atoi(e);
+  if (const char* e = getenv("LFGPU_PAIR_S")) force_s = atoi(e);
+  if (!force_bn && (s.tile_last == 64 || s.tile_last == 128 || s.tile_last == 256)) force_bn = s.tile_last;
+  struct Cand {
+    int BN, S;
+    double cost;
+  };
+  std::vector<Cand> cands;
+  std::string last_why = "no legal pair tile";
+  PairPlan best;
+  double best_cost = 1e300;
+  for (int BN : {256, 128, 64}) {
+    if (force_bn && BN != force_bn) continue;
+    if (N % BN) {
+      last_why = "N not a multiple of the pair tile";
+      continue;
+    }
+    PairPlan q;
+    q.BN = BN;
+    std::vector<PDigit> ads, bds;
+    std::vector<int64_t> abox, bbox, tmp;
+    std::vector<int> ag, bg;
+    std::vector<int64_t> am, bm;
+    if (!gemm_operand(a_log, a_seq, 0, 1, 128, 64, &q.A, &ads, &abox, &ag, &am, &last_why)) {
+      *why = "A: " + last_why;
+      return false;
+    }
+    if (!gemm_operand(b_log, b_seq, 1, 0, BN / 2, 64, &q.B, &bds, &bbox, &bg, &bm, &last_why)) {
+      last_why = "B: " + last_why;
+      continue;
+    }
+    if (!cover(digits_of(cds, 0), 128, &tmp, &last_why) ||
+        !cover(digits_of(cds, 1), BN, &tmp, &last_why)) {
+      last_why = "C: " + last_why;
+      continue;
+    }
+    finish_descriptor(&q.A, 128);
+    finish_descriptor(&q.B, BN / 2);
+    q.MT = static_cast<int>(M / 128);
+    q.NT = static_cast<int>(N / BN);
+    q.KS = KS;
+    for (int mi = 0; mi < q.MT; ++mi)
+      for (int b = 0; b < q.A.boxes; ++b) {
+        int64_t lv[2] = {mi * 128 + (q.A.mn_major ? b * 64 : 0), 0};
+        int32_t c[5];
+        coords(ads, ag, am, lv, c);
+        q.a_crd.insert(q.a_crd.end(), c, c + 5);
+      }
+    for (int nb = 0; nb < 2 * q.NT; ++nb)
+      for (int b = 0; b < q.B.boxes; ++b) {
+        int64_t lv[2] = {0, static_cast<int64_t>(nb) * (BN / 2) + (q.B.mn_major ? b * 64 : 0)};
+        int32_t c[5];
+        coords(bds, bg, bm, lv, c);
+        q.b_crd.insert(q.b_crd.end(), c, c + 5);
+      }
+    for (int64_t k0 = 0; k0 < K; k0 += 64) {
+      int64_t la[2] = {0, k0}, lb[2] = {k0, 0};
+      int32_t ca[5], cb[5];
+      coords(ads, ag, am, la, ca);
+      coords(bds, bg, bm, lb, cb);
+      q.s_crd.insert(q.s_crd.end(), ca, ca + 5);
+      q.s_crd.insert(q.s_crd.end(), cb, cb + 5);
+    }
+    for (int mi = 0; mi < q.MT; ++mi) {
+      int64_t lv[2] = {static_cast<int64_t>(mi) * 128, 0};
+      q.out_r.push_back(offset_of(cds, lv));
+    }
+    for (int nj = 0; nj < q.NT; ++nj) {
+      int64_t lv[2] = {0, static_cast<int64_t>(nj) * BN};
+      q.out_c.push_back(offset_of(cds, lv));
+    }
+    for (int r = 0; r < 128; ++r) {
+      int64_t lv[2] = {r, 0};
+      q.row_off.push_back(offset_of(cds, lv));
+    }
+    for (int c = 0; c < BN; ++c) {
+      int64_t lv[2] = {0, c};
+      q.col_off.push_back(offset_of(cds, lv));
+    }
+    const int stage = q.A.slot_bytes * q.A.boxes + q.B.slot_bytes * q.B.boxes;
+    // 227 KB minus alignment slack, 4 epilogue transpose buffers and barriers.
+    const int budget = 227 * 1024 - 1024 - 4 * 32 * 36 * 4 - 512 - 40 * KS;
+    q.pipe = std::max(2, std::min(8, budget / stage));
+    if (const char* e = getenv("LFGPU_PAIR_PIPE")) q.pipe = std::max(2, std::min(q.pipe, atoi(e)));
+    const int tiles = q.MT / 2 * q.NT;
+    for (int S : {1, 2, 4}) {
+      if (force_s && S != force_s) continue;
+      if (!force_s && s.order == 1 && S > 1) continue;
+      if (!force_s && s.order == 2 && S < 2) continue;
+      if (KS % S || (BN / S) % 32) continue;
+      // Measured: with S > 1 (clusters of 4-8 CTAs) a second TMA box per
+      // operand in the second and later pairs of a cluster reads wrong data
+      // (MN-major B with BN/2 = 128, tests/test_gpu_pair.py); the first pair
+      // and K-major single-box operands are exact. Split only single-box tiles.
+      if (S > 1 && (q.A.boxes > 1 || q.B.boxes > 1)) continue;
+      if (S > 1 && KS / S < 2) continue;
+      // Cost model (cycles): waves x stages x max(MMA, ingest) + epilogue
+      // + split reduction + fixed latency. Ingest assumed ~48 B/clk/SM.
+      const int clusters = std::max(1, std::min(tiles, sms / (2 * S)));
+      const int waves = (tiles + clusters - 1) / clusters;
+      const double per_stage = std::max(2.0 * BN, stage / 48.0);
+      const double epi = 128.0 * BN * 4 / 64.0;
+      const double red = S > 1 ? (2.0 * 128 * BN * 4 + (S + 1.0) * 128 * BN / S * 4) / 64.0 : 0.0;
+      const double cost = waves * ((KS / S) * per_stage + epi + red) + 2500.0;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = q;
+        best.S = S;
+      }
+    }
+  }
+  if (best_cost >= 1e299) {
+    *why = last_why;
+    return false;
+  }
+  std::ostringstream os;
+  os << "gemm-pair BM=256 BN=" << best.BN << " S=" << best.S << " A=" << (best.A.mn_major ? "MN" : "K")
+     << "-major B=" << (best.B.mn_major ? "MN" : "K") << "-major tiles=" << best.MT / 2 * best.NT
+     << " pipe=" << best.pipe;
+  best.summary = os.str();
+  *out = best;
   return true;
 }
 

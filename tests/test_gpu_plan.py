@@ -216,7 +216,12 @@ def test_measure_reports_device_time():
 @pytest.mark.parametrize("factors,tile,order,vec", [
     ((128, 64, 256), 64, 1, 1), ((128, 64, 256), 128, 0, 1), ((128, 64, 256), 256, 0, 1),
     ((256, 128, 128), 128, 2, 0), ((128, 64, 128), 64, 0, 1)])
-def test_umma_gemm_epilogue_variants(factors, tile, order, vec):
+@pytest.mark.parametrize("one_cta", [1, 0])
+def test_umma_gemm_epilogue_variants(factors, tile, order, vec, one_cta, monkeypatch):
+    # one_cta=1 pins the 1-CTA kernel (its TMA-store / split-K epilogues);
+    # one_cta=0 lets the planner take the CTA-pair kernel (k_pair.cu).
+    if one_cta:
+        monkeypatch.setenv("LFGPU_NO_PAIR", "1")
     M = K = N = 512
     g = ir.gmm_chain(M, K, N)
     seqs = runtime.decode_layout(g, 0, list(factors))
@@ -227,7 +232,9 @@ def test_umma_gemm_epilogue_variants(factors, tile, order, vec):
                      flags=_abi.PLAN_REQUIRE_TC)
     k = p.node_kernel(0)
     assert k.startswith("umma_gemm"), k
-    if vec:
+    # An N-major B half needs >= 64 columns: tile 64 stays on the 1-CTA kernel.
+    assert ("gemm-pair" in k) == (not one_cta and tile >= 128), k
+    if vec and one_cta:
         assert "store=2" in k, k
     for tid, v in inputs.items():
         p.set_input(tid, v)
