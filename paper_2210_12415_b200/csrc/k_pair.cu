@@ -45,19 +45,16 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr int kEpiWarp0 = 4;
-constexpr int kLd = 36;  // transpose buffer row stride (floats)
-constexpr int kEpiBytes = 4 * 32 * kLd * 4;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant, alternating 32-column chunks
+constexpr int kLd = 36;       // transpose buffer row stride (floats)
+constexpr int kEpiBytes = kEpiWarps * 32 * kLd * 4;
 
 struct PairParams {
-  const int32_t* a_crd;
-  const int32_t* b_crd;
-  const int32_t* s_crd;
-  const int64_t* out_r;
-  const int64_t* out_c;
-  const int64_t* row_off;
-  const int64_t* col_off;
+  const int4* blob;          // tables (PairBlob layout), copied to SMEM at entry
+  PairBlob lay;
+  const int64_t* col_off;    // generic epilogue only
   float* out;
   __nv_bfloat16* out_bf16;
   float* ws;
@@ -76,6 +73,7 @@ struct PairParams {
   // epilogue done per tile (first 64 of each).
   unsigned long long* dbg;
   int32_t dbg_split;  // diagnostics: >= 0 keeps only that split's partial in the reduction
+  int32_t diag;       // diagnostics (LFGPU_PAIR_DIAG, timing only): bit0 skips the epilogue's global stores
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -95,35 +93,28 @@ __device__ __forceinline__ void tile_coords(const PairParams& P, int t, int* Mi,
   *Nj = r / gs;
 }
 
-// Fused element-wise chain on 4 consecutive columns of one row.
-__device__ __forceinline__ float4 epi4(const PairParams& P, float4 x, int n, int64_t addr) {
-#pragma unroll 1
-  for (int e = 0; e < P.epi_count; ++e) {
-    const int k = P.epi_kind[e];
-    const float* ep = P.epi_ptr[e];
-    if (k == EPI_RELU) {
-      x.x = fmaxf(x.x, 0.f);
-      x.y = fmaxf(x.y, 0.f);
-      x.z = fmaxf(x.z, 0.f);
-      x.w = fmaxf(x.w, 0.f);
-    } else {
-      const float4 b = k == EPI_BIAS ? make_float4(__ldg(ep + n), __ldg(ep + n + 1), __ldg(ep + n + 2),
-                                                   __ldg(ep + n + 3))
-                                     : __ldg(reinterpret_cast<const float4*>(ep + addr));
-      x.x += b.x;
-      x.y += b.y;
-      x.z += b.z;
-      x.w += b.w;
-    }
-  }
-  return x;
-}
+// SMEM tables of one CTA (after the barriers): stage coordinates, output
+// row / column-chunk offsets, row-block / column-tile origins, the tile's bias.
+struct Smem {
+  int32_t* stage;   // KS x 10
+  int64_t* row;     // 128
+  int64_t* colc;    // BN / 32 (offset of each 32-column chunk)
+  int64_t* outr;    // MT
+  int64_t* outc;    // NT
+  int32_t* acrd;    // MT x a_boxes x 5
+  int32_t* bcrd;    // 2 NT x b_boxes x 5
+  float* bias;      // 2 x BN (double-buffered by tile parity)
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // Store 32 accumulator columns [c0, c0+32) of the calling thread's row
-// (v[j] = column c0 + j) through the per-warp transpose buffer.
-__device__ __forceinline__ void store_chunk(const PairParams& P, const float* v, float* wbuf, int q,
-                                            int lane, int c0, int n0, int64_t obase,
-                                            const int64_t* row_off, const int64_t* col_off) {
+// (v[j] = column c0 + j). Row-segment path: a per-warp SMEM transpose so each
+// store instruction writes four 128-byte row segments; every table lives in
+// SMEM (an L2 round trip per chunk would pace the epilogue), residual loads
+// are all issued before they are consumed.
+__device__ __forceinline__ void store_chunk(const PairParams& P, const Smem& T, const float* v, float* wbuf,
+                                            int q, int lane, int c0, int64_t obase, const float* bias) {
   if (P.col_unit) {
     __syncwarp();
 #pragma unroll
@@ -132,36 +123,76 @@ __device__ __forceinline__ void store_chunk(const PairParams& P, const float* v,
           make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
     __syncwarp();
     const int cl = (lane & 7) * 4;
-    const int64_t cb = obase + __ldg(col_off + c0) + cl;
+    const int64_t cb = obase + T.colc[c0 >> 5] + cl;
+    float4 x[8];
+    int64_t addr[8];
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       const int rr = it * 4 + (lane >> 3);
-      float4 x = *reinterpret_cast<const float4*>(wbuf + rr * kLd + cl);
-      const int64_t addr = cb + __ldg(row_off + q * 32 + rr);
-      x = epi4(P, x, n0 + c0 + cl, addr);
-      *reinterpret_cast<float4*>(P.out + addr) = x;
+      x[it] = *reinterpret_cast<const float4*>(wbuf + rr * kLd + cl);
+      addr[it] = cb + T.row[q * 32 + rr];
+    }
+#pragma unroll 1
+    for (int e = 0; e < P.epi_count; ++e) {
+      const int k = P.epi_kind[e];
+      if (k == EPI_RELU) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          x[it].x = fmaxf(x[it].x, 0.f);
+          x[it].y = fmaxf(x[it].y, 0.f);
+          x[it].z = fmaxf(x[it].z, 0.f);
+          x[it].w = fmaxf(x[it].w, 0.f);
+        }
+      } else if (k == EPI_BIAS) {
+        const float4 b = *reinterpret_cast<const float4*>(bias + c0 + cl);
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          x[it].x += b.x;
+          x[it].y += b.y;
+          x[it].z += b.z;
+          x[it].w += b.w;
+        }
+      } else {  // EPI_RESIDUAL: same physical layout as the output
+        float4 r[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) r[it] = __ldg(reinterpret_cast<const float4*>(P.epi_ptr[e] + addr[it]));
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          x[it].x += r[it].x;
+          x[it].y += r[it].y;
+          x[it].z += r[it].z;
+          x[it].w += r[it].w;
+        }
+      }
+    }
+    if (P.diag & 1) return;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      *reinterpret_cast<float4*>(P.out + addr[it]) = x[it];
       if (P.out_bf16) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y);
-        __nv_bfloat162 hi = __floats2bfloat162_rn(x.z, x.w);
+        __nv_bfloat162 lo = __floats2bfloat162_rn(x[it].x, x[it].y);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(x[it].z, x[it].w);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(P.out_bf16 + addr) = pk;
+        *reinterpret_cast<uint2*>(P.out_bf16 + addr[it]) = pk;
       }
     }
     return;
   }
-  // Generic layouts: thread = row, one element at a time.
-  const int64_t rb = obase + __ldg(row_off + q * 32 + lane);
+  // Generic layouts: thread = row, one element at a time (column offsets
+  // from the global table, L1-resident after the first tile).
+  const int64_t rb = obase + T.row[q * 32 + lane];
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
-    const int64_t addr = rb + __ldg(col_off + c0 + j);
+    const int64_t addr = rb + __ldg(P.col_off + c0 + j);
     float y = v[j];
 #pragma unroll 1
     for (int e = 0; e < P.epi_count; ++e) {
       const int k = P.epi_kind[e];
       if (k == EPI_RELU) y = fmaxf(y, 0.f);
-      else y += __ldg(P.epi_ptr[e] + (k == EPI_BIAS ? static_cast<int64_t>(n0 + c0 + j) : addr));
+      else if (k == EPI_BIAS) y += bias[c0 + j];
+      else y += __ldg(P.epi_ptr[e] + addr);
     }
     P.out[addr] = y;
     if (P.out_bf16) P.out_bf16[addr] = __float2bfloat16_rn(y);
@@ -171,6 +202,7 @@ __device__ __forceinline__ void store_chunk(const PairParams& P, const float* v,
 __global__ void __launch_bounds__(kThreads, 1)
     pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                 const __grid_constant__ PairParams P) {
+  if (P.dbg && threadIdx.x == 0) P.dbg[512 * blockIdx.x + 320] = gtime();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes);
@@ -182,7 +214,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tempty0 = tfull0 + 16;       // 2 accumulator-free barriers (leader)
   const uint32_t red0 = tempty0 + 16;         // 2 split-reduction barriers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * pipe + 6);
-  int32_t* s_stage = reinterpret_cast<int32_t*>(bars + 2 * pipe + 8);  // KS x 10 stage coordinates
+  int32_t* blob = reinterpret_cast<int32_t*>(bars + 2 * pipe + 8);  // 16-byte aligned
+  Smem T;
+  T.stage = blob + P.lay.stage;
+  T.row = reinterpret_cast<int64_t*>(blob + P.lay.row);
+  T.colc = reinterpret_cast<int64_t*>(blob + P.lay.colc);
+  T.outr = reinterpret_cast<int64_t*>(blob + P.lay.outr);
+  T.outc = reinterpret_cast<int64_t*>(blob + P.lay.outc);
+  T.acrd = blob + P.lay.acrd;
+  T.bcrd = blob + P.lay.bcrd;
+  T.bias = reinterpret_cast<float*>(blob + P.lay.total);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
@@ -196,18 +237,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < pipe; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);  // the pair's MMA commit (both producer warps wait on it)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull0 + 8 * b, 1);
-      mbar_init(tempty0 + 8 * b, 2 * 4);  // both CTAs' epilogue warps
-      mbar_init(red0 + 8 * b, S * 4);     // epilogue warps of the S CTAs holding these rows
+      mbar_init(tempty0 + 8 * b, 2 * kEpiWarps);  // both CTAs' epilogue warps
+      mbar_init(red0 + 8 * b, S * kEpiWarps);     // epilogue warps of the S CTAs holding these rows
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
-  for (int i = threadIdx.x; i < 10 * P.KS; i += kThreads) s_stage[i] = __ldg(P.s_crd + i);
+  // Plan tables (host-written once, never by kernels: safe before the PDL wait).
+  {  // one pass, all loads of a thread in flight together
+    const int n4 = P.lay.total / 4;
+    int4* dst = reinterpret_cast<int4*>(blob);
+    int i0 = threadIdx.x;
+    for (; i0 + 3 * kThreads < n4; i0 += 4 * kThreads) {
+      int4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __ldg(P.blob + i0 + k * kThreads);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[i0 + k * kThreads] = v[k];
+    }
+    for (; i0 < n4; i0 += kThreads) dst[i0] = __ldg(P.blob + i0);
+  }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
@@ -219,57 +273,55 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (P.dbg && threadIdx.x == 0) P.dbg[512 * blockIdx.x + 321] = gtime();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (P.dbg && threadIdx.x == 0) P.dbg[512 * blockIdx.x + 322] = gtime();
 
   const int s_lo = split * P.KS / S, s_hi = (split + 1) * P.KS / S;
   const uint32_t ring0 = smem_u32(smem);
 
-  if (warp == 0) {
-    // ---- TMA producer (both CTAs of the pair). Coordinates never come from
-    // global memory inside the stage loop: the tile part is loaded into
-    // registers once per tile, the stage part lives in SMEM (an L2 round
-    // trip per stage would pace the whole pipeline).
+  if (warp == 0 || warp == 3) {
+    // ---- TMA producers (both CTAs of the pair): warp 0 loads the A boxes
+    // (and, in the pair leader, arms the stage's expected bytes), warp 3 the
+    // B boxes. One issuing thread cannot keep a stage's boxes in flight fast
+    // enough (each UTMALDG costs hundreds of cycles to issue). Coordinates
+    // never come from global memory inside the stage loop: the tile part is
+    // loaded into registers once per tile, the stage part lives in SMEM.
+    const bool is_a = warp == 0;
     if (elect_one()) {
       const uint32_t lead_full0 = mapa(full0, lead);
       const uint32_t b_off = P.a_boxes * P.a_slot;
+      const int nbox = is_a ? P.a_boxes : P.b_boxes;
+      const int sl = is_a ? P.a_slot : P.b_slot;
+      const CUtensorMap* map = is_a ? &tma_a : &tma_b;
+      const int so = is_a ? 0 : 5;
       int g = 0;
       for (int t = cid; t < P.ntiles; t += ncl) {
         int Mi, Nj;
         tile_coords(P, t, &Mi, &Nj);
-        int32_t ta[kMaxBoxes][5], tb[kMaxBoxes][5];
-        const int32_t* ca = P.a_crd + (2 * Mi + pr) * P.a_boxes * 5;
-        const int32_t* cb = P.b_crd + (2 * Nj + pr) * P.b_boxes * 5;
+        int32_t tc[kMaxBoxes][5];
+        const int32_t* cp = is_a ? T.acrd + (2 * Mi + pr) * P.a_boxes * 5 : T.bcrd + (2 * Nj + pr) * P.b_boxes * 5;
 #pragma unroll
         for (int b = 0; b < kMaxBoxes; ++b)
 #pragma unroll
-          for (int d = 0; d < 5; ++d) {
-            ta[b][d] = b < P.a_boxes ? __ldg(ca + b * 5 + d) : 0;
-            tb[b][d] = b < P.b_boxes ? __ldg(cb + b * 5 + d) : 0;
-          }
+          for (int d = 0; d < 5; ++d) tc[b][d] = b < nbox ? cp[b * 5 + d] : 0;
         for (int s = s_lo; s < s_hi; ++s, ++g) {
           const int slot = g % pipe;
           const uint32_t ph = static_cast<uint32_t>(g / pipe) & 1u;
-          const int32_t* sc = s_stage + s * 10;
+          const int32_t* sc = T.stage + s * 10 + so;
           int32_t c[5];
           mbar_wait(empty0 + 8 * slot, ph ^ 1u);
-          if (P.dbg && g < 64) P.dbg[256 * blockIdx.x + g] = gtime();
-          if (pr == 0) mbar_expect_tx(full0 + 8 * slot, 2 * P.tx_bytes);
+          if (P.dbg && is_a && g < 64) P.dbg[512 * blockIdx.x + g] = gtime();
+          if (is_a && pr == 0) mbar_expect_tx(full0 + 8 * slot, 2 * P.tx_bytes);
           const uint32_t bar = lead_full0 + 8 * slot;
-          const uint32_t dst = ring0 + slot * P.stage_bytes;
+          const uint32_t dst = ring0 + slot * P.stage_bytes + (is_a ? 0 : b_off);
 #pragma unroll
           for (int b = 0; b < kMaxBoxes; ++b)
-            if (b < P.a_boxes) {
+            if (b < nbox) {
 #pragma unroll
-              for (int d = 0; d < 5; ++d) c[d] = ta[b][d] + sc[d];
-              tma_load5_pair(&tma_a, dst + b * P.a_slot, bar, c);
-            }
-#pragma unroll
-          for (int b = 0; b < kMaxBoxes; ++b)
-            if (b < P.b_boxes) {
-#pragma unroll
-              for (int d = 0; d < 5; ++d) c[d] = tb[b][d] + sc[5 + d];
-              tma_load5_pair(&tma_b, dst + b_off + b * P.b_slot, bar, c);
+              for (int d = 0; d < 5; ++d) c[d] = tc[b][d] + sc[d];
+              tma_load5_pair(map, dst + b * sl, bar, c);
             }
         }
       }
@@ -290,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int slot = g % pipe;
         mbar_wait(full0 + 8 * slot, static_cast<uint32_t>(g / pipe) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (P.dbg && issuer && g < 64) P.dbg[256 * blockIdx.x + 64 + g] = gtime();
+        if (P.dbg && issuer && g < 64) P.dbg[512 * blockIdx.x + 64 + g] = gtime();
         if (issuer) {
           const uint32_t a_addr = ring0 + slot * P.stage_bytes;
           const uint64_t ad = P.a_desc | (a_addr >> 4), bd = P.b_desc | ((a_addr + b_off) >> 4);
@@ -305,41 +357,57 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
   } else if (warp >= kEpiWarp0) {
-    // ---- epilogue (both CTAs): warp w reads TMEM lanes 32*(w%4)..+31
-    const int q = warp & 3;
+    // ---- epilogue (both CTAs): warp w reads TMEM lanes 32*(w%4)..+31; the
+    // two warps of a lane quadrant take alternate 32-column chunks
+    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
     const int row = q * 32 + lane;
-    float* wbuf = s_epi + q * 32 * kLd;
+    const int etid = (warp - kEpiWarp0) * 32 + lane;
+    float* wbuf = s_epi + (warp - kEpiWarp0) * 32 * kLd;
     const uint32_t lead_tempty0 = mapa(tempty0, lead);
+    bool has_bias = false;
+    const float* bias_ptr = nullptr;
+    for (int e = 0; e < P.epi_count; ++e)
+      if (P.epi_kind[e] == EPI_BIAS) {
+        has_bias = true;
+        bias_ptr = P.epi_ptr[e];
+      }
     int i = 0;
     for (int t = cid; t < P.ntiles; t += ncl, ++i) {
       int Mi, Nj;
       tile_coords(P, t, &Mi, &Nj);
       const int acc = i & 1;
       const int mi = 2 * Mi + pr;
-      const int64_t obase = __ldg(P.out_r + mi) + __ldg(P.out_c + Nj);
+      const int64_t obase = T.outr[mi] + T.outc[Nj];
       const int n0 = Nj * P.BN;
+      float* bias = T.bias + acc * P.BN;
+      if (has_bias) {  // the tile's bias slice, before waiting for the accumulator
+        for (int c = etid; c < P.BN; c += 32 * kEpiWarps) bias[c] = __ldg(bias_ptr + n0 + c);
+        epi_bar();
+      }
       mbar_wait(tfull0 + 8 * acc, static_cast<uint32_t>(i >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (P.dbg && row == 0 && i < 64) P.dbg[256 * blockIdx.x + 128 + i] = gtime();
+      if (P.dbg && etid == 0 && i < 64) P.dbg[512 * blockIdx.x + 128 + i] = gtime();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.BN);
       float v[32];
       if (S == 1) {
-        for (int c0 = 0; c0 < P.BN; c0 += 32) {
+        for (int c0 = 32 * half; c0 < P.BN; c0 += 64) {
           tmem_ld32(taddr + c0, v);
-          if (c0 + 32 == P.BN) {  // accumulator fully read: hand it back
+          if (P.dbg && etid == 0 && i == 0 && c0 < 32 * 32) P.dbg[512 * blockIdx.x + 256 + c0 / 16] = gtime();
+          if (c0 + 64 >= P.BN) {  // this warp's last read of the accumulator: hand it back
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(lead_tempty0 + 8 * acc);
+            if (lane == 0) mbar_arrive_relaxed_cluster(lead_tempty0 + 8 * acc);
           }
-          store_chunk(P, v, wbuf, q, lane, c0, n0, obase, P.row_off, P.col_off);
+          store_chunk(P, T, v, wbuf, q, lane, c0, obase, bias);
+          if (P.dbg && etid == 0 && i == 0 && c0 < 32 * 32) P.dbg[512 * blockIdx.x + 257 + c0 / 16] = gtime();
         }
-        if (P.dbg && row == 0 && i < 64) P.dbg[256 * blockIdx.x + 192 + i] = gtime();
+        if (P.dbg && etid == 0 && i < 64) P.dbg[512 * blockIdx.x + 192 + i] = gtime();
         continue;
       }
       // Split K: publish this split's partial rows ([col/4][row] float4).
       const size_t tile_floats = static_cast<size_t>(128) * P.BN;
       float4* mine = reinterpret_cast<float4*>(P.ws + ((static_cast<size_t>(t) * S + split) * 2 + pr) * tile_floats);
-      for (int c0 = 0; c0 < P.BN; c0 += 32) {
+      for (int c0 = 32 * half; c0 < P.BN; c0 += 64) {
         tmem_ld32(taddr + c0, v);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -349,12 +417,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       __threadfence();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive_cluster(lead_tempty0 + 8 * acc);
+        mbar_arrive_relaxed_cluster(lead_tempty0 + 8 * acc);
         for (int p = 0; p < S; ++p) mbar_arrive_cluster(mapa(red0 + 8 * acc, 2 * p + pr));
       }
       mbar_wait_cluster(red0 + 8 * acc, static_cast<uint32_t>(i >> 1) & 1u);
       const int W = P.BN / S;
-      for (int c0 = split * W; c0 < (split + 1) * W; c0 += 32) {
+      for (int c0 = split * W + 32 * half; c0 < (split + 1) * W; c0 += 64) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.f;
         for (int p = 0; p < S; ++p) {
@@ -370,12 +438,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[4 * j + 3] += x.w;
           }
         }
-        store_chunk(P, v, wbuf, q, lane, c0, n0, obase, P.row_off, P.col_off);
+        store_chunk(P, T, v, wbuf, q, lane, c0, obase, bias);
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync();
+  if (P.dbg && threadIdx.x == 0) P.dbg[512 * blockIdx.x + 323] = gtime();
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols)
@@ -408,20 +477,21 @@ PairLaunch pair_prepare(const PairPlan& p) {
   L.tma_a = umma_encode(p.A, p.a);
   L.tma_b = umma_encode(p.B, p.b);
   auto t = std::make_shared<PairTables>();
-  t->p[0] = upload(p.a_crd);
-  t->p[1] = upload(p.b_crd);
-  t->p[2] = upload(p.s_crd);
-  t->p[3] = upload(p.out_r);
-  t->p[4] = upload(p.out_c);
-  t->p[5] = upload(p.row_off);
-  t->p[6] = upload(p.col_off);
-  L.a_crd = static_cast<const int32_t*>(t->p[0]);
-  L.b_crd = static_cast<const int32_t*>(t->p[1]);
-  L.s_crd = static_cast<const int32_t*>(t->p[2]);
-  L.out_r = static_cast<const int64_t*>(t->p[3]);
-  L.out_c = static_cast<const int64_t*>(t->p[4]);
-  L.row_off = static_cast<const int64_t*>(t->p[5]);
-  L.col_off = static_cast<const int64_t*>(t->p[6]);
+  L.lay = pair_blob_layout(p.KS, p.MT, p.NT, p.A.boxes, p.B.boxes);
+  {
+    std::vector<int32_t> blob(L.lay.total, 0);
+    std::memcpy(blob.data() + L.lay.stage, p.s_crd.data(), 4 * p.s_crd.size());
+    std::memcpy(blob.data() + L.lay.row, p.row_off.data(), 8 * std::min<size_t>(128, p.row_off.size()));
+    for (int c = 0; c < p.BN / 32; ++c) std::memcpy(blob.data() + L.lay.colc + 2 * c, &p.col_off[32 * c], 8);
+    std::memcpy(blob.data() + L.lay.outr, p.out_r.data(), 8 * p.out_r.size());
+    std::memcpy(blob.data() + L.lay.outc, p.out_c.data(), 8 * p.out_c.size());
+    std::memcpy(blob.data() + L.lay.acrd, p.a_crd.data(), 4 * p.a_crd.size());
+    std::memcpy(blob.data() + L.lay.bcrd, p.b_crd.data(), 4 * p.b_crd.size());
+    t->p[0] = upload(blob);
+  }
+  t->p[1] = upload(p.col_off);
+  L.blob = static_cast<const int32_t*>(t->p[0]);
+  L.col_off = static_cast<const int64_t*>(t->p[1]);
   L.BN = p.BN;
   L.S = p.S;
   L.MT = p.MT;
@@ -443,7 +513,8 @@ PairLaunch pair_prepare(const PairPlan& p) {
   while (cols < 2 * p.BN) cols *= 2;
   L.tmem_cols = cols;
   L.ring_bytes = L.pipe * L.stage_bytes;
-  L.smem = 1024 + L.ring_bytes + kEpiBytes + 8 * (2 * L.pipe + 8) + 40 * static_cast<size_t>(p.KS);
+  L.smem = 1024 + L.ring_bytes + kEpiBytes + 8 * (2 * L.pipe + 8) +
+           pair_table_bytes(p.KS, p.MT, p.NT, p.BN, p.A.boxes, p.B.boxes);
   if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "pair kernel SMEM exceeds 227 KB");
   // Row-segment stores need contiguous output columns and 16-byte aligned rows.
   bool unit = true;
@@ -509,12 +580,8 @@ PairLaunch pair_prepare(const PairPlan& p) {
 cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
   PairParams P;
   std::memset(&P, 0, sizeof(P));
-  P.a_crd = L.a_crd;
-  P.b_crd = L.b_crd;
-  P.s_crd = L.s_crd;
-  P.out_r = L.out_r;
-  P.out_c = L.out_c;
-  P.row_off = L.row_off;
+  P.blob = reinterpret_cast<const int4*>(L.blob);
+  P.lay = L.lay;
   P.col_off = L.col_off;
   P.out = L.out;
   P.out_bf16 = static_cast<__nv_bfloat16*>(L.out_bf16);
@@ -548,6 +615,7 @@ cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
   P.col_unit = L.col_unit;
   P.dbg = static_cast<unsigned long long*>(umma_debug_buffer());
   P.dbg_split = getenv("LFGPU_PAIR_DBG_SPLIT") ? atoi(getenv("LFGPU_PAIR_DBG_SPLIT")) : -1;
+  P.diag = getenv("LFGPU_PAIR_DIAG") ? atoi(getenv("LFGPU_PAIR_DIAG")) : 0;
   static const bool pdl = [] {
     const char* e = getenv("LFGPU_PDL");
     return !(e && atoi(e) == 0);

@@ -26,6 +26,40 @@
 
 namespace lfg {
 
+// The kernel's tables, one int32 blob copied to SMEM in a single pass at
+// kernel start (one DRAM latency, before the PDL wait): stage coordinates,
+// output row offsets, 32-column chunk offsets, row-block / column-tile
+// origins, per-row-block A box coordinates, per-column-block B box
+// coordinates. Sections start on 16-byte boundaries.
+struct PairBlob {
+  int stage = 0, row = 0, colc = 0, outr = 0, outc = 0, acrd = 0, bcrd = 0, total = 0;  // int32 offsets
+};
+inline PairBlob pair_blob_layout(int KS, int MT, int NT, int a_boxes, int b_boxes) {
+  auto up4 = [](int x) { return (x + 3) / 4 * 4; };
+  PairBlob b;
+  int o = 0;
+  b.stage = o;
+  o += up4(10 * KS);
+  b.row = o;
+  o += 256;
+  b.colc = o;
+  o += 16;
+  b.outr = o;
+  o += up4(2 * MT);
+  b.outc = o;
+  o += up4(2 * NT);
+  b.acrd = o;
+  o += up4(MT * a_boxes * 5);
+  b.bcrd = o;
+  o += up4(2 * NT * b_boxes * 5);
+  b.total = o;
+  return b;
+}
+// SMEM bytes of the tables plus the double-buffered tile bias.
+inline size_t pair_table_bytes(int KS, int MT, int NT, int BN, int a_boxes, int b_boxes) {
+  return 4 * static_cast<size_t>(pair_blob_layout(KS, MT, NT, a_boxes, b_boxes).total) + 8 * static_cast<size_t>(BN);
+}
+
 struct PairPlan {
   int BN = 256;   // pair tile columns (each CTA stages BN/2 of B)
   int S = 1;      // K splits (cluster = 2*S CTAs)
@@ -52,13 +86,9 @@ struct PairPlan {
 struct PairLaunch {
   CUtensorMap tma_a, tma_b;
   std::shared_ptr<void> owner;  // device tables + workspace
-  const int32_t* a_crd = nullptr;
-  const int32_t* b_crd = nullptr;
-  const int32_t* s_crd = nullptr;
-  const int64_t* out_r = nullptr;
-  const int64_t* out_c = nullptr;
-  const int64_t* row_off = nullptr;
-  const int64_t* col_off = nullptr;
+  const int32_t* blob = nullptr;     // PairBlob-laid-out tables
+  PairBlob lay;
+  const int64_t* col_off = nullptr;  // full column table (generic epilogue)
   float* ws = nullptr;
   int BN = 0, S = 1, MT = 0, NT = 0, KS = 0, pipe = 0, group = 8;
   int a_boxes = 0, b_boxes = 0, a_slot = 0, b_slot = 0, stage_bytes = 0, tx_bytes = 0;

@@ -1511,7 +1511,12 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     }
     const int stage = q.A.slot_bytes * q.A.boxes + q.B.slot_bytes * q.B.boxes;
     // 227 KB minus alignment slack, 4 epilogue transpose buffers and barriers.
-    const int budget = 227 * 1024 - 1024 - 4 * 32 * 36 * 4 - 512 - 40 * KS;
+    if (q.MT + q.NT > 4096) {
+      last_why = "pair GEMM output tables exceed SMEM";
+      continue;
+    }
+    const int budget = 227 * 1024 - 1024 - 8 * 32 * 36 * 4 - 512 -
+                       static_cast<int>(pair_table_bytes(KS, q.MT, q.NT, BN, q.A.boxes, q.B.boxes));
     q.pipe = std::max(2, std::min(8, budget / stage));
     if (const char* e = getenv("LFGPU_PAIR_PIPE")) q.pipe = std::max(2, std::min(q.pipe, atoi(e)));
     const int tiles = q.MT / 2 * q.NT;

@@ -25,20 +25,29 @@ p.set_input_device("b", y)
 for _ in range(3):
     p.run()
 torch.cuda.synchronize()
-buf = torch.zeros(256 * 160, dtype=torch.int64, device="cuda")
+buf = torch.zeros(512 * 160, dtype=torch.int64, device="cuda")
 runtime.lib().lfgpu_debug_umma_trace(C.c_void_p(buf.data_ptr()))
 p2 = runtime.Plan(g, seqs, [], flags=_abi.PLAN_REQUIRE_TC)
 p2.set_input_device("a", x)
 p2.set_input_device("b", y)
 torch.cuda.synchronize()
+if os.environ.get("TRACE_COLD"):
+    fl = torch.zeros(64 << 20, device="cuda")
+    fl.add_(1.0)
+    fl.amax()
+    torch.cuda.synchronize()
 p2.run()
 torch.cuda.synchronize()
 runtime.lib().lfgpu_debug_umma_trace(None)
 print(p2.node_kernel(0))
-t = buf.cpu().numpy().reshape(-1, 256).astype(np.int64)
-ncta = int((t[:, 0] != 0).sum())
+t = buf.cpu().numpy().reshape(-1, 512).astype(np.int64)
+ncta = int((t[:, 320] != 0).sum())
 t = t[:ncta]
 t0 = t[t > 0].min()
+ent = (t[:, 320] - t0) / 1e3
+print("entry spread (us): min %.2f max %.2f; setup done %.2f; pdl wait done %.2f; exit max %.2f" % (
+    ent.min(), ent.max(), np.median(t[:, 321] - t0) / 1e3, np.median(t[:, 322] - t0) / 1e3,
+    (t[:, 323].max() - t0) / 1e3))
 for cta in (0, 1, 2, 3, ncta // 2):
     r = t[cta]
     prod = r[0:64][r[0:64] > 0] - t0
@@ -52,4 +61,8 @@ for cta in (0, 1, 2, 3, ncta // 2):
         print("   stage period median %.1f ns, p90 %.1f ns" % (np.median(d), np.percentile(d, 90)))
         k = min(len(prod), len(full))
         print("   acquire->landed latency median %.1f ns" % np.median(full[:k] - prod[:k]))
+    ch = r[256:320]
+    if (ch > 0).any():
+        c = ch[ch > 0] - t0
+        print("   tile0 chunks: ld/store stamps (us):", np.round(c[:16] / 1e3, 2))
     print("   tile ready (us):", np.round(ready[:6] / 1e3, 2), " epilogue done:", np.round(done[:6] / 1e3, 2))
