@@ -383,16 +383,13 @@ def run_ours(args, rank, world, local):
     # fused epilogues, whole-graph CUDA graph) and cfg5 BERT-base GEMM chain
     # (seq 128, 12 layers); device time per inference step, L2 flushed.
     if not args.no_e2e_graphs:
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        import bert_run
-        import resnet18_run
-        from paper_2210_12415_b200 import workloads
+        from paper_2210_12415_b200 import e2e, workloads
         try:
             t0 = time.perf_counter()
-            fac = workloads.tune_resnet18(1, lambda sub: resnet18_run.make_inputs(sub, gen), ctx=ctx)
+            fac = workloads.tune_resnet18(1, lambda sub: e2e.make_inputs(sub, gen), ctx=ctx)
             tune_s = time.perf_counter() - t0
-            g18, _, p18 = resnet18_run.build(1, fac, ctx=ctx)
-            for k, x in resnet18_run.make_inputs(g18, gen).items():
+            g18, _, p18 = e2e.build_resnet18(1, fac, ctx=ctx)
+            for k, x in e2e.make_inputs(g18, gen).items():
                 p18.set_input_device(k, x)
             m18 = p18.measure(warmup=5, reps=30, flush_l2=True)
             kinds = [p18.node_kernel(i) for i in range(len(g18.nodes))]
@@ -411,10 +408,10 @@ def run_ours(args, rank, world, local):
             gb = 64
             _, nloc = shard.batch_shard(gb, rank, world)
             t0 = time.perf_counter()
-            facb = workloads.tune_resnet18(nloc, lambda sub: resnet18_run.make_inputs(sub, gen), ctx=ctx)
+            facb = workloads.tune_resnet18(nloc, lambda sub: e2e.make_inputs(sub, gen), ctx=ctx)
             tune_b = time.perf_counter() - t0
-            gbb, _, pbb = resnet18_run.build(nloc, facb, ctx=ctx)
-            for k, x in resnet18_run.make_inputs(gbb, gen).items():
+            gbb, _, pbb = e2e.build_resnet18(nloc, facb, ctx=ctx)
+            for k, x in e2e.make_inputs(gbb, gen).items():
                 pbb.set_input_device(k, x)
             mbb = pbb.measure(warmup=3, reps=20, flush_l2=True)
             step_us = max_over_ranks(mbb.cost, world)
@@ -430,8 +427,8 @@ def run_ours(args, rank, world, local):
         try:
             best = None
             for t in (64, 128):
-                gb, _, pb = bert_run.build(12, t, 0, ctx=ctx)
-                for k, x in bert_run.make_inputs(gb, gen).items():
+                gb, _, pb = e2e.build_bert(12, t, 0, ctx=ctx)
+                for k, x in e2e.make_bert_inputs(gb, gen).items():
                     pb.set_input_device(k, x)
                 mb = pb.measure(warmup=5, reps=30, flush_l2=True)
                 if best is None or mb.cost < best[0]:

@@ -183,9 +183,13 @@ inline std::vector<lfgpu_sched> to_scheds(const Graph& g, const SeqMap& seqs,
 
 /// interpret(lower(g, seqs, scheds), inputs) on the GPU; every node output in
 /// its logical layout, like InterpResult::outputs (interp.hpp:33-42).
+/// Default: reference semantics (LFGPU_PLAN_EXACT, the 1e-5 rule of
+/// cli.cpp:30-49 holds on chained graphs). Pass LFGPU_PLAN_TENSOR_CORES to
+/// run the tcgen05 kernels (bf16 operands: exact on k/64 inputs, ~2^-9
+/// relative per chained contraction otherwise).
 inline BufferMap interpret(Context& ctx, const Graph& g, const SeqMap& seqs,
                            const std::vector<LoopSchedule>& scheds, const BufferMap& inputs,
-                           int flags = LFGPU_PLAN_DEFAULT) {
+                           int flags = LFGPU_PLAN_EXACT) {
   Desc d = describe(g, seqs);
   auto sc = to_scheds(g, seqs, scheds);
   BufferMap out;

@@ -197,7 +197,15 @@ enum {
   LFGPU_PLAN_CUDA_GRAPH = 1 << 2,
   /* Materialize every node output (no epilogue fusion); lfgpu_interpret
    * sets it so all node outputs can be compared with reference_eval. */
-  LFGPU_PLAN_KEEP_ALL = 1 << 3
+  LFGPU_PLAN_KEEP_ALL = 1 << 3,
+  /* lfgpu_interpret only: opt into the tcgen05 contractions (bf16 operands,
+   * fp32 accumulation; bit-exact on the reference's k/64 inputs, ~2^-9
+   * relative per chained contraction otherwise). Without it (or
+   * LFGPU_PLAN_REQUIRE_TC) lfgpu_interpret runs LFGPU_PLAN_EXACT: the
+   * reference's double arithmetic up to fp32 storage (1e-5 rule,
+   * proj/src/cli.cpp:30-49). Plans (lfgpu_plan_build) use tensor cores by
+   * default. */
+  LFGPU_PLAN_TENSOR_CORES = 1 << 4
 };
 
 typedef struct lfgpu_ctx lfgpu_ctx;
@@ -298,7 +306,15 @@ int lfgpu_plan_set_input_device_async(lfgpu_plan* plan, int32_t tensor, const vo
 int lfgpu_plan_run(lfgpu_plan* plan);
 /* Same, enqueued on the caller's stream instead of the plan's own (NULL:
  * the plan's stream). Stream-ordered like a kernel launch; several plans
- * may share one stream. */
+ * may share one stream. The run is joined to the plan's own stream both
+ * ways (events): it starts after work already enqueued there (e.g.
+ * lfgpu_plan_set_input_device_async) and later plan-stream work
+ * (lfgpu_plan_get_output, set-input) starts after it.
+ * Co-residency: 1-CTA split-K contractions meet at per-tile counters and
+ * assume all CTAs of their grid are resident at once; do not run two such
+ * plans concurrently on different streams of one device (the CTA-pair
+ * kernel's splits meet inside a thread-block cluster and have no such
+ * requirement). */
 int lfgpu_plan_run_on(lfgpu_plan* plan, void* stream);
 /* Convert a node output back to its logical layout and copy it to host
  * doubles (interp.cpp:441-468). Synchronises the plan's stream. */
@@ -323,7 +339,9 @@ int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t f
 /* One-call interpret: lf::interpret(lower(g, seqs, sched), inputs)
  * (interp.cpp:424-470). host_bufs has one pointer per tensor (declaration
  * order): Input/Constant entries are read (logical doubles), node-output
- * entries are written (logical doubles), other entries may be NULL. */
+ * entries are written (logical doubles), other entries may be NULL.
+ * Reference semantics by default (LFGPU_PLAN_EXACT is implied unless
+ * LFGPU_PLAN_TENSOR_CORES or LFGPU_PLAN_REQUIRE_TC is passed). */
 int lfgpu_interpret(lfgpu_ctx* ctx, const lfgpu_graph* g, int32_t nsched,
                     const lfgpu_sched* sched, int32_t flags, double* const* host_bufs);
 

@@ -27,6 +27,8 @@ PLAN_DEFAULT = 0
 PLAN_EXACT = 1
 PLAN_REQUIRE_TC = 2
 PLAN_CUDA_GRAPH = 4
+PLAN_KEEP_ALL = 8
+PLAN_TENSOR_CORES = 16  # lfgpu_interpret: opt into tcgen05 (else reference semantics, EXACT)
 
 
 class Prim(C.Structure):

@@ -224,10 +224,16 @@ struct lfgpu_plan {
   cudaStream_t stream = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  // run_on(user stream) joins the plan stream both ways: the run waits for
+  // work already enqueued on the plan stream (async set-input conversions),
+  // later plan-stream work (get_output, set-input) waits for the run.
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   int64_t bytes = 0, flops = 0, tc_nodes = 0;
   std::vector<int> order;
 
   ~lfgpu_plan() {
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
     keep.clear();
@@ -1318,7 +1324,20 @@ int lfgpu_plan_run(lfgpu_plan* plan) {
 int lfgpu_plan_run_on(lfgpu_plan* plan, void* stream) {
   return guarded([&] {
     CUDA_OK(cudaSetDevice(plan->ctx->device));
-    plan_run_steps(plan, static_cast<cudaStream_t>(stream));
+    cudaStream_t us = static_cast<cudaStream_t>(stream);
+    if (!us || us == plan->stream) {
+      plan_run_steps(plan, plan->stream);
+      return;
+    }
+    if (!plan->ev_in) {
+      CUDA_OK(cudaEventCreateWithFlags(&plan->ev_in, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&plan->ev_out, cudaEventDisableTiming));
+    }
+    CUDA_OK(cudaEventRecord(plan->ev_in, plan->stream));
+    CUDA_OK(cudaStreamWaitEvent(us, plan->ev_in, 0));
+    plan_run_steps(plan, us);
+    CUDA_OK(cudaEventRecord(plan->ev_out, us));
+    CUDA_OK(cudaStreamWaitEvent(plan->stream, plan->ev_out, 0));
   });
 }
 
@@ -1426,7 +1445,9 @@ int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t f
 int lfgpu_interpret(lfgpu_ctx* ctx, const lfgpu_graph* g, int32_t nsched,
                     const lfgpu_sched* sched, int32_t flags, double* const* host_bufs) {
   lfgpu_plan* P = nullptr;
-  int rc = lfgpu_plan_build(ctx, g, nsched, sched, flags | LFGPU_PLAN_KEEP_ALL, &P);
+  // Reference semantics unless the caller opts into tensor cores.
+  if (!(flags & (LFGPU_PLAN_TENSOR_CORES | LFGPU_PLAN_REQUIRE_TC))) flags |= LFGPU_PLAN_EXACT;
+  int rc = lfgpu_plan_build(ctx, g, nsched, sched, (flags & ~LFGPU_PLAN_TENSOR_CORES) | LFGPU_PLAN_KEEP_ALL, &P);
   if (rc != LFGPU_OK) return rc;
   rc = guarded([&] {
     for (int i = 0; i < g->ntensors; ++i) {

@@ -1,0 +1,126 @@
+"""End-to-end graphs of BASELINE.json cfg4 / cfg5 on the GPU backend.
+
+cfg4: ResNet-18 inference through one whole-graph plan (tuned per-conv
+template layouts from workloads.tune_resnet18, fused epilogues, CUDA graph).
+cfg5: the BERT-base encoder GEMM chain (seq 128, 12 layers) on GMM brick
+layouts shared by every activation, so each GMM's output is the next GMM's
+A operand with no conversion and the residual EwAdd fuses into the epilogue.
+
+Also the float64 torch model of a graph (`reference`): exact, or emulating
+the plan's numerics (bf16 operands on tensor-core contractions, fp32
+storage) — test and report infrastructure for chained graphs, where bf16
+operand rounding makes bit-exactness against reference_eval impossible.
+"""
+import math
+
+import torch
+import torch.nn.functional as F
+
+from . import _abi, ir, runtime, workloads
+
+
+def k64(shape, gen, scale=1.0):
+    return torch.randint(-64, 65, shape, generator=gen, device="cuda").float() / 64 * scale
+
+
+def make_inputs(g, gen):  # ResNet-18 (also used by BERT's weight scaling rule)
+    """k/64 values; conv / FC weights scaled by a power of two ~ 1/sqrt(fan_in)
+    so activations stay O(1) and every weight stays exact in bf16."""
+    out = {}
+    for t in g.tensors:
+        if t.role not in (ir.INPUT, ir.CONSTANT):
+            continue
+        shape = t.extents
+        if t.id.endswith("_w"):
+            fan_in = math.prod(shape[1:]) if len(shape) == 4 else shape[0]
+            out[t.id] = k64(shape, gen, 2.0 ** -round(math.log2(math.sqrt(fan_in))))
+        elif t.id.endswith("_b"):
+            out[t.id] = k64(shape, gen, 1.0 / 8)
+        else:
+            out[t.id] = k64(shape, gen)
+    return out
+
+
+def reference(g, ins, tc_nodes=frozenset(), emulate=False):
+    """Float64 forward of the graph; with emulate, tensor-core contraction
+    operands are rounded to bf16 and node outputs to fp32."""
+    v = {k: x.double() for k, x in ins.items()}
+
+    def rb(x):
+        return x.bfloat16().double() if emulate else x
+
+    def rf(x):
+        return x.float().double() if emulate else x
+
+    for i, nd in enumerate(g.nodes):
+        a = [v[t] for t in nd.inputs]
+        if nd.kind == ir.PADDING:
+            p = nd.attr("pad", 0)
+            r = F.pad(a[0], (p, p, p, p))
+        elif nd.kind == ir.LAYOUT_CONVERT:
+            r = a[0]
+        elif nd.kind == ir.C2D:
+            tc = i in tc_nodes
+            r = rf(F.conv2d(rb(a[0]) if tc else a[0], rb(a[1]) if tc else a[1],
+                            stride=nd.attr("stride", 1)))
+        elif nd.kind == ir.GMM:
+            tc = i in tc_nodes
+            r = rf((rb(a[0]) if tc else a[0]) @ (rb(a[1]) if tc else a[1]))
+        elif nd.kind == ir.BIASADD:
+            r = rf(a[0] + (a[1].view(1, -1, 1, 1) if a[0].dim() == 4 else a[1].view(1, -1)))
+        elif nd.kind == ir.EWADD:
+            r = rf(a[0] + a[1])
+        elif nd.kind == ir.RELU:
+            r = a[0].clamp_min(0)
+        elif nd.kind == ir.MAXPOOL:
+            r = F.max_pool2d(a[0], nd.attr("window", 1), nd.attr("stride", 1))
+        elif nd.kind == ir.GLOBAL_AVGPOOL:
+            r = rf(a[0].mean(dim=(2, 3)))
+        else:
+            raise ValueError(nd.kind)
+        v[nd.output] = r
+    return v
+
+
+def max_rel(a, b):
+    s = torch.maximum(torch.ones_like(a), torch.maximum(a.abs(), b.abs()))
+    return float(((a - b).abs() / s).max())
+
+
+def build_resnet18(n, factors, ctx=None):
+    g, convs = workloads.resnet18(n)
+    seqs = workloads.resnet18_seqs(g, convs, factors)
+    scheds = [runtime.sched(c["node"], fuse=1) for c in convs]
+    gi = len(g.nodes) - 2  # the FC GMM
+    scheds.append(runtime.sched(gi, fuse=1))
+    plan = runtime.Plan(g, seqs, scheds, _abi.PLAN_CUDA_GRAPH, ctx=ctx)
+    return g, convs, plan
+
+
+
+
+def make_bert_inputs(g, gen):
+    out = {}
+    for t in g.tensors:
+        if t.role not in (ir.INPUT, ir.CONSTANT):
+            continue
+        if t.id.endswith("_w"):
+            out[t.id] = k64(t.extents, gen, 2.0 ** -round(math.log2(math.sqrt(t.extents[0]))))
+        elif t.id.endswith("_b"):
+            out[t.id] = k64(t.extents, gen, 1.0 / 8)
+        else:
+            out[t.id] = k64(t.extents, gen)
+    return out
+
+
+def build_bert(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH):
+    g, gmms = workloads.bert_chain(layers)
+    seqs, scheds = {}, []
+    for ni in gmms:
+        nd = g.nodes[ni]
+        K = g.tensor(nd.inputs[0]).extents[1]
+        N = g.tensor(nd.output).extents[1]
+        seqs.update(runtime.decode_layout(g, ni, [128, min(t, K), min(t, N)]))
+        scheds.append(runtime.sched(ni, tile_last=min(t, N), order=order, fuse=1))
+    seqs = workloads.propagate_elementwise(g, seqs)
+    return g, gmms, runtime.Plan(g, seqs, scheds, flags, ctx=ctx)

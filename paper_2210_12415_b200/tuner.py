@@ -79,35 +79,114 @@ def best(results):
     return min(ok, key=lambda r: r.cost_us) if ok else None
 
 
-def sweep_distributed(graph: Graph, cands, inputs=None, measure_fn=None, **kw):
+class DeviceFault(RuntimeError):
+    """A measurement failed for a reason other than candidate legality
+    (CUDA fault, lost device): the rank stops measuring and its remaining
+    candidates are re-queued on the healthy ranks."""
+
+
+def _safe_measure(fn, graph, cand, inputs, kw):
+    """(cost_us, error, fault) for one candidate; never raises, so every rank
+    reaches the collective even when its device fails (a raise between
+    collectives would leave the other ranks blocked in all_gather)."""
+    try:
+        r = fn(graph, cand, inputs, **kw)
+        return r.cost_us, r.error, False
+    except Exception as e:  # noqa: BLE001 - turned into a fault record
+        return None, f"{type(e).__name__}: {e}", True
+
+
+def sweep_distributed(graph: Graph, cands, inputs=None, measure_fn=None, max_rounds=4, **kw):
     """One process per GPU: each rank measures candidates i with
     i % world == rank (no collective on the data path), then the (index,
     cost) pairs are all-gathered and committed in candidate-index order, so
     the winner is the reference's: strictly lowest cost, first index on ties
-    (tuner.cpp:180-189). Returns (results in index order, best index,
-    local seconds, local count)."""
+    (tuner.cpp:180-189).
+
+    Fault handling: a rank whose measurement raises anything
+    but a legality rejection marks itself failed, stops measuring, and its
+    unmeasured candidates are dealt again, round-robin, over the ranks still
+    healthy (up to `max_rounds` rounds). Every rank joins every gather, so a
+    failing device never blocks the others. Returns (results in index
+    order, best index, local seconds, local count); raises DeviceFault when
+    no healthy rank is left with candidates pending."""
     import torch.distributed as dist
     rank, world = (dist.get_rank(), dist.get_world_size()) if dist.is_initialized() else (0, 1)
     fn = measure_fn or measure
     t0 = time.perf_counter()
-    local = [(i, fn(graph, c, inputs, **kw)) for i, c in enumerate(cands) if i % world == rank]
+    done = {}                      # index -> (cost, error)
+    healthy = list(range(world))
+    pending = list(range(len(cands)))
+    me_ok = True
+    nloc = 0
+    faults = []
+    for _ in range(max_rounds):
+        if not pending:
+            break
+        if not healthy:
+            raise DeviceFault("every rank failed; unmeasured candidates: %d (%s)" % (
+                len(pending), "; ".join(faults)[:300]))
+        mine = []
+        if me_ok and rank in healthy:
+            slot = healthy.index(rank)
+            for k, i in enumerate(pending):
+                if k % len(healthy) != slot:
+                    continue
+                if not me_ok:  # device failed earlier in this round: leave the rest
+                    break
+                cost, err, fault = _safe_measure(fn, graph, cands[i], inputs, kw)
+                nloc += 1
+                if fault:
+                    me_ok = False
+                    mine.append((i, None, err, True))
+                else:
+                    mine.append((i, cost, err, False))
+        if world > 1:
+            gathered = [None] * world
+            dist.all_gather_object(gathered, (rank, me_ok, mine))
+        else:
+            gathered = [(rank, me_ok, mine)]
+        for r, ok, part in gathered:
+            if not ok and r in healthy:
+                healthy.remove(r)
+            for i, cost, err, fault in part:
+                if fault:
+                    faults.append(f"rank {r}: {err}")
+                else:
+                    done[i] = (cost, err)
+        pending = [i for i in range(len(cands)) if i not in done]
+    if pending:
+        raise DeviceFault("candidates left unmeasured after %d rounds: %d (%s)" % (
+            max_rounds, len(pending), "; ".join(faults)[:300]))
     secs = time.perf_counter() - t0
-    mine = [(i, r.cost_us, r.error) for i, r in local]
-    if world > 1:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, mine)
-    else:
-        gathered = [mine]
-    merged = {}
-    for part in gathered:
-        for i, cost, err in part:
-            merged[i] = Result(cands[i], cost, err)
-    results = [merged[i] for i in range(len(cands))]
+    results = [Result(cands[i], done[i][0], done[i][1]) for i in range(len(cands))]
     best_i, best_c = -1, float("inf")
     for i, r in enumerate(results):
         if r.cost_us is not None and r.cost_us < best_c:
             best_i, best_c = i, r.cost_us
-    return results, best_i, secs, len(local)
+    return results, best_i, secs, nloc
+
+
+def measure_top(graph: Graph, cands, predicted=None, top_k=8, inputs=None, **kw):
+    """The reference's measure_top (tuner.cpp:243-274) with the top-k
+    measurements of one call dispatched across the GPUs of the job.
+
+    Candidates are ranked by `predicted` cost (the surrogate's prediction,
+    stable sort, tuner.cpp:250-258) when given, else kept in index order; the
+    first `top_k` are measured, one GPU each (sweep_distributed), and the
+    results are committed in rank order with the strict-< best rule, so the
+    bookkeeping is identical to the serial loop. Returns (measured indices,
+    their results, best index or -1)."""
+    idx = list(range(len(cands)))
+    if predicted is not None:
+        idx.sort(key=lambda i: predicted[i])  # list.sort is stable
+    idx = idx[:top_k]
+    res, _, _, _ = sweep_distributed(graph, [cands[i] for i in idx], inputs, **kw)
+    best_i, best_c = -1, float("inf")
+    for k, r in zip(idx, res):
+        if r.cost_us is not None and r.cost_us < best_c:
+            best_i, best_c = k, r.cost_us
+    return idx, res, best_i
 
 
 # --- candidate streams -------------------------------------------------------

@@ -22,8 +22,7 @@ pytestmark = pytest.mark.gpu
     (1, 768, 3072, 2304, 128, 0),  # one full-size BERT-base layer
 ])
 def test_bert_chain_fused(layers, hid, ffn, qkv, t, order):
-    import bert_run as B
-    import resnet18_run as R
+    from paper_2210_12415_b200 import e2e as R
     from paper_2210_12415_b200 import _abi, runtime, workloads
     g, gmms = workloads.bert_chain(layers, 128, hid, ffn, qkv)
     seqs, scheds = {}, []
@@ -40,7 +39,7 @@ def test_bert_chain_fused(layers, hid, ffn, qkv, t, order):
     assert all(k in ("fused", "bf16_shadow") or k.startswith("umma") for k in kinds), kinds
     gen = torch.Generator(device="cuda")
     gen.manual_seed(7)
-    ins = B.make_inputs(g, gen)
+    ins = R.make_bert_inputs(g, gen)
     for k, x in ins.items():
         plan.set_input_device(k, x)
     plan.run()

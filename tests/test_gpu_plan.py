@@ -59,8 +59,10 @@ MICRO = [
 ]
 
 
-@pytest.mark.parametrize("flags", [_abi.PLAN_EXACT, _abi.PLAN_DEFAULT])
+@pytest.mark.parametrize("flags", [_abi.PLAN_EXACT, _abi.PLAN_DEFAULT, _abi.PLAN_TENSOR_CORES])
 def test_interpret_micrographs_identity(flags):
+    # PLAN_DEFAULT in lfgpu_interpret means reference semantics (EXACT);
+    # PLAN_TENSOR_CORES opts into the tcgen05 paths where they are legal.
     for mk in MICRO:
         g = mk()
         inputs, ref = oracle_outputs(g, 17)
@@ -118,7 +120,7 @@ def test_umma_gemm_bitexact(factors):
 
 def test_umma_gemm_cfg2_1024():
     g, seqs, inputs, ref = gemm_case(1024, 1024, 1024, (128, 64, 128))
-    got = runtime.interpret(g, seqs, [runtime.sched(0, tile_last=64)], inputs)
+    got = runtime.interpret(g, seqs, [runtime.sched(0, tile_last=64)], inputs, flags=_abi.PLAN_TENSOR_CORES)
     assert np.array_equal(got["c"], ref["c"])
 
 
@@ -356,10 +358,9 @@ def test_dep_direct(shape, f, fuse):
     g = ir.dep_chain(n, c, h, k, s, k // 2)
     seqs = {}
     if f is not None:
-        try:
-            seqs = runtime.decode_layout(g, 1, list(f))
-        except runtime.LfError:
-            pytest.skip("template point not legal for this shape")
+        # Every parametrized point is a legal template point: a decode
+        # failure is a regression, not a skip.
+        seqs = runtime.decode_layout(g, 1, list(f))
         seqs["y"] = seqs["conv"]
     inputs, ref = oracle_outputs(g, 13)
     p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=fuse)])
@@ -418,3 +419,62 @@ def test_dep_direct_fused_bias_residual(brick):
         p.set_input(tid, v)
     p.run()
     assert np.array_equal(p.get_output("y"), ref["y"])
+
+
+@pytest.mark.parametrize("knobs", [{}, {"LFGPU_NO_EPI_ALIAS": "1"}, {"LFGPU_DUAL_MMA": "1"},
+                                   {"LFGPU_DUAL_MMA": "0"}, {"LFGPU_NO_EPI_ALIAS": "1", "LFGPU_DUAL_MMA": "1"}])
+@pytest.mark.parametrize("case", ["conv", "gemm"])
+def test_umma_epilogue_alias_and_dual_issuer_parity(case, knobs, monkeypatch):
+    """The 1-CTA kernel's epilogue-in-ring aliasing (default when each CTA
+    gets at most one unit) and the two-MMA-issuer path give bit-identical
+    results to the plain variants."""
+    monkeypatch.setenv("LFGPU_NO_PAIR", "1")
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    if case == "conv":
+        g = ir.pad_conv(2, 64, 64, 56, 3, 1, 1)
+        seqs = runtime.decode_layout(g, 1, [28, 28, 64, 32, 32, 64])
+        node = 1
+    else:
+        g = ir.gemm(512, 512, 1024)
+        seqs = runtime.decode_layout(g, 0, [128, 64, 128])
+        node = 0
+    inputs, ref = oracle_outputs(g, 31)
+    p = runtime.Plan(g, seqs, [runtime.sched(node, tile_last=64 if case == "gemm" else 1)],
+                     flags=_abi.PLAN_REQUIRE_TC)
+    k = p.node_kernel(node)
+    if knobs.get("LFGPU_DUAL_MMA") == "1":
+        assert " dual" in k, k
+    if knobs.get("LFGPU_NO_EPI_ALIAS") == "1":
+        assert "epi-in-ring" not in k, k
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    out = g.nodes[-1].output
+    assert np.array_equal(p.get_output(out), ref[out])
+
+
+def test_run_on_user_stream_joins_async_set_input():
+    """set_input_device(wait=False) enqueues the K1 conversion on the plan's
+    stream; run(stream=user) must wait for it and get_output must wait for
+    the run (both races)."""
+    torch = pytest.importorskip("torch")
+    g = ir.gemm(512, 512, 512)
+    seqs = runtime.decode_layout(g, 0, [256, 64, 256])
+    inputs, ref = oracle_outputs(g, 41)
+    p = runtime.Plan(g, seqs, [], flags=_abi.PLAN_REQUIRE_TC)
+    user = torch.cuda.Stream()
+    ps = torch.cuda.ExternalStream(p.stream)
+    for rep in range(3):
+        # inputs scaled by (rep + 1): stale operands would give the previous
+        # rep's product (k/64 values doubled / tripled stay exact)
+        a = torch.tensor(inputs["a"] * (rep + 1), dtype=torch.float32, device="cuda").view(512, 512)
+        b = torch.tensor(inputs["b"], dtype=torch.float32, device="cuda").view(512, 512)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(ps):
+            torch.cuda._sleep(1_000_000)  # delay the async conversions on the plan's stream
+        p.set_input_device("a", a, wait=False)
+        p.set_input_device("b", b, wait=False)
+        p.run(stream=user.cuda_stream)
+        got = p.get_output("c")
+        assert np.array_equal(got, ref["c"] * (rep + 1)), rep

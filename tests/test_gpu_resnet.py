@@ -21,9 +21,7 @@ import oracle_lib as O
 from paper_2210_12415_b200 import _abi, ir, runtime, workloads
 from paper_2210_12415_b200.layout import reorder, split
 
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                "tools"))
-import resnet18_run as R  # noqa: E402
+from paper_2210_12415_b200 import e2e as R  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -173,7 +171,7 @@ FIXED_FACTORS_B1 = {
 def test_resnet18_b1_logits():
     gen = torch.Generator(device="cuda")
     gen.manual_seed(42)
-    g, convs, plan = R.build(1, FIXED_FACTORS_B1)
+    g, convs, plan = R.build_resnet18(1, FIXED_FACTORS_B1)
     kinds = [plan.node_kernel(i) for i in range(len(g.nodes))]
     tc = frozenset(i for i, k in enumerate(kinds) if k.startswith("umma"))
     assert len(tc) >= 17, kinds                # every conv but the stem on tcgen05

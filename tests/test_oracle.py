@@ -202,3 +202,23 @@ class TestAgainstReference:
         rc, phys = O.padding_nest([1, 2, 5, 5], 1, [], seqs["xp"], x)
         assert rc == 0
         assert np.array_equal(O.to_logical([1, 2, 7, 7], seqs["xp"], phys), bufs[1])
+
+
+def test_oracle_matches_reference_planner_graphs(golden):
+    # LayoutConvert graphs from the reference planner (oracle/gen_golden.py
+    # plan_context): the oracle's reference_eval reproduces the reference
+    # interpret's logical outputs (a LayoutConvert is the identity on
+    # logical values, interp.cpp:166-169).
+    from test_gpu_parity import _graph_from
+    n = 0
+    for c in golden["plan_context"]:
+        if c["throws"]:
+            assert "signal" in c["reference_outcome"] or "out-of-range" in c["reference_outcome"]
+            continue
+        g = _graph_from(c["graph"])
+        bufs = O.random_inputs(g, c["seed"])
+        O.reference_eval(g, bufs)
+        for tid, st in c["outputs"].items():
+            assert O.fnv1a(bufs[g.tensor_index(tid)]) == st["fnv"], (c["name"], tid)
+            n += 1
+    assert n >= 10

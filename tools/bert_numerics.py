@@ -5,8 +5,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tools"))
 import torch
 from paper_2210_12415_b200 import _abi
-import bert_run as B
-from resnet18_run import max_rel, reference
+from paper_2210_12415_b200.e2e import build_bert as _bb, make_bert_inputs as _mb  # noqa: E402
+class B:  # noqa: E302
+    build = staticmethod(_bb)
+    make_inputs = staticmethod(_mb)
+from paper_2210_12415_b200.e2e import max_rel, reference  # noqa: E402
 layers = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 for order in (0, 1):
     g, gmms, plan = B.build(layers, 64, order, flags=_abi.PLAN_DEFAULT)

@@ -1,58 +1,15 @@
-"""cfg5: the BERT-base encoder GEMM chain (seq 128, 12 layers) through one
-whole-graph plan on tuned GMM brick layouts.
-
-All activations share one brick layout [M/128][N/t][128][t] so each GMM's
-output is the next GMM's A operand with no conversion and the residual EwAdd
-reads the same layout inside the fused epilogue; weights use the GMM
-template's B bricks. Checks the output against float64 torch references
-(exact, and emulating the plan's numerics: bf16 operands, fp32 storage),
-then times the plan (CUDA graph, L2 flushed per step).
-  python tools/bert_run.py [--layers 12] [--t 64]
-"""
+"""cfg5 CLI: sweep brick widths, build, check and time the BERT-base GEMM
+chain (paper_2210_12415_b200.e2e).  python tools/bert_run.py [--layers 12] [--t 64]"""
 import argparse
-import math
 import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tools"))
 import torch  # noqa: E402
 
-from paper_2210_12415_b200 import _abi, ir, runtime, workloads  # noqa: E402
-from resnet18_run import max_rel, reference  # noqa: E402
-
-
-def k64(shape, gen, scale=1.0):
-    return torch.randint(-64, 65, shape, generator=gen, device="cuda").float() / 64 * scale
-
-
-def make_inputs(g, gen):
-    out = {}
-    for t in g.tensors:
-        if t.role not in (ir.INPUT, ir.CONSTANT):
-            continue
-        if t.id.endswith("_w"):
-            out[t.id] = k64(t.extents, gen, 2.0 ** -round(math.log2(math.sqrt(t.extents[0]))))
-        elif t.id.endswith("_b"):
-            out[t.id] = k64(t.extents, gen, 1.0 / 8)
-        else:
-            out[t.id] = k64(t.extents, gen)
-    return out
-
-
-def build(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH):
-    g, gmms = workloads.bert_chain(layers)
-    seqs, scheds = {}, []
-    for ni in gmms:
-        nd = g.nodes[ni]
-        K = g.tensor(nd.inputs[0]).extents[1]
-        N = g.tensor(nd.output).extents[1]
-        seqs.update(runtime.decode_layout(g, ni, [128, min(t, K), min(t, N)]))
-        scheds.append(runtime.sched(ni, tile_last=min(t, N), order=order, fuse=1))
-    seqs = workloads.propagate_elementwise(g, seqs)
-    return g, gmms, runtime.Plan(g, seqs, scheds, flags, ctx=ctx)
-
+from paper_2210_12415_b200 import runtime, workloads  # noqa: E402
+from paper_2210_12415_b200.e2e import build_bert as build, make_bert_inputs as make_inputs, max_rel, reference  # noqa: E402
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()

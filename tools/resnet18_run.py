@@ -1,13 +1,6 @@
-"""cfg4: ResNet-18 inference through one whole-graph plan.
-
-Tunes per-conv layouts (workloads.tune_resnet18), builds the plan (fused
-epilogues, CUDA graph), checks the logits against float64 torch references
-(exact, and emulating the plan's numerics: bf16 operands on tensor-core
-convs, fp32 storage), and times the plan.
-  python tools/resnet18_run.py [--batch 1] [--no-tune]
-"""
+"""cfg4 CLI: tune, build, check and time ResNet-18 inference
+(paper_2210_12415_b200.e2e).  python tools/resnet18_run.py [--batch 1] [--no-tune]"""
 import argparse
-import math
 import os
 import sys
 import time
@@ -15,88 +8,9 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
-import torch.nn.functional as F  # noqa: E402
 
-from paper_2210_12415_b200 import _abi, ir, runtime, workloads  # noqa: E402
-
-
-def k64(shape, gen, scale=1.0):
-    return torch.randint(-64, 65, shape, generator=gen, device="cuda").float() / 64 * scale
-
-
-def make_inputs(g, gen):
-    """k/64 values; conv / FC weights scaled by a power of two ~ 1/sqrt(fan_in)
-    so activations stay O(1) and every weight stays exact in bf16."""
-    out = {}
-    for t in g.tensors:
-        if t.role not in (ir.INPUT, ir.CONSTANT):
-            continue
-        shape = t.extents
-        if t.id.endswith("_w"):
-            fan_in = math.prod(shape[1:]) if len(shape) == 4 else shape[0]
-            out[t.id] = k64(shape, gen, 2.0 ** -round(math.log2(math.sqrt(fan_in))))
-        elif t.id.endswith("_b"):
-            out[t.id] = k64(shape, gen, 1.0 / 8)
-        else:
-            out[t.id] = k64(shape, gen)
-    return out
-
-
-def reference(g, ins, tc_nodes=frozenset(), emulate=False):
-    """Float64 forward of the graph; with emulate, tensor-core contraction
-    operands are rounded to bf16 and node outputs to fp32."""
-    v = {k: x.double() for k, x in ins.items()}
-
-    def rb(x):
-        return x.bfloat16().double() if emulate else x
-
-    def rf(x):
-        return x.float().double() if emulate else x
-
-    for i, nd in enumerate(g.nodes):
-        a = [v[t] for t in nd.inputs]
-        if nd.kind == ir.PADDING:
-            p = nd.attr("pad", 0)
-            r = F.pad(a[0], (p, p, p, p))
-        elif nd.kind == ir.LAYOUT_CONVERT:
-            r = a[0]
-        elif nd.kind == ir.C2D:
-            tc = i in tc_nodes
-            r = rf(F.conv2d(rb(a[0]) if tc else a[0], rb(a[1]) if tc else a[1],
-                            stride=nd.attr("stride", 1)))
-        elif nd.kind == ir.GMM:
-            tc = i in tc_nodes
-            r = rf((rb(a[0]) if tc else a[0]) @ (rb(a[1]) if tc else a[1]))
-        elif nd.kind == ir.BIASADD:
-            r = rf(a[0] + (a[1].view(1, -1, 1, 1) if a[0].dim() == 4 else a[1].view(1, -1)))
-        elif nd.kind == ir.EWADD:
-            r = rf(a[0] + a[1])
-        elif nd.kind == ir.RELU:
-            r = a[0].clamp_min(0)
-        elif nd.kind == ir.MAXPOOL:
-            r = F.max_pool2d(a[0], nd.attr("window", 1), nd.attr("stride", 1))
-        elif nd.kind == ir.GLOBAL_AVGPOOL:
-            r = rf(a[0].mean(dim=(2, 3)))
-        else:
-            raise ValueError(nd.kind)
-        v[nd.output] = r
-    return v
-
-
-def max_rel(a, b):
-    s = torch.maximum(torch.ones_like(a), torch.maximum(a.abs(), b.abs()))
-    return float(((a - b).abs() / s).max())
-
-
-def build(n, factors, ctx=None):
-    g, convs = workloads.resnet18(n)
-    seqs = workloads.resnet18_seqs(g, convs, factors)
-    scheds = [runtime.sched(c["node"], fuse=1) for c in convs]
-    gi = len(g.nodes) - 2  # the FC GMM
-    scheds.append(runtime.sched(gi, fuse=1))
-    plan = runtime.Plan(g, seqs, scheds, _abi.PLAN_CUDA_GRAPH, ctx=ctx)
-    return g, convs, plan
-
+from paper_2210_12415_b200 import workloads  # noqa: E402
+from paper_2210_12415_b200.e2e import build_resnet18 as build, make_inputs, max_rel, reference  # noqa: E402
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
