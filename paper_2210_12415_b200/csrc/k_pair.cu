@@ -45,7 +45,7 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 448;  // 12 role warps + 2 extra producer warps
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant, alternating 32-column chunks
 constexpr int kLd = 36;       // transpose buffer row stride (floats)
@@ -74,6 +74,9 @@ struct PairParams {
   unsigned long long* dbg;
   int32_t dbg_split;  // diagnostics: >= 0 keeps only that split's partial in the reduction
   int32_t diag;       // diagnostics (LFGPU_PAIR_DIAG, timing only): bit0 skips the epilogue's global stores
+  int32_t nprod;      // TMA producer warps (1..5)
+  int32_t xmode;      // split-K exchange: 0 L2 workspace, 1 DSMEM push (one tile per cluster)
+  int32_t rx_bytes;   // DSMEM receive buffer bytes ((S-1) x 128 x BN/S fp32)
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -113,9 +116,10 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: 
 // store instruction writes four 128-byte row segments; every table lives in
 // SMEM (an L2 round trip per chunk would pace the epilogue), residual loads
 // are all issued before they are consumed.
+template <bool UNIT>
 __device__ __forceinline__ void store_chunk(const PairParams& P, const Smem& T, const float* v, float* wbuf,
                                             int q, int lane, int c0, int64_t obase, const float* bias) {
-  if (P.col_unit) {
+  if constexpr (UNIT) {
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -178,27 +182,31 @@ __device__ __forceinline__ void store_chunk(const PairParams& P, const Smem& T, 
         *reinterpret_cast<uint2*>(P.out_bf16 + addr[it]) = pk;
       }
     }
-    return;
-  }
-  // Generic layouts: thread = row, one element at a time (column offsets
-  // from the global table, L1-resident after the first tile).
-  const int64_t rb = obase + T.row[q * 32 + lane];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int64_t addr = rb + __ldg(P.col_off + c0 + j);
-    float y = v[j];
+  } else {
+    // Generic layouts: thread = row, one element at a time (column offsets
+    // from the global table, L1-resident after the first tile).
+    const int64_t rb = obase + T.row[q * 32 + lane];
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const int64_t addr = rb + __ldg(P.col_off + c0 + j);
+      float y = v[j];
 #pragma unroll 1
-    for (int e = 0; e < P.epi_count; ++e) {
-      const int k = P.epi_kind[e];
-      if (k == EPI_RELU) y = fmaxf(y, 0.f);
-      else if (k == EPI_BIAS) y += bias[c0 + j];
-      else y += __ldg(P.epi_ptr[e] + addr);
+      for (int e = 0; e < P.epi_count; ++e) {
+        const int k = P.epi_kind[e];
+        if (k == EPI_RELU) y = fmaxf(y, 0.f);
+        else if (k == EPI_BIAS) y += bias[c0 + j];
+        else y += __ldg(P.epi_ptr[e] + addr);
+      }
+      P.out[addr] = y;
+      if (P.out_bf16) P.out_bf16[addr] = __float2bfloat16_rn(y);
     }
-    P.out[addr] = y;
-    if (P.out_bf16) P.out_bf16[addr] = __float2bfloat16_rn(y);
   }
 }
 
+// SPLIT: K splits reduce through the L2 workspace (S > 1); UNIT: row-segment
+// stores (contiguous 32-column output chunks). One instance per combination
+// keeps each kernel's code within the SM's instruction cache.
+template <bool SPLIT, bool UNIT>
 __global__ void __launch_bounds__(kThreads, 1)
     pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                 const __grid_constant__ PairParams P) {
@@ -206,7 +214,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + kEpiBytes);
+  float* s_rx = reinterpret_cast<float*>(smem + P.ring_bytes + kEpiBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + kEpiBytes + P.rx_bytes);
   const int pipe = P.pipe;
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = full0 + 8 * pipe;
@@ -226,6 +235,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   T.bias = reinterpret_cast<float*>(blob + P.lay.total);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    // Touch every 32-byte sector of the parameter block once, in parallel:
+    // a role warp's first read of a cold constant line after the PDL wait
+    // costs a serial L2 round trip each (~1 us before the first TMA issue).
+    const uint32_t np32 = static_cast<uint32_t>(sizeof(PairParams) / 32);
+    if (threadIdx.x < np32) {
+      const uint32_t x = reinterpret_cast<const uint32_t*>(&P)[threadIdx.x * 8];
+      asm volatile("" ::"r"(x));
+    }
+  }
   const uint32_t crank = cluster_ctarank();
   const int pr = static_cast<int>(crank & 1u);     // rank inside the pair
   const int split = static_cast<int>(crank >> 1);  // pair index = K split
@@ -242,8 +261,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull0 + 8 * b, 1);
       mbar_init(tempty0 + 8 * b, 2 * kEpiWarps);  // both CTAs' epilogue warps
-      mbar_init(red0 + 8 * b, S * kEpiWarps);     // epilogue warps of the S CTAs holding these rows
+      mbar_init(red0 + 8 * b, P.xmode ? 1 : (S - 1) * kEpiWarps);  // sibling splits' epilogue warps / rx bytes
     }
+    // DSMEM exchange: the receive buffer's expected bytes, armed before the
+    // cluster barrier so no sibling's push can precede it.
+    if (P.xmode) mbar_expect_tx(red0, static_cast<uint32_t>(P.rx_bytes));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
@@ -262,12 +284,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (; i0 < n4; i0 += kThreads) dst[i0] = __ldg(P.blob + i0);
   }
+  if (P.dbg && threadIdx.x == 0) P.dbg[512 * blockIdx.x + 324] = gtime();
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(P.tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    if (P.dbg && lane == 0) P.dbg[512 * blockIdx.x + 325] = gtime();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync();
@@ -281,47 +305,62 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int s_lo = split * P.KS / S, s_hi = (split + 1) * P.KS / S;
   const uint32_t ring0 = smem_u32(smem);
 
-  if (warp == 0 || warp == 3) {
-    // ---- TMA producers (both CTAs of the pair): warp 0 loads the A boxes
-    // (and, in the pair leader, arms the stage's expected bytes), warp 3 the
-    // B boxes. One issuing thread cannot keep a stage's boxes in flight fast
-    // enough (each UTMALDG costs hundreds of cycles to issue). Coordinates
-    // never come from global memory inside the stage loop: the tile part is
-    // loaded into registers once per tile, the stage part lives in SMEM.
-    const bool is_a = warp == 0;
+  const int np = P.nprod;
+  const int prod = warp == 0 ? 0 : warp == 3 ? 1 : warp == 2 ? 2 : warp >= kEpiWarp0 + kEpiWarps ? 3 + warp - (kEpiWarp0 + kEpiWarps) : -1;
+  if (prod >= 0 && prod < np) {
+    // ---- TMA producers (both CTAs of the pair). One issuing warp keeps
+    // about one request in flight (tools/micro/tma_ingest.cu: ~800 cycles
+    // per request per warp, independent of its size, while the SM takes
+    // 80-100 B/clk from several warps), so the stages are dealt round-robin
+    // to `np` producer warps; each issues the A and B boxes of its stages
+    // (in the pair leader it also arms the stage's expected bytes for both
+    // CTAs). Coordinates never come from global memory inside the loop: the
+    // tile part is loaded into registers once per tile, the stage part
+    // lives in SMEM.
     if (elect_one()) {
+      if (P.dbg && prod == 0) P.dbg[512 * blockIdx.x + 326] = gtime();
       const uint32_t lead_full0 = mapa(full0, lead);
       const uint32_t b_off = P.a_boxes * P.a_slot;
-      const int nbox = is_a ? P.a_boxes : P.b_boxes;
-      const int sl = is_a ? P.a_slot : P.b_slot;
-      const CUtensorMap* map = is_a ? &tma_a : &tma_b;
-      const int so = is_a ? 0 : 5;
       int g = 0;
       for (int t = cid; t < P.ntiles; t += ncl) {
         int Mi, Nj;
         tile_coords(P, t, &Mi, &Nj);
-        int32_t tc[kMaxBoxes][5];
-        const int32_t* cp = is_a ? T.acrd + (2 * Mi + pr) * P.a_boxes * 5 : T.bcrd + (2 * Nj + pr) * P.b_boxes * 5;
+        int32_t ta[kMaxBoxes][5], tb[kMaxBoxes][5];
+        const int32_t* ca = T.acrd + (2 * Mi + pr) * P.a_boxes * 5;
+        const int32_t* cb = T.bcrd + (2 * Nj + pr) * P.b_boxes * 5;
 #pragma unroll
         for (int b = 0; b < kMaxBoxes; ++b)
 #pragma unroll
-          for (int d = 0; d < 5; ++d) tc[b][d] = b < nbox ? cp[b * 5 + d] : 0;
+          for (int d = 0; d < 5; ++d) {
+            ta[b][d] = b < P.a_boxes ? ca[b * 5 + d] : 0;
+            tb[b][d] = b < P.b_boxes ? cb[b * 5 + d] : 0;
+          }
+        if (P.dbg && prod == 0 && g == 0) P.dbg[512 * blockIdx.x + 327] = gtime();
         for (int s = s_lo; s < s_hi; ++s, ++g) {
+          if (g % np != prod) continue;
           const int slot = g % pipe;
           const uint32_t ph = static_cast<uint32_t>(g / pipe) & 1u;
-          const int32_t* sc = T.stage + s * 10 + so;
+          const int32_t* sc = T.stage + s * 10;
           int32_t c[5];
+          if (P.dbg && g == 0) P.dbg[512 * blockIdx.x + 328] = gtime();
           mbar_wait(empty0 + 8 * slot, ph ^ 1u);
-          if (P.dbg && is_a && g < 64) P.dbg[512 * blockIdx.x + g] = gtime();
-          if (is_a && pr == 0) mbar_expect_tx(full0 + 8 * slot, 2 * P.tx_bytes);
+          if (P.dbg && g < 64) P.dbg[512 * blockIdx.x + g] = gtime();
+          if (pr == 0) mbar_expect_tx(full0 + 8 * slot, 2 * P.tx_bytes);
           const uint32_t bar = lead_full0 + 8 * slot;
-          const uint32_t dst = ring0 + slot * P.stage_bytes + (is_a ? 0 : b_off);
+          const uint32_t dst = ring0 + slot * P.stage_bytes;
 #pragma unroll
           for (int b = 0; b < kMaxBoxes; ++b)
-            if (b < nbox) {
+            if (b < P.a_boxes) {
 #pragma unroll
-              for (int d = 0; d < 5; ++d) c[d] = tc[b][d] + sc[d];
-              tma_load5_pair(map, dst + b * sl, bar, c);
+              for (int d = 0; d < 5; ++d) c[d] = ta[b][d] + sc[d];
+              tma_load5_pair(&tma_a, dst + b * P.a_slot, bar, c);
+            }
+#pragma unroll
+          for (int b = 0; b < kMaxBoxes; ++b)
+            if (b < P.b_boxes) {
+#pragma unroll
+              for (int d = 0; d < 5; ++d) c[d] = tb[b][d] + sc[5 + d];
+              tma_load5_pair(&tma_b, dst + b_off + b * P.b_slot, bar, c);
             }
         }
       }
@@ -356,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (issuer) umma2_commit_mc(tfull0 + 8 * acc, pair_mask);
       __syncwarp();
     }
-  } else if (warp >= kEpiWarp0) {
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     // ---- epilogue (both CTAs): warp w reads TMEM lanes 32*(w%4)..+31; the
     // two warps of a lane quadrant take alternate 32-column chunks
     const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
@@ -389,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (P.dbg && etid == 0 && i < 64) P.dbg[512 * blockIdx.x + 128 + i] = gtime();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * P.BN);
       float v[32];
-      if (S == 1) {
+      if constexpr (!SPLIT) {
         for (int c0 = 32 * half; c0 < P.BN; c0 += 64) {
           tmem_ld32(taddr + c0, v);
           if (P.dbg && etid == 0 && i == 0 && c0 < 32 * 32) P.dbg[512 * blockIdx.x + 256 + c0 / 16] = gtime();
@@ -398,47 +437,120 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_relaxed_cluster(lead_tempty0 + 8 * acc);
           }
-          store_chunk(P, T, v, wbuf, q, lane, c0, obase, bias);
+          store_chunk<UNIT>(P, T, v, wbuf, q, lane, c0, obase, bias);
           if (P.dbg && etid == 0 && i == 0 && c0 < 32 * 32) P.dbg[512 * blockIdx.x + 257 + c0 / 16] = gtime();
         }
         if (P.dbg && etid == 0 && i < 64) P.dbg[512 * blockIdx.x + 192 + i] = gtime();
-        continue;
-      }
-      // Split K: publish this split's partial rows ([col/4][row] float4).
+      } else {
+      const int W = P.BN / S;
+      if (P.xmode) {
+        // Split K over DSMEM (one tile per cluster): each 32x32 block of a
+        // sibling's column slice is staged in the idle operand ring as
+        // [col][row] and pushed into the sibling's receive buffer with one
+        // bulk copy that completes on the sibling's barrier; no global
+        // round trip, no fence. Receive layout: [sender][chunk][quadrant][32 col][32 row].
+        const int blk = 32 * 32 * 4;
+        uint8_t* stage_base = smem + (warp - kEpiWarp0) * (((P.BN / 64) * (S - 1) + S - 1) / S) * blk;
+        int nb = 0;
+        for (int c0 = 32 * half; c0 < P.BN; c0 += 64) {
+          const int p = c0 / W;
+          if (p == split) continue;
+          tmem_ld32(taddr + c0, v);
+          float* st = reinterpret_cast<float*>(stage_base + (nb++) * blk);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) st[j * 32 + lane] = v[j];
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int sidx = split < p ? split : split - 1;
+            const uint32_t off = static_cast<uint32_t>(((sidx * (W / 32) + (c0 - p * W) / 32) * 4 + q) * blk);
+            const uint32_t dst = mapa(smem_u32(s_rx) + off, 2 * p + pr);
+            const uint32_t rb = mapa(red0, 2 * p + pr);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                "r"(smem_u32(st)), "r"(blk), "r"(rb)
+                : "memory");
+          }
+        }
+        if (P.dbg && etid == 0 && i == 0) P.dbg[512 * blockIdx.x + 256] = gtime();
+        mbar_wait_cluster(red0, 0);
+        if (P.dbg && etid == 0 && i == 0) P.dbg[512 * blockIdx.x + 258] = gtime();
+        for (int c0 = split * W + 32 * half; c0 < (split + 1) * W; c0 += 64) {
+          float own[32];
+          tmem_ld32(taddr + c0, own);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          for (int p = 0; p < S; ++p) {  // split order: deterministic sums
+            if (p == split) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += own[j];
+              continue;
+            }
+            const int sidx = p < split ? p : p - 1;
+            const float* rx = s_rx + ((sidx * (W / 32) + (c0 - split * W) / 32) * 4 + q) * 1024;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += rx[j * 32 + lane];
+          }
+          store_chunk<UNIT>(P, T, v, wbuf, q, lane, c0, obase, bias);
+          if (P.dbg && etid == 0 && i == 0) P.dbg[512 * blockIdx.x + 259 + (c0 - split * W) / 64] = gtime();
+        }
+      } else {
+      // Split K through L2: publish the column slices the sibling splits
+      // reduce ([col/4][row] float4, coalesced); this split's own slice
+      // stays in TMEM until its reduction.
       const size_t tile_floats = static_cast<size_t>(128) * P.BN;
       float4* mine = reinterpret_cast<float4*>(P.ws + ((static_cast<size_t>(t) * S + split) * 2 + pr) * tile_floats);
       for (int c0 = 32 * half; c0 < P.BN; c0 += 64) {
+        if (c0 >= split * W && c0 < (split + 1) * W) continue;
         tmem_ld32(taddr + c0, v);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           __stcg(mine + (c0 / 4 + j) * 128 + row, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __threadfence();
+      if (P.dbg && etid == 0 && i == 0) P.dbg[512 * blockIdx.x + 256] = gtime();
+      // Release the partial at cluster scope (every reader is in this cluster).
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_relaxed_cluster(lead_tempty0 + 8 * acc);
-        for (int p = 0; p < S; ++p) mbar_arrive_cluster(mapa(red0 + 8 * acc, 2 * p + pr));
-      }
+      if (P.dbg && etid == 0 && i == 0) P.dbg[512 * blockIdx.x + 257] = gtime();
+      if (lane == 0)
+        for (int p = 0; p < S; ++p)
+          if (p != split) mbar_arrive_cluster(mapa(red0 + 8 * acc, 2 * p + pr));
       mbar_wait_cluster(red0 + 8 * acc, static_cast<uint32_t>(i >> 1) & 1u);
-      const int W = P.BN / S;
+      if (P.dbg && etid == 0 && i == 0) P.dbg[512 * blockIdx.x + 258] = gtime();
       for (int c0 = split * W + 32 * half; c0 < (split + 1) * W; c0 += 64) {
+        float own[32];
+        tmem_ld32(taddr + c0, own);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.f;
-        for (int p = 0; p < S; ++p) {
+        for (int p = 0; p < S; ++p) {  // split order: deterministic sums
           if (P.dbg_split >= 0 && p != P.dbg_split) continue;
+          if (p == split) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += own[j];
+            continue;
+          }
           const float4* src =
               reinterpret_cast<const float4*>(P.ws + ((static_cast<size_t>(t) * S + p) * 2 + pr) * tile_floats);
+          float4 x[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x[j] = __ldcg(src + (c0 / 4 + j) * 128 + row);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float4 x = __ldcg(src + (c0 / 4 + j) * 128 + row);
-            v[4 * j] += x.x;
-            v[4 * j + 1] += x.y;
-            v[4 * j + 2] += x.z;
-            v[4 * j + 3] += x.w;
+            v[4 * j] += x[j].x;
+            v[4 * j + 1] += x[j].y;
+            v[4 * j + 2] += x[j].z;
+            v[4 * j + 3] += x[j].w;
           }
         }
-        store_chunk(P, T, v, wbuf, q, lane, c0, obase, bias);
+        store_chunk<UNIT>(P, T, v, wbuf, q, lane, c0, obase, bias);
+        if (P.dbg && etid == 0 && i == 0) P.dbg[512 * blockIdx.x + 259 + (c0 - split * W) / 64] = gtime();
+      }
+      }
+      // The accumulator has been read completely: hand it back to the MMA.
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_relaxed_cluster(lead_tempty0 + 8 * acc);
+      if (P.dbg && etid == 0 && i < 64) P.dbg[512 * blockIdx.x + 192 + i] = gtime();
       }
     }
   }
@@ -468,6 +580,20 @@ void* upload(const std::vector<T>& v) {
   if (!v.empty() && cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     fail(LFGPU_ECUDA, "cudaMemcpy pair tables");
   return d;
+}
+
+// The kernel instance for (split-K, row-segment stores), with its dynamic
+// SMEM limit raised once.
+const void* pair_instance(bool split, bool unit) {
+  static const void* fns[4] = {
+      reinterpret_cast<const void*>(pair_kernel<false, false>), reinterpret_cast<const void*>(pair_kernel<false, true>),
+      reinterpret_cast<const void*>(pair_kernel<true, false>), reinterpret_cast<const void*>(pair_kernel<true, true>)};
+  static bool attr_set = [] {
+    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    return true;
+  }();
+  (void)attr_set;
+  return fns[(split ? 2 : 0) + (unit ? 1 : 0)];
 }
 
 }  // namespace
@@ -513,7 +639,9 @@ PairLaunch pair_prepare(const PairPlan& p) {
   while (cols < 2 * p.BN) cols *= 2;
   L.tmem_cols = cols;
   L.ring_bytes = L.pipe * L.stage_bytes;
-  L.smem = 1024 + L.ring_bytes + kEpiBytes + 8 * (2 * L.pipe + 8) +
+  L.rx_bytes = p.rx_bytes;
+  L.xmode = p.rx_bytes > 0 ? 1 : 0;
+  L.smem = 1024 + L.ring_bytes + kEpiBytes + L.rx_bytes + 8 * (2 * L.pipe + 8) +
            pair_table_bytes(p.KS, p.MT, p.NT, p.BN, p.A.boxes, p.B.boxes);
   if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "pair kernel SMEM exceeds 227 KB");
   // Row-segment stores need contiguous output columns and 16-byte aligned rows.
@@ -540,19 +668,19 @@ PairLaunch pair_prepare(const PairPlan& p) {
   L.out = p.out;
   L.out_bf16 = p.out_bf16;
   const int ntiles = p.MT / 2 * p.NT;
-  if (L.S > 1) {
+  if (L.S > 1) {  // L2 workspace (also the fallback when the DSMEM exchange cannot be used)
     const size_t ws = sizeof(float) * static_cast<size_t>(ntiles) * L.S * 256 * L.BN;
     if (cudaMalloc(&t->p[7], ws) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc pair split-K workspace");
     L.ws = static_cast<float*>(t->p[7]);
   }
   L.owner = t;
   if (const char* e = getenv("LFGPU_PAIR_GROUP")) L.group = std::max(1, atoi(e));
+  if (const char* e = getenv("LFGPU_PAIR_NP")) L.nprod = std::max(1, std::min(5, atoi(e)));
+  // A producer may run at most `pipe` stages ahead of the oldest unreleased
+  // one, or the parity wait on a ring slot two phases behind passes early.
+  L.nprod = std::min(L.nprod, L.pipe);
   // Persistent grid: as many clusters as can be co-resident, at most one per tile.
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  const void* kfn = pair_instance(L.S > 1, L.col_unit != 0);
   const int csize = 2 * L.S;
   int max_cl = umma_num_sms() / csize;
   {
@@ -569,10 +697,11 @@ PairLaunch pair_prepare(const PairPlan& p) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, pair_kernel, &cfg) == cudaSuccess && n > 0)
+    if (cudaOccupancyMaxActiveClusters(&n, kfn, &cfg) == cudaSuccess && n > 0)
       max_cl = std::min(max_cl, n);
     cudaGetLastError();
   }
+  if (L.xmode && max_cl < ntiles) L.xmode = 0;  // the DSMEM exchange needs one tile per cluster
   L.grid = csize * std::max(1, std::min(ntiles, max_cl));
   return L;
 }
@@ -616,6 +745,9 @@ cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
   P.dbg = static_cast<unsigned long long*>(umma_debug_buffer());
   P.dbg_split = getenv("LFGPU_PAIR_DBG_SPLIT") ? atoi(getenv("LFGPU_PAIR_DBG_SPLIT")) : -1;
   P.diag = getenv("LFGPU_PAIR_DIAG") ? atoi(getenv("LFGPU_PAIR_DIAG")) : 0;
+  P.nprod = L.nprod;
+  P.xmode = L.xmode;
+  P.rx_bytes = L.rx_bytes;
   static const bool pdl = [] {
     const char* e = getenv("LFGPU_PDL");
     return !(e && atoi(e) == 0);
@@ -635,7 +767,8 @@ cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, pair_kernel, L.tma_a, L.tma_b, P);
+  void* args[] = {const_cast<CUtensorMap*>(&L.tma_a), const_cast<CUtensorMap*>(&L.tma_b), &P};
+  return cudaLaunchKernelExC(&cfg, pair_instance(L.S > 1, L.col_unit != 0), args);
 }
 
 }  // namespace lfg

@@ -67,6 +67,7 @@ struct PairPlan {
   int NT = 0;     // BN-column pair tiles
   int KS = 0;     // K stages of 64
   int pipe = 4;
+  int rx_bytes = 0;  // S > 1 with one tile per cluster: DSMEM receive buffer
   OperandView A, B;           // A: 128-row box, B: BN/2-column box
   std::vector<int32_t> a_crd; // MT x A.boxes x 5
   std::vector<int32_t> b_crd; // 2*NT x B.boxes x 5
@@ -91,6 +92,8 @@ struct PairLaunch {
   const int64_t* col_off = nullptr;  // full column table (generic epilogue)
   float* ws = nullptr;
   int BN = 0, S = 1, MT = 0, NT = 0, KS = 0, pipe = 0, group = 8;
+  int nprod = 4;  // TMA producer warps
+  int xmode = 0, rx_bytes = 0;  // split-K exchange over DSMEM
   int a_boxes = 0, b_boxes = 0, a_slot = 0, b_slot = 0, stage_bytes = 0, tx_bytes = 0;
   uint64_t a_desc = 0, b_desc = 0;
   uint32_t a_kadv = 0, b_kadv = 0, idesc = 0, tmem_cols = 0;

@@ -1039,7 +1039,12 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
 
 void plan_run_steps(lfgpu_plan* P, cudaStream_t on = nullptr) {
   cudaStream_t st = on ? on : P->stream;
-  if ((P->flags & LFGPU_PLAN_CUDA_GRAPH) && !P->steps.empty()) {
+  // A plan of one kernel launches it directly: a graph launch costs ~3 us
+  // more per step on this B200 (tools/gemm_ceiling.py --nograph) and, unlike
+  // a direct PDL launch, cannot overlap the previous kernel's tail.
+  int64_t nl = 0;
+  for (const auto& s : P->steps) nl += s.launches;
+  if ((P->flags & LFGPU_PLAN_CUDA_GRAPH) && nl > 1) {
     if (!P->gexec) {
       CUDA_OK(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
       for (auto& s : P->steps) {

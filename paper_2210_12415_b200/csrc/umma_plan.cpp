@@ -1517,10 +1517,19 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     }
     const int budget = 227 * 1024 - 1024 - 8 * 32 * 36 * 4 - 512 -
                        static_cast<int>(pair_table_bytes(KS, q.MT, q.NT, BN, q.A.boxes, q.B.boxes));
-    q.pipe = std::max(2, std::min(8, budget / stage));
-    if (const char* e = getenv("LFGPU_PAIR_PIPE")) q.pipe = std::max(2, std::min(q.pipe, atoi(e)));
     const int tiles = q.MT / 2 * q.NT;
     for (int S : {1, 2, 4}) {
+      // Split K with one tile per cluster exchanges partials over DSMEM: a
+      // dedicated receive buffer of (S-1) x 128 x BN/S fp32 (the send
+      // staging aliases the idle operand ring).
+      bool dsm = S > 1 && tiles <= sms / (2 * S) && !getenv("LFGPU_PAIR_NO_DSMEM");
+      const int rx = (S - 1) * 128 * (BN / S) * 4;
+      // send staging: each epilogue warp stages its chunks of the sibling slices
+      if (dsm && std::max(2, std::min(8, (budget - rx) / stage)) * stage < ((BN / 64) * (S - 1) + S - 1) / S * 8 * 4096)
+        dsm = false;
+      q.rx_bytes = dsm ? rx : 0;
+      q.pipe = std::max(2, std::min(8, (budget - q.rx_bytes) / stage));
+      if (const char* e = getenv("LFGPU_PAIR_PIPE")) q.pipe = std::max(2, std::min(q.pipe, atoi(e)));
       if (force_s && S != force_s) continue;
       if (!force_s && s.order == 1 && S > 1) continue;
       if (!force_s && s.order == 2 && S < 2) continue;
@@ -1537,7 +1546,9 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
       const int waves = (tiles + clusters - 1) / clusters;
       const double per_stage = std::max(2.0 * BN, stage / 48.0);
       const double epi = 128.0 * BN * 4 / 64.0;
-      const double red = S > 1 ? (2.0 * 128 * BN * 4 + (S + 1.0) * 128 * BN / S * 4) / 64.0 : 0.0;
+      const double red = S == 1 ? 0.0
+                         : dsm ? ((S - 1.0) * 128 * BN / S * 4) / 20.0
+                               : (2.0 * 128 * BN * 4 + (S + 1.0) * 128 * BN / S * 4) / 64.0;
       const double cost = waves * ((KS / S) * per_stage + epi + red) + 2500.0;
       if (cost < best_cost) {
         best_cost = cost;

@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--tile", type=int, default=1)
     ap.add_argument("--bk", action="store_true", help="K-major B ([K/64][N][64])")
+    ap.add_argument("--nograph", action="store_true", help="plain launches instead of a CUDA graph per step")
     ap.add_argument("--cold", action="store_true", help="rotate over replicas > 2x L2 (cold operands)")
     a = ap.parse_args()
     pk = peak()
@@ -59,7 +60,7 @@ def main():
         if a.bk:
             from paper_2210_12415_b200.layout import reorder, split
             seqs["b"] = [split(0, [n // 64, 64]), reorder([0, 2, 1])]
-        p = runtime.Plan(g, seqs, [runtime.sched(0, tile_last=a.tile)], flags=_abi.PLAN_REQUIRE_TC | _abi.PLAN_CUDA_GRAPH)
+        p = runtime.Plan(g, seqs, [runtime.sched(0, tile_last=a.tile)], flags=_abi.PLAN_REQUIRE_TC | (0 if a.nograph else _abi.PLAN_CUDA_GRAPH))
         x = (torch.randint(-64, 65, (n, n), device="cuda", dtype=torch.float32) / 64).contiguous()
         y = (torch.randint(-64, 65, (n, n), device="cuda", dtype=torch.float32) / 64).contiguous()
         p.set_input_device("a", x)

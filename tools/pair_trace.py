@@ -45,6 +45,8 @@ ncta = int((t[:, 320] != 0).sum())
 t = t[:ncta]
 t0 = t[t > 0].min()
 ent = (t[:, 320] - t0) / 1e3
+print("blob copied %.2f, tmem alloc done %.2f" % (np.median(t[:, 324] - t0) / 1e3, np.median(t[:, 325] - t0) / 1e3))
+print("producer0: elected %.2f, tile coords %.2f, before first wait %.2f" % tuple(np.median(t[:, k] - t0) / 1e3 for k in (326, 327, 328)))
 print("entry spread (us): min %.2f max %.2f; setup done %.2f; pdl wait done %.2f; exit max %.2f" % (
     ent.min(), ent.max(), np.median(t[:, 321] - t0) / 1e3, np.median(t[:, 322] - t0) / 1e3,
     (t[:, 323].max() - t0) / 1e3))
