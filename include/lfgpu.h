@@ -182,6 +182,8 @@ typedef struct lfgpu_counters {
   int64_t tc_nodes;    /* nodes executed on tcgen05 tensor cores       */
   double cost;         /* median device time, microseconds            */
   double min_us;
+  double resolution_us;    /* timer granularity of one sample (event tick / runs) */
+  int64_t runs_per_sample; /* graph executions between one CUDA event pair   */
 } lfgpu_counters;
 
 /* ---- plan flags ----------------------------------------------------------- */
@@ -331,8 +333,16 @@ int lfgpu_plan_node_kernel(lfgpu_plan* plan, int32_t node, char* buf, int32_t ca
 
 /* The measure backend: replaces lf::simulate_cache (cachesim.cpp:152-174)
  * at the tuner's seam (tuner.cpp:178). Runs `warmup` untimed executions,
- * then `reps` timed ones with CUDA events; flush_l2 != 0 writes a buffer
- * larger than L2 before each timed execution. cost = median microseconds. */
+ * then `reps` samples; each sample brackets K back-to-back executions with
+ * one CUDA event pair (K sized so a sample spans ~100 us: a single event
+ * pair around a microsecond-scale graph sits on the event timer's ~1 us
+ * ladder). flush_l2 == 0: warm steady state, sample = span / K.
+ * flush_l2 != 0: cold and clean L2 — every execution is preceded by a
+ * read of a buffer 1.5x the L2 (evicting, and writing back, whatever the
+ * previous execution left), and the same K reads are timed alone right
+ * after: sample = (span(read+run) - span(read)) / K.
+ * cost = median sample (us), min_us = min sample, resolution_us = 1.024 / K
+ * (the event tick observed on this B200 spread over K executions). */
 int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t flush_l2,
                        lfgpu_counters* out);
 

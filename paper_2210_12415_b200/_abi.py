@@ -113,6 +113,8 @@ class Counters(C.Structure):
         ("tc_nodes", C.c_int64),
         ("cost", C.c_double),
         ("min_us", C.c_double),
+        ("resolution_us", C.c_double),
+        ("runs_per_sample", C.c_int64),
     ]
 
 

@@ -890,12 +890,13 @@ cudaError_t launch_digit_copy(const DigitMap& m, int src_elem, int dst_elem, con
   });
 }
 
-// L2 scrub for measurements: stream-read `bytes` (> L2) so the next timed
-// kernel starts with a cold and clean L2 (after the > L2 flush write).
+// L2 scrub for measurements: read `bytes` (> L2) with the normal L2 policy,
+// so the next timed kernel starts with a cold and clean L2 (dirty lines of
+// the previous execution are written back during the scrub).
 __global__ void __launch_bounds__(256) l2_touch(const int4* __restrict__ p, int64_t n, int* sink) {
   int acc = 0;
   for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += gridDim.x * 256ll) {
-    int4 v = __ldcs(p + i);
+    int4 v = __ldcg(p + i);  // normal L2 policy: displaces resident lines
     acc ^= v.x ^ v.y ^ v.z ^ v.w;
   }
   if (acc == 0x7fffffff) *sink = acc;

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -23,6 +24,9 @@
 #include <memory>
 #include <set>
 #include <string>
+#include <thread>
+#include <condition_variable>
+#include <mutex>
 #include <vector>
 
 #include "lf_core.hpp"
@@ -190,6 +194,14 @@ struct PTensor {
   // Input conversions (logical -> storage) compiled once per source element
   // type; key = src elem * 8 + dst elem (tables live in the plan's `keep`).
   std::map<int, CopyKernel> in_copy;
+  // Host-buffer entry points (lfgpu_plan_set_input / get_output, the
+  // reference's BufferMap of doubles): a device f64 staging buffer, a pinned
+  // host staging buffer and the output conversion, all kept with the plan so
+  // a repeated call is copies + K1 launches only.
+  void* d_f64 = nullptr;
+  double* h_pin = nullptr;
+  bool out_copy_ready = false;
+  CopyKernel out_copy;
   int dtype = LFGPU_DTYPE_F32;
   int role = LFGPU_ROLE_INTERMEDIATE;
   std::vector<Dim> logical, phys;
@@ -228,6 +240,8 @@ struct lfgpu_plan {
   // work already enqueued on the plan stream (async set-input conversions),
   // later plan-stream work (get_output, set-input) waits for the run.
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::vector<cudaEvent_t> stage_ev;  // per-chunk events of the host staging
+  int* h_err = nullptr;               // pinned: the device error flag read back with outputs
   int64_t bytes = 0, flops = 0, tc_nodes = 0;
   std::vector<int> order;
 
@@ -236,6 +250,12 @@ struct lfgpu_plan {
     if (ev_out) cudaEventDestroy(ev_out);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
+    for (auto e : stage_ev) cudaEventDestroy(e);
+    if (h_err) cudaFreeHost(h_err);
+    for (auto& x : t) {
+      if (x.d_f64) cudaFree(x.d_f64);
+      if (x.h_pin) cudaFreeHost(x.h_pin);
+    }
     keep.clear();
     if (stream) cudaStreamDestroy(stream);
   }
@@ -1263,6 +1283,127 @@ int lfgpu_plan_destroy(lfgpu_plan* plan) {
   return LFGPU_OK;
 }
 
+static void host_stage_alloc(PTensor& t, int64_t n) {
+  if (t.d_f64) return;
+  CUDA_OK(cudaMalloc(&t.d_f64, sizeof(double) * std::max<int64_t>(n, 1)));
+  CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&t.h_pin), sizeof(double) * std::max<int64_t>(n, 1),
+                        cudaHostAllocDefault));
+}
+
+// A small pool of host worker threads for the host-buffer entry points:
+// one core copies ~15 GB/s on the GPU box (tools/host_link_probe.py), the
+// pinned H2D link ~25 GB/s and D2H ~54 GB/s, so staging copies are split
+// over workers and overlapped with the DMA chunk by chunk.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p(std::max(2u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+    return p;
+  }
+  int size() const { return static_cast<int>(w_.size()); }
+  // Run fn(i) for i in [0, n) on the workers; returns when all are done.
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> one_caller(call_);  // plans on several host threads share the pool
+    std::unique_lock<std::mutex> lk(m_);
+    fn_ = &fn;
+    next_ = 0;
+    total_ = n;
+    left_ = n;
+    ++gen_;
+    cv_.notify_all();
+    done_.wait(lk, [&] { return left_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  explicit HostPool(unsigned n) {
+    for (unsigned i = 0; i < n; ++i) w_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : w_) t.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(m_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < total_); });
+      if (stop_) return;
+      while (next_ < total_) {
+        const int i = next_++;
+        const auto* fn = fn_;
+        lk.unlock();
+        (*fn)(i);
+        lk.lock();
+        if (--left_ == 0) done_.notify_all();
+      }
+      seen = gen_;
+    }
+  }
+  std::vector<std::thread> w_;
+  std::mutex call_, m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int next_ = 0, total_ = 0, left_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// memcpy of `bytes` split over the pool's workers
+static void host_copy_bytes(void* dst, const void* src, size_t bytes) {
+  HostPool& pool = HostPool::get();
+  const int nt = bytes >= (size_t(1) << 20) ? pool.size() : 1;
+  if (nt == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = (bytes / nt + 63) & ~size_t(63);
+  pool.run(nt, [&](int i) {
+    const size_t a = std::min(bytes, per * i), b = std::min(bytes, per * (i + 1));
+    if (a < b) std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+  });
+}
+
+constexpr size_t kStageChunk = size_t(2) << 20;  // bytes per overlapped staging chunk
+
+// user host -> pinned staging -> device, chunk by chunk: chunk i+1's host
+// copy overlaps chunk i's DMA (stream-ordered on `st`, not synchronised).
+static void stage_h2d(void* d_dst, void* h_pin, const void* src, size_t bytes, cudaStream_t st) {
+  for (size_t off = 0; off < bytes; off += kStageChunk) {
+    const size_t len = std::min(kStageChunk, bytes - off);
+    host_copy_bytes(static_cast<char*>(h_pin) + off, static_cast<const char*>(src) + off, len);
+    CUDA_OK(cudaMemcpyAsync(static_cast<char*>(d_dst) + off, static_cast<char*>(h_pin) + off, len,
+                            cudaMemcpyHostToDevice, st));
+  }
+}
+
+// device -> pinned staging -> user host, chunk by chunk: chunk i's host copy
+// overlaps chunk i+1's DMA. Returns after the last chunk has been copied.
+static void stage_d2h(void* dst, void* h_pin, const void* d_src, size_t bytes, cudaStream_t st,
+                      std::vector<cudaEvent_t>& ev) {
+  const size_t nch = (bytes + kStageChunk - 1) / kStageChunk;
+  while (ev.size() < nch) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+  }
+  for (size_t c = 0; c < nch; ++c) {
+    const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    CUDA_OK(cudaMemcpyAsync(static_cast<char*>(h_pin) + off, static_cast<const char*>(d_src) + off, len,
+                            cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaEventRecord(ev[c], st));
+  }
+  for (size_t c = 0; c < nch; ++c) {
+    const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    CUDA_OK(cudaEventSynchronize(ev[c]));
+    host_copy_bytes(static_cast<char*>(dst) + off, static_cast<char*>(h_pin) + off, len);
+  }
+}
+
 static void set_input_impl(lfgpu_plan* P, int32_t tensor, const void* d_logical, int32_t elem) {
   if (tensor < 0 || tensor >= static_cast<int32_t>(P->t.size()))
     fail(LFGPU_EINVAL, "tensor index out of range");
@@ -1294,11 +1435,14 @@ int lfgpu_plan_set_input(lfgpu_plan* plan, int32_t tensor, const double* host_lo
     if (n != numel(t.logical))
       fail(LFGPU_EINVAL, "input '" + t.id + "' has " + std::to_string(n) + " values, expected " +
                              std::to_string(numel(t.logical)));
-    DevBuf tmp(sizeof(double) * std::max<int64_t>(n, 1));
-    CUDA_OK(cudaMemcpyAsync(tmp.p, host_logical, sizeof(double) * n, cudaMemcpyHostToDevice,
-                            plan->stream));
-    set_input_impl(plan, tensor, tmp.p, LFGPU_ELEM_F64);
-    CUDA_OK(cudaStreamSynchronize(plan->stream));  // `tmp` is freed on return
+    PTensor& tt = plan->t[tensor];
+    host_stage_alloc(tt, n);
+    // user doubles -> pinned staging (host threads) -> device staging (DMA)
+    // -> K1 into the plan's physical layout(s); synchronous like the
+    // reference's by-value BufferMap.
+    stage_h2d(tt.d_f64, tt.h_pin, host_logical, sizeof(double) * n, plan->stream);
+    set_input_impl(plan, tensor, tt.d_f64, LFGPU_ELEM_F64);
+    CUDA_OK(cudaStreamSynchronize(plan->stream));
   });
 }
 
@@ -1349,25 +1493,34 @@ int lfgpu_plan_run_on(lfgpu_plan* plan, void* stream) {
 int lfgpu_plan_get_output(lfgpu_plan* plan, int32_t tensor, double* host_logical, int64_t n) {
   return guarded([&] {
     CUDA_OK(cudaSetDevice(plan->ctx->device));
-    check_device_error(plan);
-    const PTensor& t = plan->t.at(tensor);
+    PTensor& t = plan->t.at(tensor);
     if (n != numel(t.logical)) fail(LFGPU_EINVAL, "output size mismatch for '" + t.id + "'");
     if (!t.valid)
       fail(LFGPU_EUNSUPPORTED, "'" + t.id + "' was fused into an epilogue and not materialized");
-    CopySpec spec;
-    spec.lmap = identity_map(t.logical);
-    spec.src_seq = t.seq;  // forward map back to logical (interp.cpp:441-468)
-    spec.mode = FoldMode::Clamp;
-    std::vector<std::unique_ptr<DevBuf>> keep;
-    bool oob;
+    if (!t.out_copy_ready) {
+      CopySpec spec;
+      spec.lmap = identity_map(t.logical);
+      spec.src_seq = t.seq;  // forward map back to logical (interp.cpp:441-468)
+      spec.mode = FoldMode::Clamp;
+      bool oob;
+      t.out_copy = compile_copy(spec, t.d ? t.elem : LFGPU_ELEM_BF16, LFGPU_ELEM_F64, plan->keep, &oob);
+      t.out_copy_ready = true;
+    }
+    host_stage_alloc(t, n);
+    if (!plan->h_err) {
+      CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&plan->h_err), sizeof(int), cudaHostAllocDefault));
+      *plan->h_err = 0;
+    }
     const void* src = t.d ? t.d : t.d_bf16;
-    int se = t.d ? t.elem : LFGPU_ELEM_BF16;
-    CopyKernel k = compile_copy(spec, se, LFGPU_ELEM_F64, keep, &oob);
-    DevBuf tmp(sizeof(double) * std::max<int64_t>(n, 1));
-    CUDA_OK(run_copy(k, src, tmp.p, plan->ctx->d_err, plan->stream));
-    CUDA_OK(cudaMemcpyAsync(host_logical, tmp.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
-                            plan->stream));
-    CUDA_OK(cudaStreamSynchronize(plan->stream));
+    CUDA_OK(run_copy(t.out_copy, src, t.d_f64, plan->ctx->d_err, plan->stream));
+    int* h = plan->h_err;  // the out-of-range flag of this execution, read with the data
+    CUDA_OK(cudaMemcpyAsync(h, plan->ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, plan->stream));
+    stage_d2h(host_logical, t.h_pin, t.d_f64, sizeof(double) * n, plan->stream, plan->stage_ev);
+    if (*h) {
+      CUDA_OK(cudaMemsetAsync(plan->ctx->d_err, 0, sizeof(int), plan->stream));
+      CUDA_OK(cudaStreamSynchronize(plan->stream));
+      fail(LFGPU_ERANGE, "out-of-range access during execution");
+    }
   });
 }
 
@@ -1412,38 +1565,56 @@ int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t f
     lfgpu_ctx* ctx = plan->ctx;
     CUDA_OK(cudaSetDevice(ctx->device));
     if (flush_l2 && !ctx->flush) {
-      ctx->flush_bytes = size_t(512) << 20;  // 256 MB write + 256 MB read (L2 is 126 MB)
+      ctx->flush_bytes = size_t(192) << 20;  // 1.5x the 126 MB L2, read once per execution
       CUDA_OK(cudaMalloc(&ctx->flush, ctx->flush_bytes));
+      CUDA_OK(cudaMemsetAsync(ctx->flush, 0, ctx->flush_bytes, plan->stream));
     }
+    auto touch = [&] {
+      CUDA_OK(launch_l2_touch(ctx->flush, ctx->flush_bytes, static_cast<int*>(ctx->flush), plan->stream));
+    };
     for (int i = 0; i < warmup; ++i) plan_run_steps(plan);
-    std::vector<cudaEvent_t> ev(2 * std::max(reps, 1));
-    for (auto& e : ev) CUDA_OK(cudaEventCreate(&e));
-    for (int r = 0; r < reps; ++r) {
-      if (flush_l2) {
-        // > L2 write (the flush), then a > L2 read so the measured graph
-        // starts with a cold *and clean* L2 (no dirty-line write-backs).
-        CUDA_OK(cudaMemsetAsync(ctx->flush, r & 0xff, ctx->flush_bytes / 2, plan->stream));
-        CUDA_OK(launch_l2_touch(static_cast<char*>(ctx->flush) + ctx->flush_bytes / 2,
-                                ctx->flush_bytes / 2, static_cast<int*>(ctx->flush),
-                                plan->stream));
-      }
-      CUDA_OK(cudaEventRecord(ev[2 * r], plan->stream));
-      plan_run_steps(plan);
-      CUDA_OK(cudaEventRecord(ev[2 * r + 1], plan->stream));
-    }
+    reps = std::max(reps, 1);
+    cudaEvent_t e[4];
+    for (auto& x : e) CUDA_OK(cudaEventCreate(&x));
+    auto span = [&](cudaEvent_t a, cudaEvent_t b) {
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, a, b));
+      return ms * 1000.0;
+    };
+    // K: executions per event pair, from a 4-execution estimate (warm)
+    CUDA_OK(cudaEventRecord(e[0], plan->stream));
+    for (int i = 0; i < 4; ++i) plan_run_steps(plan);
+    CUDA_OK(cudaEventRecord(e[1], plan->stream));
     CUDA_OK(cudaStreamSynchronize(plan->stream));
+    const double est = std::max(0.5, span(e[0], e[1]) / 4.0);
+    int K = static_cast<int>(std::lround(100.0 / est));
+    K = std::max(flush_l2 ? 2 : 4, std::min(flush_l2 ? 8 : 64, K));
     std::vector<double> us;
     for (int r = 0; r < reps; ++r) {
-      float ms = 0;
-      CUDA_OK(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
-      us.push_back(ms * 1000.0);
+      CUDA_OK(cudaEventRecord(e[0], plan->stream));
+      for (int k = 0; k < K; ++k) {
+        if (flush_l2) touch();
+        plan_run_steps(plan);
+      }
+      CUDA_OK(cudaEventRecord(e[1], plan->stream));
+      if (flush_l2) {
+        CUDA_OK(cudaEventRecord(e[2], plan->stream));
+        for (int k = 0; k < K; ++k) touch();
+        CUDA_OK(cudaEventRecord(e[3], plan->stream));
+      }
+      CUDA_OK(cudaStreamSynchronize(plan->stream));
+      double t = span(e[0], e[1]);
+      if (flush_l2) t -= span(e[2], e[3]);
+      us.push_back(t / K);
     }
-    for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& x : e) cudaEventDestroy(x);
     check_device_error(plan);
     std::sort(us.begin(), us.end());
     lfgpu_plan_info(plan, out);
-    out->cost = us.empty() ? 0.0 : us[us.size() / 2];
-    out->min_us = us.empty() ? 0.0 : us.front();
+    out->cost = us[us.size() / 2];
+    out->min_us = us.front();
+    out->runs_per_sample = K;
+    out->resolution_us = 1.024 / K;
   });
 }
 

@@ -274,9 +274,13 @@ class Plan:
         else:
             check(lib().lfgpu_plan_run_on(self.ptr, C.c_void_p(stream)))
 
-    def get_output(self, tid):
+    def get_output(self, tid, out=None):
+        """Logical doubles of `tid` (the reference's BufferMap entry); `out`
+        (a C-contiguous float64 array of the right size) is filled in place."""
         n = self.graph.tensor(tid).num_elements()
-        out = np.zeros(n, dtype=np.float64)
+        if out is None:
+            out = np.empty(n, dtype=np.float64)
+        assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == n
         check(lib().lfgpu_plan_get_output(self.ptr, self.index(tid),
                                           out.ctypes.data_as(C.POINTER(C.c_double)), n))
         return out

@@ -172,6 +172,18 @@ def ref_interpret(g: Graph, seqs, scheds, bufs):
     return rc
 
 
+def ref_simulate_cache(g: Graph, seqs, scheds):
+    """lf::simulate_cache(lower(g, seqs, scheds), CacheConfig{}) (cachesim.cpp:152-174):
+    the reference's measurement backend. Returns (cost, l1_misses)."""
+    cg = g.to_c(seqs)
+    ns = len(scheds)
+    sarr = (_abi.Sched * max(1, ns))(*scheds)
+    cost, miss = C.c_double(), C.c_int64()
+    rc = ref().ref_simulate_cache(cg.ptr(), ns, sarr, C.byref(cost), C.byref(miss))
+    assert rc == 0, ref().ref_last_error()
+    return cost.value, miss.value
+
+
 def ref_decode_layout(g: Graph, node, factors, tiling_levels=1):
     cg = g.to_c()
     f, fp = i64(factors)
