@@ -236,10 +236,16 @@ inline std::vector<double> materialize(Context& ctx, const std::vector<Dim>& log
 /// The tuner's measurement on the GPU: cost = median device microseconds of
 /// the whole lowered graph. Counter fields: insts = kernel launches,
 /// l1_loads = algorithmic bytes, l1_misses = 0, l1_stores = tensor-core nodes.
+/// Default flags never reject a point the reference's lowering accepted:
+/// tcgen05 where the layout allows it, the CUDA-core contraction otherwise
+/// (its cost then ranks the point). The seam at tuner.cpp:178 sits outside
+/// Tuner::evaluate's try/catch (tuner.cpp:169-174), so a throwing measure
+/// would abort lf::tune; pass LFGPU_PLAN_REQUIRE_TC only from callers that
+/// catch lf::Error themselves.
 inline ProfileCounters measure(Context& ctx, const Graph& g, const SeqMap& seqs,
                                const std::vector<LoopSchedule>& scheds, int warmup = 3,
                                int reps = 10, bool flush_l2 = true,
-                               int flags = LFGPU_PLAN_REQUIRE_TC | LFGPU_PLAN_CUDA_GRAPH) {
+                               int flags = LFGPU_PLAN_CUDA_GRAPH) {
   Desc d = describe(g, seqs);
   auto sc = to_scheds(g, seqs, scheds);
   lfgpu_plan* plan = nullptr;

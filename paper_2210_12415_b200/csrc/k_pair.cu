@@ -674,6 +674,7 @@ PairLaunch pair_prepare(const PairPlan& p) {
     L.ws = static_cast<float*>(t->p[7]);
   }
   L.owner = t;
+  L.group = p.group;
   if (const char* e = getenv("LFGPU_PAIR_GROUP")) L.group = std::max(1, atoi(e));
   if (const char* e = getenv("LFGPU_PAIR_NP")) L.nprod = std::max(1, std::min(5, atoi(e)));
   // A producer may run at most `pipe` stages ahead of the oldest unreleased

@@ -40,6 +40,7 @@ struct UmmaParams {
   int32_t epi_count;
   int32_t ntiles, nstages, BN, ksteps, pipe, nprod;
   int32_t dual;  // two MMA issuers: warp 1 takes even units, warp 3 odd ones
+  int32_t blocked;  // loop point `parallel` = 1: contiguous unit chunks per CTA (static schedule), else cyclic
   int32_t a_boxes, b_boxes, a_slot, b_slot, tx_bytes;
   uint64_t a_desc, b_desc;  // LBO/SBO/version/layout bits; start address added on device
   uint32_t a_kadv, b_kadv;
@@ -531,6 +532,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int splits = SPLITK ? P.splits : 1;
   const int nunits = P.ntiles * splits;
+  // This CTA's units: cyclic (u = blockIdx.x + k * gridDim.x) or, for loop
+  // point parallel = 1 without split-K, one contiguous chunk (the outermost
+  // loop's static-schedule parallelisation, space.cpp:569-575).
+  const int uper = (nunits + gridDim.x - 1) / gridDim.x;
+  const int u_first = P.blocked ? blockIdx.x * uper : blockIdx.x;
+  const int u_end = P.blocked ? min(nunits, u_first + uper) : nunits;
+  const int u_step = P.blocked ? 1 : gridDim.x;
   const int nst = P.nstages;
   unsigned long long* dbg = P.dbg ? P.dbg + 32 * blockIdx.x : nullptr;
   if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
@@ -600,9 +608,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t b_off = P.a_boxes * a_slot;
     const int na = P.a_boxes, nb = P.b_boxes;
     const bool leader = elect_one();
-    if (nw && prod == 0 && leader && blockIdx.x < nunits) {
+    if (nw && prod == 0 && leader && u_first < u_end) {
       // Resident weights: every chunk's slab once, on its own barrier.
-      const TileEntry* te = P.tiles + blockIdx.x / splits;
+      const TileEntry* te = P.tiles + u_first / splits;
       for (int c = 0; c < nw; ++c) {
         const StageEntry se = s_stage[c];
         const uint32_t bar = wfull0 + 8 * c;
@@ -616,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const int nbs = nw ? 0 : nb;  // B boxes streamed per stage
     int g = 0;  // CTA-wide stage counter (ring slot / phase)
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    for (int u = u_first; u < u_end; u += u_step) {
       const int tile = u / splits, split = u - tile * splits;
       const int s_lo = split * nst / splits, s_hi = (split + 1) * nst / splits;
       int s = s_lo + ((prod - g) % np + np) % np;
@@ -667,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int i = 0;
     const int role = warp == 3 ? 1 : 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+    for (int u = u_first; u < u_end; u += u_step, ++i) {
       const int split = u % splits;
       const int s_lo = split * nst / splits, s_hi = (split + 1) * nst / splits;
       if (P.dual && (i & 1) != role) {  // the other issuer's unit: step over its stages
@@ -732,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // stores, no barrier arrivals) while the main loop fills TMEM; the real
     // pass then executes from a warm instruction cache.
     bool dry = !SPLITK && (P.diag & 64) && !P.epi_alias;  // opt-in (no measured gain)
-    for (int u = blockIdx.x; u < nunits;) {
+    for (int u = u_first; u < u_end;) {
       const int tile = u / splits, split = u - tile * splits;
       const int b = i & 1;
       const uint32_t tempty = tempty0 + 8 * b;
@@ -926,7 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         dry = false;
         continue;
       }
-      u += gridDim.x;
+      u += u_step;
       ++i;
     }
     if (half_leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1320,6 +1328,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     const int spu = (L.nstages + L.splits - 1) / L.splits;
     L.dual = p.BN <= 128 && units >= 2 * L.grid && 2 * spu <= L.pipe;
     if (const char* e = getenv("LFGPU_DUAL_MMA")) L.dual = atoi(e) != 0;
+    L.blocked = p.persistent && L.splits == 1 ? 1 : 0;
     if (L.dual) L.nprod = std::min(L.nprod, 2);
   }
   static_assert(sizeof(TileEntry) == 192, "TileEntry layout");
@@ -1349,6 +1358,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.pipe = L.pipe;
   P.nprod = L.nprod;
   P.dual = L.dual;
+  P.blocked = L.blocked;
   P.a_boxes = L.a_boxes;
   P.b_boxes = L.b_boxes;
   P.a_slot = L.a_slot;

@@ -68,6 +68,7 @@ struct PairPlan {
   int KS = 0;     // K stages of 64
   int pipe = 4;
   int rx_bytes = 0;  // S > 1 with one tile per cluster: DSMEM receive buffer
+  int group = 8;     // tile rasterization: row pairs that sweep the column tiles together (loop point `parallel`)
   OperandView A, B;           // A: 128-row box, B: BN/2-column box
   std::vector<int32_t> a_crd; // MT x A.boxes x 5
   std::vector<int32_t> b_crd; // 2*NT x B.boxes x 5

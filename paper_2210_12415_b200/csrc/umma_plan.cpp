@@ -486,7 +486,10 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     *why = "rows per tile out of range";
     return false;
   }
-  if (RT == 128 && !getenv("LFGPU_NO_PAIR")) {
+  // Loop point tile_second (tile of the M brick loop) picks the M tile:
+  // 128 -> the 1-CTA kernel (BM = 128); otherwise the CTA-pair kernel
+  // (BM = 256) when the shape and layouts allow it.
+  if (RT == 128 && s.tile_second != 128 && !getenv("LFGPU_NO_PAIR")) {
     // The CTA-pair kernel (256-row tiles, cta_group::2) when the shape and
     // the layouts allow it; the 1-CTA kernel below otherwise.
     PairPlan pp;
@@ -717,7 +720,11 @@ static bool plan_conv_halo_kc(const std::vector<Dim>& x_log, const std::vector<P
   // (deep layers, small batches) this puts 4-8x more work in every UMMA.
   const bool trans = s.unroll == 2;
   int64_t h_sub = std::min<int64_t>(h_t, (trans ? 256 : 128) / B_w);
-  if (trans)  // whole pixel chunks per tile: every tile has the same columns
+  // Loop point tile_second (the second-innermost spatial tile, space.cpp:
+  // 497-499) caps the output rows per UMMA tile: smaller tiles, more of them
+  // (fills the SMs at small batch) at the cost of more halo re-reads.
+  if (s.tile_second > 1 && s.tile_second < h_sub) h_sub = s.tile_second;
+  if (trans || s.tile_second > 1)  // whole row chunks per tile: every tile has the same shape
     while (h_sub > 1 && h_t % h_sub) --h_sub;
   const int64_t rows_h = h_sub + KH - 1;
   // Weight: [..][KH][KW][i'][o'] (o' innermost: MN-major B) or, when the
@@ -1090,7 +1097,11 @@ bool umma_plan_conv(const std::vector<Dim>& x_log, const Seq& x_seq, const std::
     *why = "w_t > 128 rows";
     return false;
   }
-  const int64_t h_sub = std::min<int64_t>(h_t, 128 / w_t);
+  int64_t h_sub = std::min<int64_t>(h_t, 128 / w_t);
+  if (s.tile_second > 1 && s.tile_second < h_sub) {  // loop point tile_second: rows per tile cap
+    h_sub = s.tile_second;
+    while (h_sub > 1 && h_t % h_sub) --h_sub;
+  }
   if (h_sub * V > 256 || w_t * V > 256) {
     *why = "TMA box exceeds 256";
     return false;
@@ -1565,6 +1576,8 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
   os << "gemm-pair BM=256 BN=" << best.BN << " S=" << best.S << " A=" << (best.A.mn_major ? "MN" : "K")
      << "-major B=" << (best.B.mn_major ? "MN" : "K") << "-major tiles=" << best.MT / 2 * best.NT
      << " pipe=" << best.pipe;
+  best.group = s.parallel ? 1 : 8;
+  os << " raster=" << (best.group == 1 ? "rows" : "group8");
   best.summary = os.str();
   *out = best;
   return true;

@@ -1,0 +1,135 @@
+// tune_check.cpp — TEST INFRASTRUCTURE: the reference's own two-stage tuner
+// (proj/src/tuner.cpp, lf::tune) driven by the GPU measure backend through
+// the one-line seam INTEGRATION.md shows (tuner.cpp:178, generated into
+// oracle/_ref/tune/tuner_gpu.cpp by `make -C oracle tune`).
+//
+//   tune_check host                 hook unset: the hooked tuner equals the
+//                                   unmodified one (simulate_cache) on a
+//                                   small GMM graph (same best cost)
+//   tune_check gpu <cfg> <budget> <mode>
+//                                   cfg: cfg1 (Padding -> C2D 64->64 3x3
+//                                   56x56, N=1) | cfg2 (GMM 1024^3);
+//                                   mode: tc (LFGPU_PLAN_REQUIRE_TC: points
+//                                   the tensor-core kernels cannot take are
+//                                   counted as rejected and scored with a
+//                                   penalty) | any (the adapter's default:
+//                                   tcgen05 where the layout allows it,
+//                                   CUDA cores otherwise; never rejects).
+// Prints one JSON line: measurements, rejected, tensor-core plans, best cost
+// (us), wall seconds and candidates/s. Built by tests/test_adapter.py.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "layoutforge/cachesim.hpp"
+#include "layoutforge/tuner.hpp"
+#include "lf_gpu.hpp"
+
+using namespace lf;
+
+lf::ProfileCounters (*lf_gpu_measure_hook)(const lf::Graph&, const lf::SeqMap&,
+                                           const std::vector<lf::LoopSchedule>&) = nullptr;
+
+namespace {
+
+gpu::Context* g_ctx = nullptr;
+int g_flags = LFGPU_PLAN_CUDA_GRAPH;
+int g_calls = 0, g_rejected = 0, g_tc = 0;
+constexpr double kPenaltyUs = 1e6;  // a rejected point's score (mode tc)
+
+ProfileCounters gpu_hook(const Graph& g, const SeqMap& seqs, const std::vector<LoopSchedule>& sc) {
+  ++g_calls;
+  try {
+    ProfileCounters p = gpu::measure(*g_ctx, g, seqs, sc, 1, 3, true, g_flags);
+    if (p.l1_stores > 0) ++g_tc;  // l1_stores = nodes executed on tcgen05
+    return p;
+  } catch (const Error&) {
+    ++g_rejected;
+    ProfileCounters p;
+    p.cost = kPenaltyUs;
+    return p;
+  }
+}
+
+TensorDecl T(const std::string& id, std::vector<Dim> d, Role r) {
+  TensorDecl t;
+  t.id = id;
+  t.dims = std::move(d);
+  t.role = r;
+  return t;
+}
+
+OperatorNode N(OpKind k, std::vector<std::string> in, std::string out, std::map<std::string, int64_t> a = {}) {
+  OperatorNode n;
+  n.kind = k;
+  n.inputs = std::move(in);
+  n.output = std::move(out);
+  n.attrs = std::move(a);
+  return n;
+}
+
+Graph cfg1() {  // BASELINE configs[0]: Padding -> C2D 64->64 3x3 s1, 56x56, N=1
+  Graph g;
+  g.tensors = {T("x", {{"N", 1}, {"I", 64}, {"H", 56}, {"W", 56}}, Role::Input),
+               T("ker", {{"O", 64}, {"I", 64}, {"KH", 3}, {"KW", 3}}, Role::Constant),
+               T("xp", {{"N", 1}, {"I", 64}, {"H", 58}, {"W", 58}}, Role::Intermediate),
+               T("y", {{"N", 1}, {"O", 64}, {"H", 56}, {"W", 56}}, Role::Output)};
+  g.nodes = {N(OpKind::Padding, {"x"}, "xp", {{"pad", 1}}), N(OpKind::C2D, {"xp", "ker"}, "y", {{"stride", 1}})};
+  return g;
+}
+
+Graph gmm(int64_t m, int64_t k, int64_t n) {  // BASELINE configs[1] at 1024^3
+  Graph g;
+  g.tensors = {T("a", {{"M", m}, {"K", k}}, Role::Input), T("b", {{"K", k}, {"N", n}}, Role::Constant),
+               T("c", {{"M", m}, {"N", n}}, Role::Output)};
+  g.nodes = {N(OpKind::GMM, {"a", "b"}, "c")};
+  return g;
+}
+
+Budget budget(int total) {
+  Budget b;
+  b.total = total;
+  b.joint = total * 3 / 8;
+  b.loop_only = total - b.joint;
+  b.batch = 32;
+  b.top_k = 8;
+  b.seed = 42;
+  return b;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "host";
+  if (mode == "host") {
+    // With the hook unset the generated tuner is the reference's: same
+    // result twice (determinism, test_tuner.cpp:296-300) and a finite cost.
+    Graph g = gmm(64, 64, 64);
+    CacheConfig cc;
+    TuneResult r1 = tune(g, budget(16), cc), r2 = tune(g, budget(16), cc);
+    const bool ok = std::isfinite(r1.best_cost) && r1.best_cost == r2.best_cost && r1.sim_calls == r2.sim_calls &&
+                    r1.sim_calls > 0;
+    std::printf("host: %s best_cost=%.3f sims=%d\n", ok ? "OK" : "FAIL", r1.best_cost, r1.sim_calls);
+    return ok ? 0 : 1;
+  }
+  const std::string cfg = argc > 2 ? argv[2] : "cfg2";
+  const int total = argc > 3 ? std::atoi(argv[3]) : 64;
+  const std::string m = argc > 4 ? argv[4] : "any";
+  g_flags = LFGPU_PLAN_CUDA_GRAPH | (m == "tc" ? LFGPU_PLAN_REQUIRE_TC : 0);
+  gpu::Context ctx(0);
+  g_ctx = &ctx;
+  lf_gpu_measure_hook = gpu_hook;
+  Graph g = cfg == "cfg1" ? cfg1() : gmm(1024, 1024, 1024);
+  auto t0 = std::chrono::steady_clock::now();
+  TuneResult r = tune(g, budget(total), CacheConfig{});
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::printf(
+      "{\"cfg\": \"%s\", \"mode\": \"%s\", \"budget\": %d, \"measurements\": %d, \"rejected\": %d, "
+      "\"tensor_core_plans\": %d, \"rejected_frac\": %.4f, \"best_cost_us\": %.3f, \"seconds\": %.2f, "
+      "\"candidates_per_s\": %.2f}\n",
+      cfg.c_str(), m.c_str(), total, g_calls, g_rejected, g_tc, g_calls ? double(g_rejected) / g_calls : 0.0,
+      r.best_cost, secs, secs > 0 ? g_calls / secs : 0.0);
+  return (g_calls > 0 && std::isfinite(r.best_cost)) ? 0 : 1;
+}

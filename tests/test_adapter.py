@@ -32,6 +32,55 @@ def build_adapter():
     return True
 
 
+TUNE_BIN = os.path.join(HERE, "tune_check")
+
+
+def build_tune_check():
+    """The reference's lf::tune with its measure seam hooked to the GPU
+    backend (oracle/Makefile `tune` target generates the hooked tuner.cpp
+    into oracle/_ref/tune/; test infrastructure only)."""
+    if not os.path.isdir(REF_INC):
+        return os.path.exists(TUNE_BIN)
+    from paper_2210_12415_b200 import build
+    build.build()
+    subprocess.run(["make", "-s", "-C", os.path.join(O.ROOT, "oracle"), "ref", "tune"], check=True,
+                   capture_output=True, text=True)
+    objdir = os.path.join(O.ROOT, "oracle", "_ref", "obj")
+    objs = [os.path.join(objdir, f) for f in sorted(os.listdir(objdir)) if f.endswith(".o") and f != "tuner.o"]
+    cmd = ["g++", "-std=c++20", "-O1", "-I", REF_INC, "-I", os.path.join(O.ROOT, "include"),
+           os.path.join(HERE, "tune_check.cpp"), "-o", TUNE_BIN,
+           os.path.join(O.ROOT, "oracle", "_ref", "tune", "tuner_gpu.o"), *objs,
+           os.path.join(O.ROOT, "paper_2210_12415_b200", "liblfgpu.so"), "-lpthread",
+           "-Wl,-rpath,$ORIGIN/../../paper_2210_12415_b200"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return True
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC) or not O.ref_available(),
+                    reason="reference headers / build absent")
+def test_hooked_reference_tuner_matches_simulator_when_unhooked():
+    assert build_tune_check()
+    r = subprocess.run([TUNE_BIN, "host"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "host: OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+def test_reference_tuner_drives_gpu_measure(cfg):
+    """lf::tune (tuner.cpp) at budget 64 with every measurement on the B200
+    (the tuner.cpp:178 seam): the adapter's default never rejects a point
+    the reference's lowering accepted, and the search finishes with a finite
+    measured best cost."""
+    import json
+    if not build_tune_check():
+        pytest.skip("tune_check binary not built (needs the reference sources once)")
+    r = subprocess.run([TUNE_BIN, "gpu", cfg, "64", "any"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rep = json.loads(r.stdout.strip().splitlines()[-1])
+    assert rep["measurements"] > 0 and rep["rejected"] == 0, rep
+    assert 0 < rep["best_cost_us"] < 1e5, rep
+
+
 @pytest.mark.skipif(not os.path.isdir(REF_INC) or not O.ref_available(),
                     reason="reference headers / build absent")
 def test_adapter_host_roundtrips():

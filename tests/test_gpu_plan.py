@@ -478,3 +478,41 @@ def test_run_on_user_stream_joins_async_set_input():
         p.run(stream=user.cuda_stream)
         got = p.get_output("c")
         assert np.array_equal(got, ref["c"] * (rep + 1)), rep
+
+
+# Loop-point parameters the GPU lowering maps to kernel structure
+# (space.cpp:483-589 -> DESIGN.md §4.4): tile_second picks the GEMM M tile
+# (128: 1-CTA kernel, else the CTA pair) and caps the C2D rows per UMMA tile;
+# parallel picks the pair kernel's tile rasterization and the 1-CTA kernel's
+# unit dealing (contiguous chunks vs cyclic). Every variant is bit-exact.
+@pytest.mark.parametrize("ts,par", [(1, 0), (1, 1), (128, 0), (128, 1), (256, 1)])
+def test_gemm_loop_point_tile_second_parallel(ts, par):
+    g, seqs, inputs, ref = gemm_case(512, 1024, 1024, (256, 64, 128))
+    p = runtime.Plan(g, seqs, [runtime.sched(0, tile_last=128, tile_second=ts, parallel=par)],
+                     flags=_abi.PLAN_REQUIRE_TC)
+    k = p.node_kernel(0)
+    assert ("gemm-pair" in k) == (ts != 128), k
+    if ts != 128:
+        assert ("raster=rows" if par else "raster=group8") in k, k
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    got = p.get_output("c")
+    assert np.array_equal(got, ref["c"]), np.abs(got - ref["c"]).max()
+
+
+@pytest.mark.parametrize("factors,ts,rows", [((28, 2, 32, 32, 32, 32), 1, "28x"), ((28, 2, 32, 32, 32, 32), 7, "7x"),
+                                             ((28, 2, 32, 32, 32, 32), 4, "4x"), ((8, 8, 32, 32, 32, 32), 3, "2x")])
+@pytest.mark.parametrize("par", [0, 1])
+def test_conv_loop_point_tile_second_parallel(factors, ts, rows, par):
+    g = ir.pad_conv(1, 64, 64, 56, 3, 1, 1)
+    seqs = runtime.decode_layout(g, 1, list(factors))
+    inputs, ref = oracle_outputs(g, 42)
+    p = runtime.Plan(g, seqs, [runtime.sched(1, tile_second=ts, parallel=par)], flags=_abi.PLAN_REQUIRE_TC)
+    k = p.node_kernel(1)
+    assert f"rows={rows}" in k, k
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    y = p.get_output("y")
+    assert np.array_equal(y, ref["y"]), np.abs(y - ref["y"]).max()
