@@ -75,6 +75,24 @@ def conv_b16best(reps=3):
     conv(reps, 16, (8, 28, 64, 32, 32, 64))
 
 
+def gemm_pair(reps=3):
+    """cfg2 on the CTA-pair kernel (BN=128, 2 K splits over DSMEM)."""
+    gemm(reps, (256, 64, 256), 128, 0)
+
+
+def gemm_bench(reps=3):
+    """cfg2 on the layout the r02 bench tuner picked (1-CTA BM=128 BN=64)."""
+    gemm(reps, (512, 512, 256), 64, 0)
+
+
+def conv_b16r02(reps=3):
+    conv(reps, 16, (28, 28, 64, 32, 32, 64))
+
+
+def conv_b1r02(reps=3):
+    conv(reps, 1, (28, 2, 32, 32, 32, 32))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["gemm", "conv", "transform"]
     for w in which:
