@@ -73,7 +73,25 @@ enum {
    *   explicitly padded input (no implicit padding, like C2D).
    * GlobalAvgPool: out[b,c] = (sum_{h,w} in[b,c,h,w]) / (H*W), rank 4 -> 2. */
   LFGPU_OP_MAXPOOL = 8,
-  LFGPU_OP_GLOBAL_AVGPOOL = 9
+  LFGPU_OP_GLOBAL_AVGPOOL = 9,
+  /* Extensions for a full BERT encoder; all over the
+   * last logical dim or per attention head, f32, not element-wise except
+   * GELU (which fuses into a contraction's epilogue like ReLU):
+   * GELU:      y = 0.5 x (1 + erf(x / sqrt(2)))
+   * Softmax:   y[.., j] = exp(x[.., j] - max) / sum_j' exp(x[.., j'] - max)
+   * LayerNorm: inputs x[.., D], gb[2, D] (row 0 gamma, row 1 beta);
+   *            y = (x - mean) / sqrt(var + 10^-eps_exp) * gamma + beta,
+   *            mean / biased var over the last dim (eps_exp default 12)
+   * BmmQK:     per-head scores; q[T, H*Dh], k[T', H*Dh] -> s[H, T, T'],
+   *            s[h,i,j] = sum_d q[i, h*Dh+d] * k[j, h*Dh+d]  (attrs heads = H)
+   * BmmPV:     per-head context; p[H, T, T'], v[T', H*Dh] -> o[T, H*Dh],
+   *            o[i, h*Dh+d] = sum_j p[h,i,j] * v[j, h*Dh+d]
+   * Reductions run in index order (d, j ascending), like interp.cpp. */
+  LFGPU_OP_GELU = 10,
+  LFGPU_OP_SOFTMAX = 11,
+  LFGPU_OP_LAYERNORM = 12,
+  LFGPU_OP_BMM_QK = 13,
+  LFGPU_OP_BMM_PV = 14
 };
 
 /* lf::DType (ir.hpp:26) and lf::Role (ir.hpp:27) */
@@ -135,6 +153,8 @@ typedef struct lfgpu_node {
   int32_t inputs[2];
   int32_t output;
   int32_t window; /* MaxPool window (KH = KW); 0 elsewhere */
+  int32_t heads;  /* attrs["heads"], BmmQK / BmmPV; 0 elsewhere */
+  int32_t eps_exp; /* attrs["eps_exp"], LayerNorm: eps = 10^-eps_exp (default 12) */
   int64_t stride; /* attrs["stride"], C2D/DEP/MaxPool (default 1) */
   int64_t pad;    /* attrs["pad"], Padding (default 0)    */
 } lfgpu_node;

@@ -17,6 +17,7 @@ SPLIT, REORDER, FUSE, UNFOLD, PAD, STORE_AT, FOLD, UNPAD, DECOUPLE_AT = range(9)
 # lf::OpKind (ir.hpp:42)
 C2D, DEP, GMM, PADDING, RELU, BIASADD, EWADD, LAYOUT_CONVERT = range(8)
 MAXPOOL, GLOBAL_AVGPOOL = 8, 9  # extensions beyond lf::OpKind (lfgpu.h)
+GELU, SOFTMAX, LAYERNORM, BMM_QK, BMM_PV = 10, 11, 12, 13, 14  # BERT encoder set
 # lf::DType / lf::Role
 F32, I32 = 0, 1
 INPUT, CONSTANT, INTERMEDIATE, OUTPUT = range(4)
@@ -71,6 +72,8 @@ class Node(C.Structure):
         ("inputs", C.c_int32 * 2),
         ("output", C.c_int32),
         ("window", C.c_int32),
+        ("heads", C.c_int32),
+        ("eps_exp", C.c_int32),
         ("stride", C.c_int64),
         ("pad", C.c_int64),
     ]

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(256)
     double r;
     switch (P.op) {
       case GEN_RELU: r = x > 0.0 ? x : 0.0; break;
+      case GEN_GELU: r = 0.5 * x * (1.0 + erf(x * 0.70710678118654752440)); break;
       case GEN_BIASADD:
       case GEN_EWADD: r = x + y; break;
       default: r = x; break;

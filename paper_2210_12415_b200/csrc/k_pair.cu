@@ -147,6 +147,14 @@ __device__ __forceinline__ void store_chunk(const PairParams& P, const Smem& T, 
           x[it].z = fmaxf(x[it].z, 0.f);
           x[it].w = fmaxf(x[it].w, 0.f);
         }
+      } else if (k == EPI_GELU) {
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          x[it].x = epi_gelu(x[it].x);
+          x[it].y = epi_gelu(x[it].y);
+          x[it].z = epi_gelu(x[it].z);
+          x[it].w = epi_gelu(x[it].w);
+        }
       } else if (k == EPI_BIAS) {
         const float4 b = *reinterpret_cast<const float4*>(bias + c0 + cl);
 #pragma unroll
@@ -194,6 +202,7 @@ __device__ __forceinline__ void store_chunk(const PairParams& P, const Smem& T, 
       for (int e = 0; e < P.epi_count; ++e) {
         const int k = P.epi_kind[e];
         if (k == EPI_RELU) y = fmaxf(y, 0.f);
+        else if (k == EPI_GELU) y = epi_gelu(y);
         else if (k == EPI_BIAS) y += bias[c0 + j];
         else y += __ldg(P.epi_ptr[e] + addr);
       }

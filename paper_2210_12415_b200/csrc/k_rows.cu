@@ -1,0 +1,352 @@
+// k_rows.cu — the BERT-encoder op-set extension on sm_100a (lf_rows.hpp):
+// Softmax / LayerNorm over the last logical dim (one warp per row, operands
+// through separable offset tables) and the per-head batched matmuls of
+// attention (SMEM-tiled CUDA-core kernels: at seq 128 the two of them are
+// 2 x 12.6 M MAC per layer, ~1.4% of the layer's GEMM work).
+// Semantics and reduction order follow lfgpu.h and the oracle
+// (oracle/lf_oracle.c lfo_softmax / lfo_layernorm / lfo_bmm_*).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "lf_pdl.hpp"
+#include "lf_rows.hpp"
+
+namespace lfg {
+
+namespace {
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+constexpr int kRowWarps = 8;
+
+// One warp per row; lane l holds columns l, l+32, ... in registers (rows up
+// to NC*32 long: NC is the instance's register budget, chosen on the host).
+template <int NC>
+__global__ void __launch_bounds__(32 * kRowWarps) rows_kernel(const RowsParams P) {
+  LFG_PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowWarps + (threadIdx.x >> 5);
+  if (r >= P.rows) return;
+  const float* x = P.x + __ldg(P.row_x + r);
+  const int64_t ry = __ldg(P.row_y + r);
+  float* y = P.y + ry;
+  __nv_bfloat16* yb = P.y_bf16 ? static_cast<__nv_bfloat16*>(P.y_bf16) + ry : nullptr;
+  const int d = P.d;
+  float v[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int j = lane + 32 * k;
+    v[k] = j < d ? __ldg(x + __ldg(P.col_x + j)) : 0.f;
+  }
+  if (P.op == ROWS_SOFTMAX) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+      if (lane + 32 * k < d) m = fmaxf(m, v[k]);
+    m = warp_max(m);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+      if (lane + 32 * k < d) {
+        v[k] = expf(v[k] - m);
+        s += v[k];
+      }
+    const float inv = 1.f / warp_sum(s);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int j = lane + 32 * k;
+      if (j < d) {
+        const int64_t o = __ldg(P.col_y + j);
+        y[o] = v[k] * inv;
+        if (P.y_bf16) yb[o] = __float2bfloat16_rn(v[k] * inv);
+      }
+    }
+  } else {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) s += v[k];  // zero-padded past d
+    const float mean = warp_sum(s) / static_cast<float>(d);
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+      if (lane + 32 * k < d) q += (v[k] - mean) * (v[k] - mean);
+    const float inv = rsqrtf(warp_sum(q) / static_cast<float>(d) + P.eps);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int j = lane + 32 * k;
+      if (j < d) {
+        const int64_t o = __ldg(P.col_y + j);
+        const float t = (v[k] - mean) * inv * __ldg(P.gb + __ldg(P.col_gb + j)) + __ldg(P.gb + __ldg(P.col_gb + d + j));
+        y[o] = t;
+        if (P.y_bf16) yb[o] = __float2bfloat16_rn(t);
+      }
+    }
+  }
+}
+
+// Long rows (LayerNorm over the hidden dim): one CTA of 256 threads per row,
+// EPT elements per thread; the row's column offsets are read coalesced once.
+template <int EPT>
+__global__ void __launch_bounds__(256) rows_cta_kernel(const RowsParams P) {
+  LFG_PDL_ENTRY();
+  __shared__ float red[2][8];
+  const int64_t r = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int d = P.d;
+  const float* x = P.x + __ldg(P.row_x + r);
+  const int64_t ry = __ldg(P.row_y + r);
+  float v[EPT];
+  int64_t oy[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int j = tid + 256 * k;
+    oy[k] = j < d ? __ldg(P.col_y + j) : 0;
+    v[k] = j < d ? __ldg(x + __ldg(P.col_x + j)) : 0.f;
+  }
+  auto block_sum = [&](float a, int slot) {
+    a = warp_sum(a);
+    if (lane == 0) red[slot][w] = a;
+    __syncthreads();
+    float t = lane < 8 ? red[slot][lane] : 0.f;
+    return warp_sum(t);
+  };
+  auto block_max = [&](float a, int slot) {
+    a = warp_max(a);
+    if (lane == 0) red[slot][w] = a;
+    __syncthreads();
+    float t = lane < 8 ? red[slot][lane] : -INFINITY;
+    return warp_max(t);
+  };
+  float* y = P.y + ry;
+  __nv_bfloat16* yb = P.y_bf16 ? static_cast<__nv_bfloat16*>(P.y_bf16) + ry : nullptr;
+  if (P.op == ROWS_SOFTMAX) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (tid + 256 * k < d) m = fmaxf(m, v[k]);
+    m = block_max(m, 0);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (tid + 256 * k < d) {
+        v[k] = expf(v[k] - m);
+        s += v[k];
+      }
+    const float inv = 1.f / block_sum(s, 1);
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (tid + 256 * k < d) {
+        y[oy[k]] = v[k] * inv;
+        if (yb) yb[oy[k]] = __float2bfloat16_rn(v[k] * inv);
+      }
+    return;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) s += v[k];
+  const float mean = block_sum(s, 0) / static_cast<float>(d);
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < EPT; ++k)
+    if (tid + 256 * k < d) q += (v[k] - mean) * (v[k] - mean);
+  const float inv = rsqrtf(block_sum(q, 1) / static_cast<float>(d) + P.eps);
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int j = tid + 256 * k;
+    if (j < d) {
+      const float t = (v[k] - mean) * inv * __ldg(P.gb + __ldg(P.col_gb + j)) + __ldg(P.gb + __ldg(P.col_gb + d + j));
+      y[oy[k]] = t;
+      if (yb) yb[oy[k]] = __float2bfloat16_rn(t);
+    }
+  }
+}
+
+constexpr int kTile = 32;
+constexpr int kMaxDh = 128;
+
+// QK: one CTA per (32 i x 32 j) tile of head h. The tile's row / column
+// offsets are staged in SMEM first (coalesced), so every operand element is
+// one load; q / k rows then live in SMEM.
+template <typename Acc>
+__global__ void __launch_bounds__(256) bmm_qk_kernel(const BmmParams P) {
+  LFG_PDL_ENTRY();
+  __shared__ float qs[kTile][kMaxDh + 1];
+  __shared__ float ks[kTile][kMaxDh + 1];
+  __shared__ int64_t qr[kTile], kr[kTile], qc[kMaxDh], kc[kMaxDh];
+  const int h = blockIdx.z, i0 = blockIdx.y * kTile, j0 = blockIdx.x * kTile;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int Dh = P.Dh;
+  const int t = threadIdx.x;
+  if (t < kTile) qr[t] = i0 + t < P.T ? __ldg(P.ta + P.a_off[0] + i0 + t) : 0;
+  else if (t < 2 * kTile) kr[t - kTile] = j0 + t - kTile < P.T2 ? __ldg(P.tb + P.b_off[0] + j0 + t - kTile) : 0;
+  if (t < Dh) {
+    qc[t] = __ldg(P.ta + P.a_off[1] + h * Dh + t);
+    kc[t] = __ldg(P.tb + P.b_off[1] + h * Dh + t);
+  }
+  __syncthreads();
+  {
+    // every thread's loads in flight together (a loop of load -> st.shared
+    // pairs would serialise one L2 round trip per element)
+    constexpr int kPer = kTile * kMaxDh / 256;
+    float qv[kPer], kv[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = t + 256 * u, r = e / Dh, c = e % Dh;
+      const bool in = e < kTile * Dh;
+      qv[u] = in && i0 + r < P.T ? __ldg(P.a + qr[r] + qc[c]) : 0.f;
+      kv[u] = in && j0 + r < P.T2 ? __ldg(P.b + kr[r] + kc[c]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = t + 256 * u, r = e / Dh, c = e % Dh;
+      if (e < kTile * Dh) {
+        qs[r][c] = qv[u];
+        ks[r][c] = kv[u];
+      }
+    }
+  }
+  __syncthreads();
+  Acc acc[4] = {0, 0, 0, 0};
+  for (int c = 0; c < Dh; ++c) {
+    const float kv = ks[tx][c];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] += static_cast<Acc>(qs[ty + 8 * k][c]) * kv;
+  }
+  const int j = j0 + tx;
+  const int64_t oj = j < P.T2 ? __ldg(P.to + P.o_off[2] + j) : 0;
+  const int64_t oh = __ldg(P.to + P.o_off[0] + h);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = i0 + ty + 8 * k;
+    if (i < P.T && j < P.T2) {
+      const int64_t o = oh + __ldg(P.to + P.o_off[1] + i) + oj;
+      P.out[o] = static_cast<float>(acc[k]);
+      if (P.out_bf16) static_cast<__nv_bfloat16*>(P.out_bf16)[o] = __float2bfloat16_rn(static_cast<float>(acc[k]));
+    }
+  }
+}
+
+// PV: one CTA per (32 i rows, half of the head's Dh columns, head h); p / v
+// staged 32 j at a time, their offsets staged in SMEM once.
+constexpr int kMaxT2 = 512;
+template <typename Acc>
+__global__ void __launch_bounds__(256) bmm_pv_kernel(const BmmParams P) {
+  LFG_PDL_ENTRY();
+  __shared__ float ps[kTile][kTile + 1];
+  __shared__ float vs[kTile][kMaxDh / 2 + 1];
+  __shared__ int64_t pj[kMaxT2], vr[kMaxT2], pi[kTile], vc[kMaxDh / 2];
+  const int h = blockIdx.y, i0 = blockIdx.x * kTile;
+  const int dh = P.Dh / 2, d0 = blockIdx.z * dh;  // this CTA's column half
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int t = threadIdx.x;
+  const int64_t ph = __ldg(P.ta + P.a_off[0] + h);
+  for (int e = t; e < P.T2; e += 256) {
+    pj[e] = __ldg(P.ta + P.a_off[2] + e);
+    vr[e] = __ldg(P.tb + P.b_off[0] + e);
+  }
+  if (t < kTile) pi[t] = i0 + t < P.T ? __ldg(P.ta + P.a_off[1] + i0 + t) : 0;
+  if (t < dh) vc[t] = __ldg(P.tb + P.b_off[1] + h * P.Dh + d0 + t);
+  const int nd = (dh + 31) / 32;
+  Acc acc[4][kMaxDh / 64];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int m = 0; m < kMaxDh / 64; ++m) acc[k][m] = 0;
+  for (int j0 = 0; j0 < P.T2; j0 += kTile) {
+    constexpr int kPp = kTile * kTile / 256, kPv = kTile * (kMaxDh / 2) / 256;
+    float pr[kPp], vv[kPv];  // this chunk's loads, all in flight together
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPp; ++u) {
+      const int e = t + 256 * u, r = e / kTile, c = e % kTile;
+      pr[u] = i0 + r < P.T && j0 + c < P.T2 ? __ldg(P.a + ph + pi[r] + pj[j0 + c]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kPv; ++u) {
+      const int e = t + 256 * u, r = e / dh, c = e % dh;
+      vv[u] = e < kTile * dh && j0 + r < P.T2 ? __ldg(P.b + vr[j0 + r] + vc[c]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kPp; ++u) {
+      const int e = t + 256 * u;
+      ps[e / kTile][e % kTile] = pr[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kPv; ++u) {
+      const int e = t + 256 * u;
+      if (e < kTile * dh) vs[e / dh][e % dh] = vv[u];
+    }
+    __syncthreads();
+    for (int jj = 0; jj < kTile; ++jj) {
+      float pv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pv[k] = ps[ty + 8 * k][jj];
+#pragma unroll
+      for (int m = 0; m < kMaxDh / 64; ++m)
+        if (m < nd) {
+          const float vv = vs[jj][tx + 32 * m];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[k][m] += static_cast<Acc>(pv[k]) * vv;
+        }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = i0 + ty + 8 * k;
+    if (i >= P.T) continue;
+    const int64_t oi = __ldg(P.to + P.o_off[0] + i);
+#pragma unroll
+    for (int m = 0; m < kMaxDh / 64; ++m) {
+      const int c = tx + 32 * m;
+      if (m < nd && c < dh) {
+        const int64_t o = oi + __ldg(P.to + P.o_off[1] + h * P.Dh + d0 + c);
+        P.out[o] = static_cast<float>(acc[k][m]);
+        if (P.out_bf16) static_cast<__nv_bfloat16*>(P.out_bf16)[o] = __float2bfloat16_rn(static_cast<float>(acc[k][m]));
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_rows(const RowsParams& P, cudaStream_t stream) {
+  if (P.rows == 0) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>((P.rows + kRowWarps - 1) / kRowWarps);
+  const dim3 g(blocks), b(32 * kRowWarps);
+  // Short rows: a warp each (8 rows per CTA); long rows: a CTA each, so the
+  // grid has enough CTAs to hide the gathers' latency.
+  if (P.d <= 128) return launch_pdl(rows_kernel<4>, g, b, 0, stream, P);
+  if (P.d <= 256) return launch_pdl(rows_kernel<8>, g, b, 0, stream, P);
+  const dim3 gr(static_cast<unsigned>(P.rows));
+  if (P.d <= 512) return launch_pdl(rows_cta_kernel<2>, gr, dim3(256), 0, stream, P);
+  if (P.d <= 1024) return launch_pdl(rows_cta_kernel<4>, gr, dim3(256), 0, stream, P);
+  if (P.d <= 2048) return launch_pdl(rows_cta_kernel<8>, gr, dim3(256), 0, stream, P);
+  return cudaErrorInvalidValue;  // the plan rejects longer rows
+}
+
+cudaError_t launch_bmm(const BmmParams& P, bool exact, cudaStream_t stream) {
+  if (P.Dh > kMaxDh || P.Dh < 1) return cudaErrorInvalidValue;
+  if (P.mode == 0) {
+    dim3 grid((P.T2 + kTile - 1) / kTile, (P.T + kTile - 1) / kTile, P.H);
+    return exact ? launch_pdl(bmm_qk_kernel<double>, grid, dim3(256), 0, stream, P)
+                 : launch_pdl(bmm_qk_kernel<float>, grid, dim3(256), 0, stream, P);
+  }
+  if (P.T2 > kMaxT2 || P.Dh % 2) return cudaErrorInvalidValue;
+  dim3 grid((P.T + kTile - 1) / kTile, P.H, 2);
+  return exact ? launch_pdl(bmm_pv_kernel<double>, grid, dim3(256), 0, stream, P)
+               : launch_pdl(bmm_pv_kernel<float>, grid, dim3(256), 0, stream, P);
+}
+
+}  // namespace lfg

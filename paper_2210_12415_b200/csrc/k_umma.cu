@@ -394,6 +394,14 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
           x[it].z = fmaxf(x[it].z, 0.0f);
           x[it].w = fmaxf(x[it].w, 0.0f);
         }
+      } else if (k == EPI_GELU) {
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          x[it].x = epi_gelu(x[it].x);
+          x[it].y = epi_gelu(x[it].y);
+          x[it].z = epi_gelu(x[it].z);
+          x[it].w = epi_gelu(x[it].w);
+        }
       } else if (k == EPI_BIAS) {
         const float* bp = ep + n_base + c;
         const float4 bb = c < cols ? make_float4(__ldg(bp), __ldg(bp + 1), __ldg(bp + 2), __ldg(bp + 3))
@@ -472,6 +480,7 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (k == EPI_RELU) y[j] = fmaxf(y[j], 0.0f);
+          else if (k == EPI_GELU) y[j] = epi_gelu(y[j]);
           else if (cv[j])
             y[j] += __ldg(ep + (k == EPI_BIAS ? static_cast<int64_t>(n_base + (P.bias_rows ? row : c0 + j0 + j))
                                               : a[j]));
@@ -857,6 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 if (kk == EPI_RELU) v[j] = fmaxf(v[j], 0.0f);
+                else if (kk == EPI_GELU) v[j] = epi_gelu(v[j]);
                 else
                   v[j] += __ldg(ep + (kk == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j)
                                                      : addr + (cs ? s_col[c0 + j] : c0 + j)));

@@ -18,7 +18,8 @@ enum GenOp : int32_t {
   GEN_DEP = 5,
   GEN_GMM = 6,
   GEN_MAXPOOL = 7,         // window max (KH = KW = window, stride V); b unused
-  GEN_GLOBAL_AVGPOOL = 8   // [N,C,H,W] -> [N,C]: sum over (h, w) / (H*W); b unused
+  GEN_GLOBAL_AVGPOOL = 8,  // [N,C,H,W] -> [N,C]: sum over (h, w) / (H*W); b unused
+  GEN_GELU = 9             // element-wise 0.5 x (1 + erf(x / sqrt 2))
 };
 
 // Element-wise node: out physical element f -> logical l (out_prog), then

@@ -1,0 +1,53 @@
+// lf_rows.hpp — the BERT-encoder op-set extension (lfgpu.h LFGPU_OP_SOFTMAX,
+// LAYERNORM, BMM_QK, BMM_PV): row reductions over the last logical dim and
+// the per-head batched matmuls of attention. Every operand is read and
+// written in its own physical layout through separable per-dim offset
+// tables (split / reorder layouts, e.g. the GMM output bricks), so no
+// layout conversion sits between these ops and the tcgen05 GEMMs.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lfg {
+
+enum RowsOp : int32_t { ROWS_SOFTMAX = 0, ROWS_LAYERNORM = 1 };
+
+struct RowsParams {
+  int32_t op = ROWS_SOFTMAX;
+  int32_t d = 0;        // row length (last logical dim)
+  int64_t rows = 0;     // product of the leading dims
+  float eps = 1e-12f;   // LayerNorm
+  const float* x = nullptr;
+  float* y = nullptr;
+  void* y_bf16 = nullptr;           // optional bf16 copy of y (tensor-core consumer), same layout
+  const float* gb = nullptr;        // LayerNorm [2, d]: gamma, beta
+  const int64_t* row_x = nullptr;   // rows: base offset of each row in x
+  const int64_t* row_y = nullptr;
+  const int64_t* col_x = nullptr;   // d: offset of column j
+  const int64_t* col_y = nullptr;
+  const int64_t* col_gb = nullptr;  // 2 x d: gamma then beta offsets in gb
+};
+
+// QK: s[h,i,j] = sum_d q[i, h*Dh+d] k[j, h*Dh+d]
+// PV: o[i, h*Dh+d] = sum_j p[h,i,j] v[j, h*Dh+d]
+struct BmmParams {
+  int32_t mode = 0;  // 0 QK, 1 PV
+  int32_t H = 0, T = 0, T2 = 0, Dh = 0;
+  const float* a = nullptr;  // q (QK) / p (PV)
+  const float* b = nullptr;  // k (QK) / v (PV)
+  float* out = nullptr;      // s (QK) / o (PV)
+  void* out_bf16 = nullptr;  // optional bf16 copy of out, same layout
+  // separable tables: rank-2 operands [rows, H*Dh] use 2 tables, rank-3
+  // [H, T, T2] use 3 (concatenated; *_off = start of each dim's table)
+  const int64_t* ta = nullptr;
+  const int64_t* tb = nullptr;
+  const int64_t* to = nullptr;
+  int64_t a_off[3] = {}, b_off[3] = {}, o_off[3] = {};
+};
+
+cudaError_t launch_rows(const RowsParams& P, cudaStream_t stream);
+cudaError_t launch_bmm(const BmmParams& P, bool exact, cudaStream_t stream);
+
+}  // namespace lfg

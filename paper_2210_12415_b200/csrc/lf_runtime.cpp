@@ -29,6 +29,7 @@
 #include <mutex>
 #include <vector>
 
+#include "lf_rows.hpp"
 #include "lf_core.hpp"
 #include "lf_direct.hpp"
 #include "lf_generic.hpp"
@@ -299,6 +300,34 @@ int64_t* tables_for(lfgpu_plan* P, const PTensor& t, std::vector<int64_t>* off) 
   return upload(P->keep, tab.data(), tab.size());
 }
 
+bool same_extents(const std::vector<Dim>& a, const std::vector<Dim>& b) {
+  if (a.size() != b.size()) return false;
+  for (size_t i = 0; i < a.size(); ++i)
+    if (a[i].extent != b[i].extent) return false;
+  return true;
+}
+
+// Row / column offsets of a separable layout seen as [rows, last dim]: the
+// row base of every multi-index of the leading dims (row-major order) and
+// the offset of every last-dim index.
+void row_col_offsets(const PTensor& t, std::vector<int64_t>* rows, std::vector<int64_t>* cols) {
+  std::vector<int64_t> tab, off;
+  if (!separable_tables(t.logical, t.seq, &tab, &off))
+    fail(LFGPU_EUNSUPPORTED, "layout of '" + t.id + "' is not separable per logical dim: " + seq_str(t.seq));
+  const size_t r = t.logical.size();
+  const int64_t d = t.logical.back().extent;
+  cols->assign(d, 0);
+  for (int64_t j = 0; j < d; ++j) (*cols)[j] = tab[off[r - 1] + j];
+  rows->assign(1, 0);
+  for (size_t k = 0; k + 1 < r; ++k) {
+    std::vector<int64_t> next;
+    next.reserve(rows->size() * t.logical[k].extent);
+    for (int64_t base : *rows)
+      for (int64_t i = 0; i < t.logical[k].extent; ++i) next.push_back(base + tab[off[k] + i]);
+    rows->swap(next);
+  }
+}
+
 IxProgram* out_program(lfgpu_plan* P, const PTensor& t) {
   CopySpec spec;
   spec.lmap = identity_map(t.logical);
@@ -438,14 +467,17 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   for (size_t k = 0; k < P->order.size(); ++k) pos[P->order[k]] = static_cast<int>(k);
   // Epilogue fusion of the single-consumer element-wise chain after node ni
   // (lower.cpp:566-608) while every member keeps the output's physical layout.
-  auto fuse_chain = [&](int ni, const PTensor& Cc) {
+  // GELU fuses only into the tcgen05 epilogues (tc = true).
+  auto fuse_chain = [&](int ni, const PTensor& Cc, bool tc = false) {
     std::vector<EpiOp> epi;
     int cur = P->nodes[ni].output;
     while (true) {
       const auto& cons = P->t[cur].consumers;
       if (cons.size() != 1) break;
       const auto& c = P->nodes[cons[0]];
-      if (c.kind != LFGPU_OP_RELU && c.kind != LFGPU_OP_BIASADD && c.kind != LFGPU_OP_EWADD) break;
+      if (c.kind != LFGPU_OP_RELU && c.kind != LFGPU_OP_BIASADD && c.kind != LFGPU_OP_EWADD &&
+          !(tc && c.kind == LFGPU_OP_GELU))
+        break;
       if (c.inputs[0] != cur) break;
       if (!seq_equal(P->t[c.output].seq, Cc.seq)) break;
       if (c.kind == LFGPU_OP_EWADD && !seq_equal(P->t[c.inputs[1]].seq, Cc.seq)) break;
@@ -454,13 +486,17 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
       if (c.kind == LFGPU_OP_RELU && !epi.empty() && epi.back().kind == EPI_RELU) break;
       // The epilogue reads a residual / bias when the contraction runs: its
       // producer must already have run (e.g. a ResNet downsample branch).
-      if (c.kind != LFGPU_OP_RELU) {
+      const bool unary = c.kind == LFGPU_OP_RELU || c.kind == LFGPU_OP_GELU;
+      if (!unary) {
         const int pr = P->t[c.inputs[1]].producer;
         if (pr >= 0 && pos[pr] > pos[ni]) break;
       }
       EpiOp e;
-      e.kind = c.kind == LFGPU_OP_RELU ? EPI_RELU : c.kind == LFGPU_OP_BIASADD ? EPI_BIAS : EPI_RESIDUAL;
-      e.tensor = c.kind == LFGPU_OP_RELU ? -1 : c.inputs[1];
+      e.kind = c.kind == LFGPU_OP_RELU ? EPI_RELU
+               : c.kind == LFGPU_OP_GELU ? EPI_GELU
+               : c.kind == LFGPU_OP_BIASADD ? EPI_BIAS
+                                            : EPI_RESIDUAL;
+      e.tensor = unary ? -1 : c.inputs[1];
       e.out_tensor = c.output;
       epi.push_back(e);
       fused_away.insert(cons[0]);
@@ -542,7 +578,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
         }
         if (ic) {
           if (s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL)) {
-            std::vector<EpiOp> epi = fuse_chain(ni, Cc);
+            std::vector<EpiOp> epi = fuse_chain(ni, Cc, true);
             for (const auto& e : epi) ug.epi[ug.epi_count++] = e;
           }
           im2col[ni] = ug;
@@ -566,7 +602,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
       continue;
     }
     if (s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL)) {
-      std::vector<EpiOp> epi = fuse_chain(ni, Cc);
+      std::vector<EpiOp> epi = fuse_chain(ni, Cc, true);
       for (const auto& e : epi) up.epi[up.epi_count++] = e;
     }
     umma[ni] = up;
@@ -1001,6 +1037,134 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           P->bytes += A.numel * elem_size(A.elem) + B.numel * elem_size(B.elem) +
                       out.numel * elem_size(out.elem);
         }
+        break;
+      }
+      case LFGPU_OP_GELU: {
+        // Element-wise (fused into the producing contraction's epilogue when
+        // the schedule asks for it; here the stand-alone node).
+        GenEltwise G;
+        G.op = GEN_GELU;
+        G.rank = static_cast<int32_t>(out.logical.size());
+        G.n = out.numel;
+        const PTensor& x = P->t[n.inputs[0]];
+        if (!x.d) fail(LFGPU_EUNSUPPORTED, "element-wise read of a bf16-only tensor");
+        if (out.dtype != LFGPU_DTYPE_F32) fail(LFGPU_EUNSUPPORTED, "GELU is defined for f32 tensors only");
+        std::vector<int64_t> off;
+        G.tab0 = tables_for(P, x, &off);
+        for (size_t j = 0; j < off.size(); ++j) G.tab_off[j] = off[j];
+        G.in0 = x.d;
+        IxProgram* prog = out_program(P, out);
+        int elem = out.elem;
+        void* dst = out.d;
+        step.kernel = "gen_eltwise";
+        step.run = [prog, G, elem, dst, d_err](cudaStream_t s) {
+          return launch_gen_eltwise(prog, G, elem, dst, d_err, s);
+        };
+        P->bytes += x.numel * elem_size(x.elem) + out.numel * elem_size(out.elem);
+        break;
+      }
+      case LFGPU_OP_SOFTMAX:
+      case LFGPU_OP_LAYERNORM: {
+        // Row reductions over the last logical dim (k_rows.cu), every operand
+        // through its separable offset tables.
+        const PTensor& X = P->t[n.inputs[0]];
+        const char* nm = n.kind == LFGPU_OP_SOFTMAX ? "Softmax" : "LayerNorm";
+        if (out.dtype != LFGPU_DTYPE_F32 || X.dtype != LFGPU_DTYPE_F32)
+          fail(LFGPU_EUNSUPPORTED, std::string(nm) + " is defined for f32 tensors only");
+        if (!same_extents(X.logical, out.logical))
+          fail(LFGPU_EINVAL, std::string(nm) + " output shape mismatch for '" + out.id + "'");
+        const int64_t d = out.logical.back().extent;
+        if (d > 2048) fail(LFGPU_EUNSUPPORTED, std::string(nm) + " rows longer than 2048");
+        if (!X.d) fail(LFGPU_EUNSUPPORTED, "row read of a bf16-only tensor");
+        RowsParams R;
+        R.op = n.kind == LFGPU_OP_SOFTMAX ? ROWS_SOFTMAX : ROWS_LAYERNORM;
+        R.d = static_cast<int32_t>(d);
+        R.rows = out.numel / std::max<int64_t>(d, 1);
+        std::vector<int64_t> rx, cx, ry, cy;
+        row_col_offsets(X, &rx, &cx);
+        row_col_offsets(out, &ry, &cy);
+        R.row_x = upload(P->keep, rx.data(), rx.size());
+        R.col_x = upload(P->keep, cx.data(), cx.size());
+        R.row_y = upload(P->keep, ry.data(), ry.size());
+        R.col_y = upload(P->keep, cy.data(), cy.size());
+        R.x = static_cast<const float*>(X.d);
+        R.y = static_cast<float*>(out.d);
+        if (out.d_bf16) {  // a tensor-core consumer's operand, written in the same pass
+          R.y_bf16 = out.d_bf16;
+          out.shadow_by_producer = true;
+        }
+        if (n.kind == LFGPU_OP_LAYERNORM) {
+          const PTensor& GB = P->t[n.inputs[1]];
+          if (GB.logical.size() != 2 || GB.logical[0].extent != 2 || GB.logical[1].extent != d)
+            fail(LFGPU_EINVAL, "LayerNorm parameters must be [2, " + std::to_string(d) + "] (gamma; beta)");
+          if (!GB.d) fail(LFGPU_EUNSUPPORTED, "LayerNorm parameters must be f32");
+          std::vector<int64_t> rg, cg;
+          row_col_offsets(GB, &rg, &cg);
+          std::vector<int64_t> cgb(2 * d);
+          for (int64_t j = 0; j < d; ++j) {
+            cgb[j] = rg[0] + cg[j];
+            cgb[d + j] = rg[1] + cg[j];
+          }
+          R.col_gb = upload(P->keep, cgb.data(), cgb.size());
+          R.gb = static_cast<const float*>(GB.d);
+          R.eps = static_cast<float>(std::pow(10.0, -static_cast<double>(n.eps_exp)));
+          P->bytes += GB.numel * 4;
+        }
+        step.kernel = n.kind == LFGPU_OP_SOFTMAX ? "rows_softmax" : "rows_layernorm";
+        step.run = [R](cudaStream_t s) { return launch_rows(R, s); };
+        P->bytes += X.numel * 4 + out.numel * 4;
+        break;
+      }
+      case LFGPU_OP_BMM_QK:
+      case LFGPU_OP_BMM_PV: {
+        const PTensor& A = P->t[n.inputs[0]];
+        const PTensor& B = P->t[n.inputs[1]];
+        const int64_t H = n.heads;
+        if (H < 1) fail(LFGPU_EINVAL, "batched matmul needs heads >= 1");
+        if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "batched matmul reads f32 operands");
+        if (out.dtype != LFGPU_DTYPE_F32) fail(LFGPU_EUNSUPPORTED, "batched matmul is defined for f32 only");
+        BmmParams M;
+        M.mode = n.kind == LFGPU_OP_BMM_QK ? 0 : 1;
+        M.H = static_cast<int32_t>(H);
+        if (n.kind == LFGPU_OP_BMM_QK) {  // q [T, H*Dh], k [T2, H*Dh] -> s [H, T, T2]
+          if (A.logical.size() != 2 || B.logical.size() != 2 || out.logical.size() != 3 ||
+              A.logical[1].extent != B.logical[1].extent || A.logical[1].extent % H ||
+              out.logical[0].extent != H || out.logical[1].extent != A.logical[0].extent ||
+              out.logical[2].extent != B.logical[0].extent)
+            fail(LFGPU_EINVAL, "BmmQK shapes: q [T, H*Dh], k [T2, H*Dh] -> s [H, T, T2]");
+          M.T = static_cast<int32_t>(A.logical[0].extent);
+          M.T2 = static_cast<int32_t>(B.logical[0].extent);
+          M.Dh = static_cast<int32_t>(A.logical[1].extent / H);
+        } else {  // p [H, T, T2], v [T2, H*Dh] -> o [T, H*Dh]
+          if (A.logical.size() != 3 || B.logical.size() != 2 || out.logical.size() != 2 ||
+              A.logical[0].extent != H || A.logical[2].extent != B.logical[0].extent ||
+              B.logical[1].extent % H || out.logical[0].extent != A.logical[1].extent ||
+              out.logical[1].extent != B.logical[1].extent)
+            fail(LFGPU_EINVAL, "BmmPV shapes: p [H, T, T2], v [T2, H*Dh] -> o [T, H*Dh]");
+          M.T = static_cast<int32_t>(A.logical[1].extent);
+          M.T2 = static_cast<int32_t>(A.logical[2].extent);
+          M.Dh = static_cast<int32_t>(B.logical[1].extent / H);
+        }
+        if (M.Dh > 128 || M.Dh % 2) fail(LFGPU_EUNSUPPORTED, "batched matmul head dim must be even and <= 128");
+        if (M.mode == 1 && M.T2 > 512) fail(LFGPU_EUNSUPPORTED, "BmmPV reduction length > 512");
+        std::vector<int64_t> oa, ob, oo;
+        M.ta = tables_for(P, A, &oa);
+        M.tb = tables_for(P, B, &ob);
+        M.to = tables_for(P, out, &oo);
+        for (size_t j = 0; j < oa.size() && j < 3; ++j) M.a_off[j] = oa[j];
+        for (size_t j = 0; j < ob.size() && j < 3; ++j) M.b_off[j] = ob[j];
+        for (size_t j = 0; j < oo.size() && j < 3; ++j) M.o_off[j] = oo[j];
+        M.a = static_cast<const float*>(A.d);
+        M.b = static_cast<const float*>(B.d);
+        M.out = static_cast<float*>(out.d);
+        if (out.d_bf16) {
+          M.out_bf16 = out.d_bf16;
+          out.shadow_by_producer = true;
+        }
+        step.kernel = n.kind == LFGPU_OP_BMM_QK ? "bmm_qk" : "bmm_pv";
+        step.run = [M, exact](cudaStream_t s) { return launch_bmm(M, exact, s); };
+        P->flops += 2 * static_cast<int64_t>(M.H) * M.T * M.T2 * M.Dh;
+        P->bytes += A.numel * 4 + B.numel * 4 + out.numel * 4;
         break;
       }
       case LFGPU_OP_MAXPOOL:

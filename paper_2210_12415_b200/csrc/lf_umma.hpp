@@ -28,7 +28,11 @@ struct PairPlan;    // lf_pair.hpp
 struct PairLaunch;
 
 enum { UMMA_GEMM = 0, UMMA_CONV = 1 };
-enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_RELU = 2, EPI_RESIDUAL = 3 };
+enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_RELU = 2, EPI_RESIDUAL = 3, EPI_GELU = 4 };
+#ifdef __CUDACC__
+// GELU as lfgpu.h defines it (exact erf form), in fp32 in the epilogue.
+__device__ __forceinline__ float epi_gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+#endif
 constexpr int kMaxEpi = 4;
 constexpr int kMaxBoxes = 4;
 constexpr int kMaxTaps = 32;  // taps of the halo C2D path (KH*KW)

@@ -76,6 +76,25 @@ def reference(g, ins, tc_nodes=frozenset(), emulate=False):
             r = F.max_pool2d(a[0], nd.attr("window", 1), nd.attr("stride", 1))
         elif nd.kind == ir.GLOBAL_AVGPOOL:
             r = rf(a[0].mean(dim=(2, 3)))
+        elif nd.kind == ir.GELU:
+            r = rf(0.5 * a[0] * (1.0 + torch.special.erf(a[0] / math.sqrt(2.0))))
+        elif nd.kind == ir.SOFTMAX:
+            r = rf(torch.softmax(a[0], dim=-1))
+        elif nd.kind == ir.LAYERNORM:
+            x = a[0]
+            mu = x.mean(dim=-1, keepdim=True)
+            var = ((x - mu) ** 2).mean(dim=-1, keepdim=True)
+            eps = 10.0 ** -nd.attr("eps_exp", 12)
+            r = rf((x - mu) / torch.sqrt(var + eps) * a[1][0] + a[1][1])
+        elif nd.kind == ir.BMM_QK:
+            H = nd.attr("heads", 1)
+            q, k = a[0], a[1]
+            r = rf(torch.einsum("ihd,jhd->hij", q.view(q.shape[0], H, -1), k.view(k.shape[0], H, -1)))
+        elif nd.kind == ir.BMM_PV:
+            H = nd.attr("heads", 1)
+            pr, vv = a[0], a[1]
+            o = torch.einsum("hij,jhd->ihd", pr, vv.view(vv.shape[0], H, -1))
+            r = rf(o.reshape(o.shape[0], -1))
         else:
             raise ValueError(nd.kind)
         v[nd.output] = r
@@ -111,6 +130,49 @@ def make_bert_inputs(g, gen):
         else:
             out[t.id] = k64(t.extents, gen)
     return out
+
+
+def make_encoder_inputs(g, gen, head_dim=64):
+    """BERT encoder inputs: k/64 activations, weights scaled by a power of
+    two ~ 1/sqrt(fan_in), the query projection also by 1/sqrt(head_dim) (a
+    power of two for Dh = 64, so bf16-exact), LayerNorm gamma = 1 + k/512,
+    beta = k/512."""
+    out = {}
+    qs = 2.0 ** -round(math.log2(math.sqrt(head_dim)))
+    for t in g.tensors:
+        if t.role not in (ir.INPUT, ir.CONSTANT):
+            continue
+        q = qs if "_q_" in t.id else 1.0
+        if t.id.endswith("_w"):
+            out[t.id] = k64(t.extents, gen, q * 2.0 ** -round(math.log2(math.sqrt(t.extents[0]))))
+        elif t.id.endswith("_b"):
+            out[t.id] = k64(t.extents, gen, q / 8)
+        elif t.id.endswith("_gb"):
+            gb = k64(t.extents, gen, 1.0 / 8)
+            gb[0] += 1.0
+            out[t.id] = gb
+        else:
+            out[t.id] = k64(t.extents, gen)
+    return out
+
+
+def build_encoder(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH, seq=128, hidden=768, heads=12,
+                  ffn=3072):
+    """cfg5 as a full BERT-base encoder (workloads.bert_encoder): every GMM
+    on tcgen05 in GMM brick layouts (m_t = seq, k_t = n_t = t) with its
+    BiasAdd / residual EwAdd / GELU fused into the epilogue; attention
+    (BmmQK, Softmax, BmmPV) and LayerNorm read and write those bricks
+    through separable offset tables."""
+    g, gmms = workloads.bert_encoder(layers, seq, hidden, heads, ffn)
+    seqs, scheds = {}, []
+    for ni in gmms:
+        nd = g.nodes[ni]
+        K = g.tensor(nd.inputs[0]).extents[1]
+        N = g.tensor(nd.output).extents[1]
+        seqs.update(runtime.decode_layout(g, ni, [seq, min(t, K), min(t, N)]))
+        scheds.append(runtime.sched(ni, tile_last=min(t, N), order=order, fuse=1))
+    seqs = workloads.propagate_elementwise(g, seqs)
+    return g, gmms, runtime.Plan(g, seqs, scheds, flags, ctx=ctx)
 
 
 def build_bert(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH):

@@ -19,18 +19,22 @@ C2D, DEP, GMM, PADDING, RELU, BIASADD, EWADD, LAYOUT_CONVERT = (
     _abi.LAYOUT_CONVERT)
 # Op-set extension: the pools ResNet-18 needs.
 MAXPOOL, GLOBAL_AVGPOOL = _abi.MAXPOOL, _abi.GLOBAL_AVGPOOL
+# ... and the rest of a BERT encoder (lfgpu.h documents each op's semantics).
+GELU, SOFTMAX, LAYERNORM, BMM_QK, BMM_PV = (_abi.GELU, _abi.SOFTMAX, _abi.LAYERNORM,
+                                            _abi.BMM_QK, _abi.BMM_PV)
 
 OP_NAMES = {C2D: "C2D", DEP: "DEP", GMM: "GMM", PADDING: "Padding", RELU: "ReLU",
             BIASADD: "BiasAdd", EWADD: "EwAdd", LAYOUT_CONVERT: "LayoutConvert",
-            MAXPOOL: "MaxPool", GLOBAL_AVGPOOL: "GlobalAvgPool"}
+            MAXPOOL: "MaxPool", GLOBAL_AVGPOOL: "GlobalAvgPool", GELU: "GELU",
+            SOFTMAX: "Softmax", LAYERNORM: "LayerNorm", BMM_QK: "BmmQK", BMM_PV: "BmmPV"}
 
 
 def is_complex_op(k):  # ir.cpp:26-28
     return k in (C2D, DEP, GMM)
 
 
-def is_elementwise_op(k):  # ir.cpp:30-32
-    return k in (RELU, BIASADD, EWADD)
+def is_elementwise_op(k):  # ir.cpp:30-32 (+ GELU, fused into epilogues like ReLU)
+    return k in (RELU, BIASADD, EWADD, GELU)
 
 
 @dataclass
@@ -110,6 +114,10 @@ class Graph:
                 attrs["stride"] = nd.stride
             if nd.kind == MAXPOOL:
                 attrs["window"] = nd.window
+            if nd.kind in (BMM_QK, BMM_PV):
+                attrs["heads"] = nd.heads
+            if nd.kind == LAYERNORM:
+                attrs["eps_exp"] = nd.eps_exp
             if nd.kind == PADDING:
                 attrs["pad"] = nd.pad
             g.nodes.append(OperatorNode(nd.kind,
@@ -151,6 +159,8 @@ class CGraph:
             d.stride = int(n.attr("stride", 1))
             d.pad = int(n.attr("pad", 0))
             d.window = int(n.attr("window", 0))
+            d.heads = int(n.attr("heads", 0))
+            d.eps_exp = int(n.attr("eps_exp", 12 if n.kind == LAYERNORM else 0))
         items = [(k, v) for k, v in seqs.items() if v]
         self.prim_arrays = []
         self.seqs = (_abi.Seq * max(1, len(items)))()

@@ -106,6 +106,62 @@ def bert_chain(layers=12, seq=128, hidden=768, ffn=3072, qkv=2304):
 BERT_FLOPS_PER_LAYER = 2.0 * 128 * (768 * 2304 + 768 * 768 + 768 * 3072 + 3072 * 768)
 
 
+def bert_encoder(layers=12, seq=128, hidden=768, heads=12, ffn=3072):
+    """cfg5 as a real BERT-base encoder (post-LN, as in BERT) on the op-set
+    extension (lfgpu.h: GELU, Softmax, LayerNorm, BmmQK, BmmPV). Per layer,
+    on h[seq, hidden]:
+      q, k, v = GMM(h, W{q,k,v}) + b{q,k,v}  (Wq, bq carry the 1/sqrt(Dh)
+                                               attention scale)
+      p       = Softmax(BmmQK(q, k))          [heads, seq, seq]
+      c       = BmmPV(p, v)                   [seq, hidden]
+      h1      = LayerNorm(GMM(c, Wo) + bo + h)
+      h'      = LayerNorm(GELU(GMM(h1, W1) + b1) @ W2 + b2 + h1)
+    Returns (graph, gmm node indices)."""
+    b = Builder()
+    I, C, O = ir.INPUT, ir.CONSTANT, ir.OUTPUT
+    gmms = []
+
+    def mat(tid, m, n, role=ir.INTERMEDIATE):
+        return b.t(tid, [("M", m), ("N", n)], role)
+
+    def linear(name, x, k, n, out_id=None):
+        w = b.t(f"{name}_w", [("K", k), ("N", n)], C)
+        bias = b.t(f"{name}_b", [("N", n)], C)
+        y = mat(f"{name}_y", seq, n)
+        b.op(ir.GMM, [x, w], y)
+        gmms.append(len(b.g.nodes) - 1)
+        return b.op(ir.BIASADD, [y, bias], mat(out_id or f"{name}_yb", seq, n))
+
+    def layernorm(name, x, out_id, role=ir.INTERMEDIATE):
+        gb = b.t(f"{name}_gb", [("P", 2), ("N", hidden)], C)
+        return b.op(ir.LAYERNORM, [x, gb], mat(out_id, seq, hidden, role), eps_exp=12)
+
+    h = mat("h0", seq, hidden, I)
+    for l in range(layers):
+        last = l == layers - 1
+        q = linear(f"l{l}_q", h, hidden, hidden)
+        k = linear(f"l{l}_k", h, hidden, hidden)
+        v = linear(f"l{l}_v", h, hidden, hidden)
+        s_ = b.op(ir.BMM_QK, [q, k], b.t(f"l{l}_s", [("H", heads), ("M", seq), ("T", seq)]), heads=heads)
+        p_ = b.op(ir.SOFTMAX, [s_], b.t(f"l{l}_p", [("H", heads), ("M", seq), ("T", seq)]))
+        c = b.op(ir.BMM_PV, [p_, v], mat(f"l{l}_c", seq, hidden), heads=heads)
+        ao = linear(f"l{l}_ao", c, hidden, hidden)
+        a = b.op(ir.EWADD, [ao, h], mat(f"l{l}_a", seq, hidden))
+        h1 = layernorm(f"l{l}_ln1", a, f"l{l}_h1")
+        f1 = linear(f"l{l}_f1", h1, hidden, ffn)
+        f = b.op(ir.GELU, [f1], mat(f"l{l}_f", seq, ffn))
+        f2 = linear(f"l{l}_f2", f, ffn, hidden)
+        o = b.op(ir.EWADD, [f2, h1], mat(f"l{l}_o", seq, hidden))
+        h = layernorm(f"l{l}_ln2", o, "out" if last else f"l{l + 1}_h", O if last else ir.INTERMEDIATE)
+    return b.g, gmms
+
+
+def bert_encoder_flops(layers=12, seq=128, hidden=768, heads=12, ffn=3072):
+    gemm = 2.0 * seq * (4 * hidden * hidden + 2 * hidden * ffn)
+    attn = 2.0 * 2 * seq * seq * hidden  # BmmQK + BmmPV over all heads
+    return layers * (gemm + attn)
+
+
 # ---------------------------------------------------------------------------
 # cfg4: ResNet-18 inference graph (BatchNorm folded into the conv bias).
 

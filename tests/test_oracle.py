@@ -222,3 +222,49 @@ def test_oracle_matches_reference_planner_graphs(golden):
             assert O.fnv1a(bufs[g.tensor_index(tid)]) == st["fnv"], (c["name"], tid)
             n += 1
     assert n >= 10
+
+
+# ---- BERT-encoder op-set extension (lfgpu.h LFGPU_OP_GELU .. BMM_PV): the
+# reference has no such ops (ir.hpp:42), so the oracle's restatement is
+# checked against an independent numpy formulation of lfgpu.h's semantics.
+def _run_oracle(g, seed=5):
+    bufs = O.random_inputs(g, seed)
+    O.reference_eval(g, bufs)
+    return {t.id: bufs[i] for i, t in enumerate(g.tensors)}
+
+
+def _graph(tensors, nodes):
+    g = ir.Graph()
+    g.tensors = [ir.TensorDecl(tid, dims, role) for tid, dims, role in tensors]
+    g.nodes = [ir.OperatorNode(*n) for n in nodes]
+    return g
+
+
+def test_oracle_encoder_ops_match_numpy():
+    import math
+    T, H, Dh = 6, 2, 4
+    D = H * Dh
+    g = _graph([("q", [("M", T), ("N", D)], ir.INPUT), ("k", [("M", T), ("N", D)], ir.INPUT),
+                ("v", [("M", T), ("N", D)], ir.INPUT), ("gb", [("P", 2), ("N", D)], ir.CONSTANT),
+                ("s", [("H", H), ("M", T), ("T", T)], ir.INTERMEDIATE),
+                ("p", [("H", H), ("M", T), ("T", T)], ir.INTERMEDIATE),
+                ("c", [("M", T), ("N", D)], ir.INTERMEDIATE), ("n", [("M", T), ("N", D)], ir.INTERMEDIATE),
+                ("y", [("M", T), ("N", D)], ir.OUTPUT)],
+               [(ir.BMM_QK, ["q", "k"], "s", {"heads": H}), (ir.SOFTMAX, ["s"], "p"),
+                (ir.BMM_PV, ["p", "v"], "c", {"heads": H}), (ir.LAYERNORM, ["c", "gb"], "n", {"eps_exp": 5}),
+                (ir.GELU, ["n"], "y")])
+    b = _run_oracle(g)
+    q, k, v = (b[x].reshape(T, H, Dh) for x in "qkv")
+    s = np.einsum("ihd,jhd->hij", q, k)
+    assert np.allclose(b["s"].reshape(H, T, T), s, rtol=1e-13, atol=1e-13)
+    e = np.exp(s - s.max(-1, keepdims=True))
+    p = e / e.sum(-1, keepdims=True)
+    assert np.allclose(b["p"].reshape(H, T, T), p, rtol=1e-13, atol=1e-13)
+    c = np.einsum("hij,jhd->ihd", p, v).reshape(T, D)
+    assert np.allclose(b["c"].reshape(T, D), c, rtol=1e-13, atol=1e-13)
+    gb = b["gb"].reshape(2, D)
+    mu, var = c.mean(-1, keepdims=True), c.var(-1, keepdims=True)
+    n = (c - mu) / np.sqrt(var + 1e-5) * gb[0] + gb[1]
+    assert np.allclose(b["n"].reshape(T, D), n, rtol=1e-12, atol=1e-12)
+    y = 0.5 * n * (1.0 + np.vectorize(math.erf)(n / math.sqrt(2.0)))
+    assert np.allclose(b["y"].reshape(T, D), y, rtol=1e-12, atol=1e-12)
