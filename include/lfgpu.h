@@ -366,6 +366,12 @@ int lfgpu_plan_node_kernel(lfgpu_plan* plan, int32_t node, char* buf, int32_t ca
 int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t flush_l2,
                        lfgpu_counters* out);
 
+/* lf::random_inputs (interp.cpp:487-503), bit-identical (same libstdc++
+ * mt19937_64 and distributions): fills bufs[t] (numel doubles, logical
+ * row-major) for every Input/Constant tensor t in declaration order;
+ * other entries may be NULL. Host-only (no device work). */
+int lfgpu_random_inputs(const lfgpu_graph* g, uint64_t seed, double* const* bufs);
+
 /* One-call interpret: lf::interpret(lower(g, seqs, sched), inputs)
  * (interp.cpp:424-470). host_bufs has one pointer per tensor (declaration
  * order): Input/Constant entries are read (logical doubles), node-output

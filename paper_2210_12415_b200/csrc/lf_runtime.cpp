@@ -23,6 +23,7 @@
 #include <map>
 #include <memory>
 #include <set>
+#include <random>
 #include <string>
 #include <thread>
 #include <condition_variable>
@@ -1779,6 +1780,31 @@ int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t f
     out->min_us = us.front();
     out->runs_per_sample = K;
     out->resolution_us = 1.024 / K;
+  });
+}
+
+int lfgpu_random_inputs(const lfgpu_graph* g, uint64_t seed, double* const* bufs) {
+  // lf::random_inputs (interp.cpp:487-503) with the same standard-library
+  // engine and distributions, so the values are the reference's bit for bit:
+  // one mt19937_64 stream over the Input/Constant tensors in declaration
+  // order; floats U(-1, 1) rounded to k/64, int32 U{-4..4}.
+  return guarded([&] {
+    std::mt19937_64 rng(seed);
+    for (int t = 0; t < g->ntensors; ++t) {
+      const lfgpu_tensor& td = g->tensors[t];
+      if (td.role != LFGPU_ROLE_INPUT && td.role != LFGPU_ROLE_CONSTANT) continue;
+      if (!bufs[t]) fail(LFGPU_EINVAL, std::string("missing buffer for tensor '") + td.id + "'");
+      int64_t n = 1;
+      for (int d = 0; d < td.rank; ++d) n *= td.dims[d].extent;
+      double* b = bufs[t];
+      if (td.dtype == LFGPU_DTYPE_I32) {
+        std::uniform_int_distribution<int> dist(-4, 4);
+        for (int64_t i = 0; i < n; ++i) b[i] = dist(rng);
+      } else {
+        std::uniform_real_distribution<double> dist(-1.0, 1.0);
+        for (int64_t i = 0; i < n; ++i) b[i] = std::round(dist(rng) * 64.0) / 64.0;
+      }
+    }
   });
 }
 

@@ -29,7 +29,7 @@ EXPORTS = [
     "lfgpu_plan_set_input_device_async",
     "lfgpu_plan_run", "lfgpu_plan_run_on", "lfgpu_plan_get_output", "lfgpu_plan_tensor_buffer", "lfgpu_plan_stream",
     "lfgpu_plan_info", "lfgpu_plan_node_kernel", "lfgpu_plan_measure", "lfgpu_interpret",
-    "lfgpu_debug_umma_trace", "lfgpu_materialize_host",
+    "lfgpu_debug_umma_trace", "lfgpu_materialize_host", "lfgpu_random_inputs",
 ]
 
 
@@ -81,6 +81,7 @@ def lib():
         L.lfgpu_ctx_create.argtypes = [C.c_int, P(C.c_void_p)]
         L.lfgpu_ctx_destroy.argtypes = [C.c_void_p]
         L.lfgpu_ctx_launch_count.argtypes = [C.c_void_p, P(C.c_int64)]
+        L.lfgpu_random_inputs.argtypes = [P(_abi.GraphDesc), C.c_uint64, P(P(C.c_double))]
         L.lfgpu_interpret.argtypes = [C.c_void_p, P(_abi.GraphDesc), C.c_int32, P(_abi.Sched),
                                       C.c_int32, P(P(C.c_double))]
         L.lfgpu_convert_kind.argtypes = [C.c_int32, P(_abi.Dim), C.c_int32, P(_abi.Prim),
@@ -312,6 +313,19 @@ class Plan:
         c = _abi.Counters()
         check(lib().lfgpu_plan_measure(self.ptr, warmup, reps, 1 if flush_l2 else 0, C.byref(c)))
         return c
+
+
+def random_inputs(graph: Graph, seed):
+    """lf::random_inputs (interp.cpp:487-503), bit-identical to the
+    reference: {tensor id: logical float64 array} for Input/Constant tensors."""
+    cg = graph.to_c({})
+    out, ptrs = {}, (C.POINTER(C.c_double) * max(1, len(graph.tensors)))()
+    for i, t in enumerate(graph.tensors):
+        if t.role in (_abi.INPUT, _abi.CONSTANT):
+            out[t.id] = np.empty(t.num_elements(), dtype=np.float64)
+            ptrs[i] = out[t.id].ctypes.data_as(C.POINTER(C.c_double))
+    check(lib().lfgpu_random_inputs(cg.ptr(), C.c_uint64(seed), ptrs))
+    return out
 
 
 def interpret(graph: Graph, seqs, scheds, inputs, flags=_abi.PLAN_DEFAULT, ctx=None):
