@@ -37,6 +37,7 @@
 #include <memory>
 
 #include "lf_pair.hpp"
+#include "lf_alloc.hpp"
 #include "lf_ptx.hpp"
 
 namespace lfg {
@@ -577,7 +578,7 @@ struct PairTables {
   void* p[8] = {};
   ~PairTables() {
     for (auto* q : p)
-      if (q) cudaFree(q);
+      if (q) dev_free(q);
   }
 };
 
@@ -585,7 +586,7 @@ template <typename T>
 void* upload(const std::vector<T>& v) {
   void* d = nullptr;
   const size_t bytes = sizeof(T) * std::max<size_t>(v.size(), 1);
-  if (cudaMalloc(&d, bytes) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc pair tables");
+  if (!(d = dev_alloc(bytes))) fail(LFGPU_ECUDA, "device allocation of pair tables");
   if (!v.empty() && cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     fail(LFGPU_ECUDA, "cudaMemcpy pair tables");
   return d;
@@ -679,7 +680,7 @@ PairLaunch pair_prepare(const PairPlan& p) {
   const int ntiles = p.MT / 2 * p.NT;
   if (L.S > 1) {  // L2 workspace (also the fallback when the DSMEM exchange cannot be used)
     const size_t ws = sizeof(float) * static_cast<size_t>(ntiles) * L.S * 256 * L.BN;
-    if (cudaMalloc(&t->p[7], ws) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc pair split-K workspace");
+    if (!(t->p[7] = dev_alloc(ws))) fail(LFGPU_ECUDA, "device allocation of the pair split-K workspace");
     L.ws = static_cast<float*>(t->p[7]);
   }
   L.owner = t;

@@ -22,6 +22,7 @@
 #include <memory>
 
 #include "lf_pair.hpp"
+#include "lf_alloc.hpp"
 #include "lf_umma.hpp"
 
 namespace lfg {
@@ -1041,7 +1042,7 @@ struct Tables {
   void* p[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   ~Tables() {
     for (auto* q : p)
-      if (q) cudaFree(q);
+      if (q) dev_free(q);
   }
 };
 
@@ -1049,7 +1050,7 @@ template <typename T>
 void* up(const std::vector<T>& v) {
   void* d = nullptr;
   size_t bytes = sizeof(T) * std::max<size_t>(v.size(), 1);
-  if (cudaMalloc(&d, bytes) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc tables");
+  if (!(d = dev_alloc(bytes))) fail(LFGPU_ECUDA, "device allocation of tables");
   if (!v.empty() && cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess)
     fail(LFGPU_ECUDA, "cudaMemcpy tables");
   return d;
@@ -1309,8 +1310,8 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   for (int t = 0; t < p.ntaps; ++t) L.a_tap[t] = p.a_tap[t];
   if (L.splits > 1) {
     const size_t ws = sizeof(float) * static_cast<size_t>(L.ntiles) * L.splits * 128 * L.BN;
-    if (cudaMalloc(&t->p[4], ws) != cudaSuccess) fail(LFGPU_ECUDA, "cudaMalloc split-K workspace");
-    if (cudaMalloc(&t->p[5], 2 * sizeof(int) * L.ntiles) != cudaSuccess ||
+    if (!(t->p[4] = dev_alloc(ws))) fail(LFGPU_ECUDA, "device allocation of the split-K workspace");
+    if (!(t->p[5] = dev_alloc(2 * sizeof(int) * L.ntiles)) ||
         cudaMemset(t->p[5], 0, 2 * sizeof(int) * L.ntiles) != cudaSuccess)
       fail(LFGPU_ECUDA, "cudaMalloc split-K counters");
     L.ws = static_cast<float*>(t->p[4]);

@@ -30,6 +30,7 @@
 #include <mutex>
 #include <vector>
 
+#include "lf_alloc.hpp"
 #include "lf_rows.hpp"
 #include "lf_core.hpp"
 #include "lf_direct.hpp"
@@ -98,10 +99,10 @@ struct DevBuf {
   void* p = nullptr;
   DevBuf() = default;
   explicit DevBuf(size_t bytes) {
-    if (bytes) CUDA_OK(cudaMalloc(&p, bytes));
+    if (bytes && !(p = dev_alloc(bytes))) fail(LFGPU_ECUDA, "device allocation of " + std::to_string(bytes) + " bytes");
   }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -248,6 +249,9 @@ struct lfgpu_plan {
   std::vector<int> order;
 
   ~lfgpu_plan() {
+    // Buffers go back to the allocator cache for the next plan: no launch
+    // of this plan may still be reading or writing them.
+    if (stream) cudaStreamSynchronize(stream);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -255,7 +259,7 @@ struct lfgpu_plan {
     for (auto e : stage_ev) cudaEventDestroy(e);
     if (h_err) cudaFreeHost(h_err);
     for (auto& x : t) {
-      if (x.d_f64) cudaFree(x.d_f64);
+      if (x.d_f64) dev_free(x.d_f64);
       if (x.h_pin) cudaFreeHost(x.h_pin);
     }
     keep.clear();
@@ -1450,7 +1454,8 @@ int lfgpu_plan_destroy(lfgpu_plan* plan) {
 
 static void host_stage_alloc(PTensor& t, int64_t n) {
   if (t.d_f64) return;
-  CUDA_OK(cudaMalloc(&t.d_f64, sizeof(double) * std::max<int64_t>(n, 1)));
+  t.d_f64 = dev_alloc(sizeof(double) * std::max<int64_t>(n, 1));
+  if (!t.d_f64) fail(LFGPU_ECUDA, "device allocation of the f64 staging buffer");
   CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&t.h_pin), sizeof(double) * std::max<int64_t>(n, 1),
                         cudaHostAllocDefault));
 }
@@ -1753,7 +1758,7 @@ int lfgpu_plan_measure(lfgpu_plan* plan, int32_t warmup, int32_t reps, int32_t f
     CUDA_OK(cudaStreamSynchronize(plan->stream));
     const double est = std::max(0.5, span(e[0], e[1]) / 4.0);
     int K = static_cast<int>(std::lround(100.0 / est));
-    K = std::max(flush_l2 ? 2 : 4, std::min(flush_l2 ? 8 : 64, K));
+    K = std::max(flush_l2 ? 2 : 4, std::min(flush_l2 ? 4 : 64, K));
     std::vector<double> us;
     for (int r = 0; r < reps; ++r) {
       CUDA_OK(cudaEventRecord(e[0], plan->stream));
