@@ -76,6 +76,7 @@ struct PairParams {
   int32_t dbg_split;  // diagnostics: >= 0 keeps only that split's partial in the reduction
   int32_t diag;       // diagnostics (LFGPU_PAIR_DIAG, timing only): bit0 skips the epilogue's global stores
   int32_t nprod;      // TMA producer warps (1..5)
+  int32_t a_tx;       // bytes of the A boxes of one stage (diagnostics)
   int32_t xmode;      // split-K exchange: 0 L2 workspace, 1 DSMEM push (one tile per cluster)
   int32_t rx_bytes;   // DSMEM receive buffer bytes ((S-1) x 128 x BN/S fp32)
 };
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (P.dbg && g == 0) P.dbg[512 * blockIdx.x + 328] = gtime();
           mbar_wait(empty0 + 8 * slot, ph ^ 1u);
           if (P.dbg && g < 64) P.dbg[512 * blockIdx.x + g] = gtime();
-          if (pr == 0) mbar_expect_tx(full0 + 8 * slot, 2 * P.tx_bytes);
+          if (pr == 0) mbar_expect_tx(full0 + 8 * slot, (P.diag & 4) ? 2 * P.a_tx : 2 * P.tx_bytes);
           const uint32_t bar = lead_full0 + 8 * slot;
           const uint32_t dst = ring0 + slot * P.stage_bytes;
 #pragma unroll
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
           for (int b = 0; b < kMaxBoxes; ++b)
-            if (b < P.b_boxes) {
+            if (b < P.b_boxes && !(P.diag & 4)) {  // diag bit 2: A operand only (ingest probe)
 #pragma unroll
               for (int d = 0; d < 5; ++d) c[d] = tb[b][d] + sc[5 + d];
               tma_load5_pair(&tma_b, dst + b_off + b * P.b_slot, bar, c);
@@ -395,9 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (issuer) {
           const uint32_t a_addr = ring0 + slot * P.stage_bytes;
           const uint64_t ad = P.a_desc | (a_addr >> 4), bd = P.b_desc | ((a_addr + b_off) >> 4);
+          if (!(P.diag & 2))  // diag bit 1: no MMAs (ingest probe; results are garbage)
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma2_bf16(d, ad + k * akadv, bd + k * bkadv, P.idesc, (s != s_lo) | k);
+            for (int k = 0; k < 4; ++k)
+              umma2_bf16(d, ad + k * akadv, bd + k * bkadv, P.idesc, (s != s_lo) | k);
           umma2_commit_mc(empty0 + 8 * slot, pair_mask);
         }
         __syncwarp();
@@ -640,6 +642,7 @@ PairLaunch pair_prepare(const PairPlan& p) {
   L.b_slot = p.B.slot_bytes;
   L.stage_bytes = L.a_boxes * L.a_slot + L.b_boxes * L.b_slot;
   L.tx_bytes = L.a_boxes * p.A.box_bytes + L.b_boxes * p.B.box_bytes;
+  L.a_box_bytes = p.A.box_bytes;
   L.a_desc = umma_desc_bits(p.A);
   L.b_desc = umma_desc_bits(p.B);
   L.a_kadv = p.A.k_adv;
@@ -757,6 +760,7 @@ cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
   P.dbg_split = getenv("LFGPU_PAIR_DBG_SPLIT") ? atoi(getenv("LFGPU_PAIR_DBG_SPLIT")) : -1;
   P.diag = getenv("LFGPU_PAIR_DIAG") ? atoi(getenv("LFGPU_PAIR_DIAG")) : 0;
   P.nprod = L.nprod;
+  P.a_tx = L.a_boxes * L.a_box_bytes;
   P.xmode = L.xmode;
   P.rx_bytes = L.rx_bytes;
   static const bool pdl = [] {

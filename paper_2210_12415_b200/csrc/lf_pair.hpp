@@ -96,6 +96,7 @@ struct PairLaunch {
   int nprod = 4;  // TMA producer warps
   int xmode = 0, rx_bytes = 0;  // split-K exchange over DSMEM
   int a_boxes = 0, b_boxes = 0, a_slot = 0, b_slot = 0, stage_bytes = 0, tx_bytes = 0;
+  int a_box_bytes = 0;
   uint64_t a_desc = 0, b_desc = 0;
   uint32_t a_kadv = 0, b_kadv = 0, idesc = 0, tmem_cols = 0;
   int ring_bytes = 0;
