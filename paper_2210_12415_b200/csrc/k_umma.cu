@@ -73,6 +73,8 @@ struct UmmaParams {
                             // epilogue's stores, 2 traces, 4 unshifted taps, 8 one tap
   int64_t col0;             // col_off[0] folded into the tile base in store mode 1
   unsigned long long* dbg;  // optional per-CTA %globaltimer checkpoints (8 per CTA)
+  unsigned long long* cdbg;  // optional chain trace slot: [0] entry min, [1] wait min, [2] wait max,
+                             // [3] first stage landed min, [4] exit max, [5] epilogue done max
   // Split-K: unit (tile, split) accumulates stages [split*n/S, (split+1)*n/S);
   // partial tiles go to `ws`, the last CTA of a tile (per-tile counter) sums
   // them in split order and runs the fused epilogue.
@@ -552,6 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nst = P.nstages;
   unsigned long long* dbg = P.dbg ? P.dbg + 32 * blockIdx.x : nullptr;
   if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
+  if (P.cdbg && threadIdx.x == 0) atomicMin(P.cdbg, gtimer());
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < pipe; ++s) {
@@ -608,6 +611,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
+  if (P.cdbg && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    atomicMin(P.cdbg + 1, t);
+    atomicMax(P.cdbg + 2, t);
+  }
 
   const int prod = warp == 0 ? 0 : (warp == 2 || warp == 3 ? warp - 1 : -1);
   if (prod >= 0 && prod < P.nprod) {
@@ -703,6 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int s = s_lo; s < s_hi; ++s) {
         mbar_wait(full0 + 8 * slot, phase);
         if (dbg && leader && i == 0 && s == s_lo) dbg[3] = gtimer();
+        if (P.cdbg && leader && i == 0 && s == s_lo) atomicMin(P.cdbg + 3, gtimer());
         if (dbg && leader && (P.diag & 256) && i == 0 && s - s_lo < 16) dbg[16 + s - s_lo] = gtimer();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (nw) {
@@ -950,9 +959,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (half_leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (dbg && threadIdx.x == kEpiWarp0 * 32) dbg[6] = gtimer();
+    if (P.cdbg && threadIdx.x == kEpiWarp0 * 32) atomicMax(P.cdbg + 5, gtimer());
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (P.cdbg && threadIdx.x == 0) atomicMax(P.cdbg + 4, gtimer());
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -1073,6 +1084,8 @@ uint64_t umma_desc_bits(const OperandView& v) { return desc_bits(v); }
 uint32_t umma_idesc(int M, int N, bool a_mn, bool b_mn) { return idesc_of(M, N, a_mn, b_mn); }
 
 static void* g_umma_dbg = nullptr;
+static unsigned long long* g_chain_dbg = nullptr;
+void umma_set_chain_buffer(void* p) { g_chain_dbg = static_cast<unsigned long long*>(p); }
 void* umma_debug_buffer() { return g_umma_dbg; }
 void umma_set_debug_buffer(void* p) { g_umma_dbg = p; }
 
@@ -1410,6 +1423,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.ws = L.ws;
   P.counters = L.counters;
   P.dbg = static_cast<unsigned long long*>(umma_debug_buffer());
+  P.cdbg = g_chain_dbg && L.chain_slot >= 0 ? g_chain_dbg + 8 * L.chain_slot : nullptr;
   using KernelFn = void (*)(CUtensorMap, CUtensorMap, UmmaParams, CUtensorMap, CUtensorMap);
   static const KernelFn fns[3][2] = {{umma_kernel<0, false>, umma_kernel<0, true>},
                                      {umma_kernel<1, false>, umma_kernel<1, true>},

@@ -857,6 +857,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           for (int e = 0; e + 1 < up.epi_count; ++e) P->t[up.epi[e].out_tensor].valid = false;
           if (up.epi_count) out.valid = false;
           UmmaLaunch L = umma_prepare(up);
+          L.chain_slot = static_cast<int>(P->steps.size());
           step.kernel = "im2col_umma";
           step.launches = 2;
           step.run = [Q, L](cudaStream_t st) {
@@ -1001,6 +1002,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           for (int e = 0; e + 1 < up.epi_count; ++e) P->t[up.epi[e].out_tensor].valid = false;
           if (up.epi_count) out.valid = false;
           UmmaLaunch L = umma_prepare(up);
+          L.chain_slot = static_cast<int>(P->steps.size());
           step.kernel = up.kind == UMMA_CONV ? "umma_conv" : "umma_gemm";
           step.run = [L](cudaStream_t s) { return umma_launch(L, s); };
           P->tc_nodes += 1;
@@ -1842,6 +1844,17 @@ int lfgpu_interpret(lfgpu_ctx* ctx, const lfgpu_graph* g, int32_t nsched,
 }
 
 }  // extern "C"
+
+namespace lfg {
+void umma_set_chain_buffer(void* p);
+}
+// Diagnostics: per-launch [entry, wait, first data, exit] timestamps of the
+// tcgen05 kernels of a plan (8 uint64 per plan step; the caller
+// initialises the min slots to ~0 and the max slots to 0).
+extern "C" int lfgpu_debug_chain_trace(void* d_buf) {
+  lfg::umma_set_chain_buffer(d_buf);
+  return LFGPU_OK;
+}
 
 extern "C" int lfgpu_debug_umma_trace(void* d_buf) {
   lfg::umma_set_debug_buffer(d_buf);

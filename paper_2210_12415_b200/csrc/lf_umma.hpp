@@ -153,6 +153,7 @@ struct UmmaPlan {
 // Per-launch device state (tables uploaded, tensor maps encoded).
 struct UmmaLaunch {
   CUtensorMap tma_a, tma_b;
+  int chain_slot = -1;  // diagnostics: this launch's slot in the chain trace (plan step index)
   void* d_tiles = nullptr;
   void* d_stages = nullptr;
   void* d_rows = nullptr;

@@ -55,6 +55,13 @@ __global__ void __launch_bounds__(256, 1) ingest(const __grid_constant__ CUtenso
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + q * req),
               "l"(src + c * chunk + q * req), "r"(req), "r"(bar)
               : "memory");
+        } else if (mode == 2) {
+          const int y = static_cast<int>((c * nreq + q) * rows % (1 << 14));
+          asm volatile(
+              "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+                  dst + q * req),
+              "l"(reinterpret_cast<uint64_t>(&map)), "r"(0), "r"(y), "r"(0), "r"(0), "r"(0), "r"(bar)
+              : "memory");
         } else {
           // tensor dims {64, R, KS}: element (k1, r, k0); chunk c covers rows [c*rows*nreq ...)
           const int y = static_cast<int>((c * nreq + q) * rows % (1 << 14));
@@ -91,28 +98,24 @@ int main() {
     int mode, chunk, nreq, slots, kd, grid, nprod;
   };
   std::vector<Case> cases;
-  for (int grid : {148})
-    for (int kd : {1, 2, 4})
-      for (int chunk : {16384, 32768, 49152, 65536, 98304}) {
-        for (int slots : {2, 3, 4, 8}) {
-          if (chunk * slots > 200 * 1024) continue;
-          for (int nprod : {1, 2, 4})
-            for (int nreq : {1, 2}) {
-              if (slots % nprod) continue;
-              if (chunk / nreq / (128 * kd) < 8 || chunk / nreq / (128 * kd) > 256 || (chunk / nreq) % (128 * kd)) continue;
-              cases.push_back({1, chunk, nreq, slots, kd, grid, nprod});
-            }
-        }
-      }
+  for (int mode : {1, 2})
+    for (int chunk : {16384, 24576, 32768})
+      for (int slots : {4, 7})
+        for (int nprod : {1, 2, 3})
+          for (int nreq : {1, 2}) {
+            if (chunk * slots > 200 * 1024) continue;
+            if ((chunk / nreq) % 128 || chunk / nreq / 128 > 256) continue;
+            cases.push_back({mode, chunk, nreq, slots, 1, 24, nprod});
+          }
   printf("grid mode kd chunk nreq slots nprod inflight_KB  B/clk/SM  cyc/slot\n");
   for (const Case& c : cases) {
     CUtensorMap map;
     const int rows = c.chunk / c.nreq / (128 * c.kd);
-    cuuint64_t dims[3] = {64, 16384, 4};
-    cuuint64_t strides[2] = {128, 128ull * 16384};
-    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(rows), static_cast<cuuint32_t>(c.kd)};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, src, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint64_t dims[5] = {64, 16384, 4, 1, 1};
+    cuuint64_t strides[4] = {128, 128ull * 16384, 128ull * 16384 * 4, 128ull * 16384 * 4};
+    cuuint32_t box[5] = {64, static_cast<cuuint32_t>(rows), static_cast<cuuint32_t>(c.kd), 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, c.mode == 2 ? 5 : 3, src, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
         CUDA_SUCCESS) {
       printf("encode failed\n");
