@@ -241,8 +241,17 @@ def transform_bench(torch, gen, dev, ctx, pk, steps):
     fns[0]()
     torch.cuda.synchronize()
     ok = bool(torch.equal(y.view(Nn, 4, 56, 56, 16), x.view(Nn, 4, 16, 56, 56).permute(0, 1, 3, 4, 2)))
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_transform_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
     return {"bytes": byts, "us": round(us, 2), "GB_per_s": round(gbs, 1),
             "frac_of_hbm": round(gbs / pk["hbm_gbs"], 4), "verified_exact": ok,
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(gbs / pk["hbm_gbs"], 4), "traffic": traffic,
+                         "kernel": "digit_transpose_vec (K1)",
+                         "algorithmic": f"{byts} B per launch (source read + destination write)"},
             "l2": "6 rotating source/destination pairs, 617 MB (> 4x L2), back to back"}
 
 

@@ -75,6 +75,19 @@ def conv_b16best(reps=3):
     conv(reps, 16, (8, 28, 64, 32, 32, 64))
 
 
+def transform_rotating(reps=12, n=64):
+    """K1 back to back over 6 rotating source/destination pairs (617 MB, the
+    bench's regime): profile a late launch with --cache-control none so the
+    L2 write-backs of earlier destinations land in its DRAM counters."""
+    pairs = [(k64((n, 64, 56, 56)), torch.empty(n * 64 * 56 * 56, device="cuda")) for _ in range(6)]
+    dims = [("N", n), ("C", 64), ("H", 56), ("W", 56)]
+    seq = [split(1, [4, 16]), reorder([0, 1, 3, 4, 2])]
+    for i in range(reps):
+        x, y = pairs[i % 6]
+        runtime.layout_convert(x, dims, [], seq, y)
+    torch.cuda.synchronize()
+
+
 def gemm_pair(reps=3):
     """cfg2 on the CTA-pair kernel (BN=128, 2 K splits over DSMEM)."""
     gemm(reps, (256, 64, 256), 128, 0)
