@@ -5,13 +5,10 @@ layout (each GMM's output feeds the next GMM's A operand through its bf16
 shadow). Checked against float64 torch: exactly emulating the plan's
 numerics (bf16 operands, fp32 storage) and within the stated chained-bf16
 tolerance of the exact result."""
-import os
-import sys
 
 import pytest
 
 torch = pytest.importorskip("torch")
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
 
 pytestmark = pytest.mark.gpu
 

@@ -1,4 +1,4 @@
-import sys; sys.path.insert(0, "/root/repo")
+import sys; sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 import torch
 from paper_2210_12415_b200 import e2e, workloads
 gen = torch.Generator(device="cuda"); gen.manual_seed(1)
