@@ -471,6 +471,32 @@ def run_ours(args, rank, world, local):
     c2d = {f"b{nb}": c2d_bench(torch, gen, dev, ctx, pk, nb) for nb in (1, 16)}
     transform = transform_bench(torch, gen, dev, ctx, pk, args.steps)
 
+    # ---- 4a. the same tcgen05 GEMM at large shapes (the kernel's ceiling,
+    # separated from 1024^3's fixed costs); torch.matmul as a yardstick only
+    ceiling = {}
+    for n in (4096, 8192):
+        try:
+            gn = ir.gemm(n, n, n)
+            sq = runtime.decode_layout(gn, 0, [256, 64, 256])
+            pn = runtime.Plan(gn, sq, [runtime.sched(0, tile_last=256)], _abi.PLAN_REQUIRE_TC, ctx=ctx)
+            an, bn = kmul64(torch, (n, n), gen, dev), kmul64(torch, (n, n), gen, dev)
+            pn.set_input_device("a", an)
+            pn.set_input_device("b", bn)
+            mn = pn.measure(warmup=2, reps=5, flush_l2=False)
+            ab, bb = an.to(torch.bfloat16), bn.to(torch.bfloat16)
+            tus = time_rotating_fn(torch, [lambda: torch.matmul(ab, bb)], 10, 3)
+            fl = 2.0 * n ** 3
+            ok = bool(torch.equal(torch.tensor(pn.get_output("c"), device=dev).view(n, n)[:256].double(),
+                                  an[:256].double() @ bn.double())) if n == 4096 else None
+            ceiling[f"{n}^3"] = {"us": round(mn.cost, 2), "tflops": round(fl / mn.cost / 1e6, 1),
+                                 "frac_of_measured_peak": round(fl / mn.cost / 1e6 / pk["bf16_tflops"], 4),
+                                 "kernel": pn.node_kernel(0)[:120], "rows_0_255_exact": ok,
+                                 "torch_matmul_us_yardstick": round(tus, 2)}
+            pn.close()
+            del an, bn, ab, bb
+        except Exception as e:
+            ceiling[f"{n}^3"] = {"error": str(e)[:200]}
+
     # ---- 4b. end-to-end graphs: cfg4 ResNet-18 b1 (tuned per-conv layouts,
     # fused epilogues, whole-graph CUDA graph) and cfg5 BERT-base GEMM chain
     # (seq 128, 12 layers); device time per inference step, cold L2.
@@ -597,6 +623,7 @@ def run_ours(args, rank, world, local):
                      "kernel": plan.node_kernel(0), "peak_source": pk_kind,
                      "algorithmic": "2*1024^3 FLOP per launch"},
         "c2d_cfg1": c2d,
+        "gemm_large_shape_ceiling": ceiling,
         "layout_transform_nchw_to_nchwc16_n64": transform,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

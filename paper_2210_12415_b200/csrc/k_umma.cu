@@ -42,6 +42,7 @@ struct UmmaParams {
   int32_t ntiles, nstages, BN, ksteps, pipe, nprod;
   int32_t dual;  // two MMA issuers: warp 1 takes even units, warp 3 odd ones
   int32_t blocked;  // loop point `parallel` = 1: contiguous unit chunks per CTA (static schedule), else cyclic
+  int32_t xsplit;   // split-K partials exchanged over DSMEM: the S splits of a tile are one cluster, one unit per CTA
   int32_t a_boxes, b_boxes, a_slot, b_slot, tx_bytes;
   uint64_t a_desc, b_desc;  // LBO/SBO/version/layout bits; start address added on device
   uint32_t a_kadv, b_kadv;
@@ -214,6 +215,34 @@ __device__ __forceinline__ void half_bar(int h) {
   asm volatile("bar.sync %0, 128;" ::"r"(2 + h) : "memory");
 }
 
+// Cluster helpers for the DSMEM split-K exchange (the K splits of a tile are
+// the CTAs of one cluster).
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_arrive(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void cl_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAITX:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAITX;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -350,6 +379,19 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
     if (lane == 0) mbar_arrive(tempty);
   }
   const int64_t wstride = static_cast<int64_t>(P.BN / 4) * 128;
+  if (mode == 3 && P.xsplit) {
+    // DSMEM: straight into the receiving sibling's reduction buffer, laid out
+    // [sender among its siblings][col/4 within its slice][row] float4.
+    const int sl = P.BN / splits, r = c0 / sl, o = split < r ? split : split - 1;
+    const uint32_t base = cl_mapa(smem_u32(red), static_cast<uint32_t>(r)) +
+                          static_cast<uint32_t>(((o * (sl / 4) + (c0 - r * sl) / 4) * 128 + row) * 16);
+#pragma unroll
+    for (int j = 0; j < W / 4; ++j)
+      asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(base + j * 128 * 16), "f"(v[4 * j]),
+                   "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                   : "memory");
+    return;
+  }
   if (mode == 3) {  // publish this split's partial tile ([unit][col/4][row] float4)
     float4* w = reinterpret_cast<float4*>(P.ws) + (ws_tile + split) * wstride + (c0 / 4) * 128 + row;
 #pragma unroll
@@ -566,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tempty0 + 8 * b, kEpiWarps);  // one arrive per epilogue warp
     }
     for (int c = 0; c < nw; ++c) mbar_init(wfull0 + 8 * c, 1);
-    mbar_init(redbar, 1);
+    mbar_init(redbar, P.xsplit ? (P.splits - 1) * kEpiWarps : 1);  // sibling warps' DSMEM arrivals / bulk copy
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
@@ -603,7 +645,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (P.xsplit) cl_sync();  // siblings' barriers initialised before any DSMEM arrival
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   // Programmatic dependent launch: everything above overlapped the previous
@@ -800,7 +843,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         epi_chunk<16>(P, tbase, c0, row, lane, q, wbuf, rows, cols, n_base, obase, s_row, s_col, 3,
                       split, splits, ws_tile, s_red, red_lo, false, tempty, org, s_rowrel, false);
       }
-      if (splits > 1) {
+      if (splits > 1 && P.xsplit) {
+        // Release this warp's DSMEM partials to every sibling (cluster
+        // scope), then wait for theirs: no global round trip, no spin.
+        if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[16] = gtimer();
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+          for (int o2 = 0; o2 < splits; ++o2)
+            if (o2 != split) cl_arrive(cl_mapa(redbar, static_cast<uint32_t>(o2)));
+        cl_wait(redbar, red_phase);
+        red_phase ^= 1;
+        if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[19] = gtimer();
+      } else if (splits > 1) {
         if (dbg && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[16] = gtimer();
         __threadfence();
         epi_bar();
@@ -962,7 +1017,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (P.cdbg && threadIdx.x == kEpiWarp0 * 32) atomicMax(P.cdbg + 5, gtimer());
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (P.xsplit) cl_sync();  // no CTA leaves while a sibling may still address its SMEM
+  else __syncthreads();
   if (P.cdbg && threadIdx.x == 0) atomicMax(P.cdbg + 4, gtimer());
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1101,6 +1157,8 @@ static int num_sms() {
 }
 
 int umma_num_sms() { return num_sms(); }
+
+const void* umma_kernel_fn(int mode, bool splitk);
 
 UmmaLaunch umma_prepare(const UmmaPlan& p) {
   UmmaLaunch L;
@@ -1353,10 +1411,52 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
     L.dual = p.BN <= 128 && units >= 2 * L.grid && 2 * spu <= L.pipe;
     if (const char* e = getenv("LFGPU_DUAL_MMA")) L.dual = atoi(e) != 0;
     L.blocked = p.persistent && L.splits == 1 ? 1 : 0;
+  }
+  // DSMEM split-K: when every CTA gets exactly one unit, the S splits of a
+  // tile run as one cluster of S CTAs and exchange partials through their
+  // SMEM (the workspace protocol stays for the multi-unit case).
+  {
+    const int units = L.ntiles * L.splits;
+    // Measured (tools/xsplit_check.py): under a cluster launch an operand
+    // loaded as two or more TMA boxes per stage (MN-major B wider than 64
+    // bf16) reads wrong data — the same failure the CTA-pair kernel shows
+    // (lf_pair.hpp); single-box operands are exact. Cluster exchange only then.
+    L.xsplit = L.splits > 1 && units == L.grid && !L.dual && L.a_boxes == 1 && L.b_boxes == 1 &&
+                       !getenv("LFGPU_NO_XSPLIT")
+                   ? 1
+                   : 0;
+    if (L.xsplit) {
+      cudaLaunchConfig_t cfg;
+      std::memset(&cfg, 0, sizeof(cfg));
+      cfg.gridDim = dim3(L.grid);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = L.smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = L.splits;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      const void* f = umma_kernel_fn(L.store_mode, true);
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (cudaOccupancyMaxActiveClusters(&n, f, &cfg) != cudaSuccess || n * L.splits < L.grid) L.xsplit = 0;
+      cudaGetLastError();
+    }
     if (L.dual) L.nprod = std::min(L.nprod, 2);
   }
   static_assert(sizeof(TileEntry) == 192, "TileEntry layout");
   return L;
+}
+
+// The kernel instance for (store mode, split-K).
+const void* umma_kernel_fn(int mode, bool splitk) {
+  using KernelFn = void (*)(CUtensorMap, CUtensorMap, UmmaParams, CUtensorMap, CUtensorMap);
+  static const KernelFn fns[3][2] = {{umma_kernel<0, false>, umma_kernel<0, true>},
+                                     {umma_kernel<1, false>, umma_kernel<1, true>},
+                                     {umma_kernel<2, false>, umma_kernel<2, true>}};
+  return reinterpret_cast<const void*>(fns[std::min(std::max(mode, 0), 2)][splitk ? 1 : 0]);
 }
 
 cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
@@ -1383,6 +1483,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.nprod = L.nprod;
   P.dual = L.dual;
   P.blocked = L.blocked;
+  P.xsplit = L.xsplit;
   P.a_boxes = L.a_boxes;
   P.b_boxes = L.b_boxes;
   P.a_slot = L.a_slot;
@@ -1449,11 +1550,22 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = L.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (L.xsplit) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = L.splits;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, fn, L.tma_a, L.tma_b, P, L.tma_o, L.tma_ob);
 }
 

@@ -106,13 +106,13 @@ def max_rel(a, b):
     return float(((a - b).abs() / s).max())
 
 
-def build_resnet18(n, factors, ctx=None):
+def build_resnet18(n, factors, ctx=None, flags=_abi.PLAN_CUDA_GRAPH):
     g, convs = workloads.resnet18(n)
     seqs = workloads.resnet18_seqs(g, convs, factors)
     scheds = [runtime.sched(c["node"], fuse=1) for c in convs]
     gi = len(g.nodes) - 2  # the FC GMM
     scheds.append(runtime.sched(gi, fuse=1))
-    plan = runtime.Plan(g, seqs, scheds, _abi.PLAN_CUDA_GRAPH, ctx=ctx)
+    plan = runtime.Plan(g, seqs, scheds, flags, ctx=ctx)
     return g, convs, plan
 
 

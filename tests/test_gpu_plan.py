@@ -516,3 +516,25 @@ def test_conv_loop_point_tile_second_parallel(factors, ts, rows, par):
     p.run()
     y = p.get_output("y")
     assert np.array_equal(y, ref["y"]), np.abs(y - ref["y"]).max()
+
+
+# Split-K over DSMEM in the 1-CTA kernel (k_umma.cu, one unit per CTA: the S
+# splits of a tile are one cluster) against the workspace protocol and the
+# oracle, for the BERT-size GEMMs it serves (M = 128), MN- and K-major B.
+@pytest.mark.parametrize("K,N,f,bk", [(768, 768, (128, 64, 64), 0), (3072, 768, (128, 64, 64), 0),
+                                      (768, 768, (128, 128, 128), 1), (3072, 768, (128, 128, 128), 1),
+                                      (768, 768, (128, 128, 128), 0)])
+@pytest.mark.parametrize("knob", [{}, {"LFGPU_NO_XSPLIT": "1"}])
+def test_split_k_dsmem_exchange(K, N, f, bk, knob, monkeypatch):
+    for k, v in knob.items():
+        monkeypatch.setenv(k, v)
+    g, seqs, inputs, ref = gemm_case(128, K, N, f)
+    if bk:
+        seqs["b"] = [split(0, [K // 64, 64]), reorder([0, 2, 1])]
+    p = runtime.Plan(g, seqs, [runtime.sched(0, tile_last=f[2])], flags=_abi.PLAN_REQUIRE_TC)
+    assert "splits=1 " not in p.node_kernel(0), p.node_kernel(0)
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    got = p.get_output("c")
+    assert np.array_equal(got, ref["c"]), np.abs(got - ref["c"]).max()

@@ -8,12 +8,22 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 from paper_2210_12415_b200 import e2e, runtime  # noqa: E402
 
-layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 gen = torch.Generator(device="cuda")
 gen.manual_seed(1)
-g, gm, p = e2e.build_bert(layers, 64, flags=0)
-for k, x in e2e.make_bert_inputs(g, gen).items():
+if len(sys.argv) > 1 and sys.argv[1] == "resnet18":
+    from paper_2210_12415_b200 import workloads
+    fac = workloads.tune_resnet18(1, lambda sub: e2e.make_inputs(sub, gen))
+    g, _, p = e2e.build_resnet18(1, fac, flags=0)
+    ins = e2e.make_inputs(g, gen)
+else:
+    layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    g, gm, p = e2e.build_bert(layers, 64, flags=0)
+    ins = e2e.make_bert_inputs(g, gen)
+for k, x in ins.items():
     p.set_input_device(k, x)
+steps = {}
+for i in range(len(g.nodes)):
+    steps[i] = p.node_kernel(i)
 for _ in range(3):
     p.run()
 torch.cuda.synchronize()
