@@ -56,6 +56,7 @@ struct UmmaParams {
   // B slab is loaded once per CTA into SMEM at w_off (w_chunk bytes apart,
   // barrier wfull[c]); the ring then carries A only.
   int32_t wres, w_off, w_chunk, w_tx;
+  int32_t w_prewait;  // resident weights are constants no earlier kernel of this run writes: load before the PDL wait
   int32_t red_bytes;        // split-K: SMEM for the siblings' column slices
   // Store mode 2 (TMA store): staging buffers (2 x stg_f32 fp32 + 2 x stg_bf
   // bf16 bytes) at stg_off; per-tile box origins; row positions in the box
@@ -649,6 +650,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // Resident weights that are plan constants can be loaded before the PDL
+  // wait: no kernel of this run writes them and every kernel before this
+  // one's predecessor has completed (the predecessor only released us after
+  // its own wait). Their load then overlaps the previous kernel.
+  const bool w_early = P.w_prewait && nw && warp == 0 && u_first < u_end;
+  if (w_early && elect_one()) {
+    const TileEntry* te = P.tiles + u_first / splits;
+    const uint32_t ring0w = smem_u32(smem);
+    for (int c = 0; c < nw; ++c) {
+      const StageEntry se = s_stage[c];
+      const uint32_t bar = wfull0 + 8 * c;
+      mbar_expect_tx(bar, P.w_tx);
+      for (int b = 0; b < P.b_boxes; ++b)
+        tma_load5(&tma_b, ring0w + P.w_off + c * P.w_chunk + b * P.b_slot, bar, __ldg(&te->cb[b][0]) + se.sb[0],
+                  __ldg(&te->cb[b][1]) + se.sb[1], __ldg(&te->cb[b][2]) + se.sb[2], __ldg(&te->cb[b][3]) + se.sb[3],
+                  __ldg(&te->cb[b][4]) + se.sb[4]);
+    }
+  }
+  __syncwarp();
   // Programmatic dependent launch: everything above overlapped the previous
   // kernel's tail; operands / outputs are touched only after this wait.
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -669,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t b_off = P.a_boxes * a_slot;
     const int na = P.a_boxes, nb = P.b_boxes;
     const bool leader = elect_one();
-    if (nw && prod == 0 && leader && u_first < u_end) {
+    if (nw && prod == 0 && leader && u_first < u_end && !w_early) {
       // Resident weights: every chunk's slab once, on its own barrier.
       const TileEntry* te = P.tiles + u_first / splits;
       for (int c = 0; c < nw; ++c) {
@@ -1490,6 +1510,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.b_slot = L.b_slot;
   P.tx_bytes = L.a_boxes * L.a_bytes + (L.wres ? 0 : L.b_boxes * L.b_bytes);
   P.wres = L.wres;
+  P.w_prewait = L.w_prewait;
   P.w_off = L.ring_bytes;
   P.w_chunk = L.w_chunk;
   P.w_tx = L.w_tx;

@@ -1003,6 +1003,13 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           if (up.epi_count) out.valid = false;
           UmmaLaunch L = umma_prepare(up);
           L.chain_slot = static_cast<int>(P->steps.size());
+          {
+            // Resident weights may load before the PDL wait when they are a
+            // plan constant (no producer) and this is not the run's first
+            // kernel (which may follow a set_input conversion of them).
+            const PTensor& W = P->t[n.inputs[1]];
+            L.w_prewait = L.wres && !P->steps.empty() && W.producer < 0 && !getenv("LFGPU_NO_W_PREWAIT") ? 1 : 0;
+          }
           step.kernel = up.kind == UMMA_CONV ? "umma_conv" : "umma_gemm";
           step.run = [L](cudaStream_t s) { return umma_launch(L, s); };
           P->tc_nodes += 1;

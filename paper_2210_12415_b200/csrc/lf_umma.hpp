@@ -191,6 +191,7 @@ struct UmmaLaunch {
   int dual = 0;                 // two MMA issuers (warps 1 and 3) on alternate units
   int blocked = 0;              // contiguous unit chunks per CTA (loop point parallel = 1)
   int xsplit = 0;               // split-K over DSMEM inside a cluster (one unit per CTA)
+  int w_prewait = 0;            // set by the plan: resident weights loaded before the PDL wait
   float* ws = nullptr;          // split-K partial tiles
   int* counters = nullptr;      // split-K per-tile arrival counters
   std::shared_ptr<void> owner;  // keeps the device tables alive
