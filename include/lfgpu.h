@@ -227,7 +227,15 @@ enum {
    * reference's double arithmetic up to fp32 storage (1e-5 rule,
    * proj/src/cli.cpp:30-49). Plans (lfgpu_plan_build) use tensor cores by
    * default. */
-  LFGPU_PLAN_TENSOR_CORES = 1 << 4
+  LFGPU_PLAN_TENSOR_CORES = 1 << 4,
+  /* GMM on tensor cores at fp32-level precision: each fp32 operand is split
+   * into three bf16 pieces (x = x0 + x1 + x2, 24 significand bits) and the six
+   * leading piece products are one bf16 GEMM with K' = 6K (the operands
+   * concatenated along K, fp32 accumulation in TMEM), at 6x the tensor-core
+   * work. Operand rounding disappears; the fp32 accumulation remains (max
+   * rel diff ~1e-5..1e-4 on general inputs at K ~ 1e3, stated tolerance
+   * 1e-4; LFGPU_PLAN_EXACT is the 1e-5 path). */
+  LFGPU_PLAN_TC_SPLIT = 1 << 5
 };
 
 typedef struct lfgpu_ctx lfgpu_ctx;

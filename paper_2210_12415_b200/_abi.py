@@ -30,6 +30,7 @@ PLAN_REQUIRE_TC = 2
 PLAN_CUDA_GRAPH = 4
 PLAN_KEEP_ALL = 8
 PLAN_TENSOR_CORES = 16  # lfgpu_interpret: opt into tcgen05 (else reference semantics, EXACT)
+PLAN_TC_SPLIT = 32  # GMM on tcgen05 with 3-way bf16 operand splits (fp32-level precision)
 
 
 class Prim(C.Structure):

@@ -81,11 +81,17 @@ struct PairParams {
   int32_t rx_bytes;   // DSMEM receive buffer bytes ((S-1) x 128 x BN/S fp32)
 };
 
+#ifdef LFG_PAIR_CLOCK_STAMPS
+// diagnostics build: SM cycle counter scaled to ns at 1.965 GHz (per-SM, not
+// comparable across SMs) instead of %globaltimer
+__device__ __forceinline__ unsigned long long gtime() { return static_cast<unsigned long long>(clock64() / 1.965); }
+#else
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#endif
 
 // Grouped rasterisation: `group` row tiles sweep the column tiles together
 // so concurrently running clusters share A row blocks and B column blocks in L2.

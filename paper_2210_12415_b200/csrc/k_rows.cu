@@ -319,7 +319,38 @@ __global__ void __launch_bounds__(256) bmm_pv_kernel(const BmmParams P) {
   }
 }
 
+__global__ void __launch_bounds__(256) split_bf16_kernel(const SplitParams P) {
+  LFG_PDL_ENTRY();
+  // piece index per term, smallest products first (x2y0, x1y1, x0y2, x1y0,
+  // x0y1, x0y0): the accumulator is still small while the low-order terms
+  // land, so the tensor core's accumulation keeps their bits.
+  const int pa[kSplitTerms] = {2, 1, 0, 1, 0, 0}, pb[kSplitTerms] = {0, 1, 2, 0, 1, 0};
+  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(P.dst);
+  const int64_t n = P.R * P.C;
+  for (int64_t e = blockIdx.x * 256ll + threadIdx.x; e < n; e += gridDim.x * 256ll) {
+    const int64_t r = e / P.C, c = e - r * P.C;
+    const float x = __ldg(P.src + __ldg(P.src_row + r) + __ldg(P.src_col + c));
+    __nv_bfloat16 pc[3];
+    pc[0] = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(pc[0]);  // exact in fp32
+    pc[1] = __float2bfloat16_rn(r1);
+    pc[2] = __float2bfloat16_rn(r1 - __bfloat162float(pc[1]));
+#pragma unroll
+    for (int t = 0; t < kSplitTerms; ++t) {
+      const int64_t o = P.side == 0 ? __ldg(P.dst_row + r) + __ldg(P.dst_col + t * P.K + c)
+                                    : __ldg(P.dst_row + t * P.K + r) + __ldg(P.dst_col + c);
+      dst[o] = pc[P.side == 0 ? pa[t] : pb[t]];
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_split_bf16(const SplitParams& P, cudaStream_t stream) {
+  const int64_t n = P.R * P.C;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  return launch_pdl(split_bf16_kernel, dim3(std::max(1u, blocks)), dim3(256), 0, stream, P);
+}
 
 cudaError_t launch_rows(const RowsParams& P, cudaStream_t stream) {
   if (P.rows == 0) return cudaSuccess;

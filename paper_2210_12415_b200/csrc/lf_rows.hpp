@@ -47,6 +47,23 @@ struct BmmParams {
   int64_t a_off[3] = {}, b_off[3] = {}, o_off[3] = {};
 };
 
+// LFGPU_PLAN_TC_SPLIT operand preparation: x = x0 + x1 + x2 (bf16 pieces);
+// the K extent becomes kTerms*K with term t holding piece kPiece[side][t]
+// (A: columns t*K + k, B: rows t*K + k), so one bf16 GEMM sums the six
+// leading piece products, smallest first: x2y0 + x1y1 + x0y2 + x1y0 + x0y1 + x0y0.
+constexpr int kSplitTerms = 6;
+struct SplitParams {
+  int32_t side = 0;  // 0: A [M, K] (K = columns), 1: B [K, N] (K = rows)
+  int64_t R = 0, C = 0, K = 0;  // source logical extents; K = the contraction extent
+  const float* src = nullptr;
+  const int64_t* src_row = nullptr;  // R
+  const int64_t* src_col = nullptr;  // C
+  void* dst = nullptr;               // bf16
+  const int64_t* dst_row = nullptr;  // A: R; B: kSplitTerms * R
+  const int64_t* dst_col = nullptr;  // A: kSplitTerms * C; B: C
+};
+cudaError_t launch_split_bf16(const SplitParams& P, cudaStream_t stream);
+
 cudaError_t launch_rows(const RowsParams& P, cudaStream_t stream);
 cudaError_t launch_bmm(const BmmParams& P, bool exact, cudaStream_t stream);
 

@@ -466,6 +466,11 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   std::map<int, std::vector<EpiOp>> direct;  // CUDA-core direct convs (k_direct.cu)
   std::map<int, std::vector<EpiOp>> depd;    // K6 depthwise (k_direct.cu)
   std::map<int, UmmaPlan> im2col;            // small-I C2D: im2col + tcgen05 GEMM
+  struct SplitGmm {                          // LFGPU_PLAN_TC_SPLIT operands (K' = 6K)
+    std::vector<Dim> a_log, b_log;
+    Seq a_seq, b_seq;
+  };
+  std::map<int, SplitGmm> split_gmm;
   std::map<int, int> im2col_pad;             // im2col node -> Padding node it reads through
   std::set<int> fused_away;  // element-wise nodes absorbed into an epilogue
   std::vector<int> pos(P->nodes.size(), 0);
@@ -536,6 +541,39 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
     lfgpu_sched s{};
     s.node = ni;
     if (sched_of.count(ni)) s = sched_of[ni];
+    if (n.kind == LFGPU_OP_GMM && (P->flags & LFGPU_PLAN_TC_SPLIT)) {
+      // fp32-level precision on tensor cores: the node's operands are split
+      // into bf16 pieces concatenated along K (lf_rows.hpp), laid out in
+      // plain GMM bricks; the output keeps the node's own layout.
+      const int64_t M = A.logical[0].extent, K = A.logical[1].extent, N = B.logical[1].extent;
+      const int64_t K6 = kSplitTerms * K, bn = N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : 0;
+      SplitGmm sg;
+      std::string w3;
+      bool ok3 = bn && M % 128 == 0 && K6 % 64 == 0;
+      if (ok3) {
+        sg.a_log = {{"M", M}, {"K", K6}};
+        sg.b_log = {{"K", K6}, {"N", N}};
+        sg.a_seq = {make_split(0, {M / 128, 128}), make_split(2, {K6 / 64, 64}), make_reorder({0, 2, 1, 3})};
+        sg.b_seq = {make_split(0, {K6 / 64, 64}), make_split(2, {N / bn, bn}), make_reorder({0, 2, 1, 3})};
+        lfgpu_sched s3 = s;
+        s3.tile_last = static_cast<int32_t>(bn);
+        ok3 = umma_plan_gemm(sg.a_log, sg.a_seq, sg.b_log, sg.b_seq, Cc.logical, Cc.seq, s3, &up, &w3);
+      }
+      if (ok3) {
+        if (s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL)) {
+          std::vector<EpiOp> epi = fuse_chain(ni, Cc, true);
+          for (const auto& e : epi) up.epi[up.epi_count++] = e;
+        }
+        up.summary += " split=bf16x3";
+        umma[ni] = up;
+        split_gmm[ni] = sg;
+        continue;
+      }
+      if (P->flags & LFGPU_PLAN_REQUIRE_TC)
+        fail(LFGPU_EUNSUPPORTED, "node " + std::to_string(ni) + " not tensor-core legal (split mode): " +
+                                     (w3.empty() ? "needs M % 128, N % 64" : w3));
+      continue;
+    }
     bool ok = n.kind == LFGPU_OP_GMM
                   ? umma_plan_gemm(A.logical, A.seq, B.logical, B.seq, Cc.logical, Cc.seq, s,
                                    &up, &why)
@@ -652,7 +690,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   // 2. Storage decisions: bf16 for tensor-core operands, f32/i32 otherwise.
   for (auto& t : P->t) {
     for (int c : t.consumers) {
-      bool tc_operand = umma.count(c) && (P->nodes[c].inputs[0] == &t - &P->t[0] ||
+      bool tc_operand = umma.count(c) && !split_gmm.count(c) && (P->nodes[c].inputs[0] == &t - &P->t[0] ||
                                           P->nodes[c].inputs[1] == &t - &P->t[0]);
       // A tensor read only as an epilogue residual/bias stays fp32.
       if (tc_operand) t.need_bf16 = true;
@@ -982,6 +1020,51 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           UmmaPlan up = it->second;
           up.a = up.swap_ab ? B.d_bf16 : A.d_bf16;
           up.b = up.swap_ab ? A.d_bf16 : B.d_bf16;
+          SplitParams sa, sb;
+          const bool split3 = split_gmm.count(ni) > 0;
+          if (split3) {
+            const SplitGmm& sg = split_gmm.at(ni);
+            if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "split-precision GMM needs fp32 operands");
+            const int64_t M = A.logical[0].extent, K = A.logical[1].extent, N = B.logical[1].extent;
+            auto dst_tables = [&](const std::vector<Dim>& lg, const Seq& sq, std::vector<int64_t>* r,
+                                  std::vector<int64_t>* c) {
+              std::vector<int64_t> tab, off;
+              if (!separable_tables(lg, sq, &tab, &off)) fail(LFGPU_EINVAL, "split operand layout");
+              r->assign(tab.begin() + off[0], tab.begin() + off[0] + lg[0].extent);
+              c->assign(tab.begin() + off[1], tab.begin() + off[1] + lg[1].extent);
+            };
+            std::vector<int64_t> ar, ac, br, bc, dar, dac, dbr, dbc;
+            row_col_offsets(A, &ar, &ac);
+            row_col_offsets(B, &br, &bc);
+            dst_tables(sg.a_log, sg.a_seq, &dar, &dac);
+            dst_tables(sg.b_log, sg.b_seq, &dbr, &dbc);
+            P->keep.push_back(std::make_unique<DevBuf>(2 * M * kSplitTerms * K));
+            void* a3 = P->keep.back()->p;
+            P->keep.push_back(std::make_unique<DevBuf>(2 * kSplitTerms * K * N));
+            void* b3 = P->keep.back()->p;
+            sa.side = 0;
+            sa.R = M;
+            sa.C = K;
+            sa.K = K;
+            sa.src = static_cast<const float*>(A.d);
+            sa.src_row = upload(P->keep, ar.data(), ar.size());
+            sa.src_col = upload(P->keep, ac.data(), ac.size());
+            sa.dst = a3;
+            sa.dst_row = upload(P->keep, dar.data(), dar.size());
+            sa.dst_col = upload(P->keep, dac.data(), dac.size());
+            sb.side = 1;
+            sb.R = K;
+            sb.C = N;
+            sb.K = K;
+            sb.src = static_cast<const float*>(B.d);
+            sb.src_row = upload(P->keep, br.data(), br.size());
+            sb.src_col = upload(P->keep, bc.data(), bc.size());
+            sb.dst = b3;
+            sb.dst_row = upload(P->keep, dbr.data(), dbr.size());
+            sb.dst_col = upload(P->keep, dbc.data(), dbc.size());
+            up.a = a3;
+            up.b = b3;
+          }
           // The chain's final output is the one written; intermediates of a
           // fused chain are also written when the caller keeps them.
           int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : n.output;
@@ -1011,7 +1094,16 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
             L.w_prewait = L.wres && !P->steps.empty() && W.producer < 0 && !getenv("LFGPU_NO_W_PREWAIT") ? 1 : 0;
           }
           step.kernel = up.kind == UMMA_CONV ? "umma_conv" : "umma_gemm";
-          step.run = [L](cudaStream_t s) { return umma_launch(L, s); };
+          if (split3) {
+            step.launches = 3;
+            step.run = [L, sa, sb](cudaStream_t s) {
+              cudaError_t e = launch_split_bf16(sa, s);
+              if (e == cudaSuccess) e = launch_split_bf16(sb, s);
+              return e != cudaSuccess ? e : umma_launch(L, s);
+            };
+          } else {
+            step.run = [L](cudaStream_t s) { return umma_launch(L, s); };
+          }
           P->tc_nodes += 1;
           P->bytes += A.numel * 2 + B.numel * 2 + P->t[final_t].numel * 4;
           P->summary[ni] = up.summary + " store=" + std::to_string(L.store_mode) +
@@ -1826,7 +1918,7 @@ int lfgpu_interpret(lfgpu_ctx* ctx, const lfgpu_graph* g, int32_t nsched,
                     const lfgpu_sched* sched, int32_t flags, double* const* host_bufs) {
   lfgpu_plan* P = nullptr;
   // Reference semantics unless the caller opts into tensor cores.
-  if (!(flags & (LFGPU_PLAN_TENSOR_CORES | LFGPU_PLAN_REQUIRE_TC))) flags |= LFGPU_PLAN_EXACT;
+  if (!(flags & (LFGPU_PLAN_TENSOR_CORES | LFGPU_PLAN_REQUIRE_TC | LFGPU_PLAN_TC_SPLIT))) flags |= LFGPU_PLAN_EXACT;
   int rc = lfgpu_plan_build(ctx, g, nsched, sched, (flags & ~LFGPU_PLAN_TENSOR_CORES) | LFGPU_PLAN_KEEP_ALL, &P);
   if (rc != LFGPU_OK) return rc;
   rc = guarded([&] {
