@@ -687,6 +687,52 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
     }
   }
 
+  // 1c. LayoutConvert absorbed into its producer (propagation.cpp:265-313
+  // inserts the conversion; the paper's producer-yields-the-consumer's-layout,
+  // PAPER.md:379-381): when the converted tensor is the final tensor of a
+  // tcgen05 contraction (after its fused chain) and feeds only the
+  // conversion, the contraction is re-planned to write the conversion's
+  // layout directly and the conversion step disappears.
+  std::map<int, int> out_redirect;  // umma node -> tensor it writes instead of its chain's final tensor
+  if (!(P->flags & (LFGPU_PLAN_KEEP_ALL | LFGPU_PLAN_EXACT)) && !getenv("LFGPU_NO_CONVERT_ABSORB")) {
+    for (int cn : P->order) {
+      const auto& cnode = P->nodes[cn];
+      if (cnode.kind != LFGPU_OP_LAYOUT_CONVERT || fused_away.count(cn)) continue;
+      const int tin = cnode.inputs[0];
+      const PTensor& T = P->t[tin];
+      if (T.consumers.size() != 1 || T.role == LFGPU_ROLE_OUTPUT) continue;
+      int u = T.producer;
+      while (u >= 0 && fused_away.count(u)) u = P->t[P->nodes[u].inputs[0]].producer;
+      if (u < 0 || !umma.count(u) || absorbed_pad.count(u) || split_gmm.count(u) || out_redirect.count(u)) continue;
+      const UmmaPlan& old = umma[u];
+      const int final_t = old.epi_count ? old.epi[old.epi_count - 1].out_tensor : P->nodes[u].output;
+      if (final_t != tin) continue;
+      bool residual = false;  // a residual operand is read in the output's own layout
+      for (int e = 0; e < old.epi_count; ++e) residual = residual || old.epi[e].kind == EPI_RESIDUAL;
+      if (residual) continue;
+      const auto& un = P->nodes[u];
+      const PTensor& UA = P->t[un.inputs[0]];
+      const PTensor& UB = P->t[un.inputs[1]];
+      const PTensor& U = P->t[cnode.output];
+      lfgpu_sched su{};
+      su.node = u;
+      if (sched_of.count(u)) su = sched_of[u];
+      UmmaPlan np;
+      std::string why;
+      const bool ok = un.kind == LFGPU_OP_GMM
+                          ? umma_plan_gemm(UA.logical, UA.seq, UB.logical, UB.seq, U.logical, U.seq, su, &np, &why)
+                          : umma_plan_conv(UA.logical, UA.seq, UB.logical, UB.seq, U.logical, U.seq, un.stride, su,
+                                           &np, &why);
+      if (!ok) continue;
+      for (int e = 0; e < old.epi_count; ++e) np.epi[e] = old.epi[e];
+      np.epi_count = old.epi_count;
+      np.summary += " (writes " + U.id + ": LayoutConvert absorbed)";
+      umma[u] = np;
+      out_redirect[u] = cnode.output;
+      fused_away.insert(cn);
+    }
+  }
+
   // 2. Storage decisions: bf16 for tensor-core operands, f32/i32 otherwise.
   for (auto& t : P->t) {
     for (int c : t.consumers) {
@@ -709,6 +755,9 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
         t.need_f32 = false;
     }
   }
+  // An absorbed LayoutConvert's output is written by the contraction's
+  // epilogue, which stores fp32 (and the bf16 copy alongside).
+  for (const auto& kv : out_redirect) P->t[kv.second].need_f32 = true;
   for (auto& t : P->t) {
     size_t es = elem_size(t.elem);
     if (t.need_f32 || !t.need_bf16) {
@@ -880,6 +929,10 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           up.a = Q.a;
           up.b = Q.b;
           int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : n.output;
+          if (out_redirect.count(ni)) {  // the absorbed LayoutConvert's output, in its layout
+            P->t[final_t].valid = false;
+            final_t = out_redirect.at(ni);
+          }
           up.out = static_cast<float*>(P->t[final_t].d);
           if (P->t[final_t].d && P->t[final_t].d_bf16 && P->t[final_t].elem == LFGPU_ELEM_F32) {
             up.out_bf16 = P->t[final_t].d_bf16;
@@ -1068,6 +1121,10 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           // The chain's final output is the one written; intermediates of a
           // fused chain are also written when the caller keeps them.
           int final_t = up.epi_count ? up.epi[up.epi_count - 1].out_tensor : n.output;
+          if (out_redirect.count(ni)) {  // the absorbed LayoutConvert's output, in its layout
+            P->t[final_t].valid = false;
+            final_t = out_redirect.at(ni);
+          }
           up.out = static_cast<float*>(P->t[final_t].d);
           if (P->t[final_t].d && P->t[final_t].d_bf16 &&
               P->t[final_t].elem == LFGPU_ELEM_F32) {  // dual store: no shadow pass

@@ -251,3 +251,56 @@ def test_split_precision_chain_interpret():
     for nd in g.nodes:
         d = O.max_rel_diff(got[nd.output], bufs[g.tensor_index(nd.output)])
         assert d <= 1e-4, (nd.output, d)
+
+
+def _gmm_convert_gmm(m=256, k=512, n=256, n2=256):
+    """GMM -> LayoutConvert -> GMM: the conversion the reference planner
+    inserts between two contractions whose brick layouts differ
+    (propagation.cpp:265-313; test_propagation.cpp:140-161 for convs)."""
+    g = ir.Graph()
+    g.tensors = [ir.TensorDecl("a", [("M", m), ("K", k)], ir.INPUT),
+                 ir.TensorDecl("b1", [("K", k), ("N", n)], ir.CONSTANT),
+                 ir.TensorDecl("c1", [("M", m), ("N", n)], ir.INTERMEDIATE),
+                 ir.TensorDecl("c1__cv0", [("M", m), ("N", n)], ir.INTERMEDIATE),
+                 ir.TensorDecl("b2", [("K", n), ("N", n2)], ir.CONSTANT),
+                 ir.TensorDecl("c2", [("M", m), ("N", n2)], ir.OUTPUT)]
+    g.nodes = [ir.OperatorNode(ir.GMM, ["a", "b1"], "c1"),
+               ir.OperatorNode(ir.LAYOUT_CONVERT, ["c1"], "c1__cv0"),
+               ir.OperatorNode(ir.GMM, ["c1__cv0", "b2"], "c2")]
+    return g
+
+
+def test_layout_convert_absorbed_into_producer(monkeypatch):
+    """The producing tcgen05 GEMM writes the conversion's layout itself (the
+    paper's producer-yields-the-consumer's-layout, PAPER.md:379-381): the
+    LayoutConvert step disappears and every value is bit-identical to
+    running it as a K1 step."""
+    g = _gmm_convert_gmm()
+    seqs = runtime.decode_layout(g, 0, [128, 64, 128])
+    s2 = runtime.decode_layout(g, 2, [128, 64, 64])
+    seqs["c1__cv0"], seqs["b2"], seqs["c2"] = s2["c1__cv0"], s2["b2"], s2["c2"]
+    assert seqs["c1"] != seqs["c1__cv0"]
+    bufs = O.random_inputs(g, 9)
+    ins = {t.id: bufs[i].copy() for i, t in enumerate(g.tensors) if t.role in (ir.INPUT, ir.CONSTANT)}
+    O.reference_eval(g, bufs)
+    scheds = [runtime.sched(0, tile_last=64), runtime.sched(2, tile_last=64)]
+    outs = {}
+    for absorb in (True, False):
+        if absorb:
+            monkeypatch.delenv("LFGPU_NO_CONVERT_ABSORB", raising=False)
+        else:
+            monkeypatch.setenv("LFGPU_NO_CONVERT_ABSORB", "1")
+        p = runtime.Plan(g, seqs, scheds, flags=_abi.PLAN_REQUIRE_TC)
+        kinds = [p.node_kernel(i) for i in range(len(g.nodes))]
+        assert (kinds[1] == "fused") == absorb, kinds
+        if absorb:
+            assert "LayoutConvert absorbed" in kinds[0], kinds[0]
+        for kk, v in ins.items():
+            p.set_input(kk, v)
+        p.run()
+        outs[absorb] = p.get_output("c2")
+    assert np.array_equal(outs[True], outs[False])
+    # GMM 2 reads c1 (not k/64 any more) through bf16 operands: normwise
+    # within the chained-bf16 tolerance (2^-9 per rounded operand)
+    ref = bufs[g.tensor_index("c2")]
+    assert np.linalg.norm(outs[True] - ref) / np.linalg.norm(ref) <= 5e-3
