@@ -6,7 +6,7 @@
 //   tune_check host                 hook unset: the hooked tuner equals the
 //                                   unmodified one (simulate_cache) on a
 //                                   small GMM graph (same best cost)
-//   tune_check gpu <cfg> <budget> <mode>
+//   tune_check gpu <cfg> <budget> <mode> [parallel]
 //                                   cfg: cfg1 (Padding -> C2D 64->64 3x3
 //                                   56x56, N=1) | cfg2 (GMM 1024^3);
 //                                   mode: tc (LFGPU_PLAN_REQUIRE_TC: points
@@ -14,7 +14,8 @@
 //                                   counted as rejected and scored with a
 //                                   penalty) | any (the adapter's default:
 //                                   tcgen05 where the layout allows it,
-//                                   CUDA cores otherwise; never rejects).
+//                                   CUDA cores otherwise; never rejects);
+//                                   parallel: TuneOptions::parallel_eval.
 // Prints one JSON line: measurements, rejected, tensor-core plans, best cost
 // (us), wall seconds and candidates/s. Built by tests/test_adapter.py.
 #include <chrono>
@@ -117,19 +118,24 @@ int main(int argc, char** argv) {
   const std::string cfg = argc > 2 ? argv[2] : "cfg2";
   const int total = argc > 3 ? std::atoi(argv[3]) : 64;
   const std::string m = argc > 4 ? argv[4] : "any";
+  // the reference's own parallel lowering + feature extraction (std::async,
+  // tuner.cpp:196-221)
+  const bool par = argc > 5 && std::string(argv[5]) == "parallel";
   g_flags = LFGPU_PLAN_CUDA_GRAPH | (m == "tc" ? LFGPU_PLAN_REQUIRE_TC : 0);
   gpu::Context ctx(0);
   g_ctx = &ctx;
   lf_gpu_measure_hook = gpu_hook;
   Graph g = cfg == "cfg1" ? cfg1() : gmm(1024, 1024, 1024);
   auto t0 = std::chrono::steady_clock::now();
-  TuneResult r = tune(g, budget(total), CacheConfig{});
+  TuneOptions opts;
+  opts.parallel_eval = par;
+  TuneResult r = tune(g, budget(total), CacheConfig{}, opts);
   const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   std::printf(
-      "{\"cfg\": \"%s\", \"mode\": \"%s\", \"budget\": %d, \"measurements\": %d, \"rejected\": %d, "
+      "{\"cfg\": \"%s\", \"mode\": \"%s\", \"parallel_eval\": %d, \"budget\": %d, \"measurements\": %d, \"rejected\": %d, "
       "\"tensor_core_plans\": %d, \"rejected_frac\": %.4f, \"best_cost_us\": %.3f, \"seconds\": %.2f, "
       "\"candidates_per_s\": %.2f}\n",
-      cfg.c_str(), m.c_str(), total, g_calls, g_rejected, g_tc, g_calls ? double(g_rejected) / g_calls : 0.0,
+      cfg.c_str(), m.c_str(), par ? 1 : 0, total, g_calls, g_rejected, g_tc, g_calls ? double(g_rejected) / g_calls : 0.0,
       r.best_cost, secs, secs > 0 ? g_calls / secs : 0.0);
   return (g_calls > 0 && std::isfinite(r.best_cost)) ? 0 : 1;
 }
