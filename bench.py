@@ -565,17 +565,18 @@ def run_ours(args, rank, world, local):
         # LayerNorm and GELU on the op-set extension, GMMs on tcgen05
         try:
             best = None
-            for t in (64, 128):
-                genc, _, pe = e2e.build_encoder(12, t, 0, ctx=ctx)
-                for k, x in e2e.make_encoder_inputs(genc, gen).items():
-                    pe.set_input_device(k, x)
-                me = pe.measure(warmup=3, reps=7, flush_l2=True)
-                if best is None or me.cost < best[0]:
-                    best = (me.cost, t, int(me.kernels))
-                pe.close()
+            for packed in (False, True):  # three q/k/v GMMs, or one packed QKV GMM
+                for t in (64, 128):
+                    genc, _, pe = e2e.build_encoder(12, t, 0, ctx=ctx, packed_qkv=packed)
+                    for k, x in e2e.make_encoder_inputs(genc, gen).items():
+                        pe.set_input_device(k, x)
+                    me = pe.measure(warmup=3, reps=7, flush_l2=True)
+                    if best is None or me.cost < best[0]:
+                        best = (me.cost, t, int(me.kernels), packed)
+                    pe.close()
             fl = workloads.bert_encoder_flops(12)
             sec["bert_base_encoder_seq128_12l"] = {
-                "latency_us": round(best[0], 2), "brick_t": best[1], "launches": best[2],
+                "latency_us": round(best[0], 2), "brick_t": best[1], "launches": best[2], "packed_qkv": best[3],
                 "tflops": round(fl / (best[0] * 1e-6) / 1e12, 2), "gflop": round(fl / 1e9, 3)}
         except Exception as e:
             sec["bert_base_encoder_seq128_12l"] = {"error": str(e)[:200]}

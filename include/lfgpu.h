@@ -82,10 +82,15 @@ enum {
    * LayerNorm: inputs x[.., D], gb[2, D] (row 0 gamma, row 1 beta);
    *            y = (x - mean) / sqrt(var + 10^-eps_exp) * gamma + beta,
    *            mean / biased var over the last dim (eps_exp default 12)
-   * BmmQK:     per-head scores; q[T, H*Dh], k[T', H*Dh] -> s[H, T, T'],
-   *            s[h,i,j] = sum_d q[i, h*Dh+d] * k[j, h*Dh+d]  (attrs heads = H)
-   * BmmPV:     per-head context; p[H, T, T'], v[T', H*Dh] -> o[T, H*Dh],
-   *            o[i, h*Dh+d] = sum_j p[h,i,j] * v[j, h*Dh+d]
+   * BmmQK:     per-head scores; q[T, Cq], k[T', Ck] -> s[H, T, T'],
+   *            s[h,i,j] = sum_d q[i, a0+h*Dh+d] * k[j, b0+h*Dh+d]
+   *            (attrs heads = H, a_col0 = a0, b_col0 = b0, head_dim = Dh;
+   *            head_dim 0 means Dh = Cq / H with Cq == Ck and a0 = b0 = 0).
+   *            With column offsets q and k are slices of one packed QKV
+   *            tensor; a0 + H*Dh <= Cq and b0 + H*Dh <= Ck.
+   * BmmPV:     per-head context; p[H, T, T'], v[T', Cv] -> o[T, H*Dh],
+   *            o[i, h*Dh+d] = sum_j p[h,i,j] * v[j, b0+h*Dh+d]
+   *            (Dh = head_dim, 0 = Cv / H; o has H*Dh columns; b0 + H*Dh <= Cv)
    * Reductions run in index order (d, j ascending), like interp.cpp. */
   LFGPU_OP_GELU = 10,
   LFGPU_OP_SOFTMAX = 11,
@@ -155,6 +160,9 @@ typedef struct lfgpu_node {
   int32_t window; /* MaxPool window (KH = KW); 0 elsewhere */
   int32_t heads;  /* attrs["heads"], BmmQK / BmmPV; 0 elsewhere */
   int32_t eps_exp; /* attrs["eps_exp"], LayerNorm: eps = 10^-eps_exp (default 12) */
+  int32_t a_col0;  /* attrs["a_col0"], BmmQK: first column of q in its operand (packed QKV); 0 elsewhere */
+  int32_t b_col0;  /* attrs["b_col0"], BmmQK / BmmPV: first column of k / v in their operand */
+  int32_t head_dim; /* attrs["head_dim"], BmmQK / BmmPV: Dh (0 = operand width / heads) */
   int64_t stride; /* attrs["stride"], C2D/DEP/MaxPool (default 1) */
   int64_t pad;    /* attrs["pad"], Padding (default 0)    */
 } lfgpu_node;

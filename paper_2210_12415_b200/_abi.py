@@ -75,6 +75,9 @@ class Node(C.Structure):
         ("window", C.c_int32),
         ("heads", C.c_int32),
         ("eps_exp", C.c_int32),
+        ("a_col0", C.c_int32),
+        ("b_col0", C.c_int32),
+        ("head_dim", C.c_int32),
         ("stride", C.c_int64),
         ("pad", C.c_int64),
     ]

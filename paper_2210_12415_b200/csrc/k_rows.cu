@@ -319,6 +319,203 @@ __global__ void __launch_bounds__(256) bmm_pv_kernel(const BmmParams P) {
   }
 }
 
+// Fused attention core: BmmQK -> Softmax -> BmmPV of one head for kAttnRows
+// query rows per CTA, the [rows, T2] scores never leaving shared memory.
+// Every stage repeats the unfused kernels' arithmetic in the same order (QK:
+// acc += q*k over d ascending; softmax: rows_kernel's per-lane partition and
+// xor tree; PV: acc += p*v over j ascending), so for T2 <= 256 (where the
+// unfused softmax is rows_kernel) the output is bit-identical to the
+// three-kernel path. K and V stream through one SMEM chunk of up to 128 rows;
+// the offset tables are staged before the grid-dependency wait (they are
+// plan constants), the operands after it.
+constexpr int kAttnRows = 16;
+constexpr int kAttnChunk = 128;
+
+struct AttnSmem {
+  int chunk, dh, t2;
+  size_t qs, kv, ss, tab, total;
+};
+
+__host__ __device__ inline AttnSmem attn_smem(int T2, int Dh) {
+  AttnSmem L;
+  L.t2 = T2;
+  L.dh = Dh;
+  L.chunk = T2 < kAttnChunk ? ((T2 + 31) / 32) * 32 : kAttnChunk;
+  L.qs = 0;
+  L.kv = L.qs + sizeof(float) * kAttnRows * Dh;
+  L.ss = L.kv + sizeof(float) * L.chunk * (Dh + 1);
+  L.tab = L.ss + sizeof(float) * kAttnRows * T2;
+  L.tab = (L.tab + 15) & ~size_t(15);
+  // kr[T2], vr[T2], qr[rows], orow[rows], qc[Dh], kc[Dh], vc[Dh], oc[Dh]
+  L.total = L.tab + sizeof(int64_t) * (2 * T2 + 2 * kAttnRows + 4 * Dh);
+  return L;
+}
+
+template <typename Acc>
+__global__ void __launch_bounds__(256) attn_kernel(const BmmParams Q, const BmmParams V) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int h = blockIdx.y, i0 = blockIdx.x * kAttnRows;
+  const int T = Q.T, T2 = Q.T2, Dh = Q.Dh;
+  const AttnSmem L = attn_smem(T2, Dh);
+  float* qs = reinterpret_cast<float*>(smem + L.qs);
+  float* kv = reinterpret_cast<float*>(smem + L.kv);
+  float* ss = reinterpret_cast<float*>(smem + L.ss);
+  int64_t* kr = reinterpret_cast<int64_t*>(smem + L.tab);
+  int64_t* vr = kr + T2;
+  int64_t* qr = vr + T2;
+  int64_t* orow = qr + kAttnRows;
+  int64_t* qc = orow + kAttnRows;
+  int64_t* kc = qc + Dh;
+  int64_t* vc = kc + Dh;
+  int64_t* oc = vc + Dh;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int e = t; e < T2; e += 256) {
+    kr[e] = __ldg(Q.tb + Q.b_off[0] + e);
+    vr[e] = __ldg(V.tb + V.b_off[0] + e);
+  }
+  if (t < kAttnRows) {
+    qr[t] = i0 + t < T ? __ldg(Q.ta + Q.a_off[0] + i0 + t) : 0;
+    orow[t] = i0 + t < T ? __ldg(V.to + V.o_off[0] + i0 + t) : 0;
+  }
+  for (int e = t; e < Dh; e += 256) {
+    qc[e] = __ldg(Q.ta + Q.a_off[1] + h * Dh + e);
+    kc[e] = __ldg(Q.tb + Q.b_off[1] + h * Dh + e);
+    vc[e] = __ldg(V.tb + V.b_off[1] + h * Dh + e);
+    oc[e] = __ldg(V.to + V.o_off[1] + h * Dh + e);
+  }
+  LFG_PDL_ENTRY();
+  __syncthreads();
+  // q rows: up to 16 x 128 elements, 8 loads per thread in flight
+  {
+    constexpr int kPer = kAttnRows * kMaxDh / 256;
+    float qv[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = t + 256 * u, r = e / Dh, c = e - r * Dh;
+      qv[u] = e < kAttnRows * Dh && i0 + r < T ? __ldg(Q.a + qr[r] + qc[c]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+      if (t + 256 * u < kAttnRows * Dh) qs[t + 256 * u] = qv[u];
+  }
+  // one chunk of K (mode 0) or V (mode 1) rows into kv[chunk][Dh + 1]:
+  // 16 loads per thread in flight per batch
+  auto load_chunk = [&](int j0, int mode) {
+    const float* src = mode == 0 ? Q.b : V.b;
+    const int64_t* rows = mode == 0 ? kr : vr;
+    const int64_t* cols = mode == 0 ? kc : vc;
+    const int n = L.chunk * Dh;
+    for (int b0 = 0; b0 < n; b0 += 256 * 16) {
+      float x[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = b0 + t + 256 * u, r = e / Dh, c = e - r * Dh;
+        x[u] = e < n && j0 + r < T2 ? __ldg(src + rows[j0 + r] + cols[c]) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = b0 + t + 256 * u, r = e / Dh, c = e - r * Dh;
+        if (e < n) kv[r * (Dh + 1) + c] = x[u];
+      }
+    }
+  };
+  // scores: thread (w, lane) owns rows w, w+8 and chunk columns lane + 32m
+  for (int j0 = 0; j0 < T2; j0 += L.chunk) {
+    __syncthreads();
+    load_chunk(j0, 0);
+    __syncthreads();
+    Acc acc[2][kAttnChunk / 32];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int m = 0; m < kAttnChunk / 32; ++m) acc[r][m] = 0;
+    const int nm = L.chunk / 32;
+    for (int c = 0; c < Dh; ++c) {
+      const float q0 = qs[w * Dh + c], q1 = qs[(w + 8) * Dh + c];
+#pragma unroll
+      for (int m = 0; m < kAttnChunk / 32; ++m)
+        if (m < nm) {
+          const float kx = kv[(lane + 32 * m) * (Dh + 1) + c];
+          acc[0][m] += static_cast<Acc>(q0) * kx;
+          acc[1][m] += static_cast<Acc>(q1) * kx;
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < kAttnChunk / 32; ++m) {
+      const int j = j0 + lane + 32 * m;
+      if (m < nm && j < T2) {
+        ss[w * T2 + j] = static_cast<float>(acc[0][m]);
+        ss[(w + 8) * T2 + j] = static_cast<float>(acc[1][m]);
+      }
+    }
+  }
+  __syncthreads();
+  // softmax over each row: warp w owns rows w, w+8 (rows_kernel's arithmetic)
+  constexpr int kNC = kMaxT2 / 32;
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    float* row = ss + (w + 8 * rr) * T2;
+    float v[kNC];
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kNC; ++k) {
+      const int j = lane + 32 * k;
+      v[k] = j < T2 ? row[j] : 0.f;
+      if (j < T2) m = fmaxf(m, v[k]);
+    }
+    m = warp_max(m);
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < kNC; ++k)
+      if (lane + 32 * k < T2) {
+        v[k] = expf(v[k] - m);
+        sum += v[k];
+      }
+    const float inv = 1.f / warp_sum(sum);
+#pragma unroll
+    for (int k = 0; k < kNC; ++k)
+      if (lane + 32 * k < T2) row[lane + 32 * k] = v[k] * inv;
+  }
+  // context: thread (w, lane) owns rows w, w+8 and columns lane + 32m
+  Acc acc[2][kMaxDh / 32];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int m = 0; m < kMaxDh / 32; ++m) acc[r][m] = 0;
+  const int nd = (Dh + 31) / 32;
+  for (int j0 = 0; j0 < T2; j0 += L.chunk) {
+    __syncthreads();
+    load_chunk(j0, 1);
+    __syncthreads();
+    const int jn = min(L.chunk, T2 - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      const float p0 = ss[w * T2 + j0 + jj], p1 = ss[(w + 8) * T2 + j0 + jj];
+#pragma unroll
+      for (int m = 0; m < kMaxDh / 32; ++m)
+        if (m < nd && lane + 32 * m < Dh) {
+          const float vx = kv[jj * (Dh + 1) + lane + 32 * m];
+          acc[0][m] += static_cast<Acc>(p0) * vx;
+          acc[1][m] += static_cast<Acc>(p1) * vx;
+        }
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int r = w + 8 * rr;
+    if (i0 + r >= T) continue;
+#pragma unroll
+    for (int m = 0; m < kMaxDh / 32; ++m) {
+      const int c = lane + 32 * m;
+      if (m < nd && c < Dh) {
+        const int64_t o = orow[r] + oc[c];
+        const float y = static_cast<float>(acc[rr][m]);
+        V.out[o] = y;
+        if (V.out_bf16) static_cast<__nv_bfloat16*>(V.out_bf16)[o] = __float2bfloat16_rn(y);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) split_bf16_kernel(const SplitParams P) {
   LFG_PDL_ENTRY();
   // piece index per term, smallest products first (x2y0, x1y1, x0y2, x1y0,
@@ -378,6 +575,25 @@ cudaError_t launch_bmm(const BmmParams& P, bool exact, cudaStream_t stream) {
   dim3 grid((P.T + kTile - 1) / kTile, P.H, 2);
   return exact ? launch_pdl(bmm_pv_kernel<double>, grid, dim3(256), 0, stream, P)
                : launch_pdl(bmm_pv_kernel<float>, grid, dim3(256), 0, stream, P);
+}
+
+size_t attn_smem_bytes(int T2, int Dh) { return attn_smem(T2, Dh).total; }
+
+cudaError_t launch_attention(const BmmParams& QK, const BmmParams& PV, bool exact, cudaStream_t stream) {
+  if (QK.Dh > kMaxDh || QK.Dh < 1 || QK.T2 > kMaxT2 || QK.T2 < 1 || PV.Dh != QK.Dh) return cudaErrorInvalidValue;
+  const size_t smem = attn_smem(QK.T2, QK.Dh).total;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[exact]) {
+    cudaError_t e = exact ? cudaFuncSetAttribute(attn_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(attn_smem(kMaxT2, kMaxDh).total))
+                          : cudaFuncSetAttribute(attn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(attn_smem(kMaxT2, kMaxDh).total));
+    if (e != cudaSuccess) return e;
+    attr_set[exact] = true;
+  }
+  const dim3 grid((QK.T + kAttnRows - 1) / kAttnRows, QK.H);
+  return exact ? launch_pdl(attn_kernel<double>, grid, dim3(256), smem, stream, QK, PV)
+               : launch_pdl(attn_kernel<float>, grid, dim3(256), smem, stream, QK, PV);
 }
 
 }  // namespace lfg

@@ -733,6 +733,33 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
     }
   }
 
+  // 1d. Attention fusion: BmmQK -> Softmax -> BmmPV whose scores and
+  // probabilities are single-consumer intermediates runs as one kernel
+  // (k_rows.cu attn_kernel) at the BmmPV's position; s and p are never
+  // materialized. The shapes are checked when the BmmPV step is built.
+  std::map<int, int> attn_of;  // BmmPV node -> its BmmQK node
+  if (!(P->flags & LFGPU_PLAN_KEEP_ALL) && !getenv("LFGPU_NO_ATTN_FUSE")) {
+    for (int qn = 0; qn < static_cast<int>(P->nodes.size()); ++qn) {
+      const auto& qk = P->nodes[qn];
+      if (qk.kind != LFGPU_OP_BMM_QK) continue;
+      const PTensor& S = P->t[qk.output];
+      if (S.role != LFGPU_ROLE_INTERMEDIATE || S.consumers.size() != 1) continue;
+      const auto& sm = P->nodes[S.consumers[0]];
+      if (sm.kind != LFGPU_OP_SOFTMAX || sm.inputs[0] != qk.output) continue;
+      const PTensor& Pr = P->t[sm.output];
+      if (Pr.role != LFGPU_ROLE_INTERMEDIATE || Pr.consumers.size() != 1) continue;
+      const int pn = Pr.consumers[0];
+      const auto& pv = P->nodes[pn];
+      if (pv.kind != LFGPU_OP_BMM_PV || pv.inputs[0] != sm.output || pv.heads != qk.heads) continue;
+      if (S.logical.size() != 3 || S.logical[2].extent > 512) continue;
+      attn_of[pn] = qn;
+      fused_away.insert(qn);
+      fused_away.insert(S.consumers[0]);
+      P->t[qk.output].valid = false;  // never allocated or written
+      P->t[sm.output].valid = false;
+    }
+  }
+
   // 2. Storage decisions: bf16 for tensor-core operands, f32/i32 otherwise.
   for (auto& t : P->t) {
     for (int c : t.consumers) {
@@ -759,6 +786,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   // epilogue, which stores fp32 (and the bf16 copy alongside).
   for (const auto& kv : out_redirect) P->t[kv.second].need_f32 = true;
   for (auto& t : P->t) {
+    if (!t.valid) continue;  // fused away before storage (attention scores)
     size_t es = elem_size(t.elem);
     if (t.need_f32 || !t.need_bf16) {
       P->keep.push_back(std::make_unique<DevBuf>(es * t.numel));
@@ -795,6 +823,68 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
     sh.kernel = "bf16_shadow";
     sh.run = [k, src, dst, d_err](cudaStream_t s) { return run_copy(k, src, dst, d_err, s); };
     P->steps.push_back(std::move(sh));
+  };
+
+  // Batched-matmul parameters of node bn (BmmQK / BmmPV): shape checks,
+  // separable tables, column slices.
+  auto bmm_params = [&](int bn) {
+    const auto& n = P->nodes[bn];
+    const PTensor& out = P->t[n.output];
+    const PTensor& A = P->t[n.inputs[0]];
+    const PTensor& B = P->t[n.inputs[1]];
+    const int64_t H = n.heads;
+    if (H < 1) fail(LFGPU_EINVAL, "batched matmul needs heads >= 1");
+    if ((!A.d && A.valid) || !B.d) fail(LFGPU_EUNSUPPORTED, "batched matmul reads f32 operands");
+    if (out.dtype != LFGPU_DTYPE_F32) fail(LFGPU_EUNSUPPORTED, "batched matmul is defined for f32 only");
+    BmmParams M;
+    M.mode = n.kind == LFGPU_OP_BMM_QK ? 0 : 1;
+    M.H = static_cast<int32_t>(H);
+    if (n.kind == LFGPU_OP_BMM_QK) {  // q [T, Cq], k [T2, Ck] -> s [H, T, T2]
+      if (A.logical.size() != 2 || B.logical.size() != 2 || out.logical.size() != 3 ||
+          out.logical[0].extent != H || out.logical[1].extent != A.logical[0].extent ||
+          out.logical[2].extent != B.logical[0].extent)
+        fail(LFGPU_EINVAL, "BmmQK shapes: q [T, Cq], k [T2, Ck] -> s [H, T, T2]");
+      int64_t dh = n.head_dim;
+      if (dh == 0) {
+        if (A.logical[1].extent != B.logical[1].extent || A.logical[1].extent % H || n.a_col0 || n.b_col0)
+          fail(LFGPU_EINVAL, "BmmQK without head_dim: q [T, H*Dh], k [T2, H*Dh], no column offsets");
+        dh = A.logical[1].extent / H;
+      }
+      if (n.a_col0 < 0 || n.b_col0 < 0 || n.a_col0 + H * dh > A.logical[1].extent ||
+          n.b_col0 + H * dh > B.logical[1].extent)
+        fail(LFGPU_EINVAL, "BmmQK column slice out of range");
+      M.T = static_cast<int32_t>(A.logical[0].extent);
+      M.T2 = static_cast<int32_t>(B.logical[0].extent);
+      M.Dh = static_cast<int32_t>(dh);
+    } else {  // p [H, T, T2], v [T2, Cv] -> o [T, H*Dh]
+      if (A.logical.size() != 3 || B.logical.size() != 2 || out.logical.size() != 2 ||
+          A.logical[0].extent != H || A.logical[2].extent != B.logical[0].extent ||
+          out.logical[1].extent % H || out.logical[0].extent != A.logical[1].extent || n.a_col0 ||
+          n.b_col0 < 0 || n.b_col0 + out.logical[1].extent > B.logical[1].extent)
+        fail(LFGPU_EINVAL, "BmmPV shapes: p [H, T, T2], v [T2, Cv] -> o [T, H*Dh], b_col0 + H*Dh <= Cv");
+      M.T = static_cast<int32_t>(A.logical[1].extent);
+      M.T2 = static_cast<int32_t>(A.logical[2].extent);
+      M.Dh = static_cast<int32_t>(out.logical[1].extent / H);
+      if ((n.head_dim && n.head_dim != M.Dh) || (!n.head_dim && out.logical[1].extent != B.logical[1].extent))
+        fail(LFGPU_EINVAL, "BmmPV: o columns must be heads * head_dim (head_dim 0: o and v equally wide)");
+    }
+    if (M.Dh > 128 || M.Dh % 2) fail(LFGPU_EUNSUPPORTED, "batched matmul head dim must be even and <= 128");
+    if (M.mode == 1 && M.T2 > 512) fail(LFGPU_EUNSUPPORTED, "BmmPV reduction length > 512");
+    std::vector<int64_t> oa, ob, oo;
+    M.ta = tables_for(P, A, &oa);
+    M.tb = tables_for(P, B, &ob);
+    M.to = tables_for(P, out, &oo);
+    for (size_t j = 0; j < oa.size() && j < 3; ++j) M.a_off[j] = oa[j];
+    for (size_t j = 0; j < ob.size() && j < 3; ++j) M.b_off[j] = ob[j];
+    // packed operands: a column slice is the same column table entered
+    // a_col0 / b_col0 entries later
+    if (n.kind == LFGPU_OP_BMM_QK) M.a_off[1] += n.a_col0;
+    M.b_off[1] += n.b_col0;
+    for (size_t j = 0; j < oo.size() && j < 3; ++j) M.o_off[j] = oo[j];
+    M.a = static_cast<const float*>(A.d);
+    M.b = static_cast<const float*>(B.d);
+    M.out = static_cast<float*>(out.d);
+    return M;
   };
 
   // 3. One step per node.
@@ -1280,54 +1370,31 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
       }
       case LFGPU_OP_BMM_QK:
       case LFGPU_OP_BMM_PV: {
-        const PTensor& A = P->t[n.inputs[0]];
-        const PTensor& B = P->t[n.inputs[1]];
-        const int64_t H = n.heads;
-        if (H < 1) fail(LFGPU_EINVAL, "batched matmul needs heads >= 1");
-        if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "batched matmul reads f32 operands");
-        if (out.dtype != LFGPU_DTYPE_F32) fail(LFGPU_EUNSUPPORTED, "batched matmul is defined for f32 only");
-        BmmParams M;
-        M.mode = n.kind == LFGPU_OP_BMM_QK ? 0 : 1;
-        M.H = static_cast<int32_t>(H);
-        if (n.kind == LFGPU_OP_BMM_QK) {  // q [T, H*Dh], k [T2, H*Dh] -> s [H, T, T2]
-          if (A.logical.size() != 2 || B.logical.size() != 2 || out.logical.size() != 3 ||
-              A.logical[1].extent != B.logical[1].extent || A.logical[1].extent % H ||
-              out.logical[0].extent != H || out.logical[1].extent != A.logical[0].extent ||
-              out.logical[2].extent != B.logical[0].extent)
-            fail(LFGPU_EINVAL, "BmmQK shapes: q [T, H*Dh], k [T2, H*Dh] -> s [H, T, T2]");
-          M.T = static_cast<int32_t>(A.logical[0].extent);
-          M.T2 = static_cast<int32_t>(B.logical[0].extent);
-          M.Dh = static_cast<int32_t>(A.logical[1].extent / H);
-        } else {  // p [H, T, T2], v [T2, H*Dh] -> o [T, H*Dh]
-          if (A.logical.size() != 3 || B.logical.size() != 2 || out.logical.size() != 2 ||
-              A.logical[0].extent != H || A.logical[2].extent != B.logical[0].extent ||
-              B.logical[1].extent % H || out.logical[0].extent != A.logical[1].extent ||
-              out.logical[1].extent != B.logical[1].extent)
-            fail(LFGPU_EINVAL, "BmmPV shapes: p [H, T, T2], v [T2, H*Dh] -> o [T, H*Dh]");
-          M.T = static_cast<int32_t>(A.logical[1].extent);
-          M.T2 = static_cast<int32_t>(A.logical[2].extent);
-          M.Dh = static_cast<int32_t>(B.logical[1].extent / H);
-        }
-        if (M.Dh > 128 || M.Dh % 2) fail(LFGPU_EUNSUPPORTED, "batched matmul head dim must be even and <= 128");
-        if (M.mode == 1 && M.T2 > 512) fail(LFGPU_EUNSUPPORTED, "BmmPV reduction length > 512");
-        std::vector<int64_t> oa, ob, oo;
-        M.ta = tables_for(P, A, &oa);
-        M.tb = tables_for(P, B, &ob);
-        M.to = tables_for(P, out, &oo);
-        for (size_t j = 0; j < oa.size() && j < 3; ++j) M.a_off[j] = oa[j];
-        for (size_t j = 0; j < ob.size() && j < 3; ++j) M.b_off[j] = ob[j];
-        for (size_t j = 0; j < oo.size() && j < 3; ++j) M.o_off[j] = oo[j];
-        M.a = static_cast<const float*>(A.d);
-        M.b = static_cast<const float*>(B.d);
-        M.out = static_cast<float*>(out.d);
+        BmmParams M = bmm_params(ni);
         if (out.d_bf16) {
           M.out_bf16 = out.d_bf16;
           out.shadow_by_producer = true;
         }
+        const PTensor& A = P->t[n.inputs[0]];
+        P->bytes += (n.kind == LFGPU_OP_BMM_QK ? (int64_t(M.T) + M.T2) * M.H * M.Dh
+                                               : A.numel + int64_t(M.T2) * M.H * M.Dh) * 4 +
+                    out.numel * 4;
+        P->flops += 2 * static_cast<int64_t>(M.H) * M.T * M.T2 * M.Dh;
+        if (n.kind == LFGPU_OP_BMM_PV && attn_of.count(ni)) {
+          // the fused attention core: QK's operands, PV's v and output
+          const int qn = attn_of.at(ni);
+          const BmmParams Q = bmm_params(qn);
+          if (Q.T2 != M.T2 || Q.T != M.T || Q.Dh != M.Dh)
+            fail(LFGPU_EINVAL, "attention: BmmQK / BmmPV shapes disagree");
+          P->bytes -= A.numel * 4;  // p is never read from memory
+          P->flops += 2 * static_cast<int64_t>(Q.H) * Q.T * Q.T2 * Q.Dh;
+          P->bytes += (int64_t(Q.T) + Q.T2) * Q.H * Q.Dh * 4;
+          step.kernel = "attention";
+          step.run = [Q, M, exact](cudaStream_t s) { return launch_attention(Q, M, exact, s); };
+          break;
+        }
         step.kernel = n.kind == LFGPU_OP_BMM_QK ? "bmm_qk" : "bmm_pv";
         step.run = [M, exact](cudaStream_t s) { return launch_bmm(M, exact, s); };
-        P->flops += 2 * static_cast<int64_t>(M.H) * M.T * M.T2 * M.Dh;
-        P->bytes += A.numel * 4 + B.numel * 4 + out.numel * 4;
         break;
       }
       case LFGPU_OP_MAXPOOL:
@@ -1824,7 +1891,7 @@ int lfgpu_plan_get_output(lfgpu_plan* plan, int32_t tensor, double* host_logical
     PTensor& t = plan->t.at(tensor);
     if (n != numel(t.logical)) fail(LFGPU_EINVAL, "output size mismatch for '" + t.id + "'");
     if (!t.valid)
-      fail(LFGPU_EUNSUPPORTED, "'" + t.id + "' was fused into an epilogue and not materialized");
+      fail(LFGPU_EUNSUPPORTED, "'" + t.id + "' was fused away (epilogue or attention core) and not materialized");
     if (!t.out_copy_ready) {
       CopySpec spec;
       spec.lmap = identity_map(t.logical);

@@ -87,13 +87,19 @@ def reference(g, ins, tc_nodes=frozenset(), emulate=False):
             eps = 10.0 ** -nd.attr("eps_exp", 12)
             r = rf((x - mu) / torch.sqrt(var + eps) * a[1][0] + a[1][1])
         elif nd.kind == ir.BMM_QK:
-            H = nd.attr("heads", 1)
+            H, dh = nd.attr("heads", 1), nd.attr("head_dim", 0)
             q, k = a[0], a[1]
-            r = rf(torch.einsum("ihd,jhd->hij", q.view(q.shape[0], H, -1), k.view(k.shape[0], H, -1)))
+            if dh:  # column slices of packed operands
+                a0, b0 = nd.attr("a_col0", 0), nd.attr("b_col0", 0)
+                q, k = q[:, a0:a0 + H * dh], k[:, b0:b0 + H * dh]
+            r = rf(torch.einsum("ihd,jhd->hij", q.reshape(q.shape[0], H, -1), k.reshape(k.shape[0], H, -1)))
         elif nd.kind == ir.BMM_PV:
-            H = nd.attr("heads", 1)
+            H, dh = nd.attr("heads", 1), nd.attr("head_dim", 0)
             pr, vv = a[0], a[1]
-            o = torch.einsum("hij,jhd->ihd", pr, vv.view(vv.shape[0], H, -1))
+            if dh:
+                b0 = nd.attr("b_col0", 0)
+                vv = vv[:, b0:b0 + H * dh]
+            o = torch.einsum("hij,jhd->ihd", pr, vv.reshape(vv.shape[0], H, -1))
             r = rf(o.reshape(o.shape[0], -1))
         else:
             raise ValueError(nd.kind)
@@ -143,10 +149,17 @@ def make_encoder_inputs(g, gen, head_dim=64):
         if t.role not in (ir.INPUT, ir.CONSTANT):
             continue
         q = qs if "_q_" in t.id else 1.0
+        packed = "_qkv_" in t.id  # packed [., 3*hidden]: the query third carries the scale
         if t.id.endswith("_w"):
-            out[t.id] = k64(t.extents, gen, q * 2.0 ** -round(math.log2(math.sqrt(t.extents[0]))))
+            w = k64(t.extents, gen, q * 2.0 ** -round(math.log2(math.sqrt(t.extents[0]))))
+            if packed:
+                w[:, :t.extents[1] // 3] *= qs
+            out[t.id] = w
         elif t.id.endswith("_b"):
-            out[t.id] = k64(t.extents, gen, q / 8)
+            bb = k64(t.extents, gen, q / 8)
+            if packed:
+                bb[:t.extents[0] // 3] *= qs
+            out[t.id] = bb
         elif t.id.endswith("_gb"):
             gb = k64(t.extents, gen, 1.0 / 8)
             gb[0] += 1.0
@@ -157,13 +170,13 @@ def make_encoder_inputs(g, gen, head_dim=64):
 
 
 def build_encoder(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH, seq=128, hidden=768, heads=12,
-                  ffn=3072):
+                  ffn=3072, packed_qkv=False):
     """cfg5 as a full BERT-base encoder (workloads.bert_encoder): every GMM
     on tcgen05 in GMM brick layouts (m_t = seq, k_t = n_t = t) with its
     BiasAdd / residual EwAdd / GELU fused into the epilogue; attention
     (BmmQK, Softmax, BmmPV) and LayerNorm read and write those bricks
     through separable offset tables."""
-    g, gmms = workloads.bert_encoder(layers, seq, hidden, heads, ffn)
+    g, gmms = workloads.bert_encoder(layers, seq, hidden, heads, ffn, packed_qkv)
     seqs, scheds = {}, []
     for ni in gmms:
         nd = g.nodes[ni]

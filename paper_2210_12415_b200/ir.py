@@ -116,6 +116,12 @@ class Graph:
                 attrs["window"] = nd.window
             if nd.kind in (BMM_QK, BMM_PV):
                 attrs["heads"] = nd.heads
+                if nd.a_col0:
+                    attrs["a_col0"] = nd.a_col0
+                if nd.b_col0:
+                    attrs["b_col0"] = nd.b_col0
+                if nd.head_dim:
+                    attrs["head_dim"] = nd.head_dim
             if nd.kind == LAYERNORM:
                 attrs["eps_exp"] = nd.eps_exp
             if nd.kind == PADDING:
@@ -161,6 +167,9 @@ class CGraph:
             d.window = int(n.attr("window", 0))
             d.heads = int(n.attr("heads", 0))
             d.eps_exp = int(n.attr("eps_exp", 12 if n.kind == LAYERNORM else 0))
+            d.a_col0 = int(n.attr("a_col0", 0))
+            d.b_col0 = int(n.attr("b_col0", 0))
+            d.head_dim = int(n.attr("head_dim", 0))
         items = [(k, v) for k, v in seqs.items() if v]
         self.prim_arrays = []
         self.seqs = (_abi.Seq * max(1, len(items)))()

@@ -299,7 +299,8 @@ def infer_shapes(g: ir.Graph) -> ir.Graph:
         elif k == ir.BMM_QK:
             shape = [n.attr("heads", 1), a[0], b[0]]
         elif k == ir.BMM_PV:
-            shape = [a[1], b[1]]
+            dh = n.attr("head_dim", 0)
+            shape = [a[1], n.attr("heads", 1) * dh if dh else b[1]]
         else:  # element-wise, LayoutConvert, Softmax, LayerNorm
             shape = list(a)
         out = g.tensor(n.output)

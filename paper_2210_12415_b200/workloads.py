@@ -106,7 +106,7 @@ def bert_chain(layers=12, seq=128, hidden=768, ffn=3072, qkv=2304):
 BERT_FLOPS_PER_LAYER = 2.0 * 128 * (768 * 2304 + 768 * 768 + 768 * 3072 + 3072 * 768)
 
 
-def bert_encoder(layers=12, seq=128, hidden=768, heads=12, ffn=3072):
+def bert_encoder(layers=12, seq=128, hidden=768, heads=12, ffn=3072, packed_qkv=False):
     """cfg5 as a real BERT-base encoder (post-LN, as in BERT) on the op-set
     extension (lfgpu.h: GELU, Softmax, LayerNorm, BmmQK, BmmPV). Per layer,
     on h[seq, hidden]:
@@ -116,6 +116,10 @@ def bert_encoder(layers=12, seq=128, hidden=768, heads=12, ffn=3072):
       c       = BmmPV(p, v)                   [seq, hidden]
       h1      = LayerNorm(GMM(c, Wo) + bo + h)
       h'      = LayerNorm(GELU(GMM(h1, W1) + b1) @ W2 + b2 + h1)
+    packed_qkv: one GMM(h, Wqkv[hidden, 3*hidden]) + bqkv instead of three;
+    BmmQK reads q and k, BmmPV reads v as column slices of it (a_col0 /
+    b_col0 / head_dim) — the same arithmetic per element, 2 fewer launches
+    per layer.
     Returns (graph, gmm node indices)."""
     b = Builder()
     I, C, O = ir.INPUT, ir.CONSTANT, ir.OUTPUT
@@ -139,12 +143,20 @@ def bert_encoder(layers=12, seq=128, hidden=768, heads=12, ffn=3072):
     h = mat("h0", seq, hidden, I)
     for l in range(layers):
         last = l == layers - 1
-        q = linear(f"l{l}_q", h, hidden, hidden)
-        k = linear(f"l{l}_k", h, hidden, hidden)
-        v = linear(f"l{l}_v", h, hidden, hidden)
-        s_ = b.op(ir.BMM_QK, [q, k], b.t(f"l{l}_s", [("H", heads), ("M", seq), ("T", seq)]), heads=heads)
-        p_ = b.op(ir.SOFTMAX, [s_], b.t(f"l{l}_p", [("H", heads), ("M", seq), ("T", seq)]))
-        c = b.op(ir.BMM_PV, [p_, v], mat(f"l{l}_c", seq, hidden), heads=heads)
+        dh = hidden // heads
+        if packed_qkv:
+            qkv = linear(f"l{l}_qkv", h, hidden, 3 * hidden)
+            s_ = b.op(ir.BMM_QK, [qkv, qkv], b.t(f"l{l}_s", [("H", heads), ("M", seq), ("T", seq)]), heads=heads,
+                      a_col0=0, b_col0=hidden, head_dim=dh)
+            p_ = b.op(ir.SOFTMAX, [s_], b.t(f"l{l}_p", [("H", heads), ("M", seq), ("T", seq)]))
+            c = b.op(ir.BMM_PV, [p_, qkv], mat(f"l{l}_c", seq, hidden), heads=heads, b_col0=2 * hidden, head_dim=dh)
+        else:
+            q = linear(f"l{l}_q", h, hidden, hidden)
+            k = linear(f"l{l}_k", h, hidden, hidden)
+            v = linear(f"l{l}_v", h, hidden, hidden)
+            s_ = b.op(ir.BMM_QK, [q, k], b.t(f"l{l}_s", [("H", heads), ("M", seq), ("T", seq)]), heads=heads)
+            p_ = b.op(ir.SOFTMAX, [s_], b.t(f"l{l}_p", [("H", heads), ("M", seq), ("T", seq)]))
+            c = b.op(ir.BMM_PV, [p_, v], mat(f"l{l}_c", seq, hidden), heads=heads)
         ao = linear(f"l{l}_ao", c, hidden, hidden)
         a = b.op(ir.EWADD, [ao, h], mat(f"l{l}_a", seq, hidden))
         h1 = layernorm(f"l{l}_ln1", a, f"l{l}_h1")

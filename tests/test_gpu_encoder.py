@@ -85,11 +85,79 @@ def test_attention_core(layout):
         "c": _brick(T, D, 128, 64), "p": [split(2, [4, 32]), reorder([0, 2, 1, 3])]}
     # scores of O(1): k/64 inputs scaled like q / sqrt(Dh)
     ins, ref = _oracle(g, 12, {"q": 0.25, "k": 0.25})
-    p = _run(g, seqs, ins)
-    assert [p.node_kernel(i) for i in range(3)] == ["bmm_qk", "rows_softmax", "bmm_pv"]
+    _check_attention(g, seqs, ins, ref)
+
+
+def _check_attention(g, seqs, ins, ref):
+    """Three kernels when every tensor is kept (s, p checked), one fused
+    attention kernel otherwise (s, p never materialized); the fused output is
+    bit-identical to the three-kernel one (same arithmetic, same order, T2 <=
+    256) and both meet the oracle's 1e-5."""
+    p3 = _run(g, seqs, ins, flags=_abi.PLAN_KEEP_ALL)
+    assert [p3.node_kernel(i) for i in range(3)] == ["bmm_qk", "rows_softmax", "bmm_pv"]
     for t in ("s", "p", "c"):
-        d = O.max_rel_diff(p.get_output(t), ref[t])
+        d = O.max_rel_diff(p3.get_output(t), ref[t])
         assert d <= 1e-5, (t, d)
+    p1 = _run(g, seqs, ins)
+    assert [p1.node_kernel(i) for i in range(3)] == ["fused", "fused", "attention"]
+    c1, c3 = p1.get_output("c"), p3.get_output("c")
+    assert O.max_rel_diff(c1, ref["c"]) <= 1e-5
+    assert np.array_equal(c1, c3)
+    with pytest.raises(runtime.LfError, match="not materialized"):
+        p1.get_output("s")
+    for e in (True, False):  # exact mode: double accumulation, same structure
+        pe = _run(g, seqs, ins, flags=_abi.PLAN_EXACT | (_abi.PLAN_KEEP_ALL if e else 0))
+        assert pe.node_kernel(2) == ("bmm_pv" if e else "attention")
+        assert O.max_rel_diff(pe.get_output("c"), ref["c"]) <= 1e-5
+
+
+@pytest.mark.parametrize("layout", ["logical", "brick"])
+def test_attention_core_packed_qkv(layout):
+    """BmmQK / BmmPV reading q, k, v as column slices of one packed
+    [T, 3*H*Dh] tensor (a_col0 / b_col0 / head_dim), in the logical layout
+    and in the packed QKV GEMM's brick layout."""
+    T, H, Dh = 128, 12, 64
+    D = H * Dh
+    g = _graph([("qkv", [("M", T), ("N", 3 * D)], ir.INPUT),
+                ("s", [("H", H), ("M", T), ("T", T)], ir.INTERMEDIATE),
+                ("p", [("H", H), ("M", T), ("T", T)], ir.INTERMEDIATE),
+                ("c", [("M", T), ("N", D)], ir.OUTPUT)],
+               [(ir.BMM_QK, ["qkv", "qkv"], "s", {"heads": H, "a_col0": 0, "b_col0": D, "head_dim": Dh}),
+                (ir.SOFTMAX, ["s"], "p"),
+                (ir.BMM_PV, ["p", "qkv"], "c", {"heads": H, "b_col0": 2 * D, "head_dim": Dh})])
+    seqs = {} if layout == "logical" else {"qkv": _brick(T, 3 * D, 128, 128), "c": _brick(T, D, 128, 64)}
+    ins, ref = _oracle(g, 14, {"qkv": 0.25})
+    _check_attention(g, seqs, ins, ref)
+    # a slice past the operand's columns is the planner's EINVAL
+    g.nodes[2].attrs["b_col0"] = 2 * D + 2
+    with pytest.raises(runtime.LfError):
+        runtime.Plan(g, seqs, [], flags=_abi.PLAN_DEFAULT)
+
+
+@pytest.mark.parametrize("T,T2,H,Dh", [(40, 72, 3, 32), (128, 384, 2, 128), (16, 512, 1, 16)])
+def test_attention_fused_shapes(T, T2, H, Dh):
+    """The fused kernel's edges: ragged query blocks (T % 16), K / V chunks
+    that do not divide T2, the largest T2 (512) and Dh (128); T2 > 256 uses
+    the CTA-per-row softmax unfused, so fused vs unfused is held to 1e-6
+    there instead of bit equality."""
+    D = H * Dh
+    g = _graph([("q", [("M", T), ("N", D)], ir.INPUT), ("k", [("M", T2), ("N", D)], ir.INPUT),
+                ("v", [("M", T2), ("N", D)], ir.INPUT),
+                ("s", [("H", H), ("M", T), ("T", T2)], ir.INTERMEDIATE),
+                ("p", [("H", H), ("M", T), ("T", T2)], ir.INTERMEDIATE),
+                ("c", [("M", T), ("N", D)], ir.OUTPUT)],
+               [(ir.BMM_QK, ["q", "k"], "s", {"heads": H}), (ir.SOFTMAX, ["s"], "p"),
+                (ir.BMM_PV, ["p", "v"], "c", {"heads": H})])
+    ins, ref = _oracle(g, 15, {"q": 0.25, "k": 0.25})
+    p3 = _run(g, {}, ins, flags=_abi.PLAN_KEEP_ALL)
+    p1 = _run(g, {}, ins)
+    assert p1.node_kernel(2) == "attention"
+    c1, c3 = p1.get_output("c"), p3.get_output("c")
+    assert O.max_rel_diff(c1, ref["c"]) <= 1e-5 and O.max_rel_diff(c3, ref["c"]) <= 1e-5
+    if T2 <= 256:
+        assert np.array_equal(c1, c3)
+    else:
+        assert O.max_rel_diff(c1, c3) <= 1e-6
 
 
 @pytest.mark.parametrize("factors,tile", [((128, 64, 128), 128), ((256, 64, 256), 128), ((128, 64, 64), 64)])
@@ -155,3 +223,33 @@ def test_encoder_full_size_layer_fused():
     # each); measured 7e-4 at the layer output (tools/encoder_debug.py).
     assert e2e.max_rel(out, emu) <= 2e-3
     assert e2e.max_rel(out, ex) <= 2e-2
+
+
+def test_encoder_packed_qkv_matches_unpacked():
+    """The packed-QKV encoder (one GMM(h, Wqkv) per layer, attention on its
+    column slices) computes the same layer as the three-projection graph on
+    the same weights: against the same emulating model and within the
+    chained-bf16 tolerance of the unpacked plan's output."""
+    import torch
+    from paper_2210_12415_b200 import e2e
+    g0, gmms0, plan0 = e2e.build_encoder(1, 128)
+    g1, gmms1, plan1 = e2e.build_encoder(1, 128, packed_qkv=True)
+    assert len(g1.nodes) == len(g0.nodes) - 4 and len(gmms1) == len(gmms0) - 2
+    kinds = [plan1.node_kernel(i) for i in range(len(g1.nodes))]
+    assert all(kinds[i].startswith("umma_gemm") for i in gmms1), kinds
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(9)
+    ins0 = e2e.make_encoder_inputs(g0, gen)
+    ins1 = {k: v for k, v in ins0.items() if not any(f"_{x}_" in k for x in "qkv")}
+    ins1["l0_qkv_w"] = torch.cat([ins0[f"l0_{x}_w"] for x in "qkv"], 1)
+    ins1["l0_qkv_b"] = torch.cat([ins0[f"l0_{x}_b"] for x in "qkv"], 0)
+    outs = []
+    for g, gmms, plan, ins in ((g0, gmms0, plan0, ins0), (g1, gmms1, plan1, ins1)):
+        for k, x in ins.items():
+            plan.set_input_device(k, x)
+        plan.run()
+        out = torch.tensor(plan.get_output("out"), device="cuda").view(128, 768)
+        emu = e2e.reference(g, ins, frozenset(gmms), emulate=True)["out"]
+        assert e2e.max_rel(out, emu) <= 2e-3
+        outs.append(out)
+    assert e2e.max_rel(outs[0], outs[1]) <= 2e-3

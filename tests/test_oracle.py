@@ -268,3 +268,26 @@ def test_oracle_encoder_ops_match_numpy():
     assert np.allclose(b["n"].reshape(T, D), n, rtol=1e-12, atol=1e-12)
     y = 0.5 * n * (1.0 + np.vectorize(math.erf)(n / math.sqrt(2.0)))
     assert np.allclose(b["y"].reshape(T, D), y, rtol=1e-12, atol=1e-12)
+
+
+def test_oracle_packed_qkv_slices_match_numpy():
+    """BmmQK / BmmPV on column slices of one packed [T, 3*H*Dh] operand
+    (a_col0 / b_col0 / head_dim) equal the unpacked ops on the slices."""
+    T, H, Dh = 5, 2, 4
+    D = H * Dh
+    g = _graph([("qkv", [("M", T), ("N", 3 * D)], ir.INPUT),
+                ("s", [("H", H), ("M", T), ("T", T)], ir.INTERMEDIATE),
+                ("c", [("M", T), ("N", D)], ir.OUTPUT)],
+               [(ir.BMM_QK, ["qkv", "qkv"], "s", {"heads": H, "a_col0": 0, "b_col0": D, "head_dim": Dh}),
+                (ir.BMM_PV, ["s", "qkv"], "c", {"heads": H, "b_col0": 2 * D, "head_dim": Dh})])
+    b = _run_oracle(g)
+    x = b["qkv"].reshape(T, 3 * D)
+    q, k, v = (x[:, i * D:(i + 1) * D].reshape(T, H, Dh) for i in range(3))
+    s = np.einsum("ihd,jhd->hij", q, k)
+    assert np.allclose(b["s"].reshape(H, T, T), s, rtol=1e-13, atol=1e-13)
+    c = np.einsum("hij,jhd->ihd", s, v).reshape(T, D)
+    assert np.allclose(b["c"].reshape(T, D), c, rtol=1e-13, atol=1e-13)
+    # out-of-range slices are rejected (the planner's EINVAL, lf_runtime.cpp)
+    g.nodes[0].attrs["b_col0"] = 2 * D + 1
+    with pytest.raises(Exception):
+        _run_oracle(g)

@@ -5,7 +5,7 @@ import torch  # noqa: E402
 from paper_2210_12415_b200 import _abi, e2e  # noqa: E402
 gen = torch.Generator(device="cuda")
 gen.manual_seed(1)
-g, gm, p = e2e.build_encoder(1, 64, flags=0)
+g, gm, p = e2e.build_encoder(1, 64, flags=0, packed_qkv="packed" in sys.argv)
 for k, x in e2e.make_encoder_inputs(g, gen).items():
     p.set_input_device(k, x)
 for _ in range(3):
