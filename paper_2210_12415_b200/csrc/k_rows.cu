@@ -325,40 +325,91 @@ __global__ void __launch_bounds__(256) bmm_pv_kernel(const BmmParams P) {
 // acc += q*k over d ascending; softmax: rows_kernel's per-lane partition and
 // xor tree; PV: acc += p*v over j ascending), so for T2 <= 256 (where the
 // unfused softmax is rows_kernel) the output is bit-identical to the
-// three-kernel path. K and V stream through one SMEM chunk of up to 128 rows;
-// the offset tables are staged before the grid-dependency wait (they are
-// plan constants), the operands after it.
+// three-kernel path. The offset tables are staged before the grid-dependency
+// wait (they are plan constants); q, K and V then arrive by cp.async
+// gathers all in flight together (16-byte pieces when every operand's head
+// columns are contiguous in aligned runs of 4, Q.vec), K and V resident for
+// T2 up to the chunk (one pass), streamed in chunks beyond it.
+// SMEM rows are padded to Dp = roundup4(Dh) + 4 floats: 16-byte aligned rows
+// whose float4 reads by 8 consecutive rows hit distinct banks; the padding
+// columns hold zeros (acc += 0 * 0 leaves an accumulator unchanged).
 constexpr int kAttnRows = 16;
-constexpr int kAttnChunk = 128;
 
 struct AttnSmem {
-  int chunk, dh, t2;
-  size_t qs, kv, ss, tab, total;
+  int chunk, dp, t2p;
+  size_t qs, ks, vs, ss, tab, total;
 };
 
 __host__ __device__ inline AttnSmem attn_smem(int T2, int Dh) {
   AttnSmem L;
-  L.t2 = T2;
-  L.dh = Dh;
-  L.chunk = T2 < kAttnChunk ? ((T2 + 31) / 32) * 32 : kAttnChunk;
+  L.dp = ((Dh + 3) / 4) * 4 + 4;
+  L.t2p = ((T2 + 3) / 4) * 4;
+  // K and V chunks of up to ~150 KB together, a multiple of 32 rows
+  int cap = static_cast<int>((150 * 1024) / (2 * sizeof(float) * L.dp)) / 32 * 32;
+  if (cap < 32) cap = 32;
+  const int t2r = ((T2 + 31) / 32) * 32;
+  L.chunk = t2r < cap ? t2r : cap;
   L.qs = 0;
-  L.kv = L.qs + sizeof(float) * kAttnRows * Dh;
-  L.ss = L.kv + sizeof(float) * L.chunk * (Dh + 1);
-  L.tab = L.ss + sizeof(float) * kAttnRows * T2;
-  L.tab = (L.tab + 15) & ~size_t(15);
+  L.ks = L.qs + sizeof(float) * kAttnRows * L.dp;
+  L.vs = L.ks + sizeof(float) * L.chunk * L.dp;
+  L.ss = L.vs + sizeof(float) * L.chunk * L.dp;
+  L.tab = L.ss + sizeof(float) * kAttnRows * L.t2p;
   // kr[T2], vr[T2], qr[rows], orow[rows], qc[Dh], kc[Dh], vc[Dh], oc[Dh]
   L.total = L.tab + sizeof(int64_t) * (2 * T2 + 2 * kAttnRows + 4 * Dh);
   return L;
 }
 
-template <typename Acc>
-__global__ void __launch_bounds__(256) attn_kernel(const BmmParams Q, const BmmParams V) {
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory"); }
+
+constexpr int kAttnThreads = 512;
+
+// rows [r0, r0 + nr) of an operand (row offsets rtab, column offsets ctab,
+// head columns [0, Dh)) into dst[nr][dp]; rows at or past `valid` and the
+// padding columns are zero-filled.
+template <int DH>
+__device__ __forceinline__ void attn_gather(float* dst, int dp_rt, const float* src, const int64_t* rtab,
+                                            const int64_t* ctab, int r0, int nr, int valid, int dh_rt, bool vec) {
+  const int Dh = DH ? DH : dh_rt;
+  const int dp = DH ? ((DH + 3) / 4) * 4 + 4 : dp_rt;
+  const int t = threadIdx.x;
+  if (vec) {
+    const int q4 = dp / 4;
+    for (int e = t; e < nr * q4; e += kAttnThreads) {
+      const int r = e / q4, c = (e - r * q4) * 4;
+      float* d = dst + r * dp + c;
+      if (r0 + r < valid && c < Dh) cp_async16(d, src + rtab[r0 + r] + ctab[c]);
+      else *reinterpret_cast<float4*>(d) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  } else {
+    for (int e = t; e < nr * dp; e += kAttnThreads) {
+      const int r = e / dp, c = e - r * dp;
+      if (r0 + r < valid && c < Dh) cp_async4(dst + e, src + rtab[r0 + r] + ctab[c]);
+      else dst[e] = 0.f;
+    }
+  }
+}
+
+// DH: the head dim as a compile-time constant (64, 128) or 0 (any even Dh <= 128).
+template <typename Acc, int DH>
+__global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const BmmParams Q, const BmmParams V) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int h = blockIdx.y, i0 = blockIdx.x * kAttnRows;
-  const int T = Q.T, T2 = Q.T2, Dh = Q.Dh;
+  const int T = Q.T, T2 = Q.T2, Dh = DH ? DH : Q.Dh;
   const AttnSmem L = attn_smem(T2, Dh);
+  const int dp = DH ? ((DH + 3) / 4) * 4 + 4 : L.dp, t2p = L.t2p;
   float* qs = reinterpret_cast<float*>(smem + L.qs);
-  float* kv = reinterpret_cast<float*>(smem + L.kv);
+  float* ks = reinterpret_cast<float*>(smem + L.ks);
+  float* vs = reinterpret_cast<float*>(smem + L.vs);
   float* ss = reinterpret_cast<float*>(smem + L.ss);
   int64_t* kr = reinterpret_cast<int64_t*>(smem + L.tab);
   int64_t* vr = kr + T2;
@@ -369,7 +420,7 @@ __global__ void __launch_bounds__(256) attn_kernel(const BmmParams Q, const BmmP
   int64_t* vc = kc + Dh;
   int64_t* oc = vc + Dh;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  for (int e = t; e < T2; e += 256) {
+  for (int e = t; e < T2; e += kAttnThreads) {
     kr[e] = __ldg(Q.tb + Q.b_off[0] + e);
     vr[e] = __ldg(V.tb + V.b_off[0] + e);
   }
@@ -377,7 +428,7 @@ __global__ void __launch_bounds__(256) attn_kernel(const BmmParams Q, const BmmP
     qr[t] = i0 + t < T ? __ldg(Q.ta + Q.a_off[0] + i0 + t) : 0;
     orow[t] = i0 + t < T ? __ldg(V.to + V.o_off[0] + i0 + t) : 0;
   }
-  for (int e = t; e < Dh; e += 256) {
+  for (int e = t; e < Dh; e += kAttnThreads) {
     qc[e] = __ldg(Q.ta + Q.a_off[1] + h * Dh + e);
     kc[e] = __ldg(Q.tb + Q.b_off[1] + h * Dh + e);
     vc[e] = __ldg(V.tb + V.b_off[1] + h * Dh + e);
@@ -385,76 +436,58 @@ __global__ void __launch_bounds__(256) attn_kernel(const BmmParams Q, const BmmP
   }
   LFG_PDL_ENTRY();
   __syncthreads();
-  // q rows: up to 16 x 128 elements, 8 loads per thread in flight
-  {
-    constexpr int kPer = kAttnRows * kMaxDh / 256;
-    float qv[kPer];
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = t + 256 * u, r = e / Dh, c = e - r * Dh;
-      qv[u] = e < kAttnRows * Dh && i0 + r < T ? __ldg(Q.a + qr[r] + qc[c]) : 0.f;
+  const bool vec = Q.vec != 0;
+  const int nchunks = (T2 + L.chunk - 1) / L.chunk;
+  attn_gather<DH>(qs, dp, Q.a, qr, qc, 0, kAttnRows, T - i0, Dh, vec);
+  attn_gather<DH>(ks, dp, Q.b, kr, kc, 0, L.chunk, T2, Dh, vec);
+  if (nchunks == 1) attn_gather<DH>(vs, dp, V.b, vr, vc, 0, L.chunk, T2, Dh, vec);
+  cp_async_wait_all();
+  __syncthreads();
+  // scores: thread t owns chunk column (t & 127) + 128 b and rows 4 (t >> 7) .. + 3
+  const int tj = t & 127, tr = (t >> 7) * 4;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int j0 = ch * L.chunk;
+    if (ch > 0) {
+      __syncthreads();
+      attn_gather<DH>(ks, dp, Q.b, kr, kc, j0, L.chunk, T2, Dh, vec);
+      cp_async_wait_all();
+      __syncthreads();
     }
+    for (int jb = 0; jb < L.chunk; jb += 128) {
+      const int jj = jb + tj;
+      if (jj >= L.chunk) break;
+      Acc acc[4];
 #pragma unroll
-    for (int u = 0; u < kPer; ++u)
-      if (t + 256 * u < kAttnRows * Dh) qs[t + 256 * u] = qv[u];
-  }
-  // one chunk of K (mode 0) or V (mode 1) rows into kv[chunk][Dh + 1]:
-  // 16 loads per thread in flight per batch
-  auto load_chunk = [&](int j0, int mode) {
-    const float* src = mode == 0 ? Q.b : V.b;
-    const int64_t* rows = mode == 0 ? kr : vr;
-    const int64_t* cols = mode == 0 ? kc : vc;
-    const int n = L.chunk * Dh;
-    for (int b0 = 0; b0 < n; b0 += 256 * 16) {
-      float x[16];
+      for (int r = 0; r < 4; ++r) acc[r] = 0;
+      const float* krow = ks + jj * dp;
+#pragma unroll 4
+      for (int c = 0; c < dp - 4; c += 4) {
+        const float4 k4 = *reinterpret_cast<const float4*>(krow + c);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int e = b0 + t + 256 * u, r = e / Dh, c = e - r * Dh;
-        x[u] = e < n && j0 + r < T2 ? __ldg(src + rows[j0 + r] + cols[c]) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int e = b0 + t + 256 * u, r = e / Dh, c = e - r * Dh;
-        if (e < n) kv[r * (Dh + 1) + c] = x[u];
-      }
-    }
-  };
-  // scores: thread (w, lane) owns rows w, w+8 and chunk columns lane + 32m
-  for (int j0 = 0; j0 < T2; j0 += L.chunk) {
-    __syncthreads();
-    load_chunk(j0, 0);
-    __syncthreads();
-    Acc acc[2][kAttnChunk / 32];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int m = 0; m < kAttnChunk / 32; ++m) acc[r][m] = 0;
-    const int nm = L.chunk / 32;
-    for (int c = 0; c < Dh; ++c) {
-      const float q0 = qs[w * Dh + c], q1 = qs[(w + 8) * Dh + c];
-#pragma unroll
-      for (int m = 0; m < kAttnChunk / 32; ++m)
-        if (m < nm) {
-          const float kx = kv[(lane + 32 * m) * (Dh + 1) + c];
-          acc[0][m] += static_cast<Acc>(q0) * kx;
-          acc[1][m] += static_cast<Acc>(q1) * kx;
+        for (int r = 0; r < 4; ++r) {
+          const float4 q4 = *reinterpret_cast<const float4*>(qs + (tr + r) * dp + c);
+          acc[r] += static_cast<Acc>(q4.x) * k4.x;
+          acc[r] += static_cast<Acc>(q4.y) * k4.y;
+          acc[r] += static_cast<Acc>(q4.z) * k4.z;
+          acc[r] += static_cast<Acc>(q4.w) * k4.w;
         }
-    }
+      }
+      if (j0 + jj < T2) {
 #pragma unroll
-    for (int m = 0; m < kAttnChunk / 32; ++m) {
-      const int j = j0 + lane + 32 * m;
-      if (m < nm && j < T2) {
-        ss[w * T2 + j] = static_cast<float>(acc[0][m]);
-        ss[(w + 8) * T2 + j] = static_cast<float>(acc[1][m]);
+        for (int r = 0; r < 4; ++r) ss[(tr + r) * t2p + j0 + jj] = static_cast<float>(acc[r]);
       }
     }
+  }
+  if (nchunks > 1) {  // V was not prefetched: its first chunk now, under the softmax
+    __syncthreads();
+    attn_gather<DH>(vs, dp, V.b, vr, vc, 0, L.chunk, T2, Dh, vec);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   __syncthreads();
-  // softmax over each row: warp w owns rows w, w+8 (rows_kernel's arithmetic)
-  constexpr int kNC = kMaxT2 / 32;
-#pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    float* row = ss + (w + 8 * rr) * T2;
+  // softmax over each row: warp w owns row w (rows_kernel's arithmetic)
+  {
+    constexpr int kNC = kMaxT2 / 32;
+    float* row = ss + w * t2p;
     float v[kNC];
     float m = -INFINITY;
 #pragma unroll
@@ -473,42 +506,66 @@ __global__ void __launch_bounds__(256) attn_kernel(const BmmParams Q, const BmmP
       }
     const float inv = 1.f / warp_sum(sum);
 #pragma unroll
-    for (int k = 0; k < kNC; ++k)
-      if (lane + 32 * k < T2) row[lane + 32 * k] = v[k] * inv;
+    for (int k = 0; k < kNC; ++k) {
+      const int j = lane + 32 * k;
+      if (j < T2) row[j] = v[k] * inv;
+      else if (j < t2p) row[j] = 0.f;
+    }
   }
-  // context: thread (w, lane) owns rows w, w+8 and columns lane + 32m
-  Acc acc[2][kMaxDh / 32];
+  // context: thread t owns columns (t % DW) + DW m and RP rows from RP (t / DW)
+  constexpr int DW = DH >= 128 ? 128 : 64;
+  constexpr int RP = kAttnRows * DW / kAttnThreads;
+  constexpr int MM = DH ? (DH + DW - 1) / DW : kMaxDh / DW;
+  const int td = t % DW, tq = (t / DW) * RP;
+  Acc acc[RP][MM];
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
+  for (int r = 0; r < RP; ++r)
 #pragma unroll
-    for (int m = 0; m < kMaxDh / 32; ++m) acc[r][m] = 0;
-  const int nd = (Dh + 31) / 32;
-  for (int j0 = 0; j0 < T2; j0 += L.chunk) {
-    __syncthreads();
-    load_chunk(j0, 1);
+    for (int m = 0; m < MM; ++m) acc[r][m] = 0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int j0 = ch * L.chunk;
+    if (nchunks > 1) {
+      if (ch > 0) {
+        __syncthreads();
+        attn_gather<DH>(vs, dp, V.b, vr, vc, j0, L.chunk, T2, Dh, vec);
+      }
+      cp_async_wait_all();
+    }
     __syncthreads();
     const int jn = min(L.chunk, T2 - j0);
-    for (int jj = 0; jj < jn; ++jj) {
-      const float p0 = ss[w * T2 + j0 + jj], p1 = ss[(w + 8) * T2 + j0 + jj];
+#pragma unroll 2
+    for (int j = 0; j < jn; j += 4) {
+      float4 p4[RP];
 #pragma unroll
-      for (int m = 0; m < kMaxDh / 32; ++m)
-        if (m < nd && lane + 32 * m < Dh) {
-          const float vx = kv[jj * (Dh + 1) + lane + 32 * m];
-          acc[0][m] += static_cast<Acc>(p0) * vx;
-          acc[1][m] += static_cast<Acc>(p1) * vx;
+      for (int r = 0; r < RP; ++r) p4[r] = *reinterpret_cast<const float4*>(ss + (tq + r) * t2p + j0 + j);
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const int d = td + DW * m;
+        if (d < Dh) {
+          const float v0 = vs[j * dp + d], v1 = vs[(j + 1) * dp + d], v2 = vs[(j + 2) * dp + d],
+                      v3 = vs[(j + 3) * dp + d];
+#pragma unroll
+          for (int r = 0; r < RP; ++r) {
+            // columns past T2 are zero in both p and V (zero-filled rows)
+            acc[r][m] += static_cast<Acc>(p4[r].x) * v0;
+            acc[r][m] += static_cast<Acc>(p4[r].y) * v1;
+            acc[r][m] += static_cast<Acc>(p4[r].z) * v2;
+            acc[r][m] += static_cast<Acc>(p4[r].w) * v3;
+          }
         }
+      }
     }
   }
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int r = w + 8 * rr;
-    if (i0 + r >= T) continue;
+  for (int r = 0; r < RP; ++r) {
+    const int i = tq + r;
+    if (i0 + i >= T) continue;
 #pragma unroll
-    for (int m = 0; m < kMaxDh / 32; ++m) {
-      const int c = lane + 32 * m;
-      if (m < nd && c < Dh) {
-        const int64_t o = orow[r] + oc[c];
-        const float y = static_cast<float>(acc[rr][m]);
+    for (int m = 0; m < MM; ++m) {
+      const int c = td + DW * m;
+      if (c < Dh) {
+        const int64_t o = orow[i] + oc[c];
+        const float y = static_cast<float>(acc[r][m]);
         V.out[o] = y;
         if (V.out_bf16) static_cast<__nv_bfloat16*>(V.out_bf16)[o] = __float2bfloat16_rn(y);
       }
@@ -579,21 +636,26 @@ cudaError_t launch_bmm(const BmmParams& P, bool exact, cudaStream_t stream) {
 
 size_t attn_smem_bytes(int T2, int Dh) { return attn_smem(T2, Dh).total; }
 
+template <typename Acc, int DH>
+cudaError_t launch_attn_inst(const BmmParams& QK, const BmmParams& PV, size_t smem, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_kernel<Acc, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const dim3 grid((QK.T + kAttnRows - 1) / kAttnRows, QK.H);
+  return launch_pdl(attn_kernel<Acc, DH>, grid, dim3(kAttnThreads), smem, stream, QK, PV);
+}
+
 cudaError_t launch_attention(const BmmParams& QK, const BmmParams& PV, bool exact, cudaStream_t stream) {
   if (QK.Dh > kMaxDh || QK.Dh < 1 || QK.T2 > kMaxT2 || QK.T2 < 1 || PV.Dh != QK.Dh) return cudaErrorInvalidValue;
   const size_t smem = attn_smem(QK.T2, QK.Dh).total;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[exact]) {
-    cudaError_t e = exact ? cudaFuncSetAttribute(attn_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(attn_smem(kMaxT2, kMaxDh).total))
-                          : cudaFuncSetAttribute(attn_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(attn_smem(kMaxT2, kMaxDh).total));
-    if (e != cudaSuccess) return e;
-    attr_set[exact] = true;
-  }
-  const dim3 grid((QK.T + kAttnRows - 1) / kAttnRows, QK.H);
-  return exact ? launch_pdl(attn_kernel<double>, grid, dim3(256), smem, stream, QK, PV)
-               : launch_pdl(attn_kernel<float>, grid, dim3(256), smem, stream, QK, PV);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (exact) return launch_attn_inst<double, 0>(QK, PV, smem, stream);
+  if (QK.Dh == 64) return launch_attn_inst<float, 64>(QK, PV, smem, stream);
+  if (QK.Dh == 128) return launch_attn_inst<float, 128>(QK, PV, smem, stream);
+  return launch_attn_inst<float, 0>(QK, PV, smem, stream);
 }
 
 }  // namespace lfg

@@ -45,6 +45,9 @@ struct BmmParams {
   const int64_t* tb = nullptr;
   const int64_t* to = nullptr;
   int64_t a_off[3] = {}, b_off[3] = {}, o_off[3] = {};
+  // fused attention: every operand's head columns contiguous in 16-byte
+  // aligned runs of 4 (16-byte gathers)
+  int32_t vec = 0;
 };
 
 // LFGPU_PLAN_TC_SPLIT operand preparation: x = x0 + x1 + x2 (bf16 pieces);

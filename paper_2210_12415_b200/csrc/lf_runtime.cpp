@@ -305,6 +305,23 @@ int64_t* tables_for(lfgpu_plan* P, const PTensor& t, std::vector<int64_t>* off) 
   return upload(P->keep, tab.data(), tab.size());
 }
 
+// Columns [c0, c0 + width) of a rank-2 separable tensor: every row offset a
+// multiple of 4 and the columns contiguous in runs of 4 starting 16-byte
+// aligned (the fused attention kernel's 16-byte gathers).
+bool cols_vec4(const PTensor& t, int64_t c0, int64_t width) {
+  std::vector<int64_t> tab, off;
+  if (t.logical.size() != 2 || c0 % 4 || width % 4 || !separable_tables(t.logical, t.seq, &tab, &off)) return false;
+  for (int64_t i = 0; i < t.logical[0].extent; ++i)
+    if (tab[off[0] + i] % 4) return false;
+  for (int64_t c = c0; c < c0 + width; c += 4) {
+    const int64_t b = tab[off[1] + c];
+    if (b % 4) return false;
+    for (int k = 1; k < 4; ++k)
+      if (tab[off[1] + c + k] != b + k) return false;
+  }
+  return true;
+}
+
 bool same_extents(const std::vector<Dim>& a, const std::vector<Dim>& b) {
   if (a.size() != b.size()) return false;
   for (size_t i = 0; i < a.size(); ++i)
@@ -1383,12 +1400,17 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
         if (n.kind == LFGPU_OP_BMM_PV && attn_of.count(ni)) {
           // the fused attention core: QK's operands, PV's v and output
           const int qn = attn_of.at(ni);
-          const BmmParams Q = bmm_params(qn);
+          BmmParams Q = bmm_params(qn);
           if (Q.T2 != M.T2 || Q.T != M.T || Q.Dh != M.Dh)
             fail(LFGPU_EINVAL, "attention: BmmQK / BmmPV shapes disagree");
           P->bytes -= A.numel * 4;  // p is never read from memory
           P->flops += 2 * static_cast<int64_t>(Q.H) * Q.T * Q.T2 * Q.Dh;
           P->bytes += (int64_t(Q.T) + Q.T2) * Q.H * Q.Dh * 4;
+          const auto& qkn = P->nodes[qn];
+          const int64_t w = int64_t(Q.H) * Q.Dh;
+          Q.vec = Q.Dh % 4 == 0 && cols_vec4(P->t[qkn.inputs[0]], qkn.a_col0, w) &&
+                  cols_vec4(P->t[qkn.inputs[1]], qkn.b_col0, w) && cols_vec4(P->t[n.inputs[1]], n.b_col0, w);
+          if (getenv("LFGPU_ATTN_SCALAR")) Q.vec = 0;
           step.kernel = "attention";
           step.run = [Q, M, exact](cudaStream_t s) { return launch_attention(Q, M, exact, s); };
           break;
