@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "lf_pdl.hpp"
 #include "lf_rows.hpp"
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(256) bmm_pv_kernel(const BmmParams P) {
   }
 }
 
-// Fused attention core: BmmQK -> Softmax -> BmmPV of one head for kAttnRows
+// Fused attention core: BmmQK -> Softmax -> BmmPV of one head for R
 // query rows per CTA, the [rows, T2] scores never leaving shared memory.
 // Every stage repeats the unfused kernels' arithmetic in the same order (QK:
 // acc += q*k over d ascending; softmax: rows_kernel's per-lane partition and
@@ -333,14 +334,13 @@ __global__ void __launch_bounds__(256) bmm_pv_kernel(const BmmParams P) {
 // SMEM rows are padded to Dp = roundup4(Dh) + 4 floats: 16-byte aligned rows
 // whose float4 reads by 8 consecutive rows hit distinct banks; the padding
 // columns hold zeros (acc += 0 * 0 leaves an accumulator unchanged).
-constexpr int kAttnRows = 16;
 
 struct AttnSmem {
   int chunk, dp, t2p;
   size_t qs, ks, vs, ss, tab, total;
 };
 
-__host__ __device__ inline AttnSmem attn_smem(int T2, int Dh) {
+__host__ __device__ inline AttnSmem attn_smem(int T2, int Dh, int R) {
   AttnSmem L;
   L.dp = ((Dh + 3) / 4) * 4 + 4;
   L.t2p = ((T2 + 3) / 4) * 4;
@@ -350,12 +350,12 @@ __host__ __device__ inline AttnSmem attn_smem(int T2, int Dh) {
   const int t2r = ((T2 + 31) / 32) * 32;
   L.chunk = t2r < cap ? t2r : cap;
   L.qs = 0;
-  L.ks = L.qs + sizeof(float) * kAttnRows * L.dp;
+  L.ks = L.qs + sizeof(float) * R * L.dp;
   L.vs = L.ks + sizeof(float) * L.chunk * L.dp;
   L.ss = L.vs + sizeof(float) * L.chunk * L.dp;
-  L.tab = L.ss + sizeof(float) * kAttnRows * L.t2p;
+  L.tab = L.ss + sizeof(float) * R * L.t2p;
   // kr[T2], vr[T2], qr[rows], orow[rows], qc[Dh], kc[Dh], vc[Dh], oc[Dh]
-  L.total = L.tab + sizeof(int64_t) * (2 * T2 + 2 * kAttnRows + 4 * Dh);
+  L.total = L.tab + sizeof(int64_t) * (2 * T2 + 2 * R + 4 * Dh);
   return L;
 }
 
@@ -371,12 +371,10 @@ __device__ __forceinline__ void cp_async16(float* dst, const float* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory"); }
 
-constexpr int kAttnThreads = 512;
-
 // rows [r0, r0 + nr) of an operand (row offsets rtab, column offsets ctab,
 // head columns [0, Dh)) into dst[nr][dp]; rows at or past `valid` and the
 // padding columns are zero-filled.
-template <int DH>
+template <int DH, int NT>
 __device__ __forceinline__ void attn_gather(float* dst, int dp_rt, const float* src, const int64_t* rtab,
                                             const int64_t* ctab, int r0, int nr, int valid, int dh_rt, bool vec) {
   const int Dh = DH ? DH : dh_rt;
@@ -384,14 +382,14 @@ __device__ __forceinline__ void attn_gather(float* dst, int dp_rt, const float* 
   const int t = threadIdx.x;
   if (vec) {
     const int q4 = dp / 4;
-    for (int e = t; e < nr * q4; e += kAttnThreads) {
+    for (int e = t; e < nr * q4; e += NT) {
       const int r = e / q4, c = (e - r * q4) * 4;
       float* d = dst + r * dp + c;
       if (r0 + r < valid && c < Dh) cp_async16(d, src + rtab[r0 + r] + ctab[c]);
       else *reinterpret_cast<float4*>(d) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   } else {
-    for (int e = t; e < nr * dp; e += kAttnThreads) {
+    for (int e = t; e < nr * dp; e += NT) {
       const int r = e / dp, c = e - r * dp;
       if (r0 + r < valid && c < Dh) cp_async4(dst + e, src + rtab[r0 + r] + ctab[c]);
       else dst[e] = 0.f;
@@ -399,13 +397,15 @@ __device__ __forceinline__ void attn_gather(float* dst, int dp_rt, const float* 
   }
 }
 
-// DH: the head dim as a compile-time constant (64, 128) or 0 (any even Dh <= 128).
-template <typename Acc, int DH>
-__global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const BmmParams Q, const BmmParams V) {
+// DH: the head dim as a compile-time constant (64, 128) or 0 (any even Dh <= 128);
+// R query rows per CTA, NT threads.
+template <typename Acc, int DH, int R, int NT>
+__global__ void __launch_bounds__(NT, 1) attn_kernel(const BmmParams Q, const BmmParams V) {
+  static_assert(NT >= 128 && (R * 128) % NT == 0 && R >= NT / 32, "attention tile");
   extern __shared__ __align__(16) unsigned char smem[];
-  const int h = blockIdx.y, i0 = blockIdx.x * kAttnRows;
+  const int h = blockIdx.y, i0 = blockIdx.x * R;
   const int T = Q.T, T2 = Q.T2, Dh = DH ? DH : Q.Dh;
-  const AttnSmem L = attn_smem(T2, Dh);
+  const AttnSmem L = attn_smem(T2, Dh, R);
   const int dp = DH ? ((DH + 3) / 4) * 4 + 4 : L.dp, t2p = L.t2p;
   float* qs = reinterpret_cast<float*>(smem + L.qs);
   float* ks = reinterpret_cast<float*>(smem + L.ks);
@@ -414,21 +414,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const BmmParams Q
   int64_t* kr = reinterpret_cast<int64_t*>(smem + L.tab);
   int64_t* vr = kr + T2;
   int64_t* qr = vr + T2;
-  int64_t* orow = qr + kAttnRows;
-  int64_t* qc = orow + kAttnRows;
+  int64_t* orow = qr + R;
+  int64_t* qc = orow + R;
   int64_t* kc = qc + Dh;
   int64_t* vc = kc + Dh;
   int64_t* oc = vc + Dh;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  for (int e = t; e < T2; e += kAttnThreads) {
+  for (int e = t; e < T2; e += NT) {
     kr[e] = __ldg(Q.tb + Q.b_off[0] + e);
     vr[e] = __ldg(V.tb + V.b_off[0] + e);
   }
-  if (t < kAttnRows) {
+  if (t < R) {
     qr[t] = i0 + t < T ? __ldg(Q.ta + Q.a_off[0] + i0 + t) : 0;
     orow[t] = i0 + t < T ? __ldg(V.to + V.o_off[0] + i0 + t) : 0;
   }
-  for (int e = t; e < Dh; e += kAttnThreads) {
+  for (int e = t; e < Dh; e += NT) {
     qc[e] = __ldg(Q.ta + Q.a_off[1] + h * Dh + e);
     kc[e] = __ldg(Q.tb + Q.b_off[1] + h * Dh + e);
     vc[e] = __ldg(V.tb + V.b_off[1] + h * Dh + e);
@@ -438,33 +438,34 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const BmmParams Q
   __syncthreads();
   const bool vec = Q.vec != 0;
   const int nchunks = (T2 + L.chunk - 1) / L.chunk;
-  attn_gather<DH>(qs, dp, Q.a, qr, qc, 0, kAttnRows, T - i0, Dh, vec);
-  attn_gather<DH>(ks, dp, Q.b, kr, kc, 0, L.chunk, T2, Dh, vec);
-  if (nchunks == 1) attn_gather<DH>(vs, dp, V.b, vr, vc, 0, L.chunk, T2, Dh, vec);
+  attn_gather<DH, NT>(qs, dp, Q.a, qr, qc, 0, R, T - i0, Dh, vec);
+  attn_gather<DH, NT>(ks, dp, Q.b, kr, kc, 0, L.chunk, T2, Dh, vec);
+  if (nchunks == 1) attn_gather<DH, NT>(vs, dp, V.b, vr, vc, 0, L.chunk, T2, Dh, vec);
   cp_async_wait_all();
   __syncthreads();
-  // scores: thread t owns chunk column (t & 127) + 128 b and rows 4 (t >> 7) .. + 3
-  const int tj = t & 127, tr = (t >> 7) * 4;
+  // scores: thread t owns chunk column (t & 127) + 128 b and RS rows from RS (t >> 7)
+  constexpr int RS = R * 128 / NT;
+  const int tj = t & 127, tr = (t >> 7) * RS;
   for (int ch = 0; ch < nchunks; ++ch) {
     const int j0 = ch * L.chunk;
     if (ch > 0) {
       __syncthreads();
-      attn_gather<DH>(ks, dp, Q.b, kr, kc, j0, L.chunk, T2, Dh, vec);
+      attn_gather<DH, NT>(ks, dp, Q.b, kr, kc, j0, L.chunk, T2, Dh, vec);
       cp_async_wait_all();
       __syncthreads();
     }
     for (int jb = 0; jb < L.chunk; jb += 128) {
       const int jj = jb + tj;
       if (jj >= L.chunk) break;
-      Acc acc[4];
+      Acc acc[RS];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] = 0;
+      for (int r = 0; r < RS; ++r) acc[r] = 0;
       const float* krow = ks + jj * dp;
 #pragma unroll 4
       for (int c = 0; c < dp - 4; c += 4) {
         const float4 k4 = *reinterpret_cast<const float4*>(krow + c);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < RS; ++r) {
           const float4 q4 = *reinterpret_cast<const float4*>(qs + (tr + r) * dp + c);
           acc[r] += static_cast<Acc>(q4.x) * k4.x;
           acc[r] += static_cast<Acc>(q4.y) * k4.y;
@@ -474,20 +475,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const BmmParams Q
       }
       if (j0 + jj < T2) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) ss[(tr + r) * t2p + j0 + jj] = static_cast<float>(acc[r]);
+        for (int r = 0; r < RS; ++r) ss[(tr + r) * t2p + j0 + jj] = static_cast<float>(acc[r]);
       }
     }
   }
   if (nchunks > 1) {  // V was not prefetched: its first chunk now, under the softmax
     __syncthreads();
-    attn_gather<DH>(vs, dp, V.b, vr, vc, 0, L.chunk, T2, Dh, vec);
+    attn_gather<DH, NT>(vs, dp, V.b, vr, vc, 0, L.chunk, T2, Dh, vec);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   __syncthreads();
-  // softmax over each row: warp w owns row w (rows_kernel's arithmetic)
-  {
+  // softmax over each row: warp w owns rows w + (NT / 32) k (rows_kernel's arithmetic)
+#pragma unroll 1
+  for (int rw = w; rw < R; rw += NT / 32) {
     constexpr int kNC = kMaxT2 / 32;
-    float* row = ss + w * t2p;
+    float* row = ss + rw * t2p;
     float v[kNC];
     float m = -INFINITY;
 #pragma unroll
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const BmmParams Q
   }
   // context: thread t owns columns (t % DW) + DW m and RP rows from RP (t / DW)
   constexpr int DW = DH >= 128 ? 128 : 64;
-  constexpr int RP = kAttnRows * DW / kAttnThreads;
+  constexpr int RP = R * DW / NT;
   constexpr int MM = DH ? (DH + DW - 1) / DW : kMaxDh / DW;
   const int td = t % DW, tq = (t / DW) * RP;
   Acc acc[RP][MM];
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const BmmParams Q
     if (nchunks > 1) {
       if (ch > 0) {
         __syncthreads();
-        attn_gather<DH>(vs, dp, V.b, vr, vc, j0, L.chunk, T2, Dh, vec);
+        attn_gather<DH, NT>(vs, dp, V.b, vr, vc, j0, L.chunk, T2, Dh, vec);
       }
       cp_async_wait_all();
     }
@@ -634,28 +636,39 @@ cudaError_t launch_bmm(const BmmParams& P, bool exact, cudaStream_t stream) {
                : launch_pdl(bmm_pv_kernel<float>, grid, dim3(256), 0, stream, P);
 }
 
-size_t attn_smem_bytes(int T2, int Dh) { return attn_smem(T2, Dh).total; }
 
-template <typename Acc, int DH>
-cudaError_t launch_attn_inst(const BmmParams& QK, const BmmParams& PV, size_t smem, cudaStream_t stream) {
+template <typename Acc, int DH, int R, int NT>
+cudaError_t launch_attn_inst(const BmmParams& QK, const BmmParams& PV, cudaStream_t stream) {
+  const size_t smem = attn_smem(QK.T2, QK.Dh, R).total;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_kernel<Acc, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_kernel<Acc, DH, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const dim3 grid((QK.T + kAttnRows - 1) / kAttnRows, QK.H);
-  return launch_pdl(attn_kernel<Acc, DH>, grid, dim3(kAttnThreads), smem, stream, QK, PV);
+  const dim3 grid((QK.T + R - 1) / R, QK.H);
+  return launch_pdl(attn_kernel<Acc, DH, R, NT>, grid, dim3(NT), smem, stream, QK, PV);
+}
+
+template <int DH>
+cudaError_t launch_attn_dh(const BmmParams& QK, const BmmParams& PV, int variant, cudaStream_t stream) {
+  switch (variant) {
+    case 1: return launch_attn_inst<float, DH, 8, 256>(QK, PV, stream);
+    case 2: return launch_attn_inst<float, DH, 16, 256>(QK, PV, stream);
+    case 3: return launch_attn_inst<float, DH, 32, 512>(QK, PV, stream);
+    default: return launch_attn_inst<float, DH, 16, 512>(QK, PV, stream);
+  }
 }
 
 cudaError_t launch_attention(const BmmParams& QK, const BmmParams& PV, bool exact, cudaStream_t stream) {
   if (QK.Dh > kMaxDh || QK.Dh < 1 || QK.T2 > kMaxT2 || QK.T2 < 1 || PV.Dh != QK.Dh) return cudaErrorInvalidValue;
-  const size_t smem = attn_smem(QK.T2, QK.Dh).total;
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  if (exact) return launch_attn_inst<double, 0>(QK, PV, smem, stream);
-  if (QK.Dh == 64) return launch_attn_inst<float, 64>(QK, PV, smem, stream);
-  if (QK.Dh == 128) return launch_attn_inst<float, 128>(QK, PV, smem, stream);
-  return launch_attn_inst<float, 0>(QK, PV, smem, stream);
+  static const int variant = getenv("LFGPU_ATTN_VARIANT") ? atoi(getenv("LFGPU_ATTN_VARIANT")) : 0;
+  if (exact) return launch_attn_inst<double, 0, 16, 512>(QK, PV, stream);
+  if (QK.Dh == 64) return launch_attn_dh<64>(QK, PV, variant, stream);
+  if (QK.Dh == 128) return launch_attn_dh<128>(QK, PV, variant, stream);
+  return launch_attn_inst<float, 0, 16, 512>(QK, PV, stream);
 }
 
 }  // namespace lfg

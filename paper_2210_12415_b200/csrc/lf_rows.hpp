@@ -72,6 +72,5 @@ cudaError_t launch_bmm(const BmmParams& P, bool exact, cudaStream_t stream);
 // BmmQK -> Softmax -> BmmPV in one kernel (k_rows.cu attn_kernel): QK's q / k
 // operands and PV's v operand and output; the scores stay in SMEM.
 cudaError_t launch_attention(const BmmParams& QK, const BmmParams& PV, bool exact, cudaStream_t stream);
-size_t attn_smem_bytes(int T2, int Dh);
 
 }  // namespace lfg

@@ -1699,12 +1699,29 @@ int lfgpu_plan_destroy(lfgpu_plan* plan) {
   return LFGPU_OK;
 }
 
+// Staging bytes per tensor: n doubles, or (narrowed staging) n floats plus
+// n bf16 at a 256-byte aligned offset — never more than 8n + 256.
+static size_t stage_bytes(int64_t n) { return sizeof(double) * std::max<int64_t>(n, 1) + 256; }
+static size_t stage_bf16_offset(int64_t n) { return (sizeof(float) * std::max<int64_t>(n, 1) + 255) & ~size_t(255); }
+
 static void host_stage_alloc(PTensor& t, int64_t n) {
   if (t.d_f64) return;
-  t.d_f64 = dev_alloc(sizeof(double) * std::max<int64_t>(n, 1));
+  t.d_f64 = dev_alloc(stage_bytes(n));
   if (!t.d_f64) fail(LFGPU_ECUDA, "device allocation of the f64 staging buffer");
-  CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&t.h_pin), sizeof(double) * std::max<int64_t>(n, 1),
-                        cudaHostAllocDefault));
+  CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&t.h_pin), stage_bytes(n), cudaHostAllocDefault));
+}
+
+// Host restatements of the device conversions the K1 copy applies to f64
+// sources (k_copy.cu Elem<float>::from_d = cvt.rn.f32.f64, Elem<bf16>::from_d
+// = cvt.rn.bf16.f32 of that float): round to nearest even, subnormals kept,
+// any NaN -> the canonical bf16 NaN 0x7fff. Narrowing on the host moves 4 or
+// 2 bytes per element over the link instead of 8 with bit-identical values.
+static inline uint16_t host_bf16_rn(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  if ((x & 0x7fffffffu) > 0x7f800000u) return 0x7fffu;
+  x += 0x7fffu + ((x >> 16) & 1u);
+  return static_cast<uint16_t>(x >> 16);
 }
 
 // A small pool of host worker threads for the host-buffer entry points:
@@ -1821,6 +1838,84 @@ static void stage_d2h(void* dst, void* h_pin, const void* d_src, size_t bytes, c
   }
 }
 
+// user doubles -> (host threads: narrow to f32 and / or bf16) -> pinned ->
+// device staging, chunk by chunk: chunk i+1's conversion overlaps chunk i's DMA.
+static void stage_h2d_narrow(PTensor& t, const double* src, int64_t n, bool want_f32, bool want_bf16,
+                             cudaStream_t st) {
+  float* hf = reinterpret_cast<float*>(t.h_pin);
+  uint16_t* hb = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(t.h_pin) + stage_bf16_offset(n));
+  char* df = static_cast<char*>(t.d_f64);
+  char* db = df + stage_bf16_offset(n);
+  constexpr int64_t kChunk = 512 * 1024;  // elements
+  HostPool& pool = HostPool::get();
+  for (int64_t off = 0; off < n; off += kChunk) {
+    const int64_t len = std::min(kChunk, n - off);
+    const int nt = len >= 65536 ? pool.size() : 1;
+    auto work = [&](int i) {
+      const int64_t per = (len + nt - 1) / nt;
+      const int64_t a = off + std::min(len, per * i), b = off + std::min(len, per * (i + 1));
+      for (int64_t e = a; e < b; ++e) {
+        const float f = static_cast<float>(src[e]);
+        if (want_f32) hf[e] = f;
+        if (want_bf16) hb[e] = host_bf16_rn(f);
+      }
+    };
+    if (nt == 1) work(0);
+    else pool.run(nt, work);
+    if (want_f32)
+      CUDA_OK(cudaMemcpyAsync(df + 4 * off, hf + off, 4 * len, cudaMemcpyHostToDevice, st));
+    if (want_bf16)
+      CUDA_OK(cudaMemcpyAsync(db + 2 * off, hb + off, 2 * len, cudaMemcpyHostToDevice, st));
+  }
+}
+
+// device f32 staging -> pinned -> user doubles (float -> double is exact),
+// chunk i's widening overlapping chunk i+1's DMA.
+static void stage_d2h_widen(double* dst, const PTensor& t, int64_t n, cudaStream_t st, std::vector<cudaEvent_t>& ev) {
+  constexpr int64_t kChunk = 512 * 1024;
+  const int64_t nch = (n + kChunk - 1) / kChunk;
+  while (static_cast<int64_t>(ev.size()) < nch) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+  }
+  const float* hf = reinterpret_cast<const float*>(t.h_pin);
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t off = c * kChunk, len = std::min(kChunk, n - off);
+    CUDA_OK(cudaMemcpyAsync(reinterpret_cast<float*>(t.h_pin) + off, static_cast<const float*>(t.d_f64) + off, 4 * len, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaEventRecord(ev[c], st));
+  }
+  HostPool& pool = HostPool::get();
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t off = c * kChunk, len = std::min(kChunk, n - off);
+    CUDA_OK(cudaEventSynchronize(ev[c]));
+    const int nt = len >= 65536 ? pool.size() : 1;
+    auto work = [&](int i) {
+      const int64_t per = (len + nt - 1) / nt;
+      const int64_t a = off + std::min(len, per * i), b = off + std::min(len, per * (i + 1));
+      for (int64_t e = a; e < b; ++e) dst[e] = hf[e];
+    };
+    if (nt == 1) work(0);
+    else pool.run(nt, work);
+  }
+}
+
+// The K1 conversion from a logical source of element type `se` into tensor
+// t's physical storage of element type `de`, compiled once per pair.
+static const CopyKernel& in_copy_kernel(lfgpu_plan* P, PTensor& t, int se, int de) {
+  const int key = se * 8 + de;
+  auto it = t.in_copy.find(key);
+  if (it == t.in_copy.end()) {
+    CopySpec spec;
+    spec.lmap = identity_map(t.logical);
+    spec.dst_seq = t.seq;  // materialize_tensor (interp.cpp:280-337)
+    spec.mode = FoldMode::Clamp;
+    bool oob;
+    it = t.in_copy.emplace(key, compile_copy(spec, se, de, P->keep, &oob)).first;
+  }
+  return it->second;
+}
+
 static void set_input_impl(lfgpu_plan* P, int32_t tensor, const void* d_logical, int32_t elem) {
   if (tensor < 0 || tensor >= static_cast<int32_t>(P->t.size()))
     fail(LFGPU_EINVAL, "tensor index out of range");
@@ -1828,21 +1923,9 @@ static void set_input_impl(lfgpu_plan* P, int32_t tensor, const void* d_logical,
   // Compiled once per (source, destination) element pair and kept with the
   // plan, so a repeated call is only the K1 launch(es), stream-ordered on the
   // plan's stream with no host synchronisation (the serving / e2e path).
-  auto conv = [&](int de) -> const CopyKernel& {
-    const int key = elem * 8 + de;
-    auto it = t.in_copy.find(key);
-    if (it == t.in_copy.end()) {
-      CopySpec spec;
-      spec.lmap = identity_map(t.logical);
-      spec.dst_seq = t.seq;  // materialize_tensor (interp.cpp:280-337)
-      spec.mode = FoldMode::Clamp;
-      bool oob;
-      it = t.in_copy.emplace(key, compile_copy(spec, elem, de, P->keep, &oob)).first;
-    }
-    return it->second;
-  };
-  if (t.d) CUDA_OK(run_copy(conv(t.elem), d_logical, t.d, P->ctx->d_err, P->stream));
-  if (t.d_bf16) CUDA_OK(run_copy(conv(LFGPU_ELEM_BF16), d_logical, t.d_bf16, P->ctx->d_err, P->stream));
+  if (t.d) CUDA_OK(run_copy(in_copy_kernel(P, t, elem, t.elem), d_logical, t.d, P->ctx->d_err, P->stream));
+  if (t.d_bf16)
+    CUDA_OK(run_copy(in_copy_kernel(P, t, elem, LFGPU_ELEM_BF16), d_logical, t.d_bf16, P->ctx->d_err, P->stream));
 }
 
 int lfgpu_plan_set_input(lfgpu_plan* plan, int32_t tensor, const double* host_logical, int64_t n) {
@@ -1857,8 +1940,21 @@ int lfgpu_plan_set_input(lfgpu_plan* plan, int32_t tensor, const double* host_lo
     // user doubles -> pinned staging (host threads) -> device staging (DMA)
     // -> K1 into the plan's physical layout(s); synchronous like the
     // reference's by-value BufferMap.
-    stage_h2d(tt.d_f64, tt.h_pin, host_logical, sizeof(double) * n, plan->stream);
-    set_input_impl(plan, tensor, tt.d_f64, LFGPU_ELEM_F64);
+    const bool f32 = tt.d && tt.elem == LFGPU_ELEM_F32, bf = tt.d_bf16 != nullptr;
+    if ((f32 || !tt.d) && !getenv("LFGPU_STAGE_F64")) {
+      // float storage: narrowed on the host exactly as the device would
+      stage_h2d_narrow(tt, host_logical, n, f32, bf, plan->stream);
+      int* d_err = plan->ctx->d_err;
+      if (f32)
+        CUDA_OK(run_copy(in_copy_kernel(plan, tt, LFGPU_ELEM_F32, LFGPU_ELEM_F32), tt.d_f64, tt.d, d_err,
+                         plan->stream));
+      if (bf)
+        CUDA_OK(run_copy(in_copy_kernel(plan, tt, LFGPU_ELEM_BF16, LFGPU_ELEM_BF16),
+                         static_cast<char*>(tt.d_f64) + stage_bf16_offset(n), tt.d_bf16, d_err, plan->stream));
+    } else {
+      stage_h2d(tt.d_f64, tt.h_pin, host_logical, sizeof(double) * n, plan->stream);
+      set_input_impl(plan, tensor, tt.d_f64, LFGPU_ELEM_F64);
+    }
     CUDA_OK(cudaStreamSynchronize(plan->stream));
   });
 }
@@ -1914,13 +2010,17 @@ int lfgpu_plan_get_output(lfgpu_plan* plan, int32_t tensor, double* host_logical
     if (n != numel(t.logical)) fail(LFGPU_EINVAL, "output size mismatch for '" + t.id + "'");
     if (!t.valid)
       fail(LFGPU_EUNSUPPORTED, "'" + t.id + "' was fused away (epilogue or attention core) and not materialized");
+    // float storage comes back as f32 (exact for f32 and bf16) and is
+    // widened on the host; int32 as f64
+    const int se = t.d ? t.elem : LFGPU_ELEM_BF16;
+    const bool narrow = se != LFGPU_ELEM_I32 && !getenv("LFGPU_STAGE_F64");
     if (!t.out_copy_ready) {
       CopySpec spec;
       spec.lmap = identity_map(t.logical);
       spec.src_seq = t.seq;  // forward map back to logical (interp.cpp:441-468)
       spec.mode = FoldMode::Clamp;
       bool oob;
-      t.out_copy = compile_copy(spec, t.d ? t.elem : LFGPU_ELEM_BF16, LFGPU_ELEM_F64, plan->keep, &oob);
+      t.out_copy = compile_copy(spec, se, narrow ? LFGPU_ELEM_F32 : LFGPU_ELEM_F64, plan->keep, &oob);
       t.out_copy_ready = true;
     }
     host_stage_alloc(t, n);
@@ -1932,7 +2032,8 @@ int lfgpu_plan_get_output(lfgpu_plan* plan, int32_t tensor, double* host_logical
     CUDA_OK(run_copy(t.out_copy, src, t.d_f64, plan->ctx->d_err, plan->stream));
     int* h = plan->h_err;  // the out-of-range flag of this execution, read with the data
     CUDA_OK(cudaMemcpyAsync(h, plan->ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, plan->stream));
-    stage_d2h(host_logical, t.h_pin, t.d_f64, sizeof(double) * n, plan->stream, plan->stage_ev);
+    if (narrow) stage_d2h_widen(host_logical, t, n, plan->stream, plan->stage_ev);
+    else stage_d2h(host_logical, t.h_pin, t.d_f64, sizeof(double) * n, plan->stream, plan->stage_ev);
     if (*h) {
       CUDA_OK(cudaMemsetAsync(plan->ctx->d_err, 0, sizeof(int), plan->stream));
       CUDA_OK(cudaStreamSynchronize(plan->stream));

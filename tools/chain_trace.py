@@ -15,6 +15,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "resnet18":
     fac = workloads.tune_resnet18(1, lambda sub: e2e.make_inputs(sub, gen))
     g, _, p = e2e.build_resnet18(1, fac, flags=0)
     ins = e2e.make_inputs(g, gen)
+elif len(sys.argv) > 1 and sys.argv[1] == "encoder":  # packed-QKV encoder, 2 layers
+    g, gm, p = e2e.build_encoder(2, 64, flags=0, packed_qkv=True)
+    ins = e2e.make_encoder_inputs(g, gen)
 else:
     layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     g, gm, p = e2e.build_bert(layers, 64, flags=0)
