@@ -613,7 +613,10 @@ def run_ours(args, rank, world, local):
         "e2e": {"value": round(e2e_val, 4), "unit": "TFLOP/s",
                 "h2d_bytes_per_step": 2 * M * K * 8, "d2h_bytes_per_step": M * N * 8,
                 "path": "lfgpu_plan_set_input(a, b: host doubles) + lfgpu_plan_run + "
-                        "lfgpu_plan_get_output(c: host doubles), synchronous, one step at a time",
+                        "lfgpu_plan_get_output(c: host doubles), one step at a time; the user's "
+                        "doubles narrowed on the host to the operands' bf16 storage (bit-identical "
+                        "to the device conversion) and c widened back there",
+                "link_bytes_per_step": {"h2d": 2 * M * K * 2, "d2h": M * N * 4},
                 "ms_per_step": round(e2e_s * 1e3, 3), "verified_exact": e2e_ok},
         "e2e_pipelined_fp32": {"value": round(pipe_val, 4), "unit": "TFLOP/s",
                                "h2d_bytes_per_step": 2 * M * K * 4, "d2h_bytes_per_step": M * N * 8,

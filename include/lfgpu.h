@@ -328,7 +328,12 @@ int lfgpu_plan_destroy(lfgpu_plan* plan);
 
 /* Upload an Input/Constant tensor from a host buffer in its logical layout
  * (doubles, as lf::BufferMap holds them; interp.hpp:19-21) and materialize
- * it into the plan's physical layout on the device (K1). */
+ * it into the plan's physical layout on the device (K1). The host buffer has
+ * been read in full when the call returns (by-value, like BufferMap); float
+ * tensors are narrowed to their f32 / bf16 storage on the host, bit-identical
+ * to the device conversion, and the copy to the device is stream-ordered
+ * before the plan's next run / get_output (LFGPU_STAGE_F64=1: stage the
+ * doubles and convert on the device, synchronously). */
 int lfgpu_plan_set_input(lfgpu_plan* plan, int32_t tensor, const double* host_logical,
                          int64_t n);
 /* Same, from a device buffer of `elem` type already in the logical layout.

@@ -203,6 +203,7 @@ struct PTensor {
   // a repeated call is copies + K1 launches only.
   void* d_f64 = nullptr;
   double* h_pin = nullptr;
+  cudaEvent_t staged = nullptr;  // the last staging DMA / K1 out of h_pin / d_f64
   bool out_copy_ready = false;
   CopyKernel out_copy;
   int dtype = LFGPU_DTYPE_F32;
@@ -259,6 +260,7 @@ struct lfgpu_plan {
     for (auto e : stage_ev) cudaEventDestroy(e);
     if (h_err) cudaFreeHost(h_err);
     for (auto& x : t) {
+      if (x.staged) cudaEventDestroy(x.staged);
       if (x.d_f64) dev_free(x.d_f64);
       if (x.h_pin) cudaFreeHost(x.h_pin);
     }
@@ -1705,7 +1707,12 @@ static size_t stage_bytes(int64_t n) { return sizeof(double) * std::max<int64_t>
 static size_t stage_bf16_offset(int64_t n) { return (sizeof(float) * std::max<int64_t>(n, 1) + 255) & ~size_t(255); }
 
 static void host_stage_alloc(PTensor& t, int64_t n) {
-  if (t.d_f64) return;
+  if (t.d_f64) {
+    // the previous call's DMA / conversion out of the staging buffers
+    if (t.staged) CUDA_OK(cudaEventSynchronize(t.staged));
+    return;
+  }
+  CUDA_OK(cudaEventCreateWithFlags(&t.staged, cudaEventDisableTiming));
   t.d_f64 = dev_alloc(stage_bytes(n));
   if (!t.d_f64) fail(LFGPU_ECUDA, "device allocation of the f64 staging buffer");
   CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&t.h_pin), stage_bytes(n), cudaHostAllocDefault));
@@ -1731,7 +1738,7 @@ static inline uint16_t host_bf16_rn(float f) {
 class HostPool {
  public:
   static HostPool& get() {
-    static HostPool p(std::max(2u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+    static HostPool p(std::max(2u, std::min(16u, std::thread::hardware_concurrency())));
     return p;
   }
   int size() const { return static_cast<int>(w_.size()); }
@@ -1846,58 +1853,57 @@ static void stage_h2d_narrow(PTensor& t, const double* src, int64_t n, bool want
   uint16_t* hb = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(t.h_pin) + stage_bf16_offset(n));
   char* df = static_cast<char*>(t.d_f64);
   char* db = df + stage_bf16_offset(n);
-  constexpr int64_t kChunk = 512 * 1024;  // elements
   HostPool& pool = HostPool::get();
-  for (int64_t off = 0; off < n; off += kChunk) {
-    const int64_t len = std::min(kChunk, n - off);
-    const int nt = len >= 65536 ? pool.size() : 1;
-    auto work = [&](int i) {
-      const int64_t per = (len + nt - 1) / nt;
-      const int64_t a = off + std::min(len, per * i), b = off + std::min(len, per * (i + 1));
-      for (int64_t e = a; e < b; ++e) {
-        const float f = static_cast<float>(src[e]);
-        if (want_f32) hf[e] = f;
-        if (want_bf16) hb[e] = host_bf16_rn(f);
-      }
-    };
-    if (nt == 1) work(0);
-    else pool.run(nt, work);
-    if (want_f32)
-      CUDA_OK(cudaMemcpyAsync(df + 4 * off, hf + off, 4 * len, cudaMemcpyHostToDevice, st));
-    if (want_bf16)
-      CUDA_OK(cudaMemcpyAsync(db + 2 * off, hb + off, 2 * len, cudaMemcpyHostToDevice, st));
-  }
+  // each worker narrows one contiguous slice and enqueues its slice's DMA at
+  // once, so early slices travel while later ones are still converted
+  const int nt = n >= 65536 ? pool.size() : 1;
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  auto work = [&](int i) {
+    CUDA_OK(cudaSetDevice(dev));  // pool threads: the plan's device
+    const int64_t per = ((n + nt - 1) / nt + 127) & ~int64_t(127);
+    const int64_t a = std::min(n, per * i), b = std::min(n, per * (i + 1));
+    if (a >= b) return;
+    for (int64_t e = a; e < b; ++e) {
+      const float f = static_cast<float>(src[e]);
+      if (want_f32) hf[e] = f;
+      if (want_bf16) hb[e] = host_bf16_rn(f);
+    }
+    if (want_f32) CUDA_OK(cudaMemcpyAsync(df + 4 * a, hf + a, 4 * (b - a), cudaMemcpyHostToDevice, st));
+    if (want_bf16) CUDA_OK(cudaMemcpyAsync(db + 2 * a, hb + a, 2 * (b - a), cudaMemcpyHostToDevice, st));
+  };
+  if (nt == 1) work(0);
+  else pool.run(nt, work);
 }
 
 // device f32 staging -> pinned -> user doubles (float -> double is exact),
 // chunk i's widening overlapping chunk i+1's DMA.
 static void stage_d2h_widen(double* dst, const PTensor& t, int64_t n, cudaStream_t st, std::vector<cudaEvent_t>& ev) {
-  constexpr int64_t kChunk = 512 * 1024;
-  const int64_t nch = (n + kChunk - 1) / kChunk;
-  while (static_cast<int64_t>(ev.size()) < nch) {
+  HostPool& pool = HostPool::get();
+  const int nt = n >= 65536 ? pool.size() : 1;
+  const int64_t per = ((n + nt - 1) / nt + 127) & ~int64_t(127);
+  while (static_cast<int>(ev.size()) < nt) {
     cudaEvent_t e;
     CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ev.push_back(e);
   }
-  const float* hf = reinterpret_cast<const float*>(t.h_pin);
-  for (int64_t c = 0; c < nch; ++c) {
-    const int64_t off = c * kChunk, len = std::min(kChunk, n - off);
-    CUDA_OK(cudaMemcpyAsync(reinterpret_cast<float*>(t.h_pin) + off, static_cast<const float*>(t.d_f64) + off, 4 * len, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaEventRecord(ev[c], st));
+  float* hf = reinterpret_cast<float*>(t.h_pin);
+  const float* df = static_cast<const float*>(t.d_f64);
+  for (int i = 0; i < nt; ++i) {  // one DMA + event per worker slice
+    const int64_t a = std::min(n, per * i), b = std::min(n, per * (i + 1));
+    if (a < b) CUDA_OK(cudaMemcpyAsync(hf + a, df + a, 4 * (b - a), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaEventRecord(ev[i], st));
   }
-  HostPool& pool = HostPool::get();
-  for (int64_t c = 0; c < nch; ++c) {
-    const int64_t off = c * kChunk, len = std::min(kChunk, n - off);
-    CUDA_OK(cudaEventSynchronize(ev[c]));
-    const int nt = len >= 65536 ? pool.size() : 1;
-    auto work = [&](int i) {
-      const int64_t per = (len + nt - 1) / nt;
-      const int64_t a = off + std::min(len, per * i), b = off + std::min(len, per * (i + 1));
-      for (int64_t e = a; e < b; ++e) dst[e] = hf[e];
-    };
-    if (nt == 1) work(0);
-    else pool.run(nt, work);
-  }
+  int dev = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  auto work = [&](int i) {  // slice i widens as soon as its DMA landed
+    CUDA_OK(cudaSetDevice(dev));
+    const int64_t a = std::min(n, per * i), b = std::min(n, per * (i + 1));
+    CUDA_OK(cudaEventSynchronize(ev[i]));
+    for (int64_t e = a; e < b; ++e) dst[e] = hf[e];
+  };
+  if (nt == 1) work(0);
+  else pool.run(nt, work);
 }
 
 // The K1 conversion from a logical source of element type `se` into tensor
@@ -1951,11 +1957,15 @@ int lfgpu_plan_set_input(lfgpu_plan* plan, int32_t tensor, const double* host_lo
       if (bf)
         CUDA_OK(run_copy(in_copy_kernel(plan, tt, LFGPU_ELEM_BF16, LFGPU_ELEM_BF16),
                          static_cast<char*>(tt.d_f64) + stage_bf16_offset(n), tt.d_bf16, d_err, plan->stream));
+      // The user's buffer has been read in full; the DMA and K1 stay
+      // stream-ordered before the next run / get_output (staging reuse
+      // waits on `staged`).
+      CUDA_OK(cudaEventRecord(tt.staged, plan->stream));
     } else {
       stage_h2d(tt.d_f64, tt.h_pin, host_logical, sizeof(double) * n, plan->stream);
       set_input_impl(plan, tensor, tt.d_f64, LFGPU_ELEM_F64);
+      CUDA_OK(cudaStreamSynchronize(plan->stream));
     }
-    CUDA_OK(cudaStreamSynchronize(plan->stream));
   });
 }
 
