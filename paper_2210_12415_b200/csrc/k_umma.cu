@@ -1262,7 +1262,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   L.splits = 1;
   // A halo C2D stage is KH*KW UMMA groups (heavy), so a split may be a
   // single stage there; a GEMM / per-tap stage is one K step (>= 4 each).
-  const int min_stages = p.ntaps > 1 ? 1 : 4;
+  const int min_stages = p.kind == UMMA_GEMM ? std::max(1, 4 / p.ntaps) : (p.ntaps > 1 ? 1 : 4);
   if (p.split_pref != 1 && L.ntiles * 2 <= sms && L.nstages >= 2 * min_stages) {
     L.splits = std::min({sms / L.ntiles, L.nstages / min_stages, 8});
     if (L.splits < 2) L.splits = 1;

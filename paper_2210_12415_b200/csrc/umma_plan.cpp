@@ -302,10 +302,21 @@ bool gemm_operand(const std::vector<Dim>& log, const Seq& seq, int mn_lj, int k_
     v->boxes = 1;
     if (!cover(mnd, T_mn, &bmn, why)) return false;
     for (size_t i = 0; i < mnd.size(); ++i) box[mnd[i] - ds.data()] = bmn[i];
-    box[ds.size() - 1] = KC;
-    if (inner.ext % KC) {
-      *why = "K stage does not divide the K brick";
-      return false;
+    if (KC > 64) {
+      // A stage of KC/64 K slabs in one box: the 64-wide K brick plus the
+      // next K digit, landing as KC/64 canonical [rows][64] slabs in SMEM.
+      if (inner.ext != 64) {
+        *why = "multi-slab K stage needs 64-wide K bricks";
+        return false;
+      }
+      if (!cover(kd, KC, &bk, why)) return false;
+      for (size_t i = 0; i < kd.size(); ++i) box[kd[i] - ds.data()] = bk[i];
+    } else {
+      box[ds.size() - 1] = KC;
+      if (inner.ext % KC) {
+        *why = "K stage does not divide the K brick";
+        return false;
+      }
     }
   }
   if (!rows_ordered(ds, box)) {
@@ -532,6 +543,15 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     if (mtiles * ((N + bn - 1) / bn) >= 111) cands.push_back(bn);
   for (int bn : {64, 128, 256, 32, 16})
     if (mtiles * ((N + bn - 1) / bn) < 111) cands.push_back(bn);
+  // K per stage: up to 256 (four 64-wide K slabs per TMA box) — a producer
+  // warp sustains about one TMA request per ~800 cycles whatever its size
+  // (DESIGN.md §4.3), so fewer, larger requests per K byte (cfg2 1024^3 at
+  // BN 64: 11.9 / 10.4 / 9.3 us for 64 / 128 / 256, tools/kcs_probe.py);
+  // smaller when the layouts (K bricks of 64 outside the M / N bricks) or
+  // two stages of SMEM cannot take it. LFGPU_GEMM_KCS overrides.
+  int kcs_pref = 256;
+  if (const char* e = getenv("LFGPU_GEMM_KCS")) kcs_pref = atoi(e);
+  if (kcs_pref != 64 && kcs_pref != 128 && kcs_pref != 256) kcs_pref = 64;
   std::string last_why;
   for (int BN : cands) {
     if (N % BN && N > BN) continue;
@@ -541,7 +561,32 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     std::vector<int64_t> am, bm;
     UmmaPlan q = p;
     q.BN = BN;
-    if (!gemm_operand(a_log, a_seq, 0, 1, RT, 64, &q.A, &ads, &abox, &ag, &am, &last_why)) {
+    int kcs = kcs_pref;
+    bool a_ok = false, b_ok = false;
+    for (; kcs >= 64; kcs /= 2) {
+      if (K % kcs || (kcs > 64 && RT != 128)) continue;
+      std::string wa, wb;
+      a_ok = gemm_operand(a_log, a_seq, 0, 1, RT, kcs, &q.A, &ads, &abox, &ag, &am, &wa);
+      b_ok = a_ok && gemm_operand(b_log, b_seq, 1, 0, BN, kcs, &q.B, &bds, &bbox, &bg, &bm, &wb);
+      if (a_ok && b_ok && kcs > 64) {
+        // Two stages must fit beside the tables, and beside the epilogue
+        // buffers unless every CTA gets one tile (they then alias the ring,
+        // k_umma.cu layout_smem).
+        OperandView ta = q.A, tb = q.B;
+        finish_descriptor(&ta, 128);
+        finish_descriptor(&tb, BN);
+        const int per = ta.slot_bytes * ta.boxes + tb.slot_bytes * tb.boxes;
+        const int64_t ntiles = mtiles * ((N + BN - 1) / BN);
+        const int epi = ntiles <= 148 && !getenv("LFGPU_NO_EPI_ALIAS") ? 0 : kEpiSmemBytes;
+        if (2 * per > 227 * 1024 - epi - 12 * 1024) {
+          a_ok = b_ok = false;
+          continue;
+        }
+      }
+      if (a_ok && b_ok) break;
+      if (kcs == 64) last_why = a_ok ? wb : wa;
+    }
+    if (!a_ok) {
       *why = "A: " + last_why;
       return false;
     }
@@ -549,7 +594,7 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
       *why = "A: partial row tiles need a K-major A";
       return false;
     }
-    if (!gemm_operand(b_log, b_seq, 1, 0, BN, 64, &q.B, &bds, &bbox, &bg, &bm, &last_why)) {
+    if (!b_ok) {
       last_why = "B: " + last_why;
       continue;
     }
@@ -562,6 +607,16 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     }
     finish_descriptor(&q.A, 128);
     finish_descriptor(&q.B, BN);
+    // Multi-slab stages run as KC/64 UMMA groups ("taps") of 4 K-steps, tap t
+    // reading slab t: K-major slabs are [rows][64] (rows x 128 B), MN-major
+    // ones 64 K rows of 128 B inside each box.
+    q.ntaps = kcs / 64;
+    q.a_tap.clear();
+    q.b_tapv.clear();
+    for (int t = 0; t < q.ntaps; ++t) {
+      q.a_tap.push_back(t * (q.A.mn_major ? 64 * 128 : 128 * 128));
+      q.b_tapv.push_back(t * (q.B.mn_major ? 64 * 128 : BN * 128));
+    }
     const int64_t ntile_n = (N + BN - 1) / BN;
     for (int64_t tm = 0; tm < mtiles; ++tm)
       for (int64_t tn = 0; tn < ntile_n; ++tn) {
@@ -582,7 +637,7 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
         te.n_base = static_cast<int32_t>(tn * BN);
         q.tiles.push_back(te);
       }
-    for (int64_t k0 = 0; k0 < K; k0 += 64) {
+    for (int64_t k0 = 0; k0 < K; k0 += kcs) {
       StageEntry se;
       std::memset(&se, 0, sizeof(se));
       int64_t la[2] = {0, k0}, lb[2] = {k0, 0};
@@ -612,7 +667,7 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     }
     q.pipe = pick_pipe(q);
     std::ostringstream os;
-    os << "gemm BM=128" << (RT != 128 ? "(rows " + std::to_string(RT) + ")" : std::string()) << " BN=" << BN << " KC=64 A=" << (q.A.mn_major ? "MN" : "K") << "-major B="
+    os << "gemm BM=128" << (RT != 128 ? "(rows " + std::to_string(RT) + ")" : std::string()) << " BN=" << BN << " KC=" << kcs << " A=" << (q.A.mn_major ? "MN" : "K") << "-major B="
        << (q.B.mn_major ? "MN" : "K") << "-major tiles=" << q.tiles.size() << " pipe=" << q.pipe;
     q.summary = os.str();
     q.persistent = s.parallel;

@@ -169,8 +169,26 @@ def make_encoder_inputs(g, gen, head_dim=64):
     return out
 
 
+def kouter_activations(g, seqs, t):
+    """Activations [M, N] as column bricks [N/t][M][t] (split + reorder, a
+    layout of the reference's language): a GEMM reading one as its A operand
+    gets several 64-wide K slabs per TMA box (K bricks outside the rows),
+    which the row-major bricks [M][N/t][t] that decode_layout gives at
+    m_t = M cannot. Weights, biases and LayerNorm parameters keep theirs."""
+    from .layout import reorder, split
+    for tdecl in g.tensors:
+        if len(tdecl.extents) != 2 or tdecl.id.endswith(("_w", "_b", "_gb")):
+            continue
+        n = tdecl.extents[1]
+        tt = min(t, n)
+        if n % tt:
+            continue
+        seqs[tdecl.id] = [split(1, [n // tt, tt]), reorder([1, 0, 2])]
+    return seqs
+
+
 def build_encoder(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH, seq=128, hidden=768, heads=12,
-                  ffn=3072, packed_qkv=False):
+                  ffn=3072, packed_qkv=False, kouter=True):
     """cfg5 as a full BERT-base encoder (workloads.bert_encoder): every GMM
     on tcgen05 in GMM brick layouts (m_t = seq, k_t = n_t = t) with its
     BiasAdd / residual EwAdd / GELU fused into the epilogue; attention
@@ -185,10 +203,12 @@ def build_encoder(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH, seq=
         seqs.update(runtime.decode_layout(g, ni, [seq, min(t, K), min(t, N)]))
         scheds.append(runtime.sched(ni, tile_last=min(t, N), order=order, fuse=1))
     seqs = workloads.propagate_elementwise(g, seqs)
+    if kouter:
+        seqs = kouter_activations(g, seqs, t)
     return g, gmms, runtime.Plan(g, seqs, scheds, flags, ctx=ctx)
 
 
-def build_bert(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH):
+def build_bert(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH, kouter=True):
     g, gmms = workloads.bert_chain(layers)
     seqs, scheds = {}, []
     for ni in gmms:
@@ -198,4 +218,6 @@ def build_bert(layers, t, order=0, ctx=None, flags=_abi.PLAN_CUDA_GRAPH):
         seqs.update(runtime.decode_layout(g, ni, [128, min(t, K), min(t, N)]))
         scheds.append(runtime.sched(ni, tile_last=min(t, N), order=order, fuse=1))
     seqs = workloads.propagate_elementwise(g, seqs)
+    if kouter:
+        seqs = kouter_activations(g, seqs, t)
     return g, gmms, runtime.Plan(g, seqs, scheds, flags, ctx=ctx)

@@ -538,3 +538,37 @@ def test_split_k_dsmem_exchange(K, N, f, bk, knob, monkeypatch):
     p.run()
     got = p.get_output("c")
     assert np.array_equal(got, ref["c"]), np.abs(got - ref["c"]).max()
+
+
+@pytest.mark.parametrize("kcs", ["64", "128", "256"])
+@pytest.mark.parametrize("layout", ["tuned", "a_mn", "b_k", "kouter_rows"])
+def test_gemm_multi_slab_stages(layout, kcs, monkeypatch):
+    """K per stage of the 1-CTA GEMM: 64, 128 or 256 (several 64-wide K
+    slabs per TMA box, one UMMA group per slab) on K-major and MN-major A
+    and B, and on column-brick activations [K/64][M][64]; bit-exact against
+    the oracle whatever the stage depth."""
+    monkeypatch.setenv("LFGPU_NO_PAIR", "1")
+    monkeypatch.setenv("LFGPU_GEMM_KCS", kcs)
+    M, K, N = 256, 1024, 512
+    g = ir.gemm(M, K, N)
+    if layout == "tuned":
+        seqs = runtime.decode_layout(g, 0, [128, 64, 64])
+    elif layout == "a_mn":  # A [K/64][M/64][64 k][64 m]: MN-major A
+        seqs = runtime.decode_layout(g, 0, [128, 64, 64])
+        seqs["a"] = [split(0, [M // 64, 64]), split(2, [K // 64, 64]), reorder([2, 0, 3, 1])]
+    elif layout == "b_k":  # B [N/64][K/64][64 n][64 k]: K-major B
+        seqs = runtime.decode_layout(g, 0, [128, 64, 64])
+        seqs["b"] = [split(0, [K // 64, 64]), split(2, [N // 64, 64]), reorder([2, 0, 3, 1])]
+    else:  # A as column bricks over full rows, C the same
+        seqs = runtime.decode_layout(g, 0, [128, 64, 64])
+        seqs["a"] = [split(1, [K // 64, 64]), reorder([1, 0, 2])]
+        seqs["c"] = [split(1, [N // 64, 64]), reorder([1, 0, 2])]
+    inputs, ref = oracle_outputs(g, 37)
+    p = runtime.Plan(g, seqs, [runtime.sched(0, tile_last=64, tile_second=128)], flags=_abi.PLAN_REQUIRE_TC)
+    k = p.node_kernel(0)
+    assert k.startswith("umma_gemm") and "KC=" in k, k
+    assert int(k.split("KC=")[1].split(" ")[0]) == int(kcs), k
+    for tid, v in inputs.items():
+        p.set_input(tid, v)
+    p.run()
+    assert np.array_equal(p.get_output("c"), ref["c"]), k
