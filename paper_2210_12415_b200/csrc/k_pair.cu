@@ -66,6 +66,7 @@ struct PairParams {
   int32_t a_boxes, b_boxes, a_slot, b_slot, stage_bytes, tx_bytes, pipe, BN;
   uint64_t a_desc, b_desc;
   uint32_t a_kadv, b_kadv, idesc, tmem_cols;
+  int32_t slabs, a_slab16, b_slab16;  // multi-slab stages: slab offsets in 16-byte units
   int32_t ring_bytes;
   int32_t col_unit;
   // Diagnostics (lfgpu_debug_umma_trace): 256 %globaltimer stamps per CTA:
@@ -223,7 +224,7 @@ __device__ __forceinline__ void store_chunk(const PairParams& P, const Smem& T, 
 // SPLIT: K splits reduce through the L2 workspace (S > 1); UNIT: row-segment
 // stores (contiguous 32-column output chunks). One instance per combination
 // keeps each kernel's code within the SM's instruction cache.
-template <bool SPLIT, bool UNIT>
+template <bool SPLIT, bool UNIT, bool MULTI>
 __global__ void __launch_bounds__(kThreads, 1)
     pair_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                 const __grid_constant__ PairParams P) {
@@ -402,10 +403,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (issuer) {
           const uint32_t a_addr = ring0 + slot * P.stage_bytes;
           const uint64_t ad = P.a_desc | (a_addr >> 4), bd = P.b_desc | ((a_addr + b_off) >> 4);
-          if (!(P.diag & 2))  // diag bit 1: no MMAs (ingest probe; results are garbage)
+          if constexpr (MULTI) {  // several 64-wide K slabs per stage
+            if (!(P.diag & 2))
+              for (int sl = 0; sl < P.slabs; ++sl)
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              umma2_bf16(d, ad + k * akadv, bd + k * bkadv, P.idesc, (s != s_lo) | k);
+                for (int k = 0; k < 4; ++k)
+                  umma2_bf16(d, ad + sl * P.a_slab16 + k * akadv, bd + sl * P.b_slab16 + k * bkadv, P.idesc,
+                             (s != s_lo) | sl | k);
+          } else {
+            if (!(P.diag & 2))  // diag bit 1: no MMAs (ingest probe; results are garbage)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                umma2_bf16(d, ad + k * akadv, bd + k * bkadv, P.idesc, (s != s_lo) | k);
+          }
           umma2_commit_mc(empty0 + 8 * slot, pair_mask);
         }
         __syncwarp();
@@ -600,18 +610,24 @@ void* upload(const std::vector<T>& v) {
   return d;
 }
 
-// The kernel instance for (split-K, row-segment stores), with its dynamic
-// SMEM limit raised once.
-const void* pair_instance(bool split, bool unit) {
-  static const void* fns[4] = {
-      reinterpret_cast<const void*>(pair_kernel<false, false>), reinterpret_cast<const void*>(pair_kernel<false, true>),
-      reinterpret_cast<const void*>(pair_kernel<true, false>), reinterpret_cast<const void*>(pair_kernel<true, true>)};
+// The kernel instance for (split-K, row-segment stores, multi-slab stages),
+// with its dynamic SMEM limit raised once.
+const void* pair_instance(bool split, bool unit, bool multi) {
+  static const void* k[8] = {
+      reinterpret_cast<const void*>(pair_kernel<false, false, false>),
+      reinterpret_cast<const void*>(pair_kernel<false, true, false>),
+      reinterpret_cast<const void*>(pair_kernel<true, false, false>),
+      reinterpret_cast<const void*>(pair_kernel<true, true, false>),
+      reinterpret_cast<const void*>(pair_kernel<false, false, true>),
+      reinterpret_cast<const void*>(pair_kernel<false, true, true>),
+      reinterpret_cast<const void*>(pair_kernel<true, false, true>),
+      reinterpret_cast<const void*>(pair_kernel<true, true, true>)};
   static bool attr_set = [] {
-    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    for (const void* f : k) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     return true;
   }();
   (void)attr_set;
-  return fns[(split ? 2 : 0) + (unit ? 1 : 0)];
+  return k[(multi ? 4 : 0) + (split ? 2 : 0) + (unit ? 1 : 0)];
 }
 
 }  // namespace
@@ -653,6 +669,9 @@ PairLaunch pair_prepare(const PairPlan& p) {
   L.b_desc = umma_desc_bits(p.B);
   L.a_kadv = p.A.k_adv;
   L.b_kadv = p.B.k_adv;
+  L.slabs = p.slabs;
+  L.a_slab = p.a_slab;
+  L.b_slab = p.b_slab;
   L.idesc = umma_idesc(256, p.BN, p.A.mn_major, p.B.mn_major);
   int cols = 32;
   while (cols < 2 * p.BN) cols *= 2;
@@ -700,7 +719,7 @@ PairLaunch pair_prepare(const PairPlan& p) {
   // one, or the parity wait on a ring slot two phases behind passes early.
   L.nprod = std::min(L.nprod, L.pipe);
   // Persistent grid: as many clusters as can be co-resident, at most one per tile.
-  const void* kfn = pair_instance(L.S > 1, L.col_unit != 0);
+  const void* kfn = pair_instance(L.S > 1, L.col_unit != 0, L.slabs > 1);
   const int csize = 2 * L.S;
   int max_cl = umma_num_sms() / csize;
   {
@@ -758,6 +777,9 @@ cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
   P.b_desc = L.b_desc;
   P.a_kadv = L.a_kadv;
   P.b_kadv = L.b_kadv;
+  P.slabs = L.slabs;
+  P.a_slab16 = L.a_slab >> 4;
+  P.b_slab16 = L.b_slab >> 4;
   P.idesc = L.idesc;
   P.tmem_cols = L.tmem_cols;
   P.ring_bytes = L.ring_bytes;
@@ -789,7 +811,7 @@ cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
   void* args[] = {const_cast<CUtensorMap*>(&L.tma_a), const_cast<CUtensorMap*>(&L.tma_b), &P};
-  return cudaLaunchKernelExC(&cfg, pair_instance(L.S > 1, L.col_unit != 0), args);
+  return cudaLaunchKernelExC(&cfg, pair_instance(L.S > 1, L.col_unit != 0, L.slabs > 1), args);
 }
 
 }  // namespace lfg

@@ -65,7 +65,9 @@ struct PairPlan {
   int S = 1;      // K splits (cluster = 2*S CTAs)
   int MT = 0;     // 128-row blocks (even)
   int NT = 0;     // BN-column pair tiles
-  int KS = 0;     // K stages of 64
+  int KS = 0;     // K stages of 64 * slabs
+  int slabs = 1;  // 64-wide K slabs per stage (one TMA box each operand)
+  int a_slab = 0, b_slab = 0;  // SMEM bytes between slabs inside a box
   int pipe = 4;
   int rx_bytes = 0;  // S > 1 with one tile per cluster: DSMEM receive buffer
   int group = 8;     // tile rasterization: row pairs that sweep the column tiles together (loop point `parallel`)
@@ -99,6 +101,7 @@ struct PairLaunch {
   int a_box_bytes = 0;
   uint64_t a_desc = 0, b_desc = 0;
   uint32_t a_kadv = 0, b_kadv = 0, idesc = 0, tmem_cols = 0;
+  int slabs = 1, a_slab = 0, b_slab = 0;
   int ring_bytes = 0;
   int col_unit = 0;
   int epi_kinds[kMaxEpi] = {};

@@ -1493,8 +1493,12 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     *why = "output layout is not a brick layout";
     return false;
   }
-  const int KS = static_cast<int>(K / 64);
   const int sms = 148;
+  // K per stage as in the 1-CTA kernel (umma_plan_gemm): several 64-wide K
+  // slabs per TMA box when the layouts and two stages of SMEM allow.
+  int kcs_pref = 256;
+  if (const char* e = getenv("LFGPU_GEMM_KCS")) kcs_pref = atoi(e);
+  if (kcs_pref != 64 && kcs_pref != 128 && kcs_pref != 256) kcs_pref = 64;
   int force_bn = 0, force_s = 0;
   if (const char* e = getenv("LFGPU_PAIR_BN")) force_bn = atoi(e);
   if (const char* e = getenv("LFGPU_PAIR_S")) force_s = atoi(e);
@@ -1513,122 +1517,140 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
       last_why = "N not a multiple of the pair tile";
       continue;
     }
-    PairPlan q;
-    q.BN = BN;
-    std::vector<PDigit> ads, bds;
-    std::vector<int64_t> abox, bbox, tmp;
-    std::vector<int> ag, bg;
-    std::vector<int64_t> am, bm;
-    if (!gemm_operand(a_log, a_seq, 0, 1, 128, 64, &q.A, &ads, &abox, &ag, &am, &last_why)) {
-      *why = "A: " + last_why;
-      return false;
-    }
-    if (!gemm_operand(b_log, b_seq, 1, 0, BN / 2, 64, &q.B, &bds, &bbox, &bg, &bm, &last_why)) {
-      last_why = "B: " + last_why;
-      continue;
-    }
-    if (!cover(digits_of(cds, 0), 128, &tmp, &last_why) ||
-        !cover(digits_of(cds, 1), BN, &tmp, &last_why)) {
-      last_why = "C: " + last_why;
-      continue;
-    }
-    finish_descriptor(&q.A, 128);
-    finish_descriptor(&q.B, BN / 2);
-    q.MT = static_cast<int>(M / 128);
-    q.NT = static_cast<int>(N / BN);
-    q.KS = KS;
-    for (int mi = 0; mi < q.MT; ++mi)
-      for (int b = 0; b < q.A.boxes; ++b) {
-        int64_t lv[2] = {mi * 128 + (q.A.mn_major ? b * 64 : 0), 0};
-        int32_t c[5];
-        coords(ads, ag, am, lv, c);
-        q.a_crd.insert(q.a_crd.end(), c, c + 5);
+    // Multi-slab stages only for short K loops: deeper rings of 64-wide
+    // stages win once the tensor pipe binds (2048^3 and up, measured).
+    bool found = false;
+    for (int kcs = K <= 1024 ? kcs_pref : 64; kcs >= 64 && !found; kcs /= 2) {
+      if (K % kcs) continue;
+      PairPlan q;
+      q.BN = BN;
+      std::vector<PDigit> ads, bds;
+      std::vector<int64_t> abox, bbox, tmp;
+      std::vector<int> ag, bg;
+      std::vector<int64_t> am, bm;
+      {
+        std::string wa, wb;
+        if (!gemm_operand(a_log, a_seq, 0, 1, 128, kcs, &q.A, &ads, &abox, &ag, &am, &wa)) {
+          if (kcs == 64) {
+            *why = "A: " + wa;
+            return false;
+          }
+          continue;
+        }
+        if (!gemm_operand(b_log, b_seq, 1, 0, BN / 2, kcs, &q.B, &bds, &bbox, &bg, &bm, &wb)) {
+          last_why = "B: " + wb;
+          continue;
+        }
       }
-    for (int nb = 0; nb < 2 * q.NT; ++nb)
-      for (int b = 0; b < q.B.boxes; ++b) {
-        int64_t lv[2] = {0, static_cast<int64_t>(nb) * (BN / 2) + (q.B.mn_major ? b * 64 : 0)};
-        int32_t c[5];
-        coords(bds, bg, bm, lv, c);
-        q.b_crd.insert(q.b_crd.end(), c, c + 5);
+      const int KS = static_cast<int>(K / kcs);
+      q.slabs = kcs / 64;
+      q.a_slab = q.A.mn_major ? 64 * 128 : 128 * 128;
+      q.b_slab = q.B.mn_major ? 64 * 128 : (BN / 2) * 128;
+      if (!cover(digits_of(cds, 0), 128, &tmp, &last_why) ||
+          !cover(digits_of(cds, 1), BN, &tmp, &last_why)) {
+        last_why = "C: " + last_why;
+        continue;
       }
-    for (int64_t k0 = 0; k0 < K; k0 += 64) {
-      int64_t la[2] = {0, k0}, lb[2] = {k0, 0};
-      int32_t ca[5], cb[5];
-      coords(ads, ag, am, la, ca);
-      coords(bds, bg, bm, lb, cb);
-      q.s_crd.insert(q.s_crd.end(), ca, ca + 5);
-      q.s_crd.insert(q.s_crd.end(), cb, cb + 5);
-    }
-    for (int mi = 0; mi < q.MT; ++mi) {
-      int64_t lv[2] = {static_cast<int64_t>(mi) * 128, 0};
-      q.out_r.push_back(offset_of(cds, lv));
-    }
-    for (int nj = 0; nj < q.NT; ++nj) {
-      int64_t lv[2] = {0, static_cast<int64_t>(nj) * BN};
-      q.out_c.push_back(offset_of(cds, lv));
-    }
-    for (int r = 0; r < 128; ++r) {
-      int64_t lv[2] = {r, 0};
-      q.row_off.push_back(offset_of(cds, lv));
-    }
-    for (int c = 0; c < BN; ++c) {
-      int64_t lv[2] = {0, c};
-      q.col_off.push_back(offset_of(cds, lv));
-    }
-    const int stage = q.A.slot_bytes * q.A.boxes + q.B.slot_bytes * q.B.boxes;
-    // 227 KB minus alignment slack, 4 epilogue transpose buffers and barriers.
-    if (q.MT + q.NT > 4096) {
-      last_why = "pair GEMM output tables exceed SMEM";
-      continue;
-    }
-    const int budget = 227 * 1024 - 1024 - 8 * 32 * 36 * 4 - 512 -
-                       static_cast<int>(pair_table_bytes(KS, q.MT, q.NT, BN, q.A.boxes, q.B.boxes));
-    const int tiles = q.MT / 2 * q.NT;
-    for (int S : {1, 2, 4}) {
-      // Split K with one tile per cluster exchanges partials over DSMEM: a
-      // dedicated receive buffer of (S-1) x 128 x BN/S fp32 (the send
-      // staging aliases the idle operand ring).
-      bool dsm = S > 1 && tiles <= sms / (2 * S) && !getenv("LFGPU_PAIR_NO_DSMEM");
-      const int rx = (S - 1) * 128 * (BN / S) * 4;
-      // send staging: each epilogue warp stages its chunks of the sibling slices
-      if (dsm && std::max(2, std::min(8, (budget - rx) / stage)) * stage < ((BN / 64) * (S - 1) + S - 1) / S * 8 * 4096)
-        dsm = false;
-      q.rx_bytes = dsm ? rx : 0;
-      q.pipe = std::max(2, std::min(8, (budget - q.rx_bytes) / stage));
-      if (const char* e = getenv("LFGPU_PAIR_PIPE")) q.pipe = std::max(2, std::min(q.pipe, atoi(e)));
-      if (force_s && S != force_s) continue;
-      if (!force_s && s.order == 1 && S > 1) continue;
-      if (!force_s && s.order == 2 && S < 2) continue;
-      if (KS % S || (BN / S) % 32) continue;
-      // Measured: with S > 1 (clusters of 4-8 CTAs) a second TMA box per
-      // operand in the second and later pairs of a cluster reads wrong data
-      // (MN-major B with BN/2 = 128, tests/test_gpu_pair.py); the first pair
-      // and K-major single-box operands are exact. Split only single-box tiles.
-      if (S > 1 && (q.A.boxes > 1 || q.B.boxes > 1)) continue;
-      if (S > 1 && KS / S < 2) continue;
-      // Cost model (cycles): waves x stages x max(MMA, ingest) + epilogue
-      // + split reduction + fixed latency. Ingest assumed ~48 B/clk/SM.
-      const int clusters = std::max(1, std::min(tiles, sms / (2 * S)));
-      const int waves = (tiles + clusters - 1) / clusters;
-      const double per_stage = std::max(2.0 * BN, stage / 48.0);
-      const double epi = 128.0 * BN * 4 / 64.0;
-      const double red = S == 1 ? 0.0
-                         : dsm ? ((S - 1.0) * 128 * BN / S * 4) / 20.0
-                               : (2.0 * 128 * BN * 4 + (S + 1.0) * 128 * BN / S * 4) / 64.0;
-      const double cost = waves * ((KS / S) * per_stage + epi + red) + 2500.0;
-      if (cost < best_cost) {
-        best_cost = cost;
-        best = q;
-        best.S = S;
+      finish_descriptor(&q.A, 128);
+      finish_descriptor(&q.B, BN / 2);
+      q.MT = static_cast<int>(M / 128);
+      q.NT = static_cast<int>(N / BN);
+      q.KS = KS;
+      for (int mi = 0; mi < q.MT; ++mi)
+        for (int b = 0; b < q.A.boxes; ++b) {
+          int64_t lv[2] = {mi * 128 + (q.A.mn_major ? b * 64 : 0), 0};
+          int32_t c[5];
+          coords(ads, ag, am, lv, c);
+          q.a_crd.insert(q.a_crd.end(), c, c + 5);
+        }
+      for (int nb = 0; nb < 2 * q.NT; ++nb)
+        for (int b = 0; b < q.B.boxes; ++b) {
+          int64_t lv[2] = {0, static_cast<int64_t>(nb) * (BN / 2) + (q.B.mn_major ? b * 64 : 0)};
+          int32_t c[5];
+          coords(bds, bg, bm, lv, c);
+          q.b_crd.insert(q.b_crd.end(), c, c + 5);
+        }
+      for (int64_t k0 = 0; k0 < K; k0 += kcs) {
+        int64_t la[2] = {0, k0}, lb[2] = {k0, 0};
+        int32_t ca[5], cb[5];
+        coords(ads, ag, am, la, ca);
+        coords(bds, bg, bm, lb, cb);
+        q.s_crd.insert(q.s_crd.end(), ca, ca + 5);
+        q.s_crd.insert(q.s_crd.end(), cb, cb + 5);
       }
-    }
+      for (int mi = 0; mi < q.MT; ++mi) {
+        int64_t lv[2] = {static_cast<int64_t>(mi) * 128, 0};
+        q.out_r.push_back(offset_of(cds, lv));
+      }
+      for (int nj = 0; nj < q.NT; ++nj) {
+        int64_t lv[2] = {0, static_cast<int64_t>(nj) * BN};
+        q.out_c.push_back(offset_of(cds, lv));
+      }
+      for (int r = 0; r < 128; ++r) {
+        int64_t lv[2] = {r, 0};
+        q.row_off.push_back(offset_of(cds, lv));
+      }
+      for (int c = 0; c < BN; ++c) {
+        int64_t lv[2] = {0, c};
+        q.col_off.push_back(offset_of(cds, lv));
+      }
+      const int stage = q.A.slot_bytes * q.A.boxes + q.B.slot_bytes * q.B.boxes;
+      // 227 KB minus alignment slack, 4 epilogue transpose buffers and barriers.
+      if (q.MT + q.NT > 4096) {
+        last_why = "pair GEMM output tables exceed SMEM";
+        continue;
+      }
+      const int budget = 227 * 1024 - 1024 - 8 * 32 * 36 * 4 - 512 -
+                         static_cast<int>(pair_table_bytes(KS, q.MT, q.NT, BN, q.A.boxes, q.B.boxes));
+      const int tiles = q.MT / 2 * q.NT;
+      for (int S : {1, 2, 4}) {
+        // Split K with one tile per cluster exchanges partials over DSMEM: a
+        // dedicated receive buffer of (S-1) x 128 x BN/S fp32 (the send
+        // staging aliases the idle operand ring).
+        bool dsm = S > 1 && tiles <= sms / (2 * S) && !getenv("LFGPU_PAIR_NO_DSMEM");
+        const int rx = (S - 1) * 128 * (BN / S) * 4;
+        // send staging: each epilogue warp stages its chunks of the sibling slices
+        if (dsm && std::max(2, std::min(8, (budget - rx) / stage)) * stage < ((BN / 64) * (S - 1) + S - 1) / S * 8 * 4096)
+          dsm = false;
+        q.rx_bytes = dsm ? rx : 0;
+        q.pipe = std::max(2, std::min(8, (budget - q.rx_bytes) / stage));
+        if (const char* e = getenv("LFGPU_PAIR_PIPE")) q.pipe = std::max(2, std::min(q.pipe, atoi(e)));
+        if (force_s && S != force_s) continue;
+        if (!force_s && s.order == 1 && S > 1) continue;
+        if (!force_s && s.order == 2 && S < 2) continue;
+        if (KS % S || (BN / S) % 32) continue;
+        // Measured: with S > 1 (clusters of 4-8 CTAs) a second TMA box per
+        // operand in the second and later pairs of a cluster reads wrong data
+        // (MN-major B with BN/2 = 128, tests/test_gpu_pair.py); the first pair
+        // and K-major single-box operands are exact. Split only single-box tiles.
+        if (S > 1 && (q.A.boxes > 1 || q.B.boxes > 1)) continue;
+        if (S > 1 && KS / S < 2) continue;
+        if (budget - q.rx_bytes < 2 * stage) continue;  // two stages must fit
+        found = true;
+        // Cost model (cycles): waves x stages x max(MMA, ingest) + epilogue
+        // + split reduction + fixed latency. Ingest assumed ~48 B/clk/SM.
+        const int clusters = std::max(1, std::min(tiles, sms / (2 * S)));
+        const int waves = (tiles + clusters - 1) / clusters;
+        const double per_stage = std::max(2.0 * BN * q.slabs, stage / 48.0);
+        const double epi = 128.0 * BN * 4 / 64.0;
+        const double red = S == 1 ? 0.0
+                           : dsm ? ((S - 1.0) * 128 * BN / S * 4) / 20.0
+                                 : (2.0 * 128 * BN * 4 + (S + 1.0) * 128 * BN / S * 4) / 64.0;
+        const double cost = waves * ((KS / S) * per_stage + epi + red) + 2500.0;
+        if (cost < best_cost) {
+          best_cost = cost;
+          best = q;
+          best.S = S;
+        }
+      }
+    }  // kcs
   }
   if (best_cost >= 1e299) {
     *why = last_why;
     return false;
   }
   std::ostringstream os;
-  os << "gemm-pair BM=256 BN=" << best.BN << " S=" << best.S << " A=" << (best.A.mn_major ? "MN" : "K")
+  os << "gemm-pair BM=256 BN=" << best.BN << " KC=" << 64 * best.slabs << " S=" << best.S << " A=" << (best.A.mn_major ? "MN" : "K")
      << "-major B=" << (best.B.mn_major ? "MN" : "K") << "-major tiles=" << best.MT / 2 * best.NT
      << " pipe=" << best.pipe;
   best.group = s.parallel ? 1 : 8;
