@@ -98,6 +98,12 @@ def gemm_bench(reps=3):
     gemm(reps, (512, 512, 256), 64, 0)
 
 
+def gemm_bench_r03(reps=3):
+    """cfg2 on the layout the round-2 final bench tuner picked (1-CTA BM=128
+    BN=64, multi-slab KC=256)."""
+    gemm(reps, (128, 1024, 128), 64, 1)
+
+
 def conv_b16r02(reps=3):
     conv(reps, 16, (28, 28, 64, 32, 32, 64))
 
