@@ -36,12 +36,16 @@ constexpr int kRowWarps = 8;
 // to NC*32 long: NC is the instance's register budget, chosen on the host).
 template <int NC>
 __global__ void __launch_bounds__(32 * kRowWarps) rows_kernel(const RowsParams P) {
-  LFG_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowWarps + (threadIdx.x >> 5);
+  // row offsets: plan constants, read before the grid-dependency wait
+  const int64_t rx = r < P.rows ? __ldg(P.row_x + r) : 0, ry = r < P.rows ? __ldg(P.row_y + r) : 0;
+  int64_t ox[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) ox[k] = lane + 32 * k < P.d ? __ldg(P.col_x + lane + 32 * k) : 0;
+  LFG_PDL_ENTRY();
   if (r >= P.rows) return;
-  const float* x = P.x + __ldg(P.row_x + r);
-  const int64_t ry = __ldg(P.row_y + r);
+  const float* x = P.x + rx;
   float* y = P.y + ry;
   __nv_bfloat16* yb = P.y_bf16 ? static_cast<__nv_bfloat16*>(P.y_bf16) + ry : nullptr;
   const int d = P.d;
@@ -49,7 +53,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) rows_kernel(const RowsParams P
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int j = lane + 32 * k;
-    v[k] = j < d ? __ldg(x + __ldg(P.col_x + j)) : 0.f;
+    v[k] = j < d ? __ldg(x + ox[k]) : 0.f;
   }
   if (P.op == ROWS_SOFTMAX) {
     float m = -INFINITY;
@@ -101,20 +105,34 @@ __global__ void __launch_bounds__(32 * kRowWarps) rows_kernel(const RowsParams P
 // EPT elements per thread; the row's column offsets are read coalesced once.
 template <int EPT>
 __global__ void __launch_bounds__(256) rows_cta_kernel(const RowsParams P) {
-  LFG_PDL_ENTRY();
   __shared__ float red[2][8];
   const int64_t r = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int d = P.d;
-  const float* x = P.x + __ldg(P.row_x + r);
-  const int64_t ry = __ldg(P.row_y + r);
-  float v[EPT];
-  int64_t oy[EPT];
+  // Offset tables are built with the plan (never written by a kernel): read
+  // before the grid-dependency wait, overlapping the predecessor's tail. The
+  // gamma / beta values are tensor data (set_input may still be writing
+  // them) and are read after it, in parallel with x.
+  const int64_t rx = __ldg(P.row_x + r), ry = __ldg(P.row_y + r);
+  float v[EPT], gam[EPT], bet[EPT];
+  int64_t oy[EPT], ox[EPT], og[EPT], ob[EPT];
+  const bool ln = P.op != ROWS_SOFTMAX;
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int j = tid + 256 * k;
     oy[k] = j < d ? __ldg(P.col_y + j) : 0;
-    v[k] = j < d ? __ldg(x + __ldg(P.col_x + j)) : 0.f;
+    ox[k] = j < d ? __ldg(P.col_x + j) : 0;
+    og[k] = j < d && ln ? __ldg(P.col_gb + j) : 0;
+    ob[k] = j < d && ln ? __ldg(P.col_gb + d + j) : 0;
+  }
+  LFG_PDL_ENTRY();
+  const float* x = P.x + rx;
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const bool in = tid + 256 * k < d;
+    v[k] = in ? __ldg(x + ox[k]) : 0.f;
+    gam[k] = in && ln ? __ldg(P.gb + og[k]) : 0.f;
+    bet[k] = in && ln ? __ldg(P.gb + ob[k]) : 0.f;
   }
   auto block_sum = [&](float a, int slot) {
     a = warp_sum(a);
@@ -167,7 +185,7 @@ __global__ void __launch_bounds__(256) rows_cta_kernel(const RowsParams P) {
   for (int k = 0; k < EPT; ++k) {
     const int j = tid + 256 * k;
     if (j < d) {
-      const float t = (v[k] - mean) * inv * __ldg(P.gb + __ldg(P.col_gb + j)) + __ldg(P.gb + __ldg(P.col_gb + d + j));
+      const float t = (v[k] - mean) * inv * gam[k] + bet[k];
       y[oy[k]] = t;
       if (yb) yb[oy[k]] = __float2bfloat16_rn(t);
     }
@@ -374,11 +392,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.com
 // rows [r0, r0 + nr) of an operand (row offsets rtab, column offsets ctab,
 // head columns [0, Dh)) into dst[nr][dp]; rows at or past `valid` and the
 // padding columns are zero-filled.
-template <int DH, int NT>
+// DP: the SMEM row stride in floats as a compile-time constant (0: dp_rt).
+template <int DH, int NT, int DP = (DH ? ((DH + 3) / 4) * 4 + 4 : 0)>
 __device__ __forceinline__ void attn_gather(float* dst, int dp_rt, const float* src, const int64_t* rtab,
                                             const int64_t* ctab, int r0, int nr, int valid, int dh_rt, bool vec) {
   const int Dh = DH ? DH : dh_rt;
-  const int dp = DH ? ((DH + 3) / 4) * 4 + 4 : dp_rt;
+  const int dp = DP ? DP : dp_rt;
   const int t = threadIdx.x;
   if (vec) {
     const int q4 = dp / 4;
@@ -575,6 +594,257 @@ __global__ void __launch_bounds__(NT, 1) attn_kernel(const BmmParams Q, const Bm
   }
 }
 
+// Attention core on the tensor cores: warp-level mma.sync m16n8k8 TF32 with
+// every fp32 operand split into a TF32 high part and a TF32 residual
+// (3xTF32: lo*hi + hi*lo + hi*hi, the residual products first), which keeps
+// the products to ~2^-21 relative — fp32-level accuracy (the oracle's 1e-5
+// rule holds with three orders of margin) at a tenth of the instructions of
+// the CUDA-core path. One CTA = one head x 16 query rows (the MMA's M), 16
+// warps: S's 8-column n-tiles are dealt over the warps, then a warp-per-row
+// softmax, then PV's n-tiles over the first Dh/8 warps. Same gathers as
+// attn_kernel; SMEM strides padded so every fragment load is conflict-free
+// (K / q rows Dh+4 floats, V rows Dh+8, score rows T'+4).
+__device__ __forceinline__ unsigned long long attn_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct AttnMmaSmem {
+  int chunk, dk, dv, ts;
+  size_t qs, ks, vs, ss, tab, total;
+};
+
+__host__ __device__ inline AttnMmaSmem attn_mma_smem(int T2, int Dh) {
+  AttnMmaSmem L;
+  L.dk = Dh + 4;
+  L.dv = Dh + 8;
+  L.ts = ((T2 + 3) / 4) * 4 + 4;
+  int cap = static_cast<int>((150 * 1024) / (sizeof(float) * (L.dk + L.dv))) / 32 * 32;
+  if (cap < 32) cap = 32;
+  const int t2r = ((T2 + 31) / 32) * 32;
+  L.chunk = t2r < cap ? t2r : cap;
+  L.qs = 0;
+  L.ks = L.qs + sizeof(float) * 16 * L.dk;
+  L.vs = L.ks + sizeof(float) * L.chunk * L.dk;
+  L.ss = L.vs + sizeof(float) * L.chunk * L.dv;
+  L.tab = L.ss + sizeof(float) * 16 * L.ts;
+  L.tab = (L.tab + 15) & ~size_t(15);
+  L.total = L.tab + sizeof(int64_t) * (2 * T2 + 2 * 16 + 4 * Dh);
+  return L;
+}
+
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+
+__device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// c += a * b with a, b split (3xTF32), the residual products first
+__device__ __forceinline__ void mma_3xtf32(float* c, const float* a, const float* b) {
+  uint32_t ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tf32_split(a[i], ah[i], al[i]);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) tf32_split(b[i], bh[i], bl[i]);
+  mma_tf32(c, al, bh);
+  mma_tf32(c, ah, bl);
+  mma_tf32(c, ah, bh);
+}
+// Rows [r0, r0 + nr) of an operand into dst[nr][DP] (columns [0, DH); the
+// padding columns are never read by the MMA fragments): each thread keeps
+// one column piece and walks rows, so a 16-byte (vec) or 4-byte piece costs
+// one row-offset lookup and one cp.async.
+template <int DH, int NT, int DP>
+__device__ __forceinline__ void attn_gather_rows(float* dst, const float* src, const int64_t* rtab,
+                                                 const int64_t* ctab, int r0, int nr, int valid, bool vec) {
+  const int t = threadIdx.x;
+  if (vec) {
+    constexpr int C4 = DH / 4, RS = NT / C4;
+    const int cq = (t % C4) * 4;
+    const int64_t co = ctab[cq];
+    for (int r = t / C4; r < nr; r += RS) {
+      float* d = dst + r * DP + cq;
+      if (r0 + r < valid) cp_async16(d, src + rtab[r0 + r] + co);
+      else *reinterpret_cast<float4*>(d) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  } else {
+    constexpr int RS = NT / DH;
+    const int c = t % DH;
+    const int64_t co = ctab[c];
+    for (int r = t / DH; r < nr; r += RS) {
+      float* d = dst + r * DP + c;
+      if (r0 + r < valid) cp_async4(d, src + rtab[r0 + r] + co);
+      else *d = 0.f;
+    }
+  }
+}
+
+template <int DH, int NC>
+__global__ void __launch_bounds__(512, 1) attn_mma_kernel(const BmmParams Q, const BmmParams V) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int R = 16, NT = 512, NW = NT / 32;
+  const int h = blockIdx.y, i0 = blockIdx.x * R;
+  const int T = Q.T, T2 = Q.T2;
+  const AttnMmaSmem L = attn_mma_smem(T2, DH);
+  constexpr int dk = DH + 4, dv = DH + 8;
+  const int ts = L.ts;
+  float* qs = reinterpret_cast<float*>(smem + L.qs);
+  float* ks = reinterpret_cast<float*>(smem + L.ks);
+  float* vs = reinterpret_cast<float*>(smem + L.vs);
+  float* ss = reinterpret_cast<float*>(smem + L.ss);
+  int64_t* kr = reinterpret_cast<int64_t*>(smem + L.tab);
+  int64_t* vr = kr + T2;
+  int64_t* qr = vr + T2;
+  int64_t* orow = qr + R;
+  int64_t* qc = orow + R;
+  int64_t* kc = qc + DH;
+  int64_t* vc = kc + DH;
+  int64_t* oc = vc + DH;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int g = lane >> 2, tq = lane & 3;  // fragment row group / thread in group
+  if (Q.dbg && t == 0) Q.dbg[16384 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 0] = attn_gtime();
+  for (int e = t; e < T2; e += NT) {
+    kr[e] = __ldg(Q.tb + Q.b_off[0] + e);
+    vr[e] = __ldg(V.tb + V.b_off[0] + e);
+  }
+  if (t < R) {
+    qr[t] = i0 + t < T ? __ldg(Q.ta + Q.a_off[0] + i0 + t) : 0;
+    orow[t] = i0 + t < T ? __ldg(V.to + V.o_off[0] + i0 + t) : 0;
+  }
+  for (int e = t; e < DH; e += NT) {
+    qc[e] = __ldg(Q.ta + Q.a_off[1] + h * DH + e);
+    kc[e] = __ldg(Q.tb + Q.b_off[1] + h * DH + e);
+    vc[e] = __ldg(V.tb + V.b_off[1] + h * DH + e);
+    oc[e] = __ldg(V.to + V.o_off[1] + h * DH + e);
+  }
+  LFG_PDL_ENTRY();
+  if (Q.dbg && t == 0) Q.dbg[16384 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 1] = attn_gtime();
+  __syncthreads();
+  const bool vec = Q.vec != 0;
+  const int nchunks = (T2 + L.chunk - 1) / L.chunk;
+  attn_gather_rows<DH, NT, DH + 4>(qs, Q.a, qr, qc, 0, R, T - i0, vec);
+  attn_gather_rows<DH, NT, DH + 4>(ks, Q.b, kr, kc, 0, L.chunk, T2, vec);
+  if (nchunks == 1) attn_gather_rows<DH, NT, DH + 8>(vs, V.b, vr, vc, 0, L.chunk, T2, vec);
+  cp_async_wait_all();
+  __syncthreads();
+  if (Q.dbg && t == 0) Q.dbg[16384 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 2] = attn_gtime();
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int j0 = ch * L.chunk;
+    if (ch > 0) {
+      __syncthreads();
+      attn_gather_rows<DH, NT, DH + 4>(ks, Q.b, kr, kc, j0, L.chunk, T2, vec);
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    for (int nt = w; nt < L.chunk / 8; nt += NW) {  // this warp's 8 score columns
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* krow = ks + (nt * 8 + g) * dk + tq;
+      const float* q0 = qs + g * dk + tq;  // A fragment rows g, g+8; columns kk*8 + tq, + 4
+#pragma unroll 4
+      for (int kk = 0; kk < DH / 8; ++kk) {
+        const float a[4] = {q0[kk * 8], q0[8 * dk + kk * 8], q0[kk * 8 + 4], q0[8 * dk + kk * 8 + 4]};
+        const float b[2] = {krow[kk * 8], krow[kk * 8 + 4]};
+        mma_3xtf32(c, a, b);
+      }
+      const int j = j0 + nt * 8 + 2 * tq;
+      if (j < T2) {
+        ss[g * ts + j] = c[0];
+        ss[(g + 8) * ts + j] = c[2];
+      }
+      if (j + 1 < T2) {
+        ss[g * ts + j + 1] = c[1];
+        ss[(g + 8) * ts + j + 1] = c[3];
+      }
+    }
+  }
+  if (nchunks > 1) {
+    __syncthreads();
+    attn_gather_rows<DH, NT, DH + 8>(vs, V.b, vr, vc, 0, L.chunk, T2, vec);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  __syncthreads();
+  if (Q.dbg && t == 0) Q.dbg[16384 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 3] = attn_gtime();
+  {  // softmax: warp w owns row w (rows_kernel's arithmetic)
+    constexpr int kNC = NC;  // ceil(T2 / 32) bound of the instance
+    float* row = ss + w * ts;
+    float v[kNC];
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kNC; ++k) {
+      const int j = lane + 32 * k;
+      v[k] = j < T2 ? row[j] : 0.f;
+      if (j < T2) m = fmaxf(m, v[k]);
+    }
+    m = warp_max(m);
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < kNC; ++k)
+      if (lane + 32 * k < T2) {
+        v[k] = expf(v[k] - m);
+        sum += v[k];
+      }
+    const float inv = 1.f / warp_sum(sum);
+#pragma unroll
+    for (int k = 0; k < kNC; ++k) {
+      const int j = lane + 32 * k;
+      if (j < T2) row[j] = v[k] * inv;
+      else if (j < ts) row[j] = 0.f;
+    }
+  }
+  if (Q.dbg && t == 0) Q.dbg[16384 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 4] = attn_gtime();
+  // context: warp w < Dh/8 owns output columns [8w, 8w + 8)
+  constexpr int NTO = DH / 8;
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int j0 = ch * L.chunk;
+    if (nchunks > 1) {
+      if (ch > 0) {
+        __syncthreads();
+        attn_gather_rows<DH, NT, DH + 8>(vs, V.b, vr, vc, j0, L.chunk, T2, vec);
+      }
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    if (w < NTO) {
+      const int jn = min(L.chunk, T2 - j0);
+      const float* vcol = vs + tq * dv + w * 8 + g;
+      for (int kk = 0; kk < (jn + 7) / 8; ++kk) {  // columns past T2: p = 0 and V rows zero
+        const int jb = j0 + kk * 8 + tq;
+        const float a[4] = {ss[g * ts + jb], ss[(g + 8) * ts + jb], ss[g * ts + jb + 4], ss[(g + 8) * ts + jb + 4]};
+        const float b[2] = {vcol[kk * 8 * dv], vcol[(kk * 8 + 4) * dv]};
+        mma_3xtf32(o, a, b);
+      }
+    }
+  }
+  if (Q.dbg && t == 0) Q.dbg[16384 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 5] = attn_gtime();
+  if (w < NTO) {
+    const int c0 = w * 8 + 2 * tq;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int r = g + 8 * hh;
+      if (i0 + r >= T) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t off = orow[r] + oc[c0 + e];
+        const float y = o[2 * hh + e];
+        V.out[off] = y;
+        if (V.out_bf16) static_cast<__nv_bfloat16*>(V.out_bf16)[off] = __float2bfloat16_rn(y);
+      }
+    }
+  }
+  __syncthreads();
+  if (Q.dbg && t == 0) Q.dbg[16384 + 8 * (blockIdx.y * gridDim.x + blockIdx.x) + 6] = attn_gtime();
+}
+
 __global__ void __launch_bounds__(256) split_bf16_kernel(const SplitParams P) {
   LFG_PDL_ENTRY();
   // piece index per term, smallest products first (x2y0, x1y1, x0y2, x1y0,
@@ -658,14 +928,42 @@ cudaError_t launch_attn_dh(const BmmParams& QK, const BmmParams& PV, int variant
     case 1: return launch_attn_inst<float, DH, 8, 256>(QK, PV, stream);
     case 2: return launch_attn_inst<float, DH, 16, 256>(QK, PV, stream);
     case 3: return launch_attn_inst<float, DH, 32, 512>(QK, PV, stream);
-    default: return launch_attn_inst<float, DH, 16, 512>(QK, PV, stream);
+    default: return launch_attn_inst<float, DH, 16, 512>(QK, PV, stream);  // 0 (non-mma head dims), 4
   }
+}
+
+template <int DH, int NC>
+cudaError_t launch_attn_mma_nc(const BmmParams& QK, const BmmParams& PV, size_t smem, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_mma_kernel<DH, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const dim3 grid((QK.T + 15) / 16, QK.H);
+  return launch_pdl(attn_mma_kernel<DH, NC>, grid, dim3(512), smem, stream, QK, PV);
+}
+
+template <int DH>
+cudaError_t launch_attn_mma(const BmmParams& QK, const BmmParams& PV, cudaStream_t stream) {
+  const size_t smem = attn_mma_smem(QK.T2, DH).total;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (QK.T2 <= 128) return launch_attn_mma_nc<DH, 4>(QK, PV, smem, stream);
+  if (QK.T2 <= 256) return launch_attn_mma_nc<DH, 8>(QK, PV, smem, stream);
+  return launch_attn_mma_nc<DH, 16>(QK, PV, smem, stream);
 }
 
 cudaError_t launch_attention(const BmmParams& QK, const BmmParams& PV, bool exact, cudaStream_t stream) {
   if (QK.Dh > kMaxDh || QK.Dh < 1 || QK.T2 > kMaxT2 || QK.T2 < 1 || PV.Dh != QK.Dh) return cudaErrorInvalidValue;
-  static const int variant = getenv("LFGPU_ATTN_VARIANT") ? atoi(getenv("LFGPU_ATTN_VARIANT")) : 0;
+  const char* ve = getenv("LFGPU_ATTN_VARIANT");  // read per launch: tests switch it in-process
+  const int variant = ve ? atoi(ve) : 0;
   if (exact) return launch_attn_inst<double, 0, 16, 512>(QK, PV, stream);
+  // tensor cores (3xTF32) for the common head dims; LFGPU_ATTN_VARIANT >= 1
+  // selects the CUDA-core tiles (diagnostics / bit-identity with the
+  // three-kernel path)
+  if (variant == 0 && QK.Dh == 64) return launch_attn_mma<64>(QK, PV, stream);
+  if (variant == 0 && QK.Dh == 128) return launch_attn_mma<128>(QK, PV, stream);
   if (QK.Dh == 64) return launch_attn_dh<64>(QK, PV, variant, stream);
   if (QK.Dh == 128) return launch_attn_dh<128>(QK, PV, variant, stream);
   return launch_attn_inst<float, 0, 16, 512>(QK, PV, stream);

@@ -48,6 +48,8 @@ struct BmmParams {
   // fused attention: every operand's head columns contiguous in 16-byte
   // aligned runs of 4 (16-byte gathers)
   int32_t vec = 0;
+  // diagnostics (lfgpu_debug_umma_trace): 8 %globaltimer stamps per CTA
+  unsigned long long* dbg = nullptr;
 };
 
 // LFGPU_PLAN_TC_SPLIT operand preparation: x = x0 + x1 + x2 (bf16 pieces);

@@ -1414,7 +1414,11 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
                   cols_vec4(P->t[qkn.inputs[1]], qkn.b_col0, w) && cols_vec4(P->t[n.inputs[1]], n.b_col0, w);
           if (getenv("LFGPU_ATTN_SCALAR")) Q.vec = 0;
           step.kernel = "attention";
-          step.run = [Q, M, exact](cudaStream_t s) { return launch_attention(Q, M, exact, s); };
+          step.run = [Q, M, exact](cudaStream_t s) {
+            BmmParams q = Q;
+            q.dbg = static_cast<unsigned long long*>(umma_debug_buffer());  // diagnostics only
+            return launch_attention(q, M, exact, s);
+          };
           break;
         }
         step.kernel = n.kind == LFGPU_OP_BMM_QK ? "bmm_qk" : "bmm_pv";
