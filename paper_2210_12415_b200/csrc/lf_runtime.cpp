@@ -36,6 +36,7 @@
 #include "lf_direct.hpp"
 #include "lf_generic.hpp"
 #include "lf_kernels.hpp"
+#include "lf_small.hpp"
 #include "lf_umma.hpp"
 
 using namespace lfg;
@@ -484,6 +485,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
   std::map<int, UmmaPlan> umma;
   std::map<int, std::vector<EpiOp>> direct;  // CUDA-core direct convs (k_direct.cu)
   std::map<int, std::vector<EpiOp>> depd;    // K6 depthwise (k_direct.cu)
+  std::map<int, std::vector<EpiOp>> gemv;    // small-M GMM on CUDA cores (k_small.cu)
   std::map<int, UmmaPlan> im2col;            // small-I C2D: im2col + tcgen05 GEMM
   struct SplitGmm {                          // LFGPU_PLAN_TC_SPLIT operands (K' = 6K)
     std::vector<Dim> a_log, b_log;
@@ -661,6 +663,16 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
       }
       if (P->flags & LFGPU_PLAN_REQUIRE_TC)
         fail(LFGPU_EUNSUPPORTED, "node " + std::to_string(ni) + " not tensor-core legal: " + why);
+      // Small-M GMM (the batch-1 classifier): k_small.cu's GEMV with the
+      // element-wise chain fused, when every operand layout is separable.
+      if (n.kind == LFGPU_OP_GMM && A.logical[0].extent <= 16) {
+        std::vector<int64_t> tb, of;
+        bool sep = true;
+        for (int t : {n.inputs[0], n.inputs[1], n.output})
+          sep = sep && separable_tables(P->t[t].logical, P->t[t].seq, &tb, &of);
+        if (sep)
+          gemv[ni] = s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL) ? fuse_chain(ni, Cc) : std::vector<EpiOp>{};
+      }
       continue;
     }
     if (s.fuse && !(P->flags & LFGPU_PLAN_KEEP_ALL)) {
@@ -1276,6 +1288,46 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
                            " splits=" + std::to_string(L.splits) + " grid=" + std::to_string(L.grid) +
                            " ring=" + std::to_string(L.pipe) + (L.epi_alias ? " epi-in-ring" : "") +
                            (L.dual ? " dual" : "");
+        } else if (gemv.count(ni)) {
+          GemvParams Gv;
+          Gv.M = static_cast<int32_t>(A.logical[0].extent);
+          Gv.K = static_cast<int32_t>(A.logical[1].extent);
+          Gv.N = static_cast<int32_t>(B.logical[1].extent);
+          if (!A.d || !B.d) fail(LFGPU_EUNSUPPORTED, "CUDA-core GEMV on a bf16-only operand");
+          std::vector<int64_t> ao, bo, oo;
+          Gv.a = static_cast<const float*>(A.d);
+          Gv.at = tables_for(P, A, &ao);
+          Gv.b = static_cast<const float*>(B.d);
+          Gv.bt = tables_for(P, B, &bo);
+          for (int j = 0; j < 2; ++j) {
+            Gv.a_off[j] = ao[j];
+            Gv.b_off[j] = bo[j];
+          }
+          const auto& epi = gemv.at(ni);
+          const int final_t = epi.empty() ? n.output : epi.back().out_tensor;
+          PTensor& fo = P->t[final_t];
+          Gv.ot = tables_for(P, fo, &oo);
+          for (int j = 0; j < 2; ++j) Gv.o_off[j] = oo[j];
+          Gv.out = static_cast<float*>(fo.d);
+          if (fo.d_bf16) {
+            Gv.out_bf16 = fo.d_bf16;
+            fo.shadow_by_producer = true;
+          }
+          Gv.nepi = static_cast<int32_t>(epi.size());
+          for (size_t e = 0; e < epi.size() && e < 4; ++e) {
+            Gv.epi_kind[e] = epi[e].kind;
+            if (epi[e].tensor >= 0) {
+              const PTensor& et = P->t[epi[e].tensor];
+              if (!et.d) fail(LFGPU_EUNSUPPORTED, "epilogue operand has no fp32 buffer");
+              Gv.epi_ptr[e] = static_cast<const float*>(et.d);
+            }
+          }
+          if (epi.size() > 4) fail(LFGPU_EUNSUPPORTED, "GEMV epilogue chain longer than 4");
+          for (size_t e = 0; e + 1 < epi.size(); ++e) P->t[epi[e].out_tensor].valid = false;
+          if (!epi.empty()) out.valid = false;
+          step.kernel = "gemv";
+          step.run = [Gv](cudaStream_t st) { return launch_gemv(Gv, st); };
+          P->bytes += A.numel * 4 + B.numel * 4 + fo.numel * 4;
         } else {
           GenContract G;
           G.op = n.kind == LFGPU_OP_GMM ? GEN_GMM : n.kind == LFGPU_OP_C2D ? GEN_C2D : GEN_DEP;
@@ -1456,6 +1508,41 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           G.W = A.logical[3].extent;
         }
         if (!A.d) fail(LFGPU_EUNSUPPORTED, "pool read of a bf16-only tensor");
+        {
+          // k_small.cu's table-driven pool kernels when both layouts are
+          // separable (fp32; the exact mode keeps the generic kernel)
+          std::vector<int64_t> tb, of;
+          if (!exact && out.dtype == LFGPU_DTYPE_F32 && out.d && separable_tables(A.logical, A.seq, &tb, &of) &&
+              separable_tables(out.logical, out.seq, &tb, &of)) {
+            PoolParams Pp;
+            Pp.op = n.kind == LFGPU_OP_MAXPOOL ? 0 : 1;
+            Pp.N = static_cast<int32_t>(A.logical[0].extent);
+            Pp.C = static_cast<int32_t>(A.logical[1].extent);
+            Pp.H = static_cast<int32_t>(A.logical[2].extent);
+            Pp.W = static_cast<int32_t>(A.logical[3].extent);
+            if (Pp.op == 0) {
+              Pp.Ho = static_cast<int32_t>(out.logical[2].extent);
+              Pp.Wo = static_cast<int32_t>(out.logical[3].extent);
+              Pp.K = static_cast<int32_t>(n.window);
+              Pp.V = static_cast<int32_t>(n.stride);
+            }
+            std::vector<int64_t> xo, oo;
+            Pp.x = static_cast<const float*>(A.d);
+            Pp.xt = tables_for(P, A, &xo);
+            for (size_t j = 0; j < xo.size() && j < 4; ++j) Pp.x_off[j] = xo[j];
+            Pp.out = static_cast<float*>(out.d);
+            Pp.ot = tables_for(P, out, &oo);
+            for (size_t j = 0; j < oo.size() && j < 4; ++j) Pp.o_off[j] = oo[j];
+            if (out.d_bf16) {
+              Pp.out_bf16 = out.d_bf16;
+              out.shadow_by_producer = true;
+            }
+            step.kernel = n.kind == LFGPU_OP_MAXPOOL ? "maxpool" : "global_avgpool";
+            step.run = [Pp](cudaStream_t st) { return launch_pool(Pp, st); };
+            P->bytes += A.numel * 4 + out.numel * 4;
+            break;
+          }
+        }
         std::vector<int64_t> oa;
         G.ta = tables_for(P, A, &oa);
         for (size_t j = 0; j < oa.size(); ++j) G.a_off[j] = oa[j];

@@ -247,3 +247,49 @@ def test_padding_absorbed_into_producer_epilogue(f1, f2, monkeypatch):
                    + ins["b1"].double().view(1, -1, 1, 1)).bfloat16().double(),
         ins["w2"].double(), padding=1).flatten().cpu().numpy()
     assert np.max(np.abs(outs[0] - ref) / np.maximum(1, np.abs(ref))) < 1e-4
+
+
+@pytest.mark.parametrize("layouts", [
+    {},
+    {"x": [split(1, [4, 16]), reorder([0, 1, 3, 4, 2])],
+     "mp": [split(1, [4, 16]), split(3, [2, 7]), reorder([0, 1, 3, 4, 5, 2])]},
+])
+def test_pool_kernels_fp32(layouts):
+    """k_small.cu's table-driven MaxPool / GlobalAvgPool (the default plans;
+    the exact mode keeps the generic kernels): max exact, mean within 1e-6."""
+    g = pool_graph(2, 64, 28)
+    bufs = O.random_inputs(g, 43)
+    ins = {"x": bufs[0].copy()}
+    O.reference_eval(g, bufs)
+    p = runtime.Plan(g, layouts, [], flags=_abi.PLAN_KEEP_ALL)
+    assert p.node_kernel(1) == "maxpool" and p.node_kernel(2) == "global_avgpool"
+    p.set_input("x", ins["x"])
+    p.run()
+    assert np.array_equal(p.get_output("mp"), bufs[g.tensor_index("mp")])
+    assert O.max_rel_diff(p.get_output("y"), bufs[g.tensor_index("y")]) <= 1e-6
+
+
+@pytest.mark.parametrize("m,fuse", [(1, 1), (4, 1), (1, 0), (16, 1)])
+def test_gemv_classifier_fused(m, fuse):
+    """The small-M GMM (batch-1 classifier) with BiasAdd + ReLU fused: fp32
+    sums of k/64 products are exact, so == the oracle."""
+    K, N = 512, 1000
+    g = ir.Graph()
+    g.tensors = [ir.TensorDecl("a", [("M", m), ("K", K)], ir.INPUT),
+                 ir.TensorDecl("w", [("K", K), ("N", N)], ir.CONSTANT),
+                 ir.TensorDecl("bias", [("N", N)], ir.CONSTANT),
+                 ir.TensorDecl("c", [("M", m), ("N", N)], ir.INTERMEDIATE),
+                 ir.TensorDecl("cb", [("M", m), ("N", N)], ir.INTERMEDIATE),
+                 ir.TensorDecl("y", [("M", m), ("N", N)], ir.OUTPUT)]
+    g.nodes = [ir.OperatorNode(ir.GMM, ["a", "w"], "c"), ir.OperatorNode(ir.BIASADD, ["c", "bias"], "cb"),
+               ir.OperatorNode(ir.RELU, ["cb"], "y")]
+    bufs = O.random_inputs(g, 44)
+    ins = {t: bufs[g.tensor_index(t)].copy() for t in ("a", "w", "bias")}
+    O.reference_eval(g, bufs)
+    p = runtime.Plan(g, {}, [runtime.sched(0, fuse=fuse)])
+    kinds = [p.node_kernel(i) for i in range(3)]
+    assert kinds[0] == "gemv" and (kinds[1:] == ["fused", "fused"]) == bool(fuse), kinds
+    for k, v in ins.items():
+        p.set_input(k, v)
+    p.run()
+    assert np.array_equal(p.get_output("y"), bufs[g.tensor_index("y")])
