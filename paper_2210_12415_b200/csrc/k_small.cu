@@ -30,9 +30,21 @@ __global__ void __launch_bounds__(256) maxpool_kernel(const PoolParams P) {
     const int n = static_cast<int>(r / P.C);
     const int64_t base = __ldg(P.xt + P.x_off[0] + n) + __ldg(P.xt + P.x_off[1] + c);
     float m = -INFINITY;
-    for (int kh = 0; kh < P.K; ++kh) {
-      const int64_t hb = base + __ldg(P.xt + P.x_off[2] + oh * P.V + kh);
-      for (int kw = 0; kw < P.K; ++kw) m = fmaxf(m, __ldg(P.x + hb + __ldg(P.xt + P.x_off[3] + ow * P.V + kw)));
+    if (P.pad == 0) {
+      for (int kh = 0; kh < P.K; ++kh) {
+        const int64_t hb = base + __ldg(P.xt + P.x_off[2] + oh * P.V + kh);
+        for (int kw = 0; kw < P.K; ++kw) m = fmaxf(m, __ldg(P.x + hb + __ldg(P.xt + P.x_off[3] + ow * P.V + kw)));
+      }
+    } else {  // the absorbed Padding: its zeros take part in the max
+      for (int kh = 0; kh < P.K; ++kh) {
+        const int ih = oh * P.V + kh - P.pad;
+        const bool hin = ih >= 0 && ih < P.H;
+        const int64_t hb = hin ? base + __ldg(P.xt + P.x_off[2] + ih) : 0;
+        for (int kw = 0; kw < P.K; ++kw) {
+          const int iw = ow * P.V + kw - P.pad;
+          m = fmaxf(m, hin && iw >= 0 && iw < P.W ? __ldg(P.x + hb + __ldg(P.xt + P.x_off[3] + iw)) : 0.f);
+        }
+      }
     }
     const int64_t o = __ldg(P.ot + P.o_off[0] + n) + __ldg(P.ot + P.o_off[1] + c) + __ldg(P.ot + P.o_off[2] + oh) +
                       __ldg(P.ot + P.o_off[3] + ow);

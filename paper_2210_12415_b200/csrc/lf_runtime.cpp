@@ -764,6 +764,32 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
     }
   }
 
+  // 1c'. A Padding feeding only a MaxPool is absorbed into its reads
+  // (k_small.cu: zeros outside the unpadded input take part in the max);
+  // the padded tensor is never materialized.
+  std::map<int, int> maxpool_pad;  // MaxPool node -> Padding node it reads through
+  if (!(P->flags & (LFGPU_PLAN_KEEP_ALL | LFGPU_PLAN_EXACT)) && !getenv("LFGPU_NO_PAD_ABSORB")) {
+    for (int mn = 0; mn < static_cast<int>(P->nodes.size()); ++mn) {
+      const auto& mp = P->nodes[mn];
+      if (mp.kind != LFGPU_OP_MAXPOOL) continue;
+      const PTensor& XP = P->t[mp.inputs[0]];
+      const int pn = XP.producer;
+      if (pn < 0 || P->nodes[pn].kind != LFGPU_OP_PADDING || XP.consumers.size() != 1 ||
+          XP.role != LFGPU_ROLE_INTERMEDIATE || fused_away.count(pn))
+        continue;
+      const PTensor& X = P->t[P->nodes[pn].inputs[0]];
+      const PTensor& Y = P->t[mp.output];
+      std::vector<int64_t> tb, of;
+      if (X.logical.size() != 4 || X.dtype != LFGPU_DTYPE_F32 || Y.dtype != LFGPU_DTYPE_F32 ||
+          !separable_tables(X.logical, X.seq, &tb, &of) || !separable_tables(Y.logical, Y.seq, &tb, &of))
+        continue;
+      maxpool_pad[mn] = pn;
+      fused_away.insert(pn);
+      P->t[mp.inputs[0]].valid = false;
+      P->t[P->nodes[pn].inputs[0]].need_f32 = true;
+    }
+  }
+
   // 1d. Attention fusion: BmmQK -> Softmax -> BmmPV whose scores and
   // probabilities are single-consumer intermediates runs as one kernel
   // (k_rows.cu attn_kernel) at the BmmPV's position; s and p are never
@@ -1507,19 +1533,22 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           G.H = A.logical[2].extent;
           G.W = A.logical[3].extent;
         }
-        if (!A.d) fail(LFGPU_EUNSUPPORTED, "pool read of a bf16-only tensor");
         {
           // k_small.cu's table-driven pool kernels when both layouts are
-          // separable (fp32; the exact mode keeps the generic kernel)
+          // separable (fp32; the exact mode keeps the generic kernel), reading
+          // through an absorbed Padding when 1c' found one
+          const auto mpp = maxpool_pad.find(ni);
+          const PTensor& X = mpp != maxpool_pad.end() ? P->t[P->nodes[mpp->second].inputs[0]] : A;
           std::vector<int64_t> tb, of;
-          if (!exact && out.dtype == LFGPU_DTYPE_F32 && out.d && separable_tables(A.logical, A.seq, &tb, &of) &&
+          if (!exact && out.dtype == LFGPU_DTYPE_F32 && out.d && X.d && separable_tables(X.logical, X.seq, &tb, &of) &&
               separable_tables(out.logical, out.seq, &tb, &of)) {
             PoolParams Pp;
             Pp.op = n.kind == LFGPU_OP_MAXPOOL ? 0 : 1;
-            Pp.N = static_cast<int32_t>(A.logical[0].extent);
-            Pp.C = static_cast<int32_t>(A.logical[1].extent);
-            Pp.H = static_cast<int32_t>(A.logical[2].extent);
-            Pp.W = static_cast<int32_t>(A.logical[3].extent);
+            Pp.N = static_cast<int32_t>(X.logical[0].extent);
+            Pp.C = static_cast<int32_t>(X.logical[1].extent);
+            Pp.H = static_cast<int32_t>(X.logical[2].extent);
+            Pp.W = static_cast<int32_t>(X.logical[3].extent);
+            if (mpp != maxpool_pad.end()) Pp.pad = static_cast<int32_t>(P->nodes[mpp->second].pad);
             if (Pp.op == 0) {
               Pp.Ho = static_cast<int32_t>(out.logical[2].extent);
               Pp.Wo = static_cast<int32_t>(out.logical[3].extent);
@@ -1527,8 +1556,8 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
               Pp.V = static_cast<int32_t>(n.stride);
             }
             std::vector<int64_t> xo, oo;
-            Pp.x = static_cast<const float*>(A.d);
-            Pp.xt = tables_for(P, A, &xo);
+            Pp.x = static_cast<const float*>(X.d);
+            Pp.xt = tables_for(P, X, &xo);
             for (size_t j = 0; j < xo.size() && j < 4; ++j) Pp.x_off[j] = xo[j];
             Pp.out = static_cast<float*>(out.d);
             Pp.ot = tables_for(P, out, &oo);
@@ -1539,10 +1568,12 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
             }
             step.kernel = n.kind == LFGPU_OP_MAXPOOL ? "maxpool" : "global_avgpool";
             step.run = [Pp](cudaStream_t st) { return launch_pool(Pp, st); };
-            P->bytes += A.numel * 4 + out.numel * 4;
+            P->bytes += X.numel * 4 + out.numel * 4;
             break;
           }
+          if (mpp != maxpool_pad.end()) fail(LFGPU_EUNSUPPORTED, "absorbed Padding without the pool kernel");
         }
+        if (!A.d) fail(LFGPU_EUNSUPPORTED, "pool read of a bf16-only tensor");
         std::vector<int64_t> oa;
         G.ta = tables_for(P, A, &oa);
         for (size_t j = 0; j < oa.size(); ++j) G.a_off[j] = oa[j];

@@ -15,6 +15,7 @@ namespace lfg {
 struct PoolParams {
   int32_t op = 0;  // 0 MaxPool (window K, stride V), 1 GlobalAvgPool
   int32_t N = 0, C = 0, H = 0, W = 0, Ho = 0, Wo = 0, K = 1, V = 1;
+  int32_t pad = 0;  // MaxPool reading an absorbed Padding's input: zeros outside [0, H) x [0, W)
   const float* x = nullptr;
   const int64_t* xt = nullptr;  // input tables (n, c, h, w)
   int64_t x_off[4] = {};

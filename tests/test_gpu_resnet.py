@@ -261,12 +261,21 @@ def test_pool_kernels_fp32(layouts):
     bufs = O.random_inputs(g, 43)
     ins = {"x": bufs[0].copy()}
     O.reference_eval(g, bufs)
-    p = runtime.Plan(g, layouts, [], flags=_abi.PLAN_KEEP_ALL)
-    assert p.node_kernel(1) == "maxpool" and p.node_kernel(2) == "global_avgpool"
-    p.set_input("x", ins["x"])
+    for flags in (_abi.PLAN_KEEP_ALL, _abi.PLAN_DEFAULT):
+        p = runtime.Plan(g, layouts, [], flags=flags)
+        # without KEEP_ALL the Padding is absorbed into the MaxPool's reads
+        pad_kind = "fused" if flags == _abi.PLAN_DEFAULT else p.node_kernel(0)
+        assert [p.node_kernel(i) for i in range(3)] == [pad_kind, "maxpool", "global_avgpool"]
+        p.set_input("x", ins["x"])
+        p.run()
+        assert np.array_equal(p.get_output("mp"), bufs[g.tensor_index("mp")])
+        assert O.max_rel_diff(p.get_output("y"), bufs[g.tensor_index("y")]) <= 1e-6
+    # zero padding takes part in the max: all-negative inputs give 0 on the border
+    p.set_input("x", -np.abs(ins["x"]) - 1.0)
     p.run()
-    assert np.array_equal(p.get_output("mp"), bufs[g.tensor_index("mp")])
-    assert O.max_rel_diff(p.get_output("y"), bufs[g.tensor_index("y")]) <= 1e-6
+    mp = p.get_output("mp").reshape(2, 64, 14, 14) if not layouts else None
+    if mp is not None:
+        assert (mp[:, :, 0, :] == 0).all() and (mp[:, :, 1:, 1:] < 0).all()
 
 
 @pytest.mark.parametrize("m,fuse", [(1, 1), (4, 1), (1, 0), (16, 1)])
