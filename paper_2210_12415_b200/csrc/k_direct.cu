@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "lf_direct.hpp"
 #include "lf_pdl.hpp"
@@ -222,6 +223,100 @@ __global__ void __launch_bounds__(256, (K == 3 ? 3 : 2)) dep_direct4(const Direc
   }
 }
 
+// K6 with a rolling window over TR output rows per thread (K = 3): each
+// input row of the strip is loaded once and feeds every output row whose
+// window covers it, so a thread reads (TR-1)*V+K input rows for TR output
+// rows instead of K per row. Per output the FMAs run rh-major, rw-minor,
+// exactly as dep_direct4 and interp.cpp:90-108 — bit-identical results.
+template <int K, int V, int WS, int TR, int MINB>
+__global__ void __launch_bounds__(256, MINB) dep_direct4_rows(const DirectDep P) {
+  constexpr int NC = (WS - 1) * V + K;
+  constexpr int NR = (TR - 1) * V + K;  // input rows a task touches
+  const int C4 = P.C >> 2, WSN = (P.Wo + WS - 1) / WS, HB = (P.Ho + TR - 1) / TR;
+  const int64_t total = static_cast<int64_t>(P.N) * C4 * HB * WSN;
+  const int64_t* xt = P.xt;
+  const int64_t* wt = P.wt;
+  const int64_t* ot = P.ot;
+  const int Wi = (P.Wo - 1) * V + K, Hi = (P.Ho - 1) * V + K;
+  LFG_PDL_ENTRY();
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r = e;
+    const int c = static_cast<int>(r % C4) * 4;
+    r /= C4;
+    const int w0 = static_cast<int>(r % WSN) * WS;
+    r /= WSN;
+    const int h0 = static_cast<int>(r % HB) * TR, n = static_cast<int>(r / HB);
+    const int64_t xb = __ldg(xt + P.x_off[0] + n) + __ldg(xt + P.x_off[1] + c);
+    const int64_t wb = __ldg(wt + P.w_off[0] + c);
+    int64_t oc[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int col = w0 * V + j;
+      oc[j] = __ldg(xt + P.x_off[3] + (col < Wi ? col : 0));
+    }
+    float4 wv[K][K];
+#pragma unroll
+    for (int rh = 0; rh < K; ++rh) {
+      const int64_t kh = wb + __ldg(wt + P.w_off[1] + rh);
+#pragma unroll
+      for (int rw = 0; rw < K; ++rw) wv[rh][rw] = __ldg(reinterpret_cast<const float4*>(P.w + kh + __ldg(wt + P.w_off[2] + rw)));
+    }
+    float4 acc[TR][WS];
+#pragma unroll
+    for (int o = 0; o < TR; ++o)
+#pragma unroll
+      for (int q = 0; q < WS; ++q) acc[o][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int ir = 0; ir < NR; ++ir) {
+      const int row = h0 * V + ir;
+      const int64_t oh = xb + __ldg(xt + P.x_off[2] + (row < Hi ? row : 0));
+      float4 xv[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) xv[j] = __ldg(reinterpret_cast<const float4*>(P.x + oh + oc[j]));
+#pragma unroll
+      for (int o = 0; o < TR; ++o) {
+        const int rh = ir - o * V;
+        if (rh < 0 || rh >= K) continue;  // resolved at compile time (unrolled)
+#pragma unroll
+        for (int q = 0; q < WS; ++q)
+#pragma unroll
+          for (int rw = 0; rw < K; ++rw) {
+            const float4 a = xv[q * V + rw], b = wv[rh][rw];
+            acc[o][q].x = fmaf(a.x, b.x, acc[o][q].x);
+            acc[o][q].y = fmaf(a.y, b.y, acc[o][q].y);
+            acc[o][q].z = fmaf(a.z, b.z, acc[o][q].z);
+            acc[o][q].w = fmaf(a.w, b.w, acc[o][q].w);
+          }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < TR; ++o) {
+      const int h = h0 + o;
+      if (h >= P.Ho) continue;
+      const int64_t ob = __ldg(ot + P.o_off[0] + n) + __ldg(ot + P.o_off[1] + c) + __ldg(ot + P.o_off[2] + h);
+#pragma unroll
+      for (int q = 0; q < WS; ++q) {
+        const bool live = w0 + q < P.Wo;
+        const int64_t off = ob + __ldg(ot + P.o_off[3] + (live ? w0 + q : 0));
+        float4 v = acc[o][q];
+        for (int k = 0; k < P.nepi; ++k) {
+          if (P.epi_kind[k] == DIRECT_EPI_RELU) {
+            v.x = fmaxf(v.x, 0.f), v.y = fmaxf(v.y, 0.f), v.z = fmaxf(v.z, 0.f), v.w = fmaxf(v.w, 0.f);
+          } else {
+            const float* ep = P.epi_ptr[k];
+            const float4 b = P.epi_kind[k] == DIRECT_EPI_BIAS
+                                 ? make_float4(__ldg(ep + c), __ldg(ep + c + 1), __ldg(ep + c + 2), __ldg(ep + c + 3))
+                                 : __ldg(reinterpret_cast<const float4*>(ep + off));
+            v.x += b.x, v.y += b.y, v.z += b.z, v.w += b.w;
+          }
+        }
+        if (live) *reinterpret_cast<float4*>(P.out + off) = v;
+      }
+    }
+  }
+}
+
 template <int K, int V>
 static void launch_dep4(const DirectDep& P, unsigned grid, cudaStream_t stream) {
   launch_pdl(dep_direct4<K, V, 2>, dim3(grid), dim3(256), 0, stream, P);
@@ -246,6 +341,19 @@ cudaError_t launch_dep_direct(const DirectDep& P, cudaStream_t stream) {
     const int64_t strips = static_cast<int64_t>(P.N) * (P.C / 4) * P.Ho * ((P.Wo + ws - 1) / ws);
     const unsigned g4 = static_cast<unsigned>(std::min<int64_t>((strips + 255) / 256,
                                                                 static_cast<int64_t>(sms) * 64));
+    static const int tr = getenv("LFGPU_DEP_ROWS") ? atoi(getenv("LFGPU_DEP_ROWS")) : 8;
+    if (P.KH == 3 && tr > 1) {  // rolling window over output rows
+      const int wq = 2;
+      const int64_t tasks = static_cast<int64_t>(P.N) * (P.C / 4) * ((P.Ho + tr - 1) / tr) * ((P.Wo + wq - 1) / wq);
+      const unsigned gt = static_cast<unsigned>(std::min<int64_t>((tasks + 255) / 256, static_cast<int64_t>(sms) * 64));
+      if (P.V == 1) {
+        if (tr >= 8) launch_pdl(dep_direct4_rows<3, 1, 2, 8, 2>, dim3(gt), dim3(256), 0, stream, P);
+        else launch_pdl(dep_direct4_rows<3, 1, 2, 4, 2>, dim3(gt), dim3(256), 0, stream, P);
+      } else {
+        launch_pdl(dep_direct4_rows<3, 2, 2, 4, 2>, dim3(gt), dim3(256), 0, stream, P);
+      }
+      return cudaGetLastError();
+    }
     if (P.V == 1) {
       if (P.KH == 3) launch_dep4<3, 1>(P, g4, stream);
       else if (P.KH == 5) launch_dep4<5, 1>(P, g4, stream);

@@ -348,6 +348,8 @@ def test_store_at_rules(seqs, msg):
     ((2, 64, 28, 3, 1), None, 0),                    # logical NCHW: W is the fast dim
     ((2, 64, 28, 3, 1), (7, 14, 32, 32, 32), 1),     # channel bricks, ReLU fused
     ((1, 96, 27, 5, 2), (7, 7, 32, 32, 32), 1),      # 5x5 stride 2 (14x14 output)
+    ((1, 96, 27, 3, 2), (7, 7, 32, 32, 32), 1),      # 3x3 stride 2: rolling-window kernel, V = 2
+    ((2, 64, 30, 3, 1), (10, 15, 32, 32, 32), 0),    # 3x3: row blocks of 8 over 30 rows (ragged)
     ((1, 32, 14, 7, 1), (14, 14, 16, 16, 16), 0),    # 7x7
     ((1, 48, 10, 4, 1), None, 1),                    # even window: the generic-K path
 ])
@@ -365,6 +367,7 @@ def test_dep_direct(shape, f, fuse):
     inputs, ref = oracle_outputs(g, 13)
     p = runtime.Plan(g, seqs, [runtime.sched(1, fuse=fuse)])
     assert p.node_kernel(1).startswith("dep_direct"), p.node_kernel(1)
+    # K = 3 channel-brick points run the rolling-window variant of dep_direct4
     if f is not None and c % 4 == 0 and f[4] % 4 == 0:
         assert p.node_kernel(1) == "dep_direct4", p.node_kernel(1)
     if fuse:
