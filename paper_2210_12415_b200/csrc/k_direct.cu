@@ -430,7 +430,93 @@ __global__ void __launch_bounds__(256) im2col_stem(const Im2col Q) {
   }
 }
 
+// im2col by tiles: one CTA per A brick of RT pixels = RT / Wo whole output
+// rows. The input rows the tile's windows touch (zero-padded) are staged in
+// SMEM with coalesced loads, a per-k offset table maps k -> (i, rh, rw), and
+// the brick is written as consecutive 16-byte chunks (a warp stores 512
+// contiguous bytes). The trailing CTAs convert the weights as before.
+// Same values as im2col_stem (bf16 of the same fp32 element, zeros outside).
+__global__ void __launch_bounds__(256) im2col_tiles(const Im2col Q, int tiles) {
+  extern __shared__ __align__(16) float xs[];  // [I][rows][Wp], then int koff[Kp]
+  const int r = Q.RT / Q.Wo, rows = (r - 1) * Q.V + Q.KH, Wp = Q.W + 2 * Q.pad;
+  int* koff = reinterpret_cast<int*>(xs + static_cast<size_t>(Q.I) * rows * Wp);
+  const int kb_n = Q.Kp / 64;
+  if (static_cast<int>(blockIdx.x) >= tiles) {  // weights: B[o][k0..k0+8) as [K0][O][64]
+    LFG_PDL_ENTRY();
+    __nv_bfloat16* B = static_cast<__nv_bfloat16*>(Q.b);
+    const int64_t nb = static_cast<int64_t>(Q.O) * (Q.Kp / 8);
+    for (int64_t f = (blockIdx.x - tiles) * 256ll + threadIdx.x; f < nb; f += (gridDim.x - tiles) * 256ll) {
+      __align__(16) __nv_bfloat16 v[8];
+      const int o = static_cast<int>(f / (Q.Kp / 8)), k0 = static_cast<int>(f - static_cast<int64_t>(o) * (Q.Kp / 8)) * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0 + j;
+        v[j] = __float2bfloat16_rn(k < Q.K ? __ldg(Q.w + static_cast<int64_t>(o) * Q.K + k) : 0.f);
+      }
+      *reinterpret_cast<uint4*>(B + (static_cast<int64_t>(k0 >> 6) * Q.O + o) * 64 + (k0 & 63)) =
+          *reinterpret_cast<const uint4*>(v);
+    }
+    return;
+  }
+  const int mt = blockIdx.x;  // tile: pixels [mt*RT, (mt+1)*RT) = output rows of image n
+  const int64_t m0 = static_cast<int64_t>(mt) * Q.RT;
+  const int n = static_cast<int>(m0 / (static_cast<int64_t>(Q.Ho) * Q.Wo));
+  const int ho0 = static_cast<int>((m0 - static_cast<int64_t>(n) * Q.Ho * Q.Wo) / Q.Wo);
+  const int y0 = ho0 * Q.V - Q.pad;  // first input row staged
+  for (int k = threadIdx.x; k < Q.Kp; k += 256) {  // k -> (i, rh, rw) offset in xs
+    if (k < Q.K) {
+      const int i = k / (Q.KH * Q.KW), rr = k - i * Q.KH * Q.KW, rh = rr / Q.KW, rw = rr - rh * Q.KW;
+      koff[k] = (i * rows + rh) * Wp + rw;
+    } else {
+      koff[k] = -1;
+    }
+  }
+  LFG_PDL_ENTRY();
+  const float* xb = Q.x + static_cast<int64_t>(n) * Q.I * Q.H * Q.W;
+  const int tot = Q.I * rows * Wp;
+  for (int e = threadIdx.x; e < tot; e += 256) {
+    const int i = e / (rows * Wp), rem = e - i * rows * Wp, rr = rem / Wp, cc = rem - rr * Wp;
+    const int yy = y0 + rr, xx = cc - Q.pad;
+    xs[e] = yy >= 0 && yy < Q.H && xx >= 0 && xx < Q.W ? __ldg(xb + (static_cast<int64_t>(i) * Q.H + yy) * Q.W + xx)
+                                                       : 0.f;
+  }
+  __syncthreads();
+  __nv_bfloat16* A = static_cast<__nv_bfloat16*>(Q.a) + static_cast<int64_t>(mt) * kb_n * Q.RT * 64;
+  const int chunks = kb_n * Q.RT * 8;  // 16-byte chunks of the brick, in memory order
+  for (int L = threadIdx.x; L < chunks; L += 256) {
+    const int kb = L / (Q.RT * 8), rem = L - kb * Q.RT * 8, p = rem >> 3, c8 = rem & 7;
+    const int pr = p / Q.Wo, pc = p - pr * Q.Wo;
+    const int base = pr * Q.V * Wp + pc * Q.V;
+    const int k0 = kb * 64 + c8 * 8;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int o = koff[k0 + j];
+      v[j] = __float2bfloat16_rn(o >= 0 ? xs[o + base] : 0.f);
+    }
+    reinterpret_cast<uint4*>(A)[L] = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
 cudaError_t launch_im2col(const Im2col& Q, cudaStream_t stream) {
+  if (Q.RT % Q.Wo == 0 && !getenv("LFGPU_IM2COL_FLAT")) {
+    const int r = Q.RT / Q.Wo, rows = (r - 1) * Q.V + Q.KH, Wp = Q.W + 2 * Q.pad;
+    const size_t smem = sizeof(float) * static_cast<size_t>(Q.I) * rows * Wp + sizeof(int) * Q.Kp;
+    if (smem <= 200 * 1024) {
+      static bool attr_set = false;
+      if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(im2col_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+      }
+      const int64_t tiles = static_cast<int64_t>(Q.N) * Q.Ho * Q.Wo / Q.RT;
+      const int64_t nb = static_cast<int64_t>(Q.O) * (Q.Kp / 8);
+      const int bblocks = static_cast<int>(std::min<int64_t>((nb + 255) / 256, 64));
+      launch_pdl(im2col_tiles, dim3(static_cast<unsigned>(tiles + bblocks)), dim3(256), smem, stream, Q,
+                 static_cast<int>(tiles));
+      return cudaGetLastError();
+    }
+  }
   const int64_t total = static_cast<int64_t>(Q.N) * Q.Ho * Q.Wo * (Q.Kp / 64) + static_cast<int64_t>(Q.O) * (Q.Kp / 8);
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 64));
   launch_pdl(im2col_stem, dim3(grid), dim3(256), 0, stream, Q);

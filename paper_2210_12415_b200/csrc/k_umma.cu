@@ -520,16 +520,24 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
         a[j] = rb + (cv[j] ? s_col[c0 + j0 + j] : 0);
       }
 #pragma unroll 1
-      for (int e = 0; e < P.epi_count; ++e) {
+      for (int e = 0; e < P.epi_count; ++e) {  // one branch per op, loads batched
         const int k = P.epi_kind[e];
         const float* ep = P.epi_ptr[e];
+        if (k == EPI_RELU) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (k == EPI_RELU) y[j] = fmaxf(y[j], 0.0f);
-          else if (k == EPI_GELU) y[j] = epi_gelu(y[j]);
-          else if (cv[j])
-            y[j] += __ldg(ep + (k == EPI_BIAS ? static_cast<int64_t>(n_base + (P.bias_rows ? row : c0 + j0 + j))
-                                              : a[j]));
+          for (int j = 0; j < 8; ++j) y[j] = fmaxf(y[j], 0.0f);
+        } else if (k == EPI_GELU) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] = epi_gelu(y[j]);
+        } else {
+          float t[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            t[j] = cv[j] ? __ldg(ep + (k == EPI_BIAS ? static_cast<int64_t>(n_base + (P.bias_rows ? row : c0 + j0 + j))
+                                                     : a[j]))
+                         : 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] += t[j];
         }
       }
 #pragma unroll
@@ -944,17 +952,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (rp >= 0) {
             const int64_t addr = obase + s_row[row];
             const int cs = P.stg_cstride;
+            // One branch per op, and a bias / residual op's 16 loads all
+            // issued before the adds: a per-element branch kept each load
+            // behind the previous add (16 serial L1/L2 latencies per chunk;
+            // ncu: ~59 instructions and a long-scoreboard stall per element).
 #pragma unroll 1
             for (int e = 0; e < P.epi_count; ++e) {
               const int kk = P.epi_kind[e];
               const float* ep = P.epi_ptr[e];
+              if (kk == EPI_RELU) {
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                if (kk == EPI_RELU) v[j] = fmaxf(v[j], 0.0f);
-                else if (kk == EPI_GELU) v[j] = epi_gelu(v[j]);
-                else
-                  v[j] += __ldg(ep + (kk == EPI_BIAS ? static_cast<int64_t>(n_base + c0 + j)
-                                                     : addr + (cs ? s_col[c0 + j] : c0 + j)));
+                for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.0f);
+              } else if (kk == EPI_GELU) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = epi_gelu(v[j]);
+              } else {
+                float t[16];
+                if (kk == EPI_BIAS) {
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) t[j] = __ldg(ep + n_base + c0 + j);
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) t[j] = __ldg(ep + addr + (cs ? s_col[c0 + j] : c0 + j));
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] += t[j];
               }
             }
             if (cs) {
