@@ -473,28 +473,47 @@ __global__ void __launch_bounds__(256) im2col_tiles(const Im2col Q, int tiles) {
   }
   LFG_PDL_ENTRY();
   const float* xb = Q.x + static_cast<int64_t>(n) * Q.I * Q.H * Q.W;
-  const int tot = Q.I * rows * Wp;
-  for (int e = threadIdx.x; e < tot; e += 256) {
-    const int i = e / (rows * Wp), rem = e - i * rows * Wp, rr = rem / Wp, cc = rem - rr * Wp;
-    const int yy = y0 + rr, xx = cc - Q.pad;
-    xs[e] = yy >= 0 && yy < Q.H && xx >= 0 && xx < Q.W ? __ldg(xb + (static_cast<int64_t>(i) * Q.H + yy) * Q.W + xx)
-                                                       : 0.f;
+  // stage the input rows: warp w takes lines (channel, row) w, w + 8, ...,
+  // its lanes the columns, all of a line's loads in flight before the stores
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int ir = warp; ir < Q.I * rows; ir += 8) {
+    const int i = ir / rows, yy = y0 + ir - i * rows;
+    float* line = xs + static_cast<size_t>(ir) * Wp;
+    const bool yin = yy >= 0 && yy < Q.H;
+    const float* src = xb + (static_cast<int64_t>(i) * Q.H + (yin ? yy : 0)) * Q.W - Q.pad;
+    constexpr int kQ = 8;  // 256 columns per pass
+    for (int c0 = 0; c0 < Wp; c0 += 32 * kQ) {
+      float v[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int cc = c0 + lane + 32 * q, xx = cc - Q.pad;
+        v[q] = yin && cc < Wp && xx >= 0 && xx < Q.W ? __ldg(src + cc) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < kQ; ++q)
+        if (c0 + lane + 32 * q < Wp) line[c0 + lane + 32 * q] = v[q];
+    }
   }
   __syncthreads();
+  // thread: 16-byte chunk c8 of pixels p, p + 32, ...; per K brick the
+  // warp's stores cover 4 pixels x 128 contiguous bytes
   __nv_bfloat16* A = static_cast<__nv_bfloat16*>(Q.a) + static_cast<int64_t>(mt) * kb_n * Q.RT * 64;
-  const int chunks = kb_n * Q.RT * 8;  // 16-byte chunks of the brick, in memory order
-  for (int L = threadIdx.x; L < chunks; L += 256) {
-    const int kb = L / (Q.RT * 8), rem = L - kb * Q.RT * 8, p = rem >> 3, c8 = rem & 7;
-    const int pr = p / Q.Wo, pc = p - pr * Q.Wo;
-    const int base = pr * Q.V * Wp + pc * Q.V;
-    const int k0 = kb * 64 + c8 * 8;
-    __align__(16) __nv_bfloat16 v[8];
+  const int c8 = threadIdx.x & 7;
+  for (int kb = 0; kb < kb_n; ++kb) {
+    int ko[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int o = koff[k0 + j];
-      v[j] = __float2bfloat16_rn(o >= 0 ? xs[o + base] : 0.f);
+    for (int j = 0; j < 8; ++j) ko[j] = koff[kb * 64 + c8 * 8 + j];
+    uint4* dst = reinterpret_cast<uint4*>(A + static_cast<int64_t>(kb) * Q.RT * 64) + c8;
+    int pr = (threadIdx.x >> 3) / Q.Wo, pc = (threadIdx.x >> 3) - pr * Q.Wo;  // pixel p -> (row, col), stepped
+    for (int p = threadIdx.x >> 3; p < Q.RT; p += 32) {
+      const float* b = xs + pr * Q.V * Wp + pc * Q.V;
+      pc += 32;
+      while (pc >= Q.Wo) pc -= Q.Wo, ++pr;
+      __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn(ko[j] >= 0 ? b[ko[j]] : 0.f);
+      dst[p * 8] = *reinterpret_cast<const uint4*>(v);
     }
-    reinterpret_cast<uint4*>(A)[L] = *reinterpret_cast<const uint4*>(v);
   }
 }
 
