@@ -202,21 +202,43 @@ __device__ __forceinline__ void store_chunk(const PairParams& P, const Smem& T, 
   } else {
     // Generic layouts: thread = row, one element at a time (column offsets
     // from the global table, L1-resident after the first tile).
+    // 8 columns per step: addresses, then one branch per fused op with its
+    // loads batched (a per-element branch serialises the loads), then stores.
     const int64_t rb = obase + T.row[q * 32 + lane];
-#pragma unroll 4
-    for (int j = 0; j < 32; ++j) {
-      const int64_t addr = rb + __ldg(P.col_off + c0 + j);
-      float y = v[j];
+#pragma unroll
+    for (int j0 = 0; j0 < 32; j0 += 8) {  // unrolled: v[] stays in registers
+      int64_t addr[8];
+      float y[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        addr[j] = rb + __ldg(P.col_off + c0 + j0 + j);
+        y[j] = v[j0 + j];
+      }
 #pragma unroll 1
       for (int e = 0; e < P.epi_count; ++e) {
         const int k = P.epi_kind[e];
-        if (k == EPI_RELU) y = fmaxf(y, 0.f);
-        else if (k == EPI_GELU) y = epi_gelu(y);
-        else if (k == EPI_BIAS) y += bias[c0 + j];
-        else y += __ldg(P.epi_ptr[e] + addr);
+        if (k == EPI_RELU) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] = fmaxf(y[j], 0.f);
+        } else if (k == EPI_GELU) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] = epi_gelu(y[j]);
+        } else if (k == EPI_BIAS) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] += bias[c0 + j0 + j];
+        } else {
+          float t[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t[j] = __ldg(P.epi_ptr[e] + addr[j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) y[j] += t[j];
+        }
       }
-      P.out[addr] = y;
-      if (P.out_bf16) P.out_bf16[addr] = __float2bfloat16_rn(y);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        P.out[addr[j]] = y[j];
+        if (P.out_bf16) P.out_bf16[addr[j]] = __float2bfloat16_rn(y[j]);
+      }
     }
   }
 }
