@@ -104,6 +104,11 @@ def gemm_bench_r03(reps=3):
     gemm(reps, (128, 1024, 128), 64, 1)
 
 
+def conv_b16_final(reps=3):
+    """cfg1 b16 on the final round-2 bench pick (halo, resident weights, dual issuer)."""
+    conv(reps, 16, (56, 28, 64, 32, 32, 64))
+
+
 def conv_b16r02(reps=3):
     conv(reps, 16, (28, 28, 64, 32, 32, 64))
 
