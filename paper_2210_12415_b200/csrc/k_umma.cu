@@ -269,6 +269,19 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float* f) {
   else tmem_ld16(taddr, v);
 }
 
+// The unit's accumulator columns [c, c + W): with split issue (dual == 2)
+// the two issuers' partial accumulators (BN columns apart) summed.
+template <int W>
+__device__ __forceinline__ void acc_ld(int dual, int BN, uint32_t taddr, float* f) {
+  tmem_ld<W>(taddr, f);
+  if (dual == 2) {
+    float g[W];
+    tmem_ld<W>(taddr + static_cast<uint32_t>(BN), g);
+#pragma unroll
+    for (int j = 0; j < W; ++j) f[j] += g[j];
+  }
+}
+
 // The fused element-wise chain (BiasAdd / EwAdd / ReLU, interp.cpp:137-165;
 // fusion groups lower.cpp:566-608). Kinds are kernel parameters, so every
 // branch is warp-uniform.
@@ -368,7 +381,7 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
       P.dbg[32 * blockIdx.x + 30] == 0)
     P.dbg[32 * blockIdx.x + 30] = gtimer();
   float v[W];
-  tmem_ld<W>(taddr + c0, v);
+  acc_ld<W>(P.dual, P.BN, taddr + c0, v);
   if (P.dbg && !dry && (P.diag & 2) && threadIdx.x == kEpiWarp0 * 32 && c0 == 0 &&
       P.dbg[32 * blockIdx.x + 28] == 0)
     P.dbg[32 * blockIdx.x + 28] = gtimer();
@@ -610,10 +623,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < pipe; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, P.dual == 2 ? 2 : 1);  // split issue: both issuers release a stage
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull0 + 8 * b, 1);
+      mbar_init(tfull0 + 8 * b, P.dual == 2 ? 2 : 1);
       mbar_init(tempty0 + 8 * b, kEpiWarps);  // one arrive per epilogue warp
     }
     for (int c = 0; c < nw; ++c) mbar_init(wfull0 + 8 * c, 1);
@@ -767,7 +780,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = u_first; u < u_end; u += u_step, ++i) {
       const int split = u % splits;
       const int s_lo = split * nst / splits, s_hi = (split + 1) * nst / splits;
-      if (P.dual && (i & 1) != role) {  // the other issuer's unit: step over its stages
+      if (P.dual == 1 && (i & 1) != role) {  // the other issuer's unit: step over its stages
         for (int s = s_lo; s < s_hi; ++s)
           if (++slot == pipe) {
             slot = 0;
@@ -778,7 +791,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = i & 1;
       mbar_wait(tempty0 + 8 * b, (static_cast<uint32_t>(i >> 1) & 1u) ^ 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t dtm = tmem + static_cast<uint32_t>(b * P.BN);
+      // split issue (dual == 2): both issuers take every unit, alternate
+      // MMAs of it, each into its own accumulator (summed by the epilogue)
+      const bool split_issue = P.dual == 2;
+      const uint32_t dtm = tmem + static_cast<uint32_t>((split_issue ? 2 * b + role : b) * P.BN);
+      int mi = 0;  // this unit's MMA index (split issue: issuer `role` takes mi % 2 == role)
       for (int s = s_lo; s < s_hi; ++s) {
         mbar_wait(full0 + 8 * slot, phase);
         if (dbg && leader && i == 0 && s == s_lo) dbg[3] = gtimer();
@@ -797,10 +814,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           // carry out of the field).
           const uint64_t ad0 = adesc | (a_addr >> 4), bd0 = bdesc | (b_addr >> 4);
           const int ntaps = (P.diag & 8) ? 1 : P.ntaps;
-          for (int t = 0; t < ntaps; ++t) {
-            const uint64_t adt = ad0 + ((P.diag & 4) ? 0 : (P.a_tap[t] >> 4)), bdt = bd0 + (P.b_tap[t] >> 4);
-            for (int k = 0; k < ksteps; ++k)
-              umma_bf16(dtm, adt + k * akadv16, bdt + k * bkadv16, idesc, (s != s_lo) | t | k);
+          if (split_issue) {
+            for (int t = 0; t < ntaps; ++t) {
+              const uint64_t adt = ad0 + ((P.diag & 4) ? 0 : (P.a_tap[t] >> 4)), bdt = bd0 + (P.b_tap[t] >> 4);
+              for (int k = 0; k < ksteps; ++k, ++mi)
+                if ((mi & 1) == role)
+                  umma_bf16(dtm, adt + k * akadv16, bdt + k * bkadv16, idesc, mi >= 2);
+            }
+          } else {
+            for (int t = 0; t < ntaps; ++t) {
+              const uint64_t adt = ad0 + ((P.diag & 4) ? 0 : (P.a_tap[t] >> 4)), bdt = bd0 + (P.b_tap[t] >> 4);
+              for (int k = 0; k < ksteps; ++k)
+                umma_bf16(dtm, adt + k * akadv16, bdt + k * bkadv16, idesc, (s != s_lo) | t | k);
+            }
           }
           umma_commit(empty0 + 8 * slot);
         }
@@ -850,7 +876,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (dbg && !dry && i == 0 && threadIdx.x == kEpiWarp0 * 32) dbg[5] = gtimer();
       if (dbg && !dry && (P.diag & 32) && i == 0 && lane == 0) dbg[24 + warp - kEpiWarp0] = gtimer();
       if (dbg && !dry && i < 4 && threadIdx.x == kEpiWarp0 * 32) dbg[8 + i] = gtimer();
-      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * BN);
+      const uint32_t tbase =
+          tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>((P.dual == 2 ? 2 * b : b) * BN);
       const int64_t ws_tile = static_cast<int64_t>(tile) * splits;
       const int red_lo = split * (BN / splits);
       constexpr int mode = MODE;
@@ -940,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* stb = smem + P.stg_off + 2 * nbuf * P.stg_f32 + (half * nbuf + bi) * P.stg_bf;
           if (tr) dbg[k == half ? 24 : 29] = gtimer();
           float v[16];
-          tmem_ld<16>(tbase + c0, v);
+          acc_ld<16>(P.dual, BN, tbase + c0, v);
           if (tr && k == half) dbg[25] = gtimer();
           if (last && !dry) {
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1259,7 +1286,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   int cols = 32;
   while (cols < 2 * p.BN) cols *= 2;  // two accumulators (epilogue/main-loop overlap)
   if (cols > 512) fail(LFGPU_EUNSUPPORTED, "accumulators exceed 512 TMEM columns");
-  L.tmem_cols = cols;
+  L.tmem_cols = cols;  // split issue doubles it below
   L.a_boxes = p.A.boxes;
   L.b_boxes = p.B.boxes;
   L.a_slot = p.A.slot_bytes;
@@ -1485,6 +1512,18 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (cudaOccupancyMaxActiveClusters(&n, f, &cfg) != cudaSuccess || n * L.splits < L.grid) L.xsplit = 0;
       cudaGetLastError();
+    }
+    // Split issue (dual = 2, opt-in with LFGPU_DUAL_MMA=2): both issuers take
+    // every unit and alternate its MMAs into two accumulators the epilogue
+    // sums. Measured on the cfg1 b16 conv it does not beat one issuer (MMA
+    // phase 10.6 vs 10.1 us; the alternate-unit issuers 7.5 us): the two
+    // accumulators' MMAs do not overlap in the tensor pipe the way two
+    // units' do. Kept as a diagnostic, covered by the parity tests.
+    const int dual_units = L.dual;
+    if (const char* e = getenv("LFGPU_DUAL_MMA")) L.dual = std::max(0, std::min(2, atoi(e)));
+    if (L.dual == 2) {
+      if (L.tmem_cols * 2 > 512 || L.xsplit) L.dual = dual_units;
+      else L.tmem_cols *= 2;
     }
     if (L.dual) L.nprod = std::min(L.nprod, 2);
   }

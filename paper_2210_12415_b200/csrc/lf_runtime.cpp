@@ -1313,7 +1313,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
           P->summary[ni] = up.summary + " store=" + std::to_string(L.store_mode) +
                            " splits=" + std::to_string(L.splits) + " grid=" + std::to_string(L.grid) +
                            " ring=" + std::to_string(L.pipe) + (L.epi_alias ? " epi-in-ring" : "") +
-                           (L.dual ? " dual" : "");
+                           (L.dual == 1 ? " dual" : L.dual == 2 ? " split-issue" : "");
         } else if (gemv.count(ni)) {
           GemvParams Gv;
           Gv.M = static_cast<int32_t>(A.logical[0].extent);

@@ -425,7 +425,8 @@ def test_dep_direct_fused_bias_residual(brick):
 
 
 @pytest.mark.parametrize("knobs", [{}, {"LFGPU_NO_EPI_ALIAS": "1"}, {"LFGPU_DUAL_MMA": "1"},
-                                   {"LFGPU_DUAL_MMA": "0"}, {"LFGPU_NO_EPI_ALIAS": "1", "LFGPU_DUAL_MMA": "1"}])
+                                   {"LFGPU_DUAL_MMA": "0"}, {"LFGPU_NO_EPI_ALIAS": "1", "LFGPU_DUAL_MMA": "1"},
+                                   {"LFGPU_DUAL_MMA": "2"}])
 @pytest.mark.parametrize("case", ["conv", "gemm"])
 def test_umma_epilogue_alias_and_dual_issuer_parity(case, knobs, monkeypatch):
     """The 1-CTA kernel's epilogue-in-ring aliasing (default when each CTA
@@ -448,6 +449,8 @@ def test_umma_epilogue_alias_and_dual_issuer_parity(case, knobs, monkeypatch):
     k = p.node_kernel(node)
     if knobs.get("LFGPU_DUAL_MMA") == "1":
         assert " dual" in k, k
+    if knobs.get("LFGPU_DUAL_MMA") == "2":  # split issue: two issuers, two accumulators per unit
+        assert " split-issue" in k, k
     if knobs.get("LFGPU_NO_EPI_ALIAS") == "1":
         assert "epi-in-ring" not in k, k
     for tid, v in inputs.items():
