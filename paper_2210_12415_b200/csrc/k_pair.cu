@@ -80,6 +80,7 @@ struct PairParams {
   int32_t a_tx;       // bytes of the A boxes of one stage (diagnostics)
   int32_t xmode;      // split-K exchange: 0 L2 workspace, 1 DSMEM push (one tile per cluster)
   int32_t rx_bytes;   // DSMEM receive buffer bytes ((S-1) x 128 x BN/S fp32)
+  int32_t epi_alias, epi_off;  // one tile per cluster: epilogue buffers inside the idle ring at epi_off
 };
 
 #ifdef LFG_PAIR_CLOCK_STAMPS
@@ -253,9 +254,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (P.dbg && threadIdx.x == 0) P.dbg[512 * blockIdx.x + 320] = gtime();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* s_epi = reinterpret_cast<float*>(smem + P.ring_bytes);
-  float* s_rx = reinterpret_cast<float*>(smem + P.ring_bytes + kEpiBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + kEpiBytes + P.rx_bytes);
+  const int epi_bytes = P.epi_alias ? 0 : kEpiBytes;
+  float* s_epi = reinterpret_cast<float*>(smem + (P.epi_alias ? P.epi_off : P.ring_bytes));
+  float* s_rx = reinterpret_cast<float*>(smem + P.ring_bytes + epi_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P.ring_bytes + epi_bytes + P.rx_bytes);
   const int pipe = P.pipe;
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = full0 + 8 * pipe;
@@ -701,7 +703,12 @@ PairLaunch pair_prepare(const PairPlan& p) {
   L.ring_bytes = L.pipe * L.stage_bytes;
   L.rx_bytes = p.rx_bytes;
   L.xmode = p.rx_bytes > 0 ? 1 : 0;
-  L.smem = 1024 + L.ring_bytes + kEpiBytes + L.rx_bytes + 8 * (2 * L.pipe + 8) +
+  // Epilogue buffers inside the ring (planner: one tile per cluster), behind
+  // the DSMEM send staging of the split-K exchange.
+  L.epi_alias = p.epi_alias;
+  L.epi_off = L.xmode ? ((p.BN / 64) * (p.S - 1) + p.S - 1) / p.S * 8 * 4096 : 0;
+  if (L.epi_alias && L.epi_off + kEpiBytes > L.ring_bytes) L.epi_alias = 0;
+  L.smem = 1024 + L.ring_bytes + (L.epi_alias ? 0 : kEpiBytes) + L.rx_bytes + 8 * (2 * L.pipe + 8) +
            pair_table_bytes(p.KS, p.MT, p.NT, p.BN, p.A.boxes, p.B.boxes);
   if (L.smem > 227 * 1024) fail(LFGPU_EUNSUPPORTED, "pair kernel SMEM exceeds 227 KB");
   // Row-segment stores need contiguous output columns and 16-byte aligned rows.
@@ -763,6 +770,8 @@ PairLaunch pair_prepare(const PairPlan& p) {
     cudaGetLastError();
   }
   if (L.xmode && max_cl < ntiles) L.xmode = 0;  // the DSMEM exchange needs one tile per cluster
+  if (L.epi_alias && max_cl < ntiles)  // several tiles per cluster: the ring is not idle in the epilogue
+    fail(LFGPU_EUNSUPPORTED, "pair kernel: epilogue-in-ring needs one tile per cluster");
   L.grid = csize * std::max(1, std::min(ntiles, max_cl));
   return L;
 }
@@ -813,6 +822,8 @@ cudaError_t pair_launch(const PairLaunch& L, cudaStream_t stream) {
   P.a_tx = L.a_boxes * L.a_box_bytes;
   P.xmode = L.xmode;
   P.rx_bytes = L.rx_bytes;
+  P.epi_alias = L.epi_alias;
+  P.epi_off = L.epi_off;
   static const bool pdl = [] {
     const char* e = getenv("LFGPU_PDL");
     return !(e && atoi(e) == 0);

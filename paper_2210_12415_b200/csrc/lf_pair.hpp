@@ -70,6 +70,7 @@ struct PairPlan {
   int a_slab = 0, b_slab = 0;  // SMEM bytes between slabs inside a box
   int pipe = 4;
   int rx_bytes = 0;  // S > 1 with one tile per cluster: DSMEM receive buffer
+  int epi_alias = 0; // one tile per cluster: the epilogue transpose buffers live in the idle ring
   int group = 8;     // tile rasterization: row pairs that sweep the column tiles together (loop point `parallel`)
   OperandView A, B;           // A: 128-row box, B: BN/2-column box
   std::vector<int32_t> a_crd; // MT x A.boxes x 5
@@ -97,6 +98,7 @@ struct PairLaunch {
   int BN = 0, S = 1, MT = 0, NT = 0, KS = 0, pipe = 0, group = 8;
   int nprod = 4;  // TMA producer warps
   int xmode = 0, rx_bytes = 0;  // split-K exchange over DSMEM
+  int epi_alias = 0, epi_off = 0;  // epilogue buffers inside the ring at epi_off (one tile per cluster)
   int a_boxes = 0, b_boxes = 0, a_slot = 0, b_slot = 0, stage_bytes = 0, tx_bytes = 0;
   int a_box_bytes = 0;
   uint64_t a_desc = 0, b_desc = 0;

@@ -1607,13 +1607,39 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
         // Split K with one tile per cluster exchanges partials over DSMEM: a
         // dedicated receive buffer of (S-1) x 128 x BN/S fp32 (the send
         // staging aliases the idle operand ring).
-        bool dsm = S > 1 && tiles <= sms / (2 * S) && !getenv("LFGPU_PAIR_NO_DSMEM");
+        const bool dsm0 = S > 1 && tiles <= sms / (2 * S) && !getenv("LFGPU_PAIR_NO_DSMEM");
         const int rx = (S - 1) * 128 * (BN / S) * 4;
-        // send staging: each epilogue warp stages its chunks of the sibling slices
-        if (dsm && std::max(2, std::min(8, (budget - rx) / stage)) * stage < ((BN / 64) * (S - 1) + S - 1) / S * 8 * 4096)
-          dsm = false;
+        // send staging: each epilogue warp stages its chunks of the sibling
+        // slices in the idle operand ring
+        const int staging = ((BN / 64) * (S - 1) + S - 1) / S * 8 * 4096;
+        constexpr int kEpi = 8 * 32 * 36 * 4;
+        // Ring depth and exchange mode for a budget; with `al` the epilogue's
+        // transpose buffers live in the idle ring behind the send staging
+        // (one tile per cluster), freeing their 36 KB for the ring.
+        auto layout = [&](bool al, int* pipe_o, bool* dsm_o) {
+          const int bud = budget + (al ? kEpi : 0);
+          bool d = dsm0;
+          int pp = std::max(2, std::min(8, (bud - (d ? rx : 0)) / stage));
+          if (d && pp * stage < staging) {
+            d = false;
+            pp = std::max(2, std::min(8, bud / stage));
+          }
+          if (al && pp * stage < (d ? staging : 0) + kEpi) return false;
+          *pipe_o = pp;
+          *dsm_o = d;
+          return bud - (d ? rx : 0) >= 2 * stage;  // two stages must fit
+        };
+        bool dsm = false, fits = false;
+        int pp = 2;
+        q.epi_alias = 0;
+        if (tiles <= sms / (2 * S) && !getenv("LFGPU_PAIR_NO_EPI_ALIAS") && layout(true, &pp, &dsm)) {
+          q.epi_alias = 1;
+          fits = true;
+        } else {
+          fits = layout(false, &pp, &dsm);
+        }
         q.rx_bytes = dsm ? rx : 0;
-        q.pipe = std::max(2, std::min(8, (budget - q.rx_bytes) / stage));
+        q.pipe = pp;
         if (const char* e = getenv("LFGPU_PAIR_PIPE")) q.pipe = std::max(2, std::min(q.pipe, atoi(e)));
         if (force_s && S != force_s) continue;
         if (!force_s && s.order == 1 && S > 1) continue;
@@ -1625,7 +1651,7 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
         // and K-major single-box operands are exact. Split only single-box tiles.
         if (S > 1 && (q.A.boxes > 1 || q.B.boxes > 1)) continue;
         if (S > 1 && KS / S < 2) continue;
-        if (budget - q.rx_bytes < 2 * stage) continue;  // two stages must fit
+        if (!fits) continue;
         found = true;
         // Cost model (cycles): waves x stages x max(MMA, ingest) + epilogue
         // + split reduction + fixed latency. Ingest assumed ~48 B/clk/SM.
@@ -1654,7 +1680,7 @@ bool pair_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
      << "-major B=" << (best.B.mn_major ? "MN" : "K") << "-major tiles=" << best.MT / 2 * best.NT
      << " pipe=" << best.pipe;
   best.group = s.parallel ? 1 : 8;
-  os << " raster=" << (best.group == 1 ? "rows" : "group8");
+  os << " raster=" << (best.group == 1 ? "rows" : "group8") << (best.epi_alias ? " epi-in-ring" : "");
   best.summary = os.str();
   *out = best;
   return true;
