@@ -561,9 +561,22 @@ bool umma_plan_gemm(const std::vector<Dim>& a_log, const Seq& a_seq, const std::
     std::vector<int64_t> am, bm;
     UmmaPlan q = p;
     q.BN = BN;
-    int kcs = kcs_pref;
+    // Candidate K stages, largest first; among the ones that divide K, a
+    // stage count that is a multiple of 4 (then of 2) goes first so split-K
+    // (<= 4 splits) deals equal stage counts (K = 768: 4 x 192, not 3 x 256).
+    std::vector<int> kc_list;
+    for (int c : {256, 192, 128, 64})
+      if (c <= kcs_pref && K % c == 0) kc_list.push_back(c);
+    if (getenv("LFGPU_GEMM_KCS")) kc_list.assign(1, kcs_pref);
+    std::stable_sort(kc_list.begin(), kc_list.end(), [&](int x, int y) {
+      auto rank = [&](int c) { return (K / c) % 4 == 0 ? 0 : (K / c) % 2 == 0 ? 1 : 2; };
+      return rank(x) < rank(y);
+    });
+    if (kc_list.empty() || kc_list.back() != 64) kc_list.push_back(64);
+    int kcs = 64;
     bool a_ok = false, b_ok = false;
-    for (; kcs >= 64; kcs /= 2) {
+    for (int kci = 0; kci < static_cast<int>(kc_list.size()); ++kci) {
+      kcs = kc_list[kci];
       if (K % kcs || (kcs > 64 && RT != 128)) continue;
       std::string wa, wb;
       a_ok = gemm_operand(a_log, a_seq, 0, 1, RT, kcs, &q.A, &ads, &abox, &ag, &am, &wa);
