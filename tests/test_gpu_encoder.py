@@ -259,3 +259,34 @@ def test_encoder_packed_qkv_matches_unpacked():
         assert e2e.max_rel(out, emu) <= 2e-3
         outs.append(out)
     assert e2e.max_rel(outs[0], outs[1]) <= 2e-3
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_attention_fused_random_brick_layouts(seed):
+    """Fused attention through randomly blocked layouts of q / k / v / c
+    (column and row bricks in either order): the offset tables carry any
+    separable layout; 1e-5 vs the oracle, within 2e-6 of the unfused plan."""
+    rng = np.random.default_rng(seed)
+    T, H, Dh = 64, 4, 64
+    D = H * Dh
+    g = _graph([("q", [("M", T), ("N", D)], ir.INPUT), ("k", [("M", T), ("N", D)], ir.INPUT),
+                ("v", [("M", T), ("N", D)], ir.INPUT),
+                ("s", [("H", H), ("M", T), ("T", T)], ir.INTERMEDIATE),
+                ("p", [("H", H), ("M", T), ("T", T)], ir.INTERMEDIATE),
+                ("c", [("M", T), ("N", D)], ir.OUTPUT)],
+               [(ir.BMM_QK, ["q", "k"], "s", {"heads": H}), (ir.SOFTMAX, ["s"], "p"),
+                (ir.BMM_PV, ["p", "v"], "c", {"heads": H})])
+
+    def lay():
+        bm, bn = int(rng.choice([16, 32, 64])), int(rng.choice([32, 64, 128]))
+        if rng.integers(2):
+            return _brick(T, D, bm, bn)
+        return [split(1, [D // bn, bn]), reorder([1, 0, 2])]  # column bricks
+    seqs = {t: lay() for t in ("q", "k", "v", "c")}
+    ins, ref = _oracle(g, 30 + seed, {"q": 0.25, "k": 0.25})
+    p3 = _run(g, seqs, ins, flags=_abi.PLAN_KEEP_ALL)
+    p1 = _run(g, seqs, ins)
+    assert p1.node_kernel(2) == "attention"
+    c1 = p1.get_output("c")
+    assert O.max_rel_diff(c1, ref["c"]) <= 1e-5
+    assert O.max_rel_diff(c1, p3.get_output("c")) <= 2e-6

@@ -302,3 +302,51 @@ def test_gemv_classifier_fused(m, fuse):
         p.set_input(k, v)
     p.run()
     assert np.array_equal(p.get_output("y"), bufs[g.tensor_index("y")])
+
+
+@pytest.mark.parametrize("window,stride,pad", [(3, 2, 1), (2, 2, 0), (3, 1, 1)])
+def test_maxpool_window_stride_absorbed_padding(window, stride, pad):
+    """k_small.cu MaxPool over window / stride variants, reading through an
+    absorbed Padding when there is one: == the oracle (max is exact)."""
+    n, c, h = 2, 32, 17
+    hp = h + 2 * pad
+    ho = (hp - window) // stride + 1
+    g = ir.Graph()
+    g.tensors = [ir.TensorDecl("x", [("N", n), ("C", c), ("H", h), ("W", h)], ir.INPUT),
+                 ir.TensorDecl("xp", [("N", n), ("C", c), ("H", hp), ("W", hp)]),
+                 ir.TensorDecl("y", [("N", n), ("C", c), ("H", ho), ("W", ho)], ir.OUTPUT)]
+    g.nodes = [ir.OperatorNode(ir.PADDING, ["x"], "xp", {"pad": pad}),
+               ir.OperatorNode(ir.MAXPOOL, ["xp"], "y", {"window": window, "stride": stride})]
+    bufs = O.random_inputs(g, 45)
+    x = bufs[0].copy()
+    O.reference_eval(g, bufs)
+    p = runtime.Plan(g, {}, [])
+    assert p.node_kernel(1) == "maxpool" and p.node_kernel(0) == "fused"
+    p.set_input("x", x)
+    p.run()
+    assert np.array_equal(p.get_output("y"), bufs[g.tensor_index("y")])
+
+
+def test_gemv_residual_and_blocked_layouts():
+    """GEMV with a residual EwAdd fused, on a blocked weight layout and a
+    blocked output / residual layout: exact (k/64 products)."""
+    m, K, N = 2, 256, 1000  # N not a multiple of 16: no tensor-core tile, the GEMV path
+    g = ir.Graph()
+    g.tensors = [ir.TensorDecl("a", [("M", m), ("K", K)], ir.INPUT),
+                 ir.TensorDecl("w", [("K", K), ("N", N)], ir.CONSTANT),
+                 ir.TensorDecl("r", [("M", m), ("N", N)], ir.INPUT),
+                 ir.TensorDecl("c", [("M", m), ("N", N)], ir.INTERMEDIATE),
+                 ir.TensorDecl("y", [("M", m), ("N", N)], ir.OUTPUT)]
+    g.nodes = [ir.OperatorNode(ir.GMM, ["a", "w"], "c"), ir.OperatorNode(ir.EWADD, ["c", "r"], "y")]
+    seqs = {"w": [split(1, [N // 40, 40]), reorder([1, 0, 2])],
+            "c": [split(1, [N // 125, 125]), reorder([1, 0, 2])]}
+    seqs["y"] = seqs["r"] = seqs["c"]
+    bufs = O.random_inputs(g, 46)
+    ins = {t: bufs[g.tensor_index(t)].copy() for t in ("a", "w", "r")}
+    O.reference_eval(g, bufs)
+    p = runtime.Plan(g, seqs, [runtime.sched(0, fuse=1)])
+    assert [p.node_kernel(i) for i in range(2)] == ["gemv", "fused"]
+    for k, v in ins.items():
+        p.set_input(k, v)
+    p.run()
+    assert np.array_equal(p.get_output("y"), bufs[g.tensor_index("y")])

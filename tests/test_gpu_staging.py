@@ -101,3 +101,17 @@ def test_narrowed_staging_kernels():
     assert p.node_kernel(0).startswith("umma_gemm")
     assert p.buffer("a")[1] == _abi.ELEM_BF16
     p.close()
+
+
+def test_int32_tensors_keep_f64_staging():
+    """int32 tensors are not narrowed on the host (their conversion is the
+    device's truncating cvt): an int32 graph through set_input / get_output
+    matches the oracle exactly."""
+    g = ir.conv_chain(1, 2, 3, 6, 3, 1, 1, dtype=ir.I32)
+    import oracle_lib as O
+    bufs = O.random_inputs(g, 47)
+    ins = {t.id: bufs[i].copy() for i, t in enumerate(g.tensors) if t.role in (ir.INPUT, ir.CONSTANT)}
+    O.reference_eval(g, bufs)
+    out = runtime.interpret(g, {}, [], ins, flags=_abi.PLAN_EXACT)
+    last = g.nodes[-1].output
+    assert np.array_equal(out[last], bufs[g.tensor_index(last)])
