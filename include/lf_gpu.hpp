@@ -12,12 +12,19 @@
 //   lf::gpu::interpret(...)   replaces lf::interpret(lower(...), inputs)  interp.cpp:424-470
 //   lf::gpu::materialize(...) replaces lf::materialize_tensor           interp.cpp:280-337
 //   lf::gpu::measure(...)     replaces lf::simulate_cache at tuner.cpp:178 cachesim.cpp:152-174
+//   lf::gpu::measure_batch(...) the top-k of Tuner::measure_top (tuner.cpp:243-274)
+//                             over several devices, results in candidate order
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cctype>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "layoutforge/cachesim.hpp"
@@ -34,13 +41,15 @@ inline void check(int rc) {
 /// One device context (one host thread at a time).
 class Context {
  public:
-  explicit Context(int device = 0) { check(lfgpu_ctx_create(device, &ctx_)); }
+  explicit Context(int device = 0) : device_(device) { check(lfgpu_ctx_create(device, &ctx_)); }
   ~Context() { lfgpu_ctx_destroy(ctx_); }
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
   lfgpu_ctx* get() const { return ctx_; }
+  int device() const { return device_; }
 
  private:
+  int device_ = 0;
   lfgpu_ctx* ctx_ = nullptr;
 };
 
@@ -262,6 +271,107 @@ inline ProfileCounters measure(Context& ctx, const Graph& g, const SeqMap& seqs,
   p.l1_stores = c.tc_nodes;
   p.cost = c.cost;
   return p;
+}
+
+
+/// One measured candidate of a batch: the counters, or the lf::Error text of
+/// a candidate the backend rejected; `device` is the context index that
+/// measured it.
+struct BatchOutcome {
+  bool ok = false;
+  ProfileCounters counters;
+  std::string error;
+  int device = -1;
+};
+
+/// Tuner::measure_top's top-k (tuner.cpp:243-274) measured across devices:
+/// one host thread per context takes the next unmeasured candidate (dynamic
+/// dealing, so a slow candidate does not stall a device), and the outcomes
+/// come back indexed like `scheds`, so the caller commits them in candidate
+/// order exactly as the serial loop would (tuner.cpp:259-272). A candidate
+/// the backend rejects (lf::Error other than a device fault) is recorded as
+/// not ok. A device fault (LFGPU_ECUDA) retires that context and puts its
+/// candidate back on the queue for the others; when every context has
+/// faulted, measure_batch throws. Contexts on distinct devices measure
+/// concurrently; contexts sharing a device take turns for the timed part
+/// (one device mutex), so one context's plan build overlaps the other's
+/// measurement without disturbing it.
+inline std::vector<BatchOutcome> measure_batch(const std::vector<Context*>& ctxs, const Graph& g,
+                                               const SeqMap& seqs,
+                                               const std::vector<std::vector<LoopSchedule>>& scheds,
+                                               int warmup = 3, int reps = 10, bool flush_l2 = true,
+                                               int flags = LFGPU_PLAN_CUDA_GRAPH) {
+  if (ctxs.empty()) throw lf::Error("lfgpu: measure_batch needs at least one context");
+  std::vector<BatchOutcome> out(scheds.size());
+  std::mutex m;
+  std::deque<size_t> queue;
+  for (size_t i = 0; i < scheds.size(); ++i) queue.push_back(i);
+  int alive = static_cast<int>(ctxs.size()), inflight = 0;
+  std::condition_variable cv;  // a faulted device may re-queue work for the others
+  std::string fault;
+  std::vector<int> devs;  // one timing mutex per distinct device
+  for (auto* c : ctxs)
+    if (std::find(devs.begin(), devs.end(), c->device()) == devs.end()) devs.push_back(c->device());
+  std::vector<std::mutex> dev_m(devs.size());
+  auto worker = [&](int dev) {
+    std::mutex& timing =
+        dev_m[std::find(devs.begin(), devs.end(), ctxs[dev]->device()) - devs.begin()];
+    for (;;) {
+      size_t i;
+      {
+        std::unique_lock<std::mutex> lk(m);
+        cv.wait(lk, [&] { return !queue.empty() || inflight == 0; });
+        if (queue.empty()) return;
+        i = queue.front();
+        queue.pop_front();
+        ++inflight;
+      }
+      Desc d = describe(g, seqs);
+      auto sc = to_scheds(g, seqs, scheds[i]);
+      lfgpu_plan* plan = nullptr;
+      lfgpu_counters c;
+      int rc = lfgpu_plan_build(ctxs[dev]->get(), &d.g, static_cast<int32_t>(sc.size()), sc.data(),
+                                flags, &plan);
+      if (rc == LFGPU_OK) {
+        {
+          std::lock_guard<std::mutex> t(timing);
+          rc = lfgpu_plan_measure(plan, warmup, reps, flush_l2 ? 1 : 0, &c);
+        }
+        lfgpu_plan_destroy(plan);
+      }
+      std::lock_guard<std::mutex> lk(m);
+      --inflight;
+      cv.notify_all();
+      if (rc == LFGPU_ECUDA) {  // device fault: retire this context, re-queue
+        fault = lfgpu_last_error();
+        queue.push_front(i);
+        --alive;
+        return;
+      }
+      BatchOutcome& o = out[i];
+      o.device = dev;
+      if (rc != LFGPU_OK) {
+        o.error = std::string("lfgpu: ") + lfgpu_last_error();
+        continue;
+      }
+      o.ok = true;
+      o.counters.insts = c.kernels;
+      o.counters.l1_loads = c.bytes_moved;
+      o.counters.l1_misses = 0;
+      o.counters.l1_stores = c.tc_nodes;
+      o.counters.cost = c.cost;
+    }
+  };
+  if (ctxs.size() == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> th;
+    for (size_t k = 0; k < ctxs.size(); ++k) th.emplace_back(worker, static_cast<int>(k));
+    for (auto& t : th) t.join();
+  }
+  if (alive == 0 && !queue.empty())
+    throw lf::Error("lfgpu: every device faulted during measure_batch: " + fault);
+  return out;
 }
 
 }  // namespace lf::gpu

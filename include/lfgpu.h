@@ -337,7 +337,10 @@ int lfgpu_plan_destroy(lfgpu_plan* plan);
 int lfgpu_plan_set_input(lfgpu_plan* plan, int32_t tensor, const double* host_logical,
                          int64_t n);
 /* Same, from a device buffer of `elem` type already in the logical layout.
- * Returns once the conversion has consumed `d_logical`. */
+ * The conversion reads `d_logical` after all work enqueued before the call
+ * on the legacy default stream (the plan's own stream is non-blocking);
+ * producers on other streams must be synchronised by the caller. Returns
+ * once the conversion has consumed `d_logical`. */
 int lfgpu_plan_set_input_device(lfgpu_plan* plan, int32_t tensor, const void* d_logical,
                                 int32_t elem);
 /* Same, stream-ordered: the conversion is enqueued on the plan's stream and

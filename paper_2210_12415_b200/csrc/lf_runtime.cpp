@@ -245,6 +245,7 @@ struct lfgpu_plan {
   // work already enqueued on the plan stream (async set-input conversions),
   // later plan-stream work (get_output, set-input) waits for the run.
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaEvent_t ev_dev_in = nullptr;  // legacy-stream join of device-buffer inputs
   std::vector<cudaEvent_t> stage_ev;  // per-chunk events of the host staging
   int* h_err = nullptr;               // pinned: the device error flag read back with outputs
   int64_t bytes = 0, flops = 0, tc_nodes = 0;
@@ -255,6 +256,7 @@ struct lfgpu_plan {
     // of this plan may still be reading or writing them.
     if (stream) cudaStreamSynchronize(stream);
     if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_dev_in) cudaEventDestroy(ev_dev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
@@ -2048,6 +2050,12 @@ static void set_input_impl(lfgpu_plan* P, int32_t tensor, const void* d_logical,
   if (tensor < 0 || tensor >= static_cast<int32_t>(P->t.size()))
     fail(LFGPU_EINVAL, "tensor index out of range");
   PTensor& t = P->t[tensor];
+  // The plan's stream is non-blocking: order the read of `d_logical` after
+  // the work already enqueued on the legacy default stream (where a caller
+  // such as torch's default stream produced it).
+  if (!P->ev_dev_in) CUDA_OK(cudaEventCreateWithFlags(&P->ev_dev_in, cudaEventDisableTiming));
+  CUDA_OK(cudaEventRecord(P->ev_dev_in, cudaStreamLegacy));
+  CUDA_OK(cudaStreamWaitEvent(P->stream, P->ev_dev_in, 0));
   // Compiled once per (source, destination) element pair and kept with the
   // plan, so a repeated call is only the K1 launch(es), stream-ordered on the
   // plan's stream with no host synchronisation (the serving / e2e path).

@@ -266,6 +266,12 @@ class Plan:
         """From a torch CUDA tensor in the logical layout (float32/bfloat16/...).
         wait=False enqueues the conversion on the plan's stream and returns at
         once; the caller keeps `tensor` alive and unchanged until then."""
+        # The library orders the read after the legacy default stream; a
+        # tensor produced on another torch stream is waited for here.
+        import torch
+        cur = torch.cuda.current_stream(tensor.device)
+        if cur != torch.cuda.default_stream(tensor.device):
+            cur.synchronize()
         fn = lib().lfgpu_plan_set_input_device if wait else lib().lfgpu_plan_set_input_device_async
         check(fn(self.ptr, self.index(tid), C.c_void_p(tensor.data_ptr()), elem_of(tensor)))
 

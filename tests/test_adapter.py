@@ -81,6 +81,27 @@ def test_reference_tuner_drives_gpu_measure(cfg):
     assert 0 < rep["best_cost_us"] < 1e5, rep
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,contexts", [("cfg2", 1), ("cfg1", 1), ("cfg2", 2), ("cfg1", 2)])
+def test_reference_tuner_top_k_through_measure_batch(cfg, contexts):
+    """measure_top's top-k (tuner.cpp:243-274) handed to lf::gpu::measure_batch
+    before the tuner's own in-order loop consumes the outcomes: every
+    prefetched point is used, none rejected, the search finishes. Two
+    contexts on one device exercise the multi-device dealing (one host thread
+    per context, outcomes indexed by candidate)."""
+    import json
+    if not build_tune_check():
+        pytest.skip("tune_check binary not built (needs the reference sources once)")
+    r = subprocess.run([TUNE_BIN, "gpu", cfg, "64", "any", "serial", "batch", str(contexts)],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rep = json.loads(r.stdout.strip().splitlines()[-1])
+    assert rep["contexts"] == contexts and rep["batch_calls"] > 0, rep
+    assert rep["prefetch_used"] > 0 and rep["prefetch_used"] <= rep["batched"], rep
+    assert rep["measurements"] > 0 and rep["rejected"] == 0, rep
+    assert 0 < rep["best_cost_us"] < 1e5, rep
+
+
 @pytest.mark.skipif(not os.path.isdir(REF_INC) or not O.ref_available(),
                     reason="reference headers / build absent")
 def test_adapter_host_roundtrips():

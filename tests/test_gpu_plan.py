@@ -486,6 +486,33 @@ def test_run_on_user_stream_joins_async_set_input():
         assert np.array_equal(got, ref["c"] * (rep + 1)), rep
 
 
+def test_set_input_device_waits_for_producer_stream():
+    """The plan's stream is non-blocking: a device input still being
+    written on torch's default stream (a delayed producer) must be read only
+    after its producer, and one produced on a side stream after that stream
+    (found by the bench's 4096^3 check reading a freshly generated operand)."""
+    torch = pytest.importorskip("torch")
+    n = 1024
+    g = ir.gemm(n, n, n)
+    seqs = runtime.decode_layout(g, 0, [256, 64, 256])
+    p = runtime.Plan(g, seqs, [], flags=_abi.PLAN_REQUIRE_TC)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    side = torch.cuda.Stream()
+    for rep, stream in enumerate([None, side, None]):
+        torch.cuda.synchronize()
+        ctx = torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(torch.cuda.default_stream())
+        with ctx:
+            torch.cuda._sleep(2_000_000)  # the producer is still pending when set_input_device runs
+            a = torch.randint(-64, 65, (n, n), generator=gen, device="cuda").float() / 64
+            b = torch.randint(-64, 65, (n, n), generator=gen, device="cuda").float() / 64
+            p.set_input_device("a", a, wait=(rep != 2))
+            p.set_input_device("b", b, wait=(rep != 2))
+        p.run()
+        got = torch.tensor(p.get_output("c"), device="cuda").view(n, n)
+        assert torch.equal(got, a.double() @ b.double()), rep
+
+
 # Loop-point parameters the GPU lowering maps to kernel structure
 # (space.cpp:483-589 -> DESIGN.md §4.4): tile_second picks the GEMM M tile
 # (128: 1-CTA kernel, else the CTA pair) and caps the C2D rows per UMMA tile;
