@@ -36,6 +36,7 @@ struct UmmaParams {
   const int64_t* col_off;
   float* out;
   __nv_bfloat16* out_bf16;  // optional bf16 copy of the output (same layout)
+  int32_t out_stream;       // final graph output: streaming (evict-first) stores
   const float* epi_ptr[kMaxEpi];
   int32_t epi_kind[kMaxEpi];
   int32_t epi_count;
@@ -490,7 +491,13 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
     if (dry || (P.diag & 1)) return;  // warm-up pass / timing knob: no side effects
 #pragma unroll
     for (int it = 0; it < IT; ++it)
-      if (ok[it]) *reinterpret_cast<float4*>(P.out + addr[it]) = x[it];
+      if (ok[it]) {
+        float4* o = reinterpret_cast<float4*>(P.out + addr[it]);
+        if (P.out_stream)
+          __stcs(o, x[it]);
+        else
+          *o = x[it];
+      }
     if (P.sc.enabled) {
       // Unrolled: a rolled loop indexes x[] / ok[] dynamically and moves
       // them to local memory for the whole epilogue (ncu: STL.128 on the
@@ -556,7 +563,10 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (cv[j]) {
-          P.out[a[j]] = y[j];
+          if (P.out_stream)
+            __stcs(P.out + a[j], y[j]);
+          else
+            P.out[a[j]] = y[j];
           if (P.out_bf16) P.out_bf16[a[j]] = __float2bfloat16_rn(y[j]);
         }
       if (P.sc.enabled && c0 + j0 + 8 <= cols) {
@@ -1305,6 +1315,7 @@ UmmaLaunch umma_prepare(const UmmaPlan& p) {
   }
   L.out = p.out;
   L.out_bf16 = p.out_bf16;
+  L.out_stream = p.out_stream;
   // Split-K (schedule `order`: 0 = heuristic, 1 = never, 2 = at least 2):
   // when the tiles alone leave most of the SMs idle and the K loop is long.
   const int sms = num_sms();
@@ -1551,6 +1562,7 @@ cudaError_t umma_launch(const UmmaLaunch& L, cudaStream_t stream) {
   P.col_off = static_cast<const int64_t*>(L.d_cols);
   P.out = L.out;
   P.out_bf16 = static_cast<__nv_bfloat16*>(L.out_bf16);
+  P.out_stream = L.out_stream;
   P.epi_count = L.epi_count;
   for (int e = 0; e < L.epi_count; ++e) {
     P.epi_kind[e] = L.epi_kinds[e];

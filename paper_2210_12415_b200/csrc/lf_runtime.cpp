@@ -222,6 +222,18 @@ struct PTensor {
   bool shadow_by_producer = false;  // the producer's epilogue writes d_bf16 too
 };
 
+// LFGPU_OUT_STREAM=1: a graph output no node reads back is written with
+// streaming (evict-first) stores by the 1-CTA tcgen05 epilogue. Measured
+// neutral on the cfg2 back-to-back steady state (12.30 vs 12.30 us per
+// launch, tools/steps_regime_probe.py), so off by default.
+static int out_stream_for(const PTensor& t) {
+  static const bool on = [] {
+    const char* e = getenv("LFGPU_OUT_STREAM");
+    return e && atoi(e) != 0;
+  }();
+  return on && t.role == LFGPU_ROLE_OUTPUT && t.consumers.empty() ? 1 : 0;
+}
+
 struct PStep {
   int node = -1;
   int launches = 1;  // kernels this step launches
@@ -1083,6 +1095,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
             final_t = out_redirect.at(ni);
           }
           up.out = static_cast<float*>(P->t[final_t].d);
+          up.out_stream = out_stream_for(P->t[final_t]);
           if (P->t[final_t].d && P->t[final_t].d_bf16 && P->t[final_t].elem == LFGPU_ELEM_F32) {
             up.out_bf16 = P->t[final_t].d_bf16;
             P->t[final_t].shadow_by_producer = true;
@@ -1275,6 +1288,7 @@ void build_plan(lfgpu_plan* P, const lfgpu_graph* g, int nsched, const lfgpu_sch
             final_t = out_redirect.at(ni);
           }
           up.out = static_cast<float*>(P->t[final_t].d);
+          up.out_stream = out_stream_for(P->t[final_t]);
           if (P->t[final_t].d && P->t[final_t].d_bf16 &&
               P->t[final_t].elem == LFGPU_ELEM_F32) {  // dual store: no shadow pass
             up.out_bf16 = P->t[final_t].d_bf16;

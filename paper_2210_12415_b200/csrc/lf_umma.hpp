@@ -144,6 +144,7 @@ struct UmmaPlan {
   const void* b = nullptr;
   float* out = nullptr;
   void* out_bf16 = nullptr;  // optional bf16 copy written by the epilogue
+  int out_stream = 0;        // output is a graph output nothing reads back: streaming (evict-first) stores
   std::string summary;
   // GEMM on the CTA-pair kernel (k_pair.cu) when its tile is legal: the
   // fields above except epi/a/b/out are then unused.
@@ -168,6 +169,7 @@ struct UmmaLaunch {
   int epi_count = 0;
   float* out = nullptr;
   void* out_bf16 = nullptr;
+  int out_stream = 0;
   size_t smem = 0;
   int grid = 0;
   int per_sm = 1;  // CTAs that fit on one SM (SMEM / TMEM)

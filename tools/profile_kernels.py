@@ -104,6 +104,11 @@ def gemm_bench_r03(reps=3):
     gemm(reps, (128, 1024, 128), 64, 1)
 
 
+def gemm_bench_final(reps=3):
+    """The round-2 final bench pick (m_t=256 k_t=64 n_t=128 tile=64 order=1)."""
+    gemm(reps, (256, 64, 128), 64, 1)
+
+
 def conv_b16_final(reps=3):
     """cfg1 b16 on the final round-2 bench pick (halo, resident weights, dual issuer)."""
     conv(reps, 16, (56, 28, 64, 32, 32, 64))
