@@ -205,6 +205,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
 // runs the epilogue.
 
 constexpr int kThreads = 384;
+#ifndef LFGPU_UMMA_MINB
+#define LFGPU_UMMA_MINB 1  // resident CTAs per SM the register allocation is bounded for
+#endif
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant, alternating 16-column chunks
 constexpr int kEpiLd = 36;  // per-warp transpose buffer row stride (floats)
@@ -585,7 +588,7 @@ __device__ __forceinline__ void epi_chunk(const UmmaParams& P, uint32_t taddr, i
 // instruction caches less (ncu: ~2300 L1i misses per SM on the
 // all-paths kernel).
 template <int MODE, bool SPLITK>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, LFGPU_UMMA_MINB)
     umma_kernel(const __grid_constant__ CUtensorMap tma_a,
                 const __grid_constant__ CUtensorMap tma_b, const __grid_constant__ UmmaParams P,
                 const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ CUtensorMap tma_ob) {

@@ -17,7 +17,8 @@ from . import _abi
 from .ir import Graph
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblfgpu.so")
+# LFGPU_LIB_PATH: diagnostics only (an alternate build of the same sources)
+LIB_PATH = os.environ.get("LFGPU_LIB_PATH") or os.path.join(_PKG, "liblfgpu.so")
 
 # Every entry point include/lfgpu.h declares (tests check the exports).
 EXPORTS = [

@@ -17,7 +17,7 @@ c = tuner.Candidate({0: (512, 64, 256)}, [runtime.sched(0, tile_last=64, order=1
 A = torch.randint(-64, 65, (1024, 1024), device="cuda").float() / 64
 B = torch.randint(-64, 65, (1024, 1024), device="cuda").float() / 64
 ctx = runtime.context(0)
-for R in (1, 2, 4, 8, 32):
+for R in [int(x) for x in os.environ.get("FLOOR_R", "1 2 4 8 32").split()]:
     reps = []
     for _ in range(R):
         p = runtime.Plan(g, tuner.seqs_for(g, c), c.scheds, _abi.PLAN_REQUIRE_TC | _abi.PLAN_CUDA_GRAPH, ctx=ctx)
@@ -26,7 +26,7 @@ for R in (1, 2, 4, 8, 32):
         reps.append(p)
     for pre in (False, True):
         ms, _ = bench.time_plan_rotating(torch, reps, 64, 8, 1, preroll=pre)
-        print(f"ours R={R} {'sustained' if pre else 'burst'}: {ms / 64 * 1e3:.3f} us/launch", flush=True)
+        print(f"ours R={R} {'sustained' if pre else 'burst'}: {ms / 64 * 1e3:.3f} us/launch | {reps[0].node_kernel(0)[60:]}", flush=True)
     for p in reps:
         p.close()
 ab, bb = A.to(torch.bfloat16), B.to(torch.bfloat16)
